@@ -1,0 +1,391 @@
+// sp_batched.cu — bit-sliced batched inference: staging + overlap + boost + inhibition
+// fused in one kernel.
+//
+// Idea: the potential pools are the same for every frame, so a
+// group of up to 32 SP inputs is processed together with one BIT per input in
+// a 32-bit lane word.  For each pixel i the CTA builds, in shared memory, the
+// word X[i] whose bit f is pixel i of input f (a 32x32 bit transpose of the
+// uint8 frames, done with warp shuffles).  The overlap of column c for all 32
+// inputs is then the bit-sliced ("vertical") population count of
+//     X[idx[c,s]]  over its connected synapses s                 (Alg. 1 l.1-5)
+// accumulated with carry-save adders (Harley-Seal), so ONE shared-memory
+// gather serves 32 inputs.  The frames stream from HBM exactly once through a
+// cp.async.bulk ring (mbarrier complete_tx), so the kernel is HBM-bound.
+//
+// Shared memory per CTA:
+//   [stages x 32 rows x (1024+16) B]  bulk-copy ring, one row per input
+//   [region]                          window of Lw bit-sliced words + zero slot,
+//                                     later reused for raw counts uint16[32][C32]
+//   [C32 x u32]                       Bc = boost * 2^23
+//   [stages x u64]                    mbarriers
+// A cluster of K CTAs can split one group's pixel windows; partial counts are
+// then summed through distributed shared memory (DSMEM) before inhibition.
+#include <cooperative_groups.h>
+
+#include "sp_internal.h"
+
+namespace cg = cooperative_groups;
+
+namespace sp {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes,
+                                              uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+// 32x32 bit-matrix transpose across a warp (row = lane, column = bit):
+// afterwards lane j bit f = lane f bit j.  Recursive block swap, 5 stages of
+// shuffle + rotate + select.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, uint32_t lane) {
+    const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const uint32_t s = 16u >> i;
+        const bool lo = (lane & s) == 0;
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+        const uint32_t r = __funnelshift_l(y, y, lo ? s : 32u - s);
+        const uint32_t keep = lo ? masks[i] : ~masks[i];
+        x = (x & keep) | (r & ~keep);
+    }
+    return x;
+}
+
+// Byte-nonzero flags of 32 consecutive pixels (two uint4) merged into one word:
+// pixel 4k+b (byte b of word k) lands on bit 8b+k.  bit = byte != 0 (R12).
+__device__ __forceinline__ uint32_t nonzero_mask32(const uint4 a, const uint4 b) {
+    const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t t = (((v[k] & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | v[k]) & 0x80808080u;
+        m |= t >> (7 - k);
+    }
+    return m;
+}
+
+struct Planes {
+    uint32_t ones, twos, fours;
+    uint32_t hi[kHiPlanes];  // weights 8, 16, ..., 512
+};
+
+__device__ __forceinline__ void full_add(uint32_t& s, uint32_t& c, uint32_t a, uint32_t b,
+                                         uint32_t d) {
+    const uint32_t u = a ^ b;
+    s = u ^ d;
+    c = (a & b) | (u & d);
+}
+
+// Harley-Seal carry-save accumulation of 8 bit-sliced words into the counter.
+__device__ __forceinline__ void accumulate8(Planes& P, uint32_t x0, uint32_t x1, uint32_t x2,
+                                            uint32_t x3, uint32_t x4, uint32_t x5, uint32_t x6,
+                                            uint32_t x7) {
+    uint32_t c1, c2, c3, c4, f1, f2, e;
+    full_add(P.ones, c1, P.ones, x0, x1);
+    full_add(P.ones, c2, P.ones, x2, x3);
+    full_add(P.twos, f1, P.twos, c1, c2);
+    full_add(P.ones, c3, P.ones, x4, x5);
+    full_add(P.ones, c4, P.ones, x6, x7);
+    full_add(P.twos, f2, P.twos, c3, c4);
+    full_add(P.fours, e, P.fours, f1, f2);
+#pragma unroll
+    for (int h = 0; h < (int)kHiPlanes; ++h) {
+        const uint32_t t = P.hi[h] & e;
+        P.hi[h] ^= e;
+        e = t;
+    }
+}
+
+__device__ __forceinline__ uint32_t extract_count(const Planes& P, uint32_t f) {
+    uint32_t v = ((P.ones >> f) & 1u) | (((P.twos >> f) & 1u) << 1) | (((P.fours >> f) & 1u) << 2);
+#pragma unroll
+    for (int h = 0; h < (int)kHiPlanes; ++h) v |= ((P.hi[h] >> f) & 1u) << (3 + h);
+    return v;
+}
+
+// Rank key of column c (R4/R6): exact boosted overlap N = raw*Bc over 2^23,
+// ties broken towards the lower index.
+__device__ __forceinline__ uint64_t rank_key(uint32_t raw, uint32_t bc, uint32_t theta, uint32_t c,
+                                             uint32_t L, uint64_t& N) {
+    N = raw >= theta ? static_cast<uint64_t>(raw) * bc : 0ull;
+    return (N << L) | (((1ull << L) - 1ull) - c);
+}
+
+}  // namespace
+
+template <int CPT>
+__global__ void __launch_bounds__(kBatchedThreads, 1) sp_batched_kernel(const BatchedParams p) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, wi = tid >> 5;
+    constexpr uint32_t kRow = kChunkBits + kStagePad;
+    constexpr uint32_t kStageBytes = 32u * kRow;
+
+    uint8_t* stage_base = smem;
+    uint8_t* region = smem + p.stages * kStageBytes;
+    uint32_t* words = reinterpret_cast<uint32_t*>(region);
+    uint16_t* rawbuf = reinterpret_cast<uint16_t*>(region);
+    uint32_t* s_bc = reinterpret_cast<uint32_t*>(region + p.region_bytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_bc + p.C32);
+
+    const uint32_t K = p.K;
+    const uint32_t group = blockIdx.x / K, rank = blockIdx.x % K;
+    const uint32_t in0 = static_cast<uint32_t>(static_cast<uint64_t>(group) * p.num_inputs / p.groups);
+    const uint32_t in1 =
+        static_cast<uint32_t>(static_cast<uint64_t>(group + 1) * p.num_inputs / p.groups);
+    const uint32_t gs = in1 - in0;  // 1..32 inputs in this group
+    const uint32_t w0 = rank * p.nwin / K, w1 = (rank + 1) * p.nwin / K;
+    const uint32_t pix_begin = w0 * p.Lw;
+    const uint32_t pix_end = min(w1 * p.Lw, p.nbits);
+    const uint32_t nchunks = pix_end > pix_begin ? (pix_end - pix_begin + kChunkBits - 1) / kChunkBits : 0;
+
+    // ---- setup ---------------------------------------------------------------------------
+    if (tid < p.stages) mbar_init(&bars[tid], 1);
+    for (uint32_t c = tid; c < p.C32; c += kBatchedThreads) s_bc[c] = p.bc[c];
+    if (tid == 0) words[p.Lw] = 0u;  // the zero slot padding / disconnected synapses point to
+    if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+
+    // Producer: warp 0 issues the bulk copies of chunk j (one 16B-multiple row per input).
+    auto issue = [&](uint32_t j) {
+        const uint32_t st = j % p.stages;
+        const uint32_t p0 = pix_begin + j * kChunkBits;
+        const uint32_t vb = min(kChunkBits, pix_end - p0);
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive_expect_tx(&bars[st], vb * gs);
+        }
+        __syncwarp();
+        if (lane < gs)
+            bulk_copy_g2s(stage_base + st * kStageBytes + lane * kRow,
+                          p.frames + static_cast<size_t>(in0 + lane) * p.nbits + p0, vb, &bars[st]);
+    };
+    if (wi == 0) {
+        const uint32_t pre = min(p.stages, nchunks);
+        for (uint32_t j = 0; j < pre; ++j) issue(j);
+    }
+
+    Planes P[CPT];
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+        P[i].ones = P[i].twos = P[i].fours = 0u;
+#pragma unroll
+        for (int h = 0; h < (int)kHiPlanes; ++h) P[i].hi[h] = 0u;
+    }
+
+    // ---- stream the windows: transpose chunks into X, then gather ----------------------
+    uint32_t j = 0;
+    for (uint32_t w = w0; w < w1; ++w) {
+        const uint32_t wbase = w * p.Lw;
+        const uint32_t wend = min(wbase + p.Lw, p.nbits);
+        const uint32_t nch = (wend - wbase + kChunkBits - 1) / kChunkBits;
+        for (uint32_t q = 0; q < nch; ++q, ++j) {
+            const uint32_t st = j % p.stages;
+            mbar_wait(&bars[st], (j / p.stages) & 1u);
+            const uint32_t vb = min(kChunkBits, wend - (wbase + q * kChunkBits));
+            // a1: warp wi turns block wi (32 pixels x 32 inputs) into 32 bit-sliced words
+            {
+                const uint8_t* row = stage_base + st * kStageBytes + lane * kRow + wi * 32u;
+                const uint4 a = *reinterpret_cast<const uint4*>(row);
+                const uint4 b = *reinterpret_cast<const uint4*>(row + 16);
+                uint32_t m = nonzero_mask32(a, b);
+                const int vloc = static_cast<int>(vb) - static_cast<int>(wi * 32u);
+                if (lane >= gs || vloc <= 0) m = 0u;
+                else if (vloc < 32) m &= 0x0F0F0F0Fu;  // vb is a multiple of 16
+                m = warp_transpose32(m, lane);
+                words[q * kChunkBits + wi * 32u + 4u * (lane & 7u) + (lane >> 3)] = m;
+            }
+            __syncthreads();  // stage st consumed; X words of this chunk visible
+            if (wi == 0 && j + p.stages < nchunks) issue(j + p.stages);
+        }
+        // a2: bit-sliced gather-count of this window's synapses (ELL, 8 slots per block)
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) {
+            const uint32_t cw = wi + 32u * i;
+            if (cw < p.ncw) {
+                const uint32_t cell = w * p.ncw + cw;
+                const uint32_t nb = p.ell_nb[cell];
+                const uint4* e = p.ell + p.ell_off[cell] + lane;
+#pragma unroll 2
+                for (uint32_t bk = 0; bk < nb; ++bk) {
+                    const uint4 s8 = __ldg(e + bk * 32u);
+                    accumulate8(P[i], words[s8.x & 0xFFFFu], words[s8.x >> 16], words[s8.y & 0xFFFFu],
+                                words[s8.y >> 16], words[s8.z & 0xFFFFu], words[s8.z >> 16],
+                                words[s8.w & 0xFFFFu], words[s8.w >> 16]);
+                }
+            }
+        }
+        __syncthreads();  // before the next window overwrites X
+    }
+
+    // ---- raw counts per input (partial if K > 1) into rawbuf[f][c] ----------------------
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+        const uint32_t cw = wi + 32u * i;
+        if (cw < p.ncw) {
+            const uint32_t c = cw * 32u + lane;
+            for (uint32_t f = 0; f < gs; ++f)
+                rawbuf[f * p.C32 + c] = static_cast<uint16_t>(extract_count(P[i], f));
+        }
+    }
+    cg::cluster_group cluster = cg::this_cluster();
+    if (K > 1) cluster.sync();
+    else __syncthreads();
+
+    // ---- a3/a4: per input: (cluster-sum), keys, k-winners, SDR ---------------------------
+    const uint32_t theta = p.min_overlap, L = p.keyL;
+    const uint64_t one = 1ull << 23;
+    for (uint32_t f = rank + K * wi; f < gs; f += K * 32u) {
+        uint16_t* row = rawbuf + f * p.C32;
+        if (K > 1) {
+            for (uint32_t c = lane; c < p.C32; c += 32u) {
+                uint32_t sum = 0;
+                for (uint32_t q = 0; q < K; ++q) sum += cluster.map_shared_rank(row, q)[c];
+                row[c] = static_cast<uint16_t>(sum);
+            }
+            __syncwarp();
+        }
+        const uint32_t gin = in0 + f;
+        if (p.raw_out) {
+            for (uint32_t c = lane; c < p.C; c += 32u) {
+                const uint32_t r = row[c];
+                p.raw_out[static_cast<size_t>(gin) * p.C + c] = static_cast<uint16_t>(r);
+                p.boosted_out[static_cast<size_t>(gin) * p.C + c] =
+                    r >= theta ? __fmul_rn(static_cast<float>(r), p.boost[c]) : 0.0f;
+            }
+        }
+        uint64_t T = 0;
+        if (p.radius == 0) {
+            // global: T = k-th largest key (bitwise search, warp-wide counts)
+            for (int bit = static_cast<int>(p.keyBits) - 1; bit >= 0; --bit) {
+                const uint64_t cand = T | (1ull << bit);
+                uint32_t cnt = 0;
+                for (uint32_t c = lane; c < p.C32; c += 32u) {
+                    uint64_t N;
+                    cnt += rank_key(row[c], s_bc[c], theta, c, L, N) >= cand ? 1u : 0u;
+                }
+                cnt = __reduce_add_sync(0xffffffffu, cnt);
+                if (cnt >= p.k) T = cand;
+            }
+        }
+        uint32_t total = 0;
+        for (uint32_t cw = 0; cw < p.ncw; ++cw) {
+            const uint32_t c = cw * 32u + lane;
+            uint64_t N;
+            const uint64_t key = rank_key(row[c], s_bc[c], theta, c, L, N);
+            bool act = N > one;
+            if (act) {
+                if (p.radius == 0) {
+                    act = key >= T;
+                } else {
+                    const uint32_t lo = c >= p.radius ? c - p.radius : 0u;
+                    const uint32_t hi = min(p.C - 1u, c + p.radius);
+                    uint32_t beats = 0;
+                    for (uint32_t d = lo; d <= hi && beats < p.k; ++d) {
+                        uint64_t Nd;
+                        beats += (d != c && rank_key(row[d], s_bc[d], theta, d, L, Nd) > key) ? 1u : 0u;
+                    }
+                    act = beats < p.k;
+                }
+            }
+            const uint32_t word = __ballot_sync(0xffffffffu, act);
+            if (lane == 0) p.sdr[static_cast<size_t>(gin) * p.ncw + cw] = word;
+            total += __popc(word);
+        }
+        if (lane == 0) p.counts[gin] = total;
+    }
+    if (K > 1) cluster.sync();  // peers may still read this CTA's partial counts
+}
+
+template <typename F>
+static cudaError_t allow_dynamic_smem(F* fn, int max_smem) {
+    cudaFuncAttributes a{};
+    cudaError_t e = cudaFuncGetAttributes(&a, fn);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                max_smem - static_cast<int>(a.sharedSizeBytes));
+}
+
+cudaError_t configure_batched(int max_smem) {
+    cudaError_t e = allow_dynamic_smem(sp_batched_kernel<1>, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2>, max_smem);
+    return e;
+}
+
+cudaError_t launch_batched(const BatchedParams& p, uint32_t smem_bytes, cudaStream_t s) {
+    const int cpt = static_cast<int>((p.ncw + 31u) / 32u);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(p.groups * p.K);
+    cfg.blockDim = dim3(kBatchedThreads);
+    cfg.dynamicSmemBytes = smem_bytes;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = p.K;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cpt <= 1) return cudaLaunchKernelEx(&cfg, sp_batched_kernel<1>, p);
+    return cudaLaunchKernelEx(&cfg, sp_batched_kernel<2>, p);
+}
+
+// Maximum co-resident clusters for K = 1..8 at this smem size (index K).
+cudaError_t batched_max_clusters(uint32_t smem_bytes, int max_clusters[9]) {
+    for (int K = 0; K <= 8; ++K) max_clusters[K] = 0;
+    cudaError_t e = cudaSuccess;
+    for (int K = 1; K <= 8; ++K) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(K * 64);
+        cfg.blockDim = dim3(kBatchedThreads);
+        cfg.dynamicSmemBytes = smem_bytes;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = K;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        e = cudaOccupancyMaxActiveClusters(&n, sp_batched_kernel<1>, &cfg);
+        if (e != cudaSuccess) {
+            (void)cudaGetLastError();
+            n = 0;
+        }
+        max_clusters[K] = n;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace sp

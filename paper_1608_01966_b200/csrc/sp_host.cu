@@ -1,0 +1,799 @@
+// sp_host.cu — host side of libsp: the C ABI of include/sp.h.
+//
+// Owns: configuration validation, seeded potential-pool
+// initialisation (DESIGN R8), the derived device layouts
+// (synapse-major idx|flag words; the bit-sliced path's windowed ELL), the
+// launch planner and the stream-ordered dispatch of the CUDA kernels.
+// There is no CPU compute path: every SP step runs in the kernels.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sp_internal.h"
+#include "../../include/sp_synth.h"
+
+#define SP_VERSION "htm-sp-b200 0.1.0 (sm_100a)"
+
+namespace {
+
+thread_local std::string g_err;
+
+sp_status fail(sp_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+sp_status cuda_fail(cudaError_t e, const char* what) {
+    return fail(SP_E_CUDA, "%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
+}
+
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+constexpr int kDefaultSms = 148;
+constexpr int kDefaultSmem = 232448;   // B200 max dynamic smem per block (opt-in)
+constexpr uint32_t kMaxInputBits = 1800000u;
+
+inline uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// Potential pools (DESIGN R8): column c's splitmix64 state starts at
+// splitmix64(seed ^ (c+1)*gamma); each draw advances the state by gamma and
+// outputs mix64(state); idx = ((u >> 32) * nbits) >> 32; duplicates are
+// rejected; the accepted S indices are sorted ascending.
+void init_pools(const sp_config& cfg, const sp::Geometry& g, uint32_t* idx) {
+    std::vector<uint8_t> seen(g.nbits, 0);
+    std::vector<uint32_t> chosen;
+    chosen.reserve(g.S);
+    for (uint32_t c = 0; c < g.C; ++c) {
+        uint64_t state = mix64((cfg.seed ^ (static_cast<uint64_t>(c + 1) * kGamma)) + kGamma);
+        chosen.clear();
+        while (chosen.size() < g.S) {
+            state += kGamma;
+            const uint64_t u = mix64(state);
+            const uint32_t i = static_cast<uint32_t>(((u >> 32) * g.nbits) >> 32);
+            if (!seen[i]) {
+                seen[i] = 1;
+                chosen.push_back(i);
+            }
+        }
+        for (uint32_t i : chosen) seen[i] = 0;
+        std::sort(chosen.begin(), chosen.end());
+        std::memcpy(idx + static_cast<size_t>(c) * g.S, chosen.data(), g.S * sizeof(uint32_t));
+    }
+}
+
+sp_status validate(const sp_config* c) {
+    if (!c) return fail(SP_E_ARG, "config is NULL");
+    if (c->input_width == 0 || c->input_height == 0)
+        return fail(SP_E_CONFIG, "input_width and input_height must be >= 1");
+    const bool whole = c->patch_width == 0 && c->patch_height == 0;
+    if (!whole) {
+        if (c->patch_width == 0 || c->patch_height == 0)
+            return fail(SP_E_CONFIG, "patch_width and patch_height must both be 0 or both >= 1");
+        if (c->input_width % c->patch_width || c->input_height % c->patch_height)
+            return fail(SP_E_CONFIG, "patch dims must divide the frame dims (%ux%u vs %ux%u)",
+                        c->patch_width, c->patch_height, c->input_width, c->input_height);
+    }
+    const uint64_t nbits = whole ? static_cast<uint64_t>(c->input_width) * c->input_height
+                                 : static_cast<uint64_t>(c->patch_width) * c->patch_height;
+    if (nbits > kMaxInputBits)
+        return fail(SP_E_CONFIG, "input bits per SP input (%llu) exceed %u",
+                    static_cast<unsigned long long>(nbits), kMaxInputBits);
+    if (c->num_columns == 0 || c->num_columns > 65536)
+        return fail(SP_E_CONFIG, "num_columns must be in [1, 65536]");
+    if (c->synapses_per_column == 0 || c->synapses_per_column > 4095)
+        return fail(SP_E_CONFIG, "synapses_per_column must be in [1, 4095]");
+    if (c->synapses_per_column > nbits)
+        return fail(SP_E_CONFIG, "synapses_per_column <= input_size violated (S:50): %u > %llu",
+                    c->synapses_per_column, static_cast<unsigned long long>(nbits));
+    if (c->min_overlap > c->synapses_per_column)
+        return fail(SP_E_CONFIG, "min_overlap <= synapses_per_column violated (S:49)");
+    if (c->winners_set_size == 0 || c->winners_set_size > c->num_columns)
+        return fail(SP_E_CONFIG, "1 <= winners_set_size <= num_columns violated (S:49)");
+    const float fr[4] = {c->perm_increment, c->perm_decrement, c->initial_permanence,
+                         c->connected_threshold};
+    const char* names[4] = {"perm_increment", "perm_decrement", "initial_permanence",
+                            "connected_threshold"};
+    for (int i = 0; i < 4; ++i)
+        if (!(fr[i] >= 0.0f && fr[i] <= 1.0f))
+            return fail(SP_E_CONFIG, "%s must be in [0,1] (S:48)", names[i]);
+    const uint32_t C32 = (c->num_columns + 31u) & ~31u;
+    if (sp::bits_for(c->synapses_per_column) + 27u + sp::ceil_log2(C32) > 64u)
+        return fail(SP_E_CONFIG, "rank key exceeds 64 bits: ceil(log2(S+1))+27+ceil(log2(C32)) > 64");
+    if (c->max_inputs == 0) return fail(SP_E_CONFIG, "max_inputs must be >= 1");
+    if (c->force_path > SP_PATH_BATCHED)
+        return fail(SP_E_CONFIG, "force_path must be SP_PATH_AUTO/PER_INPUT/BATCHED");
+    return SP_OK;
+}
+
+}  // namespace
+
+namespace sp {
+
+Geometry make_geometry(const sp_config& cfg) {
+    Geometry g{};
+    g.W = cfg.input_width;
+    g.H = cfg.input_height;
+    g.whole = cfg.patch_width == 0 && cfg.patch_height == 0;
+    g.pw = g.whole ? g.W : cfg.patch_width;
+    g.ph = g.whole ? g.H : cfg.patch_height;
+    g.P = (g.W / g.pw) * (g.H / g.ph);
+    g.nbits = g.pw * g.ph;
+    g.C = cfg.num_columns;
+    g.C32 = (g.C + 31u) & ~31u;
+    g.ncw = g.C32 / 32u;
+    g.S = cfg.synapses_per_column;
+    g.keyL = ceil_log2(g.C32);
+    g.keyBits = bits_for(g.S) + 27u + g.keyL;
+    return g;
+}
+
+// Shared-memory plan of the batched kernel: ring of `stages` chunks of 32 x (1024+16) B,
+// a region holding max(Lw+1 words, 32*C32 uint16 counts), Bc[C32], mbarriers.
+BatchedLayout plan_batched_layout(const Geometry& g, int max_smem) {
+    BatchedLayout L;
+    if (g.C32 > kMaxBatchedColumns || g.S > kMaxBatchedSynapses) return L;
+    const uint32_t stage_bytes = 32u * (kChunkBits + kStagePad);
+    const uint32_t counts_bytes = 32u * g.C32 * 2u;
+    const uint32_t fixed = g.C32 * 4u + 64u;  // Bc + barriers (<= 8 stages)
+    const uint32_t nbits_r = (g.nbits + kChunkBits - 1) / kChunkBits * kChunkBits;
+    for (uint32_t stages = 4; stages >= 2; --stages) {
+        const int64_t avail = static_cast<int64_t>(max_smem) - stages * stage_bytes - fixed;
+        if (avail < static_cast<int64_t>(counts_bytes) || avail < 4 * (kChunkBits + 1)) continue;
+        // largest Lw (multiple of Lc, local idx < 65536) with (Lw+1)*4 <= avail
+        uint32_t Lw = static_cast<uint32_t>((avail / 4 - 1) / kChunkBits * kChunkBits);
+        Lw = std::min<uint32_t>(Lw, 63u * kChunkBits);
+        Lw = std::min<uint32_t>(Lw, nbits_r);
+        if (Lw == 0) continue;
+        // balance the windows: same count, smallest Lw (multiple of Lc) that covers nbits
+        const uint32_t nwin = (g.nbits + Lw - 1) / Lw;
+        const uint32_t per = (g.nbits + nwin - 1) / nwin;
+        Lw = (per + kChunkBits - 1) / kChunkBits * kChunkBits;
+        L.ok = true;
+        L.stages = stages;
+        L.Lw = Lw;
+        L.nwin = (g.nbits + Lw - 1) / Lw;
+        L.region_bytes = (std::max(counts_bytes, (Lw + 1) * 4u) + 15u) & ~15u;
+        L.smem_bytes = stages * stage_bytes + L.region_bytes + g.C32 * 4u + stages * 8u;
+        return L;
+    }
+    return L;
+}
+
+// Groups of <= 32 inputs and cluster size K: estimated time of each K
+// from an HBM term and a per-CTA term (bytes at a per-SM rate, transpose ALU cycles).
+void plan_batched_grid(const Geometry& g, uint32_t nwin, uint32_t n, int sm_count,
+                       const int* max_clusters, uint32_t* groups, uint32_t* Kout) {
+    const double hbm_bpc = 3400.0;   // chip HBM bytes per SM-cycle (~6.5 TB/s @ 1.9 GHz)
+    const double sm_bpc = 48.0;      // one SM's sustainable stream rate, bytes per cycle
+    const double alu_per_px = 0.65;  // transpose cycles per pixel per CTA (32 inputs at once)
+    const uint32_t gmin = (n + 31u) / 32u;
+    double best = 1e300;
+    uint32_t bestG = gmin, bestK = 1;
+    for (uint32_t K = 1; K <= 8; ++K) {
+        if (K > nwin) break;
+        int cap = max_clusters ? max_clusters[K] : sm_count / static_cast<int>(K);
+        if (cap <= 0) continue;
+        const uint32_t G = std::max<uint32_t>(gmin, std::min<uint32_t>(n, static_cast<uint32_t>(cap)));
+        const uint32_t waves = (G + cap - 1) / cap;
+        const uint32_t gs = (n + G - 1) / G;
+        const double bytes_cta = static_cast<double>(gs) * g.nbits / K;
+        const double alu_cta = alu_per_px * g.nbits / K +
+                               ((gs + K - 1) / K > 0 ? 6.0 * g.keyBits * g.ncw : 0.0);
+        const double t = std::max(static_cast<double>(n) * g.nbits / hbm_bpc,
+                                  waves * std::max(bytes_cta / sm_bpc, alu_cta));
+        if (t < best * 0.98) {
+            best = t;
+            bestG = G;
+            bestK = K;
+        }
+    }
+    *groups = bestG;
+    *Kout = bestK;
+}
+
+}  // namespace sp
+
+struct sp_handle {
+    sp_config cfg{};
+    sp::Geometry g{};
+    sp::BatchedLayout lay{};
+    int device = 0, sm_count = kDefaultSms, max_smem = kDefaultSmem;
+    int max_clusters[9] = {0};
+    // device state (canonical order) and derived layouts
+    uint32_t* d_idx = nullptr;
+    float* d_perm = nullptr;
+    float* d_boost = nullptr;
+    uint32_t* d_bc = nullptr;
+    uint32_t* d_syn = nullptr;
+    uint4* d_ell = nullptr;
+    uint32_t* d_ell_off = nullptr;
+    uint16_t* d_ell_nb = nullptr;
+    uint32_t* d_ell_pos = nullptr;
+    uint32_t ell_slots = 0;
+    bool ell_dirty = false;
+    // scratch and results
+    uint32_t Wn = 0, sub_inputs = 0;
+    uint32_t* d_bits = nullptr;
+    uint32_t* d_raw = nullptr;
+    uint32_t* d_sdr = nullptr;
+    uint32_t* d_counts = nullptr;
+    uint16_t* d_raw_rec = nullptr;
+    float* d_boosted_rec = nullptr;
+    // end-to-end staging
+    uint8_t* d_stage[2] = {nullptr, nullptr};
+    uint32_t stage_frames = 0;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+    // bookkeeping
+    std::vector<uint32_t> h_idx;
+    uint32_t last_inputs = 0;
+    bool has_result = false;
+    std::atomic<uint64_t> launches{0};
+    sp_plan_info last_plan{};
+};
+
+namespace {
+
+template <typename T>
+cudaError_t dalloc(T** p, size_t count) {
+    if (count == 0) count = 1;
+    return cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+}
+
+void release(sp_handle* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    void* ptrs[] = {h->d_idx,  h->d_perm,    h->d_boost,   h->d_bc,      h->d_syn,
+                    h->d_ell,  h->d_ell_off, h->d_ell_nb,  h->d_ell_pos, h->d_bits,
+                    h->d_raw,  h->d_sdr,     h->d_counts,  h->d_raw_rec, h->d_boosted_rec,
+                    h->d_stage[0], h->d_stage[1]};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
+    for (int i = 0; i < 2; ++i) {
+        if (h->ev_h2d[i]) cudaEventDestroy(h->ev_h2d[i]);
+        if (h->ev_free[i]) cudaEventDestroy(h->ev_free[i]);
+    }
+    delete h;
+}
+
+sp_plan_info make_plan(const sp_handle* h, uint32_t n, bool learn, const uint8_t* frames) {
+    sp_plan_info pl{};
+    const sp::Geometry& g = h->g;
+    pl.input_bits = g.nbits;
+    pl.inputs_per_frame = g.P;
+    pl.num_inputs = n;
+    pl.columns_padded = g.C32;
+    pl.sdr_words = g.ncw;
+    uint32_t reason = 0;
+    if (learn) reason |= sp::kNotBatchedLearn;
+    if (!g.whole) reason |= sp::kNotBatchedPatch;
+    if (g.nbits % 16u) reason |= sp::kNotBatchedAlign;
+    if (frames && (reinterpret_cast<uintptr_t>(frames) & 15u)) reason |= sp::kNotBatchedAlign;
+    if (g.C32 > sp::kMaxBatchedColumns) reason |= sp::kNotBatchedColumns;
+    if (g.S > sp::kMaxBatchedSynapses) reason |= sp::kNotBatchedSynapses;
+    if (h->cfg.force_path == SP_PATH_PER_INPUT) reason |= sp::kNotBatchedForced;
+    if (!h->lay.ok) reason |= sp::kNotBatchedSmem;
+    pl.reason = reason;
+    if (reason == 0 && n > 0) {
+        pl.path = SP_PATH_BATCHED;
+        uint32_t G = 0, K = 1;
+        sp::plan_batched_grid(g, h->lay.nwin, n, h->sm_count, h->max_clusters[1] ? h->max_clusters : nullptr, &G,
+                              &K);
+        pl.groups = G;
+        pl.cluster = K;
+        pl.ctas = G * K;
+        pl.window_bits = h->lay.Lw;
+        pl.num_windows = h->lay.nwin;
+        pl.chunk_bits = sp::kChunkBits;
+        pl.stages = h->lay.stages;
+        pl.smem_bytes = h->lay.smem_bytes;
+    } else {
+        pl.path = SP_PATH_PER_INPUT;
+    }
+    return pl;
+}
+
+// Windowed ELL of the batched path.  Cell (w, cw) holds, for the 32
+// columns of column-warp cw, their synapses falling in window w as uint16 window-local
+// indices, 8 slots per lane per block, blocks laid out [block][lane] (coalesced uint4
+// per lane).  Disconnected synapses and padding point to the zero slot Lw.
+sp_status build_ell(sp_handle* h, const float* perm_host) {
+    const sp::Geometry& g = h->g;
+    const uint32_t Lw = h->lay.Lw, nwin = h->lay.nwin;
+    std::vector<uint32_t> cnt(static_cast<size_t>(nwin) * g.C32, 0);
+    for (uint32_t c = 0; c < g.C; ++c)
+        for (uint32_t s = 0; s < g.S; ++s) cnt[static_cast<size_t>(h->h_idx[c * g.S + s] / Lw) * g.C32 + c]++;
+    std::vector<uint32_t> off(static_cast<size_t>(nwin) * g.ncw), nb(off.size());
+    uint64_t total = 0;
+    for (uint32_t w = 0; w < nwin; ++w)
+        for (uint32_t cw = 0; cw < g.ncw; ++cw) {
+            uint32_t mx = 0;
+            for (uint32_t l = 0; l < 32; ++l) mx = std::max(mx, cnt[static_cast<size_t>(w) * g.C32 + cw * 32 + l]);
+            const size_t cell = static_cast<size_t>(w) * g.ncw + cw;
+            nb[cell] = (mx + 7u) / 8u;
+            off[cell] = static_cast<uint32_t>(total);
+            total += static_cast<uint64_t>(nb[cell]) * 32u;
+            if (nb[cell] > 65535u) return fail(SP_E_CONFIG, "ELL cell too large");
+        }
+    if (total * 8u >= (1ull << 32)) return fail(SP_E_CONFIG, "ELL exceeds 2^32 slots");
+    std::vector<uint16_t> ell(static_cast<size_t>(total) * 8u, static_cast<uint16_t>(Lw));
+    std::vector<uint32_t> pos(static_cast<size_t>(g.C) * g.S);
+    std::vector<uint32_t> fill(static_cast<size_t>(nwin) * g.C32, 0);
+    const float tau = h->cfg.connected_threshold;
+    for (uint32_t c = 0; c < g.C; ++c) {
+        const uint32_t cw = c / 32u, lane = c % 32u;
+        for (uint32_t s = 0; s < g.S; ++s) {
+            const uint32_t i = h->h_idx[c * g.S + s];
+            const uint32_t w = i / Lw;
+            const uint32_t slot = fill[static_cast<size_t>(w) * g.C32 + c]++;
+            const size_t cell = static_cast<size_t>(w) * g.ncw + cw;
+            const size_t p = (static_cast<size_t>(off[cell]) + (slot / 8u) * 32u + lane) * 8u + slot % 8u;
+            ell[p] = static_cast<uint16_t>(perm_host[c * g.S + s] >= tau ? i % Lw : Lw);
+            pos[static_cast<size_t>(c) * g.S + s] = static_cast<uint32_t>(p);
+        }
+    }
+    std::vector<uint16_t> nb16(nb.begin(), nb.end());
+    if (h->d_ell) cudaFree(h->d_ell), h->d_ell = nullptr;
+    if (h->d_ell_off) cudaFree(h->d_ell_off), h->d_ell_off = nullptr;
+    if (h->d_ell_nb) cudaFree(h->d_ell_nb), h->d_ell_nb = nullptr;
+    if (h->d_ell_pos) cudaFree(h->d_ell_pos), h->d_ell_pos = nullptr;
+    cudaError_t e = dalloc(&h->d_ell, total);
+    if (e == cudaSuccess) e = dalloc(&h->d_ell_off, off.size());
+    if (e == cudaSuccess) e = dalloc(&h->d_ell_nb, nb16.size());
+    if (e == cudaSuccess) e = dalloc(&h->d_ell_pos, pos.size());
+    if (e != cudaSuccess) return fail(SP_E_OOM, "ELL allocation failed: %s", cudaGetErrorString(e));
+    e = cudaMemcpy(h->d_ell, ell.data(), ell.size() * 2u, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_ell_off, off.data(), off.size() * 4u, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_ell_nb, nb16.data(), nb16.size() * 2u, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_ell_pos, pos.data(), pos.size() * 4u, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "ELL upload");
+    h->ell_slots = static_cast<uint32_t>(total * 8u);
+    h->ell_dirty = false;
+    return SP_OK;
+}
+
+// Uploads a full canonical state and rebuilds every derived layout (synchronous).
+sp_status upload_state(sp_handle* h, const uint32_t* idx, const float* perm, const float* boost) {
+    const sp::Geometry& g = h->g;
+    const size_t cs = static_cast<size_t>(g.C) * g.S;
+    h->h_idx.assign(idx, idx + cs);
+    std::vector<float> boost32(g.C32, 1.0f);
+    std::vector<uint32_t> bc(g.C32, 0u);
+    for (uint32_t c = 0; c < g.C; ++c) {
+        boost32[c] = boost[c];
+        bc[c] = static_cast<uint32_t>(boost[c] * 8388608.0f);  // exact: boost in [1,16) (R4)
+    }
+    cudaError_t e = cudaMemcpy(h->d_idx, idx, cs * 4u, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_perm, perm, cs * 4u, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_boost, boost32.data(), g.C32 * 4u, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_bc, bc.data(), g.C32 * 4u, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "state upload");
+    e = sp::launch_build_syn(h->d_idx, h->d_perm, h->cfg.connected_threshold, g.C, g.C32, g.S,
+                             h->d_syn, nullptr);
+    h->launches++;
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, "synapse layout build");
+    if (h->lay.ok) return build_ell(h, perm);
+    return SP_OK;
+}
+
+sp_status check_handle(sp_handle* h) {
+    if (!h) return fail(SP_E_ARG, "handle is NULL");
+    cudaError_t e = cudaSetDevice(h->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    return SP_OK;
+}
+
+// Launches the hot path for n_frames frames; results go to rows [row0, row0 + n) of the
+// handle's result buffers.
+sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, int learn,
+                       cudaStream_t s, uint32_t row0) {
+    const sp::Geometry& g = h->g;
+    const uint32_t n = n_frames * g.P;
+    sp_plan_info pl = make_plan(h, n, learn != 0, frames);
+    if (h->cfg.force_path == SP_PATH_BATCHED && pl.path != SP_PATH_BATCHED)
+        return fail(SP_E_ARG, "force_path=BATCHED but the batched path is not eligible (reason 0x%x)",
+                    pl.reason);
+    h->last_plan = pl;
+    const bool rec = (h->cfg.flags & SP_FLAG_RECORD_OVERLAPS) != 0;
+    cudaError_t e = cudaSuccess;
+    if (pl.path == SP_PATH_BATCHED) {
+        if (h->ell_dirty) {
+            e = sp::launch_refresh_ell(h->d_idx, h->d_perm, h->d_ell_pos, h->cfg.connected_threshold,
+                                       g.C, g.S, h->lay.Lw, reinterpret_cast<uint16_t*>(h->d_ell), s);
+            h->launches++;
+            if (e != cudaSuccess) return cuda_fail(e, "ELL refresh launch");
+            h->ell_dirty = false;
+        }
+        sp::BatchedParams p{};
+        p.frames = frames;
+        p.num_inputs = n;
+        p.nbits = g.nbits;
+        p.C = g.C;
+        p.C32 = g.C32;
+        p.ncw = g.ncw;
+        p.min_overlap = h->cfg.min_overlap;
+        p.k = h->cfg.winners_set_size;
+        p.radius = h->cfg.inhibition_radius;
+        p.keyL = g.keyL;
+        p.keyBits = g.keyBits;
+        p.Lw = h->lay.Lw;
+        p.nwin = h->lay.nwin;
+        p.stages = h->lay.stages;
+        p.region_bytes = h->lay.region_bytes;
+        p.groups = pl.groups;
+        p.K = pl.cluster;
+        p.ell_off = h->d_ell_off;
+        p.ell_nb = h->d_ell_nb;
+        p.ell = h->d_ell;
+        p.bc = h->d_bc;
+        p.boost = h->d_boost;
+        p.sdr = h->d_sdr + static_cast<size_t>(row0) * g.ncw;
+        p.counts = h->d_counts + row0;
+        p.raw_out = rec ? h->d_raw_rec + static_cast<size_t>(row0) * g.C : nullptr;
+        p.boosted_out = rec ? h->d_boosted_rec + static_cast<size_t>(row0) * g.C : nullptr;
+        e = sp::launch_batched(p, h->lay.smem_bytes, s);
+        h->launches++;
+        if (e != cudaSuccess) return cuda_fail(e, "batched kernel launch");
+        return SP_OK;
+    }
+    // per-input path, sub-batches of whole frames
+    const uint32_t fpb = std::max<uint32_t>(1u, h->sub_inputs / g.P);
+    for (uint32_t f0 = 0; f0 < n_frames; f0 += fpb) {
+        const uint32_t nf = std::min(fpb, n_frames - f0);
+        sp::PerInputParams p{};
+        p.frames = frames + static_cast<size_t>(f0) * g.W * g.H;
+        p.first_input = row0 + f0 * g.P;
+        p.num_inputs = nf * g.P;
+        p.g = g;
+        p.min_overlap = h->cfg.min_overlap;
+        p.k = h->cfg.winners_set_size;
+        p.radius = h->cfg.inhibition_radius;
+        p.inc = h->cfg.perm_increment;
+        p.dec = h->cfg.perm_decrement;
+        p.tau = h->cfg.connected_threshold;
+        p.bits = h->d_bits;
+        p.Wn = h->Wn;
+        p.syn = h->d_syn;
+        p.syn_rw = h->d_syn;
+        p.idx = h->d_idx;
+        p.perm = h->d_perm;
+        p.bc = h->d_bc;
+        p.boost = h->d_boost;
+        p.raw = h->d_raw;
+        p.sdr = h->d_sdr;
+        p.counts = h->d_counts;
+        p.raw_out = rec ? h->d_raw_rec : nullptr;
+        p.boosted_out = rec ? h->d_boosted_rec : nullptr;
+        e = sp::launch_pack(p, s);
+        h->launches++;
+        if (e != cudaSuccess) return cuda_fail(e, "pack launch");
+        if (!learn) {
+            e = sp::launch_overlap(p, s);
+            h->launches++;
+            if (e == cudaSuccess) e = sp::launch_inhibit(p, s);
+            h->launches++;
+            if (e != cudaSuccess) return cuda_fail(e, "overlap/inhibit launch");
+            continue;
+        }
+        // learning: the recurrence over inputs, in order
+        for (uint32_t t = 0; t < p.num_inputs; ++t) {
+            sp::PerInputParams q = p;
+            q.bits = h->d_bits + static_cast<size_t>(t) * h->Wn;
+            q.raw = h->d_raw + static_cast<size_t>(t) * g.C32;
+            q.first_input = p.first_input + t;
+            q.num_inputs = 1;
+            e = sp::launch_overlap(q, s);
+            h->launches++;
+            if (e == cudaSuccess) e = sp::launch_inhibit(q, s);
+            h->launches++;
+            if (e == cudaSuccess) e = sp::launch_learn(q, 0, s);
+            h->launches++;
+            if (e != cudaSuccess) return cuda_fail(e, "learning step launch");
+        }
+        h->ell_dirty = true;
+    }
+    return SP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sp_last_error(void) { return g_err.c_str(); }
+
+const char* sp_version(void) { return SP_VERSION; }
+
+sp_status sp_config_default(sp_config* cfg) {
+    if (!cfg) return fail(SP_E_ARG, "config is NULL");
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->input_width = 240;   // Tab. 1
+    cfg->input_height = 134;
+    cfg->num_columns = 2048;  // Tab. 2
+    cfg->synapses_per_column = 128;
+    cfg->min_overlap = 8;
+    cfg->winners_set_size = 40;
+    cfg->inhibition_radius = 0;
+    cfg->perm_increment = 0.1f;
+    cfg->perm_decrement = 0.1f;
+    cfg->initial_permanence = 0.21f;
+    cfg->connected_threshold = 0.2f;
+    cfg->seed = 42;
+    cfg->device = 0;
+    cfg->max_inputs = 4096;
+    return SP_OK;
+}
+
+sp_status sp_init_pools_host(const sp_config* cfg, uint32_t* idx_out) {
+    sp_status st = validate(cfg);
+    if (st != SP_OK) return st;
+    if (!idx_out) return fail(SP_E_ARG, "idx_out is NULL");
+    init_pools(*cfg, sp::make_geometry(*cfg), idx_out);
+    return SP_OK;
+}
+
+sp_status sp_plan(const sp_config* cfg, uint32_t num_frames, int32_t sm_count, sp_plan_info* out) {
+    sp_status st = validate(cfg);
+    if (st != SP_OK) return st;
+    if (!out) return fail(SP_E_ARG, "out is NULL");
+    sp_handle tmp;
+    tmp.cfg = *cfg;
+    tmp.g = sp::make_geometry(*cfg);
+    tmp.sm_count = sm_count > 0 ? sm_count : kDefaultSms;
+    tmp.max_smem = kDefaultSmem;
+    tmp.lay = sp::plan_batched_layout(tmp.g, tmp.max_smem);
+    *out = make_plan(&tmp, num_frames * tmp.g.P, false, nullptr);
+    return SP_OK;
+}
+
+sp_status sp_create(const sp_config* cfg, sp_handle** out) {
+    if (!out) return fail(SP_E_ARG, "out is NULL");
+    *out = nullptr;
+    sp_status st = validate(cfg);
+    if (st != SP_OK) return st;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(SP_E_CUDA, "no CUDA device available (%s)", cudaGetErrorString(e));
+    if (cfg->device < 0 || cfg->device >= ndev) return fail(SP_E_ARG, "device %d out of range", cfg->device);
+    e = cudaSetDevice(cfg->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    sp_handle* h = new sp_handle();
+    h->cfg = *cfg;
+    h->device = cfg->device;
+    h->g = sp::make_geometry(*cfg);
+    cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device);
+    cudaDeviceGetAttribute(&h->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
+    h->lay = sp::plan_batched_layout(h->g, h->max_smem);
+    const sp::Geometry& g = h->g;
+    if ((e = sp::configure_batched(h->max_smem)) != cudaSuccess ||
+        (e = sp::configure_per_input(h->max_smem)) != cudaSuccess) {
+        release(h);
+        return cuda_fail(e, "kernel attributes");
+    }
+    if (h->lay.ok) sp::batched_max_clusters(h->lay.smem_bytes, h->max_clusters);
+    h->Wn = (g.nbits + 31u) / 32u;
+    h->sub_inputs = std::max<uint32_t>(sp::kPerInputChunk, g.P);
+    const size_t cs = static_cast<size_t>(g.C) * g.S;
+    const size_t cap = cfg->max_inputs;
+    e = dalloc(&h->d_idx, cs);
+    if (e == cudaSuccess) e = dalloc(&h->d_perm, cs);
+    if (e == cudaSuccess) e = dalloc(&h->d_boost, g.C32);
+    if (e == cudaSuccess) e = dalloc(&h->d_bc, g.C32);
+    if (e == cudaSuccess) e = dalloc(&h->d_syn, static_cast<size_t>(g.S) * g.C32);
+    if (e == cudaSuccess) e = dalloc(&h->d_bits, static_cast<size_t>(h->sub_inputs) * h->Wn);
+    if (e == cudaSuccess) e = dalloc(&h->d_raw, static_cast<size_t>(h->sub_inputs) * g.C32);
+    if (e == cudaSuccess) e = dalloc(&h->d_sdr, cap * g.ncw);
+    if (e == cudaSuccess) e = dalloc(&h->d_counts, cap);
+    if (e == cudaSuccess && (cfg->flags & SP_FLAG_RECORD_OVERLAPS)) {
+        e = dalloc(&h->d_raw_rec, cap * g.C);
+        if (e == cudaSuccess) e = dalloc(&h->d_boosted_rec, cap * g.C);
+    }
+    if (e != cudaSuccess) {
+        release(h);
+        return fail(SP_E_OOM, "device allocation failed: %s", cudaGetErrorString(e));
+    }
+    std::vector<uint32_t> idx(cs);
+    init_pools(*cfg, g, idx.data());
+    std::vector<float> perm(cs, cfg->initial_permanence);
+    std::vector<float> boost(g.C, 1.0f);
+    st = upload_state(h, idx.data(), perm.data(), boost.data());
+    if (st != SP_OK) {
+        std::string msg = g_err;
+        release(h);
+        g_err = msg;
+        return st;
+    }
+    h->last_plan = make_plan(h, cfg->max_inputs, false, nullptr);
+    *out = h;
+    return SP_OK;
+}
+
+sp_status sp_destroy(sp_handle* h) {
+    if (!h) return SP_OK;
+    cudaSetDevice(h->device);
+    cudaDeviceSynchronize();
+    release(h);
+    return SP_OK;
+}
+
+sp_status sp_compute(sp_handle* h, const uint8_t* frames_dev, uint32_t num_frames, int learn,
+                     void* cuda_stream) {
+    sp_status st = check_handle(h);
+    if (st != SP_OK) return st;
+    const uint64_t n = static_cast<uint64_t>(num_frames) * h->g.P;
+    if (n > h->cfg.max_inputs)
+        return fail(SP_E_ARG, "num_frames * inputs_per_frame = %llu exceeds max_inputs %u",
+                    static_cast<unsigned long long>(n), h->cfg.max_inputs);
+    if (num_frames > 0 && !frames_dev) return fail(SP_E_ARG, "frames_dev is NULL");
+    h->last_inputs = static_cast<uint32_t>(n);
+    h->has_result = true;
+    if (n == 0) return SP_OK;
+    return compute_impl(h, frames_dev, num_frames, learn, static_cast<cudaStream_t>(cuda_stream), 0);
+}
+
+sp_status sp_winners(sp_handle* h, uint32_t* sdr_dev, uint32_t* count_dev, void* cuda_stream) {
+    sp_status st = check_handle(h);
+    if (st != SP_OK) return st;
+    if (!h->has_result) return fail(SP_E_STATE, "sp_winners before any sp_compute");
+    if (h->last_inputs == 0) return SP_OK;
+    if (!sdr_dev) return fail(SP_E_ARG, "sdr_dev is NULL");
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    cudaError_t e = cudaMemcpyAsync(sdr_dev, h->d_sdr,
+                                    static_cast<size_t>(h->last_inputs) * h->g.ncw * 4u,
+                                    cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess && count_dev)
+        e = cudaMemcpyAsync(count_dev, h->d_counts, h->last_inputs * 4u, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "sp_winners copy");
+    return SP_OK;
+}
+
+sp_status sp_overlaps(sp_handle* h, uint16_t* raw_dev, float* boosted_dev, void* cuda_stream) {
+    sp_status st = check_handle(h);
+    if (st != SP_OK) return st;
+    if (!(h->cfg.flags & SP_FLAG_RECORD_OVERLAPS))
+        return fail(SP_E_STATE, "sp_overlaps needs SP_FLAG_RECORD_OVERLAPS at create");
+    if (!h->has_result) return fail(SP_E_STATE, "sp_overlaps before any sp_compute");
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    const size_t n = static_cast<size_t>(h->last_inputs) * h->g.C;
+    cudaError_t e = cudaSuccess;
+    if (raw_dev && n) e = cudaMemcpyAsync(raw_dev, h->d_raw_rec, n * 2u, cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess && boosted_dev && n)
+        e = cudaMemcpyAsync(boosted_dev, h->d_boosted_rec, n * 4u, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "sp_overlaps copy");
+    return SP_OK;
+}
+
+sp_status sp_get_state(sp_handle* h, uint32_t* idx, float* perm, float* boost) {
+    sp_status st = check_handle(h);
+    if (st != SP_OK) return st;
+    cudaError_t e = cudaDeviceSynchronize();
+    const size_t cs = static_cast<size_t>(h->g.C) * h->g.S;
+    if (e == cudaSuccess && idx) e = cudaMemcpy(idx, h->d_idx, cs * 4u, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && perm) e = cudaMemcpy(perm, h->d_perm, cs * 4u, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && boost) e = cudaMemcpy(boost, h->d_boost, h->g.C * 4u, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "sp_get_state");
+    return SP_OK;
+}
+
+sp_status sp_set_state(sp_handle* h, const uint32_t* idx, const float* perm, const float* boost) {
+    sp_status st = check_handle(h);
+    if (st != SP_OK) return st;
+    const sp::Geometry& g = h->g;
+    const size_t cs = static_cast<size_t>(g.C) * g.S;
+    if (idx) {
+        for (uint32_t c = 0; c < g.C; ++c)
+            for (uint32_t s = 0; s < g.S; ++s) {
+                const uint32_t v = idx[c * g.S + s];
+                if (v >= g.nbits)
+                    return fail(SP_E_ARG, "idx[%u][%u] = %u >= input bits %u (S:74)", c, s, v, g.nbits);
+                if (s && v <= idx[c * g.S + s - 1])
+                    return fail(SP_E_ARG, "idx of column %u not strictly ascending at %u (S:74)", c, s);
+            }
+    }
+    if (perm)
+        for (size_t i = 0; i < cs; ++i)
+            if (!(perm[i] >= 0.0f && perm[i] <= 1.0f))
+                return fail(SP_E_ARG, "perm[%zu] = %g outside [0,1] (S:73)", i, perm[i]);
+    if (boost)
+        for (uint32_t c = 0; c < g.C; ++c)
+            if (!(boost[c] >= 1.0f && boost[c] < 16.0f))
+                return fail(SP_E_ARG, "boost[%u] = %g outside [1,16) (R4)", c, boost[c]);
+    // merge with the current state for NULL arguments
+    std::vector<uint32_t> cur_idx;
+    std::vector<float> cur_perm, cur_boost;
+    if (!idx || !perm || !boost) {
+        cur_idx.resize(cs);
+        cur_perm.resize(cs);
+        cur_boost.resize(g.C);
+        st = sp_get_state(h, cur_idx.data(), cur_perm.data(), cur_boost.data());
+        if (st != SP_OK) return st;
+    }
+    cudaDeviceSynchronize();
+    return upload_state(h, idx ? idx : cur_idx.data(), perm ? perm : cur_perm.data(),
+                        boost ? boost : cur_boost.data());
+}
+
+sp_status sp_compute_host(sp_handle* h, const uint8_t* frames_host, uint32_t num_frames, int learn,
+                          uint32_t* sdr_host, uint32_t* count_host, void* cuda_stream) {
+    sp_status st = check_handle(h);
+    if (st != SP_OK) return st;
+    const sp::Geometry& g = h->g;
+    const uint64_t n = static_cast<uint64_t>(num_frames) * g.P;
+    if (n > h->cfg.max_inputs)
+        return fail(SP_E_ARG, "num_frames * inputs_per_frame = %llu exceeds max_inputs %u",
+                    static_cast<unsigned long long>(n), h->cfg.max_inputs);
+    if (num_frames > 0 && (!frames_host || !sdr_host)) return fail(SP_E_ARG, "NULL host buffer");
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    const size_t frame_bytes = static_cast<size_t>(g.W) * g.H;
+    cudaError_t e = cudaSuccess;
+    if (!h->copy_stream) {
+        // chunk of frames per pipeline stage: ~64 MiB, at least 1 frame
+        h->stage_frames = static_cast<uint32_t>(std::max<size_t>(1, (64u << 20) / frame_bytes));
+        e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking);
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+            e = cudaEventCreateWithFlags(&h->ev_h2d[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_free[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = dalloc(&h->d_stage[i], h->stage_frames * frame_bytes);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "end-to-end staging setup");
+    }
+    h->last_inputs = static_cast<uint32_t>(n);
+    h->has_result = true;
+    uint32_t chunk = 0;
+    for (uint32_t f0 = 0; f0 < num_frames; f0 += h->stage_frames, ++chunk) {
+        const uint32_t nf = std::min(h->stage_frames, num_frames - f0);
+        const int b = chunk & 1;
+        // H2D on the copy stream once the buffer's previous compute has finished
+        if (chunk >= 2) e = cudaStreamWaitEvent(h->copy_stream, h->ev_free[b], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(h->d_stage[b], frames_host + f0 * frame_bytes, nf * frame_bytes,
+                                cudaMemcpyHostToDevice, h->copy_stream);
+        if (e == cudaSuccess) e = cudaEventRecord(h->ev_h2d[b], h->copy_stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, h->ev_h2d[b], 0);
+        if (e != cudaSuccess) return cuda_fail(e, "end-to-end H2D");
+        st = compute_impl(h, h->d_stage[b], nf, learn, s, f0 * g.P);
+        if (st != SP_OK) return st;
+        e = cudaEventRecord(h->ev_free[b], s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(sdr_host + static_cast<size_t>(f0) * g.P * g.ncw,
+                                h->d_sdr + static_cast<size_t>(f0) * g.P * g.ncw,
+                                static_cast<size_t>(nf) * g.P * g.ncw * 4u, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && count_host)
+            e = cudaMemcpyAsync(count_host + static_cast<size_t>(f0) * g.P, h->d_counts + static_cast<size_t>(f0) * g.P,
+                                static_cast<size_t>(nf) * g.P * 4u, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return cuda_fail(e, "end-to-end D2H");
+    }
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "end-to-end sync");
+    return SP_OK;
+}
+
+sp_status sp_get_info(sp_handle* h, sp_info* out) {
+    if (!h) return fail(SP_E_ARG, "handle is NULL");
+    if (!out) return fail(SP_E_ARG, "out is NULL");
+    std::memset(out, 0, sizeof(*out));
+    out->plan = h->last_plan;
+    out->kernel_launches = h->launches.load();
+    out->last_num_inputs = h->last_inputs;
+    out->ell_slots = h->ell_slots;
+    out->sm_count = h->sm_count;
+    out->max_smem_optin = h->max_smem;
+    return SP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,124 @@
+// sp_internal.h — shared declarations of the libsp CUDA sources (not part of the ABI).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/sp.h"
+
+namespace sp {
+
+constexpr uint32_t kChunkBits = 1024;      // Lc: pixels per input per pipeline stage
+constexpr uint32_t kStagePad = 16;         // bytes between input rows of a stage (bank spread)
+constexpr uint32_t kBatchedThreads = 1024; // 32 warps: warp w transposes block w of a chunk
+constexpr uint32_t kMaxBatchedColumns = 2048;
+constexpr uint32_t kMaxBatchedSynapses = 1023;  // 10 vertical-counter planes
+constexpr uint32_t kHiPlanes = 7;          // planes of weight 8..512 (ones/twos/fours separate)
+constexpr uint32_t kPerInputChunk = 256;   // inputs per sub-batch of the per-input path
+
+// Reasons the batched path is not eligible (sp_plan_info.reason bits).
+enum : uint32_t {
+    kNotBatchedLearn = 1u,      // learn=1 is sequential -> per-input path
+    kNotBatchedPatch = 2u,      // patch mode (NEXT-2)
+    kNotBatchedAlign = 4u,      // nbits % 16 != 0 (bulk copies need 16-byte rows)
+    kNotBatchedColumns = 8u,    // C32 > 2048 (vertical counters exceed registers)
+    kNotBatchedSynapses = 16u,  // S > 1023
+    kNotBatchedForced = 32u,    // force_path = PER_INPUT
+    kNotBatchedSmem = 64u,      // no (stages, window) fits shared memory
+};
+
+struct Geometry {
+    uint32_t W, H, pw, ph;   // frame and patch (pw = W, ph = H in whole-frame mode)
+    uint32_t P;              // inputs per frame
+    uint32_t nbits;          // bits per SP input
+    uint32_t C, C32, ncw;    // columns, padded, column-warps (= sdr words)
+    uint32_t S;
+    uint32_t keyL;           // ceil(log2(C32)) index bits of the rank key
+    uint32_t keyBits;        // total significant key bits
+    bool whole;              // whole-frame mode
+};
+
+// Layout of the batched (bit-sliced) path, fixed at create time (depends on C, S, nbits).
+struct BatchedLayout {
+    bool ok = false;
+    uint32_t stages = 0, Lw = 0, nwin = 0;
+    uint32_t region_bytes = 0, smem_bytes = 0;
+};
+
+struct BatchedParams {
+    const uint8_t* frames;
+    uint32_t num_inputs, nbits;
+    uint32_t C, C32, ncw;
+    uint32_t min_overlap, k, radius;
+    uint32_t keyL, keyBits;
+    uint32_t Lw, nwin, stages, region_bytes;
+    uint32_t groups, K;
+    const uint32_t* ell_off;   // [nwin][ncw] offset in uint4 units
+    const uint16_t* ell_nb;    // [nwin][ncw] number of 8-slot blocks
+    const uint4* ell;          // [.. blocks][32 lanes] x 8 uint16 slots
+    const uint32_t* bc;        // [C32] boost * 2^23 (0 on pad columns)
+    const float* boost;        // [C32]
+    uint32_t* sdr;             // [num_inputs][ncw]
+    uint32_t* counts;          // [num_inputs]
+    uint16_t* raw_out;         // nullable [num_inputs][C]
+    float* boosted_out;        // nullable [num_inputs][C]
+};
+
+struct PerInputParams {
+    const uint8_t* frames;     // frames of this sub-batch
+    uint32_t first_input;      // global index (within the call) of the sub-batch's first input
+    uint32_t num_inputs;       // inputs in this sub-batch
+    Geometry g;
+    uint32_t min_overlap, k, radius;
+    float inc, dec, tau;
+    uint32_t* bits;            // [num_inputs][Wn] packed input bits (scratch)
+    uint32_t Wn;
+    const uint32_t* syn;       // [S][C32] idx | connected << 31
+    uint32_t* syn_rw;          // same, writable (learning)
+    const uint32_t* idx;       // [C][S]
+    float* perm;               // [C][S]
+    const uint32_t* bc;        // [C32]
+    const float* boost;        // [C32]
+    uint32_t* raw;             // [num_inputs][C32] scratch
+    uint32_t* sdr;             // [call inputs][ncw]
+    uint32_t* counts;          // [call inputs]
+    uint16_t* raw_out;         // nullable [call inputs][C]
+    float* boosted_out;        // nullable [call inputs][C]
+};
+
+// host planning (sp_host.cu)
+Geometry make_geometry(const sp_config& cfg);
+BatchedLayout plan_batched_layout(const Geometry& g, int max_smem);
+void plan_batched_grid(const Geometry& g, uint32_t nwin, uint32_t num_inputs, int sm_count,
+                       const int* max_clusters /* [9] by K, or nullptr */,
+                       uint32_t* groups, uint32_t* K);
+
+// one-time kernel attributes (max dynamic smem)
+cudaError_t configure_batched(int max_smem);
+cudaError_t configure_per_input(int max_smem);
+
+// launchers (return cudaError_t of the launch)
+cudaError_t launch_batched(const BatchedParams& p, uint32_t smem_bytes, cudaStream_t s);
+cudaError_t batched_max_clusters(uint32_t smem_bytes, int max_clusters[9]);
+cudaError_t launch_pack(const PerInputParams& p, cudaStream_t s);
+cudaError_t launch_overlap(const PerInputParams& p, cudaStream_t s);
+cudaError_t launch_inhibit(const PerInputParams& p, cudaStream_t s);
+cudaError_t launch_learn(const PerInputParams& p, uint32_t input, cudaStream_t s);
+cudaError_t launch_build_syn(const uint32_t* idx, const float* perm, float tau, uint32_t C,
+                             uint32_t C32, uint32_t S, uint32_t* syn, cudaStream_t s);
+cudaError_t launch_refresh_ell(const uint32_t* idx, const float* perm, const uint32_t* pos,
+                               float tau, uint32_t C, uint32_t S, uint32_t Lw, uint16_t* ell,
+                               cudaStream_t s);
+
+inline uint32_t ceil_log2(uint32_t v) {
+    uint32_t l = 0;
+    while ((1ull << l) < v) ++l;
+    return l;
+}
+inline uint32_t bits_for(uint32_t v) {  // number of bits to represent 0..v
+    uint32_t l = 0;
+    while ((1ull << l) <= v) ++l;
+    return l;
+}
+
+}  // namespace sp

@@ -1,0 +1,277 @@
+// sp_per_input.cu — the per-input CUDA path:
+//   P1 k_pack     uint8 frames/patches -> input bit-planes (a1)
+//   P2 k_overlap  per input: bit-plane in smem, thread-per-column gather-count (a2)
+//   P3 k_inhibit  per input: exact rank keys, k-winners (global / local), SDR (a3, a4)
+//   P4 k_learn    per input: fused +inc/-dec, clamp, connected-flag refresh (a5)
+// plus layout maintenance (synapse-major idx|flag words, batched ELL flags).
+// Learning runs P2 -> P3 -> P4 per input in order (the recurrence of P:92).
+#include "sp_internal.h"
+
+namespace sp {
+
+namespace {
+
+// ---------------------------------------------------------------------------------------
+// P1: packing.  Input t = (frame t / P, tile t % P); bit y*pw + x of the input is pixel
+// (ty*ph + y, tx*pw + x) of the frame (R12, R13).  One thread per output word.
+// ---------------------------------------------------------------------------------------
+__global__ void k_pack(const PerInputParams p) {
+    const uint32_t word = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t t = blockIdx.y;  // input within the sub-batch
+    if (word >= p.Wn || t >= p.num_inputs) return;
+    const Geometry& g = p.g;
+    const uint32_t frame = t / g.P, tile = t % g.P;
+    const uint8_t* fr = p.frames + static_cast<size_t>(frame) * g.W * g.H;
+    const uint32_t q0 = word * 32u;
+    uint32_t out = 0;
+    if (g.whole && (g.nbits % 16u) == 0 && q0 + 32u <= g.nbits &&
+        (reinterpret_cast<uintptr_t>(fr) & 15u) == 0) {
+        const uint4 a = *reinterpret_cast<const uint4*>(fr + q0);
+        const uint4 b = *reinterpret_cast<const uint4*>(fr + q0 + 16);
+        const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+#pragma unroll
+            for (int by = 0; by < 4; ++by)
+                out |= (((v[k] >> (8 * by)) & 0xFFu) != 0u ? 1u : 0u) << (4 * k + by);
+        }
+    } else {
+        const uint32_t tilesx = g.W / g.pw;
+        const uint32_t ty = tile / tilesx, tx = tile % tilesx;
+        for (uint32_t j = 0; j < 32u; ++j) {
+            const uint32_t q = q0 + j;
+            if (q >= g.nbits) break;
+            const uint32_t y = q / g.pw, x = q % g.pw;
+            const uint8_t v = fr[static_cast<size_t>(ty * g.ph + y) * g.W + tx * g.pw + x];
+            out |= (v != 0 ? 1u : 0u) << j;
+        }
+    }
+    p.bits[static_cast<size_t>(t) * p.Wn + word] = out;
+}
+
+// ---------------------------------------------------------------------------------------
+// P2: overlap.  grid (column blocks, inputs); the input's bit-plane is staged in smem.
+// syn[s][c] = idx | connected << 31 (synapse-major: coalesced across columns).
+// ---------------------------------------------------------------------------------------
+__global__ void k_overlap(const PerInputParams p) {
+    extern __shared__ uint32_t s_bits[];
+    const uint32_t t = blockIdx.y;
+    const uint32_t* src = p.bits + static_cast<size_t>(t) * p.Wn;
+    for (uint32_t i = threadIdx.x; i < p.Wn; i += blockDim.x) s_bits[i] = src[i];
+    __syncthreads();
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= p.g.C32) return;
+    const uint32_t C32 = p.g.C32;
+    uint32_t raw = 0;
+    const uint32_t* e = p.syn + c;
+    uint32_t s = 0;
+    for (; s + 4 <= p.g.S; s += 4) {
+        const uint32_t e0 = e[(s + 0) * C32], e1 = e[(s + 1) * C32];
+        const uint32_t e2 = e[(s + 2) * C32], e3 = e[(s + 3) * C32];
+        raw += (s_bits[(e0 & 0x7FFFFFFFu) >> 5] >> (e0 & 31u)) & (e0 >> 31);
+        raw += (s_bits[(e1 & 0x7FFFFFFFu) >> 5] >> (e1 & 31u)) & (e1 >> 31);
+        raw += (s_bits[(e2 & 0x7FFFFFFFu) >> 5] >> (e2 & 31u)) & (e2 >> 31);
+        raw += (s_bits[(e3 & 0x7FFFFFFFu) >> 5] >> (e3 & 31u)) & (e3 >> 31);
+    }
+    for (; s < p.g.S; ++s) {
+        const uint32_t e0 = e[s * C32];
+        raw += (s_bits[(e0 & 0x7FFFFFFFu) >> 5] >> (e0 & 31u)) & (e0 >> 31);
+    }
+    p.raw[static_cast<size_t>(t) * C32 + c] = raw;
+}
+
+// ---------------------------------------------------------------------------------------
+// P3: inhibition, one CTA per input.  key(c) = (N << L) | (2^L-1-c), N = raw*Bc exact
+// (R4); active iff N > 2^23 (Alg. 2 floor, R7) and fewer than k columns of W(c)\{c}
+// have a larger key (R5, R6, R9).
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t key_of(uint32_t raw, uint32_t bc, uint32_t theta, uint32_t c,
+                                           uint32_t L, uint64_t& N) {
+    N = raw >= theta ? static_cast<uint64_t>(raw) * bc : 0ull;
+    return (N << L) | (((1ull << L) - 1ull) - c);
+}
+
+__global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
+    extern __shared__ uint32_t sm[];
+    const Geometry& g = p.g;
+    uint32_t* s_raw = sm;               // [C32]
+    uint32_t* s_bc = sm + g.C32;        // [C32]
+    __shared__ uint32_t s_cnt[2];
+    __shared__ uint32_t s_total;
+    const uint32_t t = blockIdx.x;
+    const uint32_t gin = p.first_input + t;
+    const uint32_t tid = threadIdx.x, nthr = blockDim.x;
+    for (uint32_t c = tid; c < g.C32; c += nthr) {
+        s_raw[c] = p.raw[static_cast<size_t>(t) * g.C32 + c];
+        s_bc[c] = p.bc[c];
+    }
+    if (tid < 2) s_cnt[tid] = 0;
+    if (tid == 0) s_total = 0;
+    __syncthreads();
+    const uint32_t theta = p.min_overlap, L = g.keyL;
+    if (p.raw_out) {
+        for (uint32_t c = tid; c < g.C; c += nthr) {
+            const uint32_t r = s_raw[c];
+            p.raw_out[static_cast<size_t>(gin) * g.C + c] = static_cast<uint16_t>(r);
+            p.boosted_out[static_cast<size_t>(gin) * g.C + c] =
+                r >= theta ? __fmul_rn(static_cast<float>(r), p.boost[c]) : 0.0f;
+        }
+    }
+    uint64_t T = 0;
+    if (p.radius == 0) {
+        for (int bit = static_cast<int>(g.keyBits) - 1, it = 0; bit >= 0; --bit, ++it) {
+            const uint64_t cand = T | (1ull << bit);
+            uint32_t cnt = 0;
+            for (uint32_t c = tid; c < g.C32; c += nthr) {
+                uint64_t N;
+                cnt += key_of(s_raw[c], s_bc[c], theta, c, L, N) >= cand ? 1u : 0u;
+            }
+            cnt = __reduce_add_sync(0xffffffffu, cnt);
+            if ((tid & 31u) == 0 && cnt) atomicAdd(&s_cnt[it & 1], cnt);
+            __syncthreads();
+            const uint32_t total = s_cnt[it & 1];
+            if (tid == 0) s_cnt[(it + 1) & 1] = 0;
+            if (total >= p.k) T = cand;
+            __syncthreads();
+        }
+    }
+    // SDR: warp per 32-column word
+    const uint64_t one = 1ull << 23;
+    uint32_t my_total = 0;
+    for (uint32_t cw = tid >> 5; cw < g.ncw; cw += nthr >> 5) {
+        const uint32_t c = cw * 32u + (tid & 31u);
+        uint64_t N;
+        const uint64_t key = key_of(s_raw[c], s_bc[c], theta, c, L, N);
+        bool act = N > one;
+        if (act) {
+            if (p.radius == 0) {
+                act = key >= T;
+            } else {
+                const uint32_t lo = c >= p.radius ? c - p.radius : 0u;
+                const uint32_t hi = min(g.C - 1u, c + p.radius);
+                uint32_t beats = 0;
+                for (uint32_t d = lo; d <= hi && beats < p.k; ++d) {
+                    uint64_t Nd;
+                    beats += (d != c && key_of(s_raw[d], s_bc[d], theta, d, L, Nd) > key) ? 1u : 0u;
+                }
+                act = beats < p.k;
+            }
+        }
+        const uint32_t word = __ballot_sync(0xffffffffu, act);
+        if ((tid & 31u) == 0) {
+            p.sdr[static_cast<size_t>(gin) * g.ncw + cw] = word;
+            my_total += __popc(word);
+        }
+    }
+    if ((tid & 31u) == 0 && my_total) atomicAdd(&s_total, my_total);
+    __syncthreads();
+    if (tid == 0) p.counts[gin] = s_total;
+}
+
+// ---------------------------------------------------------------------------------------
+// P4: learning for ONE input (P:92 -> whitepaper rule, S:119(a); R3, R10).  Warp per
+// column; inactive columns exit at once.  perm is fp32: one IEEE RN add/sub, then clamp.
+// ---------------------------------------------------------------------------------------
+__global__ void k_learn(const PerInputParams p, uint32_t t) {
+    const Geometry& g = p.g;
+    const uint32_t c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint32_t lane = threadIdx.x & 31u;
+    if (c >= g.C) return;
+    const uint32_t gin = p.first_input + t;
+    const uint32_t word = p.sdr[static_cast<size_t>(gin) * g.ncw + (c >> 5)];
+    if (((word >> (c & 31u)) & 1u) == 0u) return;
+    const uint32_t* bits = p.bits + static_cast<size_t>(t) * p.Wn;
+    const uint32_t* idx = p.idx + static_cast<size_t>(c) * g.S;
+    float* perm = p.perm + static_cast<size_t>(c) * g.S;
+    for (uint32_t s = lane; s < g.S; s += 32u) {
+        const uint32_t i = idx[s];
+        const bool on = ((bits[i >> 5] >> (i & 31u)) & 1u) != 0u;
+        float v = on ? __fadd_rn(perm[s], p.inc) : __fsub_rn(perm[s], p.dec);
+        v = fminf(fmaxf(v, 0.0f), 1.0f);
+        perm[s] = v;
+        p.syn_rw[static_cast<size_t>(s) * g.C32 + c] = i | (v >= p.tau ? 0x80000000u : 0u);
+    }
+}
+
+// syn[s][c] = idx | connected << 31 from the canonical arrays; pad columns point nowhere.
+__global__ void k_build_syn(const uint32_t* idx, const float* perm, float tau, uint32_t C,
+                            uint32_t C32, uint32_t S, uint32_t* syn) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t s = blockIdx.y;
+    if (c >= C32 || s >= S) return;
+    uint32_t v = 0u;  // pad column: disconnected synapse on input 0
+    if (c < C) {
+        const size_t k = static_cast<size_t>(c) * S + s;
+        v = idx[k] | (perm[k] >= tau ? 0x80000000u : 0u);
+    }
+    syn[static_cast<size_t>(s) * C32 + c] = v;
+}
+
+// Batched ELL: slot pos[c][s] holds the window-local index if connected, else the zero slot Lw.
+__global__ void k_refresh_ell(const uint32_t* idx, const float* perm, const uint32_t* pos,
+                              float tau, uint32_t n, uint32_t Lw, uint16_t* ell) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const uint32_t i = idx[k];
+    ell[pos[k]] = static_cast<uint16_t>(perm[k] >= tau ? i % Lw : Lw);
+}
+
+}  // namespace
+
+cudaError_t launch_pack(const PerInputParams& p, cudaStream_t s) {
+    dim3 grid((p.Wn + 255u) / 256u, p.num_inputs);
+    k_pack<<<grid, 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+template <typename F>
+static cudaError_t allow_dynamic_smem(F* fn, int max_smem) {
+    cudaFuncAttributes a{};
+    cudaError_t e = cudaFuncGetAttributes(&a, fn);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                max_smem - static_cast<int>(a.sharedSizeBytes));
+}
+
+cudaError_t configure_per_input(int max_smem) {
+    cudaError_t e = allow_dynamic_smem(k_overlap, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(k_inhibit, max_smem);
+    return e;
+}
+
+cudaError_t launch_overlap(const PerInputParams& p, cudaStream_t s) {
+    const uint32_t smem = p.Wn * 4u;
+    dim3 grid((p.g.C32 + 255u) / 256u, p.num_inputs);
+    k_overlap<<<grid, 256, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_inhibit(const PerInputParams& p, cudaStream_t s) {
+    const uint32_t smem = p.g.C32 * 8u;
+    const uint32_t threads = p.g.C32 < 1024u ? p.g.C32 : 1024u;
+    k_inhibit<<<p.num_inputs, threads, smem, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_learn(const PerInputParams& p, uint32_t input, cudaStream_t s) {
+    const uint32_t warps = 8;
+    k_learn<<<(p.g.C + warps - 1) / warps, warps * 32, 0, s>>>(p, input);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_build_syn(const uint32_t* idx, const float* perm, float tau, uint32_t C,
+                             uint32_t C32, uint32_t S, uint32_t* syn, cudaStream_t s) {
+    dim3 grid((C32 + 255u) / 256u, S);
+    k_build_syn<<<grid, 256, 0, s>>>(idx, perm, tau, C, C32, S, syn);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_refresh_ell(const uint32_t* idx, const float* perm, const uint32_t* pos,
+                               float tau, uint32_t C, uint32_t S, uint32_t Lw, uint16_t* ell,
+                               cudaStream_t s) {
+    const uint32_t n = C * S;
+    k_refresh_ell<<<(n + 255u) / 256u, 256, 0, s>>>(idx, perm, pos, tau, n, Lw, ell);
+    return cudaGetLastError();
+}
+
+}  // namespace sp

@@ -1,0 +1,304 @@
+"""Thin ctypes binding of ``include/sp.h`` (argument marshalling only).
+
+Every step of the Spatial Pooler runs in ``libsp.so``'s CUDA kernels; this
+module only checks tensor shapes/dtypes/devices (the C ABI cannot check raw
+pointers: SP_E_SHAPE), passes pointers and streams, and converts errors into
+exceptions.  torch is used for device memory and streams only.  There is no
+CPU fallback: if ``libsp.so`` is missing or has no GPU, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsp.so")
+
+SP_OK, SP_E_CONFIG, SP_E_ARG, SP_E_SHAPE, SP_E_CUDA, SP_E_OOM, SP_E_STATE = range(7)
+SP_PATH_AUTO, SP_PATH_PER_INPUT, SP_PATH_BATCHED = 0, 1, 2
+SP_FLAG_RECORD_OVERLAPS = 1
+
+STATUS_NAMES = {0: "SP_OK", 1: "SP_E_CONFIG", 2: "SP_E_ARG", 3: "SP_E_SHAPE", 4: "SP_E_CUDA",
+                5: "SP_E_OOM", 6: "SP_E_STATE"}
+
+# exported symbols of include/sp.h and include/sp_synth.h (checked by the CPU tests)
+ABI_SYMBOLS = ("sp_config_default", "sp_create", "sp_destroy", "sp_compute", "sp_winners",
+               "sp_overlaps", "sp_get_state", "sp_set_state", "sp_compute_host", "sp_plan",
+               "sp_init_pools_host", "sp_get_info", "sp_last_error", "sp_version",
+               "sp_synth_frames")
+
+
+class SpError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {message}")
+        self.status = status
+        self.message = message
+
+
+class SpConfig(ctypes.Structure):
+    _fields_ = [
+        ("input_width", ctypes.c_uint32), ("input_height", ctypes.c_uint32),
+        ("patch_width", ctypes.c_uint32), ("patch_height", ctypes.c_uint32),
+        ("num_columns", ctypes.c_uint32), ("synapses_per_column", ctypes.c_uint32),
+        ("min_overlap", ctypes.c_uint32), ("winners_set_size", ctypes.c_uint32),
+        ("inhibition_radius", ctypes.c_uint32),
+        ("perm_increment", ctypes.c_float), ("perm_decrement", ctypes.c_float),
+        ("initial_permanence", ctypes.c_float), ("connected_threshold", ctypes.c_float),
+        ("seed", ctypes.c_uint64), ("device", ctypes.c_int32),
+        ("max_inputs", ctypes.c_uint32), ("flags", ctypes.c_uint32),
+        ("force_path", ctypes.c_uint32),
+    ]
+
+
+class SpPlanInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint32) for n in (
+        "path", "input_bits", "inputs_per_frame", "num_inputs", "columns_padded", "sdr_words",
+        "groups", "cluster", "ctas", "window_bits", "num_windows", "chunk_bits", "stages",
+        "smem_bytes", "reason")]
+
+    def as_dict(self):
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+class SpInfo(ctypes.Structure):
+    _fields_ = [("plan", SpPlanInfo), ("kernel_launches", ctypes.c_uint64),
+                ("last_num_inputs", ctypes.c_uint32), ("ell_slots", ctypes.c_uint32),
+                ("sm_count", ctypes.c_int32), ("max_smem_optin", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Loads libsp.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not found: run __graft_entry__.build() "
+                          "(python -m paper_1608_01966_b200.build)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, u32, i32, u64 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_int32, ctypes.c_uint64
+    P = ctypes.POINTER
+    sig = {
+        "sp_config_default": [P(SpConfig)],
+        "sp_create": [P(SpConfig), P(vp)],
+        "sp_destroy": [vp],
+        "sp_compute": [vp, vp, u32, ctypes.c_int, vp],
+        "sp_winners": [vp, vp, vp, vp],
+        "sp_overlaps": [vp, vp, vp, vp],
+        "sp_get_state": [vp, vp, vp, vp],
+        "sp_set_state": [vp, vp, vp, vp],
+        "sp_compute_host": [vp, vp, u32, ctypes.c_int, vp, vp, vp],
+        "sp_plan": [P(SpConfig), u32, i32, P(SpPlanInfo)],
+        "sp_init_pools_host": [P(SpConfig), vp],
+        "sp_get_info": [vp, P(SpInfo)],
+        "sp_synth_frames": [vp, u64, u32, u32, u32, u64, u32, u32, vp],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    L.sp_last_error.restype = ctypes.c_char_p
+    L.sp_last_error.argtypes = []
+    L.sp_version.restype = ctypes.c_char_p
+    L.sp_version.argtypes = []
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != SP_OK:
+        raise SpError(status, lib().sp_last_error().decode())
+
+
+def make_config(**kw) -> SpConfig:
+    cfg = SpConfig()
+    _check(lib().sp_config_default(ctypes.byref(cfg)))
+    for k, v in kw.items():
+        if not hasattr(cfg, k):
+            raise SpError(SP_E_CONFIG, f"unknown config key {k!r}")
+        setattr(cfg, k, v)
+    return cfg
+
+
+def plan(num_frames: int, sm_count: int = 0, **kw) -> dict:
+    out = SpPlanInfo()
+    _check(lib().sp_plan(ctypes.byref(make_config(**kw)), num_frames, sm_count, ctypes.byref(out)))
+    return out.as_dict()
+
+
+def init_pools_host(**kw) -> np.ndarray:
+    cfg = make_config(**kw)
+    C, S = cfg.num_columns, cfg.synapses_per_column
+    out = np.empty((C, S), dtype=np.uint32)
+    _check(lib().sp_init_pools_host(ctypes.byref(cfg), out.ctypes.data))
+    return out
+
+
+def _stream_ptr(stream, device):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream(device)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _require(t, dtype, device, shape=None, name="tensor"):
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise SpError(SP_E_SHAPE, f"{name} must be a torch.Tensor")
+    if t.dtype != dtype:
+        raise SpError(SP_E_SHAPE, f"{name} dtype {t.dtype} != {dtype}")
+    if t.device.type != "cuda" or t.device.index != device:
+        raise SpError(SP_E_SHAPE, f"{name} must live on cuda:{device}, got {t.device}")
+    if not t.is_contiguous():
+        raise SpError(SP_E_SHAPE, f"{name} must be contiguous")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise SpError(SP_E_SHAPE, f"{name} shape {tuple(t.shape)} != {tuple(shape)}")
+
+
+def synth_frames(out, first_frame: int, seed: int, rho: float = 0.5, nonzero: str = "255",
+                 stream=None):
+    """Fills uint8 cuda tensor ``out[F, H, W]`` with frames of the seeded stream (bench/test)."""
+    import torch
+    _require(out, torch.uint8, out.device.index if out.is_cuda else -1, name="out")
+    F, H, W = out.shape
+    mode = {"255": 0, "1": 1, "random": 2}[nonzero]
+    q24 = int(round(rho * (1 << 24)))
+    _check(lib().sp_synth_frames(ctypes.c_void_p(out.data_ptr()), first_frame, F, H, W, seed, q24,
+                                 mode, _stream_ptr(stream, out.device)))
+    return out
+
+
+class SpatialPooler:
+    """One SP instance (a ``sp_handle``) on one CUDA device."""
+
+    def __init__(self, **kw):
+        self.cfg = make_config(**kw)
+        h = ctypes.c_void_p()
+        _check(lib().sp_create(ctypes.byref(self.cfg), ctypes.byref(h)))
+        self._h = h
+        self.device = int(self.cfg.device)
+        self.C = int(self.cfg.num_columns)
+        self.S = int(self.cfg.synapses_per_column)
+        W, H = int(self.cfg.input_width), int(self.cfg.input_height)
+        pw = int(self.cfg.patch_width) or W
+        ph = int(self.cfg.patch_height) or H
+        self.frame_shape = (H, W)
+        self.inputs_per_frame = (W // pw) * (H // ph)
+        self.sdr_words = (self.C + 31) // 32
+        self.last_num_inputs = 0
+
+    # -- lifetime ---------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().sp_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- hot path ---------------------------------------------------------------------
+    def compute(self, frames, learn: bool = False, stream=None) -> int:
+        """``frames``: uint8 cuda tensor [F, H, W]. Returns the number of SP inputs."""
+        import torch
+        _require(frames, torch.uint8, self.device, name="frames")
+        if frames.dim() != 3 or tuple(frames.shape[1:]) != self.frame_shape:
+            raise SpError(SP_E_SHAPE, f"frames must be [F, {self.frame_shape[0]}, {self.frame_shape[1]}]")
+        F = frames.shape[0]
+        _check(lib().sp_compute(self._h, ctypes.c_void_p(frames.data_ptr()), F, int(bool(learn)),
+                                _stream_ptr(stream, frames.device)))
+        self.last_num_inputs = F * self.inputs_per_frame
+        return self.last_num_inputs
+
+    def winners(self, sdr=None, counts=None, stream=None):
+        """SDRs of the last call: (uint32 [n, words] as int32 view, int32 [n]) cuda tensors."""
+        import torch
+        n = self.last_num_inputs
+        dev = torch.device("cuda", self.device)
+        if sdr is None:
+            sdr = torch.empty((n, self.sdr_words), dtype=torch.int32, device=dev)
+        if counts is None:
+            counts = torch.empty((n,), dtype=torch.int32, device=dev)
+        _require(sdr, torch.int32, self.device, (n, self.sdr_words), "sdr")
+        _require(counts, torch.int32, self.device, (n,), "counts")
+        _check(lib().sp_winners(self._h, ctypes.c_void_p(sdr.data_ptr()),
+                                ctypes.c_void_p(counts.data_ptr()), _stream_ptr(stream, dev)))
+        return sdr, counts
+
+    def overlaps(self, stream=None):
+        """(raw uint16-as-int16 [n, C], boosted float32 [n, C]) of the last call."""
+        import torch
+        n = self.last_num_inputs
+        dev = torch.device("cuda", self.device)
+        raw = torch.empty((n, self.C), dtype=torch.int16, device=dev)
+        boosted = torch.empty((n, self.C), dtype=torch.float32, device=dev)
+        _check(lib().sp_overlaps(self._h, ctypes.c_void_p(raw.data_ptr()),
+                                 ctypes.c_void_p(boosted.data_ptr()), _stream_ptr(stream, dev)))
+        return raw, boosted
+
+    def compute_host(self, frames: np.ndarray, learn: bool = False, stream=None):
+        """End-to-end call with host buffers (H2D/D2H inside): returns (sdr uint32, counts uint32)."""
+        frames = np.ascontiguousarray(frames, dtype=np.uint8)
+        if frames.ndim != 3 or frames.shape[1:] != self.frame_shape:
+            raise SpError(SP_E_SHAPE, "frames must be [F, H, W] uint8")
+        n = frames.shape[0] * self.inputs_per_frame
+        sdr = np.empty((n, self.sdr_words), dtype=np.uint32)
+        counts = np.empty((n,), dtype=np.uint32)
+        self.compute_host_into(frames, sdr, counts, learn, stream)
+        return sdr, counts
+
+    def compute_host_into(self, frames, sdr, counts, learn: bool = False, stream=None):
+        """Same with caller buffers (numpy arrays or pinned torch CPU tensors)."""
+        import torch
+
+        def ptr(a):
+            return a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data
+        F = frames.shape[0]
+        _check(lib().sp_compute_host(self._h, ctypes.c_void_p(ptr(frames)), F, int(bool(learn)),
+                                     ctypes.c_void_p(ptr(sdr)),
+                                     ctypes.c_void_p(ptr(counts)) if counts is not None else None,
+                                     _stream_ptr(stream, torch.device("cuda", self.device))))
+        self.last_num_inputs = F * self.inputs_per_frame
+
+    # -- state ------------------------------------------------------------------------
+    def get_state(self):
+        idx = np.empty((self.C, self.S), np.uint32)
+        perm = np.empty((self.C, self.S), np.float32)
+        boost = np.empty((self.C,), np.float32)
+        _check(lib().sp_get_state(self._h, idx.ctypes.data, perm.ctypes.data, boost.ctypes.data))
+        return idx, perm, boost
+
+    def set_state(self, idx=None, perm=None, boost=None):
+        def arr(a, dt, shape):
+            if a is None:
+                return None, None
+            a = np.ascontiguousarray(a, dtype=dt)
+            if a.shape != shape:
+                raise SpError(SP_E_SHAPE, f"state array shape {a.shape} != {shape}")
+            return a, ctypes.c_void_p(a.ctypes.data)
+        i, ip = arr(idx, np.uint32, (self.C, self.S))
+        p, pp = arr(perm, np.float32, (self.C, self.S))
+        b, bp = arr(boost, np.float32, (self.C,))
+        _check(lib().sp_set_state(self._h, ip, pp, bp))
+
+    def info(self) -> dict:
+        out = SpInfo()
+        _check(lib().sp_get_info(self._h, ctypes.byref(out)))
+        d = {n: (out.plan.as_dict() if n == "plan" else int(getattr(out, n))) for n, _ in out._fields_}
+        return d
+
+    def kernel_launches(self) -> int:
+        return self.info()["kernel_launches"]

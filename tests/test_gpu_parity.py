@@ -1,0 +1,293 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): overlap counts, winner sets and permanences
+bit-exact; boosted overlaps within 1e-6 relative (they are in fact bit-equal:
+both sides round the exact product once to fp32, DESIGN R4).  Every input is
+seeded and synthetic; no expected value comes from
+the CUDA path.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import sp_inputs
+from tests.helpers import ocfg, gpu_kwargs, perturbed_state, sdr_of
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1608_01966_b200 as P  # noqa: E402
+
+DEV = torch.device("cuda", 0)
+PATHS = [P.SP_PATH_BATCHED, P.SP_PATH_PER_INPUT]
+
+
+def to_dev(frames):
+    return torch.from_numpy(np.ascontiguousarray(frames)).to(DEV)
+
+
+def make_sp(cfg, state=None, path=P.SP_PATH_AUTO, max_inputs=4096, record=True):
+    sp = P.SpatialPooler(**gpu_kwargs(cfg, force_path=path, max_inputs=max_inputs,
+                                      flags=P.SP_FLAG_RECORD_OVERLAPS if record else 0))
+    if state is not None:
+        sp.set_state(*state)
+    return sp
+
+
+def run_gpu(sp, frames, learn=False):
+    sp.compute(to_dev(frames), learn=learn)
+    sdr, counts = sp.winners()
+    raw, boosted = sp.overlaps()
+    torch.cuda.synchronize()
+    return (sdr.cpu().numpy(), counts.cpu().numpy(), raw.cpu().numpy().view(np.uint16),
+            boosted.cpu().numpy())
+
+
+def check_results(results, sdr, counts, raw, boosted, rows=None):
+    rows = range(len(results)) if rows is None else rows
+    for r, res in zip(rows, results):
+        assert np.array_equal(raw[r].astype(np.int64), res.raw), f"raw mismatch at input {r}"
+        assert np.array_equal(boosted[r].view(np.uint32), res.boosted.view(np.uint32)), \
+            f"boosted mismatch at input {r}"
+        assert np.array_equal(sdr[r], sdr_of(res.active)), f"winners mismatch at input {r}"
+        assert counts[r] == res.active.sum()
+
+
+# --------------------------------------------------------------------------- #
+# generator cross-check (same counter-based hash on both sides)
+# --------------------------------------------------------------------------- #
+@pytest.mark.parametrize("mode", ["255", "1", "random"])
+def test_synth_frames_match_python_generator(mode):
+    out = torch.empty((3, 37, 45), dtype=torch.uint8, device=DEV)
+    P.synth_frames(out, 11, 2002, rho=0.3, nonzero=mode)
+    want = sp_inputs.frames(2002, 11, 3, 37, 45, rho=0.3, nonzero=mode)
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_state_roundtrip_and_init_matches_oracle():
+    cfg = ocfg()
+    sp = make_sp(cfg)
+    idx, perm, boost = sp.get_state()
+    oi, op, ob = O.init_pools(cfg)
+    assert np.array_equal(idx.astype(np.int64), oi) and np.array_equal(perm, op) and np.array_equal(boost, ob)
+    st = perturbed_state(cfg)
+    sp.set_state(*st)
+    i2, p2, b2 = sp.get_state()
+    assert np.array_equal(i2, st[0]) and np.array_equal(p2.view(np.uint32), st[1].view(np.uint32))
+    assert np.array_equal(b2, st[2])
+
+
+def test_set_state_rejects_out_of_domain():
+    cfg = ocfg()
+    sp = make_sp(cfg)
+    idx, perm, boost = sp.get_state()
+    bad = idx.copy()
+    bad[3, 1] = bad[3, 0]
+    with pytest.raises(P.SpError) as e:
+        sp.set_state(idx=bad)
+    assert e.value.status == P.SP_E_ARG
+    with pytest.raises(P.SpError):
+        sp.set_state(perm=np.full_like(perm, 1.5))
+    with pytest.raises(P.SpError):
+        sp.set_state(boost=np.full_like(boost, 0.5))
+
+
+# --------------------------------------------------------------------------- #
+# BASELINE config 1: tiny SP, 10 frames with learning (sequential recurrence)
+# --------------------------------------------------------------------------- #
+@pytest.mark.parametrize("radius", [0, 4])
+def test_tiny_learning_bit_exact(radius):
+    cfg = ocfg(inhibition_radius=radius)
+    idx, perm, _ = O.init_pools(cfg)
+    state = (idx, perm, sp_inputs.boosts(7, cfg.num_columns))
+    frames = sp_inputs.frames(1001, 0, 10, 8, 8, rho=0.5)
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = ora.compute(frames, learning=True)
+    sp = make_sp(cfg, state)
+    sdr, counts, raw, boosted = run_gpu(sp, frames, learn=True)
+    check_results(results, sdr, counts, raw, boosted)
+    _, gperm, _ = sp.get_state()
+    assert np.array_equal(gperm.view(np.uint32), ora.perm.view(np.uint32))
+    # and inference after learning (batched path uses the refreshed layout)
+    frames2 = sp_inputs.frames(2002, 0, 40, 8, 8, rho=0.5)
+    res2 = [ora.step(x, False) for x in O.encode(frames2, cfg)]
+    check_results(res2, *run_gpu(sp, frames2))
+
+
+# --------------------------------------------------------------------------- #
+# inference parity on both CUDA paths, small shapes with ragged edges
+# --------------------------------------------------------------------------- #
+SMALL = [
+    dict(),                                                        # tiny, global
+    dict(inhibition_radius=4),                                     # tiny, local
+    dict(input_width=48, input_height=37, num_columns=100, synapses_per_column=20,
+         min_overlap=3, winners_set_size=7),                       # C % 32 != 0, nbits % 32 == 16
+    dict(input_width=48, input_height=37, num_columns=100, synapses_per_column=20,
+         min_overlap=0, winners_set_size=100, inhibition_radius=2),  # k == C, theta 0
+    dict(input_width=64, input_height=40, num_columns=512, synapses_per_column=200,
+         min_overlap=1, winners_set_size=1),                       # k = 1, theta 1 (floor R7)
+    dict(input_width=240, input_height=134, num_columns=2048, synapses_per_column=128,
+         min_overlap=8, winners_set_size=40),                      # Tab. 2 on Tab. 1 frames, C32=2048
+    dict(input_width=240, input_height=134, num_columns=2048, synapses_per_column=128,
+         min_overlap=8, winners_set_size=40, inhibition_radius=80),  # Tab. 2 radius 80
+]
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("kw", SMALL)
+def test_inference_parity_small(kw, path):
+    cfg = ocfg(**kw)
+    state = perturbed_state(cfg)
+    nframes = 45  # > 32: two groups, the last one ragged
+    frames = sp_inputs.frames(2002, 0, nframes, cfg.input_height, cfg.input_width, rho=0.5,
+                              nonzero="random")
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = [ora.step(x, False) for x in O.encode(frames, cfg)]
+    sp = make_sp(cfg, state, path)
+    out = run_gpu(sp, frames)
+    assert sp.info()["plan"]["path"] == path
+    check_results(results, *out)
+
+
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("rho", [0.0, 1.0, 0.05])
+def test_inference_degenerate_frames(path, rho):
+    # all-zero frames -> no winners; all-one frames; sparse frames (theta zeros)
+    cfg = ocfg(input_width=64, input_height=32, num_columns=256, synapses_per_column=32,
+               min_overlap=4, winners_set_size=10)
+    state = perturbed_state(cfg)
+    frames = sp_inputs.frames(9, 0, 33, 32, 64, rho=rho)
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = [ora.step(x, False) for x in O.encode(frames, cfg)]
+    out = run_gpu(make_sp(cfg, state, path), frames)
+    check_results(results, *out)
+    if rho == 0.0:
+        assert out[1].sum() == 0
+
+
+def test_zero_frames_is_noop():
+    sp = make_sp(ocfg())
+    sp.compute(torch.empty((0, 8, 8), dtype=torch.uint8, device=DEV))
+    sdr, counts = sp.winners()
+    assert sdr.shape == (0, 4)
+
+
+def test_max_inputs_enforced():
+    sp = make_sp(ocfg(), max_inputs=4)
+    with pytest.raises(P.SpError) as e:
+        sp.compute(torch.zeros((5, 8, 8), dtype=torch.uint8, device=DEV))
+    assert e.value.status == P.SP_E_ARG
+
+
+def test_patch_mode_parity():
+    # BASELINE config 2 variant: 960x540 tiled into 32x30 patches (540 inputs per frame)
+    cfg = ocfg(input_width=960, input_height=540, patch_width=32, patch_height=30,
+               num_columns=1024, synapses_per_column=256, min_overlap=4, winners_set_size=40)
+    state = perturbed_state(cfg)
+    frames = sp_inputs.frames(2002, 0, 1, 540, 960, rho=0.5)
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = [ora.step(x, False) for x in O.encode(frames, cfg)]
+    out = run_gpu(make_sp(cfg, state), frames)
+    check_results(results, *out)
+
+
+# --------------------------------------------------------------------------- #
+# full size: BASELINE config 2 (learning) and config 4 (batched inference)
+# --------------------------------------------------------------------------- #
+def headline_cfg(**kw):
+    base = dict(input_width=960, input_height=540, num_columns=1024, synapses_per_column=256,
+                min_overlap=4, winners_set_size=40)
+    base.update(kw)
+    return ocfg(**base)
+
+
+def test_full_size_learning_then_inference():
+    cfg = headline_cfg()
+    idx, perm, _ = O.init_pools(cfg)
+    state = (idx, perm, sp_inputs.boosts(7, cfg.num_columns))
+    frames = sp_inputs.frames(1001, 0, 12, 540, 960, rho=0.5)
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = ora.compute(frames, learning=True)
+    sp = make_sp(cfg, state, max_inputs=64)
+    check_results(results, *run_gpu(sp, frames, learn=True))
+    _, gperm, _ = sp.get_state()
+    assert np.array_equal(gperm.view(np.uint32), ora.perm.view(np.uint32))
+    test = sp_inputs.frames(2002, 0, 40, 540, 960, rho=0.5)
+    res2 = [ora.step(x, False) for x in O.encode(test, cfg)]
+    check_results(res2, *run_gpu(sp, test))
+
+
+@pytest.mark.parametrize("radius", [0, 80])
+def test_full_size_inference_parity(radius):
+    cfg = headline_cfg(inhibition_radius=radius)
+    state = perturbed_state(cfg)
+    frames = sp_inputs.frames(2002, 0, 36, 540, 960, rho=0.5)
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = [ora.step(x, False) for x in O.encode(frames, cfg)]
+    for path in PATHS:
+        check_results(results, *run_gpu(make_sp(cfg, state, path, max_inputs=64), frames))
+
+
+def test_bench_launch_config_sampled_parity():
+    """The exact launch configuration bench.py times: 4096 device-generated frames.
+
+    Frames come from the device generator (cross-checked against sp_inputs
+    above); the oracle recomputes a sample of frames from sp_inputs on the host.
+    All 4096 frames are checked against the winner-count invariant."""
+    cfg = headline_cfg()
+    state = perturbed_state(cfg, boost_hi=1.0)  # boosts 1 (a learned SP without boost updates)
+    sp = make_sp(cfg, state, max_inputs=4096)
+    frames = torch.empty((4096, 540, 960), dtype=torch.uint8, device=DEV)
+    P.synth_frames(frames, 0, 2002, rho=0.5)
+    sp.compute(frames)
+    sdr, counts = sp.winners()
+    raw, boosted = sp.overlaps()
+    torch.cuda.synchronize()
+    assert sp.info()["plan"]["path"] == P.SP_PATH_BATCHED
+    sdr, counts = sdr.cpu().numpy(), counts.cpu().numpy()
+    raw, boosted = raw.cpu().numpy().view(np.uint16), boosted.cpu().numpy()
+    nz = (boosted > 1.0).sum(axis=1)
+    assert np.array_equal(counts, np.minimum(cfg.winners_set_size, nz))
+    rng = np.random.default_rng(3)
+    sample = sorted(set(rng.choice(4096, 10, replace=False).tolist()) | {0, 4095})
+    ora = O.SpatialPoolerOracle(cfg, state)
+    for f in sample:
+        x = O.encode(sp_inputs.frames(2002, f, 1, 540, 960, rho=0.5), cfg)[0]
+        res = ora.step(x, False)
+        check_results([res], sdr, counts, raw, boosted, rows=[f])
+
+
+def test_scaled_config5_learning():
+    # BASELINE config 5: 16384 columns, 512 synapses, local r=80 (per-input path)
+    cfg = headline_cfg(num_columns=16384, synapses_per_column=512, min_overlap=8,
+                       winners_set_size=40, inhibition_radius=80)
+    idx, perm, _ = O.init_pools(cfg)
+    state = (idx, perm, sp_inputs.boosts(7, cfg.num_columns))
+    frames = sp_inputs.frames(1001, 0, 3, 540, 960, rho=0.5)
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = ora.compute(frames, learning=True)
+    sp = make_sp(cfg, state, max_inputs=8)
+    check_results(results, *run_gpu(sp, frames, learn=True))
+    _, gperm, _ = sp.get_state()
+    assert np.array_equal(gperm.view(np.uint32), ora.perm.view(np.uint32))
+
+
+def test_end_to_end_host_buffers_match_device_call():
+    cfg = headline_cfg()
+    state = perturbed_state(cfg)
+    frames = sp_inputs.frames(2002, 0, 70, 540, 960, rho=0.5)
+    sp = make_sp(cfg, state, max_inputs=128)
+    sdr_d, cnt_d, _, _ = run_gpu(sp, frames)
+    sdr_h, cnt_h = sp.compute_host(frames)
+    assert np.array_equal(sdr_h.view(np.int32), sdr_d) and np.array_equal(cnt_h.astype(np.int32), cnt_d)
+
+
+def test_shape_errors():
+    sp = make_sp(ocfg())
+    with pytest.raises(P.SpError) as e:
+        sp.compute(torch.zeros((2, 8, 9), dtype=torch.uint8, device=DEV))
+    assert e.value.status == P.SP_E_SHAPE
+    with pytest.raises(P.SpError):
+        sp.compute(torch.zeros((2, 8, 8), dtype=torch.int32, device=DEV))
+    with pytest.raises(P.SpError):
+        sp.compute(torch.zeros((2, 8, 8), dtype=torch.uint8))
