@@ -1,0 +1,361 @@
+"""Benchmark of the SP hot path on B200 (the driver's contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU, NCCL)
+
+Workload (BASELINE.json metric, config 4): batch inference of 4096 synthetic
+960x540 binarised frames PER GPU with a learned SP (1024 columns, 256 synapses,
+min_overlap 4, winners_set_size 40, global inhibition).  A step = one pass of
+the hot path over the batch: sp_compute (staging + overlap + boost + k-winners
+in the fused bit-sliced kernel) + sp_winners, and for N > 1 the NCCL
+all-gather of the winner SDRs to every rank (north_star's classifier gather).
+Frames are generated on the device before the timed region (counter-based
+hash by global frame index) and are 2.1 GB per GPU, i.e. larger than L2, so no
+L2 flush is needed.  The learning row (a5) is measured separately on the
+sequential learning stream that produces the learned SP ("learn" object).
+
+Rank 0 prints ONE JSON line.  --impl reference times the CPU oracle (the
+reference arm of this tier) on bounded samples of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SP frames/sec at 960x540, 1024 col/256 syn (1/2/4/8 B200); % HBM peak"
+UNIT = "frames/s"
+H, W, C, S, THETA, K_WIN = 540, 960, 1024, 256, 4, 40
+FRAME_BYTES = H * W
+ALGO_BYTES_PER_FRAME = FRAME_BYTES + C // 8  # uint8 frame in + SDR out
+SEED_STATE, SEED_LEARN, SEED_INFER = 42, 1001, 2002
+WORKLOAD = ("BASELINE config 4: batch inference of synthetic 960x540 binarised frames with a "
+            "learned SP (1024 columns, 256 synapses, min_overlap 4, winners_set_size 40, global)")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--frames", type=int, default=4096, help="frames per GPU (weak) or total (--strong)")
+    ap.add_argument("--strong", action="store_true", help="fixed total batch split over the GPUs")
+    ap.add_argument("--learn-frames", type=int, default=256)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- #
+# clocks during the timed region (B200_PROFILING.md "clocks line")
+# --------------------------------------------------------------------------- #
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+           0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.samples, self.reasons = [], set()
+        self.period = period_s
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - depends on the box
+            self.err = repr(e)
+            self.max_mhz = None
+
+    def _sample(self):
+        nv = self.nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        try:
+            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        for b, name in REASONS.items():
+            if bits & b:
+                self.reasons.add(name)
+
+    def _run(self):
+        while not self._stop.is_set():
+            self._sample()
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+            self._sample()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons - {"gpu_idle"}), "samples": len(self.samples)}
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic_per_frame():
+    """dram read+write bytes per frame of the batched kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_batched_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("dram_bytes_per_frame"), d.get("source")
+    return None, None
+
+
+# --------------------------------------------------------------------------- #
+# CPU oracle (reported baseline / reference arm)
+# --------------------------------------------------------------------------- #
+def oracle_cfg():
+    import oracle as O
+    return O.OracleConfig(input_width=W, input_height=H, num_columns=C, synapses_per_column=S,
+                          min_overlap=THETA, winners_set_size=K_WIN, inhibition_radius=0,
+                          seed=SEED_STATE)
+
+
+def time_oracle(seconds: float, first_frame: int = 0, chunk: int = 4):
+    """Oracle inference on consecutive frames of the inference stream until ~seconds of CPU work."""
+    import oracle as O
+    import sp_inputs
+    ora = O.SpatialPoolerOracle(oracle_cfg())
+    done, busy, f = 0, 0.0, first_frame
+    while busy < seconds or done == 0:
+        frames = sp_inputs.frames(SEED_INFER, f, chunk, H, W, rho=0.5)
+        t0 = time.perf_counter()
+        ora.compute(frames, learning=False)
+        busy += time.perf_counter() - t0
+        done += chunk
+        f += chunk
+    return done, busy
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    per_step = 2  # frames per step: a bounded sample of the workload
+    import oracle as O
+    import sp_inputs
+    ora = O.SpatialPoolerOracle(oracle_cfg())
+    frames = sp_inputs.frames(SEED_INFER, 0, per_step * (args.warmup + args.steps), H, W, rho=0.5)
+    for i in range(args.warmup):
+        ora.compute(frames[i * per_step:(i + 1) * per_step], learning=False)
+    t0 = time.perf_counter()
+    for i in range(args.warmup, args.warmup + args.steps):
+        ora.compute(frames[i * per_step:(i + 1) * per_step], learning=False)
+    el = time.perf_counter() - t0
+    value = per_step * args.steps / el
+    sample = f"{per_step} frames of the config-4 inference stream per step (oracle, NumPy, 1 process)"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int64/f32 (NumPy)", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "frames_per_step": per_step, "host": "cpu"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- #
+# our arm
+# --------------------------------------------------------------------------- #
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_1608_01966_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_1608_01966_b200 import dist as D
+
+    F = args.frames // world if args.strong else args.frames
+    F0 = D.shard_range(args.frames, rank, world)[0] if args.strong else rank * F
+    sp = P.SpatialPooler(input_width=W, input_height=H, num_columns=C, synapses_per_column=S,
+                         min_overlap=THETA, winners_set_size=K_WIN, inhibition_radius=0,
+                         seed=SEED_STATE, device=local, max_inputs=max(F, args.learn_frames))
+    stream = torch.cuda.current_stream(dev)
+
+    # ---- a5: learning stream on rank 0 -> learned SP, broadcast to all ranks --------------
+    learn = None
+    if rank == 0 and args.learn_frames > 0:
+        lf = torch.empty((args.learn_frames, H, W), dtype=torch.uint8, device=dev)
+        P.synth_frames(lf, 0, SEED_LEARN, 0.5)
+        sp.compute(lf[:4], learn=True)  # first 4 frames of the stream also warm the kernels up
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = sp.kernel_launches()
+        e0.record(stream)
+        sp.compute(lf[4:], learn=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        nl = args.learn_frames - 4
+        learn = {"frames": nl, "ms": ms, "us_per_frame": ms * 1e3 / nl, "frames_per_s": nl / ms * 1e3,
+                 "kernel_launches": sp.kernel_launches() - l0,
+                 "workload": "BASELINE config 2 learning stream (sequential), whole 960x540 frames"}
+        del lf
+    if world > 1:
+        D.broadcast_state(sp, src=0, device=dev)
+
+    # ---- inference frames of this rank (generated before the timed region) --------------
+    frames = torch.empty((F, H, W), dtype=torch.uint8, device=dev)
+    P.synth_frames(frames, F0, SEED_INFER, 0.5)
+    words = sp.sdr_words
+    sdr = torch.empty((F, words), dtype=torch.int32, device=dev)
+    counts = torch.empty((F,), dtype=torch.int32, device=dev)
+    gathered = torch.empty((F * world, words), dtype=torch.int32, device=dev) if world > 1 else None
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        sp.compute(frames, learn=False)
+        if ev is not None:
+            ev[1].record(stream)
+        sp.winners(sdr, counts)
+        if world > 1:
+            D.gather_sdrs(sdr, gathered)
+
+    warmup = max(args.warmup, 3)  # timing rule: W >= 3
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = sp.kernel_launches()
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for i in range(args.steps):
+            step(kev[i])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    launches = sp.kernel_launches() - launches0
+    if world > 1:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_end)
+    kernel_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
+    if world > 1:
+        t = torch.tensor([ms, kernel_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, kernel_ms = float(t[0]), float(t[1])
+    total_frames = F * world * args.steps
+    value = total_frames / (ms / 1e3)
+    plan = sp.info()["plan"]
+
+    # ---- e2e: the public host-buffer call (H2D of frames + D2H of SDRs inside) -----------
+    e2e = None
+    if not args.no_e2e:
+        host_frames = torch.empty((F, H, W), dtype=torch.uint8, pin_memory=True)
+        host_frames.copy_(frames)
+        host_sdr = torch.empty((F, words), dtype=torch.int32, pin_memory=True)
+        host_cnt = torch.empty((F,), dtype=torch.int32, pin_memory=True)
+        sp.compute_host_into(host_frames, host_sdr, host_cnt)  # warm-up (allocates staging)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            sp.compute_host_into(host_frames, host_sdr, host_cnt)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ems = a.elapsed_time(b)
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t[0])
+        e2e = {"value": F * world * args.e2e_steps / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": F * FRAME_BYTES, "d2h_bytes_per_step": F * (words * 4 + 4),
+               "steps": args.e2e_steps, "api": "sp_compute_host (pinned host frames)"}
+        del host_frames
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    peak, peak_src = measured_peak_hbm()
+    achieved = F * ALGO_BYTES_PER_FRAME / (kernel_ms / 1e3) / 1e9
+    traffic_pf, traffic_src = ncu_traffic_per_frame()
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4),
+                "traffic": (traffic_pf * F if traffic_pf else None),
+                "kernel": "sp_batched_kernel", "kernel_ms": kernel_ms,
+                "algorithmic_bytes_per_launch": F * ALGO_BYTES_PER_FRAME,
+                "peak_source": peak_src, "traffic_source": traffic_src}
+
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        done, busy = time_oracle(args.cpu_seconds)
+        cpu = {"value": done / busy, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{done} frames of the config-4 inference stream (NumPy oracle, 1 process, "
+                         f"untrained SP from the oracle's own init), {busy:.1f} s"}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if args.strong else "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (counter-hash binarised frames, generated on device)",
+            "config": {"workload": WORKLOAD, "frames_per_gpu": F, "global_batch": F * world,
+                       "frame": f"{W}x{H}", "columns": C, "synapses": S, "min_overlap": THETA,
+                       "winners_set_size": K_WIN, "inhibition": "global",
+                       "parallelism": f"dp{world} (frame shards; NCCL all-gather of SDRs)",
+                       "l2": "inputs larger than L2 (2.1 GB per GPU per step); no flush",
+                       "plan": {k: plan[k] for k in ("groups", "cluster", "ctas", "window_bits",
+                                                     "num_windows", "stages", "smem_bytes")}},
+            "hbm_frac": round(value / world * ALGO_BYTES_PER_FRAME / 1e9 / peak, 4),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "learn": learn}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -68,32 +68,71 @@ __device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32
 
 // 32x32 bit-matrix transpose across a warp (row = lane, column = bit):
 // afterwards lane j bit f = lane f bit j.  Recursive block swap, 5 stages of
-// shuffle + rotate + select.
-__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, uint32_t lane) {
-    const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+// SHFL + rotate (SHF.L.W) + select (LOP3) with per-lane rotate amounts and keep
+// masks precomputed once.
+struct TransposeLane {
+    uint32_t rot[5], keep[5];
+    __device__ __forceinline__ explicit TransposeLane(uint32_t lane) {
+        const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            const uint32_t s = 16u >> i;
+            const bool lo = (lane & s) == 0;
+            rot[i] = lo ? s : 32u - s;
+            keep[i] = lo ? masks[i] : ~masks[i];
+        }
+    }
+};
+
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, const TransposeLane& t) {
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-        const uint32_t s = 16u >> i;
-        const bool lo = (lane & s) == 0;
-        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
-        const uint32_t r = __funnelshift_l(y, y, lo ? s : 32u - s);
-        const uint32_t keep = lo ? masks[i] : ~masks[i];
-        x = (x & keep) | (r & ~keep);
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, 16u >> i);
+        const uint32_t r = __funnelshift_l(y, y, t.rot[i]);
+        x = (x & t.keep[i]) | (r & ~t.keep[i]);
     }
     return x;
 }
 
-// Byte-nonzero flags of 32 consecutive pixels (two uint4) merged into one word:
-// pixel 4k+b (byte b of word k) lands on bit 8b+k.  bit = byte != 0 (R12).
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* addr, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
+                 : "=r"(old)
+                 : "r"(smem_addr(addr)), "r"(v)
+                 : "memory");
+    return old;
+}
+
+// Byte-nonzero flags of 32 consecutive pixels (two uint4) merged into one word.
+// Flag of byte b of word k sits at bit 8b+7 after the carry trick (bit = byte != 0, R12);
+// words k < 7 are moved into place with one IMAD.HI (a right shift by a multiply on the
+// FMA pipe) and word 7 with one IMAD, then masked in with a LOP3.
+// Resulting position of pixel 4k+b: k, 7+k, 15+k, 23+k (k < 7); 14, 22, 30, 31 (k = 7).
+__device__ __forceinline__ uint32_t nz_flags(uint32_t v) {
+    return (((v & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | v) & 0x80808080u;
+}
+
 __device__ __forceinline__ uint32_t nonzero_mask32(const uint4 a, const uint4 b) {
     const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
     uint32_t m = 0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        const uint32_t t = (((v[k] & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | v[k]) & 0x80808080u;
-        m |= t >> (7 - k);
+    for (int k = 0; k < 7; ++k) {
+        const uint32_t mk = (1u << (k + 25)) | (1u << (k + 24));
+        m |= __umulhi(nz_flags(v[k]), mk) & ((1u << k) | (1u << (7 + k)) | (1u << (15 + k)) | (1u << (23 + k)));
     }
+    m |= (nz_flags(v[7]) * 0x81u) & 0xC0404000u;
     return m;
+}
+
+// Pixel (0..31 within a block) whose flag ends at bit j of nonzero_mask32's result.
+__device__ __forceinline__ uint32_t pixel_of_bit(uint32_t j) {
+    if (j == 31) return 31;
+    if (j == 30) return 30;
+    if (j == 22) return 29;
+    if (j == 14) return 28;
+    const uint32_t b = j < 7 ? 0u : (j < 14 ? 1u : (j < 22 ? 2u : 3u));
+    const uint32_t base = b == 0 ? 0u : (b == 1 ? 7u : (b == 2 ? 15u : 23u));
+    return 4u * (j - base) + b;
 }
 
 struct Planes {
@@ -145,19 +184,23 @@ __device__ __forceinline__ uint64_t rank_key(uint32_t raw, uint32_t bc, uint32_t
 
 }  // namespace
 
-template <int CPT>
+template <int CPT, int CH>
 __global__ void __launch_bounds__(kBatchedThreads, 1) sp_batched_kernel(const BatchedParams p) {
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, wi = tid >> 5;
+    constexpr uint32_t kChunkBits = CH;           // pixels per input row of a stage
+    constexpr uint32_t kBPW = CH / 1024;          // 32-pixel blocks per warp per chunk
     constexpr uint32_t kRow = kChunkBits + kStagePad;
     constexpr uint32_t kStageBytes = 32u * kRow;
+    const uint32_t NST = p.stages;
 
     uint8_t* stage_base = smem;
-    uint8_t* region = smem + p.stages * kStageBytes;
+    uint8_t* region = smem + NST * kStageBytes;
     uint32_t* words = reinterpret_cast<uint32_t*>(region);
     uint16_t* rawbuf = reinterpret_cast<uint16_t*>(region);
     uint32_t* s_bc = reinterpret_cast<uint32_t*>(region + p.region_bytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_bc + p.C32);
+    uint32_t* released = reinterpret_cast<uint32_t*>(bars + NST);  // per-stage release counters
 
     const uint32_t K = p.K;
     const uint32_t group = blockIdx.x / K, rank = blockIdx.x % K;
@@ -171,30 +214,38 @@ __global__ void __launch_bounds__(kBatchedThreads, 1) sp_batched_kernel(const Ba
     const uint32_t nchunks = pix_end > pix_begin ? (pix_end - pix_begin + kChunkBits - 1) / kChunkBits : 0;
 
     // ---- setup ---------------------------------------------------------------------------
-    if (tid < p.stages) mbar_init(&bars[tid], 1);
+    if (tid < NST) {
+        mbar_init(&bars[tid], 1);
+        released[tid] = 0u;
+    }
     for (uint32_t c = tid; c < p.C32; c += kBatchedThreads) s_bc[c] = p.bc[c];
     if (tid == 0) words[p.Lw] = 0u;  // the zero slot padding / disconnected synapses point to
     if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
 
-    // Producer: warp 0 issues the bulk copies of chunk j (one 16B-multiple row per input).
-    auto issue = [&](uint32_t j) {
-        const uint32_t st = j % p.stages;
+    // Producer step for chunk j (one thread): expect the bytes, then one bulk copy per input
+    // row.  Called by thread 0 for the prologue and afterwards by the lane that releases a
+    // stage last, so the ring refills without any CTA-wide barrier.
+    const uint8_t* frames_g = p.frames + static_cast<size_t>(in0) * p.nbits;
+    auto issue = [&](uint32_t j, uint32_t st) {
         const uint32_t p0 = pix_begin + j * kChunkBits;
         const uint32_t vb = min(kChunkBits, pix_end - p0);
-        if (lane == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive_expect_tx(&bars[st], vb * gs);
-        }
-        __syncwarp();
-        if (lane < gs)
-            bulk_copy_g2s(stage_base + st * kStageBytes + lane * kRow,
-                          p.frames + static_cast<size_t>(in0 + lane) * p.nbits + p0, vb, &bars[st]);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(&bars[st], vb * gs);
+        uint8_t* dst = stage_base + st * kStageBytes;
+        const uint8_t* src = frames_g + p0;
+        for (uint32_t f = 0; f < gs; ++f)
+            bulk_copy_g2s(dst + f * kRow, src + static_cast<size_t>(f) * p.nbits, vb, &bars[st]);
     };
-    if (wi == 0) {
-        const uint32_t pre = min(p.stages, nchunks);
-        for (uint32_t j = 0; j < pre; ++j) issue(j);
+    if (tid == 0) {
+        const uint32_t pre = min(NST, nchunks);
+        for (uint32_t j = 0; j < pre; ++j) issue(j, j);
     }
+
+    const TransposeLane tl(lane);
+    const uint32_t lane_ok = lane < gs ? 0xFFFFFFFFu : 0u;
+    const uint32_t out_bit_pixel = pixel_of_bit(lane);  // pixel of the word this lane writes
+    const uint8_t* my_row = stage_base + lane * kRow;
 
     Planes P[CPT];
 #pragma unroll
@@ -205,30 +256,44 @@ __global__ void __launch_bounds__(kBatchedThreads, 1) sp_batched_kernel(const Ba
     }
 
     // ---- stream the windows: transpose chunks into X, then gather ----------------------
-    uint32_t j = 0;
+    uint32_t j = 0, st = 0, phase = 0;
     for (uint32_t w = w0; w < w1; ++w) {
         const uint32_t wbase = w * p.Lw;
-        const uint32_t wend = min(wbase + p.Lw, p.nbits);
-        const uint32_t nch = (wend - wbase + kChunkBits - 1) / kChunkBits;
-        for (uint32_t q = 0; q < nch; ++q, ++j) {
-            const uint32_t st = j % p.stages;
-            mbar_wait(&bars[st], (j / p.stages) & 1u);
-            const uint32_t vb = min(kChunkBits, wend - (wbase + q * kChunkBits));
-            // a1: warp wi turns block wi (32 pixels x 32 inputs) into 32 bit-sliced words
-            {
-                const uint8_t* row = stage_base + st * kStageBytes + lane * kRow + wi * 32u;
+        const uint32_t wlen = min(p.Lw, p.nbits - wbase);
+        const uint32_t nch = (wlen + kChunkBits - 1) / kChunkBits;
+        for (uint32_t q = 0; q < nch; ++q) {
+            mbar_wait(&bars[st], phase);
+            // a1: warp wi turns blocks wi, wi+32, .. (32 pixels x 32 inputs each) into
+            // 32 bit-sliced words per block
+            const uint32_t rem = wlen - q * kChunkBits;  // valid pixels from this chunk on
+#pragma unroll
+            for (uint32_t i = 0; i < kBPW; ++i) {
+                const uint32_t blk = wi + 32u * i;
+                const uint8_t* row = my_row + st * kStageBytes + blk * 32u;
                 const uint4 a = *reinterpret_cast<const uint4*>(row);
                 const uint4 b = *reinterpret_cast<const uint4*>(row + 16);
                 uint32_t m = nonzero_mask32(a, b);
-                const int vloc = static_cast<int>(vb) - static_cast<int>(wi * 32u);
-                if (lane >= gs || vloc <= 0) m = 0u;
-                else if (vloc < 32) m &= 0x0F0F0F0Fu;  // vb is a multiple of 16
-                m = warp_transpose32(m, lane);
-                words[q * kChunkBits + wi * 32u + 4u * (lane & 7u) + (lane >> 3)] = m;
+                uint32_t ok = lane_ok;
+                if (rem < kChunkBits) {  // partial chunk: its length is a multiple of 16
+                    const int vloc = static_cast<int>(rem) - static_cast<int>(blk * 32u);
+                    ok &= vloc <= 0 ? 0u : (vloc < 32 ? 0x0787878Fu /* pixels 0..15 */ : 0xFFFFFFFFu);
+                }
+                m = warp_transpose32(m & ok, tl);
+                words[q * kChunkBits + blk * 32u + out_bit_pixel] = m;
             }
-            __syncthreads();  // stage st consumed; X words of this chunk visible
-            if (wi == 0 && j + p.stages < nchunks) issue(j + p.stages);
+            // release the stage; the warp that releases it last refills it (chunk j + NST)
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t prev = atom_add_acq_rel(&released[st], 1u);
+                if ((prev & 31u) == 31u && j + NST < nchunks) issue(j + NST, st);
+            }
+            ++j;
+            if (++st == NST) {
+                st = 0;
+                phase ^= 1u;
+            }
         }
+        __syncthreads();  // all words of window w written
         // a2: bit-sliced gather-count of this window's synapses (ELL, 8 slots per block)
 #pragma unroll
         for (int i = 0; i < CPT; ++i) {
@@ -266,6 +331,9 @@ __global__ void __launch_bounds__(kBatchedThreads, 1) sp_batched_kernel(const Ba
     // ---- a3/a4: per input: (cluster-sum), keys, k-winners, SDR ---------------------------
     const uint32_t theta = p.min_overlap, L = p.keyL;
     const uint64_t one = 1ull << 23;
+    const uint32_t nbN = p.keyBits - L;             // significant bits of N
+    const uint32_t sh = nbN > 16u ? nbN - 16u : 0u;  // coarse key u = N >> sh has <= 16 bits
+    uint64_t* tie_list = reinterpret_cast<uint64_t*>(stage_base) + wi * 64u;  // ring is idle now
     for (uint32_t f = rank + K * wi; f < gs; f += K * 32u) {
         uint16_t* row = rawbuf + f * p.C32;
         if (K > 1) {
@@ -285,18 +353,58 @@ __global__ void __launch_bounds__(kBatchedThreads, 1) sp_batched_kernel(const Ba
                     r >= theta ? __fmul_rn(static_cast<float>(r), p.boost[c]) : 0.0f;
             }
         }
-        uint64_t T = 0;
+        uint32_t Tu = 0;       // k-th largest coarse key
+        uint64_t T2 = 0;       // exact key threshold among the columns with u == Tu
         if (p.radius == 0) {
-            // global: T = k-th largest key (bitwise search, warp-wide counts)
-            for (int bit = static_cast<int>(p.keyBits) - 1; bit >= 0; --bit) {
-                const uint64_t cand = T | (1ull << bit);
+            // (1) coarse: bitwise search of the k-th largest u over 16 bits
+            for (int bit = 15; bit >= 0; --bit) {
+                const uint32_t cand = Tu | (1u << bit);
                 uint32_t cnt = 0;
                 for (uint32_t c = lane; c < p.C32; c += 32u) {
                     uint64_t N;
-                    cnt += rank_key(row[c], s_bc[c], theta, c, L, N) >= cand ? 1u : 0u;
+                    rank_key(row[c], s_bc[c], theta, c, L, N);
+                    cnt += static_cast<uint32_t>(N >> sh) >= cand ? 1u : 0u;
                 }
-                cnt = __reduce_add_sync(0xffffffffu, cnt);
-                if (cnt >= p.k) T = cand;
+                if (__reduce_add_sync(0xffffffffu, cnt) >= p.k) Tu = cand;
+            }
+            if (Tu > 0) {
+                // (2) exact: the columns tied at u == Tu, ranked by their exact keys
+                uint32_t ngt = 0, nties = 0;
+                for (uint32_t cw = 0; cw < p.ncw; ++cw) {
+                    const uint32_t c = cw * 32u + lane;
+                    uint64_t N;
+                    const uint64_t key = rank_key(row[c], s_bc[c], theta, c, L, N);
+                    const uint32_t u = static_cast<uint32_t>(N >> sh);
+                    ngt += u > Tu ? 1u : 0u;
+                    const uint32_t tie = __ballot_sync(0xffffffffu, u == Tu);
+                    const uint32_t pos = nties + __popc(tie & ((1u << lane) - 1u));
+                    if (u == Tu && pos < 64u) tie_list[pos] = key;
+                    nties += __popc(tie);
+                }
+                ngt = __reduce_add_sync(0xffffffffu, ngt);
+                const uint32_t need = p.k - ngt;  // >= 1 by construction of Tu
+                __syncwarp();
+                if (nties <= 64u) {
+                    const uint64_t k0 = lane < nties ? tie_list[lane] : 0ull;
+                    const uint64_t k1 = lane + 32u < nties ? tie_list[lane + 32u] : 0ull;
+                    for (int bit = static_cast<int>(p.keyBits) - 1; bit >= 0; --bit) {
+                        const uint64_t cand = T2 | (1ull << bit);
+                        const uint32_t cnt = (k0 >= cand ? 1u : 0u) + (k1 >= cand ? 1u : 0u);
+                        if (__reduce_add_sync(0xffffffffu, cnt) >= need) T2 = cand;
+                    }
+                } else {  // many ties: search over all tied columns in place
+                    for (int bit = static_cast<int>(p.keyBits) - 1; bit >= 0; --bit) {
+                        const uint64_t cand = T2 | (1ull << bit);
+                        uint32_t cnt = 0;
+                        for (uint32_t c = lane; c < p.C32; c += 32u) {
+                            uint64_t N;
+                            const uint64_t key = rank_key(row[c], s_bc[c], theta, c, L, N);
+                            cnt += (static_cast<uint32_t>(N >> sh) == Tu && key >= cand) ? 1u : 0u;
+                        }
+                        if (__reduce_add_sync(0xffffffffu, cnt) >= need) T2 = cand;
+                    }
+                }
+                __syncwarp();
             }
         }
         uint32_t total = 0;
@@ -307,7 +415,9 @@ __global__ void __launch_bounds__(kBatchedThreads, 1) sp_batched_kernel(const Ba
             bool act = N > one;
             if (act) {
                 if (p.radius == 0) {
-                    act = key >= T;
+                    const uint32_t u = static_cast<uint32_t>(N >> sh);
+                    // Tu == 0: fewer than k columns have u > 0, all of them win (floor aside)
+                    act = Tu == 0 ? u > 0 : (u > Tu || (u == Tu && key >= T2));
                 } else {
                     const uint32_t lo = c >= p.radius ? c - p.radius : 0u;
                     const uint32_t hi = min(p.C - 1u, c + p.radius);
@@ -338,8 +448,10 @@ static cudaError_t allow_dynamic_smem(F* fn, int max_smem) {
 }
 
 cudaError_t configure_batched(int max_smem) {
-    cudaError_t e = allow_dynamic_smem(sp_batched_kernel<1>, max_smem);
-    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2>, max_smem);
+    cudaError_t e = allow_dynamic_smem(sp_batched_kernel<1, 1024>, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2, 1024>, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<1, 2048>, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2, 2048>, max_smem);
     return e;
 }
 
@@ -357,8 +469,11 @@ cudaError_t launch_batched(const BatchedParams& p, uint32_t smem_bytes, cudaStre
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (cpt <= 1) return cudaLaunchKernelEx(&cfg, sp_batched_kernel<1>, p);
-    return cudaLaunchKernelEx(&cfg, sp_batched_kernel<2>, p);
+    if (p.chunk == 2048)
+        return cpt <= 1 ? cudaLaunchKernelEx(&cfg, sp_batched_kernel<1, 2048>, p)
+                        : cudaLaunchKernelEx(&cfg, sp_batched_kernel<2, 2048>, p);
+    return cpt <= 1 ? cudaLaunchKernelEx(&cfg, sp_batched_kernel<1, 1024>, p)
+                    : cudaLaunchKernelEx(&cfg, sp_batched_kernel<2, 1024>, p);
 }
 
 // Maximum co-resident clusters for K = 1..8 at this smem size (index K).
@@ -378,7 +493,7 @@ cudaError_t batched_max_clusters(uint32_t smem_bytes, int max_clusters[9]) {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int n = 0;
-        e = cudaOccupancyMaxActiveClusters(&n, sp_batched_kernel<1>, &cfg);
+        e = cudaOccupancyMaxActiveClusters(&n, sp_batched_kernel<1, 1024>, &cfg);
         if (e != cudaSuccess) {
             (void)cudaGetLastError();
             n = 0;

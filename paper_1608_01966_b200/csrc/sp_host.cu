@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -143,30 +144,44 @@ Geometry make_geometry(const sp_config& cfg) {
 // Shared-memory plan of the batched kernel: ring of `stages` chunks of 32 x (1024+16) B,
 // a region holding max(Lw+1 words, 32*C32 uint16 counts), Bc[C32], mbarriers.
 BatchedLayout plan_batched_layout(const Geometry& g, int max_smem) {
+    // Chunk rows of 2048 B keep the bulk-copy engine at HBM rate (~80 cycles per copy
+    // whatever its size: 1 KB rows cap an SM at ~24 GB/s; scripts/bench_bulk.cu,
+    // profiles/); 1024 B rows are the fallback when the ring does not fit.
     BatchedLayout L;
     if (g.C32 > kMaxBatchedColumns || g.S > kMaxBatchedSynapses) return L;
-    const uint32_t stage_bytes = 32u * (kChunkBits + kStagePad);
     const uint32_t counts_bytes = 32u * g.C32 * 2u;
-    const uint32_t fixed = g.C32 * 4u + 64u;  // Bc + barriers (<= 8 stages)
-    const uint32_t nbits_r = (g.nbits + kChunkBits - 1) / kChunkBits * kChunkBits;
-    for (uint32_t stages = 4; stages >= 2; --stages) {
+    const uint32_t fixed = g.C32 * 4u + 64u;  // Bc + barriers + release counters
+    const uint32_t options[5][2] = {{2048, 3}, {2048, 2}, {1024, 4}, {1024, 3}, {1024, 2}};
+    // development overrides (experiments only): SP_CHUNK=1024|2048, SP_STAGES=2..4
+    const char* ec = std::getenv("SP_CHUNK");
+    const char* es = std::getenv("SP_STAGES");
+    const uint32_t want_chunk = ec ? static_cast<uint32_t>(std::atoi(ec)) : 0u;
+    const uint32_t want_stages = es ? static_cast<uint32_t>(std::atoi(es)) : 0u;
+    for (const auto& o : options) {
+        const uint32_t chunk = o[0], stages = o[1];
+        if ((want_chunk && chunk != want_chunk) || (want_stages && stages != want_stages)) continue;
+        const uint32_t stage_bytes = 32u * (chunk + kStagePad);
+        const uint32_t nbits_r = (g.nbits + chunk - 1) / chunk * chunk;
         const int64_t avail = static_cast<int64_t>(max_smem) - stages * stage_bytes - fixed;
-        if (avail < static_cast<int64_t>(counts_bytes) || avail < 4 * (kChunkBits + 1)) continue;
-        // largest Lw (multiple of Lc, local idx < 65536) with (Lw+1)*4 <= avail
-        uint32_t Lw = static_cast<uint32_t>((avail / 4 - 1) / kChunkBits * kChunkBits);
-        Lw = std::min<uint32_t>(Lw, 63u * kChunkBits);
+        if (avail < static_cast<int64_t>(counts_bytes) || avail < 4 * (chunk + 1)) continue;
+        // largest Lw (multiple of the chunk, local idx < 65536) with (Lw+1)*4 <= avail
+        uint32_t Lw = static_cast<uint32_t>((avail / 4 - 1) / chunk * chunk);
+        Lw = std::min<uint32_t>(Lw, 64512u / chunk * chunk);
         Lw = std::min<uint32_t>(Lw, nbits_r);
         if (Lw == 0) continue;
-        // balance the windows: same count, smallest Lw (multiple of Lc) that covers nbits
+        // large frames need windows of >= 4 chunks or the window barriers dominate
+        if (Lw < 4 * chunk && nbits_r > Lw) continue;
+        // balance the windows: same count, smallest Lw (multiple of the chunk) covering nbits
         const uint32_t nwin = (g.nbits + Lw - 1) / Lw;
         const uint32_t per = (g.nbits + nwin - 1) / nwin;
-        Lw = (per + kChunkBits - 1) / kChunkBits * kChunkBits;
+        Lw = (per + chunk - 1) / chunk * chunk;
         L.ok = true;
+        L.chunk = chunk;
         L.stages = stages;
         L.Lw = Lw;
         L.nwin = (g.nbits + Lw - 1) / Lw;
         L.region_bytes = (std::max(counts_bytes, (Lw + 1) * 4u) + 15u) & ~15u;
-        L.smem_bytes = stages * stage_bytes + L.region_bytes + g.C32 * 4u + stages * 8u;
+        L.smem_bytes = stages * stage_bytes + L.region_bytes + g.C32 * 4u + stages * 12u;
         return L;
     }
     return L;
@@ -298,7 +313,7 @@ sp_plan_info make_plan(const sp_handle* h, uint32_t n, bool learn, const uint8_t
         pl.ctas = G * K;
         pl.window_bits = h->lay.Lw;
         pl.num_windows = h->lay.nwin;
-        pl.chunk_bits = sp::kChunkBits;
+        pl.chunk_bits = h->lay.chunk;
         pl.stages = h->lay.stages;
         pl.smem_bytes = h->lay.smem_bytes;
     } else {
@@ -435,6 +450,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         p.nwin = h->lay.nwin;
         p.stages = h->lay.stages;
         p.region_bytes = h->lay.region_bytes;
+        p.chunk = h->lay.chunk;
         p.groups = pl.groups;
         p.K = pl.cluster;
         p.ell_off = h->d_ell_off;

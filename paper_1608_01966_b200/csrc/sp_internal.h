@@ -8,7 +8,7 @@
 
 namespace sp {
 
-constexpr uint32_t kChunkBits = 1024;      // Lc: pixels per input per pipeline stage
+constexpr uint32_t kChunkMin = 1024;       // Lc options: 1024 or 2048 pixels per input row
 constexpr uint32_t kStagePad = 16;         // bytes between input rows of a stage (bank spread)
 constexpr uint32_t kBatchedThreads = 1024; // 32 warps: warp w transposes block w of a chunk
 constexpr uint32_t kMaxBatchedColumns = 2048;
@@ -41,7 +41,7 @@ struct Geometry {
 // Layout of the batched (bit-sliced) path, fixed at create time (depends on C, S, nbits).
 struct BatchedLayout {
     bool ok = false;
-    uint32_t stages = 0, Lw = 0, nwin = 0;
+    uint32_t chunk = 0, stages = 0, Lw = 0, nwin = 0;
     uint32_t region_bytes = 0, smem_bytes = 0;
 };
 
@@ -51,7 +51,7 @@ struct BatchedParams {
     uint32_t C, C32, ncw;
     uint32_t min_overlap, k, radius;
     uint32_t keyL, keyBits;
-    uint32_t Lw, nwin, stages, region_bytes;
+    uint32_t Lw, nwin, stages, region_bytes, chunk;
     uint32_t groups, K;
     const uint32_t* ell_off;   // [nwin][ncw] offset in uint4 units
     const uint16_t* ell_nb;    // [nwin][ncw] number of 8-slot blocks
