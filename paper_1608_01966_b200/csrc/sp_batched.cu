@@ -10,14 +10,15 @@
 //     X[idx[c,s]]  over its connected synapses s                 (Alg. 1 l.1-5)
 // accumulated with carry-save adders (Harley-Seal), so ONE shared-memory
 // gather serves 32 inputs.  The frames stream from HBM exactly once through a
-// cp.async.bulk ring (mbarrier complete_tx), so the kernel is HBM-bound.
+// ring of 2-D TMA boxes (128 pixels x 32 inputs, 128B swizzle, mbarrier
+// complete_tx), so the kernel is HBM-bound.
 //
 // Shared memory per CTA:
-//   [stages x 32 rows x (1024+16) B]  bulk-copy ring, one row per input
-//   [region]                          window of Lw bit-sliced words + zero slot,
-//                                     later reused for raw counts uint16[32][C32]
-//   [C32 x u32]                       Bc = boost * 2^23
-//   [stages x u64]                    mbarriers
+//   [stages x 32 KiB]   TMA ring (8 boxes per stage); after streaming it holds the
+//                       raw counts uint16[32][C32]
+//   [region]            window of Lw bit-sliced words + zero slot (later: tie lists)
+//   [C32 x u32]         Bc = boost * 2^23
+//   [stages x u64/u32]  mbarriers, release counters
 // A cluster of K CTAs can split one group's pixel windows; partial counts are
 // then summed through distributed shared memory (DSMEM) before inhibition.
 #include <cooperative_groups.h>
@@ -57,12 +58,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes,
-                                              uint64_t* bar) {
+// One 2-D TMA box {128 pixels, 32 inputs} at (x, row) of the frames' tensor map.
+__device__ __forceinline__ void tma_box_g2s(void* dst, const CUtensorMap* map, uint32_t x,
+                                            uint32_t row, uint64_t* bar) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(row), "r"(smem_addr(bar))
         : "memory");
 }
 
@@ -184,20 +186,17 @@ __device__ __forceinline__ uint64_t rank_key(uint32_t raw, uint32_t bc, uint32_t
 
 }  // namespace
 
-template <int CPT, int CH>
-__global__ void __launch_bounds__(kBatchedThreads, 1) sp_batched_kernel(const BatchedParams p) {
-    extern __shared__ __align__(128) uint8_t smem[];
+template <int CPT>
+__global__ void __launch_bounds__(kBatchedThreads, 1)
+    sp_batched_kernel(const __grid_constant__ BatchedParams p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
     const uint32_t tid = threadIdx.x, lane = tid & 31u, wi = tid >> 5;
-    constexpr uint32_t kChunkBits = CH;           // pixels per input row of a stage
-    constexpr uint32_t kBPW = CH / 1024;          // 32-pixel blocks per warp per chunk
-    constexpr uint32_t kRow = kChunkBits + kStagePad;
-    constexpr uint32_t kStageBytes = 32u * kRow;
     const uint32_t NST = p.stages;
 
-    uint8_t* stage_base = smem;
+    uint8_t* stage_base = smem;  // 1024-aligned (swizzle-128B boxes)
+    uint16_t* rawbuf = reinterpret_cast<uint16_t*>(stage_base);  // after streaming
     uint8_t* region = smem + NST * kStageBytes;
     uint32_t* words = reinterpret_cast<uint32_t*>(region);
-    uint16_t* rawbuf = reinterpret_cast<uint16_t*>(region);
     uint32_t* s_bc = reinterpret_cast<uint32_t*>(region + p.region_bytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_bc + p.C32);
     uint32_t* released = reinterpret_cast<uint32_t*>(bars + NST);  // per-stage release counters
@@ -214,6 +213,7 @@ __global__ void __launch_bounds__(kBatchedThreads, 1) sp_batched_kernel(const Ba
     const uint32_t nchunks = pix_end > pix_begin ? (pix_end - pix_begin + kChunkBits - 1) / kChunkBits : 0;
 
     // ---- setup ---------------------------------------------------------------------------
+    if (tid == 0 && (smem_addr(smem) & 1023u)) __trap();  // swizzled boxes need 1 KiB alignment
     if (tid < NST) {
         mbar_init(&bars[tid], 1);
         released[tid] = 0u;
@@ -223,19 +223,18 @@ __global__ void __launch_bounds__(kBatchedThreads, 1) sp_batched_kernel(const Ba
     if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
 
-    // Producer step for chunk j (one thread): expect the bytes, then one bulk copy per input
-    // row.  Called by thread 0 for the prologue and afterwards by the lane that releases a
-    // stage last, so the ring refills without any CTA-wide barrier.
-    const uint8_t* frames_g = p.frames + static_cast<size_t>(in0) * p.nbits;
+    // Producer step for chunk j (one thread): expect the stage's bytes, then 8 TMA boxes of
+    // 128 pixels x 32 inputs (rows beyond the batch and pixels beyond nbits are zero-filled).
+    // Called by thread 0 for the prologue and afterwards by the lane that releases a stage
+    // last, so the ring refills without any CTA-wide barrier.
     auto issue = [&](uint32_t j, uint32_t st) {
-        const uint32_t p0 = pix_begin + j * kChunkBits;
-        const uint32_t vb = min(kChunkBits, pix_end - p0);
+        const uint32_t x0 = pix_begin + j * kChunkBits;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive_expect_tx(&bars[st], vb * gs);
+        mbar_arrive_expect_tx(&bars[st], kStageBytes);
         uint8_t* dst = stage_base + st * kStageBytes;
-        const uint8_t* src = frames_g + p0;
-        for (uint32_t f = 0; f < gs; ++f)
-            bulk_copy_g2s(dst + f * kRow, src + static_cast<size_t>(f) * p.nbits, vb, &bars[st]);
+#pragma unroll
+        for (uint32_t b = 0; b < kChunkBits / kBoxBytes; ++b)
+            tma_box_g2s(dst + b * 32u * kBoxBytes, &p.tmap, x0 + b * kBoxBytes, in0, &bars[st]);
     };
     if (tid == 0) {
         const uint32_t pre = min(NST, nchunks);
@@ -244,8 +243,12 @@ __global__ void __launch_bounds__(kBatchedThreads, 1) sp_batched_kernel(const Ba
 
     const TransposeLane tl(lane);
     const uint32_t lane_ok = lane < gs ? 0xFFFFFFFFu : 0u;
-    const uint32_t out_bit_pixel = pixel_of_bit(lane);  // pixel of the word this lane writes
-    const uint8_t* my_row = stage_base + lane * kRow;
+    const uint32_t out_pixel = wi * 32u + pixel_of_bit(lane);  // word this lane writes per chunk
+    // lane f reads its 32 bytes of block wi from box wi/4, row f, 16-byte slots
+    // 2*(wi%4) and +1, swizzled by XOR with (f % 8) (CU_TENSOR_MAP_SWIZZLE_128B)
+    const uint32_t c0 = 2u * (wi & 3u);
+    const uint32_t rd0 = (wi >> 2) * (32u * kBoxBytes) + lane * kBoxBytes + ((c0 ^ (lane & 7u)) << 4);
+    const uint32_t rd1 = (wi >> 2) * (32u * kBoxBytes) + lane * kBoxBytes + (((c0 + 1u) ^ (lane & 7u)) << 4);
 
     Planes P[CPT];
 #pragma unroll
@@ -263,23 +266,13 @@ __global__ void __launch_bounds__(kBatchedThreads, 1) sp_batched_kernel(const Ba
         const uint32_t nch = (wlen + kChunkBits - 1) / kChunkBits;
         for (uint32_t q = 0; q < nch; ++q) {
             mbar_wait(&bars[st], phase);
-            // a1: warp wi turns blocks wi, wi+32, .. (32 pixels x 32 inputs each) into
-            // 32 bit-sliced words per block
-            const uint32_t rem = wlen - q * kChunkBits;  // valid pixels from this chunk on
-#pragma unroll
-            for (uint32_t i = 0; i < kBPW; ++i) {
-                const uint32_t blk = wi + 32u * i;
-                const uint8_t* row = my_row + st * kStageBytes + blk * 32u;
-                const uint4 a = *reinterpret_cast<const uint4*>(row);
-                const uint4 b = *reinterpret_cast<const uint4*>(row + 16);
-                uint32_t m = nonzero_mask32(a, b);
-                uint32_t ok = lane_ok;
-                if (rem < kChunkBits) {  // partial chunk: its length is a multiple of 16
-                    const int vloc = static_cast<int>(rem) - static_cast<int>(blk * 32u);
-                    ok &= vloc <= 0 ? 0u : (vloc < 32 ? 0x0787878Fu /* pixels 0..15 */ : 0xFFFFFFFFu);
-                }
-                m = warp_transpose32(m & ok, tl);
-                words[q * kChunkBits + blk * 32u + out_bit_pixel] = m;
+            // a1: warp wi turns block wi (32 pixels x 32 inputs) into 32 bit-sliced words
+            {
+                const uint8_t* stg = stage_base + st * kStageBytes;
+                const uint4 a = *reinterpret_cast<const uint4*>(stg + rd0);
+                const uint4 b = *reinterpret_cast<const uint4*>(stg + rd1);
+                const uint32_t m = warp_transpose32(nonzero_mask32(a, b) & lane_ok, tl);
+                words[q * kChunkBits + out_pixel] = m;
             }
             // release the stage; the warp that releases it last refills it (chunk j + NST)
             __syncwarp();
@@ -333,7 +326,7 @@ __global__ void __launch_bounds__(kBatchedThreads, 1) sp_batched_kernel(const Ba
     const uint64_t one = 1ull << 23;
     const uint32_t nbN = p.keyBits - L;             // significant bits of N
     const uint32_t sh = nbN > 16u ? nbN - 16u : 0u;  // coarse key u = N >> sh has <= 16 bits
-    uint64_t* tie_list = reinterpret_cast<uint64_t*>(stage_base) + wi * 64u;  // ring is idle now
+    uint64_t* tie_list = reinterpret_cast<uint64_t*>(region) + wi * 64u;  // X window is idle now
     for (uint32_t f = rank + K * wi; f < gs; f += K * 32u) {
         uint16_t* row = rawbuf + f * p.C32;
         if (K > 1) {
@@ -448,10 +441,8 @@ static cudaError_t allow_dynamic_smem(F* fn, int max_smem) {
 }
 
 cudaError_t configure_batched(int max_smem) {
-    cudaError_t e = allow_dynamic_smem(sp_batched_kernel<1, 1024>, max_smem);
-    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2, 1024>, max_smem);
-    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<1, 2048>, max_smem);
-    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2, 2048>, max_smem);
+    cudaError_t e = allow_dynamic_smem(sp_batched_kernel<1>, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2>, max_smem);
     return e;
 }
 
@@ -469,11 +460,8 @@ cudaError_t launch_batched(const BatchedParams& p, uint32_t smem_bytes, cudaStre
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (p.chunk == 2048)
-        return cpt <= 1 ? cudaLaunchKernelEx(&cfg, sp_batched_kernel<1, 2048>, p)
-                        : cudaLaunchKernelEx(&cfg, sp_batched_kernel<2, 2048>, p);
-    return cpt <= 1 ? cudaLaunchKernelEx(&cfg, sp_batched_kernel<1, 1024>, p)
-                    : cudaLaunchKernelEx(&cfg, sp_batched_kernel<2, 1024>, p);
+    return cpt <= 1 ? cudaLaunchKernelEx(&cfg, sp_batched_kernel<1>, p)
+                    : cudaLaunchKernelEx(&cfg, sp_batched_kernel<2>, p);
 }
 
 // Maximum co-resident clusters for K = 1..8 at this smem size (index K).
@@ -493,7 +481,7 @@ cudaError_t batched_max_clusters(uint32_t smem_bytes, int max_clusters[9]) {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int n = 0;
-        e = cudaOccupancyMaxActiveClusters(&n, sp_batched_kernel<1, 1024>, &cfg);
+        e = cudaOccupancyMaxActiveClusters(&n, sp_batched_kernel<1>, &cfg);
         if (e != cudaSuccess) {
             (void)cudaGetLastError();
             n = 0;

@@ -15,6 +15,8 @@
 #include <string>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "sp_internal.h"
 #include "../../include/sp_synth.h"
 
@@ -141,50 +143,62 @@ Geometry make_geometry(const sp_config& cfg) {
     return g;
 }
 
-// Shared-memory plan of the batched kernel: ring of `stages` chunks of 32 x (1024+16) B,
-// a region holding max(Lw+1 words, 32*C32 uint16 counts), Bc[C32], mbarriers.
+// Shared-memory plan of the batched kernel.
 BatchedLayout plan_batched_layout(const Geometry& g, int max_smem) {
-    // Chunk rows of 2048 B keep the bulk-copy engine at HBM rate (~80 cycles per copy
-    // whatever its size: 1 KB rows cap an SM at ~24 GB/s; scripts/bench_bulk.cu,
-    // profiles/); 1024 B rows are the fallback when the ring does not fit.
+    // Ring of `stages` x 32 KiB stages filled by 2-D TMA boxes of 128 B x 32 inputs (8 per
+    // stage), then the window of Lw bit-sliced words (+ zero slot), Bc, barriers.  The raw
+    // counts uint16[32][C32] reuse the ring once streaming is over, so the ring must hold
+    // them.  scripts/bench_tma.cu: 4 x 32 KiB in flight streams at ~7 TB/s.
     BatchedLayout L;
     if (g.C32 > kMaxBatchedColumns || g.S > kMaxBatchedSynapses) return L;
     const uint32_t counts_bytes = 32u * g.C32 * 2u;
-    const uint32_t fixed = g.C32 * 4u + 64u;  // Bc + barriers + release counters
-    const uint32_t options[5][2] = {{2048, 3}, {2048, 2}, {1024, 4}, {1024, 3}, {1024, 2}};
-    // development overrides (experiments only): SP_CHUNK=1024|2048, SP_STAGES=2..4
-    const char* ec = std::getenv("SP_CHUNK");
-    const char* es = std::getenv("SP_STAGES");
-    const uint32_t want_chunk = ec ? static_cast<uint32_t>(std::atoi(ec)) : 0u;
+    const uint32_t fixed = g.C32 * 4u + 128u;  // Bc + barriers + release counters
+    const uint32_t nbits_r = (g.nbits + kChunkBits - 1) / kChunkBits * kChunkBits;
+    const char* es = std::getenv("SP_STAGES");  // development override (experiments only)
     const uint32_t want_stages = es ? static_cast<uint32_t>(std::atoi(es)) : 0u;
-    for (const auto& o : options) {
-        const uint32_t chunk = o[0], stages = o[1];
-        if ((want_chunk && chunk != want_chunk) || (want_stages && stages != want_stages)) continue;
-        const uint32_t stage_bytes = 32u * (chunk + kStagePad);
-        const uint32_t nbits_r = (g.nbits + chunk - 1) / chunk * chunk;
-        const int64_t avail = static_cast<int64_t>(max_smem) - stages * stage_bytes - fixed;
-        if (avail < static_cast<int64_t>(counts_bytes) || avail < 4 * (chunk + 1)) continue;
+    for (uint32_t stages = 4; stages >= 2; --stages) {
+        if (want_stages && stages != want_stages) continue;
+        if (stages * kStageBytes < counts_bytes) continue;
+        const int64_t avail = static_cast<int64_t>(max_smem) - stages * kStageBytes - fixed;
+        if (avail < 4 * static_cast<int64_t>(kChunkBits + 1)) continue;
         // largest Lw (multiple of the chunk, local idx < 65536) with (Lw+1)*4 <= avail
-        uint32_t Lw = static_cast<uint32_t>((avail / 4 - 1) / chunk * chunk);
-        Lw = std::min<uint32_t>(Lw, 64512u / chunk * chunk);
+        uint32_t Lw = static_cast<uint32_t>((avail / 4 - 1) / kChunkBits * kChunkBits);
+        Lw = std::min<uint32_t>(Lw, 64512u);
         Lw = std::min<uint32_t>(Lw, nbits_r);
         if (Lw == 0) continue;
-        // large frames need windows of >= 4 chunks or the window barriers dominate
-        if (Lw < 4 * chunk && nbits_r > Lw) continue;
         // balance the windows: same count, smallest Lw (multiple of the chunk) covering nbits
         const uint32_t nwin = (g.nbits + Lw - 1) / Lw;
         const uint32_t per = (g.nbits + nwin - 1) / nwin;
-        Lw = (per + chunk - 1) / chunk * chunk;
+        Lw = (per + kChunkBits - 1) / kChunkBits * kChunkBits;
         L.ok = true;
-        L.chunk = chunk;
         L.stages = stages;
         L.Lw = Lw;
         L.nwin = (g.nbits + Lw - 1) / Lw;
-        L.region_bytes = (std::max(counts_bytes, (Lw + 1) * 4u) + 15u) & ~15u;
-        L.smem_bytes = stages * stage_bytes + L.region_bytes + g.C32 * 4u + stages * 12u;
+        // the window doubles as the per-warp tie lists (32 warps x 64 keys) of the top-k
+        L.region_bytes = (std::max((Lw + 1) * 4u, 32u * 64u * 8u) + 127u) & ~127u;
+        L.smem_bytes = stages * kStageBytes + L.region_bytes + g.C32 * 4u + stages * 12u;
         return L;
     }
     return L;
+}
+
+bool encode_frames_tmap(CUtensorMap* map, const uint8_t* frames, uint32_t nbits, uint32_t rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q{};
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {nbits, rows};
+    const cuuint64_t strides[1] = {nbits};
+    const cuuint32_t box[2] = {kBoxBytes, 32u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(frames), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // Groups of <= 32 inputs and cluster size K: estimated time of each K
@@ -313,7 +327,7 @@ sp_plan_info make_plan(const sp_handle* h, uint32_t n, bool learn, const uint8_t
         pl.ctas = G * K;
         pl.window_bits = h->lay.Lw;
         pl.num_windows = h->lay.nwin;
-        pl.chunk_bits = h->lay.chunk;
+        pl.chunk_bits = sp::kChunkBits;
         pl.stages = h->lay.stages;
         pl.smem_bytes = h->lay.smem_bytes;
     } else {
@@ -435,7 +449,9 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
             h->ell_dirty = false;
         }
         sp::BatchedParams p{};
-        p.frames = frames;
+        if (!sp::encode_frames_tmap(&p.tmap, frames, g.nbits, n))
+            return fail(SP_E_CUDA, "cuTensorMapEncodeTiled failed for the frames (nbits %u, rows %u)",
+                        g.nbits, n);
         p.num_inputs = n;
         p.nbits = g.nbits;
         p.C = g.C;
@@ -450,7 +466,6 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         p.nwin = h->lay.nwin;
         p.stages = h->lay.stages;
         p.region_bytes = h->lay.region_bytes;
-        p.chunk = h->lay.chunk;
         p.groups = pl.groups;
         p.K = pl.cluster;
         p.ell_off = h->d_ell_off;

@@ -2,14 +2,16 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>  // CUtensorMap (types only; the encoder is fetched via cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 
 #include "../../include/sp.h"
 
 namespace sp {
 
-constexpr uint32_t kChunkMin = 1024;       // Lc options: 1024 or 2048 pixels per input row
-constexpr uint32_t kStagePad = 16;         // bytes between input rows of a stage (bank spread)
+constexpr uint32_t kChunkBits = 1024;      // Lc: pixels per input per pipeline stage
+constexpr uint32_t kBoxBytes = 128;        // TMA box: 128 B (pixels) x 32 rows (inputs), swizzle 128B
+constexpr uint32_t kStageBytes = 32u * kChunkBits;  // 8 boxes = 32 KiB per stage
 constexpr uint32_t kBatchedThreads = 1024; // 32 warps: warp w transposes block w of a chunk
 constexpr uint32_t kMaxBatchedColumns = 2048;
 constexpr uint32_t kMaxBatchedSynapses = 1023;  // 10 vertical-counter planes
@@ -25,6 +27,7 @@ enum : uint32_t {
     kNotBatchedSynapses = 16u,  // S > 1023
     kNotBatchedForced = 32u,    // force_path = PER_INPUT
     kNotBatchedSmem = 64u,      // no (stages, window) fits shared memory
+    kNotBatchedTensorMap = 128u, // the TMA descriptor could not be encoded
 };
 
 struct Geometry {
@@ -41,17 +44,17 @@ struct Geometry {
 // Layout of the batched (bit-sliced) path, fixed at create time (depends on C, S, nbits).
 struct BatchedLayout {
     bool ok = false;
-    uint32_t chunk = 0, stages = 0, Lw = 0, nwin = 0;
+    uint32_t stages = 0, Lw = 0, nwin = 0;
     uint32_t region_bytes = 0, smem_bytes = 0;
 };
 
-struct BatchedParams {
-    const uint8_t* frames;
+struct alignas(64) BatchedParams {
+    CUtensorMap tmap;          // 2-D uint8 view of the frames: {nbits, num_inputs}, box {128, 32}
     uint32_t num_inputs, nbits;
     uint32_t C, C32, ncw;
     uint32_t min_overlap, k, radius;
     uint32_t keyL, keyBits;
-    uint32_t Lw, nwin, stages, region_bytes, chunk;
+    uint32_t Lw, nwin, stages, region_bytes;
     uint32_t groups, K;
     const uint32_t* ell_off;   // [nwin][ncw] offset in uint4 units
     const uint16_t* ell_nb;    // [nwin][ncw] number of 8-slot blocks
@@ -92,6 +95,9 @@ BatchedLayout plan_batched_layout(const Geometry& g, int max_smem);
 void plan_batched_grid(const Geometry& g, uint32_t nwin, uint32_t num_inputs, int sm_count,
                        const int* max_clusters /* [9] by K, or nullptr */,
                        uint32_t* groups, uint32_t* K);
+
+// TMA descriptor of the frames for the batched kernel (sp_host.cu); false on failure
+bool encode_frames_tmap(CUtensorMap* map, const uint8_t* frames, uint32_t nbits, uint32_t rows);
 
 // one-time kernel attributes (max dynamic smem)
 cudaError_t configure_batched(int max_smem);
