@@ -96,13 +96,26 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, const Transpose
     return x;
 }
 
-__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* addr, uint32_t v) {
-    uint32_t old;
-    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;"
-                 : "=r"(old)
-                 : "r"(smem_addr(addr)), "r"(v)
-                 : "memory");
-    return old;
+// One elected lane of the (converged) warp adds 1 to a shared counter with acq_rel
+// semantics; returns true on that lane iff the counter was at 31 mod 32 (i.e. this warp
+// is the 32nd to release the stage).
+__device__ __forceinline__ bool warp_release_is_last(uint32_t addr) {
+    uint32_t last;
+    asm volatile(
+        "{\n"
+        ".reg .pred P1, P2;\n"
+        ".reg .b32 old;\n"
+        "elect.sync _|P1, 0xffffffff;\n"
+        "mov.u32 old, 0;\n"
+        "@P1 atom.acq_rel.cta.shared::cta.add.u32 old, [%1], 1;\n"
+        "and.b32 old, old, 31;\n"
+        "setp.eq.and.u32 P2, old, 31, P1;\n"
+        "selp.u32 %0, 1, 0, P2;\n"
+        "}\n"
+        : "=r"(last)
+        : "r"(addr)
+        : "memory");
+    return last != 0;
 }
 
 // Byte-nonzero flags of 32 consecutive pixels (two uint4) merged into one word.
@@ -241,6 +254,7 @@ __global__ void __launch_bounds__(kBatchedThreads, 1)
         for (uint32_t j = 0; j < pre; ++j) issue(j, j);
     }
 
+    const uint32_t released_addr = smem_addr(released);
     const TransposeLane tl(lane);
     const uint32_t lane_ok = lane < gs ? 0xFFFFFFFFu : 0u;
     const uint32_t out_pixel = wi * 32u + pixel_of_bit(lane);  // word this lane writes per chunk
@@ -275,11 +289,7 @@ __global__ void __launch_bounds__(kBatchedThreads, 1)
                 words[q * kChunkBits + out_pixel] = m;
             }
             // release the stage; the warp that releases it last refills it (chunk j + NST)
-            __syncwarp();
-            if (lane == 0) {
-                const uint32_t prev = atom_add_acq_rel(&released[st], 1u);
-                if ((prev & 31u) == 31u && j + NST < nchunks) issue(j + NST, st);
-            }
+            if (warp_release_is_last(released_addr + 4u * st) && j + NST < nchunks) issue(j + NST, st);
             ++j;
             if (++st == NST) {
                 st = 0;
@@ -349,16 +359,25 @@ __global__ void __launch_bounds__(kBatchedThreads, 1)
         uint32_t Tu = 0;       // k-th largest coarse key
         uint64_t T2 = 0;       // exact key threshold among the columns with u == Tu
         if (p.radius == 0) {
-            // (1) coarse: bitwise search of the k-th largest u over 16 bits
+            // (1) coarse: the k-th largest u = N >> sh (16 bits) by bitwise search, over
+            //     keys packed two per register (columns 64t+lane and 64t+32+lane)
+            constexpr int NU = 16 * CPT;
+            uint32_t uu[NU];
+#pragma unroll
+            for (int t = 0; t < NU; ++t) {
+                const uint32_t ca = (2u * t) * 32u + lane, cb = ca + 32u;
+                uint64_t Na = 0, Nb = 0;
+                if (ca < p.C32) rank_key(row[ca], s_bc[ca], theta, ca, L, Na);
+                if (cb < p.C32) rank_key(row[cb], s_bc[cb], theta, cb, L, Nb);
+                uu[t] = static_cast<uint32_t>(Na >> sh) | (static_cast<uint32_t>(Nb >> sh) << 16);
+            }
             for (int bit = 15; bit >= 0; --bit) {
-                const uint32_t cand = Tu | (1u << bit);
+                const uint32_t cand = (Tu | (1u << bit)) << 16;
                 uint32_t cnt = 0;
-                for (uint32_t c = lane; c < p.C32; c += 32u) {
-                    uint64_t N;
-                    rank_key(row[c], s_bc[c], theta, c, L, N);
-                    cnt += static_cast<uint32_t>(N >> sh) >= cand ? 1u : 0u;
-                }
-                if (__reduce_add_sync(0xffffffffu, cnt) >= p.k) Tu = cand;
+#pragma unroll
+                for (int t = 0; t < NU; ++t)
+                    cnt += (uu[t] >= cand ? 1u : 0u) + ((uu[t] << 16) >= cand ? 1u : 0u);
+                if (__reduce_add_sync(0xffffffffu, cnt) >= p.k) Tu |= 1u << bit;
             }
             if (Tu > 0) {
                 // (2) exact: the columns tied at u == Tu, ranked by their exact keys
