@@ -31,6 +31,12 @@ namespace sp {
 
 namespace {
 
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -97,8 +103,9 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, const Transpose
 }
 
 // One elected lane of the (converged) warp adds 1 to a shared counter with acq_rel
-// semantics; returns true on that lane iff the counter was at 31 mod 32 (i.e. this warp
-// is the 32nd to release the stage).
+// semantics; returns true on that lane iff the counter was at NW-1 mod NW (i.e. this warp
+// is the last of the CTA's NW warps to release the stage; NW is a power of two).
+template <uint32_t NW>
 __device__ __forceinline__ bool warp_release_is_last(uint32_t addr) {
     uint32_t last;
     asm volatile(
@@ -108,12 +115,12 @@ __device__ __forceinline__ bool warp_release_is_last(uint32_t addr) {
         "elect.sync _|P1, 0xffffffff;\n"
         "mov.u32 old, 0;\n"
         "@P1 atom.acq_rel.cta.shared::cta.add.u32 old, [%1], 1;\n"
-        "and.b32 old, old, 31;\n"
-        "setp.eq.and.u32 P2, old, 31, P1;\n"
+        "and.b32 old, old, %2;\n"
+        "setp.eq.and.u32 P2, old, %2, P1;\n"
         "selp.u32 %0, 1, 0, P2;\n"
         "}\n"
         : "=r"(last)
-        : "r"(addr)
+        : "r"(addr), "n"(NW - 1)
         : "memory");
     return last != 0;
 }
@@ -123,19 +130,24 @@ __device__ __forceinline__ bool warp_release_is_last(uint32_t addr) {
 // words k < 7 are moved into place with one IMAD.HI (a right shift by a multiply on the
 // FMA pipe) and word 7 with one IMAD, then masked in with a LOP3.
 // Resulting position of pixel 4k+b: k, 7+k, 15+k, 23+k (k < 7); 14, 22, 30, 31 (k = 7).
-__device__ __forceinline__ uint32_t nz_flags(uint32_t v) {
-    return (((v & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | v) & 0x80808080u;
+// `one` is 1 at run time (a kernel parameter): the add becomes an IMAD on the FMA pipe
+// instead of an IADD on the ALU pipe, which is this loop's bottleneck.
+__device__ __forceinline__ uint32_t nz_flags(uint32_t v, uint32_t one) {
+    uint32_t t;
+    asm("mad.lo.u32 %0, %1, %2, 0x7F7F7F7F;" : "=r"(t) : "r"(v & 0x7F7F7F7Fu), "r"(one));
+    return (t | v) & 0x80808080u;
 }
 
-__device__ __forceinline__ uint32_t nonzero_mask32(const uint4 a, const uint4 b) {
+__device__ __forceinline__ uint32_t nonzero_mask32(const uint4 a, const uint4 b, uint32_t one) {
     const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
     uint32_t m = 0;
 #pragma unroll
     for (int k = 0; k < 7; ++k) {
         const uint32_t mk = (1u << (k + 25)) | (1u << (k + 24));
-        m |= __umulhi(nz_flags(v[k]), mk) & ((1u << k) | (1u << (7 + k)) | (1u << (15 + k)) | (1u << (23 + k)));
+        m |= __umulhi(nz_flags(v[k], one), mk) &
+             ((1u << k) | (1u << (7 + k)) | (1u << (15 + k)) | (1u << (23 + k)));
     }
-    m |= (nz_flags(v[7]) * 0x81u) & 0xC0404000u;
+    m |= (nz_flags(v[7], one) * 0x81u) & 0xC0404000u;
     return m;
 }
 
@@ -199,145 +211,19 @@ __device__ __forceinline__ uint64_t rank_key(uint32_t raw, uint32_t bc, uint32_t
 
 }  // namespace
 
-template <int CPT>
-__global__ void __launch_bounds__(kBatchedThreads, 1)
-    sp_batched_kernel(const __grid_constant__ BatchedParams p) {
-    extern __shared__ __align__(1024) uint8_t smem[];
-    const uint32_t tid = threadIdx.x, lane = tid & 31u, wi = tid >> 5;
-    const uint32_t NST = p.stages;
-
-    uint8_t* stage_base = smem;  // 1024-aligned (swizzle-128B boxes)
-    uint16_t* rawbuf = reinterpret_cast<uint16_t*>(stage_base);  // after streaming
-    uint8_t* region = smem + NST * kStageBytes;
-    uint32_t* words = reinterpret_cast<uint32_t*>(region);
-    uint32_t* s_bc = reinterpret_cast<uint32_t*>(region + p.region_bytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(s_bc + p.C32);
-    uint32_t* released = reinterpret_cast<uint32_t*>(bars + NST);  // per-stage release counters
-
-    const uint32_t K = p.K;
-    const uint32_t group = blockIdx.x / K, rank = blockIdx.x % K;
-    const uint32_t in0 = static_cast<uint32_t>(static_cast<uint64_t>(group) * p.num_inputs / p.groups);
-    const uint32_t in1 =
-        static_cast<uint32_t>(static_cast<uint64_t>(group + 1) * p.num_inputs / p.groups);
-    const uint32_t gs = in1 - in0;  // 1..32 inputs in this group
-    const uint32_t w0 = rank * p.nwin / K, w1 = (rank + 1) * p.nwin / K;
-    const uint32_t pix_begin = w0 * p.Lw;
-    const uint32_t pix_end = min(w1 * p.Lw, p.nbits);
-    const uint32_t nchunks = pix_end > pix_begin ? (pix_end - pix_begin + kChunkBits - 1) / kChunkBits : 0;
-
-    // ---- setup ---------------------------------------------------------------------------
-    if (tid == 0 && (smem_addr(smem) & 1023u)) __trap();  // swizzled boxes need 1 KiB alignment
-    if (tid < NST) {
-        mbar_init(&bars[tid], 1);
-        released[tid] = 0u;
-    }
-    for (uint32_t c = tid; c < p.C32; c += kBatchedThreads) s_bc[c] = p.bc[c];
-    if (tid == 0) words[p.Lw] = 0u;  // the zero slot padding / disconnected synapses point to
-    if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncthreads();
-
-    // Producer step for chunk j (one thread): expect the stage's bytes, then 8 TMA boxes of
-    // 128 pixels x 32 inputs (rows beyond the batch and pixels beyond nbits are zero-filled).
-    // Called by thread 0 for the prologue and afterwards by the lane that releases a stage
-    // last, so the ring refills without any CTA-wide barrier.
-    auto issue = [&](uint32_t j, uint32_t st) {
-        const uint32_t x0 = pix_begin + j * kChunkBits;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive_expect_tx(&bars[st], kStageBytes);
-        uint8_t* dst = stage_base + st * kStageBytes;
-#pragma unroll
-        for (uint32_t b = 0; b < kChunkBits / kBoxBytes; ++b)
-            tma_box_g2s(dst + b * 32u * kBoxBytes, &p.tmap, x0 + b * kBoxBytes, in0, &bars[st]);
-    };
-    if (tid == 0) {
-        const uint32_t pre = min(NST, nchunks);
-        for (uint32_t j = 0; j < pre; ++j) issue(j, j);
-    }
-
-    const uint32_t released_addr = smem_addr(released);
-    const TransposeLane tl(lane);
-    const uint32_t lane_ok = lane < gs ? 0xFFFFFFFFu : 0u;
-    const uint32_t out_pixel = wi * 32u + pixel_of_bit(lane);  // word this lane writes per chunk
-    // lane f reads its 32 bytes of block wi from box wi/4, row f, 16-byte slots
-    // 2*(wi%4) and +1, swizzled by XOR with (f % 8) (CU_TENSOR_MAP_SWIZZLE_128B)
-    const uint32_t c0 = 2u * (wi & 3u);
-    const uint32_t rd0 = (wi >> 2) * (32u * kBoxBytes) + lane * kBoxBytes + ((c0 ^ (lane & 7u)) << 4);
-    const uint32_t rd1 = (wi >> 2) * (32u * kBoxBytes) + lane * kBoxBytes + (((c0 + 1u) ^ (lane & 7u)) << 4);
-
-    Planes P[CPT];
-#pragma unroll
-    for (int i = 0; i < CPT; ++i) {
-        P[i].ones = P[i].twos = P[i].fours = 0u;
-#pragma unroll
-        for (int h = 0; h < (int)kHiPlanes; ++h) P[i].hi[h] = 0u;
-    }
-
-    // ---- stream the windows: transpose chunks into X, then gather ----------------------
-    uint32_t j = 0, st = 0, phase = 0;
-    for (uint32_t w = w0; w < w1; ++w) {
-        const uint32_t wbase = w * p.Lw;
-        const uint32_t wlen = min(p.Lw, p.nbits - wbase);
-        const uint32_t nch = (wlen + kChunkBits - 1) / kChunkBits;
-        for (uint32_t q = 0; q < nch; ++q) {
-            mbar_wait(&bars[st], phase);
-            // a1: warp wi turns block wi (32 pixels x 32 inputs) into 32 bit-sliced words
-            {
-                const uint8_t* stg = stage_base + st * kStageBytes;
-                const uint4 a = *reinterpret_cast<const uint4*>(stg + rd0);
-                const uint4 b = *reinterpret_cast<const uint4*>(stg + rd1);
-                const uint32_t m = warp_transpose32(nonzero_mask32(a, b) & lane_ok, tl);
-                words[q * kChunkBits + out_pixel] = m;
-            }
-            // release the stage; the warp that releases it last refills it (chunk j + NST)
-            if (warp_release_is_last(released_addr + 4u * st) && j + NST < nchunks) issue(j + NST, st);
-            ++j;
-            if (++st == NST) {
-                st = 0;
-                phase ^= 1u;
-            }
-        }
-        __syncthreads();  // all words of window w written
-        // a2: bit-sliced gather-count of this window's synapses (ELL, 8 slots per block)
-#pragma unroll
-        for (int i = 0; i < CPT; ++i) {
-            const uint32_t cw = wi + 32u * i;
-            if (cw < p.ncw) {
-                const uint32_t cell = w * p.ncw + cw;
-                const uint32_t nb = p.ell_nb[cell];
-                const uint4* e = p.ell + p.ell_off[cell] + lane;
-#pragma unroll 2
-                for (uint32_t bk = 0; bk < nb; ++bk) {
-                    const uint4 s8 = __ldg(e + bk * 32u);
-                    accumulate8(P[i], words[s8.x & 0xFFFFu], words[s8.x >> 16], words[s8.y & 0xFFFFu],
-                                words[s8.y >> 16], words[s8.z & 0xFFFFu], words[s8.z >> 16],
-                                words[s8.w & 0xFFFFu], words[s8.w >> 16]);
-                }
-            }
-        }
-        __syncthreads();  // before the next window overwrites X
-    }
-
-    // ---- raw counts per input (partial if K > 1) into rawbuf[f][c] ----------------------
-#pragma unroll
-    for (int i = 0; i < CPT; ++i) {
-        const uint32_t cw = wi + 32u * i;
-        if (cw < p.ncw) {
-            const uint32_t c = cw * 32u + lane;
-            for (uint32_t f = 0; f < gs; ++f)
-                rawbuf[f * p.C32 + c] = static_cast<uint16_t>(extract_count(P[i], f));
-        }
-    }
+// a3/a4 for the inputs of this CTA: (cluster-sum of partial counts), exact keys, k-winners,
+// SDR.  Kept out of line so its register needs do not shape the streaming loop's allocation.
+template <int CPT, uint32_t NW>
+__device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawbuf, uint8_t* region,
+                                          const uint32_t* s_bc, uint32_t in0, uint32_t gs,
+                                          uint32_t rank, uint32_t K, uint32_t wi, uint32_t lane) {
     cg::cluster_group cluster = cg::this_cluster();
-    if (K > 1) cluster.sync();
-    else __syncthreads();
-
-    // ---- a3/a4: per input: (cluster-sum), keys, k-winners, SDR ---------------------------
     const uint32_t theta = p.min_overlap, L = p.keyL;
     const uint64_t one = 1ull << 23;
     const uint32_t nbN = p.keyBits - L;             // significant bits of N
     const uint32_t sh = nbN > 16u ? nbN - 16u : 0u;  // coarse key u = N >> sh has <= 16 bits
     uint64_t* tie_list = reinterpret_cast<uint64_t*>(region) + wi * 64u;  // X window is idle now
-    for (uint32_t f = rank + K * wi; f < gs; f += K * 32u) {
+    for (uint32_t f = rank + K * wi; f < gs; f += K * NW) {
         uint16_t* row = rawbuf + f * p.C32;
         if (K > 1) {
             for (uint32_t c = lane; c < p.C32; c += 32u) {
@@ -356,12 +242,80 @@ __global__ void __launch_bounds__(kBatchedThreads, 1)
                     r >= theta ? __fmul_rn(static_cast<float>(r), p.boost[c]) : 0.0f;
             }
         }
+        if (p.radius == 0 && p.uniform_bc) {
+            // Uniform boost: the key order is (raw desc, index asc), so the k-th largest key
+            // is found from a histogram of the eligible raw counts:
+            // r* = largest r with #{raw >= r} >= k; winners = raw > r*, plus the lowest
+            // indices among raw == r* up to k.  Exact; O(C/32 + S/32) per lane.
+            uint32_t* hist = reinterpret_cast<uint32_t*>(region) + wi * 512u;  // u16 pairs
+            const uint32_t hw = (p.S + 2u) / 2u;  // words covering bins 0..S
+            for (uint32_t b = lane; b < hw; b += 32u) hist[b] = 0u;
+            __syncwarp();
+            for (uint32_t c = lane; c < p.C; c += 32u) {
+                const uint32_t r = row[c];
+                if (r >= theta) atomicAdd(&hist[r >> 1], 1u << ((r & 1u) * 16u));
+            }
+            __syncwarp();
+            // each lane owns B consecutive bins; suffix sums over lanes find the crossing
+            const uint32_t B = (p.S + 1u + 31u) / 32u;
+            const uint32_t lo_bin = lane * B;
+            uint32_t mine = 0;
+            for (uint32_t b = 0; b < B; ++b) {
+                const uint32_t r = lo_bin + b;
+                if (r <= p.S) mine += (hist[r >> 1] >> ((r & 1u) * 16u)) & 0xFFFFu;
+            }
+            uint32_t incl = mine;  // suffix sum over lanes >= this lane
+#pragma unroll
+            for (uint32_t d = 1; d < 32u; d <<= 1) {
+                const uint32_t v = __shfl_down_sync(0xffffffffu, incl, d);
+                if (lane + d < 32u) incl += v;
+            }
+            const uint32_t crossing = __ballot_sync(0xffffffffu, incl >= p.k);
+            int rstar = -1;          // -1: fewer than k eligible columns, all of them win
+            uint32_t need = 0;       // winners still to take among raw == r*
+            if (crossing) {
+                const uint32_t L = 31u - __clz(crossing);  // highest lane with incl >= k
+                uint32_t acc = __shfl_sync(0xffffffffu, incl - mine, L);  // bins above lane L
+                if (lane == L) {
+                    for (int b = static_cast<int>(B) - 1; b >= 0; --b) {
+                        const uint32_t r = lo_bin + b;
+                        if (r > p.S) continue;
+                        const uint32_t h = (hist[r >> 1] >> ((r & 1u) * 16u)) & 0xFFFFu;
+                        if (acc + h >= p.k) {
+                            rstar = static_cast<int>(r);
+                            need = p.k - acc;
+                            break;
+                        }
+                        acc += h;
+                    }
+                }
+                rstar = __shfl_sync(0xffffffffu, rstar, L);
+                need = __shfl_sync(0xffffffffu, need, L);
+            }
+            uint32_t total = 0, ties_before = 0;
+            for (uint32_t cw = 0; cw < p.ncw; ++cw) {
+                const uint32_t c = cw * 32u + lane;
+                const uint32_t r = row[c];
+                const bool elig = c < p.C && r >= theta &&
+                                  static_cast<uint64_t>(r) * s_bc[c] > one;  // Alg. 2 floor (R7)
+                const bool tie = elig && static_cast<int>(r) == rstar;
+                const uint32_t tb = __ballot_sync(0xffffffffu, tie);
+                const bool act = elig && (rstar < 0 || static_cast<int>(r) > rstar ||
+                                          (tie && ties_before + __popc(tb & ((1u << lane) - 1u)) < need));
+                ties_before += __popc(tb);
+                const uint32_t word = __ballot_sync(0xffffffffu, act);
+                if (lane == 0) p.sdr[static_cast<size_t>(gin) * p.ncw + cw] = word;
+                total += __popc(word);
+            }
+            if (lane == 0) p.counts[gin] = total;
+            continue;
+        }
         uint32_t Tu = 0;       // k-th largest coarse key
         uint64_t T2 = 0;       // exact key threshold among the columns with u == Tu
         if (p.radius == 0) {
             // (1) coarse: the k-th largest u = N >> sh (16 bits) by bitwise search, over
             //     keys packed two per register (columns 64t+lane and 64t+32+lane)
-            constexpr int NU = 16 * CPT;
+            constexpr int NU = (CPT * NW + 1) / 2;  // column-warps of this CTA, two per register
             uint32_t uu[NU];
 #pragma unroll
             for (int t = 0; t < NU; ++t) {
@@ -447,7 +401,186 @@ __global__ void __launch_bounds__(kBatchedThreads, 1)
         }
         if (lane == 0) p.counts[gin] = total;
     }
+}
+
+// NT threads per CTA (1024: 1 block of 32 pixels per warp per chunk, 64 registers;
+// 512: 2 blocks per warp per chunk, 128 registers); CPT column-warps per warp.
+template <int CPT, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    sp_batched_kernel(const __grid_constant__ BatchedParams p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    constexpr uint32_t NW = NT / 32;        // warps
+    constexpr uint32_t BPW = 32u / NW;      // 32-pixel blocks per warp per chunk
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, wi = tid >> 5;
+    const uint32_t NST = p.stages;
+
+    uint8_t* stage_base = smem;  // 1024-aligned (swizzle-128B boxes)
+    uint16_t* rawbuf = reinterpret_cast<uint16_t*>(stage_base);  // after streaming
+    uint8_t* region = smem + NST * kStageBytes;
+    uint32_t* words = reinterpret_cast<uint32_t*>(region);
+    uint32_t* s_bc = reinterpret_cast<uint32_t*>(region + p.region_bytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_bc + p.C32);
+    uint32_t* released = reinterpret_cast<uint32_t*>(bars + NST);  // per-stage release counters
+
+    const uint32_t K = p.K;
+    const uint32_t group = blockIdx.x / K, rank = blockIdx.x % K;
+    const uint32_t in0 = static_cast<uint32_t>(static_cast<uint64_t>(group) * p.num_inputs / p.groups);
+    const uint32_t in1 =
+        static_cast<uint32_t>(static_cast<uint64_t>(group + 1) * p.num_inputs / p.groups);
+    const uint32_t gs = in1 - in0;  // 1..32 inputs in this group
+    const uint32_t w0 = rank * p.nwin / K, w1 = (rank + 1) * p.nwin / K;
+    const uint32_t pix_begin = w0 * p.Lw;
+    const uint32_t pix_end = min(w1 * p.Lw, p.nbits);
+    const uint32_t nchunks = pix_end > pix_begin ? (pix_end - pix_begin + kChunkBits - 1) / kChunkBits : 0;
+
+    // ---- setup ---------------------------------------------------------------------------
+    uint64_t* trace = p.trace ? p.trace + blockIdx.x * 6u : nullptr;
+    uint64_t t_win = 0, t_gather = 0;  // phase timestamps (dev aid)
+    if (trace && tid == 0) trace[0] = global_ns();
+    if (tid == 0 && (smem_addr(smem) & 1023u)) __trap();  // swizzled boxes need 1 KiB alignment
+    if (tid < NST) {
+        mbar_init(&bars[tid], 1);
+        released[tid] = 0u;
+    }
+    for (uint32_t c = tid; c < p.C32; c += NT) s_bc[c] = p.bc[c];
+    if (tid == 0) {  // the zero slot(s) padding / disconnected synapses point to
+        words[p.Lw] = 0u;
+        if (p.xbufs == 2) words[2u * p.Lw + 1u] = 0u;
+    }
+    if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+
+    // Producer step for chunk j (one thread): expect the stage's bytes, then 8 TMA boxes of
+    // 128 pixels x 32 inputs (rows beyond the batch and pixels beyond nbits are zero-filled).
+    // Called by thread 0 for the prologue and afterwards by the lane that releases a stage
+    // last, so the ring refills without any CTA-wide barrier.
+    auto issue = [&](uint32_t j, uint32_t st) {
+        const uint32_t x0 = pix_begin + j * kChunkBits;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(&bars[st], kStageBytes);
+        uint8_t* dst = stage_base + st * kStageBytes;
+#pragma unroll
+        for (uint32_t b = 0; b < kChunkBits / kBoxBytes; ++b)
+            tma_box_g2s(dst + b * 32u * kBoxBytes, &p.tmap, x0 + b * kBoxBytes, in0, &bars[st]);
+    };
+    if (tid == 0) {
+        const uint32_t pre = min(NST, nchunks);
+        for (uint32_t j = 0; j < pre; ++j) issue(j, j);
+    }
+
+    const uint32_t released_addr = smem_addr(released);
+    const TransposeLane tl(lane);
+    const uint32_t lane_ok = lane < gs ? 0xFFFFFFFFu : 0u;
+    const uint32_t pob = pixel_of_bit(lane);  // pixel of the word this lane writes per block
+    // lane f reads its 32 bytes of block blk from box blk/4, row f, 16-byte slots
+    // 2*(blk%4) and +1, swizzled by XOR with (f % 8) (CU_TENSOR_MAP_SWIZZLE_128B); the
+    // second slot is the first XOR 16 bytes
+    uint32_t rd[BPW];
+#pragma unroll
+    for (uint32_t i = 0; i < BPW; ++i) {
+        const uint32_t blk = wi + NW * i;
+        rd[i] = (blk >> 2) * (32u * kBoxBytes) + lane * kBoxBytes + (((2u * (blk & 3u)) ^ (lane & 7u)) << 4);
+    }
+
+    Planes P[CPT];
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+        P[i].ones = P[i].twos = P[i].fours = 0u;
+#pragma unroll
+        for (int h = 0; h < (int)kHiPlanes; ++h) P[i].hi[h] = 0u;
+    }
+
+    // ---- stream the windows: transpose chunks into X, then gather ----------------------
+    // With two X buffers (p.xbufs == 2) window w+1 is transposed into the other buffer
+    // while slower warps still gather window w: one CTA barrier per window.
+    uint32_t j = 0, st = 0, phase = 0;
+    for (uint32_t w = w0; w < w1; ++w) {
+        uint32_t* X = words + (p.xbufs == 2 ? (w & 1u) * (p.Lw + 1u) : 0u);
+        const uint32_t wbase = w * p.Lw;
+        const uint32_t wlen = min(p.Lw, p.nbits - wbase);
+        const uint32_t nch = (wlen + kChunkBits - 1) / kChunkBits;
+        for (uint32_t q = 0; q < nch; ++q) {
+            mbar_wait(&bars[st], phase);
+            // a1: warp wi turns blocks wi, wi+NW, .. (32 pixels x 32 inputs each) into 32
+            // bit-sliced words per block
+            {
+                const uint8_t* stg = stage_base + st * kStageBytes;
+                uint32_t m[BPW];
+#pragma unroll
+                for (uint32_t i = 0; i < BPW; ++i) {
+                    const uint4 a = *reinterpret_cast<const uint4*>(stg + rd[i]);
+                    const uint4 b = *reinterpret_cast<const uint4*>(stg + (rd[i] ^ 16u));
+                    m[i] = nonzero_mask32(a, b, p.one) & lane_ok;
+                }
+#pragma unroll
+                for (uint32_t i = 0; i < BPW; ++i)
+                    X[q * kChunkBits + (wi + NW * i) * 32u + pob] = warp_transpose32(m[i], tl);
+            }
+            // release the stage; the warp that releases it last refills it (chunk j + NST)
+            if (warp_release_is_last<NW>(released_addr + 4u * st) && j + NST < nchunks)
+                issue(j + NST, st);
+            ++j;
+            if (++st == NST) {
+                st = 0;
+                phase ^= 1u;
+            }
+        }
+        const uint64_t tb = trace ? global_ns() : 0;
+        __syncthreads();  // all words of window w written (and, double-buffered, all gathers
+                          // of window w-1 finished, so its buffer may be overwritten next)
+        // a2: bit-sliced gather-count of this window's synapses (ELL, 8 slots per block)
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) {
+            const uint32_t cw = wi + NW * i;
+            if (cw < p.ncw) {
+                const uint32_t cell = w * p.ncw + cw;
+                const uint32_t nb = p.ell_nb[cell];
+                const uint4* e = p.ell + p.ell_off[cell] + lane;
+#pragma unroll 2
+                for (uint32_t bk = 0; bk < nb; ++bk) {
+                    const uint4 s8 = __ldg(e + bk * 32u);
+                    accumulate8(P[i], X[s8.x & 0xFFFFu], X[s8.x >> 16], X[s8.y & 0xFFFFu],
+                                X[s8.y >> 16], X[s8.z & 0xFFFFu], X[s8.z >> 16],
+                                X[s8.w & 0xFFFFu], X[s8.w >> 16]);
+                }
+            }
+        }
+        if (p.xbufs == 1) __syncthreads();  // before the next window overwrites X
+        if (trace) {
+            const uint64_t te = global_ns();
+            t_win += te - tb;
+        }
+    }
+
+    if (trace) {
+        __syncthreads();
+        if (tid == 0) {
+            trace[1] = global_ns();
+            trace[4] = t_win;
+            trace[5] = w1 - w0;
+        }
+    }
+    // ---- raw counts per input (partial if K > 1) into rawbuf[f][c] ----------------------
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+        const uint32_t cw = wi + NW * i;
+        if (cw < p.ncw) {
+            const uint32_t c = cw * 32u + lane;
+            for (uint32_t f = 0; f < gs; ++f)
+                rawbuf[f * p.C32 + c] = static_cast<uint16_t>(extract_count(P[i], f));
+        }
+    }
+    cg::cluster_group cluster = cg::this_cluster();
+    if (K > 1) cluster.sync();
+    else __syncthreads();
+    if (trace && tid == 0) trace[2] = global_ns();
+
+    batched_topk<CPT, NW>(p, rawbuf, region, s_bc, in0, gs, rank, K, wi, lane);
     if (K > 1) cluster.sync();  // peers may still read this CTA's partial counts
+    if (trace) {
+        __syncthreads();
+        if (tid == 0) trace[3] = global_ns();
+    }
 }
 
 template <typename F>
@@ -460,16 +593,19 @@ static cudaError_t allow_dynamic_smem(F* fn, int max_smem) {
 }
 
 cudaError_t configure_batched(int max_smem) {
-    cudaError_t e = allow_dynamic_smem(sp_batched_kernel<1>, max_smem);
-    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2>, max_smem);
+    cudaError_t e = allow_dynamic_smem(sp_batched_kernel<1, 1024>, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2, 1024>, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2, 512>, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<4, 512>, max_smem);
     return e;
 }
 
 cudaError_t launch_batched(const BatchedParams& p, uint32_t smem_bytes, cudaStream_t s) {
-    const int cpt = static_cast<int>((p.ncw + 31u) / 32u);
+    const uint32_t nt = p.threads == 512 ? 512u : 1024u;
+    const uint32_t cpt = (p.ncw + nt / 32u - 1u) / (nt / 32u);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.groups * p.K);
-    cfg.blockDim = dim3(kBatchedThreads);
+    cfg.blockDim = dim3(nt);
     cfg.dynamicSmemBytes = smem_bytes;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -479,8 +615,11 @@ cudaError_t launch_batched(const BatchedParams& p, uint32_t smem_bytes, cudaStre
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cpt <= 1 ? cudaLaunchKernelEx(&cfg, sp_batched_kernel<1>, p)
-                    : cudaLaunchKernelEx(&cfg, sp_batched_kernel<2>, p);
+    if (nt == 512)
+        return cpt <= 2 ? cudaLaunchKernelEx(&cfg, sp_batched_kernel<2, 512>, p)
+                        : cudaLaunchKernelEx(&cfg, sp_batched_kernel<4, 512>, p);
+    return cpt <= 1 ? cudaLaunchKernelEx(&cfg, sp_batched_kernel<1, 1024>, p)
+                    : cudaLaunchKernelEx(&cfg, sp_batched_kernel<2, 1024>, p);
 }
 
 // Maximum co-resident clusters for K = 1..8 at this smem size (index K).
@@ -490,7 +629,7 @@ cudaError_t batched_max_clusters(uint32_t smem_bytes, int max_clusters[9]) {
     for (int K = 1; K <= 8; ++K) {
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(K * 64);
-        cfg.blockDim = dim3(kBatchedThreads);
+        cfg.blockDim = dim3(1024);
         cfg.dynamicSmemBytes = smem_bytes;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -500,7 +639,7 @@ cudaError_t batched_max_clusters(uint32_t smem_bytes, int max_clusters[9]) {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int n = 0;
-        e = cudaOccupancyMaxActiveClusters(&n, sp_batched_kernel<1>, &cfg);
+        e = cudaOccupancyMaxActiveClusters(&n, sp_batched_kernel<1, 1024>, &cfg);
         if (e != cudaSuccess) {
             (void)cudaGetLastError();
             n = 0;

@@ -154,29 +154,47 @@ BatchedLayout plan_batched_layout(const Geometry& g, int max_smem) {
     const uint32_t counts_bytes = 32u * g.C32 * 2u;
     const uint32_t fixed = g.C32 * 4u + 128u;  // Bc + barriers + release counters
     const uint32_t nbits_r = (g.nbits + kChunkBits - 1) / kChunkBits * kChunkBits;
-    const char* es = std::getenv("SP_STAGES");  // development override (experiments only)
+    const char* es = std::getenv("SP_STAGES");  // development overrides (experiments only)
+    const char* eb = std::getenv("SP_XBUFS");
     const uint32_t want_stages = es ? static_cast<uint32_t>(std::atoi(es)) : 0u;
-    for (uint32_t stages = 4; stages >= 2; --stages) {
-        if (want_stages && stages != want_stages) continue;
+    const uint32_t want_xbufs = eb ? static_cast<uint32_t>(std::atoi(eb)) : 0u;
+    // preference (measured on B200, 4096 x 960x540, C=1024, 512 threads): one X window,
+    // 4 stages 0.402 ms, 3 stages 0.405 ms; (1024 threads, 3 stages) double-buffered X
+    // 0.467 vs 0.435 ms -- halving Lw costs more (windows, ELL padding) than the barrier.
+    const uint32_t options[6][2] = {{4, 1}, {3, 1}, {2, 1}, {4, 2}, {3, 2}, {2, 2}};
+    for (const auto& o : options) {
+        const uint32_t stages = o[0], xbufs = o[1];
+        if ((want_stages && stages != want_stages) || (want_xbufs && xbufs != want_xbufs)) continue;
         if (stages * kStageBytes < counts_bytes) continue;
         const int64_t avail = static_cast<int64_t>(max_smem) - stages * kStageBytes - fixed;
-        if (avail < 4 * static_cast<int64_t>(kChunkBits + 1)) continue;
-        // largest Lw (multiple of the chunk, local idx < 65536) with (Lw+1)*4 <= avail
-        uint32_t Lw = static_cast<uint32_t>((avail / 4 - 1) / kChunkBits * kChunkBits);
+        if (avail < 8 * static_cast<int64_t>(kChunkBits + 1)) continue;
+        // largest Lw (multiple of the chunk, local idx < 65536) with xbufs*(Lw+1)*4 <= avail
+        uint32_t Lw = static_cast<uint32_t>((avail / 4 / xbufs - 1) / kChunkBits * kChunkBits);
         Lw = std::min<uint32_t>(Lw, 64512u);
         Lw = std::min<uint32_t>(Lw, nbits_r);
         if (Lw == 0) continue;
+        // one buffer is pointless when a single window covers the input
+        if (xbufs == 2 && Lw >= g.nbits && !want_xbufs) continue;
+        // large inputs need windows of >= 8 chunks or the per-window barriers dominate
+        if (Lw < 8 * kChunkBits && nbits_r > Lw) continue;
         // balance the windows: same count, smallest Lw (multiple of the chunk) covering nbits
         const uint32_t nwin = (g.nbits + Lw - 1) / Lw;
         const uint32_t per = (g.nbits + nwin - 1) / nwin;
         Lw = (per + kChunkBits - 1) / kChunkBits * kChunkBits;
         L.ok = true;
         L.stages = stages;
+        L.xbufs = xbufs;
         L.Lw = Lw;
         L.nwin = (g.nbits + Lw - 1) / Lw;
-        // the window doubles as the per-warp tie lists (32 warps x 64 keys) of the top-k
-        L.region_bytes = (std::max((Lw + 1) * 4u, 32u * 64u * 8u) + 127u) & ~127u;
+        // the window(s) double as the per-warp tie lists (32 warps x 64 keys) or raw-count
+        // histograms (32 warps x (S+2)/2 words, stride 512) of the top-k
+        const uint32_t topk_bytes = std::max(32u * 64u * 8u, 32u * 512u * 4u);
+        L.region_bytes = (std::max(xbufs * (Lw + 1u) * 4u, topk_bytes) + 127u) & ~127u;
         L.smem_bytes = stages * kStageBytes + L.region_bytes + g.C32 * 4u + stages * 12u;
+        if (static_cast<int64_t>(L.smem_bytes) > max_smem) {
+            L.ok = false;
+            continue;
+        }
         return L;
     }
     return L;
@@ -253,6 +271,9 @@ struct sp_handle {
     uint32_t* d_ell_pos = nullptr;
     uint32_t ell_slots = 0;
     bool ell_dirty = false;
+    uint64_t* d_trace = nullptr;  // SP_TRACE=1: per-CTA phase timestamps of the batched kernel
+    bool uniform_bc = true;       // all boosts equal (enables the histogram top-k)
+    uint32_t batched_threads = 512;  // threads per CTA of the batched kernel
     // scratch and results
     uint32_t Wn = 0, sub_inputs = 0;
     uint32_t* d_bits = nullptr;
@@ -285,7 +306,7 @@ cudaError_t dalloc(T** p, size_t count) {
 void release(sp_handle* h) {
     if (!h) return;
     cudaSetDevice(h->device);
-    void* ptrs[] = {h->d_idx,  h->d_perm,    h->d_boost,   h->d_bc,      h->d_syn,
+    void* ptrs[] = {h->d_trace, h->d_idx,  h->d_perm,    h->d_boost,   h->d_bc,      h->d_syn,
                     h->d_ell,  h->d_ell_off, h->d_ell_nb,  h->d_ell_pos, h->d_bits,
                     h->d_raw,  h->d_sdr,     h->d_counts,  h->d_raw_rec, h->d_boosted_rec,
                     h->d_stage[0], h->d_stage[1]};
@@ -406,6 +427,8 @@ sp_status upload_state(sp_handle* h, const uint32_t* idx, const float* perm, con
         boost32[c] = boost[c];
         bc[c] = static_cast<uint32_t>(boost[c] * 8388608.0f);  // exact: boost in [1,16) (R4)
     }
+    h->uniform_bc = std::all_of(bc.begin(), bc.begin() + g.C, [&](uint32_t v) { return v == bc[0]; });
+    if (std::getenv("SP_NO_UNIFORM_TOPK")) h->uniform_bc = false;  // development override
     cudaError_t e = cudaMemcpy(h->d_idx, idx, cs * 4u, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(h->d_perm, perm, cs * 4u, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(h->d_boost, boost32.data(), g.C32 * 4u, cudaMemcpyHostToDevice);
@@ -466,6 +489,12 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         p.nwin = h->lay.nwin;
         p.stages = h->lay.stages;
         p.region_bytes = h->lay.region_bytes;
+        p.xbufs = h->lay.xbufs;
+        p.one = 1u;
+        p.S = g.S;
+        p.uniform_bc = h->uniform_bc ? 1u : 0u;
+        p.threads = h->batched_threads;
+        p.trace = h->d_trace;
         p.groups = pl.groups;
         p.K = pl.cluster;
         p.ell_off = h->d_ell_off;
@@ -617,6 +646,8 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
         return cuda_fail(e, "kernel attributes");
     }
     if (h->lay.ok) sp::batched_max_clusters(h->lay.smem_bytes, h->max_clusters);
+    if (std::getenv("SP_TRACE")) cudaMalloc(&h->d_trace, 4096u * 6u * sizeof(uint64_t));
+    if (const char* et = std::getenv("SP_THREADS")) h->batched_threads = std::atoi(et) == 1024 ? 1024u : 512u;
     h->Wn = (g.nbits + 31u) / 32u;
     h->sub_inputs = std::max<uint32_t>(sp::kPerInputChunk, g.P);
     const size_t cs = static_cast<size_t>(g.C) * g.S;
@@ -828,3 +859,13 @@ sp_status sp_get_info(sp_handle* h, sp_info* out) {
 }
 
 }  // extern "C"
+
+// Development aid (not in include/sp.h): copies the batched kernel's per-CTA phase
+// timestamps (SP_TRACE=1 at create) to host memory, uint64[ctas][6].
+extern "C" sp_status sp_debug_trace(sp_handle* h, uint64_t* out, uint32_t ctas) {
+    if (!h || !h->d_trace || !out) return SP_E_STATE;
+    cudaDeviceSynchronize();
+    return cudaMemcpy(out, h->d_trace, ctas * 6u * sizeof(uint64_t), cudaMemcpyDeviceToHost) == cudaSuccess
+               ? SP_OK
+               : SP_E_CUDA;
+}

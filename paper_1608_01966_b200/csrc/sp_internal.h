@@ -12,7 +12,6 @@ namespace sp {
 constexpr uint32_t kChunkBits = 1024;      // Lc: pixels per input per pipeline stage
 constexpr uint32_t kBoxBytes = 128;        // TMA box: 128 B (pixels) x 32 rows (inputs), swizzle 128B
 constexpr uint32_t kStageBytes = 32u * kChunkBits;  // 8 boxes = 32 KiB per stage
-constexpr uint32_t kBatchedThreads = 1024; // 32 warps: warp w transposes block w of a chunk
 constexpr uint32_t kMaxBatchedColumns = 2048;
 constexpr uint32_t kMaxBatchedSynapses = 1023;  // 10 vertical-counter planes
 constexpr uint32_t kHiPlanes = 7;          // planes of weight 8..512 (ones/twos/fours separate)
@@ -44,7 +43,7 @@ struct Geometry {
 // Layout of the batched (bit-sliced) path, fixed at create time (depends on C, S, nbits).
 struct BatchedLayout {
     bool ok = false;
-    uint32_t stages = 0, Lw = 0, nwin = 0;
+    uint32_t stages = 0, xbufs = 0, Lw = 0, nwin = 0;
     uint32_t region_bytes = 0, smem_bytes = 0;
 };
 
@@ -54,7 +53,12 @@ struct alignas(64) BatchedParams {
     uint32_t C, C32, ncw;
     uint32_t min_overlap, k, radius;
     uint32_t keyL, keyBits;
-    uint32_t Lw, nwin, stages, region_bytes;
+    uint32_t Lw, nwin, stages, region_bytes, xbufs;
+    uint32_t one;              // always 1 (opaque to the compiler; see nz_flags)
+    uint32_t S;                // synapses per column (histogram range of the fast top-k)
+    uint32_t uniform_bc;       // all boosts equal: key order = (raw desc, index asc)
+    uint32_t threads;          // 1024 or 512 threads per CTA
+    uint64_t* trace;           // nullable [ctas][4] phase timestamps (development aid)
     uint32_t groups, K;
     const uint32_t* ell_off;   // [nwin][ncw] offset in uint4 units
     const uint16_t* ell_nb;    // [nwin][ncw] number of 8-slot blocks

@@ -133,11 +133,22 @@ SMALL = [
 ]
 
 
+def with_boost(state, mode):
+    """Seeded per-column boosts, or one uniform boost (the batched kernel's histogram top-k)."""
+    idx, perm, boost = state
+    if mode == "uniform1":
+        boost = np.ones_like(boost)
+    elif mode == "uniform1.5":
+        boost = np.full_like(boost, np.float32(1.5))
+    return idx, perm, boost
+
+
+@pytest.mark.parametrize("boost_mode", ["seeded", "uniform1", "uniform1.5"])
 @pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("kw", SMALL)
-def test_inference_parity_small(kw, path):
+def test_inference_parity_small(kw, path, boost_mode):
     cfg = ocfg(**kw)
-    state = perturbed_state(cfg)
+    state = with_boost(perturbed_state(cfg), boost_mode)
     nframes = 45  # > 32: two groups, the last one ragged
     frames = sp_inputs.frames(2002, 0, nframes, cfg.input_height, cfg.input_width, rho=0.5,
                               nonzero="random")
@@ -149,13 +160,14 @@ def test_inference_parity_small(kw, path):
     check_results(results, *out)
 
 
+@pytest.mark.parametrize("boost_mode", ["seeded", "uniform1"])
 @pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("rho", [0.0, 1.0, 0.05])
-def test_inference_degenerate_frames(path, rho):
+def test_inference_degenerate_frames(path, rho, boost_mode):
     # all-zero frames -> no winners; all-one frames; sparse frames (theta zeros)
     cfg = ocfg(input_width=64, input_height=32, num_columns=256, synapses_per_column=32,
                min_overlap=4, winners_set_size=10)
-    state = perturbed_state(cfg)
+    state = with_boost(perturbed_state(cfg), boost_mode)
     frames = sp_inputs.frames(9, 0, 33, 32, 64, rho=rho)
     ora = O.SpatialPoolerOracle(cfg, state)
     results = [ora.step(x, False) for x in O.encode(frames, cfg)]
@@ -217,10 +229,11 @@ def test_full_size_learning_then_inference():
     check_results(res2, *run_gpu(sp, test))
 
 
+@pytest.mark.parametrize("boost_mode", ["seeded", "uniform1"])
 @pytest.mark.parametrize("radius", [0, 80])
-def test_full_size_inference_parity(radius):
+def test_full_size_inference_parity(radius, boost_mode):
     cfg = headline_cfg(inhibition_radius=radius)
-    state = perturbed_state(cfg)
+    state = with_boost(perturbed_state(cfg), boost_mode)
     frames = sp_inputs.frames(2002, 0, 36, 540, 960, rho=0.5)
     ora = O.SpatialPoolerOracle(cfg, state)
     results = [ora.step(x, False) for x in O.encode(frames, cfg)]
