@@ -119,6 +119,9 @@ typedef struct sp_info {
     uint32_t ell_slots;          /* batched layout size in uint16 slots (0 if none) */
     int32_t sm_count;            /* device SMs */
     int32_t max_smem_optin;      /* device max dynamic smem per block */
+    uint32_t learn_cluster;      /* CTAs per cluster of the resident learning kernel (0: learning
+                                    uses the per-input kernels) */
+    uint32_t last_learn_cluster; /* 1 if the last learn=1 call used the cluster kernel */
 } sp_info;
 
 /* Fills *cfg with Tab. 2 defaults on a 240x134 frame (Tab. 1),

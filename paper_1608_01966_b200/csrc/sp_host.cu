@@ -274,6 +274,8 @@ struct sp_handle {
     uint64_t* d_trace = nullptr;  // SP_TRACE=1: per-CTA phase timestamps of the batched kernel
     bool uniform_bc = true;       // all boosts equal (enables the histogram top-k)
     uint32_t batched_threads = 512;  // threads per CTA of the batched kernel
+    uint32_t learn_Q = 0, learn_smem = 0;  // cluster learning: CTAs per cluster (0 = not eligible)
+    bool last_learn_cluster = false;
     // scratch and results
     uint32_t Wn = 0, sub_inputs = 0;
     uint32_t* d_bits = nullptr;
@@ -511,6 +513,42 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         if (e != cudaSuccess) return cuda_fail(e, "batched kernel launch");
         return SP_OK;
     }
+    if (learn && h->learn_Q && h->cfg.force_path != SP_PATH_PER_INPUT) {
+        // the whole sequential stream in one launch of the cluster-resident kernel
+        sp::LearnParams q{};
+        q.frames = frames;
+        q.first_input = row0;
+        q.num_inputs = n;
+        q.g = g;
+        q.Q = h->learn_Q;
+        sp::learn_cluster_smem(g, q.Q, &q.cols_per_cta);
+        q.Wn = h->Wn;
+        q.min_overlap = h->cfg.min_overlap;
+        q.k = h->cfg.winners_set_size;
+        q.radius = h->cfg.inhibition_radius;
+        q.uniform_bc = h->uniform_bc ? 1u : 0u;
+        q.inc = h->cfg.perm_increment;
+        q.dec = h->cfg.perm_decrement;
+        q.tau = h->cfg.connected_threshold;
+        q.idx = h->d_idx;
+        q.perm = h->d_perm;
+        q.syn = h->d_syn;
+        q.bc = h->d_bc;
+        q.boost = h->d_boost;
+        q.bits_g = h->d_bits;
+        q.sdr = h->d_sdr;
+        q.counts = h->d_counts;
+        q.raw_out = rec ? h->d_raw_rec : nullptr;
+        q.boosted_out = rec ? h->d_boosted_rec : nullptr;
+        e = sp::launch_learn_cluster(q, h->learn_smem, s);
+        h->launches++;
+        if (e != cudaSuccess) return cuda_fail(e, "cluster learning launch");
+        h->ell_dirty = true;
+        h->last_plan.path = SP_PATH_PER_INPUT;
+        h->last_learn_cluster = true;
+        return SP_OK;
+    }
+    if (learn) h->last_learn_cluster = false;
     // per-input path, sub-batches of whole frames
     const uint32_t fpb = std::max<uint32_t>(1u, h->sub_inputs / g.P);
     for (uint32_t f0 = 0; f0 < n_frames; f0 += fpb) {
@@ -646,6 +684,21 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
         return cuda_fail(e, "kernel attributes");
     }
     if (h->lay.ok) sp::batched_max_clusters(h->lay.smem_bytes, h->max_clusters);
+    // cluster-resident learning: the largest cluster (<= 16 CTAs, >= 32 columns each) whose
+    // synapse slice + bit-plane fit in shared memory and that can be co-scheduled
+    if (sp::configure_learn(h->max_smem) == cudaSuccess && !std::getenv("SP_NO_CLUSTER_LEARN")) {
+        for (uint32_t Q = 16; Q >= 1; Q /= 2) {
+            if (Q > 1 && Q * 32u > h->g.C32) continue;
+            const uint32_t smem = sp::learn_cluster_smem(h->g, Q, nullptr);
+            if (static_cast<int>(smem) > h->max_smem - 1024) continue;
+            int n = 0;
+            sp::learn_max_clusters(Q, smem, &n);
+            if (n < 1) continue;
+            h->learn_Q = Q;
+            h->learn_smem = smem;
+            break;
+        }
+    }
     if (std::getenv("SP_TRACE")) cudaMalloc(&h->d_trace, 4096u * 6u * sizeof(uint64_t));
     if (const char* et = std::getenv("SP_THREADS")) h->batched_threads = std::atoi(et) == 1024 ? 1024u : 512u;
     h->Wn = (g.nbits + 31u) / 32u;
@@ -855,6 +908,8 @@ sp_status sp_get_info(sp_handle* h, sp_info* out) {
     out->ell_slots = h->ell_slots;
     out->sm_count = h->sm_count;
     out->max_smem_optin = h->max_smem;
+    out->learn_cluster = h->learn_Q;
+    out->last_learn_cluster = h->last_learn_cluster ? 1u : 0u;
     return SP_OK;
 }
 

@@ -93,6 +93,32 @@ struct PerInputParams {
     float* boosted_out;        // nullable [call inputs][C]
 };
 
+struct LearnParams {
+    const uint8_t* frames;     // frames of the call
+    uint32_t first_input;      // row of the first input in the result buffers
+    uint32_t num_inputs;       // inputs (frames x patches), processed in order
+    Geometry g;
+    uint32_t Q, cols_per_cta, Wn;
+    uint32_t min_overlap, k, radius, uniform_bc;
+    float inc, dec, tau;
+    const uint32_t* idx;       // [C][S]
+    float* perm;               // [C][S]
+    uint32_t* syn;             // [S][C32] idx | connected << 31 (loaded, written back)
+    const uint32_t* bc;        // [C32]
+    const float* boost;        // [C32]
+    uint32_t* bits_g;          // [Wn] scratch bit-plane (L2)
+    uint32_t* sdr;             // [rows][ncw]
+    uint32_t* counts;          // [rows]
+    uint16_t* raw_out;         // nullable
+    float* boosted_out;        // nullable
+};
+
+// cluster learning (sp_learn.cu)
+uint32_t learn_cluster_smem(const Geometry& g, uint32_t Q, uint32_t* cols_per_cta);
+cudaError_t configure_learn(int max_smem);
+cudaError_t learn_max_clusters(uint32_t Q, uint32_t smem, int* n);
+cudaError_t launch_learn_cluster(const LearnParams& p, uint32_t smem, cudaStream_t s);
+
 // host planning (sp_host.cu)
 Geometry make_geometry(const sp_config& cfg);
 BatchedLayout plan_batched_layout(const Geometry& g, int max_smem);

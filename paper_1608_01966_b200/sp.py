@@ -66,7 +66,8 @@ class SpPlanInfo(ctypes.Structure):
 class SpInfo(ctypes.Structure):
     _fields_ = [("plan", SpPlanInfo), ("kernel_launches", ctypes.c_uint64),
                 ("last_num_inputs", ctypes.c_uint32), ("ell_slots", ctypes.c_uint32),
-                ("sm_count", ctypes.c_int32), ("max_smem_optin", ctypes.c_int32)]
+                ("sm_count", ctypes.c_int32), ("max_smem_optin", ctypes.c_int32),
+                ("learn_cluster", ctypes.c_uint32), ("last_learn_cluster", ctypes.c_uint32)]
 
 
 _lib = None

@@ -95,15 +95,20 @@ def test_set_state_rejects_out_of_domain():
 # --------------------------------------------------------------------------- #
 # BASELINE config 1: tiny SP, 10 frames with learning (sequential recurrence)
 # --------------------------------------------------------------------------- #
+LEARN_PATHS = [P.SP_PATH_AUTO, P.SP_PATH_PER_INPUT]  # AUTO = cluster-resident learning kernel
+
+
+@pytest.mark.parametrize("boost_mode", ["seeded", "uniform1"])
+@pytest.mark.parametrize("path", LEARN_PATHS)
 @pytest.mark.parametrize("radius", [0, 4])
-def test_tiny_learning_bit_exact(radius):
+def test_tiny_learning_bit_exact(radius, path, boost_mode):
     cfg = ocfg(inhibition_radius=radius)
     idx, perm, _ = O.init_pools(cfg)
-    state = (idx, perm, sp_inputs.boosts(7, cfg.num_columns))
+    state = with_boost((idx, perm, sp_inputs.boosts(7, cfg.num_columns)), boost_mode)
     frames = sp_inputs.frames(1001, 0, 10, 8, 8, rho=0.5)
     ora = O.SpatialPoolerOracle(cfg, state)
     results = ora.compute(frames, learning=True)
-    sp = make_sp(cfg, state)
+    sp = make_sp(cfg, state, path)
     sdr, counts, raw, boosted = run_gpu(sp, frames, learn=True)
     check_results(results, sdr, counts, raw, boosted)
     _, gperm, _ = sp.get_state()
@@ -177,6 +182,35 @@ def test_inference_degenerate_frames(path, rho, boost_mode):
         assert out[1].sum() == 0
 
 
+LEARN_SMALL = [
+    dict(input_width=48, input_height=37, num_columns=100, synapses_per_column=20,
+         min_overlap=3, winners_set_size=7),
+    dict(input_width=48, input_height=37, num_columns=100, synapses_per_column=20,
+         min_overlap=0, winners_set_size=100, inhibition_radius=2),
+    dict(input_width=240, input_height=134, num_columns=2048, synapses_per_column=128,
+         min_overlap=8, winners_set_size=40, inhibition_radius=80),
+    dict(input_width=64, input_height=60, patch_width=32, patch_height=30, num_columns=256,
+         synapses_per_column=64, min_overlap=2, winners_set_size=10),
+]
+
+
+@pytest.mark.parametrize("boost_mode", ["seeded", "uniform1.5"])
+@pytest.mark.parametrize("path", LEARN_PATHS)
+@pytest.mark.parametrize("kw", LEARN_SMALL)
+def test_learning_parity_small(kw, path, boost_mode):
+    cfg = ocfg(**kw)
+    state = with_boost(perturbed_state(cfg), boost_mode)
+    frames = sp_inputs.frames(1001, 0, 6, cfg.input_height, cfg.input_width, rho=0.5,
+                              nonzero="random")
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = ora.compute(frames, learning=True)
+    sp = make_sp(cfg, state, path, max_inputs=64)
+    check_results(results, *run_gpu(sp, frames, learn=True))
+    assert sp.info()["last_learn_cluster"] == (1 if path == P.SP_PATH_AUTO else 0)
+    _, gperm, _ = sp.get_state()
+    assert np.array_equal(gperm.view(np.uint32), ora.perm.view(np.uint32))
+
+
 def test_zero_frames_is_noop():
     sp = make_sp(ocfg())
     sp.compute(torch.empty((0, 8, 8), dtype=torch.uint8, device=DEV))
@@ -213,15 +247,18 @@ def headline_cfg(**kw):
     return ocfg(**base)
 
 
-def test_full_size_learning_then_inference():
+@pytest.mark.parametrize("boost_mode", ["seeded", "uniform1"])
+@pytest.mark.parametrize("path", LEARN_PATHS)
+def test_full_size_learning_then_inference(path, boost_mode):
     cfg = headline_cfg()
     idx, perm, _ = O.init_pools(cfg)
-    state = (idx, perm, sp_inputs.boosts(7, cfg.num_columns))
+    state = with_boost((idx, perm, sp_inputs.boosts(7, cfg.num_columns)), boost_mode)
     frames = sp_inputs.frames(1001, 0, 12, 540, 960, rho=0.5)
     ora = O.SpatialPoolerOracle(cfg, state)
     results = ora.compute(frames, learning=True)
-    sp = make_sp(cfg, state, max_inputs=64)
+    sp = make_sp(cfg, state, path, max_inputs=64)
     check_results(results, *run_gpu(sp, frames, learn=True))
+    assert sp.info()["last_learn_cluster"] == (1 if path == P.SP_PATH_AUTO else 0)
     _, gperm, _ = sp.get_state()
     assert np.array_equal(gperm.view(np.uint32), ora.perm.view(np.uint32))
     test = sp_inputs.frames(2002, 0, 40, 540, 960, rho=0.5)
