@@ -522,6 +522,8 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         q.g = g;
         q.Q = h->learn_Q;
         sp::learn_cluster_smem(g, q.Q, &q.cols_per_cta);
+        q.syn_stride = sp::learn_syn_stride(g.S);
+        q.tpc = sp::learn_threads_per_column(q.cols_per_cta);
         q.Wn = h->Wn;
         q.min_overlap = h->cfg.min_overlap;
         q.k = h->cfg.winners_set_size;

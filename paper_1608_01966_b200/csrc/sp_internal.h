@@ -99,6 +99,8 @@ struct LearnParams {
     uint32_t num_inputs;       // inputs (frames x patches), processed in order
     Geometry g;
     uint32_t Q, cols_per_cta, Wn;
+    uint32_t syn_stride;       // padded column-major stride of the resident synapse slice
+    uint32_t tpc;              // threads per column in the overlap
     uint32_t min_overlap, k, radius, uniform_bc;
     float inc, dec, tau;
     const uint32_t* idx;       // [C][S]
@@ -115,6 +117,8 @@ struct LearnParams {
 
 // cluster learning (sp_learn.cu)
 uint32_t learn_cluster_smem(const Geometry& g, uint32_t Q, uint32_t* cols_per_cta);
+uint32_t learn_syn_stride(uint32_t S);
+uint32_t learn_threads_per_column(uint32_t cpc);
 cudaError_t configure_learn(int max_smem);
 cudaError_t learn_max_clusters(uint32_t Q, uint32_t smem, int* n);
 cudaError_t launch_learn_cluster(const LearnParams& p, uint32_t smem, cudaStream_t s);

@@ -59,8 +59,9 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
     const uint32_t c0 = q * cpc;                 // first column owned
     const uint32_t Wn = p.Wn;
 
-    uint32_t* s_syn = reinterpret_cast<uint32_t*>(smem);           // [S][cpc] idx | connected<<31
-    uint32_t* s_bits = s_syn + static_cast<size_t>(g.S) * cpc;     // [Wn] input bit-plane
+    const uint32_t ss = p.syn_stride;                               // >= S, == 8 mod 32
+    uint32_t* s_syn = reinterpret_cast<uint32_t*>(smem);           // [cpc][ss] idx | connected<<31
+    uint32_t* s_bits = s_syn + static_cast<size_t>(ss) * cpc;      // [Wn] input bit-plane
     uint32_t* s_bc = s_bits + Wn;                                   // [C32]
     uint16_t* s_raw = reinterpret_cast<uint16_t*>(s_bc + g.C32);    // [C32] all columns' raw
     uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_raw + g.C32 + (g.C32 & 1u));  // [S+1]
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
     // ---- resident state: this CTA's synapse slice, Bc -----------------------------------
     for (uint32_t i = tid; i < g.S * cpc; i += nthr) {
         const uint32_t s = i / cpc, cl = i % cpc, c = c0 + cl;
-        s_syn[i] = c < g.C32 ? p.syn[static_cast<size_t>(s) * g.C32 + c] : 0u;
+        s_syn[cl * ss + s] = c < g.C32 ? p.syn[static_cast<size_t>(s) * g.C32 + c] : 0u;
     }
     for (uint32_t c = tid; c < g.C32; c += nthr) s_bc[c] = p.bc[c];
     __syncthreads();
@@ -114,18 +115,31 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
             }
         }
         cluster.sync();  // #1: the whole bit-plane of input t is in global memory (L2)
-        for (uint32_t w = tid; w < Wn; w += nthr) s_bits[w] = __ldcg(p.bits_g + w);
+        {
+            const uint32_t n4 = Wn / 4u;
+            const uint4* src = reinterpret_cast<const uint4*>(p.bits_g);
+            for (uint32_t w = tid; w < n4; w += nthr) reinterpret_cast<uint4*>(s_bits)[w] = __ldcg(src + w);
+            for (uint32_t w = n4 * 4u + tid; w < Wn; w += nthr) s_bits[w] = __ldcg(p.bits_g + w);
+        }
         __syncthreads();
 
         // ---- a2: overlap of this CTA's columns; raw counts to every CTA (DSMEM) ----------
-        for (uint32_t cl = tid; cl < cpc; cl += nthr) {
-            const uint32_t c = c0 + cl;
+        // tpc consecutive lanes share a column (synapses s = part, part+tpc, ..), then a
+        // shuffle reduction; the padded column-major slice keeps the reads conflict-free
+        for (uint32_t base = 0; base < cpc * p.tpc; base += nthr) {
+            const uint32_t slot = base + tid;
+            const uint32_t cl = slot / p.tpc, part = slot % p.tpc;
             uint32_t raw = 0;
-            for (uint32_t s = 0; s < g.S; ++s) {
-                const uint32_t e = s_syn[s * cpc + cl];
-                raw += (s_bits[(e & 0x7FFFFFFFu) >> 5] >> (e & 31u)) & (e >> 31);
+            if (cl < cpc) {
+                const uint32_t* col = s_syn + cl * ss;
+                for (uint32_t s = part; s < g.S; s += p.tpc) {
+                    const uint32_t e = col[s];
+                    raw += (s_bits[(e & 0x7FFFFFFFu) >> 5] >> (e & 31u)) & (e >> 31);
+                }
             }
-            if (c < g.C32) {
+            for (uint32_t d = p.tpc >> 1; d > 0; d >>= 1) raw += __shfl_xor_sync(0xffffffffu, raw, d);
+            const uint32_t c = c0 + cl;
+            if (part == 0 && cl < cpc && c < g.C32) {
                 for (uint32_t r = 0; r < Q; ++r) cluster.map_shared_rank(s_raw, r)[c] = static_cast<uint16_t>(raw);
                 if (p.raw_out && c < g.C) {
                     p.raw_out[static_cast<size_t>(gin) * g.C + c] = static_cast<uint16_t>(raw);
@@ -277,7 +291,7 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
                 float v = on ? __fadd_rn(perm[s], p.inc) : __fsub_rn(perm[s], p.dec);
                 v = fminf(fmaxf(v, 0.0f), 1.0f);
                 perm[s] = v;
-                s_syn[s * cpc + cl] = i | (v >= p.tau ? 0x80000000u : 0u);
+                s_syn[cl * ss + s] = i | (v >= p.tau ? 0x80000000u : 0u);
             }
         }
         __syncthreads();  // smem flags updated before the next input's overlap
@@ -285,16 +299,25 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
     // ---- write the resident connected flags back (the per-input path reads them) ---------
     for (uint32_t i = tid; i < g.S * cpc; i += nthr) {
         const uint32_t s = i / cpc, cl = i % cpc, c = c0 + cl;
-        if (c < g.C32) p.syn[static_cast<size_t>(s) * g.C32 + c] = s_syn[i];
+        if (c < g.C32) p.syn[static_cast<size_t>(s) * g.C32 + c] = s_syn[cl * ss + s];
     }
+}
+
+uint32_t learn_syn_stride(uint32_t S) { return (S + 31u) / 32u * 32u + 8u; }
+
+// threads per column in the overlap: a power of two <= 32 with cpc * tpc <= 512
+uint32_t learn_threads_per_column(uint32_t cpc) {
+    uint32_t t = 1;
+    while (t < 32u && cpc * t * 2u <= kLearnThreads) t *= 2u;
+    return t;
 }
 
 uint32_t learn_cluster_smem(const Geometry& g, uint32_t Q, uint32_t* cols_per_cta) {
     const uint32_t cpc = ((g.C32 + Q - 1u) / Q + 31u) / 32u * 32u;
     const uint32_t Wn = (g.nbits + 31u) / 32u;
     if (cols_per_cta) *cols_per_cta = cpc;
-    return 4u * (g.S * cpc + Wn + g.C32) + 2u * (g.C32 + (g.C32 & 1u)) + 4u * (g.S + 1u + 32u + 4u) +
-           4u * (cpc / 32u);
+    return 4u * (learn_syn_stride(g.S) * cpc + (Wn + 3u) / 4u * 4u + g.C32) + 2u * (g.C32 + (g.C32 & 1u)) +
+           4u * (g.S + 1u + 32u + 4u) + 4u * (cpc / 32u);
 }
 
 cudaError_t configure_learn(int max_smem) {
