@@ -22,6 +22,7 @@
 // A cluster of K CTAs can split one group's pixel windows; partial counts are
 // then summed through distributed shared memory (DSMEM) before inhibition.
 #include <cooperative_groups.h>
+#include <cuda_fp16.h>
 
 #include "sp_internal.h"
 
@@ -244,68 +245,56 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
         }
         if (p.radius == 0 && p.uniform_bc) {
             // Uniform boost: the key order is (raw desc, index asc), so the k-th largest key
-            // is found from a histogram of the eligible raw counts:
-            // r* = largest r with #{raw >= r} >= k; winners = raw > r*, plus the lowest
-            // indices among raw == r* up to k.  Exact; O(C/32 + S/32) per lane.
-            uint32_t* hist = reinterpret_cast<uint32_t*>(region) + wi * 512u;  // u16 pairs
-            const uint32_t hw = (p.S + 2u) / 2u;  // words covering bins 0..S
-            for (uint32_t b = lane; b < hw; b += 32u) hist[b] = 0u;
-            __syncwarp();
-            for (uint32_t c = lane; c < p.C; c += 32u) {
-                const uint32_t r = row[c];
-                if (r >= theta) atomicAdd(&hist[r >> 1], 1u << ((r & 1u) * 16u));
-            }
-            __syncwarp();
-            // each lane owns B consecutive bins; suffix sums over lanes find the crossing
-            const uint32_t B = (p.S + 1u + 31u) / 32u;
-            const uint32_t lo_bin = lane * B;
-            uint32_t mine = 0;
-            for (uint32_t b = 0; b < B; ++b) {
-                const uint32_t r = lo_bin + b;
-                if (r <= p.S) mine += (hist[r >> 1] >> ((r & 1u) * 16u)) & 0xFFFFu;
-            }
-            uint32_t incl = mine;  // suffix sum over lanes >= this lane
+            // is found from a histogram of the raw counts: with one boost
+            // the floor raw*Bc > 2^23 (R7) is raw >= r_lo; r* = largest r with
+            // #{raw >= max(r, r_lo)} >= k; winners = raw > r*, plus the lowest indices among
+            // raw == r* up to k.  Exact; O(C/32 + S/32) per lane.
+            const uint32_t r_lo = max(theta, (1u << 23) / s_bc[0] + 1u);
+            // raw counts (<= 1023, exact in fp16) of this lane's columns, two per half2,
+            // zeroed below r_lo; counts of raw >= x with HSET2/HADD2 (FMA pipe, no atomics)
+            constexpr int NH = (CPT * NW + 1) / 2;
+            __half2 hr[NH];
 #pragma unroll
-            for (uint32_t d = 1; d < 32u; d <<= 1) {
-                const uint32_t v = __shfl_down_sync(0xffffffffu, incl, d);
-                if (lane + d < 32u) incl += v;
+            for (int t = 0; t < NH; ++t) {
+                const uint32_t ca = (2u * t) * 32u + lane, cb = ca + 32u;
+                uint32_t ra = ca < p.C32 ? row[ca] : 0u, rb = cb < p.C32 ? row[cb] : 0u;
+                ra = ra >= r_lo ? ra : 0u;
+                rb = rb >= r_lo ? rb : 0u;
+                hr[t] = __halves2half2(__uint2half_rn(ra), __uint2half_rn(rb));
             }
-            const uint32_t crossing = __ballot_sync(0xffffffffu, incl >= p.k);
-            int rstar = -1;          // -1: fewer than k eligible columns, all of them win
-            uint32_t need = 0;       // winners still to take among raw == r*
-            if (crossing) {
-                const uint32_t L = 31u - __clz(crossing);  // highest lane with incl >= k
-                uint32_t acc = __shfl_sync(0xffffffffu, incl - mine, L);  // bins above lane L
-                if (lane == L) {
-                    for (int b = static_cast<int>(B) - 1; b >= 0; --b) {
-                        const uint32_t r = lo_bin + b;
-                        if (r > p.S) continue;
-                        const uint32_t h = (hist[r >> 1] >> ((r & 1u) * 16u)) & 0xFFFFu;
-                        if (acc + h >= p.k) {
-                            rstar = static_cast<int>(r);
-                            need = p.k - acc;
-                            break;
-                        }
-                        acc += h;
-                    }
-                }
-                rstar = __shfl_sync(0xffffffffu, rstar, L);
-                need = __shfl_sync(0xffffffffu, need, L);
+            auto count_ge = [&](uint32_t x) -> uint32_t {
+                const __half2 hx = __half2half2(__uint2half_rn(x));
+                __half2 acc = __float2half2_rn(0.0f);
+#pragma unroll
+                for (int t = 0; t < NH; ++t) acc = __hadd2(acc, __hge2(hr[t], hx));
+                const uint32_t mine = static_cast<uint32_t>(__low2float(acc) + __high2float(acc));
+                return __reduce_add_sync(0xffffffffu, mine);
+            };
+            uint32_t rgt = r_lo;     // raw >= rgt wins outright
+            uint32_t rtie = 0xFFFFFFFFu, need = 0;  // raw == rtie: the first `need` win
+            if (count_ge(r_lo) >= p.k) {
+                // r* = largest r with #{raw >= r} >= k (bitwise search over the raw bits)
+                uint32_t T = 0;
+                for (int bit = 31 - __clz(p.S); bit >= 0; --bit)
+                    if (count_ge(T | (1u << bit)) >= p.k) T |= 1u << bit;
+                rtie = T;
+                need = p.k - count_ge(T + 1u);
+                rgt = T + 1u;
             }
-            uint32_t total = 0, ties_before = 0;
+            uint32_t total = 0, ties_before = 0, myword = 0;
             for (uint32_t cw = 0; cw < p.ncw; ++cw) {
-                const uint32_t c = cw * 32u + lane;
-                const uint32_t r = row[c];
-                const bool elig = c < p.C && r >= theta &&
-                                  static_cast<uint64_t>(r) * s_bc[c] > one;  // Alg. 2 floor (R7)
-                const bool tie = elig && static_cast<int>(r) == rstar;
-                const uint32_t tb = __ballot_sync(0xffffffffu, tie);
-                const bool act = elig && (rstar < 0 || static_cast<int>(r) > rstar ||
-                                          (tie && ties_before + __popc(tb & ((1u << lane) - 1u)) < need));
+                const uint32_t r = row[cw * 32u + lane];
+                const uint32_t tb = __ballot_sync(0xffffffffu, r == rtie);
+                const bool act = r >= rgt ||
+                                 (r == rtie && ties_before + __popc(tb & ((1u << lane) - 1u)) < need);
                 ties_before += __popc(tb);
                 const uint32_t word = __ballot_sync(0xffffffffu, act);
-                if (lane == 0) p.sdr[static_cast<size_t>(gin) * p.ncw + cw] = word;
+                if ((cw & 31u) == lane) myword = word;
                 total += __popc(word);
+                if ((cw & 31u) == 31u || cw + 1u == p.ncw) {  // coalesced store of <= 32 words
+                    const uint32_t base = cw & ~31u;
+                    if (lane <= (cw & 31u)) p.sdr[static_cast<size_t>(gin) * p.ncw + base + lane] = myword;
+                }
             }
             if (lane == 0) p.counts[gin] = total;
             continue;
@@ -494,8 +483,34 @@ __global__ void __launch_bounds__(NT, 1)
     // With two X buffers (p.xbufs == 2) window w+1 is transposed into the other buffer
     // while slower warps still gather window w: one CTA barrier per window.
     uint32_t j = 0, st = 0, phase = 0;
+    // ELL prefetch depth: the first PE blocks of each of this thread's cells for window w are
+    // loaded into registers when the window starts, so their L2 latency hides behind the
+    // window's chunk transposes instead of stalling the gather (profiles/r01_step7*.txt)
+    constexpr uint32_t PE = CPT <= 2 ? 2u : 0u;
+    // cell sizes/offsets are loaded one window ahead so the block prefetch never waits
+    uint32_t nnb[CPT], noff[CPT];
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+        const uint32_t cw = wi + NW * i;
+        nnb[i] = cw < p.ncw && w0 < w1 ? p.ell_nb[w0 * p.ncw + cw] : 0u;
+        noff[i] = cw < p.ncw && w0 < w1 ? p.ell_off[w0 * p.ncw + cw] : 0u;
+    }
     for (uint32_t w = w0; w < w1; ++w) {
         uint32_t* X = words + (p.xbufs == 2 ? (w & 1u) * (p.Lw + 1u) : 0u);
+        uint4 pre[CPT][PE > 0 ? PE : 1];
+        uint32_t pnb[CPT], poff[CPT];
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) {
+            const uint32_t cw = wi + NW * i;
+            pnb[i] = nnb[i];
+            poff[i] = noff[i];
+#pragma unroll
+            for (uint32_t b = 0; b < PE; ++b)
+                if (b < pnb[i]) pre[i][b] = __ldg(p.ell + poff[i] + lane + b * 32u);
+            const bool more = cw < p.ncw && w + 1u < w1;
+            nnb[i] = more ? p.ell_nb[(w + 1u) * p.ncw + cw] : 0u;
+            noff[i] = more ? p.ell_off[(w + 1u) * p.ncw + cw] : 0u;
+        }
         const uint32_t wbase = w * p.Lw;
         const uint32_t wlen = min(p.Lw, p.nbits - wbase);
         const uint32_t nch = (wlen + kChunkBits - 1) / kChunkBits;
@@ -531,18 +546,23 @@ __global__ void __launch_bounds__(NT, 1)
         // a2: bit-sliced gather-count of this window's synapses (ELL, 8 slots per block)
 #pragma unroll
         for (int i = 0; i < CPT; ++i) {
-            const uint32_t cw = wi + NW * i;
-            if (cw < p.ncw) {
-                const uint32_t cell = w * p.ncw + cw;
-                const uint32_t nb = p.ell_nb[cell];
-                const uint4* e = p.ell + p.ell_off[cell] + lane;
-#pragma unroll 2
-                for (uint32_t bk = 0; bk < nb; ++bk) {
-                    const uint4 s8 = __ldg(e + bk * 32u);
+            const uint32_t nb = pnb[i];
+            const uint4* e = p.ell + poff[i] + lane;
+#pragma unroll
+            for (uint32_t bk = 0; bk < PE; ++bk) {
+                if (bk < nb) {
+                    const uint4 s8 = pre[i][bk];
                     accumulate8(P[i], X[s8.x & 0xFFFFu], X[s8.x >> 16], X[s8.y & 0xFFFFu],
                                 X[s8.y >> 16], X[s8.z & 0xFFFFu], X[s8.z >> 16],
                                 X[s8.w & 0xFFFFu], X[s8.w >> 16]);
                 }
+            }
+#pragma unroll 2
+            for (uint32_t bk = PE; bk < nb; ++bk) {
+                const uint4 s8 = __ldg(e + bk * 32u);
+                accumulate8(P[i], X[s8.x & 0xFFFFu], X[s8.x >> 16], X[s8.y & 0xFFFFu],
+                            X[s8.y >> 16], X[s8.z & 0xFFFFu], X[s8.z >> 16],
+                            X[s8.w & 0xFFFFu], X[s8.w >> 16]);
             }
         }
         if (p.xbufs == 1) __syncthreads();  // before the next window overwrites X
