@@ -186,9 +186,9 @@ BatchedLayout plan_batched_layout(const Geometry& g, int max_smem) {
         L.xbufs = xbufs;
         L.Lw = Lw;
         L.nwin = (g.nbits + Lw - 1) / Lw;
-        // the window(s) double as the per-warp tie lists (32 warps x 64 keys) or raw-count
-        // histograms (32 warps x (S+2)/2 words, stride 512) of the top-k
-        const uint32_t topk_bytes = std::max(32u * 64u * 8u, 32u * 512u * 4u);
+        // the window(s) double as the per-warp scratch of the top-k: tie lists (64 keys),
+        // histograms ((S+2)/2 words) or raw bit-planes (ncw x nb <= 640 words), 32 warps
+        const uint32_t topk_bytes = std::max(32u * 64u * 8u, 32u * 640u * 4u);
         L.region_bytes = (std::max(xbufs * (Lw + 1u) * 4u, topk_bytes) + 127u) & ~127u;
         L.smem_bytes = stages * kStageBytes + L.region_bytes + g.C32 * 4u + stages * 12u;
         if (static_cast<int64_t>(L.smem_bytes) > max_smem) {

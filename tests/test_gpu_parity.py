@@ -307,6 +307,26 @@ def test_bench_launch_config_sampled_parity():
         check_results([res], sdr, counts, raw, boosted, rows=[f])
 
 
+SWEEP = [(C, S) for C in (256, 512, 1024, 2048) for S in (32, 64, 128, 256)]
+
+
+@pytest.mark.parametrize("radius", [0, 80])
+@pytest.mark.parametrize("C,S", SWEEP)
+def test_config3_sweep_sampled_parity(C, S, radius):
+    """BASELINE config 3 points (Tab. 2 min_overlap 8, k 40) on 960x540 frames: a sample of
+    4 frames through the batched kernel, bit-exact against the oracle."""
+    cfg = headline_cfg(num_columns=C, synapses_per_column=S, min_overlap=8, winners_set_size=40,
+                       inhibition_radius=radius)
+    idx, perm, boost = O.init_pools(cfg)
+    frames = sp_inputs.frames(2002, 0, 4, 540, 960, rho=0.5)
+    ora = O.SpatialPoolerOracle(cfg, (idx, perm, boost))
+    results = [ora.step(x, False) for x in O.encode(frames, cfg)]
+    sp = make_sp(cfg, None, max_inputs=8)  # the library's own init (== oracle init, R8)
+    out = run_gpu(sp, frames)
+    assert sp.info()["plan"]["path"] == P.SP_PATH_BATCHED
+    check_results(results, *out)
+
+
 def test_scaled_config5_learning():
     # BASELINE config 5: 16384 columns, 512 synapses, local r=80 (per-input path)
     cfg = headline_cfg(num_columns=16384, synapses_per_column=512, min_overlap=8,
