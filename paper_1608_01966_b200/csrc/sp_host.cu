@@ -158,10 +158,10 @@ BatchedLayout plan_batched_layout(const Geometry& g, int max_smem) {
     const char* eb = std::getenv("SP_XBUFS");
     const uint32_t want_stages = es ? static_cast<uint32_t>(std::atoi(es)) : 0u;
     const uint32_t want_xbufs = eb ? static_cast<uint32_t>(std::atoi(eb)) : 0u;
-    // preference (measured on B200, 4096 x 960x540, C=1024, 512 threads): one X window,
-    // 4 stages 0.402 ms, 3 stages 0.405 ms; (1024 threads, 3 stages) double-buffered X
-    // 0.467 vs 0.435 ms -- halving Lw costs more (windows, ELL padding) than the barrier.
-    const uint32_t options[6][2] = {{4, 1}, {3, 1}, {2, 1}, {4, 2}, {3, 2}, {2, 2}};
+    // preference (measured on B200, 4096 x 960x540, C=1024, 512 threads, ELL prefetch):
+    // 4 stages + double-buffered X 0.376 ms; 4 stages, one X 0.380; 3 stages + 2 X 0.383;
+    // 3 stages, one X 0.384.  (The 1024-thread kernel without prefetch preferred one X.)
+    const uint32_t options[6][2] = {{4, 2}, {4, 1}, {3, 2}, {3, 1}, {2, 1}, {2, 2}};
     for (const auto& o : options) {
         const uint32_t stages = o[0], xbufs = o[1];
         if ((want_stages && stages != want_stages) || (want_xbufs && xbufs != want_xbufs)) continue;
