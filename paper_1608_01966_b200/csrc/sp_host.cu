@@ -161,7 +161,11 @@ BatchedLayout plan_batched_layout(const Geometry& g, int max_smem) {
     // preference (measured on B200, 4096 x 960x540, C=1024, 512 threads, ELL prefetch):
     // 4 stages + double-buffered X 0.376 ms; 4 stages, one X 0.380; 3 stages + 2 X 0.383;
     // 3 stages, one X 0.384.  (The 1024-thread kernel without prefetch preferred one X.)
-    const uint32_t options[6][2] = {{4, 2}, {4, 1}, {3, 2}, {3, 1}, {2, 1}, {2, 2}};
+    // C32 > 1024 (4 column-warps per warp, no ELL prefetch registers): one X window wins
+    // (C=2048, S=256: 0.458 vs 0.494 ms).
+    const uint32_t pref2[6][2] = {{4, 2}, {4, 1}, {3, 2}, {3, 1}, {2, 1}, {2, 2}};
+    const uint32_t pref1[6][2] = {{4, 1}, {3, 1}, {2, 1}, {4, 2}, {3, 2}, {2, 2}};
+    const auto& options = g.C32 > 1024u ? pref1 : pref2;
     for (const auto& o : options) {
         const uint32_t stages = o[0], xbufs = o[1];
         if ((want_stages && stages != want_stages) || (want_xbufs && xbufs != want_xbufs)) continue;
