@@ -25,6 +25,7 @@
 #include <cuda_fp16.h>
 
 #include "sp_internal.h"
+#include "sp_select.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -300,81 +301,16 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             continue;
         }
         if (p.radius > 0 && p.uniform_bc) {
-            // Local inhibition, uniform boost: c wins iff x_c >= r_lo (R7) and fewer than k
-            // columns d of its window beat it, where d beats c iff x_d > x_c, or x_d == x_c
-            // and d < c (R6), x = raw (0 below r_lo).  Bit-sliced: the raw
-            // values of each 32-column word are kept as bit-planes, and one lane compares its
-            // x against 32 neighbours at once (3 LOP3 per plane), then masks the window.
-            const uint32_t r_lo = max(theta, (1u << 23) / s_bc[0] + 1u);
-            const uint32_t nb = 32u - __clz(p.S);  // bits of raw
+            // local inhibition, uniform boost: bit-sliced window comparator (sp_select.cuh)
+            const uint32_t r_lo = uniform_r_lo(theta, s_bc[0]);
+            const uint32_t nb = raw_bits(p.S);
             uint32_t* planes = reinterpret_cast<uint32_t*>(region) + wi * 640u;  // [ncw <= 64][nb <= 10]
-            for (uint32_t cw = 0; cw < p.ncw; ++cw) {
-                uint32_t x = row[cw * 32u + lane];
-                x = x >= r_lo ? x : 0u;
-                for (uint32_t b = 0; b < nb; ++b) {
-                    const uint32_t pl = __ballot_sync(0xffffffffu, (x >> b) & 1u);
-                    if (lane == b) planes[cw * nb + b] = pl;
-                }
-            }
+            build_raw_planes(row, planes, p.ncw, nb, r_lo, 0u, 1u, lane);
             __syncwarp();
-            const int R = static_cast<int>(p.radius), Cn = static_cast<int>(p.C);
             uint32_t total = 0, myword = 0;
             for (uint32_t cw = 0; cw < p.ncw; ++cw) {
-                const int c = static_cast<int>(cw * 32u + lane);
-                uint32_t x = row[c];
-                x = x >= r_lo ? x : 0u;
-                uint32_t beats = 0;
-                const int lo = max(0, c - R), hi = min(Cn - 1, c + R);  // window of c
-                const int jw0 = max(0, (static_cast<int>(cw) * 32 - R) / 32);
-                const int jw1 = min(static_cast<int>(p.ncw) - 1, (static_cast<int>(cw) * 32 + 31 + R) / 32);
-                // per-plane masks of this lane's x, hoisted out of the neighbour loop
-                uint32_t Xm[10];
-#pragma unroll
-                for (int b = 0; b < 10; ++b) Xm[b] = 0u - ((x >> b) & 1u);
-                auto window_bits = [&](int jw, uint32_t gt, uint32_t eq) -> uint32_t {
-                    // window bits of word jw for column c (self excluded), ties below c
-                    const int base = jw * 32;
-                    const int a = max(lo, base) - base, z = min(hi, base + 31) - base;
-                    uint32_t wm = a <= z ? (0xFFFFFFFFu >> (31 - z)) & (0xFFFFFFFFu << a) : 0u;
-                    const int self = c - base;
-                    uint32_t below = 0u;  // bits d < c inside this word
-                    if (self >= 32) below = 0xFFFFFFFFu;
-                    else if (self > 0) below = 0xFFFFFFFFu >> (32 - self);
-                    if (self >= 0 && self < 32) wm &= ~(1u << self);
-                    return __popc(gt & wm) + __popc(eq & wm & below);
-                };
-                int jw = jw0;
-                for (; jw + 1 <= jw1; jw += 2) {  // two independent neighbour words (ILP)
-                    const uint32_t* P0 = planes + jw * nb;
-                    const uint32_t* P1 = P0 + nb;
-                    uint32_t gt0 = 0u, eq0 = 0xFFFFFFFFu, gt1 = 0u, eq1 = 0xFFFFFFFFu;
-#pragma unroll
-                    for (int b = 9; b >= 0; --b) {
-                        if (b < static_cast<int>(nb)) {
-                            const uint32_t B0 = P0[b], B1 = P1[b], X = Xm[b];
-                            gt0 |= eq0 & B0 & ~X;
-                            eq0 &= ~(B0 ^ X);
-                            gt1 |= eq1 & B1 & ~X;
-                            eq1 &= ~(B1 ^ X);
-                        }
-                    }
-                    beats += window_bits(jw, gt0, eq0) + window_bits(jw + 1, gt1, eq1);
-                }
-                if (jw <= jw1) {
-                    const uint32_t* P0 = planes + jw * nb;
-                    uint32_t gt0 = 0u, eq0 = 0xFFFFFFFFu;
-#pragma unroll
-                    for (int b = 9; b >= 0; --b) {
-                        if (b < static_cast<int>(nb)) {
-                            const uint32_t B0 = P0[b], X = Xm[b];
-                            gt0 |= eq0 & B0 & ~X;
-                            eq0 &= ~(B0 ^ X);
-                        }
-                    }
-                    beats += window_bits(jw, gt0, eq0);
-                }
-                const bool act = c < Cn && x > 0u && beats < p.k;
-                const uint32_t word = __ballot_sync(0xffffffffu, act);
+                const uint32_t word = local_uniform_word(row, planes, p.ncw, nb, cw, p.C, p.radius, p.k,
+                                                         r_lo, lane);
                 if ((cw & 31u) == lane) myword = word;
                 total += __popc(word);
                 if ((cw & 31u) == 31u || cw + 1u == p.ncw) {

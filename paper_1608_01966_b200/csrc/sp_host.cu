@@ -561,6 +561,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         const uint32_t nf = std::min(fpb, n_frames - f0);
         sp::PerInputParams p{};
         p.frames = frames + static_cast<size_t>(f0) * g.W * g.H;
+        p.uniform_bc = h->uniform_bc ? 1u : 0u;
         p.first_input = row0 + f0 * g.P;
         p.num_inputs = nf * g.P;
         p.g = g;

@@ -73,6 +73,7 @@ struct alignas(64) BatchedParams {
 
 struct PerInputParams {
     const uint8_t* frames;     // frames of this sub-batch
+    uint32_t uniform_bc;       // all boosts equal (bit-sliced local inhibition)
     uint32_t first_input;      // global index (within the call) of the sub-batch's first input
     uint32_t num_inputs;       // inputs in this sub-batch
     Geometry g;

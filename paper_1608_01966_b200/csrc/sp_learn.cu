@@ -20,6 +20,7 @@
 #include <cooperative_groups.h>
 
 #include "sp_internal.h"
+#include "sp_select.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -68,6 +69,7 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
     uint32_t* s_red = s_hist + g.S + 1u;                            // [32] block reductions
     uint32_t* s_misc = s_red + 32u;                                 // [4]
     uint32_t* s_sdr = s_misc + 4u;                                  // [cpc/32] this CTA's SDR words
+    uint32_t* s_planes = s_sdr + cpc / 32u;                         // [ncw][nb] raw bit-planes
 
     // ---- resident state: this CTA's synapse slice, Bc -----------------------------------
     for (uint32_t i = tid; i < g.S * cpc; i += nthr) {
@@ -228,6 +230,26 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
             ties_before = block_sum(cnt, s_red);
         }
         const uint32_t wi = tid >> 5, nw = nthr >> 5;
+        if (p.radius > 0 && p.uniform_bc) {
+            // local inhibition, uniform boost: bit-sliced window comparator (sp_select.cuh)
+            const uint32_t r_lo = uniform_r_lo(theta, s_bc[0]);
+            const uint32_t nb = raw_bits(g.S);
+            build_raw_planes(s_raw, s_planes, g.ncw, nb, r_lo, wi, nw, lane);
+            __syncthreads();
+            for (uint32_t cw = wi; cw < cpc / 32u; cw += nw) {
+                const uint32_t gcw = c0 / 32u + cw;
+                uint32_t word = 0u;
+                if (gcw < g.ncw)
+                    word = local_uniform_word(s_raw, s_planes, g.ncw, nb, gcw, g.C, p.radius, p.k, r_lo, lane);
+                if (lane == 0) {
+                    s_sdr[cw] = word;
+                    if (gcw < g.ncw) {
+                        p.sdr[static_cast<size_t>(gin) * g.ncw + gcw] = word;
+                        if (word) atomicAdd(p.counts + gin, static_cast<uint32_t>(__popc(word)));
+                    }
+                }
+            }
+        } else
         for (uint32_t cw = wi; cw < cpc / 32u; cw += nw) {
             const uint32_t c = c0 + cw * 32u + lane;
             bool act = false;
@@ -317,7 +339,7 @@ uint32_t learn_cluster_smem(const Geometry& g, uint32_t Q, uint32_t* cols_per_ct
     const uint32_t Wn = (g.nbits + 31u) / 32u;
     if (cols_per_cta) *cols_per_cta = cpc;
     return 4u * (learn_syn_stride(g.S) * cpc + (Wn + 3u) / 4u * 4u + g.C32) + 2u * (g.C32 + (g.C32 & 1u)) +
-           4u * (g.S + 1u + 32u + 4u) + 4u * (cpc / 32u);
+           4u * (g.S + 1u + 32u + 4u) + 4u * (cpc / 32u) + 4u * (g.ncw * 10u);
 }
 
 cudaError_t configure_learn(int max_smem) {

@@ -6,6 +6,7 @@
 // plus layout maintenance (synapse-major idx|flag words, batched ELL flags).
 // Learning runs P2 -> P3 -> P4 per input in order (the recurrence of P:92).
 #include "sp_internal.h"
+#include "sp_select.cuh"
 
 namespace sp {
 
@@ -53,31 +54,39 @@ __global__ void k_pack(const PerInputParams p) {
 // P2: overlap.  grid (column blocks, inputs); the input's bit-plane is staged in smem.
 // syn[s][c] = idx | connected << 31 (synapse-major: coalesced across columns).
 // ---------------------------------------------------------------------------------------
-__global__ void k_overlap(const PerInputParams p) {
+__global__ void __launch_bounds__(256) k_overlap(const PerInputParams p) {
+    // 64 columns x 4 synapse quarters per CTA: reads of syn[s][c] stay coalesced across
+    // the 64 consecutive columns, and large C gets 4x the CTAs of thread-per-column.
     extern __shared__ uint32_t s_bits[];
+    __shared__ uint32_t s_part[4][64];
     const uint32_t t = blockIdx.y;
     const uint32_t* src = p.bits + static_cast<size_t>(t) * p.Wn;
     for (uint32_t i = threadIdx.x; i < p.Wn; i += blockDim.x) s_bits[i] = src[i];
     __syncthreads();
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= p.g.C32) return;
-    const uint32_t C32 = p.g.C32;
+    const uint32_t cl = threadIdx.x & 63u, part = threadIdx.x >> 6;
+    const uint32_t c = blockIdx.x * 64u + cl;
+    const uint32_t C32 = p.g.C32, S = p.g.S;
+    const uint32_t s0 = part * S / 4u, s1 = (part + 1u) * S / 4u;
     uint32_t raw = 0;
-    const uint32_t* e = p.syn + c;
-    uint32_t s = 0;
-    for (; s + 4 <= p.g.S; s += 4) {
-        const uint32_t e0 = e[(s + 0) * C32], e1 = e[(s + 1) * C32];
-        const uint32_t e2 = e[(s + 2) * C32], e3 = e[(s + 3) * C32];
-        raw += (s_bits[(e0 & 0x7FFFFFFFu) >> 5] >> (e0 & 31u)) & (e0 >> 31);
-        raw += (s_bits[(e1 & 0x7FFFFFFFu) >> 5] >> (e1 & 31u)) & (e1 >> 31);
-        raw += (s_bits[(e2 & 0x7FFFFFFFu) >> 5] >> (e2 & 31u)) & (e2 >> 31);
-        raw += (s_bits[(e3 & 0x7FFFFFFFu) >> 5] >> (e3 & 31u)) & (e3 >> 31);
+    if (c < C32) {
+        const uint32_t* e = p.syn + c;
+        uint32_t s = s0;
+        for (; s + 8 <= s1; s += 8) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = e[(s + u) * C32];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) raw += (s_bits[(v[u] & 0x7FFFFFFFu) >> 5] >> (v[u] & 31u)) & (v[u] >> 31);
+        }
+        for (; s < s1; ++s) {
+            const uint32_t e0 = e[s * C32];
+            raw += (s_bits[(e0 & 0x7FFFFFFFu) >> 5] >> (e0 & 31u)) & (e0 >> 31);
+        }
     }
-    for (; s < p.g.S; ++s) {
-        const uint32_t e0 = e[s * C32];
-        raw += (s_bits[(e0 & 0x7FFFFFFFu) >> 5] >> (e0 & 31u)) & (e0 >> 31);
-    }
-    p.raw[static_cast<size_t>(t) * C32 + c] = raw;
+    s_part[part][cl] = raw;
+    __syncthreads();
+    if (part == 0 && c < C32)
+        p.raw[static_cast<size_t>(t) * C32 + c] = s_part[0][cl] + s_part[1][cl] + s_part[2][cl] + s_part[3][cl];
 }
 
 // ---------------------------------------------------------------------------------------
@@ -96,6 +105,7 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
     const Geometry& g = p.g;
     uint32_t* s_raw = sm;               // [C32]
     uint32_t* s_bc = sm + g.C32;        // [C32]
+    uint32_t* s_planes = sm + 2u * g.C32;  // [ncw][nb] (local inhibition, uniform boost)
     __shared__ uint32_t s_cnt[2];
     __shared__ uint32_t s_total;
     const uint32_t t = blockIdx.x;
@@ -138,6 +148,21 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
     // SDR: warp per 32-column word
     const uint64_t one = 1ull << 23;
     uint32_t my_total = 0;
+    if (p.radius > 0 && p.uniform_bc) {
+        // local inhibition, uniform boost: bit-sliced window comparator (sp_select.cuh)
+        const uint32_t r_lo = uniform_r_lo(theta, s_bc[0]);
+        const uint32_t nb = raw_bits(g.S);
+        build_raw_planes(s_raw, s_planes, g.ncw, nb, r_lo, tid >> 5, nthr >> 5, tid & 31u);
+        __syncthreads();
+        for (uint32_t cw = tid >> 5; cw < g.ncw; cw += nthr >> 5) {
+            const uint32_t word = local_uniform_word(s_raw, s_planes, g.ncw, nb, cw, g.C, p.radius, p.k,
+                                                     r_lo, tid & 31u);
+            if ((tid & 31u) == 0) {
+                p.sdr[static_cast<size_t>(gin) * g.ncw + cw] = word;
+                my_total += __popc(word);
+            }
+        }
+    } else {
     for (uint32_t cw = tid >> 5; cw < g.ncw; cw += nthr >> 5) {
         const uint32_t c = cw * 32u + (tid & 31u);
         uint64_t N;
@@ -163,6 +188,8 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
             my_total += __popc(word);
         }
     }
+    }
+    __syncthreads();
     if ((tid & 31u) == 0 && my_total) atomicAdd(&s_total, my_total);
     __syncthreads();
     if (tid == 0) p.counts[gin] = s_total;
@@ -241,13 +268,13 @@ cudaError_t configure_per_input(int max_smem) {
 
 cudaError_t launch_overlap(const PerInputParams& p, cudaStream_t s) {
     const uint32_t smem = p.Wn * 4u;
-    dim3 grid((p.g.C32 + 255u) / 256u, p.num_inputs);
+    dim3 grid((p.g.C32 + 63u) / 64u, p.num_inputs);
     k_overlap<<<grid, 256, smem, s>>>(p);
     return cudaGetLastError();
 }
 
 cudaError_t launch_inhibit(const PerInputParams& p, cudaStream_t s) {
-    const uint32_t smem = p.g.C32 * 8u;
+    const uint32_t smem = p.g.C32 * 8u + p.g.ncw * 10u * 4u;  // raw, Bc, raw bit-planes
     const uint32_t threads = p.g.C32 < 1024u ? p.g.C32 : 1024u;
     k_inhibit<<<p.num_inputs, threads, smem, s>>>(p);
     return cudaGetLastError();

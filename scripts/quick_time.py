@@ -20,6 +20,11 @@ def main():
     sp = P.SpatialPooler(input_width=960, input_height=540, num_columns=C, synapses_per_column=S,
                          min_overlap=4, winners_set_size=40, inhibition_radius=r, max_inputs=n,
                          force_path=path)
+    if os.environ.get("BOOST") == "seeded":  # non-uniform boosts: the general selection paths
+        import numpy as np
+        sys.path.insert(0, ROOT)
+        import sp_inputs
+        sp.set_state(boost=sp_inputs.boosts(7, C))
     frames = torch.empty((n, 540, 960), dtype=torch.uint8, device="cuda")
     P.synth_frames(frames, 0, 2002, 0.5)
     torch.cuda.synchronize()
