@@ -322,6 +322,26 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             __syncwarp();  // planes are rewritten by this warp's next input
             continue;
         }
+        if (p.radius > 0 && p.ncw * 16u <= 1024u && NW <= 16u) {
+            // local inhibition, per-column boosts: coarse bit-sliced + exact ties
+            uint32_t* planes = reinterpret_cast<uint32_t*>(region) + wi * 1024u;  // [ncw][16]
+            build_coarse_planes(row, s_bc, planes, p.ncw, theta, sh, 0u, 1u, lane);
+            __syncwarp();
+            uint32_t total = 0, myword = 0;
+            for (uint32_t cw = 0; cw < p.ncw; ++cw) {
+                const uint32_t word = local_general_word(row, s_bc, planes, p.ncw, cw, p.C, p.radius,
+                                                         p.k, theta, sh, L, lane);
+                if ((cw & 31u) == lane) myword = word;
+                total += __popc(word);
+                if ((cw & 31u) == 31u || cw + 1u == p.ncw) {
+                    const uint32_t base = cw & ~31u;
+                    if (lane <= (cw & 31u)) p.sdr[static_cast<size_t>(gin) * p.ncw + base + lane] = myword;
+                }
+            }
+            if (lane == 0) p.counts[gin] = total;
+            __syncwarp();
+            continue;
+        }
         uint32_t Tu = 0;       // k-th largest coarse key
         uint64_t T2 = 0;       // exact key threshold among the columns with u == Tu
         if (p.radius == 0) {

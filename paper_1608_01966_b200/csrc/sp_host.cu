@@ -191,8 +191,9 @@ BatchedLayout plan_batched_layout(const Geometry& g, int max_smem) {
         L.Lw = Lw;
         L.nwin = (g.nbits + Lw - 1) / Lw;
         // the window(s) double as the per-warp scratch of the top-k: tie lists (64 keys),
-        // histograms ((S+2)/2 words) or raw bit-planes (ncw x nb <= 640 words), 32 warps
-        const uint32_t topk_bytes = std::max(32u * 64u * 8u, 32u * 640u * 4u);
+        // histograms ((S+2)/2 words) or raw bit-planes (ncw x nb <= 640 words), 32 warps;
+        // coarse-key bit-planes (ncw x 16 <= 1024 words), 16 warps
+        const uint32_t topk_bytes = std::max(32u * 64u * 8u, std::max(32u * 640u * 4u, 16u * 1024u * 4u));
         L.region_bytes = (std::max(xbufs * (Lw + 1u) * 4u, topk_bytes) + 127u) & ~127u;
         L.smem_bytes = stages * kStageBytes + L.region_bytes + g.C32 * 4u + stages * 12u;
         if (static_cast<int64_t>(L.smem_bytes) > max_smem) {

@@ -249,6 +249,25 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
                     }
                 }
             }
+        } else if (p.radius > 0) {
+            // local inhibition, per-column boosts: coarse bit-sliced + exact ties
+            const uint32_t sh = g.keyBits - L - 16u;
+            build_coarse_planes(s_raw, s_bc, s_planes, g.ncw, theta, sh, wi, nw, lane);
+            __syncthreads();
+            for (uint32_t cw = wi; cw < cpc / 32u; cw += nw) {
+                const uint32_t gcw = c0 / 32u + cw;
+                uint32_t word = 0u;
+                if (gcw < g.ncw)
+                    word = local_general_word(s_raw, s_bc, s_planes, g.ncw, gcw, g.C, p.radius, p.k, theta,
+                                              sh, L, lane);
+                if (lane == 0) {
+                    s_sdr[cw] = word;
+                    if (gcw < g.ncw) {
+                        p.sdr[static_cast<size_t>(gin) * g.ncw + gcw] = word;
+                        if (word) atomicAdd(p.counts + gin, static_cast<uint32_t>(__popc(word)));
+                    }
+                }
+            }
         } else
         for (uint32_t cw = wi; cw < cpc / 32u; cw += nw) {
             const uint32_t c = c0 + cw * 32u + lane;
@@ -339,7 +358,7 @@ uint32_t learn_cluster_smem(const Geometry& g, uint32_t Q, uint32_t* cols_per_ct
     const uint32_t Wn = (g.nbits + 31u) / 32u;
     if (cols_per_cta) *cols_per_cta = cpc;
     return 4u * (learn_syn_stride(g.S) * cpc + (Wn + 3u) / 4u * 4u + g.C32) + 2u * (g.C32 + (g.C32 & 1u)) +
-           4u * (g.S + 1u + 32u + 4u) + 4u * (cpc / 32u) + 4u * (g.ncw * 10u);
+           4u * (g.S + 1u + 32u + 4u) + 4u * (cpc / 32u) + 4u * (g.ncw * 16u);
 }
 
 cudaError_t configure_learn(int max_smem) {

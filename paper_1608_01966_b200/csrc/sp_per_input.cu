@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
     const Geometry& g = p.g;
     uint32_t* s_raw = sm;               // [C32]
     uint32_t* s_bc = sm + g.C32;        // [C32]
-    uint32_t* s_planes = sm + 2u * g.C32;  // [ncw][nb] (local inhibition, uniform boost)
+    uint32_t* s_planes = sm + 2u * g.C32;  // [ncw][<=16] bit-planes (local inhibition)
     __shared__ uint32_t s_cnt[2];
     __shared__ uint32_t s_total;
     const uint32_t t = blockIdx.x;
@@ -157,6 +157,19 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
         for (uint32_t cw = tid >> 5; cw < g.ncw; cw += nthr >> 5) {
             const uint32_t word = local_uniform_word(s_raw, s_planes, g.ncw, nb, cw, g.C, p.radius, p.k,
                                                      r_lo, tid & 31u);
+            if ((tid & 31u) == 0) {
+                p.sdr[static_cast<size_t>(gin) * g.ncw + cw] = word;
+                my_total += __popc(word);
+            }
+        }
+    } else if (p.radius > 0) {
+        // local inhibition, per-column boosts: coarse bit-sliced + exact ties (sp_select.cuh)
+        const uint32_t sh = g.keyBits - L - 16u;
+        build_coarse_planes(s_raw, s_bc, s_planes, g.ncw, theta, sh, tid >> 5, nthr >> 5, tid & 31u);
+        __syncthreads();
+        for (uint32_t cw = tid >> 5; cw < g.ncw; cw += nthr >> 5) {
+            const uint32_t word = local_general_word(s_raw, s_bc, s_planes, g.ncw, cw, g.C, p.radius, p.k,
+                                                     theta, sh, L, tid & 31u);
             if ((tid & 31u) == 0) {
                 p.sdr[static_cast<size_t>(gin) * g.ncw + cw] = word;
                 my_total += __popc(word);
@@ -274,7 +287,7 @@ cudaError_t launch_overlap(const PerInputParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_inhibit(const PerInputParams& p, cudaStream_t s) {
-    const uint32_t smem = p.g.C32 * 8u + p.g.ncw * 10u * 4u;  // raw, Bc, raw bit-planes
+    const uint32_t smem = p.g.C32 * 8u + p.g.ncw * 16u * 4u;  // raw, Bc, bit-planes
     const uint32_t threads = p.g.C32 < 1024u ? p.g.C32 : 1024u;
     k_inhibit<<<p.num_inputs, threads, smem, s>>>(p);
     return cudaGetLastError();
