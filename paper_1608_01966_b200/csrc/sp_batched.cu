@@ -646,6 +646,119 @@ __global__ void __launch_bounds__(NT, 1)
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Patch mode: every pw x ph tile of a frame is an SP
+// input (R13).  A group = up to 32 consecutive tiles of one tile-row; one 4-D TMA box
+// {pw, 32 tiles, ph, 1} brings its pixels (stage layout [y][tile][x]); the whole tile is one
+// window of X, so each group is transposed, gathered, counted and ranked in turn by a
+// persistent CTA while the ring prefetches the next groups.
+// ---------------------------------------------------------------------------------------
+template <int CPT, int NT>
+__global__ void __launch_bounds__(NT, 1) sp_patch_kernel(const __grid_constant__ BatchedParams p) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    constexpr uint32_t NW = NT / 32;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, wi = tid >> 5;
+    const uint32_t NST = p.stages;
+    const uint32_t stage_bytes = p.patch_stage_bytes;  // 32 * nbits rounded to 1 KiB
+    uint8_t* stage_base = smem;
+    uint32_t* X = reinterpret_cast<uint32_t*>(smem + NST * stage_bytes);         // [Lw + 1]
+    uint16_t* rawbuf = reinterpret_cast<uint16_t*>(X + p.Lw + 1u + ((p.Lw + 1u) & 1u));  // [32][C32]
+    uint8_t* scratch = reinterpret_cast<uint8_t*>(rawbuf + 32u * p.C32);         // top-k scratch
+    uint32_t* s_bc = reinterpret_cast<uint32_t*>(scratch + p.region_bytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(s_bc + p.C32);
+    uint32_t* released = reinterpret_cast<uint32_t*>(bars + NST);
+
+    const uint32_t tpr = p.tiles_x;                     // tiles per tile-row
+    const uint32_t gpr = (tpr + 31u) / 32u;             // groups per tile-row
+    const uint32_t G = p.groups;                        // rows * gpr
+    const uint32_t pw = p.patch_w, ph = p.patch_h;
+
+    if (tid < NST) {
+        mbar_init(&bars[tid], 1);
+        released[tid] = 0u;
+    }
+    for (uint32_t c = tid; c < p.C32; c += NT) s_bc[c] = p.bc[c];
+    if (tid == 0) X[p.Lw] = 0u;  // zero slot
+    if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+
+    // the j-th group of this CTA is g = blockIdx.x + j * gridDim.x
+    auto issue = [&](uint32_t j, uint32_t st) {
+        const uint32_t g = blockIdx.x + j * gridDim.x;
+        const uint32_t row = g / gpr, px0 = (g % gpr) * 32u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_expect_tx(&bars[st], 32u * pw * ph);
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_addr(stage_base + st * stage_bytes)),
+            "l"(reinterpret_cast<uint64_t>(&p.tmap)), "r"(0u), "r"(px0), "r"(0u), "r"(row),
+            "r"(smem_addr(&bars[st]))
+            : "memory");
+    };
+    const uint32_t ngroups = blockIdx.x < G ? (G - blockIdx.x + gridDim.x - 1u) / gridDim.x : 0u;
+    if (tid == 0)
+        for (uint32_t j = 0; j < min(NST, ngroups); ++j) issue(j, j);
+
+    const TransposeLane tl(lane);
+    const uint32_t pob = pixel_of_bit(lane);
+    const uint32_t released_addr = smem_addr(released);
+    const uint32_t bpr = pw / 32u;            // 32-pixel blocks per tile row
+    const uint32_t nblk = bpr * ph;           // blocks per tile
+    uint32_t st = 0, phase = 0;
+    for (uint32_t j = 0; j < ngroups; ++j) {
+        const uint32_t g = blockIdx.x + j * gridDim.x;
+        const uint32_t row = g / gpr, px0 = (g % gpr) * 32u;
+        const uint32_t gs = min(32u, tpr - px0);
+        const uint32_t in0 = row * tpr + px0;
+        const uint32_t lane_ok = lane < gs ? 0xFFFFFFFFu : 0u;
+        mbar_wait(&bars[st], phase);
+        // a1: lane f = tile f of the group; block b = row y, pixels 32*xb .. 32*xb+31
+        {
+            const uint8_t* stg = stage_base + st * stage_bytes;
+            for (uint32_t b = wi; b < nblk; b += NW) {
+                const uint32_t y = b / bpr, xb = b % bpr;
+                const uint8_t* src = stg + (y * 32u + lane) * pw + xb * 32u;
+                const uint4 a = *reinterpret_cast<const uint4*>(src);
+                const uint4 bb = *reinterpret_cast<const uint4*>(src + 16);
+                X[y * pw + xb * 32u + pob] = warp_transpose32(nonzero_mask32(a, bb, p.one) & lane_ok, tl);
+            }
+        }
+        if (warp_release_is_last<NW>(released_addr + 4u * st) && j + NST < ngroups) issue(j + NST, st);
+        if (++st == NST) {
+            st = 0;
+            phase ^= 1u;
+        }
+        __syncthreads();  // X of this group complete
+        // a2: gather-count of all synapses (one window)
+        Planes P[CPT];
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) {
+            P[i].ones = P[i].twos = P[i].fours = 0u;
+#pragma unroll
+            for (int h = 0; h < (int)kHiPlanes; ++h) P[i].hi[h] = 0u;
+            const uint32_t cw = wi + NW * i;
+            if (cw < p.ncw) {
+                const uint32_t nb = p.ell_nb[cw];
+                const uint4* e = p.ell + p.ell_off[cw] + lane;
+#pragma unroll 4
+                for (uint32_t bk = 0; bk < nb; ++bk) {
+                    const uint4 s8 = __ldg(e + bk * 32u);
+                    accumulate8(P[i], X[s8.x & 0xFFFFu], X[s8.x >> 16], X[s8.y & 0xFFFFu],
+                                X[s8.y >> 16], X[s8.z & 0xFFFFu], X[s8.z >> 16],
+                                X[s8.w & 0xFFFFu], X[s8.w >> 16]);
+                }
+                const uint32_t c = cw * 32u + lane;
+                for (uint32_t f = 0; f < gs; ++f)
+                    rawbuf[f * p.C32 + c] = static_cast<uint16_t>(extract_count(P[i], f));
+            }
+        }
+        __syncthreads();  // raw counts of the group complete; X may be overwritten
+        // a3/a4: per tile
+        batched_topk<CPT, NW>(p, rawbuf, scratch, s_bc, in0, gs, 0u, 1u, wi, lane);
+        __syncthreads();  // rawbuf / scratch reused by the next group
+    }
+}
+
 template <typename F>
 static cudaError_t allow_dynamic_smem(F* fn, int max_smem) {
     cudaFuncAttributes a{};
@@ -656,7 +769,8 @@ static cudaError_t allow_dynamic_smem(F* fn, int max_smem) {
 }
 
 cudaError_t configure_batched(int max_smem) {
-    cudaError_t e = allow_dynamic_smem(sp_batched_kernel<1, 1024>, max_smem);
+    cudaError_t e = allow_dynamic_smem(sp_patch_kernel<2, 512>, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<1, 1024>, max_smem);
     if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2, 1024>, max_smem);
     if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2, 512>, max_smem);
     if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<4, 512>, max_smem);
@@ -683,6 +797,11 @@ cudaError_t launch_batched(const BatchedParams& p, uint32_t smem_bytes, cudaStre
                         : cudaLaunchKernelEx(&cfg, sp_batched_kernel<4, 512>, p);
     return cpt <= 1 ? cudaLaunchKernelEx(&cfg, sp_batched_kernel<1, 1024>, p)
                     : cudaLaunchKernelEx(&cfg, sp_batched_kernel<2, 1024>, p);
+}
+
+cudaError_t launch_patch(const BatchedParams& p, uint32_t smem_bytes, uint32_t ctas, cudaStream_t s) {
+    sp_patch_kernel<2, 512><<<ctas, 512, smem_bytes, s>>>(p);
+    return cudaGetLastError();
 }
 
 // Maximum co-resident clusters for K = 1..8 at this smem size (index K).

@@ -205,6 +205,51 @@ BatchedLayout plan_batched_layout(const Geometry& g, int max_smem) {
     return L;
 }
 
+// Patch mode (NEXT-2): one X window = one tile; groups of <= 32 tiles of a tile-row.
+BatchedLayout plan_patch_layout(const Geometry& g, int max_smem) {
+    BatchedLayout L;
+    if (g.whole || g.pw % 32u || 32u * g.nbits > 49152u || g.C32 > 1024u || g.S > kMaxBatchedSynapses) return L;
+    const uint32_t stage_bytes = (32u * g.nbits + 1023u) / 1024u * 1024u;
+    const uint32_t Lw = (g.nbits + 31u) / 32u * 32u;
+    const uint32_t topk_bytes = 16u * 1024u * 4u;  // 16 warps: coarse bit-planes <= 1024 words
+    for (uint32_t stages = 4; stages >= 2; --stages) {
+        const uint32_t smem = stages * stage_bytes + (Lw + 2u) * 4u + 32u * g.C32 * 2u + topk_bytes +
+                              g.C32 * 4u + stages * 12u;
+        if (static_cast<int>(smem) > max_smem) continue;
+        L.ok = true;
+        L.stages = stages;
+        L.xbufs = 1;
+        L.Lw = Lw;
+        L.nwin = 1;
+        L.region_bytes = topk_bytes;
+        L.smem_bytes = smem;
+        return L;
+    }
+    return L;
+}
+
+bool encode_patches_tmap(CUtensorMap* map, const uint8_t* frames, const Geometry& g, uint32_t frames_n) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q{};
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    // view of the frames as {x in tile, tile, y in tile, tile-row}: tile t of tile-row r is
+    // frame r / ty, tile-row r % ty, column t (R13); box {pw, 32 tiles, ph, 1}
+    const uint32_t tx = g.W / g.pw, ty = g.H / g.ph;
+    const cuuint64_t dims[4] = {g.pw, tx, g.ph, static_cast<cuuint64_t>(ty) * frames_n};
+    const cuuint64_t strides[3] = {g.pw, g.W, static_cast<cuuint64_t>(g.W) * g.ph};
+    const cuuint32_t box[4] = {g.pw, 32u, g.ph, 1u};
+    const cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(frames), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool encode_frames_tmap(CUtensorMap* map, const uint8_t* frames, uint32_t nbits, uint32_t rows) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
@@ -337,7 +382,7 @@ sp_plan_info make_plan(const sp_handle* h, uint32_t n, bool learn, const uint8_t
     pl.sdr_words = g.ncw;
     uint32_t reason = 0;
     if (learn) reason |= sp::kNotBatchedLearn;
-    if (!g.whole) reason |= sp::kNotBatchedPatch;
+    if (!g.whole && !h->lay.ok) reason |= sp::kNotBatchedPatch | sp::kNotPatchGeometry;
     if (g.nbits % 16u) reason |= sp::kNotBatchedAlign;
     if (frames && (reinterpret_cast<uintptr_t>(frames) & 15u)) reason |= sp::kNotBatchedAlign;
     if (g.C32 > sp::kMaxBatchedColumns) reason |= sp::kNotBatchedColumns;
@@ -345,7 +390,19 @@ sp_plan_info make_plan(const sp_handle* h, uint32_t n, bool learn, const uint8_t
     if (h->cfg.force_path == SP_PATH_PER_INPUT) reason |= sp::kNotBatchedForced;
     if (!h->lay.ok) reason |= sp::kNotBatchedSmem;
     pl.reason = reason;
-    if (reason == 0 && n > 0) {
+    if (reason == 0 && n > 0 && !g.whole) {
+        // patch kernel: groups of <= 32 tiles of one tile-row, persistent CTAs
+        const uint32_t tx = g.W / g.pw;
+        pl.path = SP_PATH_BATCHED;
+        pl.groups = (n / tx) * ((tx + 31u) / 32u);
+        pl.cluster = 1;
+        pl.ctas = std::min<uint32_t>(pl.groups, static_cast<uint32_t>(h->sm_count));
+        pl.window_bits = h->lay.Lw;
+        pl.num_windows = 1;
+        pl.chunk_bits = g.nbits;
+        pl.stages = h->lay.stages;
+        pl.smem_bytes = h->lay.smem_bytes;
+    } else if (reason == 0 && n > 0) {
         pl.path = SP_PATH_BATCHED;
         uint32_t G = 0, K = 1;
         sp::plan_batched_grid(g, h->lay.nwin, n, h->sm_count, h->max_clusters[1] ? h->max_clusters : nullptr, &G,
@@ -479,7 +536,10 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
             h->ell_dirty = false;
         }
         sp::BatchedParams p{};
-        if (!sp::encode_frames_tmap(&p.tmap, frames, g.nbits, n))
+        if (!g.whole) {
+            if (!sp::encode_patches_tmap(&p.tmap, frames, g, n_frames))
+                return fail(SP_E_CUDA, "cuTensorMapEncodeTiled failed for the tiles");
+        } else if (!sp::encode_frames_tmap(&p.tmap, frames, g.nbits, n))
             return fail(SP_E_CUDA, "cuTensorMapEncodeTiled failed for the frames (nbits %u, rows %u)",
                         g.nbits, n);
         p.num_inputs = n;
@@ -513,7 +573,15 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         p.counts = h->d_counts + row0;
         p.raw_out = rec ? h->d_raw_rec + static_cast<size_t>(row0) * g.C : nullptr;
         p.boosted_out = rec ? h->d_boosted_rec + static_cast<size_t>(row0) * g.C : nullptr;
-        e = sp::launch_batched(p, h->lay.smem_bytes, s);
+        if (!g.whole) {
+            p.patch_w = g.pw;
+            p.patch_h = g.ph;
+            p.tiles_x = g.W / g.pw;
+            p.patch_stage_bytes = (32u * g.nbits + 1023u) / 1024u * 1024u;
+            e = sp::launch_patch(p, h->lay.smem_bytes, pl.ctas, s);
+        } else {
+            e = sp::launch_batched(p, h->lay.smem_bytes, s);
+        }
         h->launches++;
         if (e != cudaSuccess) return cuda_fail(e, "batched kernel launch");
         return SP_OK;
@@ -661,7 +729,8 @@ sp_status sp_plan(const sp_config* cfg, uint32_t num_frames, int32_t sm_count, s
     tmp.g = sp::make_geometry(*cfg);
     tmp.sm_count = sm_count > 0 ? sm_count : kDefaultSms;
     tmp.max_smem = kDefaultSmem;
-    tmp.lay = sp::plan_batched_layout(tmp.g, tmp.max_smem);
+    tmp.lay = tmp.g.whole ? sp::plan_batched_layout(tmp.g, tmp.max_smem)
+                          : sp::plan_patch_layout(tmp.g, tmp.max_smem);
     *out = make_plan(&tmp, num_frames * tmp.g.P, false, nullptr);
     return SP_OK;
 }
@@ -684,14 +753,14 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
     h->g = sp::make_geometry(*cfg);
     cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device);
     cudaDeviceGetAttribute(&h->max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
-    h->lay = sp::plan_batched_layout(h->g, h->max_smem);
+    h->lay = h->g.whole ? sp::plan_batched_layout(h->g, h->max_smem) : sp::plan_patch_layout(h->g, h->max_smem);
     const sp::Geometry& g = h->g;
     if ((e = sp::configure_batched(h->max_smem)) != cudaSuccess ||
         (e = sp::configure_per_input(h->max_smem)) != cudaSuccess) {
         release(h);
         return cuda_fail(e, "kernel attributes");
     }
-    if (h->lay.ok) sp::batched_max_clusters(h->lay.smem_bytes, h->max_clusters);
+    if (h->lay.ok && h->g.whole) sp::batched_max_clusters(h->lay.smem_bytes, h->max_clusters);
     // cluster-resident learning: the largest cluster (<= 16 CTAs, >= 32 columns each) whose
     // synapse slice + bit-plane fit in shared memory and that can be co-scheduled
     if (sp::configure_learn(h->max_smem) == cudaSuccess && !std::getenv("SP_NO_CLUSTER_LEARN")) {

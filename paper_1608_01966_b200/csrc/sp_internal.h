@@ -27,6 +27,7 @@ enum : uint32_t {
     kNotBatchedForced = 32u,    // force_path = PER_INPUT
     kNotBatchedSmem = 64u,      // no (stages, window) fits shared memory
     kNotBatchedTensorMap = 128u, // the TMA descriptor could not be encoded
+    kNotPatchGeometry = 256u,   // patch mode: pw % 32, pw*ph <= 1536, C32 <= 1024 needed
 };
 
 struct Geometry {
@@ -58,6 +59,8 @@ struct alignas(64) BatchedParams {
     uint32_t S;                // synapses per column (histogram range of the fast top-k)
     uint32_t uniform_bc;       // all boosts equal: key order = (raw desc, index asc)
     uint32_t threads;          // 1024 or 512 threads per CTA
+    // patch kernel
+    uint32_t patch_w, patch_h, tiles_x, patch_stage_bytes;
     uint64_t* trace;           // nullable [ctas][4] phase timestamps (development aid)
     uint32_t groups, K;
     const uint32_t* ell_off;   // [nwin][ncw] offset in uint4 units
@@ -127,12 +130,14 @@ cudaError_t launch_learn_cluster(const LearnParams& p, uint32_t smem, cudaStream
 // host planning (sp_host.cu)
 Geometry make_geometry(const sp_config& cfg);
 BatchedLayout plan_batched_layout(const Geometry& g, int max_smem);
+BatchedLayout plan_patch_layout(const Geometry& g, int max_smem);
 void plan_batched_grid(const Geometry& g, uint32_t nwin, uint32_t num_inputs, int sm_count,
                        const int* max_clusters /* [9] by K, or nullptr */,
                        uint32_t* groups, uint32_t* K);
 
 // TMA descriptor of the frames for the batched kernel (sp_host.cu); false on failure
 bool encode_frames_tmap(CUtensorMap* map, const uint8_t* frames, uint32_t nbits, uint32_t rows);
+bool encode_patches_tmap(CUtensorMap* map, const uint8_t* frames, const Geometry& g, uint32_t frames_n);
 
 // one-time kernel attributes (max dynamic smem)
 cudaError_t configure_batched(int max_smem);
@@ -140,6 +145,7 @@ cudaError_t configure_per_input(int max_smem);
 
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_batched(const BatchedParams& p, uint32_t smem_bytes, cudaStream_t s);
+cudaError_t launch_patch(const BatchedParams& p, uint32_t smem_bytes, uint32_t ctas, cudaStream_t s);
 cudaError_t batched_max_clusters(uint32_t smem_bytes, int max_clusters[9]);
 cudaError_t launch_pack(const PerInputParams& p, cudaStream_t s);
 cudaError_t launch_overlap(const PerInputParams& p, cudaStream_t s);

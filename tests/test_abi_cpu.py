@@ -93,8 +93,15 @@ def test_plan_small_batches_split_windows_over_clusters():
     assert pl["cluster"] > 1 and pl["ctas"] <= 148
 
 
+def test_plan_patch_mode_uses_the_patch_kernel():
+    # 960x540 in 32x30 tiles: 30 tiles per tile-row -> one group per tile-row (NEXT-2)
+    pl = P.plan(4, input_width=960, input_height=540, patch_width=32, patch_height=30,
+                num_columns=1024, synapses_per_column=256)
+    assert pl["path"] == P.SP_PATH_BATCHED and pl["groups"] == 4 * 18 and pl["num_windows"] == 1
+
+
 @pytest.mark.parametrize("kw,reason", [
-    (dict(input_width=960, input_height=540, patch_width=32, patch_height=30), 2),
+    (dict(input_width=960, input_height=540, patch_width=16, patch_height=30), 2),
     (dict(input_width=37, input_height=5), 4),
     (dict(input_width=960, input_height=540, num_columns=16384, synapses_per_column=512), 8),
     (dict(input_width=960, input_height=540, force_path=P.SP_PATH_PER_INPUT), 32),

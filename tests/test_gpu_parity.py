@@ -225,6 +225,31 @@ def test_max_inputs_enforced():
     assert e.value.status == P.SP_E_ARG
 
 
+PATCHES = [
+    dict(input_width=1152, input_height=60, patch_width=32, patch_height=30, num_columns=256,
+         synapses_per_column=64, min_overlap=2, winners_set_size=10),          # 36 tiles/row: 2 groups
+    dict(input_width=256, input_height=40, patch_width=64, patch_height=20, num_columns=200,
+         synapses_per_column=100, min_overlap=3, winners_set_size=17, inhibition_radius=9),
+    dict(input_width=960, input_height=90, patch_width=32, patch_height=30, num_columns=1024,
+         synapses_per_column=256, min_overlap=4, winners_set_size=40, inhibition_radius=80),
+]
+
+
+@pytest.mark.parametrize("boost_mode", ["seeded", "uniform1"])
+@pytest.mark.parametrize("kw", PATCHES)
+def test_patch_kernel_parity(kw, boost_mode):
+    cfg = ocfg(**kw)
+    state = with_boost(perturbed_state(cfg), boost_mode)
+    frames = sp_inputs.frames(2002, 0, 3, cfg.input_height, cfg.input_width, rho=0.5,
+                              nonzero="random")
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = [ora.step(x, False) for x in O.encode(frames, cfg)]
+    sp = make_sp(cfg, state, max_inputs=1024)
+    out = run_gpu(sp, frames)
+    assert sp.info()["plan"]["path"] == P.SP_PATH_BATCHED
+    check_results(results, *out)
+
+
 def test_patch_mode_parity():
     # BASELINE config 2 variant: 960x540 tiled into 32x30 patches (540 inputs per frame)
     cfg = ocfg(input_width=960, input_height=540, patch_width=32, patch_height=30,
@@ -233,8 +258,10 @@ def test_patch_mode_parity():
     frames = sp_inputs.frames(2002, 0, 1, 540, 960, rho=0.5)
     ora = O.SpatialPoolerOracle(cfg, state)
     results = [ora.step(x, False) for x in O.encode(frames, cfg)]
-    out = run_gpu(make_sp(cfg, state), frames)
-    check_results(results, *out)
+    for path in PATHS:
+        sp = make_sp(cfg, state, path)
+        check_results(results, *run_gpu(sp, frames))
+        assert sp.info()["plan"]["path"] == path
 
 
 # --------------------------------------------------------------------------- #
