@@ -254,34 +254,8 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             // raw counts (<= 1023, exact in fp16) of this lane's columns, two per half2,
             // zeroed below r_lo; counts of raw >= x with HSET2/HADD2 (FMA pipe, no atomics)
             constexpr int NH = (CPT * NW + 1) / 2;
-            __half2 hr[NH];
-#pragma unroll
-            for (int t = 0; t < NH; ++t) {
-                const uint32_t ca = (2u * t) * 32u + lane, cb = ca + 32u;
-                uint32_t ra = ca < p.C32 ? row[ca] : 0u, rb = cb < p.C32 ? row[cb] : 0u;
-                ra = ra >= r_lo ? ra : 0u;
-                rb = rb >= r_lo ? rb : 0u;
-                hr[t] = __halves2half2(__uint2half_rn(ra), __uint2half_rn(rb));
-            }
-            auto count_ge = [&](uint32_t x) -> uint32_t {
-                const __half2 hx = __half2half2(__uint2half_rn(x));
-                __half2 acc = __float2half2_rn(0.0f);
-#pragma unroll
-                for (int t = 0; t < NH; ++t) acc = __hadd2(acc, __hge2(hr[t], hx));
-                const uint32_t mine = static_cast<uint32_t>(__low2float(acc) + __high2float(acc));
-                return __reduce_add_sync(0xffffffffu, mine);
-            };
-            uint32_t rgt = r_lo;     // raw >= rgt wins outright
-            uint32_t rtie = 0xFFFFFFFFu, need = 0;  // raw == rtie: the first `need` win
-            if (count_ge(r_lo) >= p.k) {
-                // r* = largest r with #{raw >= r} >= k (bitwise search over the raw bits)
-                uint32_t T = 0;
-                for (int bit = 31 - __clz(p.S); bit >= 0; --bit)
-                    if (count_ge(T | (1u << bit)) >= p.k) T |= 1u << bit;
-                rtie = T;
-                need = p.k - count_ge(T + 1u);
-                rgt = T + 1u;
-            }
+            uint32_t rgt, rtie, need;
+            global_uniform_threshold<NH>(row, p.C32, p.S, p.k, r_lo, lane, rgt, rtie, need);
             uint32_t total = 0, ties_before = 0, myword = 0;
             for (uint32_t cw = 0; cw < p.ncw; ++cw) {
                 const uint32_t r = row[cw * 32u + lane];
@@ -345,65 +319,9 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
         uint32_t Tu = 0;       // k-th largest coarse key
         uint64_t T2 = 0;       // exact key threshold among the columns with u == Tu
         if (p.radius == 0) {
-            // (1) coarse: the k-th largest u = N >> sh (16 bits) by bitwise search, over
-            //     keys packed two per register (columns 64t+lane and 64t+32+lane)
             constexpr int NU = (CPT * NW + 1) / 2;  // column-warps of this CTA, two per register
-            uint32_t uu[NU];
-#pragma unroll
-            for (int t = 0; t < NU; ++t) {
-                const uint32_t ca = (2u * t) * 32u + lane, cb = ca + 32u;
-                uint64_t Na = 0, Nb = 0;
-                if (ca < p.C32) rank_key(row[ca], s_bc[ca], theta, ca, L, Na);
-                if (cb < p.C32) rank_key(row[cb], s_bc[cb], theta, cb, L, Nb);
-                uu[t] = static_cast<uint32_t>(Na >> sh) | (static_cast<uint32_t>(Nb >> sh) << 16);
-            }
-            for (int bit = 15; bit >= 0; --bit) {
-                const uint32_t cand = (Tu | (1u << bit)) << 16;
-                uint32_t cnt = 0;
-#pragma unroll
-                for (int t = 0; t < NU; ++t)
-                    cnt += (uu[t] >= cand ? 1u : 0u) + ((uu[t] << 16) >= cand ? 1u : 0u);
-                if (__reduce_add_sync(0xffffffffu, cnt) >= p.k) Tu |= 1u << bit;
-            }
-            if (Tu > 0) {
-                // (2) exact: the columns tied at u == Tu, ranked by their exact keys
-                uint32_t ngt = 0, nties = 0;
-                for (uint32_t cw = 0; cw < p.ncw; ++cw) {
-                    const uint32_t c = cw * 32u + lane;
-                    uint64_t N;
-                    const uint64_t key = rank_key(row[c], s_bc[c], theta, c, L, N);
-                    const uint32_t u = static_cast<uint32_t>(N >> sh);
-                    ngt += u > Tu ? 1u : 0u;
-                    const uint32_t tie = __ballot_sync(0xffffffffu, u == Tu);
-                    const uint32_t pos = nties + __popc(tie & ((1u << lane) - 1u));
-                    if (u == Tu && pos < 64u) tie_list[pos] = key;
-                    nties += __popc(tie);
-                }
-                ngt = __reduce_add_sync(0xffffffffu, ngt);
-                const uint32_t need = p.k - ngt;  // >= 1 by construction of Tu
-                __syncwarp();
-                if (nties <= 64u) {
-                    const uint64_t k0 = lane < nties ? tie_list[lane] : 0ull;
-                    const uint64_t k1 = lane + 32u < nties ? tie_list[lane + 32u] : 0ull;
-                    for (int bit = static_cast<int>(p.keyBits) - 1; bit >= 0; --bit) {
-                        const uint64_t cand = T2 | (1ull << bit);
-                        const uint32_t cnt = (k0 >= cand ? 1u : 0u) + (k1 >= cand ? 1u : 0u);
-                        if (__reduce_add_sync(0xffffffffu, cnt) >= need) T2 = cand;
-                    }
-                } else {  // many ties: search over all tied columns in place
-                    for (int bit = static_cast<int>(p.keyBits) - 1; bit >= 0; --bit) {
-                        const uint64_t cand = T2 | (1ull << bit);
-                        uint32_t cnt = 0;
-                        for (uint32_t c = lane; c < p.C32; c += 32u) {
-                            uint64_t N;
-                            const uint64_t key = rank_key(row[c], s_bc[c], theta, c, L, N);
-                            cnt += (static_cast<uint32_t>(N >> sh) == Tu && key >= cand) ? 1u : 0u;
-                        }
-                        if (__reduce_add_sync(0xffffffffu, cnt) >= need) T2 = cand;
-                    }
-                }
-                __syncwarp();
-            }
+            global_general_threshold<NU>(row, s_bc, p.C32, p.ncw, p.k, theta, sh, L, p.keyBits, tie_list,
+                                         lane, Tu, T2);
         }
         uint32_t total = 0;
         for (uint32_t cw = 0; cw < p.ncw; ++cw) {
@@ -413,9 +331,7 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             bool act = N > one;
             if (act) {
                 if (p.radius == 0) {
-                    const uint32_t u = static_cast<uint32_t>(N >> sh);
-                    // Tu == 0: fewer than k columns have u > 0, all of them win (floor aside)
-                    act = Tu == 0 ? u > 0 : (u > Tu || (u == Tu && key >= T2));
+                    act = global_general_wins(N, key, sh, Tu, T2);
                 } else {
                     const uint32_t lo = c >= p.radius ? c - p.radius : 0u;
                     const uint32_t hi = min(p.C - 1u, c + p.radius);

@@ -325,6 +325,7 @@ struct sp_handle {
     bool uniform_bc = true;       // all boosts equal (enables the histogram top-k)
     uint32_t batched_threads = 512;  // threads per CTA of the batched kernel
     uint32_t learn_Q = 0, learn_smem = 0;  // cluster learning: CTAs per cluster (0 = not eligible)
+    bool learn_dbl = false;                 // cluster learning: double-buffered bit-planes
     bool last_learn_cluster = false;
     // scratch and results
     uint32_t Wn = 0, sub_inputs = 0;
@@ -594,7 +595,9 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         q.num_inputs = n;
         q.g = g;
         q.Q = h->learn_Q;
-        sp::learn_cluster_smem(g, q.Q, &q.cols_per_cta);
+        sp::learn_cluster_smem(g, q.Q, &q.cols_per_cta, h->learn_dbl);
+        q.dbl_bits = h->learn_dbl ? 1u : 0u;
+        if (const char* d = std::getenv("SP_LEARN_DBG")) q.dbg = static_cast<uint32_t>(std::atoi(d));
         q.syn_stride = sp::learn_syn_stride(g.S);
         q.tpc = sp::learn_threads_per_column(q.cols_per_cta);
         q.Wn = h->Wn;
@@ -611,6 +614,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         q.bc = h->d_bc;
         q.boost = h->d_boost;
         q.bits_g = h->d_bits;
+        q.trace = h->d_trace;
         q.sdr = h->d_sdr;
         q.counts = h->d_counts;
         q.raw_out = rec ? h->d_raw_rec : nullptr;
@@ -763,17 +767,22 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
     if (h->lay.ok && h->g.whole) sp::batched_max_clusters(h->lay.smem_bytes, h->max_clusters);
     // cluster-resident learning: the largest cluster (<= 16 CTAs, >= 32 columns each) whose
     // synapse slice + bit-plane fit in shared memory and that can be co-scheduled
-    if (sp::configure_learn(h->max_smem) == cudaSuccess && !std::getenv("SP_NO_CLUSTER_LEARN")) {
+    // (the warp-level global selection holds C32 <= 2048 columns in registers)
+    if (h->g.C32 <= 2048u && sp::configure_learn(h->max_smem) == cudaSuccess &&
+        !std::getenv("SP_NO_CLUSTER_LEARN")) {
         for (uint32_t Q = 16; Q >= 1; Q /= 2) {
             if (Q > 1 && Q * 32u > h->g.C32) continue;
-            const uint32_t smem = sp::learn_cluster_smem(h->g, Q, nullptr);
-            if (static_cast<int>(smem) > h->max_smem - 1024) continue;
-            int n = 0;
-            sp::learn_max_clusters(Q, smem, &n);
-            if (n < 1) continue;
-            h->learn_Q = Q;
-            h->learn_smem = smem;
-            break;
+            for (int dbl = 1; dbl >= 0 && !h->learn_Q; --dbl) {
+                const uint32_t smem = sp::learn_cluster_smem(h->g, Q, nullptr, dbl != 0);
+                if (static_cast<int>(smem) > h->max_smem - 1024) continue;
+                int n = 0;
+                sp::learn_max_clusters(Q, smem, &n);
+                if (n < 1) continue;
+                h->learn_Q = Q;
+                h->learn_smem = smem;
+                h->learn_dbl = dbl != 0;
+            }
+            if (h->learn_Q) break;
         }
     }
     if (std::getenv("SP_TRACE")) cudaMalloc(&h->d_trace, 4096u * 6u * sizeof(uint64_t));
@@ -787,7 +796,9 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
     if (e == cudaSuccess) e = dalloc(&h->d_boost, g.C32);
     if (e == cudaSuccess) e = dalloc(&h->d_bc, g.C32);
     if (e == cudaSuccess) e = dalloc(&h->d_syn, static_cast<size_t>(g.S) * g.C32);
-    if (e == cudaSuccess) e = dalloc(&h->d_bits, static_cast<size_t>(h->sub_inputs) * h->Wn);
+    if (e == cudaSuccess)
+        e = dalloc(&h->d_bits, std::max<size_t>(static_cast<size_t>(h->sub_inputs) * h->Wn,
+                                                2u * ((h->Wn + 3u) / 4u * 4u)));
     if (e == cudaSuccess) e = dalloc(&h->d_raw, static_cast<size_t>(h->sub_inputs) * g.C32);
     if (e == cudaSuccess) e = dalloc(&h->d_sdr, cap * g.ncw);
     if (e == cudaSuccess) e = dalloc(&h->d_counts, cap);

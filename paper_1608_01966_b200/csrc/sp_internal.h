@@ -112,7 +112,11 @@ struct LearnParams {
     uint32_t* syn;             // [S][C32] idx | connected << 31 (loaded, written back)
     const uint32_t* bc;        // [C32]
     const float* boost;        // [C32]
-    uint32_t* bits_g;          // [Wn] scratch bit-plane (L2)
+    uint32_t* bits_g;          // [2][Wn rounded to 4] scratch bit-planes (L2), by input parity
+    uint32_t dbl_bits;         // two smem bit-plane buffers (load of t+1 overlaps learning of t)
+    uint32_t dbg;              // development switches (SP_LEARN_DBG): 1 no proxy fence, 2 no prefetch,
+                               // 4 no pack, 8 no selection (timing experiments only)
+    uint64_t* trace;           // nullable [6] summed phase times of CTA 0 (development aid)
     uint32_t* sdr;             // [rows][ncw]
     uint32_t* counts;          // [rows]
     uint16_t* raw_out;         // nullable
@@ -120,7 +124,7 @@ struct LearnParams {
 };
 
 // cluster learning (sp_learn.cu)
-uint32_t learn_cluster_smem(const Geometry& g, uint32_t Q, uint32_t* cols_per_cta);
+uint32_t learn_cluster_smem(const Geometry& g, uint32_t Q, uint32_t* cols_per_cta, bool dbl_bits);
 uint32_t learn_syn_stride(uint32_t S);
 uint32_t learn_threads_per_column(uint32_t cpc);
 cudaError_t configure_learn(int max_smem);

@@ -3,20 +3,20 @@
 // Learning is a recurrence over inputs (input t+1 sees input t's permanence
 // update), so it cannot be batched.  One launch processes the whole stream with a
 // thread-block cluster of Q CTAs (Q <= 16) that keeps the synapse table idx|connected
-// (synapse-major, the CTA's column slice) resident in shared memory:
+// (column-major, the CTA's column slice) resident in shared memory:
 //
-//   per input t:  pack a 1/Q slice of the frame -> global bit-plane (L2)
-//                 cluster barrier #1
-//                 every CTA loads the bit-plane into smem (ld.global.cg)
-//                 overlap of the CTA's columns (thread per column), raw counts are
-//                 broadcast to every CTA's smem through DSMEM
-//                 cluster barrier #2
-//                 every CTA runs the same exact k-winners over all columns, writes the
-//                 SDR words of its columns, and updates the permanences of its winners
+//   per input t:  every CTA loads the bit-plane of t (global, L2) into smem, and packs a
+//                 1/Q slice of input t+1 into the other global bit-plane buffer
+//                 overlap of the CTA's columns; raw counts are broadcast to every CTA's
+//                 smem through DSMEM (double-buffered by input parity)
+//                 cluster barrier: all raw counts of t, and the bit-plane of t+1, complete
+//                 every CTA runs the same exact k-winners (warp-level, sp_select.cuh), writes
+//                 the SDR words of its columns, and updates the permanences of its winners
 //                 (fp32 RN add/sub + clamp, R3) and their connected flags in smem
 //
-// Two cluster barriers per input; only the frame bytes and the winners' permanence rows
-// touch memory below L2.  DESIGN.md §4.2.
+// One cluster barrier per input; the frame of t+2 is prefetched into L2 (bulk prefetch)
+// two inputs ahead.  Only the frame bytes and the winners' permanence rows touch memory
+// below L2.  DESIGN.md §4.2.
 #include <cooperative_groups.h>
 
 #include "sp_internal.h"
@@ -30,313 +30,448 @@ namespace {
 
 constexpr uint32_t kLearnThreads = 512;
 
-__device__ __forceinline__ uint64_t key_of(uint32_t raw, uint32_t bc, uint32_t theta, uint32_t c,
-                                           uint32_t L, uint64_t& N) {
-    N = raw >= theta ? static_cast<uint64_t>(raw) * bc : 0ull;
-    return (N << L) | (((1ull << L) - 1ull) - c);
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
 }
 
-// Block-wide sum of one value per thread (all threads call it).
-__device__ __forceinline__ uint32_t block_sum(uint32_t v, uint32_t* scratch) {
-    const uint32_t lane = threadIdx.x & 31u, wi = threadIdx.x >> 5;
-    v = __reduce_add_sync(0xffffffffu, v);
-    __syncthreads();
-    if (lane == 0) scratch[wi] = v;
-    __syncthreads();
-    uint32_t t = 0;
-    for (uint32_t i = 0; i < (blockDim.x >> 5); ++i) t += scratch[i];
-    return t;
+// L2 prefetch of [ptr, ptr + bytes) by the bulk-copy engine (one instruction; a hint)
+__device__ __forceinline__ void prefetch_l2(const void* ptr, uint32_t bytes) {
+    if (bytes == 0u || (reinterpret_cast<uintptr_t>(ptr) & 15u) != 0u || (bytes & 15u) != 0u) return;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+}
+
+// L2 prefetch of this CTA's share of the bytes input t reads (whole frame: the CTA's
+// slice; patch mode: the CTA's share of the tile-row band, once per band)
+__device__ __forceinline__ void prefetch_input(const LearnParams& p, uint32_t t, uint32_t wbeg, uint32_t wend,
+                                               uint32_t q, uint32_t Q) {
+    const Geometry& g = p.g;
+    if (t >= p.num_inputs || (p.dbg & 2u)) return;
+    const uint32_t frame = t / g.P, tile = t % g.P;
+    const uint8_t* fr = p.frames + static_cast<size_t>(frame) * g.W * g.H;
+    if (g.whole) {
+        const uint32_t b0 = wbeg * 32u, b1 = min(wend * 32u, g.nbits);
+        if (b1 > b0) prefetch_l2(fr + b0, (b1 - b0) & ~15u);
+        return;
+    }
+    const uint32_t tilesx = g.W / g.pw;
+    if (t != 0u && tile % tilesx != 0u) return;  // band already prefetched
+    const uint32_t band = g.ph * g.W, ty = tile / tilesx;
+    const uint32_t lo = (band * q / Q) & ~15u, hi = q + 1u == Q ? band : (band * (q + 1u) / Q) & ~15u;
+    if (hi > lo) prefetch_l2(fr + static_cast<size_t>(ty) * band + lo, (hi - lo) & ~15u);
+}
+
+// store one SDR word of this CTA (lane 0): smem copy for the learning step, the global SDR
+// and the input's winner count
+__device__ __forceinline__ void emit_word(const LearnParams& p, uint32_t* s_sdr, uint32_t cw, uint32_t gcw,
+                                          uint32_t gin, uint32_t word, uint32_t lane) {
+    if (lane != 0u) return;
+    s_sdr[cw] = word;
+    if (gcw < p.g.ncw) {
+        p.sdr[static_cast<size_t>(gin) * p.g.ncw + gcw] = word;
+        if (word) atomicAdd(p.counts + gin, static_cast<uint32_t>(__popc(word)));
+    }
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(const LearnParams p) {
+// byte-nonzero flags of the 4 bytes of v as a nibble (bit j = byte j != 0): the high bit
+// of each byte of f is set iff the byte is nonzero; the multiply gathers the four flags
+// (at bits 0, 8, 16, 24 after the shift) into bits 21..24 without carries
+__device__ __forceinline__ uint32_t nz_nibble(uint32_t v) {
+    const uint32_t f = (((v & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | v) & 0x80808080u;
+    return (((f >> 7) * 0x00204081u) >> 21) & 0xFu;
+}
+
+// address of the first byte of word w of input t; run = its 32 bytes are contiguous
+__device__ __forceinline__ const uint8_t* word_src(const LearnParams& p, uint32_t t, uint32_t w, bool& run) {
+    const Geometry& g = p.g;
+    const uint32_t frame = t / g.P, tile = t % g.P;
+    const uint8_t* fr = p.frames + static_cast<size_t>(frame) * g.W * g.H;
+    const uint32_t q0 = w * 32u;
+    if (g.whole) {
+        run = q0 + 32u <= g.nbits;
+        return fr + q0;
+    }
+    const uint32_t tilesx = g.W / g.pw, ty = tile / tilesx, tx = tile % tilesx;
+    const uint32_t y = q0 / g.pw, x = q0 % g.pw;
+    run = x + 32u <= g.pw && q0 + 32u <= g.nbits;
+    return fr + static_cast<size_t>(ty * g.ph + y) * g.W + tx * g.pw + x;
+}
+
+// word w of input t bit by bit (ragged tails, patches narrower than 32 bits)
+__device__ __forceinline__ uint32_t pack_word_slow(const LearnParams& p, uint32_t t, uint32_t w) {
+    const Geometry& g = p.g;
+    const uint32_t frame = t / g.P, tile = t % g.P;
+    const uint8_t* fr = p.frames + static_cast<size_t>(frame) * g.W * g.H;
+    const uint32_t tilesx = g.W / g.pw, ty = tile / tilesx, tx = tile % tilesx;
+    uint32_t out = 0;
+#pragma unroll 1
+    for (uint32_t jj = 0; jj < 32u; ++jj) {
+        const uint32_t qq = w * 32u + jj;
+        if (qq >= g.nbits) break;
+        uint8_t b;
+        if (g.whole) {
+            b = fr[qq];
+        } else {
+            const uint32_t y = qq / g.pw, x = qq % g.pw;
+            b = fr[static_cast<size_t>(ty * g.ph + y) * g.W + tx * g.pw + x];
+        }
+        out |= (b != 0 ? 1u : 0u) << jj;
+    }
+    return out;
+}
+
+// this CTA's share (words [wbeg, wend)) of the bit-plane of input t -> global buffer dst
+// (bit j of word w = byte 32w+j != 0, R12), by threads [t0, t0 + nt) of the CTA; the loads
+// of U words per thread are issued before any is used (one L2 round trip per U words).
+// The stores are then made visible to the bulk-copy (async) proxy of the CTAs that read
+// the buffer after the next cluster barrier.
+__device__ __forceinline__ void pack_slice(const LearnParams& p, uint32_t t, uint32_t wbeg, uint32_t wend,
+                                           uint32_t* dst, uint32_t t0, uint32_t nt) {
+    if (threadIdx.x < t0 || threadIdx.x >= t0 + nt) return;
+    constexpr int U = 4;
+    for (uint32_t base = wbeg + threadIdx.x - t0; base < wend; base += U * nt) {
+        uint4 a[U], b[U];
+        bool vec[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t w = base + u * nt;
+            bool run = false;
+            const uint8_t* src = w < wend ? word_src(p, t, w, run) : nullptr;
+            vec[u] = run && (reinterpret_cast<uintptr_t>(src) & 15u) == 0;
+            if (vec[u]) {
+                if (p.dbg & 32u) {
+                    a[u] = __ldcg(reinterpret_cast<const uint4*>(src));
+                    b[u] = __ldcg(reinterpret_cast<const uint4*>(src + 16));
+                } else {
+                    a[u] = __ldcs(reinterpret_cast<const uint4*>(src));
+                    b[u] = __ldcs(reinterpret_cast<const uint4*>(src + 16));
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t w = base + u * nt;
+            if (vec[u])
+                dst[w] = nz_nibble(a[u].x) | nz_nibble(a[u].y) << 4 | nz_nibble(a[u].z) << 8 |
+                         nz_nibble(a[u].w) << 12 | nz_nibble(b[u].x) << 16 | nz_nibble(b[u].y) << 20 |
+                         nz_nibble(b[u].z) << 24 | nz_nibble(b[u].w) << 28;
+        }
+        // ragged / unaligned words bit by bit, after the vector registers are dead
+#pragma unroll 1
+        for (int u = 0; u < U; ++u) {
+            const uint32_t w = base + u * nt;
+            if (w < wend && !vec[u]) dst[w] = pack_word_slow(p, t, w);
+        }
+    }
+    if (!(p.dbg & 1u)) asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar))),
+                 "r"(count)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+
+// one thread: bulk copy (TMA engine) of the global bit-plane src[0, Wn) into smem dst,
+// completion counted on bar (expect_tx)
+__device__ __forceinline__ void bulk_load_bits(uint32_t* dst, const uint32_t* src, uint32_t Wn, uint64_t* bar) {
+    const uint32_t bytes = (Wn * 4u + 15u) & ~15u;
+    const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    constexpr uint32_t kChunk = 16384u;
+    for (uint32_t off = 0; off < bytes; off += kChunk) {
+        const uint32_t n = min(kChunk, bytes - off);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                static_cast<uint32_t>(__cvta_generic_to_shared(reinterpret_cast<uint8_t*>(dst) + off))),
+            "l"(reinterpret_cast<const uint8_t*>(src) + off), "r"(n), "r"(b)
+            : "memory");
+    }
+}
+
+// warp-level global k-winners of column-word gcw (r = 0); NR registers hold 64 * NR columns
+template <int NR>
+__device__ __forceinline__ uint32_t global_word(const LearnParams& p, const uint16_t* row, const uint32_t* s_bc,
+                                                uint64_t* ties, uint32_t gcw, uint32_t lane) {
+    const Geometry& g = p.g;
+    const uint32_t theta = p.min_overlap, L = g.keyL;
+    const uint32_t c = gcw * 32u + lane;
+    if (p.uniform_bc) {
+        const uint32_t r_lo = uniform_r_lo(theta, s_bc[0]);
+        uint32_t rgt, rtie, need;
+        global_uniform_threshold<NR>(row, g.C32, g.S, p.k, r_lo, lane, rgt, rtie, need);
+        uint32_t before = 0;  // ties at raw == r* in lower column-words
+        for (uint32_t d = lane; d < gcw * 32u; d += 32u) before += row[d] == rtie ? 1u : 0u;
+        before = __reduce_add_sync(0xffffffffu, before);
+        const uint32_t r = c < g.C ? row[c] : 0u;
+        const uint32_t tb = __ballot_sync(0xffffffffu, r == rtie);
+        return __ballot_sync(0xffffffffu,
+                             r >= rgt || (r == rtie && before + __popc(tb & ((1u << lane) - 1u)) < need));
+    }
+    const uint32_t sh = g.keyBits - L - 16u;
+    uint32_t Tu;
+    uint64_t T2;
+    global_general_threshold<NR>(row, s_bc, g.C32, g.ncw, p.k, theta, sh, L, g.keyBits, ties, lane, Tu, T2);
+    uint64_t N = 0, key = 0;
+    if (c < g.C) key = exact_key(row[c], s_bc[c], theta, c, L, N);
+    return __ballot_sync(0xffffffffu, c < g.C && global_general_wins(N, key, sh, Tu, T2));
+}
+
+// overlap of this CTA's columns for the input whose bit-plane is in bits; raw counts go
+// to every CTA's raw buffer (DSMEM).  tpc consecutive lanes share a column (synapses
+// s = part, part+tpc, ..) with a shuffle reduction; the padded column-major slice keeps
+// the reads conflict-free
+__device__ __forceinline__ void overlap_step(const LearnParams& p, cg::cluster_group& cluster, const uint32_t* s_syn,
+                                             const uint32_t* bits, uint16_t* raw_buf, uint32_t c0, uint32_t gin) {
+    const Geometry& g = p.g;
+    const uint32_t cpc = p.cols_per_cta, ss = p.syn_stride, tpc = p.tpc, Q = p.Q;
+    for (uint32_t base = 0; base < cpc * tpc; base += blockDim.x) {
+        const uint32_t slot = base + threadIdx.x;
+        const uint32_t cl = slot / tpc, part = slot % tpc;
+        uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+        if (cl < cpc) {
+            const uint32_t* col = s_syn + cl * ss;
+            uint32_t s = part;
+            for (; s + 3u * tpc < g.S; s += 4u * tpc) {  // four independent lookups
+                const uint32_t e0 = col[s], e1 = col[s + tpc], e2 = col[s + 2u * tpc], e3 = col[s + 3u * tpc];
+                r0 += (bits[(e0 & 0x7FFFFFFFu) >> 5] >> (e0 & 31u)) & (e0 >> 31);
+                r1 += (bits[(e1 & 0x7FFFFFFFu) >> 5] >> (e1 & 31u)) & (e1 >> 31);
+                r2 += (bits[(e2 & 0x7FFFFFFFu) >> 5] >> (e2 & 31u)) & (e2 >> 31);
+                r3 += (bits[(e3 & 0x7FFFFFFFu) >> 5] >> (e3 & 31u)) & (e3 >> 31);
+            }
+            for (; s < g.S; s += tpc) {
+                const uint32_t e = col[s];
+                r0 += (bits[(e & 0x7FFFFFFFu) >> 5] >> (e & 31u)) & (e >> 31);
+            }
+        }
+        uint32_t raw = (r0 + r1) + (r2 + r3);
+        for (uint32_t d = tpc >> 1; d > 0; d >>= 1) raw += __shfl_xor_sync(0xffffffffu, raw, d);
+        const uint32_t c = c0 + cl;
+        if (part == 0 && cl < cpc && c < g.C32) {
+            for (uint32_t r = 0; r < Q; ++r) cluster.map_shared_rank(raw_buf, r)[c] = static_cast<uint16_t>(raw);
+            if (p.raw_out && c < g.C) {
+                p.raw_out[static_cast<size_t>(gin) * g.C + c] = static_cast<uint16_t>(raw);
+                p.boosted_out[static_cast<size_t>(gin) * g.C + c] =
+                    raw >= p.min_overlap ? __fmul_rn(static_cast<float>(raw), p.boost[c]) : 0.0f;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(const __grid_constant__ LearnParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ __align__(8) uint64_t s_bar;  // bulk-copy completion of the bit-plane
     cg::cluster_group cluster = cg::this_cluster();
     const Geometry& g = p.g;
     const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u;
+    const uint32_t wi = tid >> 5, nw = nthr >> 5;
     const uint32_t q = cluster.block_rank(), Q = p.Q;
     const uint32_t cpc = p.cols_per_cta;        // columns owned by this CTA (multiple of 32)
+    const uint32_t ncl = cpc / 32u;              // column-words owned
     const uint32_t c0 = q * cpc;                 // first column owned
-    const uint32_t Wn = p.Wn;
+    const uint32_t Wn = p.Wn, Wn4 = (Wn + 3u) / 4u * 4u;
+    const uint32_t C32r = (g.C32 + 3u) / 4u * 4u;
+    const uint32_t n = p.num_inputs;
 
     const uint32_t ss = p.syn_stride;                               // >= S, == 8 mod 32
     uint32_t* s_syn = reinterpret_cast<uint32_t*>(smem);           // [cpc][ss] idx | connected<<31
-    uint32_t* s_bits = s_syn + static_cast<size_t>(ss) * cpc;      // [Wn] input bit-plane
-    uint32_t* s_bc = s_bits + Wn;                                   // [C32]
-    uint16_t* s_raw = reinterpret_cast<uint16_t*>(s_bc + g.C32);    // [C32] all columns' raw
-    uint32_t* s_hist = reinterpret_cast<uint32_t*>(s_raw + g.C32 + (g.C32 & 1u));  // [S+1]
-    uint32_t* s_red = s_hist + g.S + 1u;                            // [32] block reductions
-    uint32_t* s_misc = s_red + 32u;                                 // [4]
-    uint32_t* s_sdr = s_misc + 4u;                                  // [cpc/32] this CTA's SDR words
-    uint32_t* s_planes = s_sdr + cpc / 32u;                         // [ncw][nb] raw bit-planes
+    uint32_t* s_bits = s_syn + static_cast<size_t>(ss) * cpc;      // [1 or 2][Wn4] input bit-planes
+    uint32_t* s_bc = s_bits + (p.dbl_bits ? 2u : 1u) * Wn4;         // [C32]
+    uint16_t* s_raw = reinterpret_cast<uint16_t*>(s_bc + g.C32);    // [2][C32r] raw, by input parity
+    uint64_t* s_ties = reinterpret_cast<uint64_t*>(s_raw + 2u * C32r);  // [ncl][64] tie lists
+    uint32_t* s_sdr = reinterpret_cast<uint32_t*>(s_ties + ncl * 64u);  // [ncl] SDR words
+    uint32_t* s_planes = s_sdr + ncl;                               // [ncw][16] key bit-planes
+    auto bits_of = [&](uint32_t t) { return s_bits + (p.dbl_bits ? (t & 1u) * Wn4 : 0u); };
+    auto gbits_of = [&](uint32_t t) { return p.bits_g + (t & 1u) * Wn4; };
 
-    // ---- resident state: this CTA's synapse slice, Bc -----------------------------------
+    // ---- resident state: this CTA's synapse slice, Bc; counts zeroed ---------------------
     for (uint32_t i = tid; i < g.S * cpc; i += nthr) {
         const uint32_t s = i / cpc, cl = i % cpc, c = c0 + cl;
         s_syn[cl * ss + s] = c < g.C32 ? p.syn[static_cast<size_t>(s) * g.C32 + c] : 0u;
     }
     for (uint32_t c = tid; c < g.C32; c += nthr) s_bc[c] = p.bc[c];
-    __syncthreads();
+    if (q == 0)
+        for (uint32_t i = tid; i < n; i += nthr) p.counts[p.first_input + i] = 0u;
+    if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
 
     const uint32_t theta = p.min_overlap, L = g.keyL;
-    const uint64_t one = 1ull << 23;
     const uint32_t wbeg = q * Wn / Q, wend = (q + 1) * Wn / Q;  // packed words of this CTA
+    uint64_t* trace = (p.trace && q == 0 && tid == 0) ? p.trace : nullptr;
+    // phase accumulators of the traced threads live in smem (no registers held in the loop)
+    __shared__ uint64_t s_tr[8];
+    uint64_t& t_ld = s_tr[0];
+    uint64_t& t_ov = s_tr[1];
+    uint64_t& t_bar = s_tr[2];
+    uint64_t& t_sel = s_tr[3];
+    uint64_t& t_learn = s_tr[4];
+    uint64_t& t_ph = s_tr[5];
+    uint64_t& t_sub = s_tr[6];
+    uint64_t& t_pk = s_tr[7];
+    if (tid == 0)
+        for (int i = 0; i < 8; ++i) s_tr[i] = 0;
+    uint32_t phase = 0;  // parity of s_bar's next completion
+    // selection warps (global inhibition): one per owned column-word; the others pack
+    const uint32_t nsel = ncl < nw ? ncl : nw;
+    const uint32_t tpk0 = nsel < nw ? nsel * 32u : 0u, npk = nthr - tpk0;
+    // the first packing thread also traces its own phase (selection vs pack)
+    uint64_t* trace_pk = (p.trace && q == 0 && tid == tpk0 && tpk0 != 0u) ? p.trace : nullptr;
 
-    for (uint32_t t = 0; t < p.num_inputs; ++t) {
+    // ---- prologue: bit-planes of inputs 0 and 1; overlap of input 0 ----------------------
+    if (tid == 0)
+        for (uint32_t t = 0; t < 3u; ++t) prefetch_input(p, t, wbeg, wend, q, Q);
+    if (n > 0) pack_slice(p, 0, wbeg, wend, gbits_of(0), 0, nthr);
+    if (n > 1) pack_slice(p, 1, wbeg, wend, gbits_of(1), 0, nthr);
+    cluster.sync();  // bit-planes 0 (and 1) complete; smem and counts initialised
+    if (n > 0) {
+        if (tid == 0) bulk_load_bits(bits_of(0), gbits_of(0), Wn, &s_bar);
+        mbar_wait(&s_bar, phase);
+        phase ^= 1u;
+        overlap_step(p, cluster, s_syn, bits_of(0), s_raw, c0, p.first_input);
+    }
+    cluster.sync();  // raw counts of input 0 everywhere
+
+    for (uint32_t t = 0; t < n; ++t) {
         const uint32_t gin = p.first_input + t;
-        if (q == 0 && tid == 0) p.counts[gin] = 0u;  // winners are added after barrier #2
-        // ---- a1: pack this CTA's slice of input t into the global bit-plane --------------
-        {
-            const uint32_t frame = t / g.P, tile = t % g.P;
-            const uint8_t* fr = p.frames + static_cast<size_t>(frame) * g.W * g.H;
-            const bool vec = g.whole && (g.nbits % 16u) == 0 && (reinterpret_cast<uintptr_t>(fr) & 15u) == 0;
-            const uint32_t tilesx = g.W / g.pw;
-            const uint32_t ty = tile / tilesx, tx = tile % tilesx;
-            for (uint32_t w = wbeg + tid; w < wend; w += nthr) {
-                const uint32_t q0 = w * 32u;
-                uint32_t out = 0;
-                if (vec && q0 + 32u <= g.nbits) {
-                    const uint4 a = __ldcs(reinterpret_cast<const uint4*>(fr + q0));
-                    const uint4 b = __ldcs(reinterpret_cast<const uint4*>(fr + q0 + 16));
-                    const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-                    for (int k = 0; k < 8; ++k)
-#pragma unroll
-                        for (int by = 0; by < 4; ++by)
-                            out |= (((v[k] >> (8 * by)) & 0xFFu) != 0u ? 1u : 0u) << (4 * k + by);
-                } else {
-                    for (uint32_t jj = 0; jj < 32u; ++jj) {
-                        const uint32_t qq = q0 + jj;
-                        if (qq >= g.nbits) break;
-                        const uint32_t y = qq / g.pw, x = qq % g.pw;
-                        out |= (fr[static_cast<size_t>(ty * g.ph + y) * g.W + tx * g.pw + x] != 0 ? 1u : 0u) << jj;
-                    }
-                }
-                p.bits_g[w] = out;
-            }
+        const uint16_t* raw_t = s_raw + (t & 1u) * C32r;
+        const bool more = t + 1u < n;
+        if (trace) t_ph = globaltimer();
+        if (tid == 0) {
+            prefetch_input(p, t + 3u, wbeg, wend, q, Q);
+            // bit-plane of t+1 (complete since the last barrier) into its smem buffer; with
+            // one buffer it must wait until learning of t is done with the current plane
+            if (more && p.dbl_bits && !(p.dbg & 16u)) bulk_load_bits(bits_of(t + 1u), gbits_of(t + 1u), Wn, &s_bar);
         }
-        cluster.sync();  // #1: the whole bit-plane of input t is in global memory (L2)
-        {
-            const uint32_t n4 = Wn / 4u;
-            const uint4* src = reinterpret_cast<const uint4*>(p.bits_g);
-            for (uint32_t w = tid; w < n4; w += nthr) reinterpret_cast<uint4*>(s_bits)[w] = __ldcg(src + w);
-            for (uint32_t w = n4 * 4u + tid; w < Wn; w += nthr) s_bits[w] = __ldcg(p.bits_g + w);
-        }
-        __syncthreads();
-
-        // ---- a2: overlap of this CTA's columns; raw counts to every CTA (DSMEM) ----------
-        // tpc consecutive lanes share a column (synapses s = part, part+tpc, ..), then a
-        // shuffle reduction; the padded column-major slice keeps the reads conflict-free
-        for (uint32_t base = 0; base < cpc * p.tpc; base += nthr) {
-            const uint32_t slot = base + tid;
-            const uint32_t cl = slot / p.tpc, part = slot % p.tpc;
-            uint32_t raw = 0;
-            if (cl < cpc) {
-                const uint32_t* col = s_syn + cl * ss;
-                for (uint32_t s = part; s < g.S; s += p.tpc) {
-                    const uint32_t e = col[s];
-                    raw += (s_bits[(e & 0x7FFFFFFFu) >> 5] >> (e & 31u)) & (e >> 31);
-                }
-            }
-            for (uint32_t d = p.tpc >> 1; d > 0; d >>= 1) raw += __shfl_xor_sync(0xffffffffu, raw, d);
-            const uint32_t c = c0 + cl;
-            if (part == 0 && cl < cpc && c < g.C32) {
-                for (uint32_t r = 0; r < Q; ++r) cluster.map_shared_rank(s_raw, r)[c] = static_cast<uint16_t>(raw);
-                if (p.raw_out && c < g.C) {
-                    p.raw_out[static_cast<size_t>(gin) * g.C + c] = static_cast<uint16_t>(raw);
-                    p.boosted_out[static_cast<size_t>(gin) * g.C + c] =
-                        raw >= theta ? __fmul_rn(static_cast<float>(raw), p.boost[c]) : 0.0f;
-                }
-            }
-        }
-        cluster.sync();  // #2: every CTA holds all raw counts of input t
-
-        // ---- a3/a4: the same exact k-winners in every CTA ---------------------------------
-        int rstar = -1;
-        uint32_t need = 0;
-        uint64_t T = 0;
-        if (p.radius == 0 && p.uniform_bc) {
-            // histogram of the eligible raw counts; r* = largest r with #{raw >= r} >= k
-            for (uint32_t b = tid; b <= g.S; b += nthr) s_hist[b] = 0u;
-            __syncthreads();
-            for (uint32_t c = tid; c < g.C; c += nthr) {
-                const uint32_t r = s_raw[c];
-                if (r >= theta) atomicAdd(&s_hist[r], 1u);
-            }
-            __syncthreads();
-            if (tid < 32) {
-                const uint32_t B = (g.S + 1u + 31u) / 32u;
-                const uint32_t lo = tid * B;
-                uint32_t mine = 0;
-                for (uint32_t b = 0; b < B; ++b)
-                    if (lo + b <= g.S) mine += s_hist[lo + b];
-                uint32_t incl = mine;
-#pragma unroll
-                for (uint32_t d = 1; d < 32u; d <<= 1) {
-                    const uint32_t v = __shfl_down_sync(0xffffffffu, incl, d);
-                    if (tid + d < 32u) incl += v;
-                }
-                const uint32_t crossing = __ballot_sync(0xffffffffu, incl >= p.k);
-                int rs = -1;
-                uint32_t nd = 0;
-                if (crossing) {
-                    const uint32_t Lc = 31u - __clz(crossing);
-                    uint32_t acc = __shfl_sync(0xffffffffu, incl - mine, Lc);
-                    if (tid == Lc) {
-                        for (int b = static_cast<int>(B) - 1; b >= 0; --b) {
-                            const uint32_t r = lo + b;
-                            if (r > g.S) continue;
-                            if (acc + s_hist[r] >= p.k) {
-                                rs = static_cast<int>(r);
-                                nd = p.k - acc;
-                                break;
-                            }
-                            acc += s_hist[r];
-                        }
-                    }
-                    rs = __shfl_sync(0xffffffffu, rs, Lc);
-                    nd = __shfl_sync(0xffffffffu, nd, Lc);
-                }
-                if (tid == 0) {
-                    s_misc[0] = static_cast<uint32_t>(rs);
-                    s_misc[1] = nd;
-                }
-            }
-            __syncthreads();
-            rstar = static_cast<int>(s_misc[0]);
-            need = s_misc[1];
-        } else if (p.radius == 0) {
-            // exact bitwise search of the k-th largest key with block-wide counts
-            for (int bit = static_cast<int>(g.keyBits) - 1; bit >= 0; --bit) {
-                const uint64_t cand = T | (1ull << bit);
-                uint32_t cnt = 0;
-                for (uint32_t c = tid; c < g.C32; c += nthr) {
-                    uint64_t N;
-                    cnt += key_of(s_raw[c], s_bc[c], theta, c, L, N) >= cand ? 1u : 0u;
-                }
-                if (block_sum(cnt, s_red) >= p.k) T = cand;
-            }
-        }
-        // winners of this CTA's columns -> SDR words; ties among raw == r* go to the lowest
-        // indices over ALL columns, so count the ties before this CTA's range first
-        uint32_t ties_before = 0;
-        if (p.radius == 0 && p.uniform_bc && rstar >= 0) {
-            uint32_t cnt = 0;
-            for (uint32_t c = tid; c < c0 && c < g.C; c += nthr) {
-                const uint32_t r = s_raw[c];
-                cnt += (static_cast<int>(r) == rstar && static_cast<uint64_t>(r) * s_bc[c] > one) ? 1u : 0u;
-            }
-            ties_before = block_sum(cnt, s_red);
-        }
-        const uint32_t wi = tid >> 5, nw = nthr >> 5;
-        if (p.radius > 0 && p.uniform_bc) {
-            // local inhibition, uniform boost: bit-sliced window comparator (sp_select.cuh)
+        // ---- a3/a4: the same exact k-winners in every CTA (sp_select.cuh), while the
+        //      other warps pack input t+2 into the global buffer input t used ----------
+        if (p.radius > 0) {
+            const bool uni = p.uniform_bc != 0u;
             const uint32_t r_lo = uniform_r_lo(theta, s_bc[0]);
             const uint32_t nb = raw_bits(g.S);
-            build_raw_planes(s_raw, s_planes, g.ncw, nb, r_lo, wi, nw, lane);
-            __syncthreads();
-            for (uint32_t cw = wi; cw < cpc / 32u; cw += nw) {
-                const uint32_t gcw = c0 / 32u + cw;
-                uint32_t word = 0u;
-                if (gcw < g.ncw)
-                    word = local_uniform_word(s_raw, s_planes, g.ncw, nb, gcw, g.C, p.radius, p.k, r_lo, lane);
-                if (lane == 0) {
-                    s_sdr[cw] = word;
-                    if (gcw < g.ncw) {
-                        p.sdr[static_cast<size_t>(gin) * g.ncw + gcw] = word;
-                        if (word) atomicAdd(p.counts + gin, static_cast<uint32_t>(__popc(word)));
-                    }
-                }
-            }
-        } else if (p.radius > 0) {
-            // local inhibition, per-column boosts: coarse bit-sliced + exact ties
             const uint32_t sh = g.keyBits - L - 16u;
-            build_coarse_planes(s_raw, s_bc, s_planes, g.ncw, theta, sh, wi, nw, lane);
+            if (uni) build_raw_planes(raw_t, s_planes, g.ncw, nb, r_lo, wi, nw, lane);
+            else build_coarse_planes(raw_t, s_bc, s_planes, g.ncw, theta, sh, wi, nw, lane);
             __syncthreads();
-            for (uint32_t cw = wi; cw < cpc / 32u; cw += nw) {
+            for (uint32_t cw = wi; cw < ncl; cw += nw) {
                 const uint32_t gcw = c0 / 32u + cw;
                 uint32_t word = 0u;
                 if (gcw < g.ncw)
-                    word = local_general_word(s_raw, s_bc, s_planes, g.ncw, gcw, g.C, p.radius, p.k, theta,
-                                              sh, L, lane);
-                if (lane == 0) {
-                    s_sdr[cw] = word;
-                    if (gcw < g.ncw) {
-                        p.sdr[static_cast<size_t>(gin) * g.ncw + gcw] = word;
-                        if (word) atomicAdd(p.counts + gin, static_cast<uint32_t>(__popc(word)));
-                    }
-                }
+                    word = uni ? local_uniform_word(raw_t, s_planes, g.ncw, nb, gcw, g.C, p.radius, p.k, r_lo, lane)
+                               : local_general_word(raw_t, s_bc, s_planes, g.ncw, gcw, g.C, p.radius, p.k, theta,
+                                                    sh, L, lane);
+                emit_word(p, s_sdr, cw, gcw, gin, word, lane);
             }
-        } else
-        for (uint32_t cw = wi; cw < cpc / 32u; cw += nw) {
-            const uint32_t c = c0 + cw * 32u + lane;
-            bool act = false;
-            uint32_t tb = 0;
-            if (c < g.C) {
-                uint64_t N;
-                const uint64_t key = key_of(s_raw[c], s_bc[c], theta, c, L, N);
-                act = N > one;
-                if (act) {
-                    if (p.radius == 0 && p.uniform_bc) {
-                        act = rstar < 0 || static_cast<int>(s_raw[c]) > rstar;
-                    } else if (p.radius == 0) {
-                        act = key >= T;
-                    } else {
-                        const uint32_t lo = c >= p.radius ? c - p.radius : 0u;
-                        const uint32_t hi = min(g.C - 1u, c + p.radius);
-                        uint32_t beats = 0;
-                        for (uint32_t d = lo; d <= hi && beats < p.k; ++d) {
-                            uint64_t Nd;
-                            beats += (d != c && key_of(s_raw[d], s_bc[d], theta, d, L, Nd) > key) ? 1u : 0u;
-                        }
-                        act = beats < p.k;
-                    }
+        } else {
+            for (uint32_t cw = wi; cw < ncl; cw += nw) {
+                const uint32_t gcw = c0 / 32u + cw;
+                uint32_t word = 0u;
+                if (gcw < g.ncw && !(p.dbg & 8u)) {
+                    uint64_t* ties = s_ties + cw * 64u;
+                    // NR registers hold 64 * NR columns (two per register)
+                    word = g.C32 <= 512u    ? global_word<8>(p, raw_t, s_bc, ties, gcw, lane)
+                           : g.C32 <= 1024u ? global_word<16>(p, raw_t, s_bc, ties, gcw, lane)
+                                            : global_word<32>(p, raw_t, s_bc, ties, gcw, lane);
                 }
-            }
-            if (p.radius == 0 && p.uniform_bc && rstar >= 0) {
-                // ties at raw == r*: rank by column index across the whole SP
-                const bool tie = c < g.C && static_cast<int>(s_raw[c]) == rstar &&
-                                 static_cast<uint64_t>(s_raw[c]) * s_bc[c] > one;
-                tb = __ballot_sync(0xffffffffu, tie);
-                // ties in earlier column-words of this CTA
-                uint32_t earlier = 0;
-                for (uint32_t cw2 = 0; cw2 < cw; ++cw2) {
-                    const uint32_t c2 = c0 + cw2 * 32u + lane;
-                    const bool t2 = c2 < g.C && static_cast<int>(s_raw[c2]) == rstar &&
-                                    static_cast<uint64_t>(s_raw[c2]) * s_bc[c2] > one;
-                    earlier += __popc(__ballot_sync(0xffffffffu, t2));
-                }
-                if (tie) act = ties_before + earlier + __popc(tb & ((1u << lane) - 1u)) < need;
-            }
-            const uint32_t word = __ballot_sync(0xffffffffu, act);
-            if (lane == 0) {
-                s_sdr[cw] = word;
-                if (c0 / 32u + cw < g.ncw) {
-                    p.sdr[static_cast<size_t>(gin) * g.ncw + c0 / 32u + cw] = word;
-                    if (word) atomicAdd(p.counts + gin, static_cast<uint32_t>(__popc(word)));
-                }
+                emit_word(p, s_sdr, cw, gcw, gin, word, lane);
             }
         }
-        // ---- a5: permanence update of this CTA's winners (warp per column) ---------------
+        if (trace) t_sub += globaltimer() - t_ph;  // selection alone (warp 0)
+        uint64_t tp0 = 0;
+        if (trace_pk) tp0 = globaltimer();
+        if (t + 2u < n && !(p.dbg & 4u)) pack_slice(p, t + 2u, wbeg, wend, gbits_of(t + 2u), tpk0, npk);
+        if (trace_pk) t_pk += globaltimer() - tp0;
         __syncthreads();  // s_sdr complete
+        if (trace) {
+            t_sel += globaltimer() - t_ph;
+            t_ph = globaltimer();
+        }
+        // ---- a5: permanence update of this CTA's winners (warp per column) ---------------
+        // idx from the resident slice; the perm row is read in batches of 8 values per lane
+        // (independent loads, one L2 round trip), updated (fp32 RN add/sub + clamp, R3) and
+        // written back with the refreshed connected flags
+        const uint32_t* bits_t = bits_of(t);
         for (uint32_t cl = wi; cl < cpc; cl += nw) {
             const uint32_t c = c0 + cl;
             if (c >= g.C) break;
             if (((s_sdr[cl >> 5] >> (cl & 31u)) & 1u) == 0u) continue;
-            const uint32_t* idx = p.idx + static_cast<size_t>(c) * g.S;
-            float* perm = p.perm + static_cast<size_t>(c) * g.S;
-            for (uint32_t s = lane; s < g.S; s += 32u) {
-                const uint32_t i = idx[s];
-                const bool on = ((s_bits[i >> 5] >> (i & 31u)) & 1u) != 0u;
-                float v = on ? __fadd_rn(perm[s], p.inc) : __fsub_rn(perm[s], p.dec);
-                v = fminf(fmaxf(v, 0.0f), 1.0f);
-                perm[s] = v;
-                s_syn[cl * ss + s] = i | (v >= p.tau ? 0x80000000u : 0u);
+            float* __restrict__ perm = p.perm + static_cast<size_t>(c) * g.S;
+            uint32_t* col = s_syn + cl * ss;
+            for (uint32_t s0 = 0; s0 < g.S; s0 += 256u) {
+                float v[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t s = s0 + 32u * j + lane;
+                    v[j] = s < g.S ? __ldcg(perm + s) : 0.0f;
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t s = s0 + 32u * j + lane;
+                    if (s < g.S) {
+                        const uint32_t i = col[s] & 0x7FFFFFFFu;
+                        const bool on = ((bits_t[i >> 5] >> (i & 31u)) & 1u) != 0u;
+                        float x = on ? __fadd_rn(v[j], p.inc) : __fsub_rn(v[j], p.dec);
+                        x = fminf(fmaxf(x, 0.0f), 1.0f);
+                        perm[s] = x;
+                        col[s] = i | (x >= p.tau ? 0x80000000u : 0u);
+                    }
+                }
             }
         }
-        __syncthreads();  // smem flags updated before the next input's overlap
+        __syncthreads();  // flags updated (and, with one buffer, the plane of t released)
+        if (trace) {
+            t_learn += globaltimer() - t_ph;
+            t_ph = globaltimer();
+        }
+        if (!more) break;
+        // ---- a1/a2 of input t+1: its bit-plane, then the overlap of this CTA's columns ------
+        if (tid == 0 && (!p.dbl_bits || (p.dbg & 16u))) bulk_load_bits(bits_of(t + 1u), gbits_of(t + 1u), Wn, &s_bar);
+        mbar_wait(&s_bar, phase);
+        phase ^= 1u;
+        if (trace) {
+            t_ld += globaltimer() - t_ph;
+            t_ph = globaltimer();
+        }
+        // raw counts of t+1 go to the other parity buffer: a CTA still selecting input t
+        // reads this one; the buffer of t is rewritten (input t+2) only after every CTA has
+        // passed the barrier below
+        overlap_step(p, cluster, s_syn, bits_of(t + 1u), s_raw + ((t + 1u) & 1u) * C32r, c0, gin + 1u);
+        if (trace) {
+            t_ov += globaltimer() - t_ph;
+            t_ph = globaltimer();
+        }
+        cluster.sync();  // raw counts of t+1 everywhere; bit-plane of t+2 complete
+        if (trace) t_bar += globaltimer() - t_ph;
     }
+    if (trace) {
+        trace[0] = t_ld;
+        trace[1] = t_ov;
+        trace[2] = t_bar;
+        trace[3] = t_sel;
+        trace[4] = t_learn;
+        trace[5] = n;
+        trace[6] = t_sub;
+    }
+    if (trace_pk) trace_pk[7] = t_pk;
     // ---- write the resident connected flags back (the per-input path reads them) ---------
     for (uint32_t i = tid; i < g.S * cpc; i += nthr) {
         const uint32_t s = i / cpc, cl = i % cpc, c = c0 + cl;
@@ -353,12 +488,12 @@ uint32_t learn_threads_per_column(uint32_t cpc) {
     return t;
 }
 
-uint32_t learn_cluster_smem(const Geometry& g, uint32_t Q, uint32_t* cols_per_cta) {
+uint32_t learn_cluster_smem(const Geometry& g, uint32_t Q, uint32_t* cols_per_cta, bool dbl_bits) {
     const uint32_t cpc = ((g.C32 + Q - 1u) / Q + 31u) / 32u * 32u;
-    const uint32_t Wn = (g.nbits + 31u) / 32u;
+    const uint32_t Wn4 = ((g.nbits + 31u) / 32u + 3u) / 4u * 4u;
     if (cols_per_cta) *cols_per_cta = cpc;
-    return 4u * (learn_syn_stride(g.S) * cpc + (Wn + 3u) / 4u * 4u + g.C32) + 2u * (g.C32 + (g.C32 & 1u)) +
-           4u * (g.S + 1u + 32u + 4u) + 4u * (cpc / 32u) + 4u * (g.ncw * 16u);
+    return 4u * (learn_syn_stride(g.S) * cpc + (dbl_bits ? 2u : 1u) * Wn4 + g.C32) +
+           4u * ((g.C32 + 3u) / 4u * 4u) + 8u * (cpc / 32u * 64u) + 4u * (cpc / 32u) + 4u * (g.ncw * 16u);
 }
 
 cudaError_t configure_learn(int max_smem) {

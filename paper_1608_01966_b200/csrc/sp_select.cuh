@@ -14,6 +14,8 @@
 
 #include <cstdint>
 
+#include <cuda_fp16.h>
+
 namespace sp {
 
 // planes[cw * nb + b] = bit b of x over the 32 columns of word cw, for cw = cw0, cw0+step, ..
@@ -175,6 +177,140 @@ __device__ __forceinline__ uint32_t local_general_word(const RowT* row, const ui
 // r_lo = smallest raw passing both the cutoff (raw >= theta) and the floor raw*Bc > 2^23.
 __device__ __forceinline__ uint32_t uniform_r_lo(uint32_t theta, uint32_t bc) {
     return max(theta, (1u << 23) / bc + 1u);
+}
+
+// ---- global inhibition (r = 0), one warp ------------------------------------------------
+// Uniform boost (R6, R7): the key order is (raw desc, index asc) and the floor is raw >= r_lo,
+// so the k winners are: raw >= rgt, plus the first `need` columns (by index) with
+// raw == rtie.  r* = largest r with #{raw >= max(r, r_lo)} >= k, by a bitwise search over
+// the raw bits; the counts come from raw values packed two per half2 (exact: raw <= 1023)
+// with HSET2/HADD2 (no atomics, no block barrier).  NH half2 registers cover 64*NH columns.
+template <int NH, typename RowT>
+__device__ __forceinline__ void global_uniform_threshold(const RowT* row, uint32_t C32, uint32_t S,
+                                                         uint32_t k, uint32_t r_lo, uint32_t lane,
+                                                         uint32_t& rgt, uint32_t& rtie,
+                                                         uint32_t& need) {
+    __half2 hr[NH];
+#pragma unroll
+    for (int t = 0; t < NH; ++t) {
+        const uint32_t ca = (2u * t) * 32u + lane, cb = ca + 32u;
+        uint32_t ra = ca < C32 ? static_cast<uint32_t>(row[ca]) : 0u;
+        uint32_t rb = cb < C32 ? static_cast<uint32_t>(row[cb]) : 0u;
+        ra = ra >= r_lo ? ra : 0u;
+        rb = rb >= r_lo ? rb : 0u;
+        hr[t] = __halves2half2(__uint2half_rn(ra), __uint2half_rn(rb));
+    }
+    auto count_ge = [&](uint32_t x) -> uint32_t {
+        const __half2 hx = __half2half2(__uint2half_rn(x));
+        __half2 acc0 = __float2half2_rn(0.0f), acc1 = acc0;  // two chains (ILP)
+#pragma unroll
+        for (int t = 0; t < NH; t += 2) {
+            acc0 = __hadd2(acc0, __hge2(hr[t], hx));
+            if (t + 1 < NH) acc1 = __hadd2(acc1, __hge2(hr[t + 1], hx));
+        }
+        const __half2 acc = __hadd2(acc0, acc1);
+        const uint32_t mine = static_cast<uint32_t>(__low2float(acc) + __high2float(acc));
+        return __reduce_add_sync(0xffffffffu, mine);
+    };
+    rgt = r_lo;  // raw >= rgt wins outright
+    rtie = 0xFFFFFFFFu;
+    need = 0;
+    if (count_ge(r_lo) >= k) {
+        uint32_t T = 0;
+        for (int bit = 31 - __clz(S); bit >= 0; --bit)
+            if (count_ge(T | (1u << bit)) >= k) T |= 1u << bit;
+        rtie = T;
+        need = k - count_ge(T + 1u);
+        rgt = T + 1u;
+    }
+}
+
+// Per-column boosts (R4, R6): (1) the k-th largest 16-bit coarse key u = N >> sh (Tu) by a
+// bitwise search over keys packed two per register (columns 64t+lane, 64t+32+lane);
+// (2) the exact key threshold T2 among the columns tied at u == Tu (a 64-entry list in
+// tie_list, else an in-place search).  Column c wins iff N > 2^23 and
+// (Tu == 0 ? u > 0 : u > Tu || (u == Tu && key >= T2)) — see global_general_wins.
+template <int NU, typename RowT>
+__device__ __forceinline__ void global_general_threshold(const RowT* row, const uint32_t* bc,
+                                                         uint32_t C32, uint32_t ncw, uint32_t k,
+                                                         uint32_t theta, uint32_t sh, uint32_t L,
+                                                         uint32_t keyBits, uint64_t* tie_list,
+                                                         uint32_t lane, uint32_t& Tu, uint64_t& T2) {
+    Tu = 0;
+    T2 = 0;
+    uint32_t uu[NU];
+#pragma unroll
+    for (int t = 0; t < NU; ++t) {
+        const uint32_t ca = (2u * t) * 32u + lane, cb = ca + 32u;
+        uint64_t Na = 0, Nb = 0;
+        if (ca < C32) exact_key(row[ca], bc[ca], theta, ca, L, Na);
+        if (cb < C32) exact_key(row[cb], bc[cb], theta, cb, L, Nb);
+        uu[t] = static_cast<uint32_t>(Na >> sh) | (static_cast<uint32_t>(Nb >> sh) << 16);
+    }
+    for (int bit = 15; bit >= 0; --bit) {
+        const uint32_t cand = (Tu | (1u << bit)) << 16;
+        uint32_t cnt0 = 0, cnt1 = 0;
+#pragma unroll
+        for (int t = 0; t < NU; ++t) {
+            cnt0 += uu[t] >= cand ? 1u : 0u;
+            cnt1 += (uu[t] << 16) >= cand ? 1u : 0u;
+        }
+        if (__reduce_add_sync(0xffffffffu, cnt0 + cnt1) >= k) Tu |= 1u << bit;
+    }
+    if (Tu == 0) return;
+    // columns above the coarse threshold, and the exact keys of the columns tied at Tu
+    uint32_t ngt = 0, nties = 0;
+    for (uint32_t cw = 0; cw < ncw; ++cw) {
+        const uint32_t c = cw * 32u + lane;
+        uint64_t N;
+        const uint64_t key = exact_key(row[c], bc[c], theta, c, L, N);
+        const uint32_t u = static_cast<uint32_t>(N >> sh);
+        ngt += u > Tu ? 1u : 0u;
+        const uint32_t tie = __ballot_sync(0xffffffffu, u == Tu);
+        const uint32_t pos = nties + __popc(tie & ((1u << lane) - 1u));
+        if (u == Tu && pos < 64u) tie_list[pos] = key;
+        nties += __popc(tie);
+    }
+    ngt = __reduce_add_sync(0xffffffffu, ngt);
+    const uint32_t need = k - ngt;  // 1 <= need <= nties by construction of Tu
+    __syncwarp();
+    if (nties <= 64u) {
+        // T2 = the need-th largest tied key: the one with exactly need-1 larger tied keys
+        // (keys are distinct: they carry the column index)
+        const uint64_t k0 = lane < nties ? tie_list[lane] : 0ull;
+        const uint64_t k1 = lane + 32u < nties ? tie_list[lane + 32u] : 0ull;
+        uint32_t g0 = 0, g1 = 0;
+        for (uint32_t j = 0; j < nties; ++j) {
+            const uint64_t kj = tie_list[j];
+            g0 += kj > k0 ? 1u : 0u;
+            g1 += kj > k1 ? 1u : 0u;
+        }
+        const bool h0 = lane < nties && g0 + 1u == need, h1 = lane + 32u < nties && g1 + 1u == need;
+        const uint32_t src = __ffs(__ballot_sync(0xffffffffu, h0 || h1)) - 1u;
+        const uint64_t mine = h0 ? k0 : k1;
+        const uint32_t lo = __shfl_sync(0xffffffffu, static_cast<uint32_t>(mine), src);
+        const uint32_t hi = __shfl_sync(0xffffffffu, static_cast<uint32_t>(mine >> 32), src);
+        T2 = (static_cast<uint64_t>(hi) << 32) | lo;
+    } else {  // many ties: bitwise search over all tied columns in place
+        for (int bit = static_cast<int>(keyBits) - 1; bit >= 0; --bit) {
+            const uint64_t cand = T2 | (1ull << bit);
+            uint32_t cnt = 0;
+            for (uint32_t c = lane; c < C32; c += 32u) {
+                uint64_t N;
+                const uint64_t key = exact_key(row[c], bc[c], theta, c, L, N);
+                cnt += (static_cast<uint32_t>(N >> sh) == Tu && key >= cand) ? 1u : 0u;
+            }
+            if (__reduce_add_sync(0xffffffffu, cnt) >= need) T2 = cand;
+        }
+    }
+    __syncwarp();  // tie_list is reused by the caller's next input
+}
+
+__device__ __forceinline__ bool global_general_wins(uint64_t N, uint64_t key, uint32_t sh, uint32_t Tu,
+                                                    uint64_t T2) {
+    if (N <= (1ull << 23)) return false;
+    const uint32_t u = static_cast<uint32_t>(N >> sh);
+    return Tu == 0 ? u > 0 : (u > Tu || (u == Tu && key >= T2));
 }
 
 // bits needed for raw values 0..S
