@@ -236,8 +236,7 @@ def main():
         info = sp.info()
         learn = {"frames": nl, "ms": ms, "us_per_frame": ms * 1e3 / nl, "frames_per_s": nl / ms * 1e3,
                  "kernel_launches": sp.kernel_launches() - l0,
-                 "path": (f"cluster-resident kernel, {info['learn_cluster']} CTAs"
-                          if info["last_learn_cluster"] else "per-input kernels"),
+                 "path": P.learn_path_name(info),
                  "workload": "BASELINE config 2 learning stream (sequential), whole 960x540 frames"}
         del lf
     if world > 1:

@@ -55,7 +55,9 @@ enum { SP_PATH_AUTO = 0, SP_PATH_PER_INPUT = 1, SP_PATH_BATCHED = 2 };
 
 /* sp_config.flags */
 enum {
-    SP_FLAG_RECORD_OVERLAPS = 1u  /* keep raw/boosted overlaps of the last call for sp_overlaps */
+    SP_FLAG_RECORD_OVERLAPS = 1u, /* keep raw/boosted overlaps of the last call for sp_overlaps */
+    SP_FLAG_LEARN_GRID = 2u       /* learn=1: prefer the grid-resident kernel (one CTA per SM) over
+                                     the cluster-resident one (default: cluster when it fits) */
 };
 
 /*
@@ -122,7 +124,15 @@ typedef struct sp_info {
     uint32_t learn_cluster;      /* CTAs per cluster of the resident learning kernel (0: learning
                                     uses the per-input kernels) */
     uint32_t last_learn_cluster; /* 1 if the last learn=1 call used the cluster kernel */
+    uint32_t learn_grid_ctas;    /* CTAs of the grid-resident learning kernel (0: not eligible) */
+    uint32_t last_learn_path;    /* path of the last learn=1 call: SP_LEARN_PER_INPUT,
+                                    SP_LEARN_CLUSTER or SP_LEARN_GRID */
 } sp_info;
+
+/* learning paths (sp_info.last_learn_path) */
+#define SP_LEARN_PER_INPUT 0u /* per-input kernels, one launch per step per input */
+#define SP_LEARN_CLUSTER 1u   /* one launch, cluster of <= 16 CTAs, synapse table in smem */
+#define SP_LEARN_GRID 2u      /* one cooperative launch, one CTA per SM, table streamed from L2 */
 
 /* Fills *cfg with Tab. 2 defaults on a 240x134 frame (Tab. 1),
  * tau 0.2, seed 42, device 0, max_inputs 4096.  Never fails for non-NULL cfg. */

@@ -327,6 +327,14 @@ struct sp_handle {
     uint32_t learn_Q = 0, learn_smem = 0;  // cluster learning: CTAs per cluster (0 = not eligible)
     bool learn_dbl = false;                 // cluster learning: double-buffered bit-planes
     bool last_learn_cluster = false;
+    // grid-resident learning (one CTA per SM; column-major synapse table streamed from L2)
+    uint32_t* d_synT = nullptr;  // [C32][S] idx | connected << 31
+    uint32_t* d_gbar = nullptr;  // grid barrier counter
+    uint32_t grid_G = 0, grid_smem = 0, grid_own = 0, grid_win = 0, grid_ccols = 0, grid_stages = 0;
+    bool grid_dbl = false;
+    bool synT_dirty = true;      // d_synT must be rebuilt from idx/perm before grid learning
+    bool syn_dirty = false;      // d_syn must be rebuilt from idx/perm before the per-input path
+    uint32_t last_learn_path = SP_LEARN_PER_INPUT;
     // scratch and results
     uint32_t Wn = 0, sub_inputs = 0;
     uint32_t* d_bits = nullptr;
@@ -362,7 +370,7 @@ void release(sp_handle* h) {
     void* ptrs[] = {h->d_trace, h->d_idx,  h->d_perm,    h->d_boost,   h->d_bc,      h->d_syn,
                     h->d_ell,  h->d_ell_off, h->d_ell_nb,  h->d_ell_pos, h->d_bits,
                     h->d_raw,  h->d_sdr,     h->d_counts,  h->d_raw_rec, h->d_boosted_rec,
-                    h->d_stage[0], h->d_stage[1]};
+                    h->d_stage[0], h->d_stage[1], h->d_synT,  h->d_gbar};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
@@ -504,6 +512,8 @@ sp_status upload_state(sp_handle* h, const uint32_t* idx, const float* perm, con
     h->launches++;
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(e, "synapse layout build");
+    h->syn_dirty = false;
+    h->synT_dirty = true;
     if (h->lay.ok) return build_ell(h, perm);
     return SP_OK;
 }
@@ -587,7 +597,70 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         if (e != cudaSuccess) return cuda_fail(e, "batched kernel launch");
         return SP_OK;
     }
-    if (learn && h->learn_Q && h->cfg.force_path != SP_PATH_PER_INPUT) {
+    const char* lp = std::getenv("SP_LEARN_PATH");  // development override: cluster | grid | input
+    const bool want_grid = learn && h->grid_G && h->cfg.force_path != SP_PATH_PER_INPUT &&
+                           (lp ? std::strcmp(lp, "grid") == 0
+                               : ((h->cfg.flags & SP_FLAG_LEARN_GRID) != 0 || h->learn_Q == 0));
+    const bool want_cluster = learn && h->learn_Q && h->cfg.force_path != SP_PATH_PER_INPUT && !want_grid &&
+                              !(lp && std::strcmp(lp, "input") == 0);
+    if (want_grid) {
+        // the whole sequential stream in one cooperative launch over the SMs
+        if (h->synT_dirty) {
+            e = sp::launch_build_synT(h->d_idx, h->d_perm, h->cfg.connected_threshold, g.C, g.C32, g.S,
+                                      h->d_synT, s);
+            h->launches++;
+            if (e != cudaSuccess) return cuda_fail(e, "column-major synapse table build");
+            h->synT_dirty = false;
+        }
+        sp::LearnGridParams q{};
+        q.frames = frames;
+        q.first_input = row0;
+        q.num_inputs = n;
+        q.g = g;
+        q.G = h->grid_G;
+        q.Wn = h->Wn;
+        q.own_words = h->grid_own;
+        q.win_words = h->grid_win;
+        q.ccols = h->grid_ccols;
+        q.stages = h->grid_stages;
+        q.dbl_bits = h->grid_dbl ? 1u : 0u;
+        q.min_overlap = h->cfg.min_overlap;
+        q.k = h->cfg.winners_set_size;
+        q.radius = h->cfg.inhibition_radius;
+        q.uniform_bc = h->uniform_bc ? 1u : 0u;
+        q.inc = h->cfg.perm_increment;
+        q.dec = h->cfg.perm_decrement;
+        q.tau = h->cfg.connected_threshold;
+        q.synT = h->d_synT;
+        q.perm = h->d_perm;
+        q.bc = h->d_bc;
+        q.boost = h->d_boost;
+        q.bits_g = h->d_bits;
+        q.raw_g = reinterpret_cast<uint16_t*>(h->d_raw);
+        q.gbar = h->d_gbar;
+        q.sdr = h->d_sdr;
+        q.counts = h->d_counts;
+        q.raw_out = rec ? h->d_raw_rec : nullptr;
+        q.boosted_out = rec ? h->d_boosted_rec : nullptr;
+        if (const char* d = std::getenv("SP_LEARN_DBG")) q.dbg = static_cast<uint32_t>(std::atoi(d));
+        q.trace = h->d_trace;
+        e = sp::launch_learn_grid(q, h->grid_smem, s);
+        h->launches++;
+        if (e != cudaSuccess) return cuda_fail(e, "grid learning launch");
+        h->ell_dirty = true;
+        h->syn_dirty = true;
+        h->last_plan.path = SP_PATH_PER_INPUT;
+        h->last_learn_cluster = false;
+        h->last_learn_path = SP_LEARN_GRID;
+        return SP_OK;
+    }
+    if (h->syn_dirty && (learn || pl.path != SP_PATH_BATCHED)) {
+        e = sp::launch_build_syn(h->d_idx, h->d_perm, h->cfg.connected_threshold, g.C, g.C32, g.S, h->d_syn, s);
+        h->launches++;
+        if (e != cudaSuccess) return cuda_fail(e, "synapse layout build");
+        h->syn_dirty = false;
+    }
+    if (want_cluster) {
         // the whole sequential stream in one launch of the cluster-resident kernel
         sp::LearnParams q{};
         q.frames = frames;
@@ -625,9 +698,15 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         h->ell_dirty = true;
         h->last_plan.path = SP_PATH_PER_INPUT;
         h->last_learn_cluster = true;
+        h->last_learn_path = SP_LEARN_CLUSTER;
+        h->synT_dirty = true;
         return SP_OK;
     }
-    if (learn) h->last_learn_cluster = false;
+    if (learn) {
+        h->last_learn_cluster = false;
+        h->last_learn_path = SP_LEARN_PER_INPUT;
+        h->synT_dirty = true;
+    }
     // per-input path, sub-batches of whole frames
     const uint32_t fpb = std::max<uint32_t>(1u, h->sub_inputs / g.P);
     for (uint32_t f0 = 0; f0 < n_frames; f0 += fpb) {
@@ -785,6 +864,31 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
             if (h->learn_Q) break;
         }
     }
+    // grid-resident learning: S % 4 == 0 (16-byte chunk rows), local inhibition or C32 <= 2048
+    // (the global selection holds the columns in registers), co-resident CTAs
+    int coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h->device);
+    if (coop && h->g.S % 4u == 0 && (h->cfg.inhibition_radius > 0 || h->g.C32 <= 2048u) &&
+        sp::configure_learn_grid(h->max_smem) == cudaSuccess) {
+        const uint32_t G = std::min<uint32_t>(static_cast<uint32_t>(h->sm_count), h->g.ncw);
+        // deepest synapse ring that fits (>= 5 stages with two bit-plane buffers, else one)
+        for (int pass = 0; pass < 2 && !h->grid_G; ++pass)
+            for (uint32_t st = 8; st >= 2 && !h->grid_G; --st) {
+                const bool dbl = pass == 0;
+                if (dbl && st < 5) break;
+                uint32_t stages = st;
+                const uint32_t smem = sp::learn_grid_smem(h->g, h->cfg.inhibition_radius, G, dbl, &h->grid_own,
+                                                          &h->grid_win, &h->grid_ccols, &stages);
+                if (static_cast<int>(smem) > h->max_smem - 2048) continue;
+                int cap = 0;
+                sp::learn_grid_max_ctas(smem, &cap);
+                if (cap < static_cast<int>(G)) continue;
+                h->grid_G = G;
+                h->grid_smem = smem;
+                h->grid_dbl = dbl;
+                h->grid_stages = st;
+            }
+    }
     if (std::getenv("SP_TRACE")) cudaMalloc(&h->d_trace, 4096u * 6u * sizeof(uint64_t));
     if (const char* et = std::getenv("SP_THREADS")) h->batched_threads = std::atoi(et) == 1024 ? 1024u : 512u;
     h->Wn = (g.nbits + 31u) / 32u;
@@ -802,6 +906,10 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
     if (e == cudaSuccess) e = dalloc(&h->d_raw, static_cast<size_t>(h->sub_inputs) * g.C32);
     if (e == cudaSuccess) e = dalloc(&h->d_sdr, cap * g.ncw);
     if (e == cudaSuccess) e = dalloc(&h->d_counts, cap);
+    if (e == cudaSuccess && h->grid_G) {
+        e = dalloc(&h->d_synT, static_cast<size_t>(g.C32) * g.S);
+        if (e == cudaSuccess) e = dalloc(&h->d_gbar, 1);
+    }
     if (e == cudaSuccess && (cfg->flags & SP_FLAG_RECORD_OVERLAPS)) {
         e = dalloc(&h->d_raw_rec, cap * g.C);
         if (e == cudaSuccess) e = dalloc(&h->d_boosted_rec, cap * g.C);
@@ -998,6 +1106,8 @@ sp_status sp_get_info(sp_handle* h, sp_info* out) {
     out->max_smem_optin = h->max_smem;
     out->learn_cluster = h->learn_Q;
     out->last_learn_cluster = h->last_learn_cluster ? 1u : 0u;
+    out->learn_grid_ctas = h->grid_G;
+    out->last_learn_path = h->last_learn_path;
     return SP_OK;
 }
 

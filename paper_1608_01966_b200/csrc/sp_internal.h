@@ -123,6 +123,41 @@ struct LearnParams {
     float* boosted_out;        // nullable
 };
 
+struct LearnGridParams {
+    const uint8_t* frames;     // frames of the call
+    uint32_t first_input;      // row of the first input in the result buffers
+    uint32_t num_inputs;       // inputs (frames x patches), processed in order
+    Geometry g;
+    uint32_t G;                // co-resident CTAs (cooperative launch, one per SM)
+    uint32_t Wn;
+    uint32_t own_words, win_words, ccols, stages;  // smem sizing (learn_grid_smem)
+    uint32_t dbl_bits;         // two smem bit-plane buffers
+    uint32_t min_overlap, k, radius, uniform_bc;
+    float inc, dec, tau;
+    uint32_t* synT;            // [C32][S] idx | connected << 31, column-major (updated)
+    float* perm;               // [C][S]
+    const uint32_t* bc;        // [C32]
+    const float* boost;        // [C32]
+    uint32_t* bits_g;          // [2][Wn rounded to 4] bit-planes, by input parity
+    uint16_t* raw_g;           // [2][C32] raw counts, by input parity
+    uint32_t* gbar;            // grid barrier counter (zeroed before the launch)
+    uint32_t* sdr;             // [rows][ncw]
+    uint32_t* counts;          // [rows]
+    uint16_t* raw_out;         // nullable
+    float* boosted_out;        // nullable
+    uint32_t dbg;              // development switches (see LearnParams)
+    uint64_t* trace;           // nullable [6] summed phase times of CTA 0 (development aid)
+};
+
+// grid learning (sp_learn_grid.cu)
+uint32_t learn_grid_smem(const Geometry& g, uint32_t radius, uint32_t G, bool dbl_bits, uint32_t* own_words,
+                         uint32_t* win_words, uint32_t* ccols, uint32_t* stages);
+cudaError_t configure_learn_grid(int max_smem);
+cudaError_t learn_grid_max_ctas(uint32_t smem, int* n);
+cudaError_t launch_learn_grid(const LearnGridParams& p, uint32_t smem, cudaStream_t s);
+cudaError_t launch_build_synT(const uint32_t* idx, const float* perm, float tau, uint32_t C, uint32_t C32,
+                              uint32_t S, uint32_t* synT, cudaStream_t s);
+
 // cluster learning (sp_learn.cu)
 uint32_t learn_cluster_smem(const Geometry& g, uint32_t Q, uint32_t* cols_per_cta, bool dbl_bits);
 uint32_t learn_syn_stride(uint32_t S);

@@ -247,6 +247,14 @@ __global__ void k_build_syn(const uint32_t* idx, const float* perm, float tau, u
     syn[static_cast<size_t>(s) * C32 + c] = v;
 }
 
+// synT[c][s] = idx | connected << 31 (column-major, grid learning); pad columns: 0.
+__global__ void k_build_synT(const uint32_t* idx, const float* perm, float tau, uint32_t C, uint32_t C32,
+                             uint32_t S, uint32_t* synT) {
+    const size_t k = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= static_cast<size_t>(C32) * S) return;
+    synT[k] = k < static_cast<size_t>(C) * S ? (idx[k] | (perm[k] >= tau ? 0x80000000u : 0u)) : 0u;
+}
+
 // Batched ELL: slot pos[c][s] holds the window-local index if connected, else the zero slot Lw.
 __global__ void k_refresh_ell(const uint32_t* idx, const float* perm, const uint32_t* pos,
                               float tau, uint32_t n, uint32_t Lw, uint16_t* ell) {
@@ -303,6 +311,13 @@ cudaError_t launch_build_syn(const uint32_t* idx, const float* perm, float tau, 
                              uint32_t C32, uint32_t S, uint32_t* syn, cudaStream_t s) {
     dim3 grid((C32 + 255u) / 256u, S);
     k_build_syn<<<grid, 256, 0, s>>>(idx, perm, tau, C, C32, S, syn);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_build_synT(const uint32_t* idx, const float* perm, float tau, uint32_t C, uint32_t C32,
+                              uint32_t S, uint32_t* synT, cudaStream_t s) {
+    const size_t n = static_cast<size_t>(C32) * S;
+    k_build_synT<<<static_cast<uint32_t>((n + 255u) / 256u), 256, 0, s>>>(idx, perm, tau, C, C32, S, synT);
     return cudaGetLastError();
 }
 

@@ -20,6 +20,15 @@ LIB_PATH = os.path.join(HERE, "libsp.so")
 SP_OK, SP_E_CONFIG, SP_E_ARG, SP_E_SHAPE, SP_E_CUDA, SP_E_OOM, SP_E_STATE = range(7)
 SP_PATH_AUTO, SP_PATH_PER_INPUT, SP_PATH_BATCHED = 0, 1, 2
 SP_FLAG_RECORD_OVERLAPS = 1
+SP_FLAG_LEARN_GRID = 2
+SP_LEARN_PER_INPUT, SP_LEARN_CLUSTER, SP_LEARN_GRID = 0, 1, 2
+
+
+def learn_path_name(info):
+    """Human-readable learning path of the last learn=1 call (sp_info.last_learn_path)."""
+    return {SP_LEARN_PER_INPUT: "per-input kernels",
+            SP_LEARN_CLUSTER: f"cluster-resident kernel, {info['learn_cluster']} CTAs",
+            SP_LEARN_GRID: f"grid-resident kernel, {info['learn_grid_ctas']} CTAs"}[info["last_learn_path"]]
 
 STATUS_NAMES = {0: "SP_OK", 1: "SP_E_CONFIG", 2: "SP_E_ARG", 3: "SP_E_SHAPE", 4: "SP_E_CUDA",
                 5: "SP_E_OOM", 6: "SP_E_STATE"}
@@ -67,7 +76,8 @@ class SpInfo(ctypes.Structure):
     _fields_ = [("plan", SpPlanInfo), ("kernel_launches", ctypes.c_uint64),
                 ("last_num_inputs", ctypes.c_uint32), ("ell_slots", ctypes.c_uint32),
                 ("sm_count", ctypes.c_int32), ("max_smem_optin", ctypes.c_int32),
-                ("learn_cluster", ctypes.c_uint32), ("last_learn_cluster", ctypes.c_uint32)]
+                ("learn_cluster", ctypes.c_uint32), ("last_learn_cluster", ctypes.c_uint32),
+                ("learn_grid_ctas", ctypes.c_uint32), ("last_learn_path", ctypes.c_uint32)]
 
 
 _lib = None

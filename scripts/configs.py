@@ -57,7 +57,7 @@ def config2():
             _, counts = sp.winners()
             print(json.dumps({"config": "BASELINE config 2", "k": k, "radius": radius,
                               "learn_frames": 992, "learn_us_per_frame": round(lms * 1e3 / 992, 2),
-                              "learn_path": "cluster" if info["last_learn_cluster"] else "per-input",
+                              "learn_path": P.learn_path_name(info),
                               "infer_frames": 4096, "infer_ms": round(ims, 4),
                               "infer_frames_per_s": round(4096 / ims * 1e3),
                               "infer_hbm_frac": round(4096 * 518528 / (ims / 1e3) / 1e9 / HBM, 4),
@@ -69,7 +69,7 @@ def config2():
                          winners_set_size=40, max_inputs=64 * 540)
     sp.compute(learn_f[:1], learn=True)
     lms = timed(lambda: sp.compute(learn_f[1:5], learn=True))
-    info = sp.info()
+    linfo = sp.info()
     pf = infer_f[:64]
     sp.compute(pf)
     ims = timed(lambda: sp.compute(pf), reps=3)
@@ -77,7 +77,7 @@ def config2():
     print(json.dumps({"config": "BASELINE config 2 (patch 32x30)", "k": 40, "radius": 0,
                       "learn_inputs": 4 * 540, "learn_us_per_input": round(lms * 1e3 / 2160, 3),
                       "learn_ms_per_frame": round(lms / 4, 3),
-                      "learn_path": "cluster",
+                      "learn_path": P.learn_path_name(linfo),
                       "infer_frames": 64, "infer_ms": round(ims, 3),
                       "infer_frames_per_s": round(64 / ims * 1e3),
                       "infer_inputs_per_s": round(64 * 540 / ims * 1e3),
@@ -98,7 +98,7 @@ def config5():
     print(json.dumps({"config": "BASELINE config 5", "columns": 16384, "synapses": 512,
                       "radius": 80, "learn_frames": 196, "learn_us_per_frame": round(lms * 1e3 / 196, 1),
                       "learn_frames_per_s": round(196 / lms * 1e3, 1),
-                      "learn_path": "cluster" if info["last_learn_cluster"] else "per-input",
+                      "learn_path": P.learn_path_name(info),
                       "mean_winners": float(counts.float().mean()),
                       "kernel_launches_per_frame": None}), flush=True)
     sp.close()

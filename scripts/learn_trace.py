@@ -19,7 +19,8 @@ import sp_inputs  # noqa: E402
 
 
 def run(label, n, boost_seeded=False, **kw):
-    sp = P.SpatialPooler(input_width=960, input_height=540, min_overlap=4, winners_set_size=40,
+    kw.setdefault("min_overlap", 4)
+    sp = P.SpatialPooler(input_width=960, input_height=540, winners_set_size=40,
                          max_inputs=max(n * 540, 64), **kw)
     if boost_seeded:
         sp.set_state(boost=sp_inputs.boosts(7, kw["num_columns"]))
@@ -36,13 +37,14 @@ def run(label, n, boost_seeded=False, **kw):
     buf = np.zeros(12, np.uint64)
     P.lib().sp_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32]
     assert P.lib().sp_debug_trace(sp._h, buf.ctypes.data, 2) == 0
-    ni = int(buf[5])
-    ph = {k: round(float(buf[i]) / ni / 1e3, 3) for i, k in
-          enumerate(["wait_bits", "overlap", "barrier", "select+pack", "learn", "", "select_only",
-                     "pack_only"]) if k}
     info = sp.info()
+    ni = max(int(buf[5]), 1)
+    names = (["bits", "overlap", "grid_barrier", "select", "learn"] if info["last_learn_path"] == 2 else
+             ["wait_bits", "overlap", "barrier", "select+pack", "learn", "", "select_only", "pack_only"])
+    ph = {k: round(float(buf[i]) / ni / 1e3, 3) for i, k in enumerate(names) if k}
     print(json.dumps({"case": label, "inputs": ni, "us_per_input": round(ms * 1e3 / ni, 3),
-                      "cluster": info["learn_cluster"], "phases_us": ph,
+                      "path": ["per-input", "cluster", "grid"][info["last_learn_path"]],
+                      "cluster": info["learn_cluster"], "grid_ctas": info["learn_grid_ctas"], "phases_us": ph,
                       "sum_us": round(sum(ph.values()), 3)}), flush=True)
     sp.close()
 
@@ -55,3 +57,5 @@ if __name__ == "__main__":
     run("whole C2048 S256 global uniform", 100, num_columns=2048, synapses_per_column=256)
     run("patch 32x30 C1024 S256 global", 2, num_columns=1024, synapses_per_column=256,
         patch_width=32, patch_height=30)
+    run("config 5: C16384 S512 r80", 30, num_columns=16384, synapses_per_column=512, min_overlap=8,
+        inhibition_radius=80)

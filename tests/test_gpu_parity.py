@@ -27,11 +27,25 @@ def to_dev(frames):
 
 
 def make_sp(cfg, state=None, path=P.SP_PATH_AUTO, max_inputs=4096, record=True):
-    sp = P.SpatialPooler(**gpu_kwargs(cfg, force_path=path, max_inputs=max_inputs,
-                                      flags=P.SP_FLAG_RECORD_OVERLAPS if record else 0))
+    """path: an SP_PATH_* value, or a learning path "cluster" | "grid" | "input"."""
+    flags = P.SP_FLAG_RECORD_OVERLAPS if record else 0
+    if isinstance(path, str):
+        flags |= P.SP_FLAG_LEARN_GRID if path == "grid" else 0
+        path = P.SP_PATH_PER_INPUT if path == "input" else P.SP_PATH_AUTO
+    sp = P.SpatialPooler(**gpu_kwargs(cfg, force_path=path, max_inputs=max_inputs, flags=flags))
     if state is not None:
         sp.set_state(*state)
     return sp
+
+
+def check_learn_path(sp, lp):
+    """the learning call ran on the requested kernel (or the documented fallback)"""
+    info = sp.info()
+    cluster = P.SP_LEARN_CLUSTER if info["learn_cluster"] else P.SP_LEARN_PER_INPUT
+    grid = P.SP_LEARN_GRID if info["learn_grid_ctas"] else cluster
+    want = {"input": P.SP_LEARN_PER_INPUT, "grid": grid,
+            "cluster": cluster if info["learn_cluster"] else grid}[lp]
+    assert info["last_learn_path"] == want, (lp, info)
 
 
 def run_gpu(sp, frames, learn=False):
@@ -95,7 +109,7 @@ def test_set_state_rejects_out_of_domain():
 # --------------------------------------------------------------------------- #
 # BASELINE config 1: tiny SP, 10 frames with learning (sequential recurrence)
 # --------------------------------------------------------------------------- #
-LEARN_PATHS = [P.SP_PATH_AUTO, P.SP_PATH_PER_INPUT]  # AUTO = cluster-resident learning kernel
+LEARN_PATHS = ["cluster", "grid", "input"]  # cluster- / grid-resident kernels, per-input kernels
 
 
 @pytest.mark.parametrize("boost_mode", ["seeded", "uniform1"])
@@ -110,6 +124,7 @@ def test_tiny_learning_bit_exact(radius, path, boost_mode):
     results = ora.compute(frames, learning=True)
     sp = make_sp(cfg, state, path)
     sdr, counts, raw, boosted = run_gpu(sp, frames, learn=True)
+    check_learn_path(sp, path)
     check_results(results, sdr, counts, raw, boosted)
     _, gperm, _ = sp.get_state()
     assert np.array_equal(gperm.view(np.uint32), ora.perm.view(np.uint32))
@@ -206,7 +221,7 @@ def test_learning_parity_small(kw, path, boost_mode):
     results = ora.compute(frames, learning=True)
     sp = make_sp(cfg, state, path, max_inputs=64)
     check_results(results, *run_gpu(sp, frames, learn=True))
-    assert sp.info()["last_learn_cluster"] == (1 if path == P.SP_PATH_AUTO else 0)
+    check_learn_path(sp, path)
     _, gperm, _ = sp.get_state()
     assert np.array_equal(gperm.view(np.uint32), ora.perm.view(np.uint32))
 
@@ -285,7 +300,7 @@ def test_full_size_learning_then_inference(path, boost_mode):
     results = ora.compute(frames, learning=True)
     sp = make_sp(cfg, state, path, max_inputs=64)
     check_results(results, *run_gpu(sp, frames, learn=True))
-    assert sp.info()["last_learn_cluster"] == (1 if path == P.SP_PATH_AUTO else 0)
+    check_learn_path(sp, path)
     _, gperm, _ = sp.get_state()
     assert np.array_equal(gperm.view(np.uint32), ora.perm.view(np.uint32))
     test = sp_inputs.frames(2002, 0, 40, 540, 960, rho=0.5)
@@ -354,8 +369,9 @@ def test_config3_sweep_sampled_parity(C, S, radius):
     check_results(results, *out)
 
 
-def test_scaled_config5_learning():
-    # BASELINE config 5: 16384 columns, 512 synapses, local r=80 (per-input path)
+@pytest.mark.parametrize("path", ["grid", "input"])
+def test_scaled_config5_learning(path):
+    # BASELINE config 5: 16384 columns, 512 synapses, local r=80 (no cluster fits: grid kernel)
     cfg = headline_cfg(num_columns=16384, synapses_per_column=512, min_overlap=8,
                        winners_set_size=40, inhibition_radius=80)
     idx, perm, _ = O.init_pools(cfg)
@@ -363,10 +379,15 @@ def test_scaled_config5_learning():
     frames = sp_inputs.frames(1001, 0, 3, 540, 960, rho=0.5)
     ora = O.SpatialPoolerOracle(cfg, state)
     results = ora.compute(frames, learning=True)
-    sp = make_sp(cfg, state, max_inputs=8)
+    sp = make_sp(cfg, state, path, max_inputs=8)
     check_results(results, *run_gpu(sp, frames, learn=True))
+    check_learn_path(sp, path)
     _, gperm, _ = sp.get_state()
     assert np.array_equal(gperm.view(np.uint32), ora.perm.view(np.uint32))
+    # inference after learning: the per-input path rebuilds its synapse-major table
+    frames2 = sp_inputs.frames(2002, 0, 2, 540, 960, rho=0.5)
+    res2 = [ora.step(x, False) for x in O.encode(frames2, cfg)]
+    check_results(res2, *run_gpu(sp, frames2))
 
 
 def test_end_to_end_host_buffers_match_device_call():
