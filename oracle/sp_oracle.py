@@ -22,6 +22,18 @@ What it computes is the plain definition, step by step, in the paper's order
 5. learn    : for every active column and every potential synapse:
               perm = clamp01(fp32(perm + inc)) if x else clamp01(fp32(perm - dec))
                                                         (P:92 -> whitepaper; S:119(a); C3, C10)
+   full learning (NEXT-1, ``full_learning=True``; S:119(b-e); DESIGN R17-R21),
+   after (a), in this order:
+     (b) duty cycles, every column, fp32:  d = (d * (P-1) + a) / P   with
+         a = active[c] (active duty) and a = N[c] > 0 (overlap duty)
+     (c) boost from the active duty cycle: minA = 0.01 * max(adc over W(c));
+         boost = 1 if adc >= minA else 1 + ((minA - adc) / minA) * (max_boost - 1)
+     (d) weak-column bump: odc < 0.01 * max(odc over W(c)) -> every potential synapse
+         perm = min(1, perm + 0.1 * tau)
+     (e) inhibition radius (only when the configured radius is > 0):
+         r = clamp(round(mean_c(span_c * C / nbits) / 2), 1, C), span_c = max - min + 1
+         of the connected synapses' input indices (0 if none), evaluated exactly
+   W(c) is the window of the radius in force for this input (global when 0).
 6. output   : the active set / SDR bitmask (bit c of word c // 32, LSB first).
 
 Initialisation ("random initialization", P:245 init perm; C8 as amended
@@ -41,6 +53,9 @@ regression pin only, SURVEY §8(c) "What pins each part").
 from __future__ import annotations
 
 from dataclasses import dataclass, field
+from fractions import Fraction
+import math
+
 import numpy as np
 
 MASK64 = (1 << 64) - 1
@@ -67,6 +82,10 @@ class OracleConfig:
     patch_width: int = 0               # 0 = whole frame is one SP input (C13)
     patch_height: int = 0
     seed: int = 42
+    # full learning (NEXT-1; S:119(b-e))
+    full_learning: bool = False
+    duty_cycle_period: int = 1000      # S:150 "window duty_cycle_period (alpha = 1/period)"
+    max_boost: float = 2.0             # S:149 "max_boost"; 2.0
 
     @property
     def patch(self):
@@ -225,6 +244,84 @@ def learn(perm: np.ndarray, idx: np.ndarray, x: np.ndarray, active: np.ndarray,
     return out
 
 
+# --------------------------------------------------------------------------- #
+# full learning, steps (b)-(e) (NEXT-1; S:119(b-e); DESIGN R17-R21)
+# --------------------------------------------------------------------------- #
+MIN_PCT = np.float32(0.01)  # S:149 "0.01 x max"; S:119(d) "below 1% of ..."
+BUMP_PCT = np.float32(0.1)  # S:119(d) "0.1 x connected_threshold"
+
+
+def update_duty(duty: np.ndarray, flag: np.ndarray, period: int) -> np.ndarray:
+    """(b) moving average with window ``period`` (alpha = 1/period), fp32 (R17):
+    d' = fp32(fp32(fp32(d * (P-1)) + a) / P), one IEEE RN operation at a time."""
+    d = np.asarray(duty, dtype=np.float32)
+    t = (d * np.float32(period - 1)).astype(np.float32)
+    t = (t + np.asarray(flag, dtype=np.float32)).astype(np.float32)
+    return (t / np.float32(period)).astype(np.float32)
+
+
+def window_max(v: np.ndarray, radius: int) -> np.ndarray:
+    """max of v over W(c) = the neighbourhood of c INCLUDING c (C9; R18); radius 0 = global."""
+    C = len(v)
+    out = np.empty(C, dtype=v.dtype)
+    for c in range(C):
+        lo, hi = neighbourhood(c, C, radius)
+        out[c] = v[lo:hi + 1].max()
+    return out
+
+
+def boost_from_duty(adc: np.ndarray, radius: int, max_boost: float) -> np.ndarray:
+    """(c) S:149: minA = 0.01 * neighbourhood max of the active duty cycle; boost = 1 if
+    adc >= minA, else 1 + (minA - adc) / minA * (max_boost - 1); fp32, in that order (R19)."""
+    adc = np.asarray(adc, dtype=np.float32)
+    minA = (MIN_PCT * window_max(adc, radius)).astype(np.float32)
+    mb1 = np.float32(np.float32(max_boost) - np.float32(1.0))
+    boost = np.ones(len(adc), dtype=np.float32)
+    for c in range(len(adc)):
+        if adc[c] < minA[c]:
+            t1 = np.float32(minA[c] - adc[c])
+            t2 = np.float32(t1 / minA[c])
+            t3 = np.float32(t2 * mb1)
+            boost[c] = np.float32(np.float32(1.0) + t3)
+    return boost
+
+
+def bump_weak(perm: np.ndarray, odc: np.ndarray, radius: int, tau: float):
+    """(d) S:119(d): columns whose overlap duty cycle is below 1% of their neighbourhood
+    maximum get every permanence raised by 0.1 * tau, clamped to 1 (fp32, R20).
+    Returns (new perm, weak mask)."""
+    odc = np.asarray(odc, dtype=np.float32)
+    minO = (MIN_PCT * window_max(odc, radius)).astype(np.float32)
+    weak = odc < minO
+    bump = np.float32(BUMP_PCT * np.float32(tau))
+    out = perm.copy()
+    for c in np.nonzero(weak)[0]:
+        out[c] = np.minimum((out[c] + bump).astype(np.float32), np.float32(1.0))
+    return out, weak
+
+
+def connected_span(idx: np.ndarray, perm: np.ndarray, tau: float) -> np.ndarray:
+    """span_c = max - min + 1 over the input indices of c's connected synapses, 0 if none
+    (S:151 "connected-synapse input span"; R21)."""
+    C = idx.shape[0]
+    span = np.zeros(C, dtype=np.int64)
+    conn = perm >= np.float32(tau)
+    for c in range(C):
+        sel = idx[c][conn[c]]
+        if len(sel):
+            span[c] = int(sel.max()) - int(sel.min()) + 1
+    return span
+
+
+def adapt_radius(span: np.ndarray, nbits: int, num_columns: int) -> int:
+    """(e) S:151: radius = clamp(round(mean_c(span_c * C / nbits) / 2), 1, C), evaluated as
+    an exact rational (R21): mean_c(span_c * C / nbits) / 2 = sum(span) / (2 * nbits);
+    round half up."""
+    q = Fraction(int(np.sum(span, dtype=np.int64)), 2 * nbits)
+    r = math.floor(q + Fraction(1, 2))
+    return int(min(max(r, 1), num_columns))
+
+
 def sdr_words(active: np.ndarray) -> np.ndarray:
     """Active flags -> uint32 words, bit c of word c // 32 (LSB first)."""
     C = len(active)
@@ -257,15 +354,32 @@ class SpatialPoolerOracle:
             self.idx = np.asarray(idx, dtype=np.int64).copy()
             self.perm = np.asarray(perm, dtype=np.float32).copy()
             self.boost = np.asarray(boost, dtype=np.float32).copy()
+        # full-learning state ("duty cycles = 0; inhibition_radius = initial")
+        self.active_duty = np.zeros(cfg.num_columns, dtype=np.float32)
+        self.overlap_duty = np.zeros(cfg.num_columns, dtype=np.float32)
+        self.radius = int(cfg.inhibition_radius)
+        self.iteration = 0
 
     def step(self, x: np.ndarray, learning: bool, paper_literal: bool = False) -> StepResult:
         cfg = self.cfg
         raw = overlap_raw(x, self.idx, self.perm, cfg.connected_threshold)
         N, boosted = boost_overlap(raw, self.boost, cfg.min_overlap)
-        active = inhibit(N, cfg.winners_set_size, cfg.inhibition_radius, paper_literal)
+        active = inhibit(N, cfg.winners_set_size, self.radius, paper_literal)
         if learning:
             self.perm = learn(self.perm, self.idx, x, active,
-                              cfg.perm_increment, cfg.perm_decrement)
+                              cfg.perm_increment, cfg.perm_decrement)          # (a)
+            if cfg.full_learning:
+                P = cfg.duty_cycle_period
+                self.active_duty = update_duty(self.active_duty, active, P)   # (b)
+                self.overlap_duty = update_duty(self.overlap_duty, N > 0, P)
+                self.boost = boost_from_duty(self.active_duty, self.radius,   # (c)
+                                             cfg.max_boost)
+                self.perm, _ = bump_weak(self.perm, self.overlap_duty,        # (d)
+                                         self.radius, cfg.connected_threshold)
+                if cfg.inhibition_radius > 0:                                  # (e)
+                    span = connected_span(self.idx, self.perm, cfg.connected_threshold)
+                    self.radius = adapt_radius(span, cfg.input_bits, cfg.num_columns)
+            self.iteration += 1
         return StepResult(raw, N, boosted, active)
 
     def compute(self, frames: np.ndarray, learning: bool):

@@ -1,0 +1,265 @@
+"""Pins of the oracle's full learning step (SPEC S:119(b-e),
+S:149-151; readings R17-R21).
+
+Each check reaches the oracle's number by another route: a closed form, exact rational
+arithmetic with an error bound, a library routine (scipy's running maximum), a value worked
+out by hand in the test, or an invariant.  None re-types the oracle's fp32 op sequence.
+"""
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+from scipy.ndimage import maximum_filter1d
+
+import oracle as O
+import sp_inputs
+from tests.helpers import ocfg
+
+ULP1 = 2.0 ** -23  # fp32 ulp at 1
+
+
+# --------------------------------------------------------------------------- #
+# (b) duty cycles: EMA with alpha = 1/period
+# --------------------------------------------------------------------------- #
+@pytest.mark.parametrize("period", [1, 2, 10, 1000])
+def test_duty_constant_one_closed_form(period):
+    # always active: d_t = 1 - (1 - 1/P)^t exactly in the reals; fp32 error grows by at
+    # most a few ulp per step (three RN operations on values <= 1)
+    d = np.zeros(1, np.float32)
+    for t in range(1, 301):
+        d = O.update_duty(d, np.array([True]), period)
+        exact = 1.0 - (1.0 - 1.0 / period) ** t
+        assert abs(float(d[0]) - exact) <= 3 * t * ULP1
+    if period == 1:
+        assert d[0] == 1.0  # P = 1: the duty cycle is the last flag exactly
+
+
+def test_duty_zero_stays_zero_and_decays():
+    d = O.update_duty(np.zeros(4, np.float32), np.zeros(4, bool), 1000)
+    assert np.all(d == 0.0)
+    # one activation then silence: d_t = (1/P) (1 - 1/P)^(t-1)
+    d = O.update_duty(np.zeros(1, np.float32), np.array([True]), 1000)
+    assert d[0] == np.float32(0.001)
+    for t in range(2, 200):
+        d = O.update_duty(d, np.array([False]), 1000)
+        exact = 0.001 * (0.999 ** (t - 1))
+        assert abs(float(d[0]) - exact) <= 3 * t * 2.0 ** -33  # ulp at 1e-3 is 2^-33
+
+
+def test_duty_stays_in_unit_interval():
+    rng = np.random.default_rng(3)
+    d = np.zeros(64, np.float32)
+    for _ in range(500):
+        d = O.update_duty(d, rng.random(64) < 0.3, 7)
+        assert np.all((d >= 0) & (d <= 1))
+
+
+# --------------------------------------------------------------------------- #
+# window maximum over W(c) (C9, R18): scipy's running maximum with edge replication
+# is the truncated window (replicated edge values never exceed the window's own max)
+# --------------------------------------------------------------------------- #
+@pytest.mark.parametrize("radius", [1, 2, 5, 31, 127, 200])
+def test_window_max_vs_scipy(radius):
+    v = np.random.default_rng(11).random(128).astype(np.float32)
+    got = O.window_max(v, radius)
+    want = maximum_filter1d(v, size=2 * radius + 1, mode="nearest")
+    assert np.array_equal(got, want)
+
+
+def test_window_max_global():
+    v = np.random.default_rng(12).random(77).astype(np.float32)
+    assert np.all(O.window_max(v, 0) == v.max())
+
+
+# --------------------------------------------------------------------------- #
+# (c) boost rule: linear in the duty deficit, bounded by [1, max_boost]
+# --------------------------------------------------------------------------- #
+def _boost_exact(adc, maxa, max_boost):
+    """The rule in exact rationals, from the real inputs (fp32 values as Fractions)."""
+    mina = Fraction(float(np.float32(np.float32(0.01) * np.float32(maxa))))
+    a = Fraction(float(adc))
+    if a >= mina:
+        return Fraction(1)
+    return 1 + (mina - a) / mina * (Fraction(float(np.float32(max_boost))) - 1)
+
+
+@pytest.mark.parametrize("max_boost", [2.0, 3.5, 10.0])
+def test_boost_rule_exact_within_ulps(max_boost):
+    rng = np.random.default_rng(int(max_boost * 10))
+    adc = (rng.random(256) * 0.02).astype(np.float32)
+    adc[:8] = 0.0
+    adc[8] = 0.9  # the maximum: minA = 0.009
+    b = O.boost_from_duty(adc, 0, max_boost)
+    for c in range(256):
+        want = _boost_exact(adc[c], adc.max(), max_boost)
+        # four fp32 roundings (relative 2^-24 each) on values <= max_boost: within 4 fp32
+        # ulp of max_boost
+        ulp = Fraction(2) ** (math.floor(math.log2(max_boost)) - 23)
+        assert abs(Fraction(float(b[c])) - want) <= 4 * ulp
+    # adc = 0 with a positive neighbourhood maximum -> exactly max_boost (t2 = 1 exactly)
+    assert np.all(b[:8] == np.float32(max_boost))
+    # the most active column is never boosted (S:119(c) example's fixed point)
+    assert b[8] == 1.0
+    assert np.all((b >= 1.0) & (b <= np.float32(max_boost)))
+
+
+def test_boost_monotone_in_duty():
+    adc = np.linspace(0, 0.011, 200, dtype=np.float32)
+    adc = np.concatenate([adc, np.float32([1.0])])
+    b = O.boost_from_duty(adc, 0, 2.0)
+    assert np.all(np.diff(b[:-1]) <= 0)
+
+
+def test_boost_all_zero_duty_is_one():
+    # no column ever active: minA = 0, adc >= minA -> boost 1 (S:119 degenerate input)
+    assert np.all(O.boost_from_duty(np.zeros(50, np.float32), 0, 2.0) == 1.0)
+
+
+def test_boost_column_always_active_converges_to_one():
+    # S:119 example: a column active on every step for duty_cycle_period steps -> boost 1
+    # (9 steps: from perm 0 the other columns need 10 bumps of 0.1*tau to connect, S:119(d))
+    cfg = ocfg(num_columns=32, synapses_per_column=8, full_learning=True, duty_cycle_period=9,
+               min_overlap=1, winners_set_size=1)
+    idx, perm, boost = O.init_pools(cfg)
+    perm[:] = 0.0
+    perm[5] = 1.0  # column 5 is the only connected column: it wins every non-empty input
+    ora = O.SpatialPoolerOracle(cfg, (idx, perm, boost))
+    ones = np.full((9, 8, 8), 255, np.uint8)
+    for x in O.encode(ones, cfg):
+        r = ora.step(x, True)
+        assert r.active[5] and r.active.sum() == 1
+    assert ora.boost[5] == 1.0
+    # every other column never won: its duty cycle is 0 < minA -> boosted to max_boost
+    assert np.all(np.delete(ora.boost, 5) == np.float32(2.0))
+
+
+# --------------------------------------------------------------------------- #
+# (d) weak-column bump (S:119(d))
+# --------------------------------------------------------------------------- #
+def test_bump_closed_form():
+    odc = np.array([0.5, 0.004, 0.006, 0.0, 0.5], np.float32)  # minO = 0.005 globally
+    perm = np.array([[0.1, 0.2], [0.1, 0.99], [0.3, 0.3], [0.0, 1.0], [0.2, 0.2]], np.float32)
+    out, weak = O.bump_weak(perm, odc, 0, 0.2)
+    assert weak.tolist() == [False, True, False, True, False]
+    b = np.float32(np.float32(0.1) * np.float32(0.2))  # 0.02
+    assert out[1, 0] == np.float32(np.float32(0.1) + b)
+    assert out[1, 1] == 1.0 and out[3, 1] == 1.0  # clamp at 1 (S:138 closure)
+    assert out[3, 0] == b
+    assert np.array_equal(out[[0, 2, 4]], perm[[0, 2, 4]])
+
+
+def test_bump_local_window():
+    # with radius 1 the maximum is taken over the three-column window only
+    odc = np.array([1.0, 0.005, 0.0, 0.0, 0.0, 0.0001], np.float32)
+    _, weak = O.bump_weak(np.zeros((6, 1), np.float32), odc, 1, 0.2)
+    # col1: max(1, .005, 0) = 1 -> .005 < .01 weak; col2: max(.005, 0, 0) -> 0 < 5e-5 weak;
+    # col3: max 0 -> 0 < 0 false; col4: max(0,0,1e-4) -> 0 < 1e-6 weak; col5: 1e-4 < 1e-6 no
+    assert weak.tolist() == [False, True, True, False, True, False]
+
+
+# --------------------------------------------------------------------------- #
+# (e) inhibition radius
+# --------------------------------------------------------------------------- #
+def test_span_by_hand():
+    idx = np.array([[1, 4, 9, 12], [0, 2, 3, 63]], np.int64)
+    perm = np.array([[0.1, 0.3, 0.3, 0.1], [0.1, 0.1, 0.1, 0.1]], np.float32)
+    assert O.connected_span(idx, perm, 0.2).tolist() == [9 - 4 + 1, 0]
+    perm[1, 3] = 0.2
+    assert O.connected_span(idx, perm, 0.2).tolist() == [6, 1]
+
+
+def test_radius_by_hand():
+    # 4 columns over 64 bits, spans 10, 20, 0, 30: mean(span * 4/64) = 60/64; /2 = 0.47 -> 0
+    # -> clamped to 1
+    assert O.adapt_radius(np.array([10, 20, 0, 30]), 64, 4) == 1
+    # 8 columns over 16 bits, all spans 16: mean = 8, /2 = 4
+    assert O.adapt_radius(np.full(8, 16), 16, 8) == 4
+    # 3 columns over 8 bits, spans 8, 8, 7: mean(span*3/8) = 69/24 = 2.875; /2 = 1.4375 -> 1
+    assert O.adapt_radius(np.array([8, 8, 7]), 8, 3) == 1
+    # 5 columns over 10 bits, spans 10, 10, 10, 10, 5: mean(s*5/10) = 4.5; /2 = 2.25 -> 2
+    assert O.adapt_radius(np.array([10, 10, 10, 10, 5]), 10, 5) == 2
+    # exact half rounds up: 2 columns, 4 bits, spans 4, 2: mean(s*2/4) = 1.5; /2 = .75 -> 1;
+    # 2 columns, 2 bits, spans 2, 1: mean(s*2/2) = 1.5 ... use 6 columns, 4 bits, spans 4,4,4,4,4,2:
+    # mean(s*6/4) = 33/6 = 5.5, /2 = 2.75 -> 3
+    assert O.adapt_radius(np.array([4, 4, 4, 4, 4, 2]), 4, 6) == 3
+    # 2 columns, 4 bits, spans 4 and 6 is impossible (span <= nbits); 10 columns, 10 bits,
+    # spans all 5: mean(5*10/10) = 5, /2 = 2.5 -> half up -> 3
+    assert O.adapt_radius(np.full(10, 5), 10, 10) == 3
+
+
+def test_radius_permutation_pools_closed_form():
+    # S = nbits: every pool is a permutation; all connected -> span = nbits for every column
+    # -> radius = round(C / 2)
+    cfg = ocfg(num_columns=127, synapses_per_column=64)
+    idx, perm, _ = O.init_pools(cfg)
+    span = O.connected_span(idx, perm, 0.2)
+    assert np.all(span == 64)
+    assert O.adapt_radius(span, 64, 127) == 64  # 63.5 rounds half up
+    # nothing connected -> clamp to 1
+    assert O.adapt_radius(O.connected_span(idx, np.zeros_like(perm), 0.2), 64, 127) == 1
+
+
+# --------------------------------------------------------------------------- #
+# the composed step: invariants, and the reduction to the hot-path step
+# --------------------------------------------------------------------------- #
+def _run(cfg, frames, state=None):
+    ora = O.SpatialPoolerOracle(cfg, state)
+    trace = [ora.step(x, True) for x in O.encode(frames, cfg)]
+    return ora, trace
+
+
+def test_full_learning_invariants():
+    cfg = ocfg(full_learning=True, duty_cycle_period=20, inhibition_radius=8, max_boost=3.0)
+    frames = sp_inputs.frames(1001, 0, 60, 8, 8, rho=0.3)
+    ora, trace = _run(cfg, frames)
+    assert ora.iteration == 60
+    assert np.all((ora.perm >= 0) & (ora.perm <= 1))
+    assert np.all((ora.boost >= 1) & (ora.boost <= np.float32(3.0)))
+    assert np.all((ora.active_duty >= 0) & (ora.active_duty <= 1))
+    assert 1 <= ora.radius <= cfg.num_columns
+    # the boost is an exact-key-domain value (R4): boost * 2^23 is an integer
+    O.boost_integer(ora.boost)
+    # duty cycles are consistent with the trace: each column's active duty equals the EMA of
+    # its own activity, recomputed here in float64 (fp32 error bound, a few ulp per step)
+    d = np.zeros(cfg.num_columns)
+    for r in trace:
+        d = d * (19 / 20) + r.active / 20
+    assert np.max(np.abs(d - ora.active_duty)) <= 3 * 60 * ULP1
+
+
+def test_full_learning_off_equals_hot_path_step():
+    # full_learning=False leaves boost, duty and radius untouched (regression of the a5 path)
+    cfg = ocfg(inhibition_radius=4)
+    frames = sp_inputs.frames(1001, 0, 12, 8, 8, rho=0.5)
+    ora, _ = _run(cfg, frames)
+    assert np.all(ora.boost == 1.0) and ora.radius == 4 and np.all(ora.active_duty == 0)
+
+
+def test_full_learning_global_keeps_global():
+    # configured radius 0 (global) is not adapted (R21)
+    cfg = ocfg(full_learning=True, duty_cycle_period=10)
+    ora, _ = _run(cfg, sp_inputs.frames(1001, 0, 15, 8, 8, rho=0.5))
+    assert ora.radius == 0
+
+
+def test_full_learning_radius_tracks_spans():
+    # after every step the radius equals S:151 evaluated in floating point on the state
+    cfg = ocfg(full_learning=True, duty_cycle_period=10, inhibition_radius=80,
+               num_columns=96, synapses_per_column=12)
+    ora = O.SpatialPoolerOracle(cfg)
+    for x in O.encode(sp_inputs.frames(1001, 0, 10, 8, 8, rho=0.5), cfg):
+        ora.step(x, True)
+        span = O.connected_span(ora.idx, ora.perm, 0.2)
+        mean_diam = float(np.mean(span * cfg.num_columns / cfg.input_bits))
+        want = min(max(int(math.floor(mean_diam / 2 + 0.5)), 1), cfg.num_columns)
+        assert ora.radius == want
+
+
+def test_full_learning_deterministic():
+    cfg = ocfg(full_learning=True, duty_cycle_period=5, inhibition_radius=3)
+    frames = sp_inputs.frames(1001, 0, 20, 8, 8, rho=0.5)
+    a, ta = _run(cfg, frames)
+    b, tb = _run(cfg, frames)
+    assert all(np.array_equal(x.active, y.active) for x, y in zip(ta, tb))
+    assert np.array_equal(a.perm, b.perm) and np.array_equal(a.boost, b.boost)
