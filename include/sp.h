@@ -14,6 +14,9 @@
  *                (Alg. 2; DESIGN R5-R7, R9)
  *   a5 learn     winners' potential synapses: perm +inc if the input bit is set,
  *                -dec otherwise, clamped to [0,1], fp32 (P:92 -> whitepaper; S:119(a); R3, R10)
+ *   full learning (SP_FLAG_FULL_LEARNING; S:119(b-e), S:149-151;
+ *                DESIGN R17-R21), after a5 for every input: duty cycles, boost update,
+ *                weak-column bump and (configured radius > 0) inhibition-radius adaptation
  *
  * Conventions shared by every entry point:
  *  - Every function returns sp_status; on failure sp_last_error() returns a
@@ -56,8 +59,15 @@ enum { SP_PATH_AUTO = 0, SP_PATH_PER_INPUT = 1, SP_PATH_BATCHED = 2 };
 /* sp_config.flags */
 enum {
     SP_FLAG_RECORD_OVERLAPS = 1u, /* keep raw/boosted overlaps of the last call for sp_overlaps */
-    SP_FLAG_LEARN_GRID = 2u       /* learn=1: prefer the grid-resident kernel (one CTA per SM) over
+    SP_FLAG_LEARN_GRID = 2u,      /* learn=1: prefer the grid-resident kernel (one CTA per SM) over
                                      the cluster-resident one (default: cluster when it fits) */
+    SP_FLAG_FULL_LEARNING = 4u    /* learn=1 also runs S:119(b-e) after each input's permanence
+                                     update (DESIGN R17-R21): active/overlap duty cycles (EMA of
+                                     period duty_cycle_period), boost = linear rule up to
+                                     max_boost, weak-column bump by 0.1*tau, and, when
+                                     inhibition_radius > 0, the radius recomputed from the
+                                     connected spans.  The radius in force governs inhibition
+                                     of every later call (learn or not). */
 };
 
 /*
@@ -70,7 +80,9 @@ enum {
  *   min_overlap <= synapses_per_column; 1 <= winners_set_size <= num_columns;
  *   perm_increment, perm_decrement, initial_permanence, connected_threshold in [0,1];
  *   ceil(log2(S+1)) + 27 + ceil(log2(C32)) <= 64 (the exact rank key fits 64 bits, R4);
- *   max_inputs >= 1 (capacity of one sp_compute call, in SP inputs).
+ *   max_inputs >= 1 (capacity of one sp_compute call, in SP inputs);
+ *   with SP_FLAG_FULL_LEARNING: duty_cycle_period >= 1 and 1 <= max_boost < 16 (boosts
+ *     stay in the exact-key domain, R4).
  */
 typedef struct sp_config {
     uint32_t input_width, input_height;   /* frame W x H in pixels; bit = y*W + x */
@@ -89,6 +101,8 @@ typedef struct sp_config {
     uint32_t max_inputs;                  /* per-call capacity in SP inputs */
     uint32_t flags;                       /* SP_FLAG_* */
     uint32_t force_path;                  /* SP_PATH_* */
+    uint32_t duty_cycle_period;           /* full learning: EMA period P (default 1000) */
+    float max_boost;                      /* full learning: boost ceiling (default 2.0) */
 } sp_config;
 
 typedef struct sp_handle sp_handle;
@@ -135,7 +149,8 @@ typedef struct sp_info {
 #define SP_LEARN_GRID 2u      /* one cooperative launch, one CTA per SM, table streamed from L2 */
 
 /* Fills *cfg with Tab. 2 defaults on a 240x134 frame (Tab. 1),
- * tau 0.2, seed 42, device 0, max_inputs 4096.  Never fails for non-NULL cfg. */
+ * tau 0.2, seed 42, device 0, max_inputs 4096, duty_cycle_period 1000, max_boost 2.0.
+ * Never fails for non-NULL cfg. */
 sp_status sp_config_default(sp_config* cfg);
 
 /* Validates *cfg, samples the potential pools (R8: per column c a splitmix64
@@ -190,6 +205,21 @@ sp_status sp_get_state(sp_handle* h, uint32_t* idx, float* perm, float* boost);
  * ascending within a column (distinct); perm in [0,1]; boost in
  * [1,16) (the exact-key domain, R4).  NULL keeps the current array. */
 sp_status sp_set_state(sp_handle* h, const uint32_t* idx, const float* perm, const float* boost);
+
+/* Full-learning state (S:88, S:119(b-e)); host pointers, synchronous.
+ *   active_duty, overlap_duty: float[C] duty cycles (or NULL);
+ *   radius: the inhibition radius in force (0 = global) (or NULL);
+ *   iteration: number of SP inputs learned since creation (or NULL).
+ * Errors: SP_E_ARG (NULL handle), SP_E_CUDA. */
+sp_status sp_get_learning_state(sp_handle* h, float* active_duty, float* overlap_duty, uint32_t* radius,
+                                uint64_t* iteration);
+
+/* Imports the full-learning state (checkpoint / oracle injection; synchronous).
+ *   active_duty, overlap_duty: float[C] in [0,1] (SP_E_ARG otherwise), NULL keeps the current;
+ *   radius: new radius in force; must be 0 iff the configured inhibition_radius is 0, else in
+ *   [1, C] (SP_E_ARG). */
+sp_status sp_set_learning_state(sp_handle* h, const float* active_duty, const float* overlap_duty,
+                                uint32_t radius);
 
 /* End-to-end variant ("OCL" accounting of P:316): frames in HOST memory,
  * winners returned to HOST memory.  The library pipelines host->device copies,

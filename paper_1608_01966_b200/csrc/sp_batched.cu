@@ -222,6 +222,7 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
     cg::cluster_group cluster = cg::this_cluster();
     const uint32_t theta = p.min_overlap, L = p.keyL;
     const uint64_t one = 1ull << 23;
+    const uint32_t radius = p.radius_dev ? *p.radius_dev : p.radius;  // adapted by full learning
     const uint32_t nbN = p.keyBits - L;             // significant bits of N
     const uint32_t sh = nbN > 16u ? nbN - 16u : 0u;  // coarse key u = N >> sh has <= 16 bits
     uint64_t* tie_list = reinterpret_cast<uint64_t*>(region) + wi * 64u;  // X window is idle now
@@ -244,7 +245,7 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
                     r >= theta ? __fmul_rn(static_cast<float>(r), p.boost[c]) : 0.0f;
             }
         }
-        if (p.radius == 0 && p.uniform_bc) {
+        if (radius == 0 && p.uniform_bc) {
             // Uniform boost: the key order is (raw desc, index asc), so the k-th largest key
             // is found from a histogram of the raw counts: with one boost
             // the floor raw*Bc > 2^23 (R7) is raw >= r_lo; r* = largest r with
@@ -274,7 +275,7 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             if (lane == 0) p.counts[gin] = total;
             continue;
         }
-        if (p.radius > 0 && p.uniform_bc) {
+        if (radius > 0 && p.uniform_bc) {
             // local inhibition, uniform boost: bit-sliced window comparator (sp_select.cuh)
             const uint32_t r_lo = uniform_r_lo(theta, s_bc[0]);
             const uint32_t nb = raw_bits(p.S);
@@ -283,7 +284,7 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             __syncwarp();
             uint32_t total = 0, myword = 0;
             for (uint32_t cw = 0; cw < p.ncw; ++cw) {
-                const uint32_t word = local_uniform_word(row, planes, p.ncw, nb, cw, p.C, p.radius, p.k,
+                const uint32_t word = local_uniform_word(row, planes, p.ncw, nb, cw, p.C, radius, p.k,
                                                          r_lo, lane);
                 if ((cw & 31u) == lane) myword = word;
                 total += __popc(word);
@@ -296,14 +297,14 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             __syncwarp();  // planes are rewritten by this warp's next input
             continue;
         }
-        if (p.radius > 0 && p.ncw * 16u <= 1024u && NW <= 16u) {
+        if (radius > 0 && p.ncw * 16u <= 1024u && NW <= 16u) {
             // local inhibition, per-column boosts: coarse bit-sliced + exact ties
             uint32_t* planes = reinterpret_cast<uint32_t*>(region) + wi * 1024u;  // [ncw][16]
             build_coarse_planes(row, s_bc, planes, p.ncw, theta, sh, 0u, 1u, lane);
             __syncwarp();
             uint32_t total = 0, myword = 0;
             for (uint32_t cw = 0; cw < p.ncw; ++cw) {
-                const uint32_t word = local_general_word(row, s_bc, planes, p.ncw, cw, p.C, p.radius,
+                const uint32_t word = local_general_word(row, s_bc, planes, p.ncw, cw, p.C, radius,
                                                          p.k, theta, sh, L, lane);
                 if ((cw & 31u) == lane) myword = word;
                 total += __popc(word);
@@ -318,7 +319,7 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
         }
         uint32_t Tu = 0;       // k-th largest coarse key
         uint64_t T2 = 0;       // exact key threshold among the columns with u == Tu
-        if (p.radius == 0) {
+        if (radius == 0) {
             constexpr int NU = (CPT * NW + 1) / 2;  // column-warps of this CTA, two per register
             global_general_threshold<NU>(row, s_bc, p.C32, p.ncw, p.k, theta, sh, L, p.keyBits, tie_list,
                                          lane, Tu, T2);
@@ -330,11 +331,11 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             const uint64_t key = rank_key(row[c], s_bc[c], theta, c, L, N);
             bool act = N > one;
             if (act) {
-                if (p.radius == 0) {
+                if (radius == 0) {
                     act = global_general_wins(N, key, sh, Tu, T2);
                 } else {
-                    const uint32_t lo = c >= p.radius ? c - p.radius : 0u;
-                    const uint32_t hi = min(p.C - 1u, c + p.radius);
+                    const uint32_t lo = c >= radius ? c - radius : 0u;
+                    const uint32_t hi = min(p.C - 1u, c + radius);
                     uint32_t beats = 0;
                     for (uint32_t d = lo; d <= hi && beats < p.k; ++d) {
                         uint64_t Nd;

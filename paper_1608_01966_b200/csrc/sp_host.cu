@@ -118,6 +118,12 @@ sp_status validate(const sp_config* c) {
     if (c->max_inputs == 0) return fail(SP_E_CONFIG, "max_inputs must be >= 1");
     if (c->force_path > SP_PATH_BATCHED)
         return fail(SP_E_CONFIG, "force_path must be SP_PATH_AUTO/PER_INPUT/BATCHED");
+    if (c->flags & SP_FLAG_FULL_LEARNING) {
+        if (c->duty_cycle_period == 0 || c->duty_cycle_period > (1u << 24))
+            return fail(SP_E_CONFIG, "full learning: duty_cycle_period must be in [1, 2^24] (S:150)");
+        if (!(c->max_boost >= 1.0f && c->max_boost < 16.0f))
+            return fail(SP_E_CONFIG, "full learning: max_boost must be in [1,16) (S:149, R4)");
+    }
     return SP_OK;
 }
 
@@ -333,6 +339,14 @@ struct sp_handle {
     uint32_t grid_G = 0, grid_smem = 0, grid_own = 0, grid_win = 0, grid_ccols = 0, grid_stages = 0;
     bool grid_dbl = false;
     bool synT_dirty = true;      // d_synT must be rebuilt from idx/perm before grid learning
+    // full learning (NEXT-1; DESIGN R17-R21)
+    float* d_adc = nullptr;      // [C32] active duty cycles
+    float* d_odc = nullptr;      // [C32] overlap duty cycles
+    uint32_t* d_span = nullptr;  // [C32] connected spans
+    uint32_t* d_radius = nullptr;  // radius in force (device scalar)
+    float* d_fscratch = nullptr;   // window-maximum tables of k_full
+    bool span_dirty = true;      // d_span must be recomputed before full learning
+    uint64_t iteration = 0;      // SP inputs learned
     bool syn_dirty = false;      // d_syn must be rebuilt from idx/perm before the per-input path
     uint32_t last_learn_path = SP_LEARN_PER_INPUT;
     // scratch and results
@@ -370,7 +384,8 @@ void release(sp_handle* h) {
     void* ptrs[] = {h->d_trace, h->d_idx,  h->d_perm,    h->d_boost,   h->d_bc,      h->d_syn,
                     h->d_ell,  h->d_ell_off, h->d_ell_nb,  h->d_ell_pos, h->d_bits,
                     h->d_raw,  h->d_sdr,     h->d_counts,  h->d_raw_rec, h->d_boosted_rec,
-                    h->d_stage[0], h->d_stage[1], h->d_synT,  h->d_gbar};
+                    h->d_stage[0], h->d_stage[1], h->d_synT,  h->d_gbar, h->d_adc, h->d_odc,
+                    h->d_span, h->d_radius, h->d_fscratch};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
@@ -514,6 +529,7 @@ sp_status upload_state(sp_handle* h, const uint32_t* idx, const float* perm, con
     if (e != cudaSuccess) return cuda_fail(e, "synapse layout build");
     h->syn_dirty = false;
     h->synT_dirty = true;
+    h->span_dirty = true;
     if (h->lay.ok) return build_ell(h, perm);
     return SP_OK;
 }
@@ -523,6 +539,25 @@ sp_status check_handle(sp_handle* h) {
     cudaError_t e = cudaSetDevice(h->device);
     if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
     return SP_OK;
+}
+
+// Full-learning constants and device state (R17-R21) for the learning kernels.
+sp::FullLearn full_learn_params(const sp_handle* h) {
+    sp::FullLearn f{};
+    f.on = (h->cfg.flags & SP_FLAG_FULL_LEARNING) ? 1u : 0u;
+    f.adapt = f.on && h->cfg.inhibition_radius > 0 ? 1u : 0u;
+    f.pm1 = static_cast<float>(h->cfg.duty_cycle_period) - 1.0f;  // exact: P <= 2^24
+    f.P = static_cast<float>(h->cfg.duty_cycle_period);
+    f.mb1 = h->cfg.max_boost - 1.0f;           // one fp32 RN subtraction (R19)
+    f.bump = 0.1f * h->cfg.connected_threshold;  // one fp32 RN product (R20)
+    f.adc = h->d_adc;
+    f.odc = h->d_odc;
+    f.boost = h->d_boost;
+    f.bc = h->d_bc;
+    f.radius = h->d_radius;
+    f.span = f.on ? h->d_span : nullptr;
+    f.scratch = h->d_fscratch;
+    return f;
 }
 
 // Launches the hot path for n_frames frames; results go to rows [row0, row0 + n) of the
@@ -537,6 +572,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
                     pl.reason);
     h->last_plan = pl;
     const bool rec = (h->cfg.flags & SP_FLAG_RECORD_OVERLAPS) != 0;
+    const bool full = learn && (h->cfg.flags & SP_FLAG_FULL_LEARNING) != 0;
     cudaError_t e = cudaSuccess;
     if (pl.path == SP_PATH_BATCHED) {
         if (h->ell_dirty) {
@@ -584,6 +620,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         p.counts = h->d_counts + row0;
         p.raw_out = rec ? h->d_raw_rec + static_cast<size_t>(row0) * g.C : nullptr;
         p.boosted_out = rec ? h->d_boosted_rec + static_cast<size_t>(row0) * g.C : nullptr;
+        p.radius_dev = h->d_radius;
         if (!g.whole) {
             p.patch_w = g.pw;
             p.patch_h = g.ph;
@@ -598,10 +635,22 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         return SP_OK;
     }
     const char* lp = std::getenv("SP_LEARN_PATH");  // development override: cluster | grid | input
-    const bool want_grid = learn && h->grid_G && h->cfg.force_path != SP_PATH_PER_INPUT &&
+    if (full && h->span_dirty) {  // connected spans for the radius adaptation (R21)
+        e = sp::launch_span(h->d_idx, h->d_perm, h->cfg.connected_threshold, g.C, g.S, h->d_span, s);
+        h->launches++;
+        if (e != cudaSuccess) return cuda_fail(e, "span launch");
+        h->span_dirty = false;
+    }
+    if (learn) {
+        h->iteration += n;
+        if (full) h->uniform_bc = false;  // boosts now change on the device
+        else h->span_dirty = true;
+    }
+    // the grid kernel plans its shared memory for a fixed radius: no full learning there
+    const bool want_grid = learn && !full && h->grid_G && h->cfg.force_path != SP_PATH_PER_INPUT &&
                            (lp ? std::strcmp(lp, "grid") == 0
                                : ((h->cfg.flags & SP_FLAG_LEARN_GRID) != 0 || h->learn_Q == 0));
-    const bool want_cluster = learn && h->learn_Q && h->cfg.force_path != SP_PATH_PER_INPUT && !want_grid &&
+    const bool want_cluster = learn && !full && h->learn_Q && h->cfg.force_path != SP_PATH_PER_INPUT && !want_grid &&
                               !(lp && std::strcmp(lp, "input") == 0);
     if (want_grid) {
         // the whole sequential stream in one cooperative launch over the SMs
@@ -736,6 +785,9 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         p.counts = h->d_counts;
         p.raw_out = rec ? h->d_raw_rec : nullptr;
         p.boosted_out = rec ? h->d_boosted_rec : nullptr;
+        p.radius_dev = h->d_radius;
+        p.fl = full_learn_params(h);
+        if (full) p.uniform_bc = 0u;
         e = sp::launch_pack(p, s);
         h->launches++;
         if (e != cudaSuccess) return cuda_fail(e, "pack launch");
@@ -760,6 +812,10 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
             h->launches++;
             if (e == cudaSuccess) e = sp::launch_learn(q, 0, s);
             h->launches++;
+            if (full && e == cudaSuccess) {
+                e = sp::launch_full(q, 0, s);
+                h->launches++;
+            }
             if (e != cudaSuccess) return cuda_fail(e, "learning step launch");
         }
         h->ell_dirty = true;
@@ -792,6 +848,8 @@ sp_status sp_config_default(sp_config* cfg) {
     cfg->seed = 42;
     cfg->device = 0;
     cfg->max_inputs = 4096;
+    cfg->duty_cycle_period = 1000;  // S:150, SURVEY §8(f) NEXT-1
+    cfg->max_boost = 2.0f;
     return SP_OK;
 }
 
@@ -910,6 +968,16 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
         e = dalloc(&h->d_synT, static_cast<size_t>(g.C32) * g.S);
         if (e == cudaSuccess) e = dalloc(&h->d_gbar, 1);
     }
+    if (e == cudaSuccess) e = dalloc(&h->d_adc, g.C32);
+    if (e == cudaSuccess) e = dalloc(&h->d_odc, g.C32);
+    if (e == cudaSuccess) e = dalloc(&h->d_span, g.C32);
+    if (e == cudaSuccess) e = dalloc(&h->d_radius, 1);
+    if (e == cudaSuccess) e = dalloc(&h->d_fscratch, sp::full_scratch_floats(g.C32));
+    if (e == cudaSuccess) e = cudaMemset(h->d_adc, 0, g.C32 * 4u);
+    if (e == cudaSuccess) e = cudaMemset(h->d_odc, 0, g.C32 * 4u);
+    if (e == cudaSuccess) e = cudaMemset(h->d_span, 0, g.C32 * 4u);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(h->d_radius, &cfg->inhibition_radius, 4u, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && (cfg->flags & SP_FLAG_RECORD_OVERLAPS)) {
         e = dalloc(&h->d_raw_rec, cap * g.C);
         if (e == cudaSuccess) e = dalloc(&h->d_boosted_rec, cap * g.C);
@@ -1037,6 +1105,41 @@ sp_status sp_set_state(sp_handle* h, const uint32_t* idx, const float* perm, con
     cudaDeviceSynchronize();
     return upload_state(h, idx ? idx : cur_idx.data(), perm ? perm : cur_perm.data(),
                         boost ? boost : cur_boost.data());
+}
+
+sp_status sp_get_learning_state(sp_handle* h, float* active_duty, float* overlap_duty, uint32_t* radius,
+                                uint64_t* iteration) {
+    sp_status st = check_handle(h);
+    if (st != SP_OK) return st;
+    cudaError_t e = cudaDeviceSynchronize();
+    const size_t C = h->g.C;
+    if (e == cudaSuccess && active_duty) e = cudaMemcpy(active_duty, h->d_adc, C * 4u, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && overlap_duty) e = cudaMemcpy(overlap_duty, h->d_odc, C * 4u, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess && radius) e = cudaMemcpy(radius, h->d_radius, 4u, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "sp_get_learning_state");
+    if (iteration) *iteration = h->iteration;
+    return SP_OK;
+}
+
+sp_status sp_set_learning_state(sp_handle* h, const float* active_duty, const float* overlap_duty,
+                                uint32_t radius) {
+    sp_status st = check_handle(h);
+    if (st != SP_OK) return st;
+    const uint32_t C = h->g.C;
+    for (const float* d : {active_duty, overlap_duty})
+        if (d)
+            for (uint32_t c = 0; c < C; ++c)
+                if (!(d[c] >= 0.0f && d[c] <= 1.0f))
+                    return fail(SP_E_ARG, "duty cycle [%u] = %g outside [0,1]", c, d[c]);
+    if (h->cfg.inhibition_radius == 0 ? radius != 0 : (radius < 1 || radius > C))
+        return fail(SP_E_ARG, "radius %u: must be 0 iff the configured radius is 0, else in [1, C] (R21)",
+                    radius);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess && active_duty) e = cudaMemcpy(h->d_adc, active_duty, C * 4u, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && overlap_duty) e = cudaMemcpy(h->d_odc, overlap_duty, C * 4u, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(h->d_radius, &radius, 4u, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "sp_set_learning_state");
+    return SP_OK;
 }
 
 sp_status sp_compute_host(sp_handle* h, const uint8_t* frames_host, uint32_t num_frames, int learn,

@@ -72,6 +72,23 @@ struct alignas(64) BatchedParams {
     uint32_t* counts;          // [num_inputs]
     uint16_t* raw_out;         // nullable [num_inputs][C]
     float* boosted_out;        // nullable [num_inputs][C]
+    const uint32_t* radius_dev;  // nullable: radius in force (full learning adapts it), else `radius`
+};
+
+// Full learning (NEXT-1; S:119(b-e); DESIGN R17-R21): device state and constants.
+struct FullLearn {
+    uint32_t on;               // SP_FLAG_FULL_LEARNING
+    uint32_t adapt;            // radius adaptation (configured radius > 0, R21)
+    float pm1, P;              // duty_cycle_period - 1, duty_cycle_period (fp32)
+    float mb1;                 // fp32(max_boost - 1)
+    float bump;                // fp32(0.1f * tau)
+    float* adc;                // [C32] active duty cycles
+    float* odc;                // [C32] overlap duty cycles
+    float* boost;              // [C32] boosts (written)
+    uint32_t* bc;              // [C32] boost * 2^23 (written)
+    uint32_t* radius;          // device scalar: radius in force
+    uint32_t* span;            // [C32] connected spans (R21)
+    float* scratch;            // window-maximum tables: pre, suf [C32] + table [levels][C32/32]
 };
 
 struct PerInputParams {
@@ -95,6 +112,8 @@ struct PerInputParams {
     uint32_t* counts;          // [call inputs]
     uint16_t* raw_out;         // nullable [call inputs][C]
     float* boosted_out;        // nullable [call inputs][C]
+    const uint32_t* radius_dev;  // nullable: radius in force, else `radius`
+    FullLearn fl;              // full learning (k_learn keeps spans; k_full runs (b)-(e))
 };
 
 struct LearnParams {
@@ -121,6 +140,7 @@ struct LearnParams {
     uint32_t* counts;          // [rows]
     uint16_t* raw_out;         // nullable
     float* boosted_out;        // nullable
+    FullLearn fl;              // full learning, steps (b)-(e) after each input
 };
 
 struct LearnGridParams {
@@ -190,6 +210,10 @@ cudaError_t launch_pack(const PerInputParams& p, cudaStream_t s);
 cudaError_t launch_overlap(const PerInputParams& p, cudaStream_t s);
 cudaError_t launch_inhibit(const PerInputParams& p, cudaStream_t s);
 cudaError_t launch_learn(const PerInputParams& p, uint32_t input, cudaStream_t s);
+cudaError_t launch_full(const PerInputParams& p, uint32_t input, cudaStream_t s);
+cudaError_t launch_span(const uint32_t* idx, const float* perm, float tau, uint32_t C, uint32_t S,
+                        uint32_t* span, cudaStream_t s);
+size_t full_scratch_floats(uint32_t C32);
 cudaError_t launch_build_syn(const uint32_t* idx, const float* perm, float tau, uint32_t C,
                              uint32_t C32, uint32_t S, uint32_t* syn, cudaStream_t s);
 cudaError_t launch_refresh_ell(const uint32_t* idx, const float* perm, const uint32_t* pos,

@@ -5,6 +5,7 @@
 //   P4 k_learn    per input: fused +inc/-dec, clamp, connected-flag refresh (a5)
 // plus layout maintenance (synapse-major idx|flag words, batched ELL flags).
 // Learning runs P2 -> P3 -> P4 per input in order (the recurrence of P:92).
+#include "sp_duty.cuh"
 #include "sp_internal.h"
 #include "sp_select.cuh"
 
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
     const uint32_t t = blockIdx.x;
     const uint32_t gin = p.first_input + t;
     const uint32_t tid = threadIdx.x, nthr = blockDim.x;
+    const uint32_t radius = p.radius_dev ? *p.radius_dev : p.radius;  // adapted by full learning
     for (uint32_t c = tid; c < g.C32; c += nthr) {
         s_raw[c] = p.raw[static_cast<size_t>(t) * g.C32 + c];
         s_bc[c] = p.bc[c];
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
         }
     }
     uint64_t T = 0;
-    if (p.radius == 0) {
+    if (radius == 0) {
         for (int bit = static_cast<int>(g.keyBits) - 1, it = 0; bit >= 0; --bit, ++it) {
             const uint64_t cand = T | (1ull << bit);
             uint32_t cnt = 0;
@@ -148,27 +150,27 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
     // SDR: warp per 32-column word
     const uint64_t one = 1ull << 23;
     uint32_t my_total = 0;
-    if (p.radius > 0 && p.uniform_bc) {
+    if (radius > 0 && p.uniform_bc) {
         // local inhibition, uniform boost: bit-sliced window comparator (sp_select.cuh)
         const uint32_t r_lo = uniform_r_lo(theta, s_bc[0]);
         const uint32_t nb = raw_bits(g.S);
         build_raw_planes(s_raw, s_planes, g.ncw, nb, r_lo, tid >> 5, nthr >> 5, tid & 31u);
         __syncthreads();
         for (uint32_t cw = tid >> 5; cw < g.ncw; cw += nthr >> 5) {
-            const uint32_t word = local_uniform_word(s_raw, s_planes, g.ncw, nb, cw, g.C, p.radius, p.k,
+            const uint32_t word = local_uniform_word(s_raw, s_planes, g.ncw, nb, cw, g.C, radius, p.k,
                                                      r_lo, tid & 31u);
             if ((tid & 31u) == 0) {
                 p.sdr[static_cast<size_t>(gin) * g.ncw + cw] = word;
                 my_total += __popc(word);
             }
         }
-    } else if (p.radius > 0) {
+    } else if (radius > 0) {
         // local inhibition, per-column boosts: coarse bit-sliced + exact ties (sp_select.cuh)
         const uint32_t sh = g.keyBits - L - 16u;
         build_coarse_planes(s_raw, s_bc, s_planes, g.ncw, theta, sh, tid >> 5, nthr >> 5, tid & 31u);
         __syncthreads();
         for (uint32_t cw = tid >> 5; cw < g.ncw; cw += nthr >> 5) {
-            const uint32_t word = local_general_word(s_raw, s_bc, s_planes, g.ncw, cw, g.C, p.radius, p.k,
+            const uint32_t word = local_general_word(s_raw, s_bc, s_planes, g.ncw, cw, g.C, radius, p.k,
                                                      theta, sh, L, tid & 31u);
             if ((tid & 31u) == 0) {
                 p.sdr[static_cast<size_t>(gin) * g.ncw + cw] = word;
@@ -182,11 +184,11 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
         const uint64_t key = key_of(s_raw[c], s_bc[c], theta, c, L, N);
         bool act = N > one;
         if (act) {
-            if (p.radius == 0) {
+            if (radius == 0) {
                 act = key >= T;
             } else {
-                const uint32_t lo = c >= p.radius ? c - p.radius : 0u;
-                const uint32_t hi = min(g.C - 1u, c + p.radius);
+                const uint32_t lo = c >= radius ? c - radius : 0u;
+                const uint32_t hi = min(g.C - 1u, c + radius);
                 uint32_t beats = 0;
                 for (uint32_t d = lo; d <= hi && beats < p.k; ++d) {
                     uint64_t Nd;
@@ -223,6 +225,7 @@ __global__ void k_learn(const PerInputParams p, uint32_t t) {
     const uint32_t* bits = p.bits + static_cast<size_t>(t) * p.Wn;
     const uint32_t* idx = p.idx + static_cast<size_t>(c) * g.S;
     float* perm = p.perm + static_cast<size_t>(c) * g.S;
+    uint32_t smin = 0xFFFFFFFFu, smax = 0u;
     for (uint32_t s = lane; s < g.S; s += 32u) {
         const uint32_t i = idx[s];
         const bool on = ((bits[i >> 5] >> (i & 31u)) & 1u) != 0u;
@@ -230,7 +233,87 @@ __global__ void k_learn(const PerInputParams p, uint32_t t) {
         v = fminf(fmaxf(v, 0.0f), 1.0f);
         perm[s] = v;
         p.syn_rw[static_cast<size_t>(s) * g.C32 + c] = i | (v >= p.tau ? 0x80000000u : 0u);
+        span_accumulate(v >= p.tau, s, smin, smax);
     }
+    if (p.fl.span) {  // full learning: the connected span of the updated column (R21)
+        const uint32_t sp_c = span_finish(smin, smax, idx, 0xFFFFFFFFu);
+        if (lane == 0) p.fl.span[c] = sp_c;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// P5: full learning steps (b)-(e) after input t's permanence update (S:119(b-e); DESIGN
+// R17-R21), one CTA of 1024 threads: duty cycles of every column, window maxima (sp_duty.cuh),
+// boosts, the bump of weak columns (warp per weak column: perm, synapse-major flags, span)
+// and the adapted radius from the sum of the connected spans.
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_full(const PerInputParams p, uint32_t t) {
+    const Geometry& g = p.g;
+    const FullLearn& fl = p.fl;
+    const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u;
+    const uint32_t gin = p.first_input + t;
+    const uint32_t* sdr = p.sdr + static_cast<size_t>(gin) * g.ncw;
+    const uint32_t* raw = p.raw + static_cast<size_t>(t) * g.C32;
+    const uint32_t r = *fl.radius;  // radius in force for this input (W(c) of (c), (d); R18)
+    const uint32_t nb = g.C32 / 32u;
+    float* pre = fl.scratch;
+    float* suf = pre + g.C32;
+    float* table = suf + g.C32;
+    __shared__ unsigned long long s_span;
+    if (tid == 0) s_span = 0ull;
+    // (b) duty cycles
+    for (uint32_t c = tid; c < g.C; c += nthr) {
+        const bool a = ((sdr[c >> 5] >> (c & 31u)) & 1u) != 0u;
+        const bool o = raw[c] >= p.min_overlap && raw[c] > 0u;  // N > 0
+        fl.adc[c] = duty_update(fl.adc[c], a, fl.pm1, fl.P);
+        fl.odc[c] = duty_update(fl.odc[c], o, fl.pm1, fl.P);
+    }
+    __syncthreads();
+    auto sync = [] { __syncthreads(); };
+    // (c) boosts from the active duty cycles
+    wmax_build(fl.adc, g.C, g.C32, pre, suf, table, 0u, nthr, sync);
+    for (uint32_t c = tid; c < g.C; c += nthr) {
+        const float b = boost_rule(fl.adc[c], wmax_query(fl.adc, pre, suf, table, nb, g.C, c, r), fl.mb1);
+        fl.boost[c] = b;
+        fl.bc[c] = boost_bc(b);
+    }
+    __syncthreads();
+    // (d) bump of the weak columns, warp per column
+    wmax_build(fl.odc, g.C, g.C32, pre, suf, table, 0u, nthr, sync);
+    for (uint32_t c = tid >> 5; c < g.C; c += nthr >> 5) {
+        if (!weak_column(fl.odc[c], wmax_query(fl.odc, pre, suf, table, nb, g.C, c, r))) continue;
+        const uint32_t* idx = p.idx + static_cast<size_t>(c) * g.S;
+        float* perm = p.perm + static_cast<size_t>(c) * g.S;
+        uint32_t smin = 0xFFFFFFFFu, smax = 0u;
+        for (uint32_t s = lane; s < g.S; s += 32u) {
+            const float v = fminf(__fadd_rn(perm[s], fl.bump), 1.0f);
+            perm[s] = v;
+            p.syn_rw[static_cast<size_t>(s) * g.C32 + c] = idx[s] | (v >= p.tau ? 0x80000000u : 0u);
+            span_accumulate(v >= p.tau, s, smin, smax);
+        }
+        const uint32_t sp_c = span_finish(smin, smax, idx, 0xFFFFFFFFu);
+        if (lane == 0) fl.span[c] = sp_c;
+    }
+    if (!fl.adapt) return;
+    __syncthreads();
+    // (e) radius from the connected spans (exact integer form of S:151, R21)
+    unsigned long long part = 0;
+    for (uint32_t c = tid; c < g.C; c += nthr) part += fl.span[c];
+    for (uint32_t d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
+    if (lane == 0 && part) atomicAdd(&s_span, part);
+    __syncthreads();
+    if (tid == 0) *fl.radius = adapt_radius(s_span, g.nbits, g.C);
+}
+
+// spans of every column from the canonical arrays (warp per column; R21)
+__global__ void k_span(const uint32_t* idx, const float* perm, float tau, uint32_t C, uint32_t S, uint32_t* span) {
+    const uint32_t c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const uint32_t lane = threadIdx.x & 31u;
+    if (c >= C) return;
+    uint32_t smin = 0xFFFFFFFFu, smax = 0u;
+    for (uint32_t s = lane; s < S; s += 32u) span_accumulate(perm[static_cast<size_t>(c) * S + s] >= tau, s, smin, smax);
+    const uint32_t v = span_finish(smin, smax, idx + static_cast<size_t>(c) * S, 0xFFFFFFFFu);
+    if (lane == 0) span[c] = v;
 }
 
 // syn[s][c] = idx | connected << 31 from the canonical arrays; pad columns point nowhere.
@@ -306,6 +389,19 @@ cudaError_t launch_learn(const PerInputParams& p, uint32_t input, cudaStream_t s
     k_learn<<<(p.g.C + warps - 1) / warps, warps * 32, 0, s>>>(p, input);
     return cudaGetLastError();
 }
+
+cudaError_t launch_full(const PerInputParams& p, uint32_t input, cudaStream_t s) {
+    k_full<<<1, 1024, 0, s>>>(p, input);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_span(const uint32_t* idx, const float* perm, float tau, uint32_t C, uint32_t S,
+                        uint32_t* span, cudaStream_t s) {
+    k_span<<<(C + 7u) / 8u, 256, 0, s>>>(idx, perm, tau, C, S, span);
+    return cudaGetLastError();
+}
+
+size_t full_scratch_floats(uint32_t C32) { return 2u * C32 + wmax_levels(C32 / 32u) * (C32 / 32u) + 32u; }
 
 cudaError_t launch_build_syn(const uint32_t* idx, const float* perm, float tau, uint32_t C,
                              uint32_t C32, uint32_t S, uint32_t* syn, cudaStream_t s) {

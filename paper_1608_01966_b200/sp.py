@@ -21,6 +21,7 @@ SP_OK, SP_E_CONFIG, SP_E_ARG, SP_E_SHAPE, SP_E_CUDA, SP_E_OOM, SP_E_STATE = rang
 SP_PATH_AUTO, SP_PATH_PER_INPUT, SP_PATH_BATCHED = 0, 1, 2
 SP_FLAG_RECORD_OVERLAPS = 1
 SP_FLAG_LEARN_GRID = 2
+SP_FLAG_FULL_LEARNING = 4
 SP_LEARN_PER_INPUT, SP_LEARN_CLUSTER, SP_LEARN_GRID = 0, 1, 2
 
 
@@ -37,7 +38,7 @@ STATUS_NAMES = {0: "SP_OK", 1: "SP_E_CONFIG", 2: "SP_E_ARG", 3: "SP_E_SHAPE", 4:
 ABI_SYMBOLS = ("sp_config_default", "sp_create", "sp_destroy", "sp_compute", "sp_winners",
                "sp_overlaps", "sp_get_state", "sp_set_state", "sp_compute_host", "sp_plan",
                "sp_init_pools_host", "sp_get_info", "sp_last_error", "sp_version",
-               "sp_synth_frames")
+               "sp_get_learning_state", "sp_set_learning_state", "sp_synth_frames")
 
 
 class SpError(RuntimeError):
@@ -59,6 +60,7 @@ class SpConfig(ctypes.Structure):
         ("seed", ctypes.c_uint64), ("device", ctypes.c_int32),
         ("max_inputs", ctypes.c_uint32), ("flags", ctypes.c_uint32),
         ("force_path", ctypes.c_uint32),
+        ("duty_cycle_period", ctypes.c_uint32), ("max_boost", ctypes.c_float),
     ]
 
 
@@ -107,6 +109,8 @@ def lib() -> ctypes.CDLL:
         "sp_plan": [P(SpConfig), u32, i32, P(SpPlanInfo)],
         "sp_init_pools_host": [P(SpConfig), vp],
         "sp_get_info": [vp, P(SpInfo)],
+        "sp_get_learning_state": [vp, vp, vp, vp, vp],
+        "sp_set_learning_state": [vp, vp, vp, u32],
         "sp_synth_frames": [vp, u64, u32, u32, u32, u64, u32, u32, vp],
     }
     for name, args in sig.items():
@@ -304,6 +308,30 @@ class SpatialPooler:
         p, pp = arr(perm, np.float32, (self.C, self.S))
         b, bp = arr(boost, np.float32, (self.C,))
         _check(lib().sp_set_state(self._h, ip, pp, bp))
+
+    def get_learning_state(self):
+        """Full-learning state: (active_duty f32[C], overlap_duty f32[C], radius, iteration)."""
+        adc = np.empty((self.C,), np.float32)
+        odc = np.empty((self.C,), np.float32)
+        r = ctypes.c_uint32()
+        it = ctypes.c_uint64()
+        _check(lib().sp_get_learning_state(self._h, adc.ctypes.data, odc.ctypes.data,
+                                           ctypes.byref(r), ctypes.byref(it)))
+        return adc, odc, int(r.value), int(it.value)
+
+    def set_learning_state(self, active_duty=None, overlap_duty=None, radius=None):
+        def arr(a):
+            if a is None:
+                return None, None
+            a = np.ascontiguousarray(a, dtype=np.float32)
+            if a.shape != (self.C,):
+                raise SpError(SP_E_SHAPE, f"duty array shape {a.shape} != {(self.C,)}")
+            return a, ctypes.c_void_p(a.ctypes.data)
+        a, ap = arr(active_duty)
+        o, op = arr(overlap_duty)
+        if radius is None:
+            radius = self.get_learning_state()[2]
+        _check(lib().sp_set_learning_state(self._h, ap, op, int(radius)))
 
     def info(self) -> dict:
         out = SpInfo()
