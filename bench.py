@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-learn-full", action="store_true")
     return ap.parse_args()
 
 
@@ -238,6 +239,28 @@ def main():
                  "kernel_launches": sp.kernel_launches() - l0,
                  "path": P.learn_path_name(info),
                  "workload": "BASELINE config 2 learning stream (sequential), whole 960x540 frames"}
+        # full learning (NEXT-1: duty cycles, boost update, bump, radius adaptation from Tab. 2's
+        # initial radius 80) on the same stream, with its own handle
+        if not args.no_learn_full:
+            spf = P.SpatialPooler(input_width=W, input_height=H, num_columns=C, synapses_per_column=S,
+                                  min_overlap=THETA, winners_set_size=K_WIN, inhibition_radius=80,
+                                  seed=SEED_STATE, device=local, max_inputs=args.learn_frames,
+                                  flags=P.SP_FLAG_FULL_LEARNING, duty_cycle_period=1000, max_boost=2.0)
+            spf.compute(lf[:4], learn=True)
+            torch.cuda.synchronize()
+            l0 = spf.kernel_launches()
+            e0.record(stream)
+            spf.compute(lf[4:], learn=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            radius = spf.get_learning_state()[2]
+            learn["full"] = {"frames": nl, "ms": ms, "us_per_frame": ms * 1e3 / nl,
+                             "frames_per_s": nl / ms * 1e3, "kernel_launches": spf.kernel_launches() - l0,
+                             "path": P.learn_path_name(spf.info()), "radius_after": radius,
+                             "workload": "config 2 stream with full learning (S:119(b-e)): duty period "
+                                         "1000, max_boost 2, initial radius 80 (Tab. 2), adapted"}
+            spf.close()
         del lf
     if world > 1:
         D.broadcast_state(sp, src=0, device=dev)

@@ -650,7 +650,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
     const bool want_grid = learn && !full && h->grid_G && h->cfg.force_path != SP_PATH_PER_INPUT &&
                            (lp ? std::strcmp(lp, "grid") == 0
                                : ((h->cfg.flags & SP_FLAG_LEARN_GRID) != 0 || h->learn_Q == 0));
-    const bool want_cluster = learn && !full && h->learn_Q && h->cfg.force_path != SP_PATH_PER_INPUT && !want_grid &&
+    const bool want_cluster = learn && h->learn_Q && h->cfg.force_path != SP_PATH_PER_INPUT && !want_grid &&
                               !(lp && std::strcmp(lp, "input") == 0);
     if (want_grid) {
         // the whole sequential stream in one cooperative launch over the SMs
@@ -717,7 +717,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         q.num_inputs = n;
         q.g = g;
         q.Q = h->learn_Q;
-        sp::learn_cluster_smem(g, q.Q, &q.cols_per_cta, h->learn_dbl);
+        sp::learn_cluster_smem(g, q.Q, &q.cols_per_cta, h->learn_dbl, full);
         q.dbl_bits = h->learn_dbl ? 1u : 0u;
         if (const char* d = std::getenv("SP_LEARN_DBG")) q.dbg = static_cast<uint32_t>(std::atoi(d));
         q.syn_stride = sp::learn_syn_stride(g.S);
@@ -741,6 +741,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         q.counts = h->d_counts;
         q.raw_out = rec ? h->d_raw_rec : nullptr;
         q.boosted_out = rec ? h->d_boosted_rec : nullptr;
+        q.fl = full_learn_params(h);
         e = sp::launch_learn_cluster(q, h->learn_smem, s);
         h->launches++;
         if (e != cudaSuccess) return cuda_fail(e, "cluster learning launch");
@@ -910,7 +911,8 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
         for (uint32_t Q = 16; Q >= 1; Q /= 2) {
             if (Q > 1 && Q * 32u > h->g.C32) continue;
             for (int dbl = 1; dbl >= 0 && !h->learn_Q; --dbl) {
-                const uint32_t smem = sp::learn_cluster_smem(h->g, Q, nullptr, dbl != 0);
+                const uint32_t smem = sp::learn_cluster_smem(h->g, Q, nullptr, dbl != 0,
+                                                             (cfg->flags & SP_FLAG_FULL_LEARNING) != 0);
                 if (static_cast<int>(smem) > h->max_smem - 1024) continue;
                 int n = 0;
                 sp::learn_max_clusters(Q, smem, &n);

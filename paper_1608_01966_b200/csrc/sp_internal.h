@@ -179,7 +179,7 @@ cudaError_t launch_build_synT(const uint32_t* idx, const float* perm, float tau,
                               uint32_t S, uint32_t* synT, cudaStream_t s);
 
 // cluster learning (sp_learn.cu)
-uint32_t learn_cluster_smem(const Geometry& g, uint32_t Q, uint32_t* cols_per_cta, bool dbl_bits);
+uint32_t learn_cluster_smem(const Geometry& g, uint32_t Q, uint32_t* cols_per_cta, bool dbl_bits, bool full);
 uint32_t learn_syn_stride(uint32_t S);
 uint32_t learn_threads_per_column(uint32_t cpc);
 cudaError_t configure_learn(int max_smem);

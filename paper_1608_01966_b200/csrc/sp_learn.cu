@@ -15,10 +15,18 @@
 //                 (fp32 RN add/sub + clamp, R3) and their connected flags in smem
 //
 // One cluster barrier per input; the frame of t+2 is prefetched into L2 (bulk prefetch)
-// two inputs ahead.  Only the frame bytes and the winners' permanence rows touch memory
+// two inputs ahead.
+//
+// Full learning (SP_FLAG_FULL_LEARNING, NEXT-1; S:119(b-e); DESIGN R17-R21) adds, after the
+// permanence update of input t: the SDR words of every CTA are broadcast (DSMEM) -> a second
+// cluster barrier -> every CTA updates the duty cycles of ALL columns and recomputes ALL boosts
+// (the same fp32 operations in every CTA, so the replicas stay identical and the next
+// selection needs no exchange), bumps its own weak columns, and sends the sum of its columns'
+// connected spans to every CTA; the radius of input t+1 is formed after the overlap barrier.  Only the frame bytes and the winners' permanence rows touch memory
 // below L2.  DESIGN.md §4.2.
 #include <cooperative_groups.h>
 
+#include "sp_duty.cuh"
 #include "sp_internal.h"
 #include "sp_pack.cuh"
 #include "sp_select.cuh"
@@ -50,7 +58,8 @@ __device__ __forceinline__ void emit_word(const LearnParams& p, uint32_t* s_sdr,
 // s = part, part+tpc, ..) with a shuffle reduction; the padded column-major slice keeps
 // the reads conflict-free
 __device__ __forceinline__ void overlap_step(const LearnParams& p, cg::cluster_group& cluster, const uint32_t* s_syn,
-                                             const uint32_t* bits, uint16_t* raw_buf, uint32_t c0, uint32_t gin) {
+                                             const uint32_t* bits, uint16_t* raw_buf, uint32_t c0, uint32_t gin,
+                                             const uint32_t* s_bc) {
     const Geometry& g = p.g;
     const uint32_t cpc = p.cols_per_cta, ss = p.syn_stride, tpc = p.tpc, Q = p.Q;
     for (uint32_t base = 0; base < cpc * tpc; base += blockDim.x) {
@@ -79,8 +88,11 @@ __device__ __forceinline__ void overlap_step(const LearnParams& p, cg::cluster_g
             for (uint32_t r = 0; r < Q; ++r) cluster.map_shared_rank(raw_buf, r)[c] = static_cast<uint16_t>(raw);
             if (p.raw_out && c < g.C) {
                 p.raw_out[static_cast<size_t>(gin) * g.C + c] = static_cast<uint16_t>(raw);
+                // boost = Bc * 2^-23 exactly (Bc has <= 24 significant bits); the boost in
+                // force for this input (full learning updates s_bc between inputs)
+                const float b = __fmul_rn(__uint2float_rn(s_bc[c]), 1.1920928955078125e-07f);
                 p.boosted_out[static_cast<size_t>(gin) * g.C + c] =
-                    raw >= p.min_overlap ? __fmul_rn(static_cast<float>(raw), p.boost[c]) : 0.0f;
+                    raw >= p.min_overlap ? __fmul_rn(static_cast<float>(raw), b) : 0.0f;
             }
         }
     }
@@ -109,6 +121,20 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
     uint64_t* s_ties = reinterpret_cast<uint64_t*>(s_raw + 2u * C32r);  // [ncl][64] tie lists
     uint32_t* s_sdr = reinterpret_cast<uint32_t*>(s_ties + ncl * 64u);  // [ncl] SDR words
     uint32_t* s_planes = s_sdr + ncl;                               // [ncw][16] key bit-planes
+    // full learning (p.fl.on): replicated duty cycles and window-maximum tables, the SDR of
+    // the whole input, own spans, per-CTA span sums
+    const FullLearn& fl = p.fl;
+    const uint32_t nb = g.C32 / 32u;
+    float* s_adc = reinterpret_cast<float*>(s_planes + g.ncw * 16u);  // [C32]
+    float* s_odc = s_adc + g.C32;                                       // [C32]
+    float* s_pre = s_odc + g.C32;                                       // [C32]
+    float* s_suf = s_pre + g.C32;                                       // [C32]
+    float* s_table = s_suf + g.C32;                                     // [levels][nb]
+    uint32_t* s_sdr_all = reinterpret_cast<uint32_t*>(s_table + wmax_levels(nb) * nb);  // [ncw]
+    uint32_t* s_span = s_sdr_all + g.ncw;                               // [cpc]
+    unsigned long long* s_spanpart =
+        reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(s_span + cpc) + 7u) & ~uintptr_t(7));  // [Q]
+    __shared__ unsigned long long s_myspan;
     auto bits_of = [&](uint32_t t) { return s_bits + (p.dbl_bits ? (t & 1u) * Wn4 : 0u); };
     auto gbits_of = [&](uint32_t t) { return p.bits_g + (t & 1u) * Wn4; };
 
@@ -118,6 +144,15 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
         s_syn[cl * ss + s] = c < g.C32 ? p.syn[static_cast<size_t>(s) * g.C32 + c] : 0u;
     }
     for (uint32_t c = tid; c < g.C32; c += nthr) s_bc[c] = p.bc[c];
+    uint32_t R = p.radius;  // radius in force (full learning: adapted after every input)
+    if (fl.on) {
+        R = *fl.radius;
+        for (uint32_t c = tid; c < g.C32; c += nthr) {
+            s_adc[c] = c < g.C ? fl.adc[c] : 0.0f;
+            s_odc[c] = c < g.C ? fl.odc[c] : 0.0f;
+        }
+        for (uint32_t cl = tid; cl < cpc; cl += nthr) s_span[cl] = c0 + cl < g.C ? fl.span[c0 + cl] : 0u;
+    }
     if (q == 0)
         for (uint32_t i = tid; i < n; i += nthr) p.counts[p.first_input + i] = 0u;
     if (tid == 0) {
@@ -129,7 +164,7 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
     const uint32_t wbeg = q * Wn / Q, wend = (q + 1) * Wn / Q;  // packed words of this CTA
     uint64_t* trace = (p.trace && q == 0 && tid == 0) ? p.trace : nullptr;
     // phase accumulators of the traced threads live in smem (no registers held in the loop)
-    __shared__ uint64_t s_tr[8];
+    __shared__ uint64_t s_tr[9];
     uint64_t& t_ld = s_tr[0];
     uint64_t& t_ov = s_tr[1];
     uint64_t& t_bar = s_tr[2];
@@ -138,8 +173,9 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
     uint64_t& t_ph = s_tr[5];
     uint64_t& t_sub = s_tr[6];
     uint64_t& t_pk = s_tr[7];
+    uint64_t& t_full = s_tr[8];
     if (tid == 0)
-        for (int i = 0; i < 8; ++i) s_tr[i] = 0;
+        for (int i = 0; i < 9; ++i) s_tr[i] = 0;
     uint32_t phase = 0;  // parity of s_bar's next completion
     // selection warps (global inhibition): one per owned column-word; the others pack
     const uint32_t nsel = ncl < nw ? ncl : nw;
@@ -157,7 +193,7 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
         if (tid == 0) bulk_load_bits(bits_of(0), gbits_of(0), Wn, &s_bar);
         mbar_wait(&s_bar, phase);
         phase ^= 1u;
-        overlap_step(p, cluster, s_syn, bits_of(0), s_raw, c0, p.first_input);
+        overlap_step(p, cluster, s_syn, bits_of(0), s_raw, c0, p.first_input, s_bc);
     }
     cluster.sync();  // raw counts of input 0 everywhere
 
@@ -165,6 +201,11 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
         const uint32_t gin = p.first_input + t;
         const uint16_t* raw_t = s_raw + (t & 1u) * C32r;
         const bool more = t + 1u < n;
+        if (fl.adapt && t > 0u) {  // radius of input t from the span sums of input t-1 (R21)
+            unsigned long long sum = 0;
+            for (uint32_t r = 0; r < Q; ++r) sum += s_spanpart[r];
+            R = adapt_radius(sum, g.nbits, g.C);
+        }
         if (trace) t_ph = globaltimer();
         if (tid == 0) {
             prefetch_input(p, t + 3u, wbeg, wend, q, Q);
@@ -174,20 +215,20 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
         }
         // ---- a3/a4: the same exact k-winners in every CTA (sp_select.cuh), while the
         //      other warps pack input t+2 into the global buffer input t used ----------
-        if (p.radius > 0) {
+        if (R > 0) {
             const bool uni = p.uniform_bc != 0u;
             const uint32_t r_lo = uniform_r_lo(theta, s_bc[0]);
-            const uint32_t nb = raw_bits(g.S);
+            const uint32_t rb = raw_bits(g.S);
             const uint32_t sh = g.keyBits - L - 16u;
-            if (uni) build_raw_planes(raw_t, s_planes, g.ncw, nb, r_lo, wi, nw, lane);
+            if (uni) build_raw_planes(raw_t, s_planes, g.ncw, rb, r_lo, wi, nw, lane);
             else build_coarse_planes(raw_t, s_bc, s_planes, g.ncw, theta, sh, wi, nw, lane);
             __syncthreads();
             for (uint32_t cw = wi; cw < ncl; cw += nw) {
                 const uint32_t gcw = c0 / 32u + cw;
                 uint32_t word = 0u;
                 if (gcw < g.ncw)
-                    word = uni ? local_uniform_word(raw_t, s_planes, g.ncw, nb, gcw, g.C, p.radius, p.k, r_lo, lane)
-                               : local_general_word(raw_t, s_bc, s_planes, g.ncw, gcw, g.C, p.radius, p.k, theta,
+                    word = uni ? local_uniform_word(raw_t, s_planes, g.ncw, rb, gcw, g.C, R, p.k, r_lo, lane)
+                               : local_general_word(raw_t, s_bc, s_planes, g.ncw, gcw, g.C, R, p.k, theta,
                                                     sh, L, lane);
                 emit_word(p, s_sdr, cw, gcw, gin, word, lane);
             }
@@ -226,6 +267,7 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
             if (((s_sdr[cl >> 5] >> (cl & 31u)) & 1u) == 0u) continue;
             float* __restrict__ perm = p.perm + static_cast<size_t>(c) * g.S;
             uint32_t* col = s_syn + cl * ss;
+            uint32_t smin = 0xFFFFFFFFu, smax = 0u;
             for (uint32_t s0 = 0; s0 < g.S; s0 += 256u) {
                 float v[8];
 #pragma unroll
@@ -243,11 +285,78 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
                         x = fminf(fmaxf(x, 0.0f), 1.0f);
                         perm[s] = x;
                         col[s] = i | (x >= p.tau ? 0x80000000u : 0u);
+                        span_accumulate(x >= p.tau, s, smin, smax);
                     }
                 }
             }
+            if (fl.on) {  // connected span of the updated column (R21)
+                const uint32_t v = span_finish(smin, smax, col, 0x7FFFFFFFu);
+                if (lane == 0) s_span[cl] = v;
+            }
         }
         __syncthreads();  // flags updated (and, with one buffer, the plane of t released)
+        if (fl.on) {
+            if (trace) {
+                t_learn += globaltimer() - t_ph;
+                t_ph = globaltimer();
+            }
+            // ---- full learning (b)-(e) of input t (S:119(b-e); DESIGN R17-R21) -------------
+            for (uint32_t i = tid; i < ncl * Q; i += nthr) {  // this CTA's SDR words to every CTA
+                const uint32_t gcw = c0 / 32u + i % ncl;
+                if (gcw < g.ncw) cluster.map_shared_rank(s_sdr_all, i / ncl)[gcw] = s_sdr[i % ncl];
+            }
+            if (tid == 0) s_myspan = 0ull;
+            cluster.sync();  // the whole SDR of input t everywhere
+            // (b) duty cycles of every column (replicated)
+            for (uint32_t c = tid; c < g.C; c += nthr) {
+                const bool a = ((s_sdr_all[c >> 5] >> (c & 31u)) & 1u) != 0u;
+                const uint32_t r = raw_t[c];
+                s_adc[c] = duty_update(s_adc[c], a, fl.pm1, fl.P);
+                s_odc[c] = duty_update(s_odc[c], r >= theta && r > 0u, fl.pm1, fl.P);
+            }
+            __syncthreads();
+            auto sync = [] { __syncthreads(); };
+            // (c) boosts of every column (replicated): the keys of input t+1
+            wmax_build(s_adc, g.C, g.C32, s_pre, s_suf, s_table, 0u, nthr, sync);
+            for (uint32_t c = tid; c < g.C; c += nthr)
+                s_bc[c] = boost_bc(boost_rule(s_adc[c], wmax_query(s_adc, s_pre, s_suf, s_table, nb, g.C, c, R),
+                                              fl.mb1));
+            __syncthreads();
+            // (d) bump of this CTA's weak columns, warp per column
+            wmax_build(s_odc, g.C, g.C32, s_pre, s_suf, s_table, 0u, nthr, sync);
+            for (uint32_t cl = wi; cl < cpc; cl += nw) {
+                const uint32_t c = c0 + cl;
+                if (c >= g.C) break;
+                if (!weak_column(s_odc[c], wmax_query(s_odc, s_pre, s_suf, s_table, nb, g.C, c, R))) continue;
+                float* __restrict__ perm = p.perm + static_cast<size_t>(c) * g.S;
+                uint32_t* col = s_syn + cl * ss;
+                uint32_t smin = 0xFFFFFFFFu, smax = 0u;
+                for (uint32_t s = lane; s < g.S; s += 32u) {
+                    const float x = fminf(__fadd_rn(__ldcg(perm + s), fl.bump), 1.0f);
+                    perm[s] = x;
+                    col[s] = (col[s] & 0x7FFFFFFFu) | (x >= p.tau ? 0x80000000u : 0u);
+                    span_accumulate(x >= p.tau, s, smin, smax);
+                }
+                const uint32_t v = span_finish(smin, smax, col, 0x7FFFFFFFu);
+                if (lane == 0) s_span[cl] = v;
+            }
+            if (fl.adapt) {
+                __syncthreads();
+                // (e) this CTA's span sum to every CTA; the radius of t+1 is formed after the
+                // next barrier
+                unsigned long long part = 0;
+                for (uint32_t cl = tid; cl < cpc; cl += nthr) part += c0 + cl < g.C ? s_span[cl] : 0u;
+                for (uint32_t d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
+                if (lane == 0 && part) atomicAdd(&s_myspan, part);
+                __syncthreads();
+                if (tid < Q) cluster.map_shared_rank(s_spanpart, tid)[q] = s_myspan;
+            }
+            __syncthreads();  // bumped flags and new boosts visible to the overlap of t+1
+            if (trace) {
+                t_full += globaltimer() - t_ph;
+                t_ph = globaltimer();
+            }
+        }
         if (trace) {
             t_learn += globaltimer() - t_ph;
             t_ph = globaltimer();
@@ -264,7 +373,7 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
         // raw counts of t+1 go to the other parity buffer: a CTA still selecting input t
         // reads this one; the buffer of t is rewritten (input t+2) only after every CTA has
         // passed the barrier below
-        overlap_step(p, cluster, s_syn, bits_of(t + 1u), s_raw + ((t + 1u) & 1u) * C32r, c0, gin + 1u);
+        overlap_step(p, cluster, s_syn, bits_of(t + 1u), s_raw + ((t + 1u) & 1u) * C32r, c0, gin + 1u, s_bc);
         if (trace) {
             t_ov += globaltimer() - t_ph;
             t_ph = globaltimer();
@@ -280,8 +389,28 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
         trace[4] = t_learn;
         trace[5] = n;
         trace[6] = t_sub;
+        trace[8] = t_full;
     }
     if (trace_pk) trace_pk[7] = t_pk;
+    if (fl.on) {  // ---- full-learning state back to global (replicas are identical) ---------
+        if (fl.adapt) {
+            cluster.sync();  // span sums of the last input everywhere
+            unsigned long long sum = 0;
+            for (uint32_t r = 0; r < Q; ++r) sum += s_spanpart[r];
+            R = adapt_radius(sum, g.nbits, g.C);
+        }
+        if (n > 0 && q == 0) {
+            for (uint32_t c = tid; c < g.C; c += nthr) {
+                fl.adc[c] = s_adc[c];
+                fl.odc[c] = s_odc[c];
+                fl.bc[c] = s_bc[c];
+                fl.boost[c] = __fmul_rn(__uint2float_rn(s_bc[c]), 1.1920928955078125e-07f);
+            }
+            if (tid == 0) *fl.radius = R;
+        }
+        for (uint32_t cl = tid; cl < cpc; cl += nthr)
+            if (c0 + cl < g.C) fl.span[c0 + cl] = s_span[cl];
+    }
     // ---- write the resident connected flags back (the per-input path reads them) ---------
     for (uint32_t i = tid; i < g.S * cpc; i += nthr) {
         const uint32_t s = i / cpc, cl = i % cpc, c = c0 + cl;
@@ -298,12 +427,15 @@ uint32_t learn_threads_per_column(uint32_t cpc) {
     return t;
 }
 
-uint32_t learn_cluster_smem(const Geometry& g, uint32_t Q, uint32_t* cols_per_cta, bool dbl_bits) {
+uint32_t learn_cluster_smem(const Geometry& g, uint32_t Q, uint32_t* cols_per_cta, bool dbl_bits, bool full) {
     const uint32_t cpc = ((g.C32 + Q - 1u) / Q + 31u) / 32u * 32u;
     const uint32_t Wn4 = ((g.nbits + 31u) / 32u + 3u) / 4u * 4u;
     if (cols_per_cta) *cols_per_cta = cpc;
+    const uint32_t nb = g.C32 / 32u;
+    const uint32_t full_bytes = full ? 4u * (4u * g.C32 + wmax_levels(nb) * nb + g.ncw + cpc) + 8u + 8u * Q : 0u;
     return 4u * (learn_syn_stride(g.S) * cpc + (dbl_bits ? 2u : 1u) * Wn4 + g.C32) +
-           4u * ((g.C32 + 3u) / 4u * 4u) + 8u * (cpc / 32u * 64u) + 4u * (cpc / 32u) + 4u * (g.ncw * 16u);
+           4u * ((g.C32 + 3u) / 4u * 4u) + 8u * (cpc / 32u * 64u) + 4u * (cpc / 32u) + 4u * (g.ncw * 16u) +
+           full_bytes;
 }
 
 cudaError_t configure_learn(int max_smem) {

@@ -40,16 +40,28 @@ def run(label, n, boost_seeded=False, **kw):
     info = sp.info()
     ni = max(int(buf[5]), 1)
     names = (["bits", "overlap", "grid_barrier", "select", "learn"] if info["last_learn_path"] == 2 else
-             ["wait_bits", "overlap", "barrier", "select+pack", "learn", "", "select_only", "pack_only"])
+             ["wait_bits", "overlap", "barrier", "select+pack", "learn", "", "select_only", "pack_only",
+              "full_bcde"])
     ph = {k: round(float(buf[i]) / ni / 1e3, 3) for i, k in enumerate(names) if k}
+    extra = {k: ph.pop(k) for k in ("select_only", "pack_only") if k in ph}
     print(json.dumps({"case": label, "inputs": ni, "us_per_input": round(ms * 1e3 / ni, 3),
                       "path": ["per-input", "cluster", "grid"][info["last_learn_path"]],
                       "cluster": info["learn_cluster"], "grid_ctas": info["learn_grid_ctas"], "phases_us": ph,
-                      "sum_us": round(sum(ph.values()), 3)}), flush=True)
+                      "sum_us": round(sum(ph.values()), 3), "sub_phases_us": extra}), flush=True)
     sp.close()
 
 
+FULL = P.SP_FLAG_FULL_LEARNING
+
+
 if __name__ == "__main__":
+    if "full" in sys.argv[1:]:
+        run("whole C1024 S256 global full", 200, num_columns=1024, synapses_per_column=256, flags=FULL)
+        run("whole C1024 S256 r80 full", 200, num_columns=1024, synapses_per_column=256,
+            inhibition_radius=80, flags=FULL)
+        run("whole C1024 S256 r80 (a5 only, seeded boosts)", 200, True, num_columns=1024,
+            synapses_per_column=256, inhibition_radius=505)
+        sys.exit(0)
     run("whole C1024 S256 global uniform", 200, num_columns=1024, synapses_per_column=256)
     run("whole C1024 S256 global seeded", 200, True, num_columns=1024, synapses_per_column=256)
     run("whole C1024 S256 r80 uniform", 200, num_columns=1024, synapses_per_column=256,

@@ -59,6 +59,14 @@ def check_inputs(results, sdr, counts, raw, boosted):
         assert counts[r] == res.active.sum()
 
 
+def check_path(sp, path):
+    info = sp.info()
+    if path == "input" or not info["learn_cluster"]:
+        assert info["last_learn_path"] == P.SP_LEARN_PER_INPUT, info
+    else:
+        assert info["last_learn_path"] == P.SP_LEARN_CLUSTER, info
+
+
 def check_state(sp, ora):
     _, perm, boost = sp.get_state()
     adc, odc, radius, it = sp.get_learning_state()
@@ -100,6 +108,7 @@ def test_full_learning_parity(kw, path):
     sp = make_sp(cfg, state, path)
     sp.set_learning_state(adc, odc, cfg.inhibition_radius)
     check_inputs(results, *run(sp, frames, True))
+    check_path(sp, path)
     check_state(sp, ora)
     # inference with the learned boosts and the adapted radius (batched path where eligible)
     frames2 = sp_inputs.frames(2002, 0, 37, cfg.input_height, cfg.input_width, rho=0.5)
@@ -119,6 +128,7 @@ def test_full_learning_from_creation_with_bumps(path):
     results = ora.compute(frames, learning=True)
     sp = make_sp(cfg, None, path)
     check_inputs(results, *run(sp, frames, True))
+    check_path(sp, path)
     check_state(sp, ora)
     assert not np.all(ora.perm == np.float32(0.21))
 
