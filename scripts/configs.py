@@ -104,9 +104,50 @@ def config5():
     sp.close()
 
 
+def full():
+    """Full learning (NEXT-1; S:119(b-e)): config 2 (k 40; global and Tab. 2's radius 80, adapted)
+    over 1000 frames, then inference with the learned boosts/radius; config 5 over 24 frames."""
+    learn_f = frames_of(1000, 1001)
+    infer_f = frames_of(4096, 2002)
+    for radius in (0, 80):
+        sp = P.SpatialPooler(input_width=960, input_height=540, num_columns=1024, synapses_per_column=256,
+                             min_overlap=4, winners_set_size=40, inhibition_radius=radius, max_inputs=4096,
+                             flags=P.SP_FLAG_FULL_LEARNING, duty_cycle_period=1000, max_boost=2.0)
+        sp.compute(learn_f[:8], learn=True)
+        lms = timed(lambda: sp.compute(learn_f[8:], learn=True))
+        info = sp.info()
+        adc, odc, r, it = sp.get_learning_state()
+        boost = sp.get_state()[2]
+        sp.compute(infer_f)
+        ims = timed(lambda: sp.compute(infer_f), reps=10)
+        _, counts = sp.winners()
+        print(json.dumps({"config": "BASELINE config 2, full learning", "k": 40, "radius0": radius,
+                          "radius_after": r, "learn_frames": 992,
+                          "learn_us_per_frame": round(lms * 1e3 / 992, 2), "learn_path": P.learn_path_name(info),
+                          "boosted_columns": int((boost > 1).sum()), "max_boost_seen": float(boost.max()),
+                          "infer_frames": 4096, "infer_ms": round(ims, 4),
+                          "infer_frames_per_s": round(4096 / ims * 1e3),
+                          "infer_hbm_frac": round(4096 * 518528 / (ims / 1e3) / 1e9 / HBM, 4),
+                          "mean_winners": float(counts.float().mean())}), flush=True)
+        sp.close()
+    sp = P.SpatialPooler(input_width=960, input_height=540, num_columns=16384, synapses_per_column=512,
+                         min_overlap=8, winners_set_size=40, inhibition_radius=80, max_inputs=64,
+                         flags=P.SP_FLAG_FULL_LEARNING, duty_cycle_period=1000, max_boost=2.0)
+    sp.compute(learn_f[:4], learn=True)
+    lms = timed(lambda: sp.compute(learn_f[4:28], learn=True))
+    info = sp.info()
+    r = sp.get_learning_state()[2]
+    print(json.dumps({"config": "BASELINE config 5, full learning", "radius0": 80, "radius_after": r,
+                      "learn_frames": 24, "learn_us_per_frame": round(lms * 1e3 / 24, 1),
+                      "learn_path": P.learn_path_name(info)}), flush=True)
+    sp.close()
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "all"
     if which in ("2", "all"):
         config2()
     if which in ("5", "all"):
         config5()
+    if which in ("full", "all"):
+        full()
