@@ -35,6 +35,8 @@ What it computes is the plain definition, step by step, in the paper's order
          of the connected synapses' input indices (0 if none), evaluated exactly
    W(c) is the window of the radius in force for this input (global when 0).
 6. output   : the active set / SDR bitmask (bit c of word c // 32, LSB first).
+7. histogram: per video v (SP inputs [off[v], off[v+1])), counts[v, c] = #inputs where c is
+              active, hist = fp32(count) / fp32(n) (NEXT-4, DESIGN R22)
 
 Initialisation ("random initialization", P:245 init perm; C8 as amended
 in DESIGN.md R8): per column c a splitmix64 stream whose state starts at
@@ -329,6 +331,31 @@ def sdr_words(active: np.ndarray) -> np.ndarray:
     for c in np.nonzero(active)[0]:
         words[c // 32] |= np.uint32(1) << np.uint32(c % 32)
     return words
+
+
+# --------------------------------------------------------------------------- #
+# step 7: per-video SDR histograms (NEXT-4, DESIGN R22)
+# --------------------------------------------------------------------------- #
+def sdr_histograms(active: np.ndarray, offsets):
+    """``active bool[n, C]`` (the winners of n consecutive SP inputs), ``offsets`` of V+1
+    ascending input indices -> ``(counts int64[V, C], hist float32[V, C])``.
+
+    "Histograms of consecutive frames are built from SP output on a per-video basis"
+    (P:118); counts[c] = (#frames where c active) / frames.  Normalisation is one
+    fp32 IEEE division fp32(count) / fp32(n); a video with no inputs gives zeros (R22).
+    """
+    active = np.asarray(active, dtype=bool)
+    V = len(offsets) - 1
+    C = active.shape[1]
+    counts = np.zeros((V, C), dtype=np.int64)
+    hist = np.zeros((V, C), dtype=np.float32)
+    for v in range(V):
+        lo, hi = int(offsets[v]), int(offsets[v + 1])
+        for i in range(lo, hi):
+            counts[v] += active[i]
+        if hi > lo:
+            hist[v] = (counts[v].astype(np.float32) / np.float32(hi - lo)).astype(np.float32)
+    return counts, hist
 
 
 # --------------------------------------------------------------------------- #

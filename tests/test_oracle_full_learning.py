@@ -263,3 +263,39 @@ def test_full_learning_deterministic():
     b, tb = _run(cfg, frames)
     assert all(np.array_equal(x.active, y.active) for x, y in zip(ta, tb))
     assert np.array_equal(a.perm, b.perm) and np.array_equal(a.boost, b.boost)
+
+
+# --------------------------------------------------------------------------- #
+# per-video SDR histograms (NEXT-4; R22)
+# --------------------------------------------------------------------------- #
+def test_histogram_spec_examples():
+    C = 64
+    act = np.zeros((32, C), bool)
+    act[:, 3] = True            # active in all 32 frames -> 1.0
+    act[::4, 10] = True         # active in 8 of 32 frames -> 0.25
+    counts, hist = O.sdr_histograms(act, [0, 32])
+    assert hist[0, 3] == 1.0 and hist[0, 10] == 0.25 and counts[0, 10] == 8
+    assert np.all(np.delete(hist[0], [3, 10]) == 0.0)
+    # empty active sets throughout -> zero vector; an empty video -> zeros (R22)
+    counts, hist = O.sdr_histograms(np.zeros((5, C), bool), [0, 5, 5])
+    assert np.all(hist == 0) and np.all(counts == 0)
+
+
+def test_histogram_brute_force_exact_rounding():
+    rng = np.random.default_rng(9)
+    act = rng.random((200, 96)) < 0.3
+    offs = [0, 7, 7, 64, 137, 200]
+    counts, hist = O.sdr_histograms(act, offs)
+    for v in range(len(offs) - 1):
+        seg = act[offs[v]:offs[v + 1]]
+        assert np.array_equal(counts[v], seg.sum(axis=0))  # the plain count
+        n = len(seg)
+        for c in range(96):
+            if n == 0:
+                assert hist[v, c] == 0
+                continue
+            exact = Fraction(int(counts[v, c]), n)
+            got = Fraction(float(hist[v, c]))
+            # correctly rounded: within half an fp32 ulp of the exact ratio
+            ulp = Fraction(2) ** (math.frexp(float(hist[v, c]) or 1.0)[1] - 24)
+            assert abs(got - exact) <= ulp / 2
