@@ -313,6 +313,26 @@ def main():
     value = total_frames / (ms / 1e3)
     plan = sp.info()["plan"]
 
+    # ---- NEXT-4: per-video SDR histograms of the last step (videos of 32 frames) ------------
+    import numpy as np
+    offs = np.arange(0, F + 1, 32, dtype=np.uint32)
+    hc = torch.empty((len(offs) - 1, C), dtype=torch.int32, device=dev)
+    hh = torch.empty((len(offs) - 1, C), dtype=torch.float32, device=dev)
+    for _ in range(3):
+        sp.histograms(offs, hc, hh)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    sp.compute(frames, learn=False)  # keeps the device busy while the host enqueues the calls
+    a.record(stream)
+    for _ in range(10):
+        sp.histograms(offs, hc, hh)
+    b.record(stream)
+    torch.cuda.synchronize()
+    hist_ms = a.elapsed_time(b) / 10
+    histograms = {"videos": len(offs) - 1, "frames_per_video": 32, "us": hist_ms * 1e3,
+                  "share_of_step": hist_ms / (ms / args.steps),
+                  "note": "sp_histograms (NEXT-4) over the step's SDRs, device time per call (host enqueue hidden)"}
+
     # ---- e2e: the public host-buffer call (H2D of frames + D2H of SDRs inside) -----------
     e2e = None
     if not args.no_e2e:
@@ -375,7 +395,7 @@ def main():
                                                      "num_windows", "stages", "smem_bytes")}},
             "hbm_frac": round(value / world * ALGO_BYTES_PER_FRAME / 1e9 / peak, 4),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(), "learn": learn}
+            "clocks": clk.summary(), "learn": learn, "histograms": histograms}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

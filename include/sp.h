@@ -206,6 +206,20 @@ sp_status sp_get_state(sp_handle* h, uint32_t* idx, float* perm, float* boost);
  * [1,16) (the exact-key domain, R4).  NULL keeps the current array. */
 sp_status sp_set_state(sp_handle* h, const uint32_t* idx, const float* perm, const float* boost);
 
+/* Per-video SDR histograms of the last sp_compute call (P:118-120
+ * "histograms of consecutive frames are built from SP output on a per-video basis";
+ * S:422-430; DESIGN R22).  Video v is the range [offsets[v], offsets[v+1]) of SP inputs of that
+ * call (frames x patches, in order):
+ *   video_offsets_host: uint32[num_videos + 1], host memory, non-decreasing, last <= the
+ *                       number of inputs of the last call (SP_E_ARG otherwise);
+ *   counts_dev: uint32[num_videos][C] number of inputs with column c active (or NULL);
+ *   hist_dev:   float[num_videos][C] = fp32(count) / fp32(inputs of the video), one IEEE RN
+ *               division; 0 for an empty video (or NULL).
+ * Stream-ordered like sp_winners (the offsets are copied before the call returns).
+ * Errors: SP_E_ARG, SP_E_STATE (no compute yet), SP_E_OOM, SP_E_CUDA. */
+sp_status sp_histograms(sp_handle* h, const uint32_t* video_offsets_host, uint32_t num_videos,
+                        uint32_t* counts_dev, float* hist_dev, void* cuda_stream);
+
 /* Full-learning state (S:88, S:119(b-e)); host pointers, synchronous.
  *   active_duty, overlap_duty: float[C] duty cycles (or NULL);
  *   radius: the inhibition radius in force (0 = global) (or NULL);

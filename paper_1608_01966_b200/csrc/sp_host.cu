@@ -347,6 +347,11 @@ struct sp_handle {
     float* d_fscratch = nullptr;   // window-maximum tables of k_full
     bool span_dirty = true;      // d_span must be recomputed before full learning
     uint64_t iteration = 0;      // SP inputs learned
+    // per-video histograms (NEXT-4): offsets and count scratch, grown on demand
+    uint32_t* d_hist_off = nullptr;
+    uint32_t* d_hist_counts = nullptr;
+    size_t hist_off_cap = 0, hist_counts_cap = 0;
+    std::vector<uint32_t> h_hist_off;  // offsets last uploaded (skip the upload when unchanged)
     bool syn_dirty = false;      // d_syn must be rebuilt from idx/perm before the per-input path
     uint32_t last_learn_path = SP_LEARN_PER_INPUT;
     // scratch and results
@@ -385,7 +390,7 @@ void release(sp_handle* h) {
                     h->d_ell,  h->d_ell_off, h->d_ell_nb,  h->d_ell_pos, h->d_bits,
                     h->d_raw,  h->d_sdr,     h->d_counts,  h->d_raw_rec, h->d_boosted_rec,
                     h->d_stage[0], h->d_stage[1], h->d_synT,  h->d_gbar, h->d_adc, h->d_odc,
-                    h->d_span, h->d_radius, h->d_fscratch};
+                    h->d_span, h->d_radius, h->d_fscratch, h->d_hist_off, h->d_hist_counts};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
@@ -1107,6 +1112,58 @@ sp_status sp_set_state(sp_handle* h, const uint32_t* idx, const float* perm, con
     cudaDeviceSynchronize();
     return upload_state(h, idx ? idx : cur_idx.data(), perm ? perm : cur_perm.data(),
                         boost ? boost : cur_boost.data());
+}
+
+sp_status sp_histograms(sp_handle* h, const uint32_t* video_offsets_host, uint32_t num_videos,
+                        uint32_t* counts_dev, float* hist_dev, void* cuda_stream) {
+    sp_status st = check_handle(h);
+    if (st != SP_OK) return st;
+    if (!h->has_result) return fail(SP_E_STATE, "sp_histograms before any sp_compute");
+    if (num_videos == 0 || (!counts_dev && !hist_dev)) return SP_OK;
+    if (!video_offsets_host) return fail(SP_E_ARG, "video_offsets_host is NULL");
+    uint32_t longest = 0;
+    for (uint32_t v = 0; v < num_videos; ++v) {
+        if (video_offsets_host[v + 1] < video_offsets_host[v])
+            return fail(SP_E_ARG, "video offsets must be non-decreasing (offsets[%u] > offsets[%u])", v, v + 1);
+        longest = std::max(longest, video_offsets_host[v + 1] - video_offsets_host[v]);
+    }
+    if (video_offsets_host[num_videos] > h->last_inputs)
+        return fail(SP_E_ARG, "offsets[%u] = %u exceeds the %u inputs of the last call", num_videos,
+                    video_offsets_host[num_videos], h->last_inputs);
+    const size_t nc = static_cast<size_t>(num_videos) * h->g.C;
+    cudaError_t e = cudaSuccess;
+    if (h->hist_off_cap < num_videos + 1u) {
+        h->h_hist_off.clear();
+        if (h->d_hist_off) cudaFree(h->d_hist_off), h->d_hist_off = nullptr;
+        e = dalloc(&h->d_hist_off, num_videos + 1u);
+        if (e != cudaSuccess) return fail(SP_E_OOM, "histogram offsets: %s", cudaGetErrorString(e));
+        h->hist_off_cap = num_videos + 1u;
+    }
+    uint32_t* counts = counts_dev;
+    if (!counts) {
+        if (h->hist_counts_cap < nc) {
+            if (h->d_hist_counts) cudaFree(h->d_hist_counts), h->d_hist_counts = nullptr;
+            e = dalloc(&h->d_hist_counts, nc);
+            if (e != cudaSuccess) return fail(SP_E_OOM, "histogram counts: %s", cudaGetErrorString(e));
+            h->hist_counts_cap = nc;
+        }
+        counts = h->d_hist_counts;
+    }
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    // the offsets usually repeat from call to call: upload (a staged, host-synchronous copy
+    // from pageable memory) only when they change
+    if (h->h_hist_off.size() != num_videos + 1u ||
+        std::memcmp(h->h_hist_off.data(), video_offsets_host, (num_videos + 1u) * 4u) != 0) {
+        e = cudaMemcpyAsync(h->d_hist_off, video_offsets_host, (num_videos + 1u) * 4u, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(e, "histogram offsets upload");
+        h->h_hist_off.assign(video_offsets_host, video_offsets_host + num_videos + 1u);
+    }
+    uint32_t nl = 0;
+    e = sp::launch_histograms(h->d_sdr, h->g.ncw, h->g.C, h->d_hist_off, num_videos, longest, h->sm_count, counts,
+                              hist_dev, s, &nl);
+    h->launches += nl;
+    if (e != cudaSuccess) return cuda_fail(e, "histogram launch");
+    return SP_OK;
 }
 
 sp_status sp_get_learning_state(sp_handle* h, float* active_duty, float* overlap_duty, uint32_t* radius,

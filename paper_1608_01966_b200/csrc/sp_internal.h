@@ -214,6 +214,10 @@ cudaError_t launch_full(const PerInputParams& p, uint32_t input, cudaStream_t s)
 cudaError_t launch_span(const uint32_t* idx, const float* perm, float tau, uint32_t C, uint32_t S,
                         uint32_t* span, cudaStream_t s);
 size_t full_scratch_floats(uint32_t C32);
+// per-video SDR histograms (sp_hist.cu); returns the number of kernels launched in *launches
+cudaError_t launch_histograms(const uint32_t* sdr, uint32_t ncw, uint32_t C, const uint32_t* off_dev,
+                              uint32_t V, uint32_t max_video_inputs, int sm_count, uint32_t* counts,
+                              float* hist, cudaStream_t s, uint32_t* launches);
 cudaError_t launch_build_syn(const uint32_t* idx, const float* perm, float tau, uint32_t C,
                              uint32_t C32, uint32_t S, uint32_t* syn, cudaStream_t s);
 cudaError_t launch_refresh_ell(const uint32_t* idx, const float* perm, const uint32_t* pos,

@@ -60,3 +60,11 @@ def gather_sdrs(local_sdr, out=None):
                           device=local_sdr.device)
     dist.all_gather_into_tensor(out, local_sdr.contiguous())
     return out
+
+
+def gather_histograms(local_hist, out=None):
+    """All-gathers per-video SDR histograms (NEXT-4) of every rank: [V_local, C] -> [V_local*world, C].
+
+    Videos are sharded whole (each rank holds complete videos, equal counts per rank), so the
+    per-video features replace the per-frame SDR gather on the way to the classifier rank."""
+    return gather_sdrs(local_hist, out)

@@ -38,7 +38,8 @@ STATUS_NAMES = {0: "SP_OK", 1: "SP_E_CONFIG", 2: "SP_E_ARG", 3: "SP_E_SHAPE", 4:
 ABI_SYMBOLS = ("sp_config_default", "sp_create", "sp_destroy", "sp_compute", "sp_winners",
                "sp_overlaps", "sp_get_state", "sp_set_state", "sp_compute_host", "sp_plan",
                "sp_init_pools_host", "sp_get_info", "sp_last_error", "sp_version",
-               "sp_get_learning_state", "sp_set_learning_state", "sp_synth_frames")
+               "sp_get_learning_state", "sp_set_learning_state", "sp_histograms",
+               "sp_synth_frames")
 
 
 class SpError(RuntimeError):
@@ -111,6 +112,7 @@ def lib() -> ctypes.CDLL:
         "sp_get_info": [vp, P(SpInfo)],
         "sp_get_learning_state": [vp, vp, vp, vp, vp],
         "sp_set_learning_state": [vp, vp, vp, u32],
+        "sp_histograms": [vp, vp, u32, vp, vp, vp],
         "sp_synth_frames": [vp, u64, u32, u32, u32, u64, u32, u32, vp],
     }
     for name, args in sig.items():
@@ -263,6 +265,24 @@ class SpatialPooler:
         _check(lib().sp_overlaps(self._h, ctypes.c_void_p(raw.data_ptr()),
                                  ctypes.c_void_p(boosted.data_ptr()), _stream_ptr(stream, dev)))
         return raw, boosted
+
+    def histograms(self, video_offsets, counts=None, hist=None, stream=None):
+        """Per-video SDR histograms of the last call (NEXT-4): video v = SP inputs
+        [offsets[v], offsets[v+1]).  Returns (counts int32-view uint32 [V, C], hist f32 [V, C])."""
+        import torch
+        off = np.ascontiguousarray(video_offsets, dtype=np.uint32)
+        V = len(off) - 1
+        dev = torch.device("cuda", self.device)
+        if counts is None:
+            counts = torch.empty((V, self.C), dtype=torch.int32, device=dev)
+        if hist is None:
+            hist = torch.empty((V, self.C), dtype=torch.float32, device=dev)
+        _require(counts, torch.int32, self.device, (V, self.C), "counts")
+        _require(hist, torch.float32, self.device, (V, self.C), "hist")
+        _check(lib().sp_histograms(self._h, ctypes.c_void_p(off.ctypes.data), V,
+                                   ctypes.c_void_p(counts.data_ptr()), ctypes.c_void_p(hist.data_ptr()),
+                                   _stream_ptr(stream, dev)))
+        return counts, hist
 
     def compute_host(self, frames: np.ndarray, learn: bool = False, stream=None):
         """End-to-end call with host buffers (H2D/D2H inside): returns (sdr uint32, counts uint32)."""

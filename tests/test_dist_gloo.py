@@ -43,7 +43,11 @@ def _worker(rank, world, port, total, q):
         frames = sp_inputs.frames(2002, b, e - b, 8, 8)
         local = np.stack([O.sdr_words(r.active).view(np.int32) for r in ora.compute(frames, False)])
         out = D.gather_sdrs(torch.from_numpy(local))
-        q.put((rank, out.numpy(), idx, perm))
+        # per-video histograms of this rank's whole videos (3 frames each), gathered (NEXT-4)
+        act = np.stack([r.active for r in ora.compute(frames, False)])
+        _, hist = O.sdr_histograms(act, np.arange(0, e - b + 1, 3))
+        hist_all = D.gather_histograms(torch.from_numpy(hist))
+        q.put((rank, out.numpy(), idx, perm, hist_all.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -70,8 +74,11 @@ def test_sharded_inference_gathers_identical_sdrs(world):
     ora.compute(sp_inputs.frames(1001, 0, 10, 8, 8), learning=True)
     want = np.stack([O.sdr_words(r.active).view(np.int32)
                      for r in ora.compute(sp_inputs.frames(2002, 0, total, 8, 8), False)])
-    for rank, gathered, idx, perm in res:
+    act = np.stack([r.active for r in ora.compute(sp_inputs.frames(2002, 0, total, 8, 8), False)])
+    _, want_hist = O.sdr_histograms(act, np.arange(0, total + 1, 3))
+    for rank, gathered, idx, perm, hist_all in res:
         assert np.array_equal(gathered, want), f"rank {rank}"
+        assert np.array_equal(hist_all, want_hist), f"rank {rank} histograms"
         assert np.array_equal(idx.astype(np.int64), ora.idx) and np.array_equal(perm, ora.perm)
 
 
