@@ -28,6 +28,15 @@ sp_status sp_synth_frames(uint8_t* frames_dev, uint64_t first_frame, uint32_t nu
                           uint32_t height, uint32_t width, uint64_t seed, uint32_t rho_q24,
                           uint32_t nonzero_mode, void* cuda_stream);
 
+/* Colour frames for the encoder, uint8[num_frames][height][width][3]
+ * BGR, same recipe as sp_inputs.bgr_frames (integer-only):
+ *   base  = ((x*(c+1)) >> 2) + (y >> 1) + 5f + (128 inside the disc (x-cx)^2+(y-cy)^2 < r^2,
+ *           cx = (17f+200) % W, cy = (11f+150) % H, r = min(H,W)/7)
+ *   value = (base + (splitmix64(h_f ^ ((y*W+x)*3 + c)) >> 59)) & 255
+ * Errors: SP_E_ARG, SP_E_CUDA.  Asynchronous. */
+sp_status sp_synth_bgr_frames(uint8_t* frames_dev, uint64_t first_frame, uint32_t num_frames,
+                              uint32_t height, uint32_t width, uint64_t seed, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

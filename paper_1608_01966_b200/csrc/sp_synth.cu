@@ -41,7 +41,36 @@ __global__ void k_synth(uint8_t* out, uint64_t first, uint32_t npix, uint64_t se
     }
 }
 
+// Colour frames for the encoder (recipe in include/sp_synth.h), one thread per pixel.
+__global__ void k_synth_bgr(uint8_t* out, uint64_t first, uint32_t H, uint32_t W, uint64_t seed) {
+    const uint32_t f = blockIdx.y;
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;  // pixel
+    if (i >= H * W) return;
+    const int64_t fi = static_cast<int64_t>(first + f);
+    const int64_t y = i / W, x = i % W;
+    const uint64_t hf = splitmix64(seed ^ ((first + f) * 0xD1B54A32D192ED03ull));
+    const int64_t cx = (17 * fi + 200) % W, cy = (11 * fi + 150) % H, r = min(H, W) / 7;
+    const bool disc = (x - cx) * (x - cx) + (y - cy) * (y - cy) < r * r;
+    uint8_t* px = out + (static_cast<size_t>(f) * H * W + i) * 3u;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const int64_t base = ((x * (c + 1)) >> 2) + (y >> 1) + 5 * fi + (disc ? 128 : 0);
+        const uint64_t noise = splitmix64(hf ^ (static_cast<uint64_t>(i) * 3u + c)) >> 59;
+        px[c] = static_cast<uint8_t>((base + static_cast<int64_t>(noise)) & 255);
+    }
+}
+
 }  // namespace
+
+extern "C" sp_status sp_synth_bgr_frames(uint8_t* frames_dev, uint64_t first_frame, uint32_t num_frames,
+                                         uint32_t height, uint32_t width, uint64_t seed, void* cuda_stream) {
+    if (num_frames == 0) return SP_OK;
+    if (!frames_dev || height == 0 || width == 0) return SP_E_ARG;
+    dim3 grid((height * width + 255u) / 256u, num_frames);
+    k_synth_bgr<<<grid, 256, 0, static_cast<cudaStream_t>(cuda_stream)>>>(frames_dev, first_frame, height, width,
+                                                                           seed);
+    return cudaGetLastError() == cudaSuccess ? SP_OK : SP_E_CUDA;
+}
 
 extern "C" sp_status sp_synth_frames(uint8_t* frames_dev, uint64_t first_frame, uint32_t num_frames,
                                      uint32_t height, uint32_t width, uint64_t seed, uint32_t rho_q24,

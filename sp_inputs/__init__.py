@@ -36,6 +36,7 @@ __all__ = [
     "frames",
     "boosts",
     "rho_threshold",
+    "bgr_frames",
 ]
 
 GOLDEN_GAMMA = np.uint64(0x9E3779B97F4A7C15)
@@ -97,3 +98,33 @@ def boosts(seed: int, num_columns: int, lo: float = 1.0, hi: float = 2.0) -> np.
         h = splitmix64(np.uint64(seed) * FRAME_MULT + np.arange(num_columns, dtype=np.uint64))
     u = (h >> np.uint64(40)).astype(np.float64) / float(1 << 24)  # [0, 1)
     return np.float32(lo) + (np.float32(hi - lo) * u.astype(np.float32))
+
+
+def bgr_frames(seed: int, first: int, count: int, height: int, width: int) -> np.ndarray:
+    """Seeded synthetic colour frames for the encoder (NEXT-3), ``uint8[count, H, W, 3]`` BGR.
+
+    Integer-only recipe: a gradient, a bright disc moving with
+    the frame index (the paper's rendered moving shapes), and 5 bits of hash noise:
+
+        base  = ((x * (c + 1)) >> 2) + (y >> 1) + 5 f
+              + 128 if (x - cx)^2 + (y - cy)^2 < r^2,  cx = (17 f + 200) % W,
+                cy = (11 f + 150) % H, r = min(H, W) // 7
+        value = (base + (splitmix64(h_f ^ ((y W + x) 3 + c)) >> 59)) & 255
+    """
+    f = np.arange(first, first + count, dtype=np.int64)[:, None, None, None]
+    y = np.arange(height, dtype=np.int64)[None, :, None, None]
+    x = np.arange(width, dtype=np.int64)[None, None, :, None]
+    c = np.arange(3, dtype=np.int64)[None, None, None, :]
+    cx, cy, r = (17 * f + 200) % width, (11 * f + 150) % height, min(height, width) // 7
+    base = ((x * (c + 1)) >> 2) + (y >> 1) + 5 * f
+    base = base + np.where((x - cx) ** 2 + (y - cy) ** 2 < r * r, 128, 0)
+    out = np.empty((count, height, width, 3), dtype=np.uint8)
+    i = ((np.arange(height, dtype=np.uint64)[:, None, None] * np.uint64(width)
+          + np.arange(width, dtype=np.uint64)[None, :, None]) * np.uint64(3)
+         + np.arange(3, dtype=np.uint64)[None, None, :])
+    with np.errstate(over="ignore"):
+        for j in range(count):
+            hf = splitmix64(np.uint64(seed) ^ (np.uint64(first + j) * FRAME_MULT))
+            noise = (splitmix64(hf ^ i) >> np.uint64(59)).astype(np.int64)
+            out[j] = ((base[j] + noise) & 255).astype(np.uint8)
+    return out
