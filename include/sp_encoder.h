@@ -1,0 +1,78 @@
+/*
+ * sp_encoder.h — C ABI of the on-device adaptive video encoder, the
+ * step before the SP hot path: "an original video frame is converted to a binary image ...
+ * first reduced in size ... converted to a grayscale one, which is later binarized using
+ * adaptive thresholding ... 'ADAPTIVE_THRESH_GAUSSIAN_C' algorithm from OpenCV" (PAPER.md
+ * P:164-168).  Its output frames are sp_compute's input.
+ *
+ * Per frame (DESIGN R23-R25):
+ *   R23 downscale src -> dst by OpenCV INTER_AREA (fp32 area weights, OpenCV's order of
+ *       operations, round half to even), channels independent;
+ *   R24 gray: Y = (3735 B + 19235 G + 9798 R + 2^14) >> 15 (OpenCV 8-bit BGR2GRAY);
+ *   R25 mean = OpenCV's bit-exact 8-bit Gaussian blur of the block_size window (replicated
+ *       borders); output byte = 255 if Y - mean > -ceil(bias) else 0.
+ * Conventions as in sp.h: sp_status results, device pointers owned by the caller,
+ * stream-ordered asynchronous calls, no CPU fallback.
+ */
+#ifndef HTM_SP_ENCODER_H
+#define HTM_SP_ENCODER_H
+
+#include <stdint.h>
+#include "sp.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sp_encoder_config {
+    uint32_t src_width, src_height;  /* input BGR frame W0 x H0 (960 x 540) */
+    uint32_t dst_width, dst_height;  /* output W1 x H1 <= input (240 x 134) */
+    uint32_t block_size;             /* Gaussian window, odd in [3, 15] (11) */
+    float bias;                      /* C of T = mean - C, |C| <= 255 (2.0) */
+    int32_t device;
+} sp_encoder_config;
+
+typedef struct sp_encoder sp_encoder;
+
+typedef struct sp_encoder_info {
+    uint32_t band_rows;      /* output rows per streamed band */
+    uint32_t bands;          /* bands per frame */
+    uint32_t stages;         /* shared-memory ring depth (bulk copies in flight per CTA) */
+    uint32_t stage_bytes;
+    uint32_t smem_bytes;     /* dynamic shared memory per CTA */
+    uint32_t ctas_per_sm;
+    uint32_t xfast;          /* 1 if the x table is an exact 4:1 average (vectorised path) */
+    uint64_t kernel_launches;
+    int32_t kernel_q8[16];   /* the 8-bit Gaussian kernel (sum 256) */
+} sp_encoder_info;
+
+/* Defaults: 960x540 -> 240x134, block 11, bias 2, device 0.  SP_E_ARG for NULL. */
+sp_status sp_encoder_config_default(sp_encoder_config* cfg);
+
+/* Validates *cfg (SP_E_CONFIG: zero or upscaling dims, even / out-of-range block_size,
+ * bias), builds the area tables and the Gaussian kernel, uploads them to cfg->device.
+ * Errors: SP_E_ARG, SP_E_CONFIG, SP_E_CUDA. */
+sp_status sp_encoder_create(const sp_encoder_config* cfg, sp_encoder** out);
+
+/* Frees the encoder (NULL is a no-op). */
+sp_status sp_encoder_destroy(sp_encoder* enc);
+
+/* Encodes num_frames frames:
+ *   bgr_dev: uint8[num_frames][src_height][src_width][3] (B, G, R), device memory;
+ *   out_dev: uint8[num_frames][dst_height][dst_width] = 255 / 0, device memory.
+ * Rows are streamed with bulk copies when bgr_dev is 16-byte aligned and 3*src_width is a
+ * multiple of 16, else with plain loads.  Asynchronous on cuda_stream.
+ * Errors: SP_E_ARG (NULL), SP_E_CUDA.  num_frames == 0 is a no-op. */
+sp_status sp_encode(sp_encoder* enc, const uint8_t* bgr_dev, uint32_t num_frames, uint8_t* out_dev,
+                    void* cuda_stream);
+
+/* Launch plan and kernel of the encoder.  Errors: SP_E_ARG. */
+sp_status sp_encoder_get_info(sp_encoder* enc, sp_encoder_info* out);
+
+/* Thread-local message of the last failing encoder call. */
+const char* sp_encoder_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HTM_SP_ENCODER_H */

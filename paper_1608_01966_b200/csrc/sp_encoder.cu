@@ -1,0 +1,495 @@
+// sp_encoder.cu — the adaptive video encoder on the device (PAPER.md
+// "reduced in size ... converted to a grayscale one, which is later binarized using
+// adaptive thresholding ... ADAPTIVE_THRESH_GAUSSIAN_C"; DESIGN R23-R25 and
+// §4.9).  BGR uint8 frames -> binarised uint8 frames (255 / 0) that feed sp_compute.
+//
+// One persistent CTA loop over frames (2 CTAs per SM).  Per frame the source rows are streamed
+// band by band (a band = the source rows of `band_rows` output rows: contiguous bytes, one
+// cp.async.bulk per band into a ring of shared-memory stages, mbarrier completion), the band
+// is area-downscaled (R23: OpenCV INTER_AREA, its fp32 operation order) and converted to gray
+// (R24) into a resident gray image; then the Gaussian mean (R25: 8-bit bit-exact blur, exact
+// integers, so the separable passes may run in any order) and the threshold are computed by a
+// register sliding window down each column, while the ring already streams the next frame.
+// The path is HBM-bound: 3*W0*H0 bytes read, W1*H1 written per frame.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "sp_internal.h"
+#include "../../include/sp_encoder.h"
+
+namespace sp {
+
+namespace {
+
+constexpr uint32_t kEncThreads = 512;
+constexpr uint32_t kMaxStages = 4;
+
+struct EncParams {
+    const uint8_t* src;        // [F][H0][W0][3] BGR
+    uint8_t* dst;              // [F][H1][W1]
+    uint32_t F;
+    uint32_t W0, H0, W1, H1;
+    uint32_t row_bytes;        // 3 * W0
+    uint32_t bands, band_rows; // output rows per band
+    uint32_t stage_bytes, stages;
+    uint32_t bulk;             // rows are 16-byte aligned: bulk copies, else cooperative loads
+    uint32_t xfast;            // x table = {4dx + j, 0.25}, j < 4 (an exact 4:1 x scale)
+    const uint32_t* band_sy0;  // [bands] first source row of the band
+    const uint32_t* band_n;    // [bands] source rows of the band
+    const uint32_t* yoff;      // [H1 + 1] y-table range of each output row
+    const uint32_t* ysy;       // [.] source row of the entry
+    const float* ybeta;        // [.] weight
+    const uint32_t* xoff;      // [W1 + 1]
+    const uint32_t* xsx;       // [.] source column of the entry
+    const float* xalpha;       // [.]
+    int32_t K, cbias;          // Gaussian window, ceil(bias)
+    int32_t q[16];             // 8-bit quantised Gaussian kernel (sum 256)
+};
+
+__device__ __forceinline__ void mbar_init_e(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_e(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+
+// one thread: the source rows of band `b` of frame `f` into stage buffer `buf` (bulk copy)
+__device__ __forceinline__ void issue_band(const EncParams& p, uint32_t f, uint32_t b, uint8_t* buf, uint64_t* bar) {
+    const uint32_t bytes = p.band_n[b] * p.row_bytes;
+    const uint8_t* g = p.src + (static_cast<size_t>(f) * p.H0 + p.band_sy0[b]) * p.row_bytes;
+    const uint32_t ba = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of buf before async writes
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ba), "r"(bytes) : "memory");
+    constexpr uint32_t kChunk = 32768u;
+    for (uint32_t off = 0; off < bytes; off += kChunk) {
+        const uint32_t n = min(kChunk, bytes - off);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                static_cast<uint32_t>(__cvta_generic_to_shared(buf + off))),
+            "l"(g + off), "r"(n), "r"(ba)
+            : "memory");
+    }
+}
+
+// R23 + R24 for the output rows of band b: fp32 area sums in OpenCV's order, round half to
+// even, saturate, then the 15-bit gray formula
+__device__ __forceinline__ void downscale_band(const EncParams& p, uint32_t b, const uint8_t* buf, uint8_t* gray) {
+    const uint32_t dy0 = b * p.band_rows, dy1 = min(p.H1, dy0 + p.band_rows);
+    const uint32_t npx = (dy1 - dy0) * p.W1;
+    const uint32_t sy0 = p.band_sy0[b];
+    for (uint32_t i = threadIdx.x; i < npx; i += blockDim.x) {
+        const uint32_t dy = dy0 + i / p.W1, dx = i % p.W1;
+        float sb = 0.0f, sg = 0.0f, sr = 0.0f;
+        const uint32_t j0 = p.yoff[dy], j1 = p.yoff[dy + 1];
+        for (uint32_t j = j0; j < j1; ++j) {
+            const uint8_t* row = buf + (p.ysy[j] - sy0) * p.row_bytes;
+            float bb, bg, br;
+            if (p.xfast) {
+                // 4 BGR pixels = 12 bytes at 12*dx: B0 G0 R0 B1 | G1 R1 B2 G2 | R2 B3 G3 R3.
+                // Each x partial sum is a multiple of 0.25 below 2^10: the fp32 sequence
+                // ((0 + S0/4) + S1/4) + ... is exact, so it equals (S0+S1+S2+S3) * 0.25.
+                const uint32_t* w = reinterpret_cast<const uint32_t*>(row + 12u * dx);
+                const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+                const uint32_t vb = __byte_perm(__byte_perm(w0, w1, 0x0630u), w2, 0x5210u);  // B0 B1 B2 B3
+                const uint32_t vg = __byte_perm(__byte_perm(w0, w1, 0x0741u), w2, 0x6210u);  // G0 G1 G2 G3
+                const uint32_t vr = __byte_perm(__byte_perm(w0, w1, 0x0052u), w2, 0x7410u);  // R0 R1 R2 R3
+                bb = __fmul_rn(static_cast<float>(__dp4a(vb, 0x01010101u, 0u)), 0.25f);
+                bg = __fmul_rn(static_cast<float>(__dp4a(vg, 0x01010101u, 0u)), 0.25f);
+                br = __fmul_rn(static_cast<float>(__dp4a(vr, 0x01010101u, 0u)), 0.25f);
+            } else {
+                bb = bg = br = 0.0f;
+                for (uint32_t k = p.xoff[dx]; k < p.xoff[dx + 1]; ++k) {
+                    const uint8_t* s = row + 3u * p.xsx[k];
+                    const float a = p.xalpha[k];
+                    bb = __fadd_rn(bb, __fmul_rn(static_cast<float>(s[0]), a));
+                    bg = __fadd_rn(bg, __fmul_rn(static_cast<float>(s[1]), a));
+                    br = __fadd_rn(br, __fmul_rn(static_cast<float>(s[2]), a));
+                }
+            }
+            const float beta = p.ybeta[j];
+            const float tb = __fmul_rn(beta, bb), tg = __fmul_rn(beta, bg), tr = __fmul_rn(beta, br);
+            if (j == j0) {
+                sb = tb, sg = tg, sr = tr;
+            } else {
+                sb = __fadd_rn(sb, tb), sg = __fadd_rn(sg, tg), sr = __fadd_rn(sr, tr);
+            }
+        }
+        const int B = min(255, max(0, __float2int_rn(sb)));  // saturate_cast<uchar>: half to even
+        const int G = min(255, max(0, __float2int_rn(sg)));
+        const int R = min(255, max(0, __float2int_rn(sr)));
+        gray[dy * p.W1 + dx] = static_cast<uint8_t>((3735 * B + 19235 * G + 9798 * R + 16384) >> 15);
+    }
+}
+
+// R25: Gaussian mean (exact integers) and threshold, a register window of K horizontal sums
+// down column x for rows [y0, y1)
+template <int K>
+__device__ __forceinline__ void blur_column(const EncParams& p, const uint8_t* gray, uint8_t* out, uint32_t x,
+                                            uint32_t y0, uint32_t y1) {
+    constexpr int R = K / 2;
+    const int W = static_cast<int>(p.W1), H = static_cast<int>(p.H1);
+    int cx[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) cx[j] = min(W - 1, max(0, static_cast<int>(x) + j - R));
+    auto hsum = [&](int yy) {
+        const uint8_t* row = gray + min(H - 1, max(0, yy)) * W;
+        int s = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) s += p.q[j] * row[cx[j]];
+        return s;
+    };
+    int h[K];
+#pragma unroll
+    for (int i = 0; i < K - 1; ++i) h[i] = hsum(static_cast<int>(y0) - R + i);
+    for (int y = static_cast<int>(y0); y < static_cast<int>(y1); ++y) {
+        h[K - 1] = hsum(y + R);
+        int acc = 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) acc += p.q[i] * h[i];
+        const int m = (acc + 32768) >> 16;
+        const int gv = gray[y * W + static_cast<int>(x)];
+        out[static_cast<size_t>(y) * W + x] = gv - m > -p.cbias ? 255u : 0u;
+#pragma unroll
+        for (int i = 0; i < K - 1; ++i) h[i] = h[i + 1];
+    }
+}
+
+__device__ __forceinline__ void blur_frame(const EncParams& p, const uint8_t* gray, uint8_t* out) {
+    // two row halves per column (the halo rows are recomputed)
+    const uint32_t halves = blockDim.x >= 2u * p.W1 ? 2u : 1u;
+    const uint32_t mid = p.H1 / 2u;
+    for (uint32_t t = threadIdx.x; t < halves * p.W1; t += blockDim.x) {
+        const uint32_t x = t % p.W1, half = t / p.W1;
+        const uint32_t y0 = halves == 1u ? 0u : (half ? mid : 0u);
+        const uint32_t y1 = halves == 1u ? p.H1 : (half ? p.H1 : mid);
+        switch (p.K) {
+            case 3: blur_column<3>(p, gray, out, x, y0, y1); break;
+            case 5: blur_column<5>(p, gray, out, x, y0, y1); break;
+            case 7: blur_column<7>(p, gray, out, x, y0, y1); break;
+            case 9: blur_column<9>(p, gray, out, x, y0, y1); break;
+            case 11: blur_column<11>(p, gray, out, x, y0, y1); break;
+            case 13: blur_column<13>(p, gray, out, x, y0, y1); break;
+            default: blur_column<15>(p, gray, out, x, y0, y1); break;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kEncThreads) k_encode(const __grid_constant__ EncParams p) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    __shared__ __align__(8) uint64_t bars[kMaxStages];
+    uint8_t* gray = sm;
+    uint8_t* ring = sm + ((p.W1 * p.H1 + 127u) & ~127u);
+    const uint32_t nf = p.F > blockIdx.x ? (p.F - blockIdx.x + gridDim.x - 1u) / gridDim.x : 0u;
+    const uint32_t total = nf * p.bands;  // (frame, band) sequence of this CTA
+    if (threadIdx.x == 0) {
+        for (uint32_t s = 0; s < p.stages; ++s) mbar_init_e(&bars[s]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto frame_of = [&](uint32_t seq) { return blockIdx.x + (seq / p.bands) * gridDim.x; };
+    if (p.bulk && threadIdx.x == 0)
+        for (uint32_t s = 0; s < p.stages && s < total; ++s)
+            issue_band(p, frame_of(s), s % p.bands, ring + s * p.stage_bytes, &bars[s]);
+    uint32_t seq = 0;
+    for (uint32_t i = 0; i < nf; ++i) {
+        const uint32_t f = blockIdx.x + i * gridDim.x;
+        for (uint32_t b = 0; b < p.bands; ++b, ++seq) {
+            const uint32_t st = seq % p.stages;
+            uint8_t* buf = ring + st * p.stage_bytes;
+            if (p.bulk) {
+                mbar_wait_e(&bars[st], (seq / p.stages) & 1u);
+            } else {  // unaligned rows: cooperative byte copy of the band
+                const uint8_t* g = p.src + (static_cast<size_t>(f) * p.H0 + p.band_sy0[b]) * p.row_bytes;
+                const uint32_t bytes = p.band_n[b] * p.row_bytes;
+                for (uint32_t k = threadIdx.x; k < bytes; k += blockDim.x) buf[k] = g[k];
+                __syncthreads();
+            }
+            downscale_band(p, b, buf, gray);
+            __syncthreads();  // the stage is free; the band's gray rows are complete
+            if (p.bulk && threadIdx.x == 0 && seq + p.stages < total) {
+                const uint32_t nx = seq + p.stages;
+                issue_band(p, frame_of(nx), nx % p.bands, buf, &bars[st]);
+            }
+        }
+        blur_frame(p, gray, p.dst + static_cast<size_t>(f) * p.W1 * p.H1);
+        __syncthreads();  // the gray image is rewritten by the next frame's bands
+    }
+}
+
+// OpenCV computeResizeAreaTab (R23), implemented from its definition: (dst, src, weight) per
+// axis in order, weights computed in double and stored as float
+void area_table(uint32_t ssize, uint32_t dsize, std::vector<uint32_t>& off, std::vector<uint32_t>& src,
+                std::vector<float>& w) {
+    const double scale = static_cast<double>(ssize) / dsize;
+    off.assign(dsize + 1u, 0u);
+    src.clear();
+    w.clear();
+    for (uint32_t d = 0; d < dsize; ++d) {
+        off[d] = static_cast<uint32_t>(src.size());
+        const double f1 = d * scale, f2 = f1 + scale;
+        const double cell = std::min(scale, ssize - f1);
+        int s1 = static_cast<int>(std::ceil(f1)), s2 = static_cast<int>(std::floor(f2));
+        s2 = std::min(s2, static_cast<int>(ssize) - 1);
+        s1 = std::min(s1, s2);
+        if (s1 - f1 > 1e-3) {
+            src.push_back(static_cast<uint32_t>(s1 - 1));
+            w.push_back(static_cast<float>((s1 - f1) / cell));
+        }
+        for (int s = s1; s < s2; ++s) {
+            src.push_back(static_cast<uint32_t>(s));
+            w.push_back(static_cast<float>(1.0 / cell));
+        }
+        if (f2 - s2 > 1e-3) {
+            src.push_back(static_cast<uint32_t>(s2));
+            w.push_back(static_cast<float>(std::min(std::min(f2 - s2, 1.0), cell) / cell));
+        }
+    }
+    off[dsize] = static_cast<uint32_t>(src.size());
+}
+
+}  // namespace
+
+}  // namespace sp
+
+struct sp_encoder {
+    sp_encoder_config cfg{};
+    sp::EncParams p{};
+    int device = 0, sm_count = 148;
+    uint32_t smem = 0, ctas_per_sm = 1;
+    uint32_t* d_u32 = nullptr;  // band_sy0 | band_n | yoff | ysy | xoff | xsx
+    float* d_f32 = nullptr;     // ybeta | xalpha
+    uint64_t launches = 0;
+};
+
+namespace {
+
+thread_local char g_enc_err[256];
+
+sp_status efail(sp_status st, const char* msg) {
+    std::snprintf(g_enc_err, sizeof(g_enc_err), "%s", msg);
+    return st;
+}
+
+// 8-bit Gaussian kernel (R25): OpenCV's small tables for k <= 7, else exp(-x^2/(2 sigma^2))
+// with sigma = 0.15 k + 0.35, normalised; error-diffused to 8 fractional bits, centre = rest
+void gaussian_q8(int k, int* q) {
+    static const double small3[] = {0.25, 0.5, 0.25};
+    static const double small5[] = {0.0625, 0.25, 0.375, 0.25, 0.0625};
+    static const double small7[] = {0.03125, 0.109375, 0.21875, 0.28125, 0.21875, 0.109375, 0.03125};
+    const int n2 = k / 2;
+    std::vector<double> w(n2);
+    if (k <= 7) {
+        const double* t = k == 3 ? small3 : (k == 5 ? small5 : small7);
+        for (int i = 0; i < n2; ++i) w[i] = t[i];
+    } else {
+        const double sigma = k * 0.15 + 0.35;
+        const double s2 = -0.125 / (sigma * sigma);
+        double total = 0.0;
+        for (int i = 0; i < n2; ++i) {
+            const double x = 2.0 * i - (k - 1);
+            w[i] = std::exp(x * x * s2);
+            total += w[i];
+        }
+        total = 2.0 * total + 1.0;
+        const double mul = 1.0 / total;
+        for (int i = 0; i < n2; ++i) w[i] *= mul;
+    }
+    double err = 0.0;
+    int sum = 0;
+    for (int i = 0; i < n2; ++i) {
+        const double adj = w[i] * 256.0 + err;
+        const double v0 = std::nearbyint(adj);
+        err = adj - v0;
+        q[i] = q[k - 1 - i] = static_cast<int>(v0);
+        sum += 2 * static_cast<int>(v0);
+    }
+    q[n2] = 256 - sum;
+}
+
+}  // namespace
+
+extern "C" {
+
+sp_status sp_encoder_config_default(sp_encoder_config* cfg) {
+    if (!cfg) return efail(SP_E_ARG, "config is NULL");
+    cfg->src_width = 960;   // rendered frames
+    cfg->src_height = 540;
+    cfg->dst_width = 240;   // resized to 240x134
+    cfg->dst_height = 134;
+    cfg->block_size = 11;
+    cfg->bias = 2.0f;
+    cfg->device = 0;
+    return SP_OK;
+}
+
+const char* sp_encoder_last_error(void) { return g_enc_err; }
+
+sp_status sp_encoder_create(const sp_encoder_config* cfg, sp_encoder** out) {
+    if (!cfg || !out) return efail(SP_E_ARG, "NULL argument");
+    *out = nullptr;
+    if (!cfg->src_width || !cfg->src_height || !cfg->dst_width || !cfg->dst_height)
+        return efail(SP_E_CONFIG, "frame dimensions must be >= 1");
+    if (cfg->dst_width > cfg->src_width || cfg->dst_height > cfg->src_height)
+        return efail(SP_E_CONFIG, "upscaling is an input error (S:289)");
+    if (cfg->block_size < 3 || cfg->block_size > 15 || cfg->block_size % 2 == 0)
+        return efail(SP_E_CONFIG, "block_size must be odd in [3, 15]");
+    if (!std::isfinite(cfg->bias) || std::fabs(cfg->bias) > 255.0f) return efail(SP_E_CONFIG, "bias out of range");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return efail(SP_E_CUDA, "no CUDA device");
+    if (cfg->device < 0 || cfg->device >= ndev) return efail(SP_E_ARG, "device out of range");
+    cudaSetDevice(cfg->device);
+    sp_encoder* e = new sp_encoder();
+    e->cfg = *cfg;
+    e->device = cfg->device;
+    cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, e->device);
+    int max_smem = 0;
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, e->device);
+    int sm_smem = 0;
+    cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, e->device);
+    sp::EncParams& p = e->p;
+    p.W0 = cfg->src_width, p.H0 = cfg->src_height, p.W1 = cfg->dst_width, p.H1 = cfg->dst_height;
+    p.row_bytes = 3u * p.W0;
+    p.K = static_cast<int32_t>(cfg->block_size);
+    p.cbias = static_cast<int32_t>(std::ceil(cfg->bias));
+    gaussian_q8(p.K, p.q);
+    std::vector<uint32_t> yoff, ysy, xoff, xsx;
+    std::vector<float> ybeta, xalpha;
+    sp::area_table(p.H0, p.H1, yoff, ysy, ybeta);
+    sp::area_table(p.W0, p.W1, xoff, xsx, xalpha);
+    p.xfast = 1u;
+    for (uint32_t d = 0; d < p.W1 && p.xfast; ++d) {
+        if (xoff[d + 1] - xoff[d] != 4u) p.xfast = 0u;
+        for (uint32_t k = xoff[d]; k < xoff[d + 1] && p.xfast; ++k)
+            if (xsx[k] != 4u * d + (k - xoff[d]) || xalpha[k] != 0.25f) p.xfast = 0u;
+    }
+    // bands of output rows: the largest band_rows whose source rows fit a stage of <= 32 KiB,
+    // ring of 2..4 stages, 2 CTAs per SM when they fit
+    const uint32_t gray_bytes = (p.W1 * p.H1 + 127u) & ~127u;
+    uint32_t best_rows = 0, best_stages = 0, best_cps = 0, best_stage_bytes = 0;
+    std::vector<uint32_t> sy0, sn;
+    for (uint32_t rows = 1; rows <= p.H1; ++rows) {
+        uint32_t maxn = 0;
+        for (uint32_t b = 0; b * rows < p.H1; ++b) {
+            const uint32_t d0 = b * rows, d1 = std::min(p.H1, d0 + rows);
+            const uint32_t lo = ysy[yoff[d0]], hi = ysy[yoff[d1] - 1u];
+            maxn = std::max(maxn, hi - lo + 1u);
+        }
+        const uint32_t stage = (maxn * p.row_bytes + 127u) & ~127u;
+        if (rows > 1 && stage > 32768u) break;
+        for (uint32_t stages = sp::kMaxStages; stages >= 2; --stages) {
+            const uint32_t smem = gray_bytes + stages * stage;
+            if (static_cast<int>(smem) > max_smem - 1024) continue;
+            const uint32_t cps = std::min<uint32_t>(2u, static_cast<uint32_t>(sm_smem / (smem + 1024u)));
+            // prefer 2 CTAs per SM, then more bytes in flight per SM
+            if (cps > best_cps || (cps == best_cps && cps * stages * stage > best_cps * best_stages * best_stage_bytes)) {
+                best_rows = rows, best_stages = stages, best_cps = cps, best_stage_bytes = stage;
+            }
+            break;
+        }
+    }
+    if (!best_rows) {
+        delete e;
+        return efail(SP_E_CONFIG, "frame rows do not fit shared memory");
+    }
+    p.band_rows = best_rows;
+    p.stages = best_stages;
+    p.stage_bytes = best_stage_bytes;
+    e->ctas_per_sm = std::max<uint32_t>(1u, best_cps);
+    e->smem = gray_bytes + p.stages * p.stage_bytes;
+    p.bands = (p.H1 + p.band_rows - 1u) / p.band_rows;
+    for (uint32_t b = 0; b < p.bands; ++b) {
+        const uint32_t d0 = b * p.band_rows, d1 = std::min(p.H1, d0 + p.band_rows);
+        sy0.push_back(ysy[yoff[d0]]);
+        sn.push_back(ysy[yoff[d1] - 1u] - ysy[yoff[d0]] + 1u);
+    }
+    std::vector<uint32_t> u32;
+    auto put = [&](const std::vector<uint32_t>& v) {
+        const size_t o = u32.size();
+        u32.insert(u32.end(), v.begin(), v.end());
+        return o;
+    };
+    const size_t o_sy0 = put(sy0), o_sn = put(sn), o_yoff = put(yoff), o_ysy = put(ysy), o_xoff = put(xoff),
+                 o_xsx = put(xsx);
+    std::vector<float> f32(ybeta);
+    const size_t o_xa = f32.size();
+    f32.insert(f32.end(), xalpha.begin(), xalpha.end());
+    cudaError_t err = cudaMalloc(&e->d_u32, u32.size() * 4u);
+    if (err == cudaSuccess) err = cudaMalloc(&e->d_f32, f32.size() * 4u);
+    if (err == cudaSuccess) err = cudaMemcpy(e->d_u32, u32.data(), u32.size() * 4u, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess) err = cudaMemcpy(e->d_f32, f32.data(), f32.size() * 4u, cudaMemcpyHostToDevice);
+    if (err == cudaSuccess)
+        err = cudaFuncSetAttribute(sp::k_encode, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e->smem));
+    if (err != cudaSuccess) {
+        if (e->d_u32) cudaFree(e->d_u32);
+        if (e->d_f32) cudaFree(e->d_f32);
+        delete e;
+        return efail(SP_E_CUDA, cudaGetErrorString(err));
+    }
+    p.band_sy0 = e->d_u32 + o_sy0;
+    p.band_n = e->d_u32 + o_sn;
+    p.yoff = e->d_u32 + o_yoff;
+    p.ysy = e->d_u32 + o_ysy;
+    p.xoff = e->d_u32 + o_xoff;
+    p.xsx = e->d_u32 + o_xsx;
+    p.ybeta = e->d_f32;
+    p.xalpha = e->d_f32 + o_xa;
+    *out = e;
+    return SP_OK;
+}
+
+sp_status sp_encoder_destroy(sp_encoder* e) {
+    if (!e) return SP_OK;
+    cudaSetDevice(e->device);
+    cudaDeviceSynchronize();
+    cudaFree(e->d_u32);
+    cudaFree(e->d_f32);
+    delete e;
+    return SP_OK;
+}
+
+sp_status sp_encode(sp_encoder* e, const uint8_t* bgr_dev, uint32_t num_frames, uint8_t* out_dev, void* cuda_stream) {
+    if (!e) return efail(SP_E_ARG, "encoder is NULL");
+    if (num_frames == 0) return SP_OK;
+    if (!bgr_dev || !out_dev) return efail(SP_E_ARG, "NULL frame buffer");
+    cudaSetDevice(e->device);
+    sp::EncParams p = e->p;
+    p.src = bgr_dev;
+    p.dst = out_dev;
+    p.F = num_frames;
+    p.bulk = ((reinterpret_cast<uintptr_t>(bgr_dev) & 15u) == 0 && (p.row_bytes & 15u) == 0) ? 1u : 0u;
+    const uint32_t grid = std::min<uint32_t>(num_frames, e->ctas_per_sm * static_cast<uint32_t>(e->sm_count));
+    sp::k_encode<<<grid, sp::kEncThreads, e->smem, static_cast<cudaStream_t>(cuda_stream)>>>(p);
+    e->launches++;
+    const cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return efail(SP_E_CUDA, cudaGetErrorString(err));
+    return SP_OK;
+}
+
+sp_status sp_encoder_get_info(sp_encoder* e, sp_encoder_info* out) {
+    if (!e || !out) return efail(SP_E_ARG, "NULL argument");
+    out->band_rows = e->p.band_rows;
+    out->bands = e->p.bands;
+    out->stages = e->p.stages;
+    out->stage_bytes = e->p.stage_bytes;
+    out->smem_bytes = e->smem;
+    out->ctas_per_sm = e->ctas_per_sm;
+    out->xfast = e->p.xfast;
+    out->kernel_launches = e->launches;
+    for (int i = 0; i < 16; ++i) out->kernel_q8[i] = i < e->p.K ? e->p.q[i] : 0;
+    return SP_OK;
+}
+
+}  // extern "C"

@@ -39,7 +39,9 @@ ABI_SYMBOLS = ("sp_config_default", "sp_create", "sp_destroy", "sp_compute", "sp
                "sp_overlaps", "sp_get_state", "sp_set_state", "sp_compute_host", "sp_plan",
                "sp_init_pools_host", "sp_get_info", "sp_last_error", "sp_version",
                "sp_get_learning_state", "sp_set_learning_state", "sp_histograms",
-               "sp_synth_frames")
+               "sp_synth_frames", "sp_synth_bgr_frames", "sp_encoder_config_default",
+               "sp_encoder_create", "sp_encoder_destroy", "sp_encode", "sp_encoder_get_info",
+               "sp_encoder_last_error")
 
 
 class SpError(RuntimeError):
@@ -73,6 +75,18 @@ class SpPlanInfo(ctypes.Structure):
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
+
+
+class SpEncoderConfig(ctypes.Structure):
+    _fields_ = [("src_width", ctypes.c_uint32), ("src_height", ctypes.c_uint32),
+                ("dst_width", ctypes.c_uint32), ("dst_height", ctypes.c_uint32),
+                ("block_size", ctypes.c_uint32), ("bias", ctypes.c_float), ("device", ctypes.c_int32)]
+
+
+class SpEncoderInfo(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint32) for n in ("band_rows", "bands", "stages", "stage_bytes", "smem_bytes",
+                                               "ctas_per_sm", "xfast")] + \
+               [("kernel_launches", ctypes.c_uint64), ("kernel_q8", ctypes.c_int32 * 16)]
 
 
 class SpInfo(ctypes.Structure):
@@ -114,6 +128,12 @@ def lib() -> ctypes.CDLL:
         "sp_set_learning_state": [vp, vp, vp, u32],
         "sp_histograms": [vp, vp, u32, vp, vp, vp],
         "sp_synth_frames": [vp, u64, u32, u32, u32, u64, u32, u32, vp],
+        "sp_synth_bgr_frames": [vp, u64, u32, u32, u32, u64, vp],
+        "sp_encoder_config_default": [P(SpEncoderConfig)],
+        "sp_encoder_create": [P(SpEncoderConfig), P(vp)],
+        "sp_encoder_destroy": [vp],
+        "sp_encode": [vp, vp, u32, vp, vp],
+        "sp_encoder_get_info": [vp, P(SpEncoderInfo)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -123,6 +143,8 @@ def lib() -> ctypes.CDLL:
     L.sp_last_error.argtypes = []
     L.sp_version.restype = ctypes.c_char_p
     L.sp_version.argtypes = []
+    L.sp_encoder_last_error.restype = ctypes.c_char_p
+    L.sp_encoder_last_error.argtypes = []
     _lib = L
     return L
 
@@ -188,6 +210,74 @@ def synth_frames(out, first_frame: int, seed: int, rho: float = 0.5, nonzero: st
     _check(lib().sp_synth_frames(ctypes.c_void_p(out.data_ptr()), first_frame, F, H, W, seed, q24,
                                  mode, _stream_ptr(stream, out.device)))
     return out
+
+
+def synth_bgr_frames(out, first_frame: int, seed: int, stream=None):
+    """Fills uint8 cuda tensor ``out[F, H, W, 3]`` with BGR frames of the seeded recipe (bench/test)."""
+    import torch
+    _require(out, torch.uint8, out.device.index if out.is_cuda else -1, name="out")
+    F, H, W, ch = out.shape
+    if ch != 3:
+        raise SpError(SP_E_SHAPE, "out must be [F, H, W, 3]")
+    _check(lib().sp_synth_bgr_frames(ctypes.c_void_p(out.data_ptr()), first_frame, F, H, W, seed,
+                                     _stream_ptr(stream, out.device)))
+    return out
+
+
+class Encoder:
+    """The on-device adaptive video encoder (``include/sp_encoder.h``, NEXT-3): BGR frames ->
+    binarised frames for ``SpatialPooler.compute``."""
+
+    def __init__(self, **kw):
+        cfg = SpEncoderConfig()
+        _check(lib().sp_encoder_config_default(ctypes.byref(cfg)))
+        for k, v in kw.items():
+            if not hasattr(cfg, k):
+                raise SpError(SP_E_CONFIG, f"unknown encoder config key {k!r}")
+            setattr(cfg, k, v)
+        self.cfg = cfg
+        h = ctypes.c_void_p()
+        st = lib().sp_encoder_create(ctypes.byref(cfg), ctypes.byref(h))
+        if st != SP_OK:
+            raise SpError(st, lib().sp_encoder_last_error().decode())
+        self._h = h
+        self.device = int(cfg.device)
+        self.src_shape = (int(cfg.src_height), int(cfg.src_width), 3)
+        self.dst_shape = (int(cfg.dst_height), int(cfg.dst_width))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().sp_encoder_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def encode(self, bgr, out=None, stream=None):
+        """``bgr``: uint8 cuda [F, H0, W0, 3] -> uint8 cuda [F, H1, W1] (255 / 0)."""
+        import torch
+        _require(bgr, torch.uint8, self.device, name="bgr")
+        if bgr.dim() != 4 or tuple(bgr.shape[1:]) != self.src_shape:
+            raise SpError(SP_E_SHAPE, f"bgr must be [F, {self.src_shape}]")
+        F = bgr.shape[0]
+        if out is None:
+            out = torch.empty((F, *self.dst_shape), dtype=torch.uint8, device=bgr.device)
+        _require(out, torch.uint8, self.device, (F, *self.dst_shape), "out")
+        st = lib().sp_encode(self._h, ctypes.c_void_p(bgr.data_ptr()), F, ctypes.c_void_p(out.data_ptr()),
+                             _stream_ptr(stream, bgr.device))
+        if st != SP_OK:
+            raise SpError(st, lib().sp_encoder_last_error().decode())
+        return out
+
+    def info(self) -> dict:
+        out = SpEncoderInfo()
+        _check(lib().sp_encoder_get_info(self._h, ctypes.byref(out)))
+        d = {n: int(getattr(out, n)) for n, _ in out._fields_ if n != "kernel_q8"}
+        d["kernel_q8"] = list(out.kernel_q8)[:int(self.cfg.block_size)]
+        return d
 
 
 class SpatialPooler:

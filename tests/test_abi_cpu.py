@@ -21,7 +21,7 @@ def built():
 
 def declared_symbols():
     names = set()
-    for h in ("sp.h", "sp_synth.h"):
+    for h in sorted(os.listdir(os.path.join(ROOT, "include"))):
         txt = open(os.path.join(ROOT, "include", h)).read()
         names |= set(re.findall(r"^\s*(?:sp_status|const char\*)\s+(sp_\w+)\s*\(", txt, re.M))
     return names
@@ -120,3 +120,13 @@ def test_create_without_gpu_fails_loudly():
     with pytest.raises(P.SpError) as ei:
         P.SpatialPooler(input_width=8, input_height=8, num_columns=128, synapses_per_column=16)
     assert ei.value.status == P.SP_E_CUDA
+
+
+def test_encoder_create_without_gpu_fails_loudly():
+    # no CPU fallback for the encoder either: creation needs a CUDA device (CPU box: SP_E_CUDA)
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(P.SpError) as e:
+        P.Encoder()
+    assert e.value.status == P.SP_E_CUDA
