@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-learn-full", action="store_true")
+    ap.add_argument("--no-encoder", action="store_true")
+    ap.add_argument("--encoder-frames", type=int, default=2048)
     return ap.parse_args()
 
 
@@ -333,6 +335,51 @@ def main():
                   "share_of_step": hist_ms / (ms / args.steps),
                   "note": "sp_histograms (NEXT-4) over the step's SDRs, device time per call (host enqueue hidden)"}
 
+    # ---- NEXT-3: the on-device encoder (BGR 960x540 -> binarised 240x134) and the SP on its
+    # output (Tab. 2 SP: 2048 columns, 128 synapses, min_overlap 8, k 40) ------------------
+    encoder = None
+    if not args.no_encoder and world == 1:
+        EF = args.encoder_frames
+        del frames
+        torch.cuda.empty_cache()
+        bgr = torch.empty((EF, H, W, 3), dtype=torch.uint8, device=dev)
+        P.synth_bgr_frames(bgr, 0, SEED_INFER)
+        enc = P.Encoder(device=local)
+        binf = torch.empty((EF, 134, 240), dtype=torch.uint8, device=dev)
+        sp2 = P.SpatialPooler(input_width=240, input_height=134, num_columns=2048, synapses_per_column=128,
+                              min_overlap=8, winners_set_size=40, device=local, max_inputs=EF)
+        for _ in range(3):
+            enc.encode(bgr, binf)
+            sp2.compute(binf)
+        torch.cuda.synchronize()
+        ea, eb, ec = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        reps = 5
+        ea.record(stream)
+        for _ in range(reps):
+            enc.encode(bgr, binf)
+        eb.record(stream)
+        for _ in range(reps):
+            enc.encode(bgr, binf)
+            sp2.compute(binf)
+        ec.record(stream)
+        torch.cuda.synchronize()
+        enc_ms = ea.elapsed_time(eb) / reps
+        both_ms = eb.elapsed_time(ec) / reps
+        enc_bytes = EF * (H * W * 3 + 134 * 240)
+        peak_hbm, _ = measured_peak_hbm()
+        encoder = {"frames": EF, "src": f"{W}x{H} BGR", "dst": "240x134", "block_size": 11, "bias": 2.0,
+                   "ms": enc_ms, "frames_per_s": EF / enc_ms * 1e3,
+                   "achieved_gbs": enc_bytes / (enc_ms / 1e3) / 1e9,
+                   "hbm_frac": enc_bytes / (enc_ms / 1e3) / 1e9 / peak_hbm,
+                   "encode_plus_sp_frames_per_s": EF / both_ms * 1e3,
+                   "sp": "Tab. 2 SP on the encoded frames (2048 columns, 128 synapses, k 40)",
+                   "plan": {k: v for k, v in enc.info().items() if k != "kernel_q8"}}
+        enc.close()
+        sp2.close()
+        del bgr, binf
+        frames = torch.empty((F, H, W), dtype=torch.uint8, device=dev)
+        P.synth_frames(frames, F0, SEED_INFER, 0.5)
+
     # ---- e2e: the public host-buffer call (H2D of frames + D2H of SDRs inside) -----------
     e2e = None
     if not args.no_e2e:
@@ -395,7 +442,7 @@ def main():
                                                      "num_windows", "stages", "smem_bytes")}},
             "hbm_frac": round(value / world * ALGO_BYTES_PER_FRAME / 1e9 / peak, 4),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(), "learn": learn, "histograms": histograms}
+            "clocks": clk.summary(), "learn": learn, "histograms": histograms, "encoder": encoder}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

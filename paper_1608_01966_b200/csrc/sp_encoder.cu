@@ -46,6 +46,18 @@ struct EncParams {
     const float* xalpha;       // [.]
     int32_t K, cbias;          // Gaussian window, ceil(bias)
     int32_t q[16];             // 8-bit quantised Gaussian kernel (sum 256)
+    uint32_t ny_entries, nx_entries;  // table sizes (staged in shared memory per CTA)
+    uint32_t table_bytes;      // shared-memory bytes of the staged tables
+};
+
+// the area tables staged in shared memory once per CTA (warp-uniform or conflict-free reads)
+struct EncTables {
+    const uint32_t* yoff;
+    const uint32_t* ysy;
+    const float* ybeta;
+    const uint32_t* xoff;
+    const uint32_t* xsx;
+    const float* xalpha;
 };
 
 __device__ __forceinline__ void mbar_init_e(uint64_t* bar) {
@@ -85,104 +97,122 @@ __device__ __forceinline__ void issue_band(const EncParams& p, uint32_t f, uint3
 }
 
 // R23 + R24 for the output rows of band b: fp32 area sums in OpenCV's order, round half to
-// even, saturate, then the 15-bit gray formula
-__device__ __forceinline__ void downscale_band(const EncParams& p, uint32_t b, const uint8_t* buf, uint8_t* gray) {
+// even, saturate, then the 15-bit gray formula.  Thread (ty, tx) handles output pixels
+// (dy0 + ty + k*ny, tx + m*sx) of the band.
+__device__ __forceinline__ void downscale_band(const EncParams& p, const EncTables& t, uint32_t b, const uint8_t* buf,
+                                               uint8_t* gray, uint32_t ty, uint32_t tx, uint32_t ny, uint32_t sx) {
     const uint32_t dy0 = b * p.band_rows, dy1 = min(p.H1, dy0 + p.band_rows);
-    const uint32_t npx = (dy1 - dy0) * p.W1;
-    const uint32_t sy0 = p.band_sy0[b];
-    for (uint32_t i = threadIdx.x; i < npx; i += blockDim.x) {
-        const uint32_t dy = dy0 + i / p.W1, dx = i % p.W1;
-        float sb = 0.0f, sg = 0.0f, sr = 0.0f;
-        const uint32_t j0 = p.yoff[dy], j1 = p.yoff[dy + 1];
-        for (uint32_t j = j0; j < j1; ++j) {
-            const uint8_t* row = buf + (p.ysy[j] - sy0) * p.row_bytes;
-            float bb, bg, br;
+    const int32_t rb = static_cast<int32_t>(p.row_bytes);
+    const uint8_t* buf0 = buf - static_cast<int32_t>(p.band_sy0[b]) * rb;  // row sy of the band at buf0 + sy*rb
+    for (uint32_t dy = dy0 + ty; dy < dy1; dy += ny) {
+        const uint32_t j0 = t.yoff[dy], j1 = t.yoff[dy + 1];
+        for (uint32_t dx = tx; dx < p.W1; dx += sx) {
+            float sb, sg, sr;
             if (p.xfast) {
                 // 4 BGR pixels = 12 bytes at 12*dx: B0 G0 R0 B1 | G1 R1 B2 G2 | R2 B3 G3 R3.
-                // Each x partial sum is a multiple of 0.25 below 2^10: the fp32 sequence
-                // ((0 + S0/4) + S1/4) + ... is exact, so it equals (S0+S1+S2+S3) * 0.25.
-                const uint32_t* w = reinterpret_cast<const uint32_t*>(row + 12u * dx);
-                const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
-                const uint32_t vb = __byte_perm(__byte_perm(w0, w1, 0x0630u), w2, 0x5210u);  // B0 B1 B2 B3
-                const uint32_t vg = __byte_perm(__byte_perm(w0, w1, 0x0741u), w2, 0x6210u);  // G0 G1 G2 G3
-                const uint32_t vr = __byte_perm(__byte_perm(w0, w1, 0x0052u), w2, 0x7410u);  // R0 R1 R2 R3
-                bb = __fmul_rn(static_cast<float>(__dp4a(vb, 0x01010101u, 0u)), 0.25f);
-                bg = __fmul_rn(static_cast<float>(__dp4a(vg, 0x01010101u, 0u)), 0.25f);
-                br = __fmul_rn(static_cast<float>(__dp4a(vr, 0x01010101u, 0u)), 0.25f);
+                // The x partial sums ((0 + S0/4) + S1/4) + ... are multiples of 0.25 below 2^10,
+                // so exact: buf = (S0+S1+S2+S3)/4, and beta*buf = RN((beta/4) * (S0+..+S3)) with
+                // ybeta holding beta/4 (exact).  Channel sums by byte-masked dot products.
+                const uint8_t* col = buf0 + 12u * dx;
+                auto sums = [&](uint32_t j, float& b_, float& g_, float& r_) {
+                    const uint32_t* w = reinterpret_cast<const uint32_t*>(col + static_cast<int32_t>(t.ysy[j]) * rb);
+                    const uint32_t w0 = w[0], w1 = w[1], w2 = w[2];
+                    const float be = t.ybeta[j];
+                    b_ = __fmul_rn(be, static_cast<float>(__dp4a(w0, 0x01000001u, __dp4a(w1, 0x00010000u, __dp4a(w2, 0x00000100u, 0u)))));
+                    g_ = __fmul_rn(be, static_cast<float>(__dp4a(w0, 0x00000100u, __dp4a(w1, 0x01000001u, __dp4a(w2, 0x00010000u, 0u)))));
+                    r_ = __fmul_rn(be, static_cast<float>(__dp4a(w0, 0x00010000u, __dp4a(w1, 0x00000100u, __dp4a(w2, 0x01000001u, 0u)))));
+                };
+                sums(j0, sb, sg, sr);  // the first term is beta*buf itself (OpenCV: sum = beta*buf)
+                for (uint32_t j = j0 + 1u; j < j1; ++j) {
+                    float tb, tg, tr;
+                    sums(j, tb, tg, tr);
+                    sb = __fadd_rn(sb, tb), sg = __fadd_rn(sg, tg), sr = __fadd_rn(sr, tr);
+                }
             } else {
-                bb = bg = br = 0.0f;
-                for (uint32_t k = p.xoff[dx]; k < p.xoff[dx + 1]; ++k) {
-                    const uint8_t* s = row + 3u * p.xsx[k];
-                    const float a = p.xalpha[k];
-                    bb = __fadd_rn(bb, __fmul_rn(static_cast<float>(s[0]), a));
-                    bg = __fadd_rn(bg, __fmul_rn(static_cast<float>(s[1]), a));
-                    br = __fadd_rn(br, __fmul_rn(static_cast<float>(s[2]), a));
+                sb = sg = sr = 0.0f;
+                for (uint32_t j = j0; j < j1; ++j) {
+                    const uint8_t* row = buf0 + static_cast<int32_t>(t.ysy[j]) * rb;
+                    float bb = 0.0f, bg = 0.0f, br = 0.0f;
+                    for (uint32_t k = t.xoff[dx]; k < t.xoff[dx + 1]; ++k) {
+                        const uint8_t* s = row + 3u * t.xsx[k];
+                        const float a = t.xalpha[k];
+                        bb = __fadd_rn(bb, __fmul_rn(static_cast<float>(s[0]), a));
+                        bg = __fadd_rn(bg, __fmul_rn(static_cast<float>(s[1]), a));
+                        br = __fadd_rn(br, __fmul_rn(static_cast<float>(s[2]), a));
+                    }
+                    const float beta = t.ybeta[j];
+                    const float tb = __fmul_rn(beta, bb), tg = __fmul_rn(beta, bg), tr = __fmul_rn(beta, br);
+                    if (j == j0) {
+                        sb = tb, sg = tg, sr = tr;
+                    } else {
+                        sb = __fadd_rn(sb, tb), sg = __fadd_rn(sg, tg), sr = __fadd_rn(sr, tr);
+                    }
                 }
             }
-            const float beta = p.ybeta[j];
-            const float tb = __fmul_rn(beta, bb), tg = __fmul_rn(beta, bg), tr = __fmul_rn(beta, br);
-            if (j == j0) {
-                sb = tb, sg = tg, sr = tr;
-            } else {
-                sb = __fadd_rn(sb, tb), sg = __fadd_rn(sg, tg), sr = __fadd_rn(sr, tr);
-            }
+            const int B = min(255, max(0, __float2int_rn(sb)));  // saturate_cast<uchar>: half to even
+            const int G = min(255, max(0, __float2int_rn(sg)));
+            const int R = min(255, max(0, __float2int_rn(sr)));
+            gray[dy * p.W1 + dx] = static_cast<uint8_t>((3735 * B + 19235 * G + 9798 * R + 16384) >> 15);
         }
-        const int B = min(255, max(0, __float2int_rn(sb)));  // saturate_cast<uchar>: half to even
-        const int G = min(255, max(0, __float2int_rn(sg)));
-        const int R = min(255, max(0, __float2int_rn(sr)));
-        gray[dy * p.W1 + dx] = static_cast<uint8_t>((3735 * B + 19235 * G + 9798 * R + 16384) >> 15);
     }
 }
 
 // R25: Gaussian mean (exact integers) and threshold, a register window of K horizontal sums
-// down column x for rows [y0, y1)
+// down columns x and x+1 (one thread, shared loads) for rows [y0, y1)
 template <int K>
-__device__ __forceinline__ void blur_column(const EncParams& p, const uint8_t* gray, uint8_t* out, uint32_t x,
-                                            uint32_t y0, uint32_t y1) {
+__device__ __forceinline__ void blur_columns(const EncParams& p, const uint8_t* gray, uint8_t* out, uint32_t x,
+                                             uint32_t y0, uint32_t y1) {
     constexpr int R = K / 2;
     const int W = static_cast<int>(p.W1), H = static_cast<int>(p.H1);
-    int cx[K];
+    const bool two = static_cast<int>(x) + 1 < W;
+    int cx[K + 1];
 #pragma unroll
-    for (int j = 0; j < K; ++j) cx[j] = min(W - 1, max(0, static_cast<int>(x) + j - R));
-    auto hsum = [&](int yy) {
+    for (int j = 0; j <= K; ++j) cx[j] = min(W - 1, max(0, static_cast<int>(x) + j - R));
+    int q[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) q[j] = p.q[j];
+    auto hsum = [&](int yy, int& a, int& b) {
         const uint8_t* row = gray + min(H - 1, max(0, yy)) * W;
-        int s = 0;
+        int v[K + 1];
 #pragma unroll
-        for (int j = 0; j < K; ++j) s += p.q[j] * row[cx[j]];
-        return s;
+        for (int j = 0; j <= K; ++j) v[j] = row[cx[j]];
+        a = 0, b = 0;
+#pragma unroll
+        for (int j = 0; j < K; ++j) a += q[j] * v[j], b += q[j] * v[j + 1];
     };
-    int h[K];
+    int ha[K], hb[K];
 #pragma unroll
-    for (int i = 0; i < K - 1; ++i) h[i] = hsum(static_cast<int>(y0) - R + i);
+    for (int i = 0; i < K - 1; ++i) hsum(static_cast<int>(y0) - R + i, ha[i], hb[i]);
     for (int y = static_cast<int>(y0); y < static_cast<int>(y1); ++y) {
-        h[K - 1] = hsum(y + R);
-        int acc = 0;
+        hsum(y + R, ha[K - 1], hb[K - 1]);
+        int acca = 0, accb = 0;
 #pragma unroll
-        for (int i = 0; i < K; ++i) acc += p.q[i] * h[i];
-        const int m = (acc + 32768) >> 16;
-        const int gv = gray[y * W + static_cast<int>(x)];
-        out[static_cast<size_t>(y) * W + x] = gv - m > -p.cbias ? 255u : 0u;
+        for (int i = 0; i < K; ++i) acca += q[i] * ha[i], accb += q[i] * hb[i];
+        const uint8_t* grow = gray + y * W + x;
+        uint8_t* orow = out + static_cast<size_t>(y) * W + x;
+        orow[0] = static_cast<int>(grow[0]) - ((acca + 32768) >> 16) > -p.cbias ? 255u : 0u;
+        if (two) orow[1] = static_cast<int>(grow[1]) - ((accb + 32768) >> 16) > -p.cbias ? 255u : 0u;
 #pragma unroll
-        for (int i = 0; i < K - 1; ++i) h[i] = h[i + 1];
+        for (int i = 0; i < K - 1; ++i) ha[i] = ha[i + 1], hb[i] = hb[i + 1];
     }
 }
 
 __device__ __forceinline__ void blur_frame(const EncParams& p, const uint8_t* gray, uint8_t* out) {
-    // two row halves per column (the halo rows are recomputed)
-    const uint32_t halves = blockDim.x >= 2u * p.W1 ? 2u : 1u;
-    const uint32_t mid = p.H1 / 2u;
-    for (uint32_t t = threadIdx.x; t < halves * p.W1; t += blockDim.x) {
-        const uint32_t x = t % p.W1, half = t / p.W1;
-        const uint32_t y0 = halves == 1u ? 0u : (half ? mid : 0u);
-        const uint32_t y1 = halves == 1u ? p.H1 : (half ? p.H1 : mid);
+    // column pairs x0 = 2c; the rows are split into segments so that all threads have work
+    // (the K-1 halo rows of a segment are recomputed)
+    const uint32_t pairs = (p.W1 + 1u) / 2u;
+    const uint32_t segs = max(1u, min(p.H1 / 16u, blockDim.x / pairs));
+    for (uint32_t t = threadIdx.x; t < segs * pairs; t += blockDim.x) {
+        const uint32_t x = 2u * (t % pairs), sgi = t / pairs;
+        const uint32_t y0 = p.H1 * sgi / segs, y1 = p.H1 * (sgi + 1u) / segs;
         switch (p.K) {
-            case 3: blur_column<3>(p, gray, out, x, y0, y1); break;
-            case 5: blur_column<5>(p, gray, out, x, y0, y1); break;
-            case 7: blur_column<7>(p, gray, out, x, y0, y1); break;
-            case 9: blur_column<9>(p, gray, out, x, y0, y1); break;
-            case 11: blur_column<11>(p, gray, out, x, y0, y1); break;
-            case 13: blur_column<13>(p, gray, out, x, y0, y1); break;
-            default: blur_column<15>(p, gray, out, x, y0, y1); break;
+            case 3: blur_columns<3>(p, gray, out, x, y0, y1); break;
+            case 5: blur_columns<5>(p, gray, out, x, y0, y1); break;
+            case 7: blur_columns<7>(p, gray, out, x, y0, y1); break;
+            case 9: blur_columns<9>(p, gray, out, x, y0, y1); break;
+            case 11: blur_columns<11>(p, gray, out, x, y0, y1); break;
+            case 13: blur_columns<13>(p, gray, out, x, y0, y1); break;
+            default: blur_columns<15>(p, gray, out, x, y0, y1); break;
         }
     }
 }
@@ -192,6 +222,29 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const __grid_constant__ 
     __shared__ __align__(8) uint64_t bars[kMaxStages];
     uint8_t* gray = sm;
     uint8_t* ring = sm + ((p.W1 * p.H1 + 127u) & ~127u);
+    // area tables -> shared memory (after the ring)
+    EncTables t;
+    {
+        uint32_t* tu = reinterpret_cast<uint32_t*>(ring + p.stages * p.stage_bytes);
+        uint32_t* yoff = tu;
+        uint32_t* ysy = yoff + p.H1 + 1u;
+        float* ybeta = reinterpret_cast<float*>(ysy + p.ny_entries);
+        uint32_t* xoff = reinterpret_cast<uint32_t*>(ybeta + p.ny_entries);
+        uint32_t* xsx = xoff + p.W1 + 1u;
+        float* xalpha = reinterpret_cast<float*>(xsx + p.nx_entries);
+        for (uint32_t i = threadIdx.x; i <= p.H1; i += blockDim.x) yoff[i] = p.yoff[i];
+        for (uint32_t i = threadIdx.x; i < p.ny_entries; i += blockDim.x) ysy[i] = p.ysy[i], ybeta[i] = p.ybeta[i];
+        if (!p.xfast) {
+            for (uint32_t i = threadIdx.x; i <= p.W1; i += blockDim.x) xoff[i] = p.xoff[i];
+            for (uint32_t i = threadIdx.x; i < p.nx_entries; i += blockDim.x) xsx[i] = p.xsx[i], xalpha[i] = p.xalpha[i];
+        }
+        t = EncTables{yoff, ysy, ybeta, xoff, xsx, xalpha};
+    }
+    // pixel mapping of the downscale: rows of W1 threads (W1 <= blockDim), else one row
+    const uint32_t ny = p.W1 <= blockDim.x ? blockDim.x / p.W1 : 1u;
+    const uint32_t ty = p.W1 <= blockDim.x ? threadIdx.x / p.W1 : 0u;
+    const uint32_t tx = p.W1 <= blockDim.x ? threadIdx.x % p.W1 : threadIdx.x;
+    const uint32_t sxs = p.W1 <= blockDim.x ? p.W1 : blockDim.x;
     const uint32_t nf = p.F > blockIdx.x ? (p.F - blockIdx.x + gridDim.x - 1u) / gridDim.x : 0u;
     const uint32_t total = nf * p.bands;  // (frame, band) sequence of this CTA
     if (threadIdx.x == 0) {
@@ -203,26 +256,26 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const __grid_constant__ 
     if (p.bulk && threadIdx.x == 0)
         for (uint32_t s = 0; s < p.stages && s < total; ++s)
             issue_band(p, frame_of(s), s % p.bands, ring + s * p.stage_bytes, &bars[s]);
-    uint32_t seq = 0;
+    uint32_t seq = 0, st = 0, phase = 0;  // ring position: stage and its mbarrier parity
     for (uint32_t i = 0; i < nf; ++i) {
         const uint32_t f = blockIdx.x + i * gridDim.x;
         for (uint32_t b = 0; b < p.bands; ++b, ++seq) {
-            const uint32_t st = seq % p.stages;
             uint8_t* buf = ring + st * p.stage_bytes;
             if (p.bulk) {
-                mbar_wait_e(&bars[st], (seq / p.stages) & 1u);
+                mbar_wait_e(&bars[st], phase);
             } else {  // unaligned rows: cooperative byte copy of the band
                 const uint8_t* g = p.src + (static_cast<size_t>(f) * p.H0 + p.band_sy0[b]) * p.row_bytes;
                 const uint32_t bytes = p.band_n[b] * p.row_bytes;
                 for (uint32_t k = threadIdx.x; k < bytes; k += blockDim.x) buf[k] = g[k];
                 __syncthreads();
             }
-            downscale_band(p, b, buf, gray);
+            if (ty < ny) downscale_band(p, t, b, buf, gray, ty, tx, ny, sxs);
             __syncthreads();  // the stage is free; the band's gray rows are complete
             if (p.bulk && threadIdx.x == 0 && seq + p.stages < total) {
                 const uint32_t nx = seq + p.stages;
                 issue_band(p, frame_of(nx), nx % p.bands, buf, &bars[st]);
             }
+            if (++st == p.stages) st = 0, phase ^= 1u;
         }
         blur_frame(p, gray, p.dst + static_cast<size_t>(f) * p.W1 * p.H1);
         __syncthreads();  // the gray image is rewritten by the next frame's bands
@@ -375,9 +428,17 @@ sp_status sp_encoder_create(const sp_encoder_config* cfg, sp_encoder** out) {
         for (uint32_t k = xoff[d]; k < xoff[d + 1] && p.xfast; ++k)
             if (xsx[k] != 4u * d + (k - xoff[d]) || xalpha[k] != 0.25f) p.xfast = 0u;
     }
-    // bands of output rows: the largest band_rows whose source rows fit a stage of <= 32 KiB,
-    // ring of 2..4 stages, 2 CTAs per SM when they fit
+    // bands of output rows: the fewest bands (largest band_rows, stage <= 48 KiB) whose ring of
+    // >= 2 stages lets 2 CTAs share an SM; then the deepest ring that keeps that occupancy
     const uint32_t gray_bytes = (p.W1 * p.H1 + 127u) & ~127u;
+    p.ny_entries = static_cast<uint32_t>(ysy.size());
+    p.nx_entries = static_cast<uint32_t>(xsx.size());
+    p.table_bytes = 4u * (p.H1 + 1u + 2u * p.ny_entries + p.W1 + 1u + 2u * p.nx_entries);
+    int static_smem = 0;
+    {
+        cudaFuncAttributes fa{};
+        if (cudaFuncGetAttributes(&fa, sp::k_encode) == cudaSuccess) static_smem = static_cast<int>(fa.sharedSizeBytes);
+    }
     uint32_t best_rows = 0, best_stages = 0, best_cps = 0, best_stage_bytes = 0;
     std::vector<uint32_t> sy0, sn;
     for (uint32_t rows = 1; rows <= p.H1; ++rows) {
@@ -388,16 +449,16 @@ sp_status sp_encoder_create(const sp_encoder_config* cfg, sp_encoder** out) {
             maxn = std::max(maxn, hi - lo + 1u);
         }
         const uint32_t stage = (maxn * p.row_bytes + 127u) & ~127u;
-        if (rows > 1 && stage > 32768u) break;
+        if (rows > 1 && stage > 49152u) break;
         for (uint32_t stages = sp::kMaxStages; stages >= 2; --stages) {
-            const uint32_t smem = gray_bytes + stages * stage;
-            if (static_cast<int>(smem) > max_smem - 1024) continue;
-            const uint32_t cps = std::min<uint32_t>(2u, static_cast<uint32_t>(sm_smem / (smem + 1024u)));
-            // prefer 2 CTAs per SM, then more bytes in flight per SM
-            if (cps > best_cps || (cps == best_cps && cps * stages * stage > best_cps * best_stages * best_stage_bytes)) {
-                best_rows = rows, best_stages = stages, best_cps = cps, best_stage_bytes = stage;
-            }
-            break;
+            const uint32_t smem = gray_bytes + stages * stage + p.table_bytes;
+            if (static_cast<int>(smem) > max_smem - static_smem) continue;
+            const uint32_t cps = std::min<uint32_t>(2u, static_cast<uint32_t>(sm_smem) /
+                                                            (smem + static_smem + 1024u));
+            if (cps == 0) continue;
+            const bool better = cps > best_cps || (cps == best_cps && (rows > best_rows ||
+                                                                         (rows == best_rows && stages > best_stages)));
+            if (better) best_rows = rows, best_stages = stages, best_cps = cps, best_stage_bytes = stage;
         }
     }
     if (!best_rows) {
@@ -408,7 +469,7 @@ sp_status sp_encoder_create(const sp_encoder_config* cfg, sp_encoder** out) {
     p.stages = best_stages;
     p.stage_bytes = best_stage_bytes;
     e->ctas_per_sm = std::max<uint32_t>(1u, best_cps);
-    e->smem = gray_bytes + p.stages * p.stage_bytes;
+    e->smem = gray_bytes + p.stages * p.stage_bytes + p.table_bytes;
     p.bands = (p.H1 + p.band_rows - 1u) / p.band_rows;
     for (uint32_t b = 0; b < p.bands; ++b) {
         const uint32_t d0 = b * p.band_rows, d1 = std::min(p.H1, d0 + p.band_rows);
@@ -421,6 +482,8 @@ sp_status sp_encoder_create(const sp_encoder_config* cfg, sp_encoder** out) {
         u32.insert(u32.end(), v.begin(), v.end());
         return o;
     };
+    if (p.xfast)
+        for (float& bta : ybeta) bta *= 0.25f;  // beta/4 is exact (R23 fast path)
     const size_t o_sy0 = put(sy0), o_sn = put(sn), o_yoff = put(yoff), o_ysy = put(ysy), o_xoff = put(xoff),
                  o_xsx = put(xsx);
     std::vector<float> f32(ybeta);
