@@ -163,3 +163,23 @@ def test_learning_state_validation():
     with pytest.raises(P.SpError) as e:
         P.SpatialPooler(**gpu_kwargs(cfg, flags=P.SP_FLAG_FULL_LEARNING, max_boost=16.0))
     assert e.value.status == P.SP_E_CONFIG
+
+
+@pytest.mark.parametrize("path", LEARN_PATHS)
+def test_full_learning_full_size(path):
+    # BASELINE config 2 sizes (960x540, 1024 columns, 256 synapses, min_overlap 4, k 40) with
+    # Tab. 2's radius 80 adapted, seeded duty cycles so boosts and bumps act from the start
+    cfg = ocfg(full_learning=True, input_width=960, input_height=540, num_columns=1024,
+               synapses_per_column=256, min_overlap=4, winners_set_size=40, inhibition_radius=80,
+               duty_cycle_period=50)
+    state = perturbed_state(cfg)
+    frames = sp_inputs.frames(1001, 0, 5, 540, 960, rho=0.5)
+    ora = O.SpatialPoolerOracle(cfg, state)
+    adc, odc = seeded_duty(31, 1024), seeded_duty(32, 1024)
+    ora.active_duty, ora.overlap_duty = adc.copy(), odc.copy()
+    results = ora.compute(frames, learning=True)
+    sp = make_sp(cfg, state, path, max_inputs=8)
+    sp.set_learning_state(adc, odc, 80)
+    check_inputs(results, *run(sp, frames, True))
+    check_path(sp, path)
+    check_state(sp, ora)
