@@ -300,12 +300,13 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
         if (radius > 0 && p.ncw * 16u <= 1024u && NW <= 16u) {
             // local inhibition, per-column boosts: coarse bit-sliced + exact ties
             uint32_t* planes = reinterpret_cast<uint32_t*>(region) + wi * 1024u;  // [ncw][16]
-            build_coarse_planes(row, s_bc, planes, p.ncw, theta, sh, 0u, 1u, lane);
+            const CoarseMap cm = coarse_map_warp(row, s_bc, theta, 0u, p.ncw, lane);
+            build_coarse_planes15(row, s_bc, planes, p.ncw, theta, cm, 0u, 1u, lane);
             __syncwarp();
             uint32_t total = 0, myword = 0;
             for (uint32_t cw = 0; cw < p.ncw; ++cw) {
-                const uint32_t word = local_general_word(row, s_bc, planes, p.ncw, cw, p.C, radius,
-                                                         p.k, theta, sh, L, lane);
+                const uint32_t word = local_general_word15(row, s_bc, planes, p.ncw, cw, p.C, radius,
+                                                           p.k, theta, cm, L, lane);
                 if ((cw & 31u) == lane) myword = word;
                 total += __popc(word);
                 if ((cw & 31u) == 31u || cw + 1u == p.ncw) {

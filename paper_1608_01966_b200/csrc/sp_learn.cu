@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
     unsigned long long* s_spanpart =
         reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(s_span + cpc) + 7u) & ~uintptr_t(7));  // [Q]
     __shared__ unsigned long long s_myspan;
+    __shared__ unsigned long long s_mm[2];  // eligible-N range of the coarse map
     auto bits_of = [&](uint32_t t) { return s_bits + (p.dbl_bits ? (t & 1u) * Wn4 : 0u); };
     auto gbits_of = [&](uint32_t t) { return p.bits_g + (t & 1u) * Wn4; };
 
@@ -219,17 +220,21 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
             const bool uni = p.uniform_bc != 0u;
             const uint32_t r_lo = uniform_r_lo(theta, s_bc[0]);
             const uint32_t rb = raw_bits(g.S);
-            const uint32_t sh = g.keyBits - L - 16u;
-            if (uni) build_raw_planes(raw_t, s_planes, g.ncw, rb, r_lo, wi, nw, lane);
-            else build_coarse_planes(raw_t, s_bc, s_planes, g.ncw, theta, sh, wi, nw, lane);
+            CoarseMap cm{0ull, 0u};
+            if (uni) {
+                build_raw_planes(raw_t, s_planes, g.ncw, rb, r_lo, wi, nw, lane);
+            } else {
+                cm = coarse_map_block(raw_t, s_bc, theta, 0u, g.ncw, s_mm);
+                build_coarse_planes15(raw_t, s_bc, s_planes, g.ncw, theta, cm, wi, nw, lane);
+            }
             __syncthreads();
             for (uint32_t cw = wi; cw < ncl; cw += nw) {
                 const uint32_t gcw = c0 / 32u + cw;
                 uint32_t word = 0u;
                 if (gcw < g.ncw)
                     word = uni ? local_uniform_word(raw_t, s_planes, g.ncw, rb, gcw, g.C, R, p.k, r_lo, lane)
-                               : local_general_word(raw_t, s_bc, s_planes, g.ncw, gcw, g.C, R, p.k, theta,
-                                                    sh, L, lane);
+                               : local_general_word15(raw_t, s_bc, s_planes, g.ncw, gcw, g.C, R, p.k, theta,
+                                                      cm, L, lane);
                 emit_word(p, s_sdr, cw, gcw, gin, word, lane);
             }
         } else {

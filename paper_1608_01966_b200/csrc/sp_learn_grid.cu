@@ -65,6 +65,7 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t b
 
 __global__ void __launch_bounds__(kGridThreads, 1) sp_learn_grid_kernel(const __grid_constant__ LearnGridParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
+    __shared__ unsigned long long s_mm[2];  // eligible-N range of the coarse map
     __shared__ __align__(8) uint64_t s_bar_bits;
     __shared__ __align__(8) uint64_t s_bar_ring[8];
     const Geometry& g = p.g;
@@ -229,16 +230,20 @@ __global__ void __launch_bounds__(kGridThreads, 1) sp_learn_grid_kernel(const __
             const bool uni = p.uniform_bc != 0u;
             const uint32_t r_lo = uniform_r_lo(theta, uni ? p.bc[0] : 1u);
             const uint32_t nb = raw_bits(S);
-            const uint32_t sh = g.keyBits - L - 16u;
             uint32_t* planes = s_planes - jlo * (uni ? nb : 16u);
-            if (uni) build_raw_planes(row, planes, jhi + 1u, nb, r_lo, jlo + wi, nw, lane);
-            else build_coarse_planes(row, bcr, planes, jhi + 1u, theta, sh, jlo + wi, nw, lane);
+            CoarseMap cm{0ull, 0u};
+            if (uni) {
+                build_raw_planes(row, planes, jhi + 1u, nb, r_lo, jlo + wi, nw, lane);
+            } else {
+                cm = coarse_map_block(row, bcr, theta, jlo, jhi + 1u, s_mm);
+                build_coarse_planes15(row, bcr, planes, jhi + 1u, theta, cm, jlo + wi, nw, lane);
+            }
             __syncthreads();
             for (uint32_t cw = wi; cw < nown; cw += nw) {
                 const uint32_t gcw = wb0 + cw;
                 const uint32_t word =
                     uni ? local_uniform_word(row, planes, ncw, nb, gcw, g.C, R, p.k, r_lo, lane)
-                        : local_general_word(row, bcr, planes, ncw, gcw, g.C, R, p.k, theta, sh, L, lane);
+                        : local_general_word15(row, bcr, planes, ncw, gcw, g.C, R, p.k, theta, cm, L, lane);
                 if (lane == 0) {
                     s_sdr[cw] = word;
                     p.sdr[static_cast<size_t>(gin) * ncw + gcw] = word;

@@ -166,12 +166,13 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
         }
     } else if (radius > 0) {
         // local inhibition, per-column boosts: coarse bit-sliced + exact ties (sp_select.cuh)
-        const uint32_t sh = g.keyBits - L - 16u;
-        build_coarse_planes(s_raw, s_bc, s_planes, g.ncw, theta, sh, tid >> 5, nthr >> 5, tid & 31u);
+        __shared__ unsigned long long s_mm[2];
+        const CoarseMap cm = coarse_map_block(s_raw, s_bc, theta, 0u, g.ncw, s_mm);
+        build_coarse_planes15(s_raw, s_bc, s_planes, g.ncw, theta, cm, tid >> 5, nthr >> 5, tid & 31u);
         __syncthreads();
         for (uint32_t cw = tid >> 5; cw < g.ncw; cw += nthr >> 5) {
-            const uint32_t word = local_general_word(s_raw, s_bc, s_planes, g.ncw, cw, g.C, radius, p.k,
-                                                     theta, sh, L, tid & 31u);
+            const uint32_t word = local_general_word15(s_raw, s_bc, s_planes, g.ncw, cw, g.C, radius, p.k,
+                                                       theta, cm, L, tid & 31u);
             if ((tid & 31u) == 0) {
                 p.sdr[static_cast<size_t>(gin) * g.ncw + cw] = word;
                 my_total += __popc(word);

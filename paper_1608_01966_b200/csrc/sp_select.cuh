@@ -174,6 +174,158 @@ __device__ __forceinline__ uint32_t local_general_word(const RowT* row, const ui
     return __ballot_sync(0xffffffffu, c < Cn && u > 0u && beats < k);
 }
 
+// ---- local inhibition, per-column boosts, with a per-input coarse map ---------------------
+// The coarse key is only an accelerator: exactness comes from the exact comparison of the
+// columns whose coarse keys tie.  Mapping the eligible N onto 15 bits relative to the input's
+// own range [Nmin, Nmax] (instead of a fixed shift) makes coarse ties rare, and a "lossless"
+// flag (the dropped low bits are zero) resolves the common remaining case, equal N, by index
+// alone (d beats c iff d < c): exact keys are compared only for ties involving a lossy column.
+struct CoarseMap {
+    uint64_t nlo;  // smallest eligible N
+    uint32_t sh;   // right shift of N - nlo, so that u - 1 < 2^15
+};
+
+__device__ __forceinline__ CoarseMap coarse_map(uint64_t nmin, uint64_t nmax) {
+    CoarseMap m{0ull, 0u};
+    if (nmin > nmax) return m;  // no eligible column
+    m.nlo = nmin;
+    const uint64_t range = nmax - nmin;
+    while ((range >> m.sh) > 32766ull) ++m.sh;
+    return m;
+}
+
+// N of column c if it passes the cutoff and the floor (N > 2^23), else 0
+__device__ __forceinline__ uint64_t eligible_N(uint32_t raw, uint32_t bc, uint32_t theta) {
+    const uint64_t N = raw >= theta ? static_cast<uint64_t>(raw) * bc : 0ull;
+    return N > (1ull << 23) ? N : 0ull;
+}
+
+// u in [1, 2^15] for eligible columns (0 otherwise) and whether the map dropped nonzero bits
+__device__ __forceinline__ uint32_t coarse_u15(uint64_t N, const CoarseMap& m, bool& lossy) {
+    if (N == 0ull) {
+        lossy = false;
+        return 0u;
+    }
+    const uint64_t d = N - m.nlo;
+    lossy = (d & ((1ull << m.sh) - 1ull)) != 0ull;
+    return static_cast<uint32_t>(d >> m.sh) + 1u;
+}
+
+__device__ __forceinline__ void minmax64_warp(uint64_t& mn, uint64_t& mx) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        const uint64_t a = __shfl_xor_sync(0xffffffffu, mn, d), b = __shfl_xor_sync(0xffffffffu, mx, d);
+        mn = a < mn ? a : mn;
+        mx = b > mx ? b : mx;
+    }
+}
+
+// eligible-N range of words [w0, w1) by one warp (all lanes get the result)
+template <typename RowT>
+__device__ __forceinline__ CoarseMap coarse_map_warp(const RowT* row, const uint32_t* bc, uint32_t theta, uint32_t w0,
+                                                     uint32_t w1, uint32_t lane) {
+    uint64_t mn = ~0ull, mx = 0ull;
+    for (uint32_t cw = w0; cw < w1; ++cw) {
+        const uint32_t c = cw * 32u + lane;
+        const uint64_t N = eligible_N(row[c], bc[c], theta);
+        if (N) mn = N < mn ? N : mn, mx = N > mx ? N : mx;
+    }
+    minmax64_warp(mn, mx);
+    return coarse_map(mn, mx);
+}
+
+// the same by the threads [0, nthr) of a CTA; s_mm[2] is shared scratch.  Contains barriers.
+template <typename RowT>
+__device__ __forceinline__ CoarseMap coarse_map_block(const RowT* row, const uint32_t* bc, uint32_t theta, uint32_t w0,
+                                                      uint32_t w1, unsigned long long* s_mm) {
+    const uint32_t tid = threadIdx.x, nthr = blockDim.x;
+    if (tid == 0) s_mm[0] = ~0ull, s_mm[1] = 0ull;
+    __syncthreads();
+    uint64_t mn = ~0ull, mx = 0ull;
+    for (uint32_t c = w0 * 32u + tid; c < w1 * 32u; c += nthr) {
+        const uint64_t N = eligible_N(row[c], bc[c], theta);
+        if (N) mn = N < mn ? N : mn, mx = N > mx ? N : mx;
+    }
+    minmax64_warp(mn, mx);
+    if ((tid & 31u) == 0 && mn <= mx) {
+        atomicMin(&s_mm[0], static_cast<unsigned long long>(mn));
+        atomicMax(&s_mm[1], static_cast<unsigned long long>(mx));
+    }
+    __syncthreads();
+    return coarse_map(s_mm[0], s_mm[1]);
+}
+
+// planes[cw*16 + 0] = lossy flags, planes[cw*16 + 1 + b] = bit b of u (b < 15)
+template <typename RowT>
+__device__ __forceinline__ void build_coarse_planes15(const RowT* row, const uint32_t* bc, uint32_t* planes,
+                                                      uint32_t ncw, uint32_t theta, const CoarseMap& m,
+                                                      uint32_t cw0, uint32_t step, uint32_t lane) {
+    for (uint32_t cw = cw0; cw < ncw; cw += step) {
+        const uint32_t c = cw * 32u + lane;
+        bool lossy;
+        const uint32_t u = coarse_u15(eligible_N(row[c], bc[c], theta), m, lossy);
+        const uint32_t pl = __ballot_sync(0xffffffffu, lossy);
+        if (lane == 0) planes[cw * 16u] = pl;
+#pragma unroll
+        for (uint32_t b = 0; b < 15u; ++b) {
+            const uint32_t q = __ballot_sync(0xffffffffu, (u >> b) & 1u);
+            if (lane == b + 1u) planes[cw * 16u + 1u + b] = q;
+        }
+    }
+}
+
+// Winners of word cw (local inhibition, per-column boosts), all lanes of the warp call it.
+template <typename RowT>
+__device__ __forceinline__ uint32_t local_general_word15(const RowT* row, const uint32_t* bc,
+                                                         const uint32_t* planes, uint32_t ncw, uint32_t cw,
+                                                         uint32_t C, uint32_t radius, uint32_t k, uint32_t theta,
+                                                         const CoarseMap& m, uint32_t L, uint32_t lane) {
+    const int c = static_cast<int>(cw * 32u + lane);
+    uint64_t Nc;
+    const uint64_t keyc = exact_key(row[c], bc[c], theta, static_cast<uint32_t>(c), L, Nc);
+    bool lossy_c;
+    const uint32_t u = coarse_u15(Nc > (1ull << 23) ? Nc : 0ull, m, lossy_c);
+    const int R = static_cast<int>(radius), Cn = static_cast<int>(C);
+    const int lo = max(0, c - R), hi = min(Cn - 1, c + R);
+    const int jw0 = max(0, (static_cast<int>(cw) * 32 - R) / 32);
+    const int jw1 = min(static_cast<int>(ncw) - 1, (static_cast<int>(cw) * 32 + 31 + R) / 32);
+    uint32_t Xm[15];
+#pragma unroll
+    for (int b = 0; b < 15; ++b) Xm[b] = 0u - ((u >> b) & 1u);
+    uint32_t beats = 0;
+    for (int jw = jw0; jw <= jw1; ++jw) {
+        const uint32_t* P0 = planes + jw * 16;
+        uint32_t gt = 0u, eq = 0xFFFFFFFFu;
+#pragma unroll
+        for (int b = 14; b >= 0; --b) {
+            const uint32_t B = P0[1 + b], X = Xm[b];
+            gt |= eq & B & ~X;
+            eq &= ~(B ^ X);
+        }
+        const int base = jw * 32;
+        const int a = max(lo, base) - base, z = min(hi, base + 31) - base;
+        uint32_t wm = a <= z ? (0xFFFFFFFFu >> (31 - z)) & (0xFFFFFFFFu << a) : 0u;
+        const int self = c - base;
+        if (self >= 0 && self < 32) wm &= ~(1u << self);
+        beats += __popc(gt & wm);
+        if (u > 0u) {
+            const uint32_t ties = eq & wm;
+            uint32_t exact = lossy_c ? ties : (ties & P0[0]);  // pairs with a lossy column
+            uint32_t below = 0u;                                // bits d < c of this word
+            if (self >= 32) below = 0xFFFFFFFFu;
+            else if (self > 0) below = 0xFFFFFFFFu >> (32 - self);
+            beats += __popc(ties & ~exact & below);             // equal N: the lower index wins
+            while (exact) {
+                const int d = base + __ffs(exact) - 1;
+                exact &= exact - 1u;
+                uint64_t Nd;
+                beats += exact_key(row[d], bc[d], theta, static_cast<uint32_t>(d), L, Nd) > keyc ? 1u : 0u;
+            }
+        }
+    }
+    return __ballot_sync(0xffffffffu, c < Cn && u > 0u && beats < k);
+}
+
 // r_lo = smallest raw passing both the cutoff (raw >= theta) and the floor raw*Bc > 2^23.
 __device__ __forceinline__ uint32_t uniform_r_lo(uint32_t theta, uint32_t bc) {
     return max(theta, (1u << 23) / bc + 1u);
