@@ -44,6 +44,7 @@ constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
 constexpr int kDefaultSms = 148;
 constexpr int kDefaultSmem = 232448;   // B200 max dynamic smem per block (opt-in)
 constexpr uint32_t kMaxInputBits = 1800000u;
+constexpr uint32_t kPrepackInputs = 1024u;  // inputs per prepacked learning chunk
 
 inline uint64_t mix64(uint64_t z) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -345,6 +346,8 @@ struct sp_handle {
     uint32_t* d_span = nullptr;  // [C32] connected spans
     uint32_t* d_radius = nullptr;  // radius in force (device scalar)
     float* d_fscratch = nullptr;   // window-maximum tables of k_full
+    uint32_t* d_bits_all = nullptr;  // prepacked bit-planes of a learning chunk [inputs][Wn4]
+    uint32_t bits_all_cap = 0;       // capacity in inputs
     bool span_dirty = true;      // d_span must be recomputed before full learning
     uint64_t iteration = 0;      // SP inputs learned
     // per-video histograms (NEXT-4): offsets and count scratch, grown on demand
@@ -390,7 +393,8 @@ void release(sp_handle* h) {
                     h->d_ell,  h->d_ell_off, h->d_ell_nb,  h->d_ell_pos, h->d_bits,
                     h->d_raw,  h->d_sdr,     h->d_counts,  h->d_raw_rec, h->d_boosted_rec,
                     h->d_stage[0], h->d_stage[1], h->d_synT,  h->d_gbar, h->d_adc, h->d_odc,
-                    h->d_span, h->d_radius, h->d_fscratch, h->d_hist_off, h->d_hist_counts};
+                    h->d_span, h->d_radius, h->d_fscratch, h->d_hist_off, h->d_hist_counts,
+                    h->d_bits_all};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
@@ -747,9 +751,44 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         q.raw_out = rec ? h->d_raw_rec : nullptr;
         q.boosted_out = rec ? h->d_boosted_rec : nullptr;
         q.fl = full_learn_params(h);
-        e = sp::launch_learn_cluster(q, h->learn_smem, s);
-        h->launches++;
-        if (e != cudaSuccess) return cuda_fail(e, "cluster learning launch");
+        // the bit-planes do not depend on learning: k_pack packs a chunk of inputs ahead (an
+        // HBM-bound pass), and the cluster kernel only bulk-loads them (no packing on the
+        // sequential critical path).  Chunks bound the scratch; the state carries over.
+        const uint32_t Wn4 = (h->Wn + 3u) / 4u * 4u;
+        const bool prepack = !std::getenv("SP_NO_PREPACK");
+        const uint32_t fpc = prepack ? std::max<uint32_t>(1u, kPrepackInputs / g.P) : n_frames;
+        const uint32_t cap = std::min(fpc * g.P, std::max(h->cfg.max_inputs / g.P, 1u) * g.P);
+        if (prepack && h->bits_all_cap < std::min(fpc, n_frames) * g.P) {
+            // sized once for the largest chunk a call can have (allocation synchronises)
+            if (h->d_bits_all) cudaFree(h->d_bits_all), h->d_bits_all = nullptr;
+            e = dalloc(&h->d_bits_all, static_cast<size_t>(cap) * Wn4);
+            if (e != cudaSuccess) return fail(SP_E_OOM, "prepacked bit-planes: %s", cudaGetErrorString(e));
+            h->bits_all_cap = cap;
+        }
+        for (uint32_t f0 = 0; f0 < n_frames; f0 += fpc) {
+            const uint32_t nf = std::min(fpc, n_frames - f0);
+            sp::LearnParams qc = q;
+            qc.frames = frames + static_cast<size_t>(f0) * g.W * g.H;
+            qc.first_input = row0 + f0 * g.P;
+            qc.num_inputs = nf * g.P;
+            if (prepack) {
+                sp::PerInputParams pk{};
+                pk.frames = qc.frames;
+                pk.num_inputs = qc.num_inputs;
+                pk.g = g;
+                pk.bits = h->d_bits_all;
+                pk.Wn = h->Wn;
+                pk.bits_stride = Wn4;
+                e = sp::launch_pack(pk, s);
+                h->launches++;
+                if (e != cudaSuccess) return cuda_fail(e, "prepack launch");
+                qc.bits_g = h->d_bits_all;
+                qc.prepacked = 1u;
+            }
+            e = sp::launch_learn_cluster(qc, h->learn_smem, s);
+            h->launches++;
+            if (e != cudaSuccess) return cuda_fail(e, "cluster learning launch");
+        }
         h->ell_dirty = true;
         h->last_plan.path = SP_PATH_PER_INPUT;
         h->last_learn_cluster = true;

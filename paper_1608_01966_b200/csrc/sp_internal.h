@@ -99,8 +99,9 @@ struct PerInputParams {
     Geometry g;
     uint32_t min_overlap, k, radius;
     float inc, dec, tau;
-    uint32_t* bits;            // [num_inputs][Wn] packed input bits (scratch)
+    uint32_t* bits;            // [num_inputs][bits_stride] packed input bits (scratch)
     uint32_t Wn;
+    uint32_t bits_stride;      // words between planes (0: Wn)
     const uint32_t* syn;       // [S][C32] idx | connected << 31
     uint32_t* syn_rw;          // same, writable (learning)
     const uint32_t* idx;       // [C][S]
@@ -131,7 +132,9 @@ struct LearnParams {
     uint32_t* syn;             // [S][C32] idx | connected << 31 (loaded, written back)
     const uint32_t* bc;        // [C32]
     const float* boost;        // [C32]
-    uint32_t* bits_g;          // [2][Wn rounded to 4] scratch bit-planes (L2), by input parity
+    uint32_t* bits_g;          // [2][Wn rounded to 4] scratch bit-planes (L2), by input parity, or
+                               // [num_inputs][Wn rounded to 4] planes prepacked by k_pack
+    uint32_t prepacked;        // bits_g holds every input's plane (no packing in the kernel)
     uint32_t dbl_bits;         // two smem bit-plane buffers (load of t+1 overlaps learning of t)
     uint32_t dbg;              // development switches (SP_LEARN_DBG): 1 no proxy fence, 2 no prefetch,
                                // 4 no pack, 8 no selection (timing experiments only)

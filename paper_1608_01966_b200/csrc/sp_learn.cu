@@ -57,6 +57,17 @@ __device__ __forceinline__ void emit_word(const LearnParams& p, uint32_t* s_sdr,
 // to every CTA's raw buffer (DSMEM).  tpc consecutive lanes share a column (synapses
 // s = part, part+tpc, ..) with a shuffle reduction; the padded column-major slice keeps
 // the reads conflict-free
+// L2 prefetch ahead of use: the prepacked bit-plane of input t (CTA 0 only: every CTA reads the
+// whole plane), else this CTA's share of the frame bytes it will pack
+__device__ __forceinline__ void prefetch_plane_or_input(const LearnParams& p, uint32_t t, uint32_t wbeg, uint32_t wend,
+                                                        uint32_t q, uint32_t Q, const uint32_t* plane, uint32_t Wn4) {
+    if (!p.prepacked) {
+        prefetch_input(p, t, wbeg, wend, q, Q);
+        return;
+    }
+    if (q == 0 && t < p.num_inputs && !(p.dbg & 2u)) prefetch_l2(plane, Wn4 * 4u);
+}
+
 __device__ __forceinline__ void overlap_step(const LearnParams& p, cg::cluster_group& cluster, const uint32_t* s_syn,
                                              const uint32_t* bits, uint16_t* raw_buf, uint32_t c0, uint32_t gin,
                                              const uint32_t* s_bc) {
@@ -137,7 +148,9 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
     __shared__ unsigned long long s_myspan;
     __shared__ unsigned long long s_mm[2];  // eligible-N range of the coarse map
     auto bits_of = [&](uint32_t t) { return s_bits + (p.dbl_bits ? (t & 1u) * Wn4 : 0u); };
-    auto gbits_of = [&](uint32_t t) { return p.bits_g + (t & 1u) * Wn4; };
+    // bit-planes in global memory: prepacked by k_pack for the whole launch (p.prepacked), or
+    // packed by the CTAs themselves into two buffers by input parity
+    auto gbits_of = [&](uint32_t t) { return p.bits_g + (p.prepacked ? t : (t & 1u)) * Wn4; };
 
     // ---- resident state: this CTA's synapse slice, Bc; counts zeroed ---------------------
     for (uint32_t i = tid; i < g.S * cpc; i += nthr) {
@@ -186,9 +199,11 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
 
     // ---- prologue: bit-planes of inputs 0 and 1; overlap of input 0 ----------------------
     if (tid == 0)
-        for (uint32_t t = 0; t < 3u; ++t) prefetch_input(p, t, wbeg, wend, q, Q);
-    if (n > 0) pack_slice(p, 0, wbeg, wend, gbits_of(0), 0, nthr);
-    if (n > 1) pack_slice(p, 1, wbeg, wend, gbits_of(1), 0, nthr);
+        for (uint32_t t = 0; t < 3u; ++t) prefetch_plane_or_input(p, t, wbeg, wend, q, Q, gbits_of(t), Wn4);
+    if (!p.prepacked) {
+        if (n > 0) pack_slice(p, 0, wbeg, wend, gbits_of(0), 0, nthr);
+        if (n > 1) pack_slice(p, 1, wbeg, wend, gbits_of(1), 0, nthr);
+    }
     cluster.sync();  // bit-planes 0 (and 1) complete; smem and counts initialised
     if (n > 0) {
         if (tid == 0) bulk_load_bits(bits_of(0), gbits_of(0), Wn, &s_bar);
@@ -209,7 +224,7 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
         }
         if (trace) t_ph = globaltimer();
         if (tid == 0) {
-            prefetch_input(p, t + 3u, wbeg, wend, q, Q);
+            prefetch_plane_or_input(p, t + 3u, wbeg, wend, q, Q, gbits_of(t + 3u), Wn4);
             // bit-plane of t+1 (complete since the last barrier) into its smem buffer; with
             // one buffer it must wait until learning of t is done with the current plane
             if (more && p.dbl_bits && !(p.dbg & 16u)) bulk_load_bits(bits_of(t + 1u), gbits_of(t + 1u), Wn, &s_bar);
@@ -254,7 +269,8 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
         if (trace) t_sub += globaltimer() - t_ph;  // selection alone (warp 0)
         uint64_t tp0 = 0;
         if (trace_pk) tp0 = globaltimer();
-        if (t + 2u < n && !(p.dbg & 4u)) pack_slice(p, t + 2u, wbeg, wend, gbits_of(t + 2u), tpk0, npk);
+        if (!p.prepacked && t + 2u < n && !(p.dbg & 4u))
+            pack_slice(p, t + 2u, wbeg, wend, gbits_of(t + 2u), tpk0, npk);
         if (trace_pk) t_pk += globaltimer() - tp0;
         __syncthreads();  // s_sdr complete
         if (trace) {

@@ -48,7 +48,7 @@ __global__ void k_pack(const PerInputParams p) {
             out |= (v != 0 ? 1u : 0u) << j;
         }
     }
-    p.bits[static_cast<size_t>(t) * p.Wn + word] = out;
+    p.bits[static_cast<size_t>(t) * (p.bits_stride ? p.bits_stride : p.Wn) + word] = out;
 }
 
 // ---------------------------------------------------------------------------------------
