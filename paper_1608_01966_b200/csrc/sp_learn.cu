@@ -24,6 +24,8 @@
 // selection needs no exchange), bumps its own weak columns, and sends the sum of its columns'
 // connected spans to every CTA; the radius of input t+1 is formed after the overlap barrier.  Only the frame bytes and the winners' permanence rows touch memory
 // below L2.  DESIGN.md §4.2.
+#include <algorithm>
+
 #include <cooperative_groups.h>
 
 #include "sp_duty.cuh"
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
     // the whole input, own spans, per-CTA span sums
     const FullLearn& fl = p.fl;
     const uint32_t nb = g.C32 / 32u;
-    float* s_adc = reinterpret_cast<float*>(s_planes + g.ncw * 16u);  // [C32]
+    float* s_adc = reinterpret_cast<float*>(s_planes + max(g.ncw * 16u, 512u));  // [C32]
     float* s_odc = s_adc + g.C32;                                       // [C32]
     float* s_pre = s_odc + g.C32;                                       // [C32]
     float* s_suf = s_pre + g.C32;                                       // [C32]
@@ -250,6 +252,18 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
                     word = uni ? local_uniform_word(raw_t, s_planes, g.ncw, rb, gcw, g.C, R, p.k, r_lo, lane)
                                : local_general_word15(raw_t, s_bc, s_planes, g.ncw, gcw, g.C, R, p.k, theta,
                                                       cm, L, lane);
+                emit_word(p, s_sdr, cw, gcw, gin, word, lane);
+            }
+        } else if (p.prepacked && !p.uniform_bc && !(p.dbg & 64u)) {
+            // per-column boosts and no packing to overlap: the whole CTA selects (two-level
+            // radix select, sp_select.cuh) instead of one warp per owned word
+            const CoarseMap cm = coarse_map_block(raw_t, s_bc, theta, 0u, g.ncw, s_mm);
+            const GlobalSel gs = global_select_cta(raw_t, s_bc, theta, g.C, g.ncw, p.k, L, g.keyBits, cm, s_planes,
+                                                   s_ties, ncl * 64u);
+            for (uint32_t cw = wi; cw < ncl; cw += nw) {
+                const uint32_t gcw = c0 / 32u + cw;
+                uint32_t word = 0u;
+                if (gcw < g.ncw) word = global_select_word(raw_t, s_bc, theta, g.C, gcw, L, cm, gs, s_planes, g.ncw, lane);
                 emit_word(p, s_sdr, cw, gcw, gin, word, lane);
             }
         } else {
@@ -455,8 +469,8 @@ uint32_t learn_cluster_smem(const Geometry& g, uint32_t Q, uint32_t* cols_per_ct
     const uint32_t nb = g.C32 / 32u;
     const uint32_t full_bytes = full ? 4u * (4u * g.C32 + wmax_levels(nb) * nb + g.ncw + cpc) + 8u + 8u * Q : 0u;
     return 4u * (learn_syn_stride(g.S) * cpc + (dbl_bits ? 2u : 1u) * Wn4 + g.C32) +
-           4u * ((g.C32 + 3u) / 4u * 4u) + 8u * (cpc / 32u * 64u) + 4u * (cpc / 32u) + 4u * (g.ncw * 16u) +
-           full_bytes;
+           4u * ((g.C32 + 3u) / 4u * 4u) + 8u * (cpc / 32u * 64u) + 4u * (cpc / 32u) +
+           4u * std::max(g.ncw * 16u, 512u) + full_bytes;
 }
 
 cudaError_t configure_learn(int max_smem) {

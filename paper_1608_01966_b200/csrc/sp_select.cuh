@@ -326,6 +326,196 @@ __device__ __forceinline__ uint32_t local_general_word15(const RowT* row, const 
     return __ballot_sync(0xffffffffu, c < Cn && u > 0u && beats < k);
 }
 
+// ---- global inhibition by a whole CTA (cluster learning) ---------------------------------
+// Exact k-winners over all C columns (R4-R7): a two-level radix select of the k-th largest
+// 15-bit coarse key u (histograms of (u-1) >> 7, then of (u-1) & 127 inside the bucket, shared
+// atomics), then the columns tied at the threshold Tu: if none of them is lossy they all have
+// the same N and the lowest indices win (a prefix count over the tie masks); otherwise the
+// need-th largest exact key T2 among them is found (a tie list, or a bitwise search with CTA
+// counts when the list overflows).  Every thread of the CTA must call it (barriers).
+// scratch: >= 400 + 2*ncw + 1 words; ties: tie_cap keys.
+struct GlobalSel {
+    uint32_t Tu;     // coarse threshold (0: fewer than k eligible columns, all eligible win)
+    uint32_t need;   // winners among the columns with u == Tu
+    uint32_t exact;  // 1: decide the tied columns by exact key >= T2, 0: by index rank
+    uint64_t T2;
+};
+
+template <typename RowT>
+__device__ __forceinline__ GlobalSel global_select_cta(const RowT* row, const uint32_t* bc, uint32_t theta, uint32_t C,
+                                                       uint32_t ncw, uint32_t k, uint32_t L, uint32_t keyBits,
+                                                       const CoarseMap& m, uint32_t* scratch, uint64_t* ties,
+                                                       uint32_t tie_cap) {
+    const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u, wi = tid >> 5, nw = nthr >> 5;
+    uint32_t* h1 = scratch;            // [256]
+    uint32_t* h2 = scratch + 256;      // [128]
+    uint32_t* misc = scratch + 384;    // [16]
+    uint32_t* tmask = scratch + 400;   // [ncw]
+    uint32_t* tscan = tmask + ncw;     // [ncw + 1]
+    for (uint32_t i = tid; i < 400u; i += nthr) scratch[i] = 0u;
+    __syncthreads();
+    for (uint32_t c = tid; c < C; c += nthr) {
+        bool lossy;
+        const uint32_t u = coarse_u15(eligible_N(row[c], bc[c], theta), m, lossy);
+        if (u) atomicAdd(&h1[(u - 1u) >> 7], 1u);
+    }
+    __syncthreads();
+    if (wi == 0) {  // bucket of the k-th largest: suffix counts from the top, 8 bins per lane
+        uint32_t v[8], sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = h1[lane * 8u + j], sum += v[j];
+        uint32_t above = sum;  // inclusive suffix over lanes >= lane
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_down_sync(0xffffffffu, above, d);
+            if (lane + d < 32u) above += o;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, above, 0);
+        // bin b = 8*lane + j: count of bins > b = (above - sum) + sum of v[j+1..7]
+        uint32_t hi_above = above - sum, found = 0xFFFFFFFFu, f_above = 0;
+#pragma unroll
+        for (int j = 7; j >= 0; --j) {
+            if (found == 0xFFFFFFFFu && hi_above < k && hi_above + v[j] >= k) found = lane * 8u + j, f_above = hi_above;
+            hi_above += v[j];
+        }
+        const uint32_t who = __ballot_sync(0xffffffffu, found != 0xFFFFFFFFu);
+        if (lane == 0) misc[0] = total;
+        if (who && lane == static_cast<uint32_t>(__ffs(who) - 1)) misc[1] = found, misc[2] = f_above;
+    }
+    __syncthreads();
+    GlobalSel r{0u, 0u, 0u, 0ull};
+    if (misc[0] < k) return r;  // fewer than k eligible: all of them win (Tu = 0)
+    const uint32_t B1 = misc[1], above1 = misc[2];
+    for (uint32_t c = tid; c < C; c += nthr) {
+        bool lossy;
+        const uint32_t u = coarse_u15(eligible_N(row[c], bc[c], theta), m, lossy);
+        if (u && ((u - 1u) >> 7) == B1) atomicAdd(&h2[(u - 1u) & 127u], 1u);
+    }
+    __syncthreads();
+    if (wi == 0) {
+        const uint32_t kk = k - above1;
+        uint32_t v[4], sum = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = h2[lane * 4u + j], sum += v[j];
+        uint32_t above = sum;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_down_sync(0xffffffffu, above, d);
+            if (lane + d < 32u) above += o;
+        }
+        uint32_t hi_above = above - sum, found = 0xFFFFFFFFu, f_above = 0;
+#pragma unroll
+        for (int j = 3; j >= 0; --j) {
+            if (found == 0xFFFFFFFFu && hi_above < kk && hi_above + v[j] >= kk) found = lane * 4u + j, f_above = hi_above;
+            hi_above += v[j];
+        }
+        const uint32_t who = __ballot_sync(0xffffffffu, found != 0xFFFFFFFFu);
+        if (who && lane == static_cast<uint32_t>(__ffs(who) - 1)) {
+            misc[3] = ((B1 << 7) | found) + 1u;  // Tu
+            misc[4] = kk - f_above;              // need (>= 1)
+        }
+        if (lane == 0) misc[5] = 0u, misc[6] = 0u;  // lossy-tie flag, tie count
+    }
+    __syncthreads();
+    r.Tu = misc[3];
+    r.need = misc[4];
+    // the columns tied at Tu: masks per word, lossy flag, and their exact keys (list)
+    for (uint32_t cw = wi; cw < ncw; cw += nw) {
+        const uint32_t c = cw * 32u + lane;
+        bool lossy = false;
+        uint64_t N = 0;
+        const uint64_t key = c < C ? exact_key(row[c], bc[c], theta, c, L, N) : 0ull;
+        const uint32_t u = c < C ? coarse_u15(N > (1ull << 23) ? N : 0ull, m, lossy) : 0u;
+        const bool tied = u == r.Tu;
+        const uint32_t tm = __ballot_sync(0xffffffffu, tied);
+        if (lane == 0) tmask[cw] = tm;
+        if (__any_sync(0xffffffffu, tied && lossy) && lane == 0) atomicOr(&misc[5], 1u);
+        if (tied) {
+            const uint32_t pos = atomicAdd(&misc[6], 1u);
+            if (pos < tie_cap) ties[pos] = key;
+        }
+    }
+    __syncthreads();
+    r.exact = misc[5];
+    if (!r.exact) {
+        if (wi == 0) {  // exclusive scan of the tie counts per word
+            uint32_t carry = 0;
+            for (uint32_t base = 0; base < ncw; base += 32u) {
+                const uint32_t cw = base + lane;
+                const uint32_t v = cw < ncw ? __popc(tmask[cw]) : 0u;
+                uint32_t x = v;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t o = __shfl_up_sync(0xffffffffu, x, d);
+                    if (lane >= static_cast<uint32_t>(d)) x += o;
+                }
+                if (cw < ncw) tscan[cw] = carry + x - v;
+                carry += __shfl_sync(0xffffffffu, x, 31);
+            }
+        }
+        __syncthreads();
+        return r;
+    }
+    const uint32_t nt = misc[6];
+    if (nt <= tie_cap) {
+        // T2 = the need-th largest tied key: the one with exactly need-1 larger ones (distinct)
+        for (uint32_t i = tid; i < nt; i += nthr) {
+            const uint64_t ki = ties[i];
+            uint32_t g = 0;
+            for (uint32_t j = 0; j < nt; ++j) g += ties[j] > ki ? 1u : 0u;
+            if (g + 1u == r.need) misc[8] = static_cast<uint32_t>(ki), misc[9] = static_cast<uint32_t>(ki >> 32);
+        }
+    } else {
+        // bitwise search over the tied columns in place, CTA counts (rare: many lossy ties)
+        uint64_t T2 = 0;
+        for (int bit = static_cast<int>(keyBits) - 1; bit >= 0; --bit) {
+            const uint64_t cand = T2 | (1ull << bit);
+            uint32_t cnt = 0;
+            for (uint32_t c = tid; c < C; c += nthr) {
+                if (!((tmask[c >> 5] >> (c & 31u)) & 1u)) continue;
+                uint64_t N;
+                cnt += exact_key(row[c], bc[c], theta, c, L, N) >= cand ? 1u : 0u;
+            }
+            cnt = __reduce_add_sync(0xffffffffu, cnt);
+            if (tid == 0) misc[10] = 0u;
+            __syncthreads();
+            if (lane == 0 && cnt) atomicAdd(&misc[10], cnt);
+            __syncthreads();
+            if (misc[10] >= r.need) T2 = cand;
+            __syncthreads();
+        }
+        if (tid == 0) misc[8] = static_cast<uint32_t>(T2), misc[9] = static_cast<uint32_t>(T2 >> 32);
+    }
+    __syncthreads();
+    r.T2 = (static_cast<uint64_t>(misc[9]) << 32) | misc[8];
+    return r;
+}
+
+// SDR word cw from a GlobalSel (all lanes of a warp call it)
+template <typename RowT>
+__device__ __forceinline__ uint32_t global_select_word(const RowT* row, const uint32_t* bc, uint32_t theta, uint32_t C,
+                                                       uint32_t cw, uint32_t L, const CoarseMap& m, const GlobalSel& r,
+                                                       const uint32_t* scratch, uint32_t ncw, uint32_t lane) {
+    const uint32_t c = cw * 32u + lane;
+    uint64_t N = 0;
+    const uint64_t key = c < C ? exact_key(row[c], bc[c], theta, c, L, N) : 0ull;
+    bool lossy;
+    const uint32_t u = c < C ? coarse_u15(N > (1ull << 23) ? N : 0ull, m, lossy) : 0u;
+    bool win;
+    if (r.Tu == 0u) {
+        win = u > 0u;
+    } else if (u != r.Tu) {
+        win = u > r.Tu;
+    } else if (r.exact) {
+        win = key >= r.T2;
+    } else {
+        const uint32_t* tmask = scratch + 400;
+        const uint32_t* tscan = tmask + ncw;
+        win = tscan[cw] + __popc(tmask[cw] & ((1u << lane) - 1u)) < r.need;
+    }
+    return __ballot_sync(0xffffffffu, c < C && win);
+}
+
 // r_lo = smallest raw passing both the cutoff (raw >= theta) and the floor raw*Bc > 2^23.
 __device__ __forceinline__ uint32_t uniform_r_lo(uint32_t theta, uint32_t bc) {
     return max(theta, (1u << 23) / bc + 1u);
