@@ -101,6 +101,31 @@ __device__ __forceinline__ float wmax_query(const float* v, const float* pre, co
     return m;
 }
 
+// Maxima of a[0..C) and b[0..C) (values >= 0) over the whole CTA, for windows that cover all
+// columns (radius 0 or >= C-1): one reduction instead of the window tables.  s_red >= 64
+// floats of shared scratch; every thread of the CTA calls it and gets both maxima.
+__device__ __forceinline__ void block_max2(const float* a, const float* b, uint32_t C, float* s_red, float& ma,
+                                           float& mb) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, wi = tid >> 5, nw = blockDim.x >> 5;
+    float x = 0.0f, y = 0.0f;
+    for (uint32_t c = tid; c < C; c += blockDim.x) x = fmaxf(x, a[c]), y = fmaxf(y, b[c]);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, d));
+        y = fmaxf(y, __shfl_xor_sync(0xffffffffu, y, d));
+    }
+    if (lane == 0) s_red[wi] = x, s_red[32 + wi] = y;
+    __syncthreads();
+    x = lane < nw ? s_red[lane] : 0.0f;
+    y = lane < nw ? s_red[32 + lane] : 0.0f;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, d));
+        y = fmaxf(y, __shfl_xor_sync(0xffffffffu, y, d));
+    }
+    ma = x, mb = y;
+}
+
 // span of a column from its connected synapses: lanes hold (connected, s) pairs; returns
 // max - min + 1 of idx over the connected ones, 0 if none (warp-collective; idx ascending)
 __device__ __forceinline__ void span_accumulate(bool conn, uint32_t s, uint32_t& smin, uint32_t& smax) {

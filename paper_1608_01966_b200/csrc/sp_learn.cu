@@ -244,15 +244,49 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
                 cm = coarse_map_block(raw_t, s_bc, theta, 0u, g.ncw, s_mm);
                 build_coarse_planes15(raw_t, s_bc, s_planes, g.ncw, theta, cm, wi, nw, lane);
             }
+            const uint32_t parts = nw / ncl;  // warps per owned word (its window split between them)
+            uint32_t* s_beats = reinterpret_cast<uint32_t*>(s_ties);  // [ncl][32]
+            if (parts > 1u)
+                for (uint32_t i = tid; i < ncl * 32u; i += nthr) s_beats[i] = 0u;
             __syncthreads();
-            for (uint32_t cw = wi; cw < ncl; cw += nw) {
-                const uint32_t gcw = c0 / 32u + cw;
-                uint32_t word = 0u;
-                if (gcw < g.ncw)
-                    word = uni ? local_uniform_word(raw_t, s_planes, g.ncw, rb, gcw, g.C, R, p.k, r_lo, lane)
-                               : local_general_word15(raw_t, s_bc, s_planes, g.ncw, gcw, g.C, R, p.k, theta,
-                                                      cm, L, lane);
-                emit_word(p, s_sdr, cw, gcw, gin, word, lane);
+            if (parts > 1u && !(p.dbg & 128u)) {
+                if (wi < ncl * parts) {
+                    const uint32_t cw = wi % ncl, part = wi / ncl, gcw = c0 / 32u + cw;
+                    if (gcw < g.ncw) {
+                        uint32_t v;
+                        const uint32_t b =
+                            uni ? local_uniform_beats_part(raw_t, s_planes, g.ncw, rb, gcw, g.C, R, r_lo, lane, part,
+                                                           parts, v)
+                                : local_general_beats15(raw_t, s_bc, s_planes, g.ncw, gcw, g.C, R, theta, cm, L, lane,
+                                                        part, parts, v);
+                        if (b) atomicAdd(&s_beats[cw * 32u + lane], b);
+                    }
+                }
+                __syncthreads();
+                for (uint32_t cw = wi; cw < ncl; cw += nw) {
+                    const uint32_t gcw = c0 / 32u + cw, c = gcw * 32u + lane;
+                    bool elig = false;
+                    if (gcw < g.ncw && c < g.C) {
+                        if (uni) {
+                            elig = raw_t[c] >= r_lo;
+                        } else {
+                            bool lossy;
+                            elig = coarse_u15(eligible_N(raw_t[c], s_bc[c], theta), cm, lossy) > 0u;
+                        }
+                    }
+                    const uint32_t word = __ballot_sync(0xffffffffu, elig && s_beats[cw * 32u + lane] < p.k);
+                    emit_word(p, s_sdr, cw, gcw, gin, word, lane);
+                }
+            } else {
+                for (uint32_t cw = wi; cw < ncl; cw += nw) {
+                    const uint32_t gcw = c0 / 32u + cw;
+                    uint32_t word = 0u;
+                    if (gcw < g.ncw)
+                        word = uni ? local_uniform_word(raw_t, s_planes, g.ncw, rb, gcw, g.C, R, p.k, r_lo, lane)
+                                   : local_general_word15(raw_t, s_bc, s_planes, g.ncw, gcw, g.C, R, p.k, theta,
+                                                          cm, L, lane);
+                    emit_word(p, s_sdr, cw, gcw, gin, word, lane);
+                }
             }
         } else if (p.prepacked && !p.uniform_bc && !(p.dbg & 64u)) {
             // per-column boosts and no packing to overlap: the whole CTA selects (two-level
@@ -351,18 +385,26 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
             }
             __syncthreads();
             auto sync = [] { __syncthreads(); };
-            // (c) boosts of every column (replicated): the keys of input t+1
-            wmax_build(s_adc, g.C, g.C32, s_pre, s_suf, s_table, 0u, nthr, sync);
+            // (c) boosts of every column (replicated): the keys of input t+1.  A window that
+            // covers every column (radius 0 or >= C-1) needs only the two maxima.
+            const bool gwin = R == 0u || R + 1u >= g.C;
+            float gA = 0.0f, gO = 0.0f;
+            if (gwin) {
+                block_max2(s_adc, s_odc, g.C, s_pre, gA, gO);
+            } else {
+                wmax_build(s_adc, g.C, g.C32, s_pre, s_suf, s_table, 0u, nthr, sync);
+            }
             for (uint32_t c = tid; c < g.C; c += nthr)
-                s_bc[c] = boost_bc(boost_rule(s_adc[c], wmax_query(s_adc, s_pre, s_suf, s_table, nb, g.C, c, R),
-                                              fl.mb1));
+                s_bc[c] = boost_bc(boost_rule(
+                    s_adc[c], gwin ? gA : wmax_query(s_adc, s_pre, s_suf, s_table, nb, g.C, c, R), fl.mb1));
             __syncthreads();
             // (d) bump of this CTA's weak columns, warp per column
-            wmax_build(s_odc, g.C, g.C32, s_pre, s_suf, s_table, 0u, nthr, sync);
+            if (!gwin) wmax_build(s_odc, g.C, g.C32, s_pre, s_suf, s_table, 0u, nthr, sync);
             for (uint32_t cl = wi; cl < cpc; cl += nw) {
                 const uint32_t c = c0 + cl;
                 if (c >= g.C) break;
-                if (!weak_column(s_odc[c], wmax_query(s_odc, s_pre, s_suf, s_table, nb, g.C, c, R))) continue;
+                if (!weak_column(s_odc[c], gwin ? gO : wmax_query(s_odc, s_pre, s_suf, s_table, nb, g.C, c, R)))
+                    continue;
                 float* __restrict__ perm = p.perm + static_cast<size_t>(c) * g.S;
                 uint32_t* col = s_syn + cl * ss;
                 uint32_t smin = 0xFFFFFFFFu, smax = 0u;

@@ -97,6 +97,41 @@ __device__ __forceinline__ uint32_t local_uniform_word(const RowT* row, const ui
     return __ballot_sync(0xffffffffu, c < Cn && x > 0u && beats < k);
 }
 
+// Beats of lane's column of word cw counted over the neighbour words jw0+part, jw0+part+parts,
+// .. only (several warps share one word's window); x_out = the column's value (0: ineligible)
+template <typename RowT>
+__device__ __forceinline__ uint32_t local_uniform_beats_part(const RowT* row, const uint32_t* planes, uint32_t ncw,
+                                                             uint32_t nb, uint32_t cw, uint32_t C, uint32_t radius,
+                                                             uint32_t r_lo, uint32_t lane, uint32_t part,
+                                                             uint32_t parts, uint32_t& x_out) {
+    const int c = static_cast<int>(cw * 32u + lane);
+    uint32_t x = row[c];
+    x = x >= r_lo ? x : 0u;
+    x_out = c < static_cast<int>(C) ? x : 0u;
+    const int R = static_cast<int>(radius), Cn = static_cast<int>(C);
+    const int lo = max(0, c - R), hi = min(Cn - 1, c + R);
+    const int jw0 = max(0, (static_cast<int>(cw) * 32 - R) / 32);
+    const int jw1 = min(static_cast<int>(ncw) - 1, (static_cast<int>(cw) * 32 + 31 + R) / 32);
+    uint32_t Xm[10];
+#pragma unroll
+    for (int b = 0; b < 10; ++b) Xm[b] = 0u - ((x >> b) & 1u);
+    uint32_t beats = 0;
+    for (int jw = jw0 + static_cast<int>(part); jw <= jw1; jw += static_cast<int>(parts)) {
+        const uint32_t* P0 = planes + jw * nb;
+        uint32_t gt0 = 0u, eq0 = 0xFFFFFFFFu;
+#pragma unroll
+        for (int b = 9; b >= 0; --b) {
+            if (b < static_cast<int>(nb)) {
+                const uint32_t B0 = P0[b], X = Xm[b];
+                gt0 |= eq0 & B0 & ~X;
+                eq0 &= ~(B0 ^ X);
+            }
+        }
+        beats += window_beats(jw, c, lo, hi, gt0, eq0);
+    }
+    return beats;
+}
+
 // ---- general boosts ---------------------------------------------------------------------
 // Exact rank key (R4, R6): N = raw*Bc (exact), key = N << L | (2^L-1-c).
 __device__ __forceinline__ uint64_t exact_key(uint32_t raw, uint32_t bc, uint32_t theta, uint32_t c,
@@ -274,17 +309,19 @@ __device__ __forceinline__ void build_coarse_planes15(const RowT* row, const uin
     }
 }
 
-// Winners of word cw (local inhibition, per-column boosts), all lanes of the warp call it.
+// Beats of lane's column of word cw (local inhibition, per-column boosts) over the neighbour
+// words jw0+part, jw0+part+parts, ..; u_out = the column's coarse key (0: ineligible)
 template <typename RowT>
-__device__ __forceinline__ uint32_t local_general_word15(const RowT* row, const uint32_t* bc,
-                                                         const uint32_t* planes, uint32_t ncw, uint32_t cw,
-                                                         uint32_t C, uint32_t radius, uint32_t k, uint32_t theta,
-                                                         const CoarseMap& m, uint32_t L, uint32_t lane) {
+__device__ __forceinline__ uint32_t local_general_beats15(const RowT* row, const uint32_t* bc, const uint32_t* planes,
+                                                          uint32_t ncw, uint32_t cw, uint32_t C, uint32_t radius,
+                                                          uint32_t theta, const CoarseMap& m, uint32_t L, uint32_t lane,
+                                                          uint32_t part, uint32_t parts, uint32_t& u_out) {
     const int c = static_cast<int>(cw * 32u + lane);
     uint64_t Nc;
     const uint64_t keyc = exact_key(row[c], bc[c], theta, static_cast<uint32_t>(c), L, Nc);
     bool lossy_c;
     const uint32_t u = coarse_u15(Nc > (1ull << 23) ? Nc : 0ull, m, lossy_c);
+    u_out = c < static_cast<int>(C) ? u : 0u;
     const int R = static_cast<int>(radius), Cn = static_cast<int>(C);
     const int lo = max(0, c - R), hi = min(Cn - 1, c + R);
     const int jw0 = max(0, (static_cast<int>(cw) * 32 - R) / 32);
@@ -293,7 +330,7 @@ __device__ __forceinline__ uint32_t local_general_word15(const RowT* row, const 
 #pragma unroll
     for (int b = 0; b < 15; ++b) Xm[b] = 0u - ((u >> b) & 1u);
     uint32_t beats = 0;
-    for (int jw = jw0; jw <= jw1; ++jw) {
+    for (int jw = jw0 + static_cast<int>(part); jw <= jw1; jw += static_cast<int>(parts)) {
         const uint32_t* P0 = planes + jw * 16;
         uint32_t gt = 0u, eq = 0xFFFFFFFFu;
 #pragma unroll
@@ -323,7 +360,18 @@ __device__ __forceinline__ uint32_t local_general_word15(const RowT* row, const 
             }
         }
     }
-    return __ballot_sync(0xffffffffu, c < Cn && u > 0u && beats < k);
+    return beats;
+}
+
+// Winners of word cw (local inhibition, per-column boosts), all lanes of the warp call it.
+template <typename RowT>
+__device__ __forceinline__ uint32_t local_general_word15(const RowT* row, const uint32_t* bc,
+                                                         const uint32_t* planes, uint32_t ncw, uint32_t cw,
+                                                         uint32_t C, uint32_t radius, uint32_t k, uint32_t theta,
+                                                         const CoarseMap& m, uint32_t L, uint32_t lane) {
+    uint32_t u;
+    const uint32_t beats = local_general_beats15(row, bc, planes, ncw, cw, C, radius, theta, m, L, lane, 0u, 1u, u);
+    return __ballot_sync(0xffffffffu, u > 0u && beats < k);
 }
 
 // ---- global inhibition by a whole CTA (cluster learning) ---------------------------------
