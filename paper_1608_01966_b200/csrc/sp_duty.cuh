@@ -101,6 +101,70 @@ __device__ __forceinline__ float wmax_query(const float* v, const float* pre, co
     return m;
 }
 
+// Windows of radius r with 2r+1 >= C (the adapted radius is typically ~C/2, R21) always reach
+// an end of the column range: W(c) = [0, hi] or [lo, C-1].  Prefix and suffix maxima answer
+// them: in-block scans (warp shuffles) plus the exclusive prefix/suffix maxima of the block
+// maxima (one warp), two barriers instead of the sparse table's log2(nb) + 1.
+__device__ __forceinline__ void wmax_build_ends(const float* v, uint32_t C, uint32_t C32, float* pre, float* suf,
+                                                float* table) {
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, nb = C32 / 32u;
+    for (uint32_t b = tid >> 5; b < nb; b += blockDim.x >> 5) {
+        const uint32_t c = b * 32u + lane;
+        const float x = c < C ? v[c] : 0.0f;
+        float p = x, s = x;
+#pragma unroll
+        for (uint32_t d = 1; d < 32u; d <<= 1) {
+            const float up = __shfl_up_sync(0xffffffffu, p, d);
+            const float dn = __shfl_down_sync(0xffffffffu, s, d);
+            if (lane >= d) p = fmaxf(p, up);
+            if (lane + d < 32u) s = fmaxf(s, dn);
+        }
+        pre[c] = p;
+        suf[c] = s;
+        if (lane == 0) table[b] = s;  // block maximum
+    }
+    __syncthreads();
+    if (tid < 32u) {  // table[nb + b] = max of blocks < b, table[2nb + b] = max of blocks > b
+        float carry = 0.0f;
+        for (uint32_t base = 0; base < nb; base += 32u) {  // exclusive prefix max
+            const uint32_t b = base + lane;
+            const float x = b < nb ? table[b] : 0.0f;
+            float p = x;
+#pragma unroll
+            for (uint32_t d = 1; d < 32u; d <<= 1) {
+                const float up = __shfl_up_sync(0xffffffffu, p, d);
+                if (lane >= d) p = fmaxf(p, up);
+            }
+            const float ex = fmaxf(carry, __shfl_up_sync(0xffffffffu, p, 1));
+            if (b < nb) table[nb + b] = lane == 0 ? carry : ex;
+            carry = fmaxf(carry, __shfl_sync(0xffffffffu, p, 31));
+        }
+        carry = 0.0f;
+        for (int base = static_cast<int>((nb - 1u) / 32u) * 32; base >= 0; base -= 32) {  // exclusive suffix max
+            const uint32_t b = static_cast<uint32_t>(base) + lane;
+            const float x = b < nb ? table[b] : 0.0f;
+            float s = x;
+#pragma unroll
+            for (uint32_t d = 1; d < 32u; d <<= 1) {
+                const float dn = __shfl_down_sync(0xffffffffu, s, d);
+                if (lane + d < 32u) s = fmaxf(s, dn);
+            }
+            const float ex = fmaxf(carry, __shfl_down_sync(0xffffffffu, s, 1));
+            if (b < nb) table[2u * nb + b] = lane == 31u ? carry : ex;
+            carry = fmaxf(carry, __shfl_sync(0xffffffffu, s, 0));
+        }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ float wmax_query_ends(const float* pre, const float* suf, const float* table, uint32_t nb,
+                                                 uint32_t C, uint32_t c, uint32_t r) {
+    const uint32_t lo = c < r ? 0u : c - r;
+    const uint32_t hi = c + r >= C ? C - 1u : c + r;
+    if (lo == 0u) return fmaxf(pre[hi], table[nb + (hi >> 5)]);
+    return fmaxf(suf[lo], table[2u * nb + (lo >> 5)]);  // hi == C-1 when 2r+1 >= C
+}
+
 // Maxima of a[0..C) and b[0..C) (values >= 0) over the whole CTA, for windows that cover all
 // columns (radius 0 or >= C-1): one reduction instead of the window tables.  s_red >= 64
 // floats of shared scratch; every thread of the CTA calls it and gets both maxima.

@@ -142,8 +142,8 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
     float* s_odc = s_adc + g.C32;                                       // [C32]
     float* s_pre = s_odc + g.C32;                                       // [C32]
     float* s_suf = s_pre + g.C32;                                       // [C32]
-    float* s_table = s_suf + g.C32;                                     // [levels][nb]
-    uint32_t* s_sdr_all = reinterpret_cast<uint32_t*>(s_table + wmax_levels(nb) * nb);  // [ncw]
+    float* s_table = s_suf + g.C32;                                     // [levels + 3][nb]
+    uint32_t* s_sdr_all = reinterpret_cast<uint32_t*>(s_table + (wmax_levels(nb) + 3u) * nb);  // [ncw]
     uint32_t* s_span = s_sdr_all + g.ncw;                               // [cpc]
     unsigned long long* s_spanpart =
         reinterpret_cast<unsigned long long*>((reinterpret_cast<uintptr_t>(s_span + cpc) + 7u) & ~uintptr_t(7));  // [Q]
@@ -388,23 +388,25 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
             // (c) boosts of every column (replicated): the keys of input t+1.  A window that
             // covers every column (radius 0 or >= C-1) needs only the two maxima.
             const bool gwin = R == 0u || R + 1u >= g.C;
+            const bool ends = !gwin && 2u * R + 1u >= g.C;  // every window reaches an end
             float gA = 0.0f, gO = 0.0f;
-            if (gwin) {
-                block_max2(s_adc, s_odc, g.C, s_pre, gA, gO);
-            } else {
-                wmax_build(s_adc, g.C, g.C32, s_pre, s_suf, s_table, 0u, nthr, sync);
-            }
+            auto wq = [&](const float* v, uint32_t c) {
+                return ends ? wmax_query_ends(s_pre, s_suf, s_table, nb, g.C, c, R)
+                            : wmax_query(v, s_pre, s_suf, s_table, nb, g.C, c, R);
+            };
+            if (gwin) block_max2(s_adc, s_odc, g.C, s_pre, gA, gO);
+            else if (ends) wmax_build_ends(s_adc, g.C, g.C32, s_pre, s_suf, s_table);
+            else wmax_build(s_adc, g.C, g.C32, s_pre, s_suf, s_table, 0u, nthr, sync);
             for (uint32_t c = tid; c < g.C; c += nthr)
-                s_bc[c] = boost_bc(boost_rule(
-                    s_adc[c], gwin ? gA : wmax_query(s_adc, s_pre, s_suf, s_table, nb, g.C, c, R), fl.mb1));
+                s_bc[c] = boost_bc(boost_rule(s_adc[c], gwin ? gA : wq(s_adc, c), fl.mb1));
             __syncthreads();
             // (d) bump of this CTA's weak columns, warp per column
-            if (!gwin) wmax_build(s_odc, g.C, g.C32, s_pre, s_suf, s_table, 0u, nthr, sync);
+            if (ends) wmax_build_ends(s_odc, g.C, g.C32, s_pre, s_suf, s_table);
+            else if (!gwin) wmax_build(s_odc, g.C, g.C32, s_pre, s_suf, s_table, 0u, nthr, sync);
             for (uint32_t cl = wi; cl < cpc; cl += nw) {
                 const uint32_t c = c0 + cl;
                 if (c >= g.C) break;
-                if (!weak_column(s_odc[c], gwin ? gO : wmax_query(s_odc, s_pre, s_suf, s_table, nb, g.C, c, R)))
-                    continue;
+                if (!weak_column(s_odc[c], gwin ? gO : wq(s_odc, c))) continue;
                 float* __restrict__ perm = p.perm + static_cast<size_t>(c) * g.S;
                 uint32_t* col = s_syn + cl * ss;
                 uint32_t smin = 0xFFFFFFFFu, smax = 0u;
@@ -509,7 +511,7 @@ uint32_t learn_cluster_smem(const Geometry& g, uint32_t Q, uint32_t* cols_per_ct
     const uint32_t Wn4 = ((g.nbits + 31u) / 32u + 3u) / 4u * 4u;
     if (cols_per_cta) *cols_per_cta = cpc;
     const uint32_t nb = g.C32 / 32u;
-    const uint32_t full_bytes = full ? 4u * (4u * g.C32 + wmax_levels(nb) * nb + g.ncw + cpc) + 8u + 8u * Q : 0u;
+    const uint32_t full_bytes = full ? 4u * (4u * g.C32 + (wmax_levels(nb) + 3u) * nb + g.ncw + cpc) + 8u + 8u * Q : 0u;
     return 4u * (learn_syn_stride(g.S) * cpc + (dbl_bits ? 2u : 1u) * Wn4 + g.C32) +
            4u * ((g.C32 + 3u) / 4u * 4u) + 8u * (cpc / 32u * 64u) + 4u * (cpc / 32u) +
            4u * std::max(g.ncw * 16u, 512u) + full_bytes;
