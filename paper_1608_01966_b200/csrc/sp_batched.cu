@@ -276,8 +276,39 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             continue;
         }
         if (radius > 0 && p.uniform_bc) {
-            // local inhibition, uniform boost: bit-sliced window comparator (sp_select.cuh)
             const uint32_t r_lo = uniform_r_lo(theta, s_bc[0]);
+            // range of the eligible raw counts of this input: the wavelet path needs <= 8 levels
+            uint32_t xmn = 0xFFFFFFFFu, xmx = 0u;
+            for (uint32_t c = lane; c < p.C; c += 32u) {
+                const uint32_t x = row[c];
+                if (x >= r_lo) xmn = min(xmn, x), xmx = max(xmx, x);
+            }
+            xmn = __reduce_min_sync(0xffffffffu, xmn);
+            xmx = __reduce_max_sync(0xffffffffu, xmx);
+            const uint32_t B = xmn <= xmx ? 32u - __clz(xmx - xmn + 1u) : 1u;
+            // per-warp scratch sized for the largest B (8): the warps' regions must not depend on
+            // their inputs' ranges
+            const uint32_t wbytes = (2u * p.C32 + 8u * 8u * (p.ncw + 2u) + 127u) & ~127u;
+            if (B <= 8u && wbytes * NW <= p.region_bytes) {
+                // wavelet matrix over the positions (sp_select.cuh): O(C log range) per input
+                uint8_t* base = region + wi * wbytes;
+                uint32_t* bv = reinterpret_cast<uint32_t*>(base + 2u * p.C32);
+                uint32_t* pc = bv + B * (p.ncw + 2u);
+                uint32_t total = 0, myword = 0;
+                local_uniform_wavelet(row, p.C, p.C32, p.ncw, radius, p.k, r_lo, xmn, B, base, base + p.C32, bv, pc,
+                                      lane, [&](uint32_t cw, uint32_t word) {
+                                          if ((cw & 31u) == lane) myword = word;
+                                          total += __popc(word);
+                                          if ((cw & 31u) == 31u || cw + 1u == p.ncw) {
+                                              const uint32_t b0 = cw & ~31u;
+                                              if (lane <= (cw & 31u))
+                                                  p.sdr[static_cast<size_t>(gin) * p.ncw + b0 + lane] = myword;
+                                          }
+                                      });
+                if (lane == 0) p.counts[gin] = total;
+                continue;
+            }
+            // local inhibition, uniform boost: bit-sliced window comparator (sp_select.cuh)
             const uint32_t nb = raw_bits(p.S);
             uint32_t* planes = reinterpret_cast<uint32_t*>(region) + wi * 640u;  // [ncw <= 64][nb <= 10]
             build_raw_planes(row, planes, p.ncw, nb, r_lo, 0u, 1u, lane);

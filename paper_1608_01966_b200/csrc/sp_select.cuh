@@ -132,6 +132,94 @@ __device__ __forceinline__ uint32_t local_uniform_beats_part(const RowT* row, co
     return beats;
 }
 
+// Local inhibition, uniform boost, by one warp with a wavelet matrix over the positions (any
+// radius, O(C log range) per input instead of O(C * r)).  Values x' = x - xmin + 1 for the
+// eligible columns (x >= r_lo), 0 otherwise, B = bits(xmax - xmin + 1) <= 8 levels.  For
+// column c with window [lo, hi]:
+//     beats(c) = #{d in [lo, hi] : x'_d > x'_c} + #{d in [lo, c) : x'_d == x'_c}
+// from one descent through the levels tracking the positions lo, c and hi+1 (rank queries
+// on per-level bit-vectors with per-word prefix counts).  emit(cw, word) gets the SDR words
+// in order (warp-uniform).  Scratch: buf0, buf1 [C32] bytes; bv, pc [B][ncw + 2] words.
+__device__ __forceinline__ uint32_t wm_rank(const uint32_t* bvl, const uint32_t* pcl, uint32_t p) {
+    return pcl[p >> 5] + __popc(bvl[p >> 5] & ((1u << (p & 31u)) - 1u));
+}
+
+template <typename RowT, typename Emit>
+__device__ __forceinline__ void local_uniform_wavelet(const RowT* row, uint32_t C, uint32_t C32, uint32_t ncw,
+                                                      uint32_t radius, uint32_t k, uint32_t r_lo, uint32_t xmin,
+                                                      uint32_t B, uint8_t* buf0, uint8_t* buf1, uint32_t* bv,
+                                                      uint32_t* pc, uint32_t lane, Emit emit) {
+    const uint32_t stride = ncw + 2u;
+    auto xval = [&](uint32_t c) -> uint32_t {
+        const uint32_t x = c < C ? static_cast<uint32_t>(row[c]) : 0u;
+        return x >= r_lo ? x - xmin + 1u : 0u;
+    };
+    for (uint32_t i = lane; i < C32; i += 32u) buf0[i] = static_cast<uint8_t>(xval(i));
+    __syncwarp();
+    uint8_t* src = buf0;
+    uint8_t* dst = buf1;
+    for (int l = static_cast<int>(B) - 1; l >= 0; --l) {
+        uint32_t* bvl = bv + l * stride;
+        uint32_t* pcl = pc + l * stride;
+        uint32_t ones = 0;
+#pragma unroll 8
+        for (uint32_t j = 0; j < ncw; ++j) {
+            const uint32_t w = __ballot_sync(0xffffffffu, (src[j * 32u + lane] >> l) & 1u);
+            if (lane == 0) bvl[j] = w, pcl[j] = ones;
+            ones += __popc(w);
+        }
+        const uint32_t Z = C32 - ones;
+        if (lane == 0) bvl[ncw] = 0u, pcl[ncw] = ones, pcl[ncw + 1u] = Z;
+        __syncwarp();
+#pragma unroll 8
+        for (uint32_t j = 0; j < ncw; ++j) {
+            const uint32_t i = j * 32u + lane;
+            const uint32_t v = src[i];
+            const uint32_t r = pcl[j] + __popc(bvl[j] & ((1u << lane) - 1u));
+            dst[((v >> l) & 1u) ? Z + r : i - r] = static_cast<uint8_t>(v);
+        }
+        __syncwarp();
+        uint8_t* t = src;
+        src = dst;
+        dst = t;
+    }
+    const int R = static_cast<int>(radius), Cn = static_cast<int>(C);
+    // beats of column c (its descent through the levels); independent columns interleave
+    auto beats_of = [&](uint32_t c, uint32_t x) -> uint32_t {
+        const uint32_t lo = static_cast<uint32_t>(max(0, static_cast<int>(c) - R));
+        const uint32_t hi = static_cast<uint32_t>(min(Cn - 1, static_cast<int>(c) + R)) + 1u;
+        uint32_t a = lo, m = c, b = hi, less = 0;
+        for (int l = static_cast<int>(B) - 1; l >= 0; --l) {
+            const uint32_t* bvl = bv + l * stride;
+            const uint32_t* pcl = pc + l * stride;
+            const uint32_t ra = wm_rank(bvl, pcl, a), rm = wm_rank(bvl, pcl, m), rb = wm_rank(bvl, pcl, b);
+            if ((x >> l) & 1u) {
+                const uint32_t Z = pcl[ncw + 1u];
+                less += (b - a) - (rb - ra);
+                a = Z + ra, m = Z + rm, b = Z + rb;
+            } else {
+                a -= ra, m -= rm, b -= rb;
+            }
+        }
+        return ((hi - lo) - less - (b - a)) + (m - a);  // greater + equal before c
+    };
+    uint32_t cw = 0;
+    for (; cw + 1u < ncw; cw += 2u) {
+        const uint32_t c0 = cw * 32u + lane, c1 = c0 + 32u;
+        const uint32_t x0 = xval(c0), x1 = xval(c1);
+        const uint32_t b0 = x0 ? beats_of(c0, x0) : 0u, b1 = x1 ? beats_of(c1, x1) : 0u;
+        emit(cw, __ballot_sync(0xffffffffu, x0 > 0u && b0 < k));
+        emit(cw + 1u, __ballot_sync(0xffffffffu, x1 > 0u && b1 < k));
+    }
+    if (cw < ncw) {
+        const uint32_t c0 = cw * 32u + lane;
+        const uint32_t x0 = xval(c0);
+        const uint32_t b0 = x0 ? beats_of(c0, x0) : 0u;
+        emit(cw, __ballot_sync(0xffffffffu, x0 > 0u && b0 < k));
+    }
+    __syncwarp();
+}
+
 // ---- general boosts ---------------------------------------------------------------------
 // Exact rank key (R4, R6): N = raw*Bc (exact), key = N << L | (2^L-1-c).
 __device__ __forceinline__ uint64_t exact_key(uint32_t raw, uint32_t bc, uint32_t theta, uint32_t c,
