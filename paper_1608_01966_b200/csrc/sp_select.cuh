@@ -304,16 +304,19 @@ __device__ __forceinline__ uint32_t local_general_word(const RowT* row, const ui
 // flag (the dropped low bits are zero) resolves the common remaining case, equal N, by index
 // alone (d beats c iff d < c): exact keys are compared only for ties involving a lossy column.
 struct CoarseMap {
-    uint64_t nlo;  // smallest eligible N
+    uint64_t nlo;  // smallest eligible N, rounded down to a multiple of 2^sh
     uint32_t sh;   // right shift of N - nlo, so that u - 1 < 2^15
 };
 
 __device__ __forceinline__ CoarseMap coarse_map(uint64_t nmin, uint64_t nmax) {
     CoarseMap m{0ull, 0u};
     if (nmin > nmax) return m;  // no eligible column
-    m.nlo = nmin;
-    const uint64_t range = nmax - nmin;
-    while ((range >> m.sh) > 32766ull) ++m.sh;
+    // nlo aligned to 2^sh: then "lossless" is N % 2^sh == 0, which holds for every column with a
+    // boost of 1 (N = raw * 2^23) whenever sh <= 23, so equal-N ties stay index ties
+    for (;; ++m.sh) {
+        m.nlo = nmin & ~((1ull << m.sh) - 1ull);
+        if (((nmax - m.nlo) >> m.sh) <= 32766ull) break;
+    }
     return m;
 }
 
