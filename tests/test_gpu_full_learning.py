@@ -183,3 +183,21 @@ def test_full_learning_full_size(path):
     check_inputs(results, *run(sp, frames, True))
     check_path(sp, path)
     check_state(sp, ora)
+
+
+@pytest.mark.parametrize("full", [False, True])
+def test_learning_stream_longer_than_a_prepack_chunk(full):
+    # > 1024 inputs in one call: the cluster path packs and learns in chunks; the state
+    # (permanences, flags, duty cycles, boosts, radius) carries across the chunk launches
+    cfg = ocfg(full_learning=full, inhibition_radius=6, duty_cycle_period=50)
+    frames = sp_inputs.frames(4242, 0, 1100, 8, 8, rho=0.4)
+    ora = O.SpatialPoolerOracle(cfg)
+    results = ora.compute(frames, learning=True)
+    flags = P.SP_FLAG_RECORD_OVERLAPS | (P.SP_FLAG_FULL_LEARNING if full else 0)
+    sp = P.SpatialPooler(**gpu_kwargs(cfg, max_inputs=1100, flags=flags, duty_cycle_period=50))
+    check_inputs(results, *run(sp, frames, True))
+    assert sp.info()["last_learn_path"] == P.SP_LEARN_CLUSTER
+    if full:
+        check_state(sp, ora)
+    else:
+        assert np.array_equal(sp.get_state()[1].view(np.uint32), ora.perm.view(np.uint32))
