@@ -550,6 +550,16 @@ sp_status check_handle(sp_handle* h) {
     return SP_OK;
 }
 
+// CTAs per input of k_inhibit: local inhibition over many columns is O(C * r) per input, so
+// the SDR words of one input are split over CTAs (each builds the key planes it needs) until
+// the SMs are busy; global inhibition and small C keep one CTA per input.
+uint32_t inhibit_parts(const sp_handle* h, uint32_t inputs) {
+    const sp::Geometry& g = h->g;
+    if (h->cfg.inhibition_radius == 0 || g.C32 < 2048u || std::getenv("SP_NO_SPLIT_INHIBIT")) return 1u;
+    const uint32_t want = (2u * static_cast<uint32_t>(h->sm_count) + inputs - 1u) / std::max(inputs, 1u);
+    return std::max(1u, std::min(want, g.ncw / 4u));
+}
+
 // Full-learning constants and device state (R17-R21) for the learning kernels.
 sp::FullLearn full_learn_params(const sp_handle* h) {
     sp::FullLearn f{};
@@ -839,7 +849,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         if (!learn) {
             e = sp::launch_overlap(p, s);
             h->launches++;
-            if (e == cudaSuccess) e = sp::launch_inhibit(p, s);
+            if (e == cudaSuccess) e = sp::launch_inhibit(p, s, inhibit_parts(h, p.num_inputs));
             h->launches++;
             if (e != cudaSuccess) return cuda_fail(e, "overlap/inhibit launch");
             continue;
@@ -853,13 +863,14 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
             q.num_inputs = 1;
             e = sp::launch_overlap(q, s);
             h->launches++;
-            if (e == cudaSuccess) e = sp::launch_inhibit(q, s);
+            if (e == cudaSuccess) e = sp::launch_inhibit(q, s, inhibit_parts(h, 1u));
             h->launches++;
             if (e == cudaSuccess) e = sp::launch_learn(q, 0, s);
             h->launches++;
             if (full && e == cudaSuccess) {
-                e = sp::launch_full(q, 0, s);
-                h->launches++;
+                uint32_t nl = 0;
+                e = sp::launch_full(q, 0, s, &nl);
+                h->launches += nl;
             }
             if (e != cudaSuccess) return cuda_fail(e, "learning step launch");
         }
@@ -1019,6 +1030,7 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
     if (e == cudaSuccess) e = dalloc(&h->d_span, g.C32);
     if (e == cudaSuccess) e = dalloc(&h->d_radius, 1);
     if (e == cudaSuccess) e = dalloc(&h->d_fscratch, sp::full_scratch_floats(g.C32));
+    if (e == cudaSuccess) e = cudaMemset(h->d_fscratch, 0, sp::full_scratch_floats(g.C32) * 4u);
     if (e == cudaSuccess) e = cudaMemset(h->d_adc, 0, g.C32 * 4u);
     if (e == cudaSuccess) e = cudaMemset(h->d_odc, 0, g.C32 * 4u);
     if (e == cudaSuccess) e = cudaMemset(h->d_span, 0, g.C32 * 4u);

@@ -211,9 +211,9 @@ cudaError_t launch_patch(const BatchedParams& p, uint32_t smem_bytes, uint32_t c
 cudaError_t batched_max_clusters(uint32_t smem_bytes, int max_clusters[9]);
 cudaError_t launch_pack(const PerInputParams& p, cudaStream_t s);
 cudaError_t launch_overlap(const PerInputParams& p, cudaStream_t s);
-cudaError_t launch_inhibit(const PerInputParams& p, cudaStream_t s);
+cudaError_t launch_inhibit(const PerInputParams& p, cudaStream_t s, uint32_t parts = 1);
 cudaError_t launch_learn(const PerInputParams& p, uint32_t input, cudaStream_t s);
-cudaError_t launch_full(const PerInputParams& p, uint32_t input, cudaStream_t s);
+cudaError_t launch_full(const PerInputParams& p, uint32_t input, cudaStream_t s, uint32_t* launches);
 cudaError_t launch_span(const uint32_t* idx, const float* perm, float tau, uint32_t C, uint32_t S,
                         uint32_t* span, cudaStream_t s);
 size_t full_scratch_floats(uint32_t C32);

@@ -5,6 +5,9 @@
 //   P4 k_learn    per input: fused +inc/-dec, clamp, connected-flag refresh (a5)
 // plus layout maintenance (synapse-major idx|flag words, batched ELL flags).
 // Learning runs P2 -> P3 -> P4 per input in order (the recurrence of P:92).
+#include <algorithm>
+#include <cstdlib>
+
 #include "sp_duty.cuh"
 #include "sp_internal.h"
 #include "sp_select.cuh"
@@ -111,6 +114,10 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
     __shared__ uint32_t s_total;
     const uint32_t t = blockIdx.x;
     const uint32_t gin = p.first_input + t;
+    // gridDim.y CTAs share an input: CTA y emits the SDR words [w0, w1) (every CTA builds the
+    // full key planes / threshold its windows need); counts then meet with atomics
+    const uint32_t parts = gridDim.y;
+    const uint32_t w0 = blockIdx.y * g.ncw / parts, w1 = (blockIdx.y + 1u) * g.ncw / parts;
     const uint32_t tid = threadIdx.x, nthr = blockDim.x;
     const uint32_t radius = p.radius_dev ? *p.radius_dev : p.radius;  // adapted by full learning
     for (uint32_t c = tid; c < g.C32; c += nthr) {
@@ -122,7 +129,7 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
     __syncthreads();
     const uint32_t theta = p.min_overlap, L = g.keyL;
     if (p.raw_out) {
-        for (uint32_t c = tid; c < g.C; c += nthr) {
+        for (uint32_t c = w0 * 32u + tid; c < min(g.C, w1 * 32u); c += nthr) {
             const uint32_t r = s_raw[c];
             p.raw_out[static_cast<size_t>(gin) * g.C + c] = static_cast<uint16_t>(r);
             p.boosted_out[static_cast<size_t>(gin) * g.C + c] =
@@ -156,7 +163,7 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
         const uint32_t nb = raw_bits(g.S);
         build_raw_planes(s_raw, s_planes, g.ncw, nb, r_lo, tid >> 5, nthr >> 5, tid & 31u);
         __syncthreads();
-        for (uint32_t cw = tid >> 5; cw < g.ncw; cw += nthr >> 5) {
+        for (uint32_t cw = w0 + (tid >> 5); cw < w1; cw += nthr >> 5) {
             const uint32_t word = local_uniform_word(s_raw, s_planes, g.ncw, nb, cw, g.C, radius, p.k,
                                                      r_lo, tid & 31u);
             if ((tid & 31u) == 0) {
@@ -170,7 +177,7 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
         const CoarseMap cm = coarse_map_block(s_raw, s_bc, theta, 0u, g.ncw, s_mm);
         build_coarse_planes15(s_raw, s_bc, s_planes, g.ncw, theta, cm, tid >> 5, nthr >> 5, tid & 31u);
         __syncthreads();
-        for (uint32_t cw = tid >> 5; cw < g.ncw; cw += nthr >> 5) {
+        for (uint32_t cw = w0 + (tid >> 5); cw < w1; cw += nthr >> 5) {
             const uint32_t word = local_general_word15(s_raw, s_bc, s_planes, g.ncw, cw, g.C, radius, p.k,
                                                        theta, cm, L, tid & 31u);
             if ((tid & 31u) == 0) {
@@ -179,7 +186,7 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
             }
         }
     } else {
-    for (uint32_t cw = tid >> 5; cw < g.ncw; cw += nthr >> 5) {
+    for (uint32_t cw = w0 + (tid >> 5); cw < w1; cw += nthr >> 5) {
         const uint32_t c = cw * 32u + (tid & 31u);
         uint64_t N;
         const uint64_t key = key_of(s_raw[c], s_bc[c], theta, c, L, N);
@@ -208,7 +215,10 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
     __syncthreads();
     if ((tid & 31u) == 0 && my_total) atomicAdd(&s_total, my_total);
     __syncthreads();
-    if (tid == 0) p.counts[gin] = s_total;
+    if (tid == 0) {
+        if (parts == 1u) p.counts[gin] = s_total;
+        else if (s_total) atomicAdd(p.counts + gin, s_total);  // zeroed before the launch
+    }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -306,6 +316,120 @@ __global__ void __launch_bounds__(1024) k_full(const PerInputParams p, uint32_t 
     if (tid == 0) *fl.radius = adapt_radius(s_span, g.nbits, g.C);
 }
 
+// P5 for many columns (C32 >= 4096), split over the SMs in two launches:
+//   k_full_a: duty cycles (b) of every column; in-block prefix/suffix maxima and block maxima of
+//             both duty arrays -> global scratch
+//   k_full_b: every CTA builds the sparse tables over the block maxima in shared memory, then
+//             boosts (c) and bumps (d) of its column range, the span sum of its range; the last
+//             CTA to finish (ticket) forms the adapted radius (e)
+__global__ void __launch_bounds__(1024) k_full_a(const PerInputParams p, uint32_t t) {
+    const Geometry& g = p.g;
+    const FullLearn& fl = p.fl;
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x, lane = threadIdx.x & 31u;
+    const uint32_t nb = g.C32 / 32u;
+    float* preA = fl.scratch;
+    float* sufA = preA + g.C32;
+    float* preO = sufA + g.C32;
+    float* sufO = preO + g.C32;
+    float* bmA = sufO + g.C32;
+    float* bmO = bmA + nb;
+    float a = 0.0f, o = 0.0f;
+    if (c < g.C) {
+        const uint32_t gin = p.first_input + t;
+        const bool act = ((p.sdr[static_cast<size_t>(gin) * g.ncw + (c >> 5)] >> (c & 31u)) & 1u) != 0u;
+        const uint32_t r = p.raw[static_cast<size_t>(t) * g.C32 + c];
+        a = duty_update(fl.adc[c], act, fl.pm1, fl.P);
+        o = duty_update(fl.odc[c], r >= p.min_overlap && r > 0u, fl.pm1, fl.P);
+        fl.adc[c] = a;
+        fl.odc[c] = o;
+    }
+    if (c >= g.C32) return;  // whole warps past the padded range
+    float pa = a, sa = a, po = o, so = o;
+#pragma unroll
+    for (uint32_t d = 1; d < 32u; d <<= 1) {
+        const float ua = __shfl_up_sync(0xffffffffu, pa, d), da = __shfl_down_sync(0xffffffffu, sa, d);
+        const float uo = __shfl_up_sync(0xffffffffu, po, d), dn = __shfl_down_sync(0xffffffffu, so, d);
+        if (lane >= d) pa = fmaxf(pa, ua), po = fmaxf(po, uo);
+        if (lane + d < 32u) sa = fmaxf(sa, da), so = fmaxf(so, dn);
+    }
+    preA[c] = pa, sufA[c] = sa, preO[c] = po, sufO[c] = so;
+    if (lane == 0) bmA[c >> 5] = sa, bmO[c >> 5] = so;
+}
+
+__global__ void __launch_bounds__(1024) k_full_b(const PerInputParams p) {
+    extern __shared__ float s_tab[];  // [2][levels][nb]
+    const Geometry& g = p.g;
+    const FullLearn& fl = p.fl;
+    const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u;
+    const uint32_t nb = g.C32 / 32u, Lv = wmax_levels(nb);
+    const float* preA = fl.scratch;
+    const float* sufA = preA + g.C32;
+    const float* preO = sufA + g.C32;
+    const float* sufO = preO + g.C32;
+    const float* bmA = sufO + g.C32;
+    const float* bmO = bmA + nb;
+    unsigned long long* acc = reinterpret_cast<unsigned long long*>(fl.scratch + 4u * g.C32 + 2u * nb + 2u);
+    uint32_t* ticket = reinterpret_cast<uint32_t*>(acc + 1);
+    float* tA = s_tab;
+    float* tO = s_tab + Lv * nb;
+    for (uint32_t b = tid; b < nb; b += nthr) tA[b] = bmA[b], tO[b] = bmO[b];
+    __syncthreads();
+    for (uint32_t l = 1; l < Lv; ++l) {
+        const uint32_t half = 1u << (l - 1);
+        for (uint32_t b = tid; b + (1u << l) <= nb; b += nthr) {
+            tA[l * nb + b] = fmaxf(tA[(l - 1) * nb + b], tA[(l - 1) * nb + b + half]);
+            tO[l * nb + b] = fmaxf(tO[(l - 1) * nb + b], tO[(l - 1) * nb + b + half]);
+        }
+        __syncthreads();
+    }
+    const uint32_t r = *fl.radius;  // radius in force for this input (R18)
+    const uint32_t c0 = blockIdx.x * g.C / gridDim.x, c1 = (blockIdx.x + 1u) * g.C / gridDim.x;
+    for (uint32_t c = c0 + tid; c < c1; c += nthr) {  // (c) boosts
+        const float b = boost_rule(fl.adc[c], wmax_query(fl.adc, preA, sufA, tA, nb, g.C, c, r), fl.mb1);
+        fl.boost[c] = b;
+        fl.bc[c] = boost_bc(b);
+    }
+    for (uint32_t c = c0 + (tid >> 5); c < c1; c += nthr >> 5) {  // (d) bumps, warp per column
+        if (!weak_column(fl.odc[c], wmax_query(fl.odc, preO, sufO, tO, nb, g.C, c, r))) continue;
+        const uint32_t* idx = p.idx + static_cast<size_t>(c) * g.S;
+        float* perm = p.perm + static_cast<size_t>(c) * g.S;
+        uint32_t smin = 0xFFFFFFFFu, smax = 0u;
+        for (uint32_t s = lane; s < g.S; s += 32u) {
+            const float v = fminf(__fadd_rn(perm[s], fl.bump), 1.0f);
+            perm[s] = v;
+            p.syn_rw[static_cast<size_t>(s) * g.C32 + c] = idx[s] | (v >= p.tau ? 0x80000000u : 0u);
+            span_accumulate(v >= p.tau, s, smin, smax);
+        }
+        const uint32_t sp_c = span_finish(smin, smax, idx, 0xFFFFFFFFu);
+        if (lane == 0) fl.span[c] = sp_c;
+    }
+    if (!fl.adapt) return;
+    __syncthreads();
+    // (e) this range's span sum; the last CTA forms the radius and resets the accumulator
+    __shared__ unsigned long long s_part;
+    __shared__ uint32_t s_last;
+    if (tid == 0) s_part = 0ull;
+    __syncthreads();
+    unsigned long long part = 0;
+    for (uint32_t c = c0 + tid; c < c1; c += nthr) part += fl.span[c];
+    for (uint32_t d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
+    if (lane == 0 && part) atomicAdd(&s_part, part);
+    __syncthreads();
+    if (tid == 0) {
+        atomicAdd(acc, s_part);
+        __threadfence();
+        s_last = atomicAdd(ticket, 1u) + 1u == gridDim.x ? 1u : 0u;
+    }
+    __syncthreads();
+    if (s_last && tid == 0) {
+        __threadfence();
+        const unsigned long long total = atomicAdd(acc, 0ull);
+        *fl.radius = adapt_radius(total, g.nbits, g.C);
+        *acc = 0ull;
+        *ticket = 0u;
+    }
+}
+
 // spans of every column from the canonical arrays (warp per column; R21)
 __global__ void k_span(const uint32_t* idx, const float* perm, float tau, uint32_t C, uint32_t S, uint32_t* span) {
     const uint32_t c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -368,6 +492,7 @@ static cudaError_t allow_dynamic_smem(F* fn, int max_smem) {
 cudaError_t configure_per_input(int max_smem) {
     cudaError_t e = allow_dynamic_smem(k_overlap, max_smem);
     if (e == cudaSuccess) e = allow_dynamic_smem(k_inhibit, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(k_full_b, max_smem);
     return e;
 }
 
@@ -378,10 +503,14 @@ cudaError_t launch_overlap(const PerInputParams& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_inhibit(const PerInputParams& p, cudaStream_t s) {
+cudaError_t launch_inhibit(const PerInputParams& p, cudaStream_t s, uint32_t parts) {
     const uint32_t smem = p.g.C32 * 8u + p.g.ncw * 16u * 4u;  // raw, Bc, bit-planes
     const uint32_t threads = p.g.C32 < 1024u ? p.g.C32 : 1024u;
-    k_inhibit<<<p.num_inputs, threads, smem, s>>>(p);
+    if (parts > 1u) {
+        cudaError_t e = cudaMemsetAsync(p.counts + p.first_input, 0, p.num_inputs * 4u, s);
+        if (e != cudaSuccess) return e;
+    }
+    k_inhibit<<<dim3(p.num_inputs, parts), threads, smem, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -391,8 +520,18 @@ cudaError_t launch_learn(const PerInputParams& p, uint32_t input, cudaStream_t s
     return cudaGetLastError();
 }
 
-cudaError_t launch_full(const PerInputParams& p, uint32_t input, cudaStream_t s) {
-    k_full<<<1, 1024, 0, s>>>(p, input);
+cudaError_t launch_full(const PerInputParams& p, uint32_t input, cudaStream_t s, uint32_t* launches) {
+    const uint32_t C32 = p.g.C32;
+    if (C32 < 4096u || std::getenv("SP_FULL_ONE_CTA")) {
+        k_full<<<1, 1024, 0, s>>>(p, input);
+        *launches = 1;
+        return cudaGetLastError();
+    }
+    const uint32_t nb = C32 / 32u;
+    k_full_a<<<(C32 + 1023u) / 1024u, 1024, 0, s>>>(p, input);
+    const uint32_t G = std::min<uint32_t>(148u, (p.g.C + 255u) / 256u);
+    k_full_b<<<G, 1024, 2u * wmax_levels(nb) * nb * 4u, s>>>(p);
+    *launches = 2;
     return cudaGetLastError();
 }
 
@@ -402,7 +541,10 @@ cudaError_t launch_span(const uint32_t* idx, const float* perm, float tau, uint3
     return cudaGetLastError();
 }
 
-size_t full_scratch_floats(uint32_t C32) { return 2u * C32 + wmax_levels(C32 / 32u) * (C32 / 32u) + 32u; }
+size_t full_scratch_floats(uint32_t C32) {
+    const size_t nb = C32 / 32u;
+    return std::max<size_t>(2u * C32 + wmax_levels(nb) * nb + 32u, 4u * C32 + 2u * nb + 8u);
+}
 
 cudaError_t launch_build_syn(const uint32_t* idx, const float* perm, float tau, uint32_t C,
                              uint32_t C32, uint32_t S, uint32_t* syn, cudaStream_t s) {

@@ -201,3 +201,22 @@ def test_learning_stream_longer_than_a_prepack_chunk(full):
         check_state(sp, ora)
     else:
         assert np.array_equal(sp.get_state()[1].view(np.uint32), ora.perm.view(np.uint32))
+
+
+def test_full_learning_many_columns_per_input_path():
+    # C32 >= 4096: the per-input path splits inhibition over CTAs and runs the full-learning
+    # steps as the two-launch multi-CTA variant; the radius adapts from 100 towards C/2
+    cfg = ocfg(full_learning=True, input_width=64, input_height=48, num_columns=4100,
+               synapses_per_column=48, min_overlap=3, winners_set_size=25, inhibition_radius=100,
+               duty_cycle_period=20)
+    state = perturbed_state(cfg)
+    frames = sp_inputs.frames(314, 0, 6, 48, 64, rho=0.4)
+    ora = O.SpatialPoolerOracle(cfg, state)
+    adc, odc = seeded_duty(41, cfg.num_columns), seeded_duty(42, cfg.num_columns)
+    ora.active_duty, ora.overlap_duty = adc.copy(), odc.copy()
+    results = ora.compute(frames, learning=True)
+    sp = make_sp(cfg, state, "input", max_inputs=8)
+    sp.set_learning_state(adc, odc, 100)
+    check_inputs(results, *run(sp, frames, True))
+    check_state(sp, ora)
+    assert ora.radius != 100
