@@ -560,6 +560,32 @@ uint32_t inhibit_parts(const sp_handle* h, uint32_t inputs) {
     return std::max(1u, std::min(want, g.ncw / 4u));
 }
 
+// Scratch for the bit-planes a learning chunk prepacks: sized once for the largest chunk a call
+// can have (the allocation synchronises).
+sp_status ensure_prepack_scratch(sp_handle* h, uint32_t fpc, uint32_t n_frames, uint32_t Wn4) {
+    const sp::Geometry& g = h->g;
+    if (h->bits_all_cap >= std::min(fpc, n_frames) * g.P) return SP_OK;
+    const uint32_t cap = std::min(fpc * g.P, std::max(h->cfg.max_inputs / g.P, 1u) * g.P);
+    if (h->d_bits_all) cudaFree(h->d_bits_all), h->d_bits_all = nullptr;
+    const cudaError_t e = dalloc(&h->d_bits_all, static_cast<size_t>(cap) * Wn4);
+    if (e != cudaSuccess) return fail(SP_E_OOM, "prepacked bit-planes: %s", cudaGetErrorString(e));
+    h->bits_all_cap = cap;
+    return SP_OK;
+}
+
+// k_pack of a chunk's inputs into the prepacked planes (stride Wn4 words)
+cudaError_t launch_prepack(sp_handle* h, const uint8_t* frames, uint32_t inputs, uint32_t Wn4, cudaStream_t s) {
+    sp::PerInputParams pk{};
+    pk.frames = frames;
+    pk.num_inputs = inputs;
+    pk.g = h->g;
+    pk.bits = h->d_bits_all;
+    pk.Wn = h->Wn;
+    pk.bits_stride = Wn4;
+    h->launches++;
+    return sp::launch_pack(pk, s);
+}
+
 // Full-learning constants and device state (R17-R21) for the learning kernels.
 sp::FullLearn full_learn_params(const sp_handle* h) {
     sp::FullLearn f{};
@@ -712,9 +738,30 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         q.boosted_out = rec ? h->d_boosted_rec : nullptr;
         if (const char* d = std::getenv("SP_LEARN_DBG")) q.dbg = static_cast<uint32_t>(std::atoi(d));
         q.trace = h->d_trace;
-        e = sp::launch_learn_grid(q, h->grid_smem, s);
-        h->launches++;
-        if (e != cudaSuccess) return cuda_fail(e, "grid learning launch");
+        // bit-planes prepacked per chunk by k_pack (as for the cluster kernel)
+        const uint32_t Wn4 = (h->Wn + 3u) / 4u * 4u;
+        const bool prepack = !std::getenv("SP_NO_PREPACK");
+        const uint32_t fpc = prepack ? std::max<uint32_t>(1u, kPrepackInputs / g.P) : n_frames;
+        if (prepack) {
+            sp_status st = ensure_prepack_scratch(h, fpc, n_frames, Wn4);
+            if (st != SP_OK) return st;
+        }
+        for (uint32_t f0 = 0; f0 < n_frames; f0 += fpc) {
+            const uint32_t nf = std::min(fpc, n_frames - f0);
+            sp::LearnGridParams qc = q;
+            qc.frames = frames + static_cast<size_t>(f0) * g.W * g.H;
+            qc.first_input = row0 + f0 * g.P;
+            qc.num_inputs = nf * g.P;
+            if (prepack) {
+                e = launch_prepack(h, qc.frames, qc.num_inputs, Wn4, s);
+                if (e != cudaSuccess) return cuda_fail(e, "prepack launch");
+                qc.bits_g = h->d_bits_all;
+                qc.prepacked = 1u;
+            }
+            e = sp::launch_learn_grid(qc, h->grid_smem, s);
+            h->launches++;
+            if (e != cudaSuccess) return cuda_fail(e, "grid learning launch");
+        }
         h->ell_dirty = true;
         h->syn_dirty = true;
         h->last_plan.path = SP_PATH_PER_INPUT;
@@ -767,13 +814,9 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         const uint32_t Wn4 = (h->Wn + 3u) / 4u * 4u;
         const bool prepack = !std::getenv("SP_NO_PREPACK");
         const uint32_t fpc = prepack ? std::max<uint32_t>(1u, kPrepackInputs / g.P) : n_frames;
-        const uint32_t cap = std::min(fpc * g.P, std::max(h->cfg.max_inputs / g.P, 1u) * g.P);
-        if (prepack && h->bits_all_cap < std::min(fpc, n_frames) * g.P) {
-            // sized once for the largest chunk a call can have (allocation synchronises)
-            if (h->d_bits_all) cudaFree(h->d_bits_all), h->d_bits_all = nullptr;
-            e = dalloc(&h->d_bits_all, static_cast<size_t>(cap) * Wn4);
-            if (e != cudaSuccess) return fail(SP_E_OOM, "prepacked bit-planes: %s", cudaGetErrorString(e));
-            h->bits_all_cap = cap;
+        if (prepack) {
+            sp_status st = ensure_prepack_scratch(h, fpc, n_frames, Wn4);
+            if (st != SP_OK) return st;
         }
         for (uint32_t f0 = 0; f0 < n_frames; f0 += fpc) {
             const uint32_t nf = std::min(fpc, n_frames - f0);
@@ -782,15 +825,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
             qc.first_input = row0 + f0 * g.P;
             qc.num_inputs = nf * g.P;
             if (prepack) {
-                sp::PerInputParams pk{};
-                pk.frames = qc.frames;
-                pk.num_inputs = qc.num_inputs;
-                pk.g = g;
-                pk.bits = h->d_bits_all;
-                pk.Wn = h->Wn;
-                pk.bits_stride = Wn4;
-                e = sp::launch_pack(pk, s);
-                h->launches++;
+                e = launch_prepack(h, qc.frames, qc.num_inputs, Wn4, s);
                 if (e != cudaSuccess) return cuda_fail(e, "prepack launch");
                 qc.bits_g = h->d_bits_all;
                 qc.prepacked = 1u;

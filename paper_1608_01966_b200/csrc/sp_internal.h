@@ -161,7 +161,9 @@ struct LearnGridParams {
     float* perm;               // [C][S]
     const uint32_t* bc;        // [C32]
     const float* boost;        // [C32]
-    uint32_t* bits_g;          // [2][Wn rounded to 4] bit-planes, by input parity
+    uint32_t* bits_g;          // [2][Wn rounded to 4] bit-planes, by input parity, or
+                               // [num_inputs][Wn rounded to 4] planes prepacked by k_pack
+    uint32_t prepacked;        // bits_g holds every input's plane
     uint16_t* raw_g;           // [2][C32] raw counts, by input parity
     uint32_t* gbar;            // grid barrier counter (zeroed before the launch)
     uint32_t* sdr;             // [rows][ncw]

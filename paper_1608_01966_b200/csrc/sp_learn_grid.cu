@@ -95,7 +95,13 @@ __global__ void __launch_bounds__(kGridThreads, 1) sp_learn_grid_kernel(const __
     uint64_t* s_ties = reinterpret_cast<uint64_t*>(s_sdr + (p.own_words + 1u) / 2u * 2u);  // [own][64]
     uint16_t* s_rw = reinterpret_cast<uint16_t*>(s_ties + p.own_words * 64u);      // [win*32]
     auto bits_of = [&](uint32_t t) { return s_bits + (p.dbl_bits ? (t & 1u) * Wn4 : 0u); };
-    auto gbits_of = [&](uint32_t t) { return p.bits_g + (t & 1u) * Wn4; };
+    const uint32_t pb0_ = b * Wn / G, pb1_ = (b + 1u) * Wn / G;  // packed words of this CTA
+    // global bit-planes: prepacked by k_pack for the whole launch, or two by input parity
+    auto gbits_of = [&](uint32_t t) { return p.bits_g + (p.prepacked ? t : (t & 1u)) * Wn4; };
+    auto prefetch = [&](uint32_t t) {  // L2 prefetch ahead of use (thread 0)
+        if (!p.prepacked) prefetch_input(p, t, pb0_, pb1_, b, G);
+        else if (b == 0 && t < n) prefetch_l2(gbits_of(t), Wn4 * 4u);
+    };
     const uint32_t* my_syn = p.synT + static_cast<size_t>(c0) * S;
     const uint32_t bits_bytes = (Wn * 4u + 15u) & ~15u;
     // phase timers of CTA 0 / thread 0 (SP_TRACE): [0] start..bits ready, [1] overlap,
@@ -114,12 +120,11 @@ __global__ void __launch_bounds__(kGridThreads, 1) sp_learn_grid_kernel(const __
     if (p.uniform_bc == 0u || R == 0u)
         for (uint32_t i = tid; i < nwin * 32u; i += nthr) s_bcw[i] = p.bc[cwin + i];
     for (uint32_t i = b * nthr + tid; i < n; i += G * nthr) p.counts[p.first_input + i] = 0u;
-    const uint32_t pb0 = b * Wn / G, pb1 = (b + 1u) * Wn / G;  // packed words of this CTA
     if (tid == 0) {
-        prefetch_input(p, 0, pb0, pb1, b, G);
-        prefetch_input(p, 1, pb0, pb1, b, G);
+        prefetch(0);
+        prefetch(1);
     }
-    if (n > 0) pack_slice(p, 0, pb0, pb1, gbits_of(0), 0, nthr);
+    if (n > 0 && !p.prepacked) pack_slice(p, 0, pb0_, pb1_, gbits_of(0), 0, nthr);
     uint32_t nbar = 0;  // grid barriers passed
     grid_barrier(p.gbar, ++nbar * G);
     uint32_t bits_phase = 0, cc = 0;  // s_bar_bits parity; chunks consumed
@@ -140,10 +145,10 @@ __global__ void __launch_bounds__(kGridThreads, 1) sp_learn_grid_kernel(const __
             for (uint32_t j = 0; j < min(stages, nchunks); ++j)
                 bulk_copy(s_ring + ((cc + j) % stages) * chunk_words, my_syn + static_cast<size_t>(j) * chunk_words,
                           chunk_words * 4u, &s_bar_ring[(cc + j) % stages]);
-            prefetch_input(p, t + 2u, pb0, pb1, b, G);
+            prefetch(t + 2u);
         }
         // ---- a1: this CTA's share of input t+1 -> global plane (read after the barrier) ----
-        if (t + 1u < n) pack_slice(p, t + 1u, pb0, pb1, gbits_of(t + 1u), 0, nthr);
+        if (t + 1u < n && !p.prepacked) pack_slice(p, t + 1u, pb0_, pb1_, gbits_of(t + 1u), 0, nthr);
         for (uint32_t i = tid; i < ncols; i += nthr) s_craw[i] = 0u;
         mbar_wait(&s_bar_bits, bits_phase);
         bits_phase ^= 1u;
