@@ -288,6 +288,15 @@ __global__ void __launch_bounds__(kLearnThreads, 1) sp_learn_cluster_kernel(cons
                     emit_word(p, s_sdr, cw, gcw, gin, word, lane);
                 }
             }
+        } else if (p.prepacked && p.uniform_bc && g.S + 4u <= max(g.ncw * 16u, 512u) && !(p.dbg & 64u)) {
+            // uniform boost, no packing to overlap: the whole CTA builds the raw histogram
+            const UniformSel us = global_uniform_cta(raw_t, g.C, g.S, p.k, uniform_r_lo(theta, s_bc[0]), s_planes);
+            for (uint32_t cw = wi; cw < ncl; cw += nw) {
+                const uint32_t gcw = c0 / 32u + cw;
+                uint32_t word = 0u;
+                if (gcw < g.ncw) word = global_uniform_word_sel(raw_t, g.C, gcw, us, lane);
+                emit_word(p, s_sdr, cw, gcw, gin, word, lane);
+            }
         } else if (p.prepacked && !p.uniform_bc && !(p.dbg & 64u)) {
             // per-column boosts and no packing to overlap: the whole CTA selects (two-level
             // radix select, sp_select.cuh) instead of one warp per owned word

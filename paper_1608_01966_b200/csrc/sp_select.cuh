@@ -630,6 +630,75 @@ __device__ __forceinline__ GlobalSel global_select_cta(const RowT* row, const ui
     return r;
 }
 
+// Global k-winners with a uniform boost by a whole CTA: a histogram of the eligible raw counts
+// (shared atomics), one warp scans it from the top for r* (the k-th largest raw); the winners
+// are raw > r* plus the first `need` columns (by index) with raw == r* (R6, R7).  Every thread
+// of the CTA calls it (barriers).  hist: >= S + 4 words of shared scratch.
+struct UniformSel {
+    uint32_t rgt;   // raw >= rgt wins outright
+    uint32_t rtie;  // raw == rtie wins for the `need` lowest indices (0xFFFFFFFF: none)
+    uint32_t need;
+};
+
+template <typename RowT>
+__device__ __forceinline__ UniformSel global_uniform_cta(const RowT* row, uint32_t C, uint32_t S, uint32_t k,
+                                                         uint32_t r_lo, uint32_t* hist) {
+    const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u;
+    uint32_t* misc = hist + S + 1u;  // [3]
+    for (uint32_t v = tid; v <= S; v += nthr) hist[v] = 0u;
+    __syncthreads();
+    for (uint32_t c = tid; c < C; c += nthr) {
+        const uint32_t x = row[c];
+        if (x >= r_lo) atomicAdd(&hist[x], 1u);
+    }
+    __syncthreads();
+    if (tid < 32u) {
+        // lane owns bins [lane*per, (lane+1)*per); suffix counts from the top
+        const uint32_t per = (S + 32u) / 32u;
+        uint32_t sum = 0;
+        for (uint32_t j = 0; j < per; ++j) {
+            const uint32_t v = lane * per + j;
+            sum += v <= S ? hist[v] : 0u;
+        }
+        uint32_t above = sum;  // inclusive suffix over lanes >= lane
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_down_sync(0xffffffffu, above, d);
+            if (lane + d < 32u) above += o;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, above, 0);
+        uint32_t hi_above = above - sum, found = 0xFFFFFFFFu, f_above = 0;
+        for (int j = static_cast<int>(per) - 1; j >= 0; --j) {
+            const uint32_t v = lane * per + static_cast<uint32_t>(j);
+            const uint32_t h = v <= S ? hist[v] : 0u;
+            if (found == 0xFFFFFFFFu && hi_above < k && hi_above + h >= k) found = v, f_above = hi_above;
+            hi_above += h;
+        }
+        const uint32_t who = __ballot_sync(0xffffffffu, found != 0xFFFFFFFFu);
+        if (total < k) {  // fewer than k eligible: all of them win
+            if (lane == 0) misc[0] = r_lo, misc[1] = 0xFFFFFFFFu, misc[2] = 0u;
+        } else if (who && lane == static_cast<uint32_t>(__ffs(who) - 1)) {
+            misc[0] = found + 1u, misc[1] = found, misc[2] = k - f_above;
+        }
+    }
+    __syncthreads();
+    return UniformSel{misc[0], misc[1], misc[2]};
+}
+
+// SDR word gcw from a UniformSel (all lanes of a warp call it)
+template <typename RowT>
+__device__ __forceinline__ uint32_t global_uniform_word_sel(const RowT* row, uint32_t C, uint32_t gcw,
+                                                            const UniformSel& u, uint32_t lane) {
+    uint32_t before = 0;  // ties at raw == rtie in lower column-words
+    for (uint32_t d = lane; d < gcw * 32u; d += 32u) before += row[d] == u.rtie ? 1u : 0u;
+    before = __reduce_add_sync(0xffffffffu, before);
+    const uint32_t c = gcw * 32u + lane;
+    const uint32_t r = c < C ? static_cast<uint32_t>(row[c]) : 0u;
+    const uint32_t tb = __ballot_sync(0xffffffffu, r == u.rtie && c < C);
+    return __ballot_sync(0xffffffffu, c < C && (r >= u.rgt ||
+                                                (r == u.rtie && before + __popc(tb & ((1u << lane) - 1u)) < u.need)));
+}
+
 // SDR word cw from a GlobalSel (all lanes of a warp call it)
 template <typename RowT>
 __device__ __forceinline__ uint32_t global_select_word(const RowT* row, const uint32_t* bc, uint32_t theta, uint32_t C,
