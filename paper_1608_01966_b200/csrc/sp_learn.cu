@@ -97,8 +97,10 @@ __device__ __forceinline__ void overlap_step(const LearnParams& p, cg::cluster_g
         uint32_t raw = (r0 + r1) + (r2 + r3);
         for (uint32_t d = tpc >> 1; d > 0; d >>= 1) raw += __shfl_xor_sync(0xffffffffu, raw, d);
         const uint32_t c = c0 + cl;
+        // the tpc lanes of a column all hold its count: they share the Q remote stores
+        if (cl < cpc && c < g.C32)
+            for (uint32_t r = part; r < Q; r += tpc) cluster.map_shared_rank(raw_buf, r)[c] = static_cast<uint16_t>(raw);
         if (part == 0 && cl < cpc && c < g.C32) {
-            for (uint32_t r = 0; r < Q; ++r) cluster.map_shared_rank(raw_buf, r)[c] = static_cast<uint16_t>(raw);
             if (p.raw_out && c < g.C) {
                 p.raw_out[static_cast<size_t>(gin) * g.C + c] = static_cast<uint16_t>(raw);
                 // boost = Bc * 2^-23 exactly (Bc has <= 24 significant bits); the boost in

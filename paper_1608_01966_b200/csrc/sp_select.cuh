@@ -690,6 +690,7 @@ template <typename RowT>
 __device__ __forceinline__ uint32_t global_uniform_word_sel(const RowT* row, uint32_t C, uint32_t gcw,
                                                             const UniformSel& u, uint32_t lane) {
     uint32_t before = 0;  // ties at raw == rtie in lower column-words
+#pragma unroll 8
     for (uint32_t d = lane; d < gcw * 32u; d += 32u) before += row[d] == u.rtie ? 1u : 0u;
     before = __reduce_add_sync(0xffffffffu, before);
     const uint32_t c = gcw * 32u + lane;
