@@ -471,8 +471,8 @@ __device__ __forceinline__ uint32_t local_general_word15(const RowT* row, const 
 // atomics), then the columns tied at the threshold Tu: if none of them is lossy they all have
 // the same N and the lowest indices win (a prefix count over the tie masks); otherwise the
 // need-th largest exact key T2 among them is found (a tie list, or a bitwise search with CTA
-// counts when the list overflows).  Every thread of the CTA must call it (barriers).
-// scratch: >= 400 + 2*ncw + 1 words; ties: tie_cap keys.
+// counts when the list overflows).  Every thread of the CTA must call it (barriers);
+// C <= 4 * blockDim.x.  scratch: >= 400 + 2*ncw + 1 words; ties: tie_cap keys.
 struct GlobalSel {
     uint32_t Tu;     // coarse threshold (0: fewer than k eligible columns, all eligible win)
     uint32_t need;   // winners among the columns with u == Tu
@@ -492,12 +492,19 @@ __device__ __forceinline__ GlobalSel global_select_cta(const RowT* row, const ui
     uint32_t* tmask = scratch + 400;   // [ncw]
     uint32_t* tscan = tmask + ncw;     // [ncw + 1]
     for (uint32_t i = tid; i < 400u; i += nthr) scratch[i] = 0u;
-    __syncthreads();
-    for (uint32_t c = tid; c < C; c += nthr) {
+    // the coarse keys of this thread's columns (c = tid + j*nthr), kept for both histograms
+    constexpr int kMaxPer = 4;  // C <= 4 * blockDim.x (cluster learning: C32 <= 2048, 512 threads)
+    uint32_t uc[kMaxPer];
+#pragma unroll
+    for (int j = 0; j < kMaxPer; ++j) {
+        const uint32_t c = tid + j * nthr;
         bool lossy;
-        const uint32_t u = coarse_u15(eligible_N(row[c], bc[c], theta), m, lossy);
-        if (u) atomicAdd(&h1[(u - 1u) >> 7], 1u);
+        uc[j] = c < C ? coarse_u15(eligible_N(row[c], bc[c], theta), m, lossy) : 0u;
     }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kMaxPer; ++j)
+        if (uc[j]) atomicAdd(&h1[(uc[j] - 1u) >> 7], 1u);
     __syncthreads();
     if (wi == 0) {  // bucket of the k-th largest: suffix counts from the top, 8 bins per lane
         uint32_t v[8], sum = 0;
@@ -525,11 +532,9 @@ __device__ __forceinline__ GlobalSel global_select_cta(const RowT* row, const ui
     GlobalSel r{0u, 0u, 0u, 0ull};
     if (misc[0] < k) return r;  // fewer than k eligible: all of them win (Tu = 0)
     const uint32_t B1 = misc[1], above1 = misc[2];
-    for (uint32_t c = tid; c < C; c += nthr) {
-        bool lossy;
-        const uint32_t u = coarse_u15(eligible_N(row[c], bc[c], theta), m, lossy);
-        if (u && ((u - 1u) >> 7) == B1) atomicAdd(&h2[(u - 1u) & 127u], 1u);
-    }
+#pragma unroll
+    for (int j = 0; j < kMaxPer; ++j)
+        if (uc[j] && ((uc[j] - 1u) >> 7) == B1) atomicAdd(&h2[(uc[j] - 1u) & 127u], 1u);
     __syncthreads();
     if (wi == 0) {
         const uint32_t kk = k - above1;
