@@ -217,6 +217,52 @@ __device__ __forceinline__ void blur_frame(const EncParams& p, const uint8_t* gr
     }
 }
 
+// R23 + R24 for an exact 4:1 x scale and an even W1: one thread per pair of output pixels
+// (dx, dx+1) of a row, whose 8 source pixels are 24 contiguous bytes (three 8-byte loads).
+// Same operations and order as downscale_band's fast path (the x sums are exact).
+__device__ __forceinline__ uint32_t chan_sums(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t c) {
+    // B0 G0 R0 B1 | G1 R1 B2 G2 | R2 B3 G3 R3: byte masks of channel c in the three words
+    const uint32_t m0 = c == 0 ? 0x01000001u : (c == 1 ? 0x00000100u : 0x00010000u);
+    const uint32_t m1 = c == 0 ? 0x00010000u : (c == 1 ? 0x01000001u : 0x00000100u);
+    const uint32_t m2 = c == 0 ? 0x00000100u : (c == 1 ? 0x00010000u : 0x01000001u);
+    return __dp4a(w0, m0, __dp4a(w1, m1, __dp4a(w2, m2, 0u)));
+}
+
+__device__ __forceinline__ void downscale_band_pairs(const EncParams& p, const EncTables& t, uint32_t b,
+                                                     const uint8_t* buf, uint8_t* gray) {
+    const uint32_t dy0 = b * p.band_rows, dy1 = min(p.H1, dy0 + p.band_rows);
+    const uint32_t pairs = p.W1 / 2u;
+    const int32_t rb = static_cast<int32_t>(p.row_bytes);
+    const uint8_t* buf0 = buf - static_cast<int32_t>(p.band_sy0[b]) * rb;
+    for (uint32_t i = threadIdx.x; i < (dy1 - dy0) * pairs; i += blockDim.x) {
+        const uint32_t dy = dy0 + i / pairs, dx = 2u * (i % pairs);
+        const uint8_t* col = buf0 + 12u * dx;
+        const uint32_t j0 = t.yoff[dy], j1 = t.yoff[dy + 1];
+        float s[6];
+        for (uint32_t j = j0; j < j1; ++j) {
+            const uint2* w = reinterpret_cast<const uint2*>(col + static_cast<int32_t>(t.ysy[j]) * rb);
+            const uint2 a = w[0], bb = w[1], cc = w[2];
+            const float be = t.ybeta[j];  // beta / 4
+#pragma unroll
+            for (uint32_t ch = 0; ch < 3u; ++ch) {
+                const float ta = __fmul_rn(be, static_cast<float>(chan_sums(a.x, a.y, bb.x, ch)));
+                const float tb = __fmul_rn(be, static_cast<float>(chan_sums(bb.y, cc.x, cc.y, ch)));
+                if (j == j0) {
+                    s[ch] = ta, s[3 + ch] = tb;
+                } else {
+                    s[ch] = __fadd_rn(s[ch], ta), s[3 + ch] = __fadd_rn(s[3 + ch], tb);
+                }
+            }
+        }
+        int v[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) v[q] = min(255, max(0, __float2int_rn(s[q])));
+        const uint8_t g0 = static_cast<uint8_t>((3735 * v[0] + 19235 * v[1] + 9798 * v[2] + 16384) >> 15);
+        const uint8_t g1 = static_cast<uint8_t>((3735 * v[3] + 19235 * v[4] + 9798 * v[5] + 16384) >> 15);
+        *reinterpret_cast<uint16_t*>(gray + dy * p.W1 + dx) = static_cast<uint16_t>(g0 | (g1 << 8));
+    }
+}
+
 __global__ void __launch_bounds__(kEncThreads) k_encode(const __grid_constant__ EncParams p) {
     extern __shared__ __align__(128) uint8_t sm[];
     __shared__ __align__(8) uint64_t bars[kMaxStages];
@@ -269,7 +315,8 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const __grid_constant__ 
                 for (uint32_t k = threadIdx.x; k < bytes; k += blockDim.x) buf[k] = g[k];
                 __syncthreads();
             }
-            if (ty < ny) downscale_band(p, t, b, buf, gray, ty, tx, ny, sxs);
+            if (p.xfast && (p.W1 & 1u) == 0u) downscale_band_pairs(p, t, b, buf, gray);
+            else if (ty < ny) downscale_band(p, t, b, buf, gray, ty, tx, ny, sxs);
             __syncthreads();  // the stage is free; the band's gray rows are complete
             if (p.bulk && threadIdx.x == 0 && seq + p.stages < total) {
                 const uint32_t nx = seq + p.stages;
