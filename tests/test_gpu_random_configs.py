@@ -33,7 +33,21 @@ def draw(seed):
     full = bool(rng.random() < 0.4)
     boost = str(rng.choice(["uniform1", "uniform1.5", "seeded"]))
     rho = float(rng.choice([0.1, 0.5, 0.9]))
-    return dict(W=W, H=H, C=C, S=S, theta=theta, k=k, radius=radius, full=full, boost=boost, rho=rho)
+    grid = bool(rng.random() < 0.3)  # prefer the grid-resident learning kernel
+    return dict(W=W, H=H, C=C, S=S, theta=theta, k=k, radius=radius, full=full, boost=boost, rho=rho,
+                grid=grid, pw=0, ph=0)
+
+
+def draw_patch(seed):
+    d = draw(seed)
+    rng = np.random.default_rng(seed + 99)
+    d["pw"], d["ph"] = int(rng.choice([32, 64])), int(rng.choice([5, 10, 30]))
+    d["W"], d["H"] = d["pw"] * int(rng.integers(1, 4)), d["ph"] * int(rng.integers(1, 3))
+    d["S"] = int(min(d["pw"] * d["ph"], d["S"]))
+    d["theta"] = int(min(d["theta"], d["S"]))
+    d["C"] = int(min(d["C"], 1100))
+    d["k"] = int(min(d["k"], d["C"]))
+    return d
 
 
 def state_for(cfg, boost, seed):
@@ -54,20 +68,25 @@ def run(sp, frames, learn):
             boosted.cpu().numpy())
 
 
-@pytest.mark.parametrize("seed", range(64))
-def test_random_config(seed):
-    d = draw(1000 + seed)
+CASES = [("whole", s) for s in range(64)] + [("patch", s) for s in range(16)]
+
+
+@pytest.mark.parametrize("mode,seed", CASES)
+def test_random_config(mode, seed):
+    d = draw(1000 + seed) if mode == "whole" else draw_patch(5000 + seed)
     cfg = ocfg(input_width=d["W"], input_height=d["H"], num_columns=d["C"], synapses_per_column=d["S"],
                min_overlap=d["theta"], winners_set_size=d["k"], inhibition_radius=d["radius"],
-               full_learning=d["full"], duty_cycle_period=7)
+               full_learning=d["full"], duty_cycle_period=7, patch_width=d["pw"], patch_height=d["ph"])
     state = state_for(cfg, d["boost"], seed)
-    learn_frames = sp_inputs.frames(7000 + seed, 0, 5, d["H"], d["W"], rho=d["rho"], nonzero="random")
-    infer_frames = sp_inputs.frames(8000 + seed, 0, 35, d["H"], d["W"], rho=d["rho"])
+    nl, ni = (5, 35) if mode == "whole" else (2, 6)
+    learn_frames = sp_inputs.frames(7000 + seed, 0, nl, d["H"], d["W"], rho=d["rho"], nonzero="random")
+    infer_frames = sp_inputs.frames(8000 + seed, 0, ni, d["H"], d["W"], rho=d["rho"])
     ora = O.SpatialPoolerOracle(cfg, state)
     want_learn = ora.compute(learn_frames, learning=True)
     want_infer = [ora.step(x, False) for x in O.encode(infer_frames, cfg)]
-    flags = P.SP_FLAG_RECORD_OVERLAPS | (P.SP_FLAG_FULL_LEARNING if d["full"] else 0)
-    sp = P.SpatialPooler(**gpu_kwargs(cfg, max_inputs=64, flags=flags, duty_cycle_period=7))
+    flags = (P.SP_FLAG_RECORD_OVERLAPS | (P.SP_FLAG_FULL_LEARNING if d["full"] else 0) |
+             (P.SP_FLAG_LEARN_GRID if d["grid"] else 0))
+    sp = P.SpatialPooler(**gpu_kwargs(cfg, max_inputs=256, flags=flags, duty_cycle_period=7))
     sp.set_state(*state)
     for phase, want, frames, learn in (("learn", want_learn, learn_frames, True),
                                        ("infer", want_infer, infer_frames, False)):
