@@ -276,12 +276,12 @@ def main():
     gathered = torch.empty((F * world, words), dtype=torch.int32, device=dev) if world > 1 else None
 
     def step(ev=None):
+        # sp_compute_into: the kernel writes the winners straight into this rank's tensors
         if ev is not None:
             ev[0].record(stream)
-        sp.compute(frames, learn=False)
+        sp.compute_into(frames, sdr, counts, learn=False)
         if ev is not None:
             ev[1].record(stream)
-        sp.winners(sdr, counts)
         if world > 1:
             D.gather_sdrs(sdr, gathered)
 

@@ -178,6 +178,14 @@ sp_status sp_destroy(sp_handle* h);
 sp_status sp_compute(sp_handle* h, const uint8_t* frames_dev, uint32_t num_frames,
                      int learn, void* cuda_stream);
 
+/* sp_compute writing the winners straight into caller buffers (no copy afterwards):
+ *   sdr_dev:   uint32[num_frames * P][sdr_words], count_dev: uint32[num_frames * P], device
+ *              memory on the handle's device.  They stay the "last call's results" for
+ *              sp_winners / sp_histograms until the next compute call, so the caller keeps them
+ *              alive until then.  Errors: as sp_compute; SP_E_ARG for NULL buffers. */
+sp_status sp_compute_into(sp_handle* h, const uint8_t* frames_dev, uint32_t num_frames, int learn,
+                          uint32_t* sdr_dev, uint32_t* count_dev, void* cuda_stream);
+
 /* Copies the winners of the last sp_compute call:
  *   sdr_dev:   uint32[num_inputs][sdr_words]; bit c of word c/32 (LSB first)
  *              set iff column c is active (the SDR).

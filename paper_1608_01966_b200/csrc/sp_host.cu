@@ -363,6 +363,9 @@ struct sp_handle {
     uint32_t* d_raw = nullptr;
     uint32_t* d_sdr = nullptr;
     uint32_t* d_counts = nullptr;
+    // where the last call's results live: the handle's buffers, or the caller's (sp_compute_into)
+    uint32_t* res_sdr = nullptr;
+    uint32_t* res_counts = nullptr;
     uint16_t* d_raw_rec = nullptr;
     float* d_boosted_rec = nullptr;
     // end-to-end staging
@@ -661,8 +664,8 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         p.ell = h->d_ell;
         p.bc = h->d_bc;
         p.boost = h->d_boost;
-        p.sdr = h->d_sdr + static_cast<size_t>(row0) * g.ncw;
-        p.counts = h->d_counts + row0;
+        p.sdr = h->res_sdr + static_cast<size_t>(row0) * g.ncw;
+        p.counts = h->res_counts + row0;
         p.raw_out = rec ? h->d_raw_rec + static_cast<size_t>(row0) * g.C : nullptr;
         p.boosted_out = rec ? h->d_boosted_rec + static_cast<size_t>(row0) * g.C : nullptr;
         p.radius_dev = h->d_radius;
@@ -732,8 +735,8 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         q.bits_g = h->d_bits;
         q.raw_g = reinterpret_cast<uint16_t*>(h->d_raw);
         q.gbar = h->d_gbar;
-        q.sdr = h->d_sdr;
-        q.counts = h->d_counts;
+        q.sdr = h->res_sdr;
+        q.counts = h->res_counts;
         q.raw_out = rec ? h->d_raw_rec : nullptr;
         q.boosted_out = rec ? h->d_boosted_rec : nullptr;
         if (const char* d = std::getenv("SP_LEARN_DBG")) q.dbg = static_cast<uint32_t>(std::atoi(d));
@@ -803,8 +806,8 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         q.boost = h->d_boost;
         q.bits_g = h->d_bits;
         q.trace = h->d_trace;
-        q.sdr = h->d_sdr;
-        q.counts = h->d_counts;
+        q.sdr = h->res_sdr;
+        q.counts = h->res_counts;
         q.raw_out = rec ? h->d_raw_rec : nullptr;
         q.boosted_out = rec ? h->d_boosted_rec : nullptr;
         q.fl = full_learn_params(h);
@@ -871,8 +874,8 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         p.bc = h->d_bc;
         p.boost = h->d_boost;
         p.raw = h->d_raw;
-        p.sdr = h->d_sdr;
-        p.counts = h->d_counts;
+        p.sdr = h->res_sdr;
+        p.counts = h->res_counts;
         p.raw_out = rec ? h->d_raw_rec : nullptr;
         p.boosted_out = rec ? h->d_boosted_rec : nullptr;
         p.radius_dev = h->d_radius;
@@ -1091,6 +1094,8 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
         return st;
     }
     h->last_plan = make_plan(h, cfg->max_inputs, false, nullptr);
+    h->res_sdr = h->d_sdr;
+    h->res_counts = h->d_counts;
     *out = h;
     return SP_OK;
 }
@@ -1114,6 +1119,26 @@ sp_status sp_compute(sp_handle* h, const uint8_t* frames_dev, uint32_t num_frame
     if (num_frames > 0 && !frames_dev) return fail(SP_E_ARG, "frames_dev is NULL");
     h->last_inputs = static_cast<uint32_t>(n);
     h->has_result = true;
+    h->res_sdr = h->d_sdr;
+    h->res_counts = h->d_counts;
+    if (n == 0) return SP_OK;
+    return compute_impl(h, frames_dev, num_frames, learn, static_cast<cudaStream_t>(cuda_stream), 0);
+}
+
+sp_status sp_compute_into(sp_handle* h, const uint8_t* frames_dev, uint32_t num_frames, int learn, uint32_t* sdr_dev,
+                          uint32_t* count_dev, void* cuda_stream) {
+    sp_status st = check_handle(h);
+    if (st != SP_OK) return st;
+    const uint64_t n = static_cast<uint64_t>(num_frames) * h->g.P;
+    if (n > h->cfg.max_inputs)
+        return fail(SP_E_ARG, "num_frames * inputs_per_frame = %llu exceeds max_inputs %u",
+                    static_cast<unsigned long long>(n), h->cfg.max_inputs);
+    if (num_frames > 0 && (!frames_dev || !sdr_dev || !count_dev))
+        return fail(SP_E_ARG, "frames_dev, sdr_dev and count_dev must be non-NULL");
+    h->last_inputs = static_cast<uint32_t>(n);
+    h->has_result = true;
+    h->res_sdr = sdr_dev;
+    h->res_counts = count_dev;
     if (n == 0) return SP_OK;
     return compute_impl(h, frames_dev, num_frames, learn, static_cast<cudaStream_t>(cuda_stream), 0);
 }
@@ -1125,11 +1150,12 @@ sp_status sp_winners(sp_handle* h, uint32_t* sdr_dev, uint32_t* count_dev, void*
     if (h->last_inputs == 0) return SP_OK;
     if (!sdr_dev) return fail(SP_E_ARG, "sdr_dev is NULL");
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
-    cudaError_t e = cudaMemcpyAsync(sdr_dev, h->d_sdr,
+    if (sdr_dev == h->res_sdr && (!count_dev || count_dev == h->res_counts)) return SP_OK;  // already there
+    cudaError_t e = cudaMemcpyAsync(sdr_dev, h->res_sdr,
                                     static_cast<size_t>(h->last_inputs) * h->g.ncw * 4u,
                                     cudaMemcpyDeviceToDevice, s);
     if (e == cudaSuccess && count_dev)
-        e = cudaMemcpyAsync(count_dev, h->d_counts, h->last_inputs * 4u, cudaMemcpyDeviceToDevice, s);
+        e = cudaMemcpyAsync(count_dev, h->res_counts, h->last_inputs * 4u, cudaMemcpyDeviceToDevice, s);
     if (e != cudaSuccess) return cuda_fail(e, "sp_winners copy");
     return SP_OK;
 }
@@ -1245,7 +1271,7 @@ sp_status sp_histograms(sp_handle* h, const uint32_t* video_offsets_host, uint32
         h->h_hist_off.assign(video_offsets_host, video_offsets_host + num_videos + 1u);
     }
     uint32_t nl = 0;
-    e = sp::launch_histograms(h->d_sdr, h->g.ncw, h->g.C, h->d_hist_off, num_videos, longest, h->sm_count, counts,
+    e = sp::launch_histograms(h->res_sdr, h->g.ncw, h->g.C, h->d_hist_off, num_videos, longest, h->sm_count, counts,
                               hist_dev, s, &nl);
     h->launches += nl;
     if (e != cudaSuccess) return cuda_fail(e, "histogram launch");
@@ -1297,6 +1323,8 @@ sp_status sp_compute_host(sp_handle* h, const uint8_t* frames_host, uint32_t num
         return fail(SP_E_ARG, "num_frames * inputs_per_frame = %llu exceeds max_inputs %u",
                     static_cast<unsigned long long>(n), h->cfg.max_inputs);
     if (num_frames > 0 && (!frames_host || !sdr_host)) return fail(SP_E_ARG, "NULL host buffer");
+    h->res_sdr = h->d_sdr;  // results staged in the handle's buffers
+    h->res_counts = h->d_counts;
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     const size_t frame_bytes = static_cast<size_t>(g.W) * g.H;
     cudaError_t e = cudaSuccess;

@@ -39,7 +39,7 @@ ABI_SYMBOLS = ("sp_config_default", "sp_create", "sp_destroy", "sp_compute", "sp
                "sp_overlaps", "sp_get_state", "sp_set_state", "sp_compute_host", "sp_plan",
                "sp_init_pools_host", "sp_get_info", "sp_last_error", "sp_version",
                "sp_get_learning_state", "sp_set_learning_state", "sp_histograms",
-               "sp_synth_frames", "sp_synth_bgr_frames", "sp_encoder_config_default",
+               "sp_compute_into", "sp_synth_frames", "sp_synth_bgr_frames", "sp_encoder_config_default",
                "sp_encoder_create", "sp_encoder_destroy", "sp_encode", "sp_encoder_get_info",
                "sp_encoder_last_error")
 
@@ -116,6 +116,7 @@ def lib() -> ctypes.CDLL:
         "sp_create": [P(SpConfig), P(vp)],
         "sp_destroy": [vp],
         "sp_compute": [vp, vp, u32, ctypes.c_int, vp],
+        "sp_compute_into": [vp, vp, u32, ctypes.c_int, vp, vp, vp],
         "sp_winners": [vp, vp, vp, vp],
         "sp_overlaps": [vp, vp, vp, vp],
         "sp_get_state": [vp, vp, vp, vp],
@@ -328,7 +329,25 @@ class SpatialPooler:
         _check(lib().sp_compute(self._h, ctypes.c_void_p(frames.data_ptr()), F, int(bool(learn)),
                                 _stream_ptr(stream, frames.device)))
         self.last_num_inputs = F * self.inputs_per_frame
+        self._res = None
         return self.last_num_inputs
+
+    def compute_into(self, frames, sdr, counts, learn: bool = False, stream=None) -> int:
+        """``compute`` with the winners written straight into ``sdr`` (int32 [n, words]) and
+        ``counts`` (int32 [n]) cuda tensors (no copy afterwards)."""
+        import torch
+        _require(frames, torch.uint8, self.device, name="frames")
+        if frames.dim() != 3 or tuple(frames.shape[1:]) != self.frame_shape:
+            raise SpError(SP_E_SHAPE, f"frames must be [F, {self.frame_shape[0]}, {self.frame_shape[1]}]")
+        n = frames.shape[0] * self.inputs_per_frame
+        _require(sdr, torch.int32, self.device, (n, self.sdr_words), "sdr")
+        _require(counts, torch.int32, self.device, (n,), "counts")
+        _check(lib().sp_compute_into(self._h, ctypes.c_void_p(frames.data_ptr()), frames.shape[0],
+                                     int(bool(learn)), ctypes.c_void_p(sdr.data_ptr()),
+                                     ctypes.c_void_p(counts.data_ptr()), _stream_ptr(stream, frames.device)))
+        self.last_num_inputs = n
+        self._res = (sdr, counts)  # keep the result buffers alive until the next call
+        return n
 
     def winners(self, sdr=None, counts=None, stream=None):
         """SDRs of the last call: (uint32 [n, words] as int32 view, int32 [n]) cuda tensors."""

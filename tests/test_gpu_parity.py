@@ -409,3 +409,33 @@ def test_shape_errors():
         sp.compute(torch.zeros((2, 8, 8), dtype=torch.int32, device=DEV))
     with pytest.raises(P.SpError):
         sp.compute(torch.zeros((2, 8, 8), dtype=torch.uint8))
+
+
+def test_compute_into_writes_caller_buffers():
+    cfg = ocfg(input_width=48, input_height=37, num_columns=100, synapses_per_column=20, min_overlap=3,
+               winners_set_size=7)
+    state = perturbed_state(cfg)
+    frames = to_dev(sp_inputs.frames(2002, 0, 45, 37, 48, rho=0.5))
+    a = make_sp(cfg, state)
+    b = make_sp(cfg, state)
+    a.compute(frames)
+    want_sdr, want_cnt = a.winners()
+    sdr = torch.full((45, 4), -1, dtype=torch.int32, device=DEV)
+    cnt = torch.full((45,), -1, dtype=torch.int32, device=DEV)
+    b.compute_into(frames, sdr, cnt)
+    torch.cuda.synchronize()
+    assert torch.equal(sdr, want_sdr) and torch.equal(cnt, want_cnt)
+    s2, c2 = b.winners()  # copies from the caller's buffers
+    assert torch.equal(s2, want_sdr) and torch.equal(c2, want_cnt)
+    h1, _ = a.histograms([0, 20, 45])
+    h2, _ = b.histograms([0, 20, 45])
+    assert torch.equal(h1, h2)
+    # learning through compute_into (cluster kernel) writes the caller's buffers too
+    lf = to_dev(sp_inputs.frames(1001, 0, 6, 37, 48, rho=0.5))
+    a.compute(lf, learn=True)
+    ws, wc = a.winners()
+    s3 = torch.empty((6, 4), dtype=torch.int32, device=DEV)
+    c3 = torch.empty((6,), dtype=torch.int32, device=DEV)
+    b.compute_into(lf, s3, c3, learn=True)
+    torch.cuda.synchronize()
+    assert torch.equal(s3, ws) and torch.equal(c3, wc)
