@@ -32,15 +32,14 @@ __global__ void __launch_bounds__(256) k_hist_count(const uint32_t* __restrict__
     const uint32_t* p = sdr + cw;
     uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
     uint32_t i = b;
-    for (; i + 4u <= e; i += 4u) {  // four independent loads in flight
-        const uint32_t w0 = __ldg(p + static_cast<size_t>(i) * ncw);
-        const uint32_t w1 = __ldg(p + static_cast<size_t>(i + 1u) * ncw);
-        const uint32_t w2 = __ldg(p + static_cast<size_t>(i + 2u) * ncw);
-        const uint32_t w3 = __ldg(p + static_cast<size_t>(i + 3u) * ncw);
-        c0 += (w0 >> lane) & 1u;
-        c1 += (w1 >> lane) & 1u;
-        c2 += (w2 >> lane) & 1u;
-        c3 += (w3 >> lane) & 1u;
+    for (; i + 8u <= e; i += 8u) {  // eight independent loads in flight
+        uint32_t w[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) w[u] = __ldg(p + static_cast<size_t>(i + u) * ncw);
+        c0 += ((w[0] >> lane) & 1u) + ((w[4] >> lane) & 1u);
+        c1 += ((w[1] >> lane) & 1u) + ((w[5] >> lane) & 1u);
+        c2 += ((w[2] >> lane) & 1u) + ((w[6] >> lane) & 1u);
+        c3 += ((w[3] >> lane) & 1u) + ((w[7] >> lane) & 1u);
     }
     for (; i < e; ++i) c0 += (__ldg(p + static_cast<size_t>(i) * ncw) >> lane) & 1u;
     const uint32_t cnt = (c0 + c1) + (c2 + c3);
