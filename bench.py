@@ -56,6 +56,9 @@ def parse():
     ap.add_argument("--no-learn-full", action="store_true")
     ap.add_argument("--no-encoder", action="store_true")
     ap.add_argument("--encoder-frames", type=int, default=2048)
+    ap.add_argument("--overlap-gather", action="store_true",
+                    help="N > 1: all-gather of step i on NCCL's stream while step i+1 computes "
+                         "(SURVEY 8(e) streamed mode; double-buffered SDR tensors)")
     return ap.parse_args()
 
 
@@ -271,23 +274,38 @@ def main():
     frames = torch.empty((F, H, W), dtype=torch.uint8, device=dev)
     P.synth_frames(frames, F0, SEED_INFER, 0.5)
     words = sp.sdr_words
-    sdr = torch.empty((F, words), dtype=torch.int32, device=dev)
-    counts = torch.empty((F,), dtype=torch.int32, device=dev)
-    gathered = torch.empty((F * world, words), dtype=torch.int32, device=dev) if world > 1 else None
+    nbuf = 2 if (args.overlap_gather and world > 1) else 1
+    sdrs = [torch.empty((F, words), dtype=torch.int32, device=dev) for _ in range(nbuf)]
+    cnts = [torch.empty((F,), dtype=torch.int32, device=dev) for _ in range(nbuf)]
+    gath = [torch.empty((F * world, words), dtype=torch.int32, device=dev) for _ in range(nbuf)] \
+        if world > 1 else None
+    sdr, counts = sdrs[0], cnts[0]
+    works = []  # --overlap-gather: the all-gather of step i runs while step i+1 computes
 
-    def step(ev=None):
+    def step(i, ev=None):
         # sp_compute_into: the kernel writes the winners straight into this rank's tensors
+        b = i % nbuf
+        if nbuf > 1 and len(works) >= nbuf:
+            works[-nbuf].wait()  # the gather that read this buffer has finished
         if ev is not None:
             ev[0].record(stream)
-        sp.compute_into(frames, sdr, counts, learn=False)
+        sp.compute_into(frames, sdrs[b], cnts[b], learn=False)
         if ev is not None:
             ev[1].record(stream)
         if world > 1:
-            D.gather_sdrs(sdr, gathered)
+            if nbuf > 1:
+                works.append(dist.all_gather_into_tensor(gath[b], sdrs[b], async_op=True))
+            else:
+                D.gather_sdrs(sdrs[b], gath[b])
+
+    def drain():
+        while works:
+            works.pop(0).wait()
 
     warmup = max(args.warmup, 3)  # timing rule: W >= 3
-    for _ in range(warmup):
-        step()
+    for i in range(warmup):
+        step(i)
+    drain()
     torch.cuda.synchronize()
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
@@ -299,7 +317,8 @@ def main():
     with ClockSampler(local) as clk:
         t_start.record(stream)
         for i in range(args.steps):
-            step(kev[i])
+            step(i, kev[i])
+        drain()  # the last gathers are part of the timed work
         t_end.record(stream)
         torch.cuda.synchronize()
     launches = sp.kernel_launches() - launches0
@@ -436,7 +455,8 @@ def main():
             "config": {"workload": WORKLOAD, "frames_per_gpu": F, "global_batch": F * world,
                        "frame": f"{W}x{H}", "columns": C, "synapses": S, "min_overlap": THETA,
                        "winners_set_size": K_WIN, "inhibition": "global",
-                       "parallelism": f"dp{world} (frame shards; NCCL all-gather of SDRs)",
+                       "parallelism": f"dp{world} (frame shards; NCCL all-gather of SDRs"
+                                      f"{', overlapped with the next step' if nbuf > 1 else ''})",
                        "l2": "inputs larger than L2 (2.1 GB per GPU per step); no flush",
                        "plan": {k: plan[k] for k in ("groups", "cluster", "ctas", "window_bits",
                                                      "num_windows", "stages", "smem_bytes")}},
