@@ -76,7 +76,8 @@ enum {
  *   input_width, input_height >= 1; patch_width/patch_height both 0 (the
  *     whole frame is one SP input) or both >= 1 and dividing the frame dims;
  *   nbits = input bits per SP input = pw*ph (whole frame: W*H) <= 1,800,000;
- *   1 <= num_columns <= 65536; 1 <= synapses_per_column <= min(nbits, 4095);
+ *   1 <= num_columns <= 20480 (the per-input inhibition holds 10 bytes per column in one
+ *     CTA's shared memory); 1 <= synapses_per_column <= min(nbits, 4095);
  *   min_overlap <= synapses_per_column; 1 <= winners_set_size <= num_columns;
  *   perm_increment, perm_decrement, initial_permanence, connected_threshold in [0,1];
  *   ceil(log2(S+1)) + 27 + ceil(log2(C32)) <= 64 (the exact rank key fits 64 bits, R4);

@@ -95,8 +95,10 @@ sp_status validate(const sp_config* c) {
     if (nbits > kMaxInputBits)
         return fail(SP_E_CONFIG, "input bits per SP input (%llu) exceed %u",
                     static_cast<unsigned long long>(nbits), kMaxInputBits);
-    if (c->num_columns == 0 || c->num_columns > 65536)
-        return fail(SP_E_CONFIG, "num_columns must be in [1, 65536]");
+    // the per-input inhibition keeps raw counts, Bc and key bit-planes of every column in one
+    // CTA's shared memory (10 bytes per column)
+    if (c->num_columns == 0 || c->num_columns > 20480)
+        return fail(SP_E_CONFIG, "num_columns must be in [1, 20480]");
     if (c->synapses_per_column == 0 || c->synapses_per_column > 4095)
         return fail(SP_E_CONFIG, "synapses_per_column must be in [1, 4095]");
     if (c->synapses_per_column > nbits)

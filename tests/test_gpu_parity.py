@@ -439,3 +439,27 @@ def test_compute_into_writes_caller_buffers():
     b.compute_into(lf, s3, c3, learn=True)
     torch.cuda.synchronize()
     assert torch.equal(s3, ws) and torch.equal(c3, wc)
+
+
+@pytest.mark.parametrize("case", ["max_columns_global", "max_columns_local", "max_synapses", "max_bits"])
+def test_extreme_sizes(case):
+    # the largest configurations the ABI accepts run (per-input paths) and stay bit-exact
+    kw = dict(max_columns_global=dict(input_width=64, input_height=32, num_columns=20480,
+                                      synapses_per_column=24, min_overlap=3, winners_set_size=40),
+              max_columns_local=dict(input_width=64, input_height=32, num_columns=20480,
+                                     synapses_per_column=24, min_overlap=3, winners_set_size=40,
+                                     inhibition_radius=300),
+              max_synapses=dict(input_width=128, input_height=64, num_columns=64, synapses_per_column=4095,
+                                min_overlap=100, winners_set_size=5),
+              max_bits=dict(input_width=1500, input_height=1200, num_columns=96, synapses_per_column=64,
+                            min_overlap=4, winners_set_size=9))[case]
+    cfg = ocfg(**kw)
+    state = perturbed_state(cfg)
+    frames = sp_inputs.frames(606, 0, 3, cfg.input_height, cfg.input_width, rho=0.5)
+    ora = O.SpatialPoolerOracle(cfg, state)
+    want = ora.compute(frames, learning=True)
+    sp = make_sp(cfg, state, max_inputs=8)
+    check_results(want, *run_gpu(sp, frames, learn=True))
+    assert np.array_equal(sp.get_state()[1].view(np.uint32), ora.perm.view(np.uint32))
+    want2 = [ora.step(x, False) for x in O.encode(frames, cfg)]
+    check_results(want2, *run_gpu(sp, frames))
