@@ -136,8 +136,10 @@ struct LearnParams {
                                // [num_inputs][Wn rounded to 4] planes prepacked by k_pack
     uint32_t prepacked;        // bits_g holds every input's plane (no packing in the kernel)
     uint32_t dbl_bits;         // two smem bit-plane buffers (load of t+1 overlaps learning of t)
-    uint32_t dbg;              // development switches (SP_LEARN_DBG): 1 no proxy fence, 2 no prefetch,
-                               // 4 no pack, 8 no selection (timing experiments only)
+    uint32_t dbg;              // development switches (SP_LEARN_DBG, timing experiments only): 1 no proxy
+                               // fence, 2 no prefetch, 4 no pack, 8 no selection, 16 load the next plane
+                               // late, 32 packing loads via L2 (.cg), 64 warp-level global selection,
+                               // 128 no window split of the local selection
     uint64_t* trace;           // nullable [6] summed phase times of CTA 0 (development aid)
     uint32_t* sdr;             // [rows][ncw]
     uint32_t* counts;          // [rows]
