@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "sp_internal.h"
@@ -23,7 +24,7 @@ namespace sp {
 
 namespace {
 
-constexpr uint32_t kEncThreads = 512;
+constexpr uint32_t kEncThreads = 256;
 constexpr uint32_t kMaxStages = 4;
 
 struct EncParams {
@@ -480,13 +481,16 @@ sp_status sp_encoder_create(const sp_encoder_config* cfg, sp_encoder** out) {
     const uint32_t gray_bytes = (p.W1 * p.H1 + 127u) & ~127u;
     p.ny_entries = static_cast<uint32_t>(ysy.size());
     p.nx_entries = static_cast<uint32_t>(xsx.size());
-    p.table_bytes = 4u * (p.H1 + 1u + 2u * p.ny_entries + p.W1 + 1u + 2u * p.nx_entries);
+    // the x tables are only staged for the generic path (the 4:1 fast path does not read them)
+    p.table_bytes = 4u * (p.H1 + 1u + 2u * p.ny_entries + (p.xfast ? 0u : p.W1 + 1u + 2u * p.nx_entries));
     int static_smem = 0;
     {
         cudaFuncAttributes fa{};
         if (cudaFuncGetAttributes(&fa, sp::k_encode) == cudaSuccess) static_smem = static_cast<int>(fa.sharedSizeBytes);
     }
     uint32_t best_rows = 0, best_stages = 0, best_cps = 0, best_stage_bytes = 0;
+    const char* mc = std::getenv("SP_ENC_MAXCPS");  // development override (experiments)
+    const uint32_t max_cps = mc ? static_cast<uint32_t>(std::atoi(mc)) : 2u;
     std::vector<uint32_t> sy0, sn;
     for (uint32_t rows = 1; rows <= p.H1; ++rows) {
         uint32_t maxn = 0;
@@ -500,8 +504,8 @@ sp_status sp_encoder_create(const sp_encoder_config* cfg, sp_encoder** out) {
         for (uint32_t stages = sp::kMaxStages; stages >= 2; --stages) {
             const uint32_t smem = gray_bytes + stages * stage + p.table_bytes;
             if (static_cast<int>(smem) > max_smem - static_smem) continue;
-            const uint32_t cps = std::min<uint32_t>(2u, static_cast<uint32_t>(sm_smem) /
-                                                            (smem + static_smem + 1024u));
+            const uint32_t cps = std::min<uint32_t>(max_cps, static_cast<uint32_t>(sm_smem) /
+                                                                 (smem + static_smem + 1024u));
             if (cps == 0) continue;
             const bool better = cps > best_cps || (cps == best_cps && (rows > best_rows ||
                                                                          (rows == best_rows && stages > best_stages)));
