@@ -215,14 +215,18 @@ __device__ __forceinline__ uint64_t rank_key(uint32_t raw, uint32_t bc, uint32_t
 
 // a3/a4 for the inputs of this CTA: (cluster-sum of partial counts), exact keys, k-winners,
 // SDR.  Kept out of line so its register needs do not shape the streaming loop's allocation.
+// big / big_bytes: shared memory idle during the top-k (region plus, in the whole-frame kernel,
+// the ring behind the raw counts) for the per-column-boost wavelet.
 template <int CPT, uint32_t NW>
 __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawbuf, uint8_t* region,
+                                          uint8_t* big, uint32_t big_bytes,
                                           const uint32_t* s_bc, uint32_t in0, uint32_t gs,
                                           uint32_t rank, uint32_t K, uint32_t wi, uint32_t lane) {
     cg::cluster_group cluster = cg::this_cluster();
     const uint32_t theta = p.min_overlap, L = p.keyL;
     const uint64_t one = 1ull << 23;
-    const uint32_t radius = p.radius_dev ? *p.radius_dev : p.radius;  // adapted by full learning
+    uint32_t radius = p.radius_dev ? *p.radius_dev : p.radius;  // adapted by full learning
+    if (radius + 1u >= p.C) radius = 0u;  // every window holds all columns: global inhibition (R9)
     const uint32_t nbN = p.keyBits - L;             // significant bits of N
     const uint32_t sh = nbN > 16u ? nbN - 16u : 0u;  // coarse key u = N >> sh has <= 16 bits
     uint64_t* tie_list = reinterpret_cast<uint64_t*>(region) + wi * 64u;  // X window is idle now
@@ -326,6 +330,28 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             }
             if (lane == 0) p.counts[gin] = total;
             __syncwarp();  // planes are rewritten by this warp's next input
+            continue;
+        }
+        const uint32_t gwb = (4u * p.C32 + 2u * 16u * (p.ncw + 2u) * 4u + 127u) & ~127u;  // <= 15 levels + lossy
+        if (radius > 0 && radius >= p.wm_min_radius && gwb * NW <= big_bytes) {
+            // local inhibition, per-column boosts: wavelet matrix over the coarse keys + exact
+            // lossy ties (sp_select.cuh), O(C log 2^15) per input
+            uint8_t* base = big + wi * gwb;
+            uint16_t* b0 = reinterpret_cast<uint16_t*>(base);
+            uint2* lv = reinterpret_cast<uint2*>(base + 4u * p.C32);
+            const CoarseMap cm = coarse_map_warp(row, s_bc, theta, 0u, p.ncw, lane);
+            uint32_t total = 0, myword = 0;
+            local_general_wavelet(row, s_bc, p.C, p.C32, p.ncw, radius, p.k, theta, L, cm, b0, b0 + p.C32, lv,
+                                  lane, [&](uint32_t cw, uint32_t word) {
+                                      if ((cw & 31u) == lane) myword = word;
+                                      total += __popc(word);
+                                      if ((cw & 31u) == 31u || cw + 1u == p.ncw) {
+                                          const uint32_t w0 = cw & ~31u;
+                                          if (lane <= (cw & 31u))
+                                              p.sdr[static_cast<size_t>(gin) * p.ncw + w0 + lane] = myword;
+                                      }
+                                  });
+            if (lane == 0) p.counts[gin] = total;
             continue;
         }
         if (radius > 0 && p.ncw * 16u <= 1024u && NW <= 16u) {
@@ -587,7 +613,10 @@ __global__ void __launch_bounds__(NT, 1)
     else __syncthreads();
     if (trace && tid == 0) trace[2] = global_ns();
 
-    batched_topk<CPT, NW>(p, rawbuf, region, s_bc, in0, gs, rank, K, wi, lane);
+    // idle shared memory behind the raw counts: the rest of the ring and the X windows
+    const uint32_t raw_bytes = (32u * p.C32 * 2u + 127u) & ~127u;
+    const uint32_t big_bytes = NST * kStageBytes > raw_bytes ? NST * kStageBytes - raw_bytes + p.region_bytes : 0u;
+    batched_topk<CPT, NW>(p, rawbuf, region, smem + raw_bytes, big_bytes, s_bc, in0, gs, rank, K, wi, lane);
     if (K > 1) cluster.sync();  // peers may still read this CTA's partial counts
     if (trace) {
         __syncthreads();
@@ -703,7 +732,7 @@ __global__ void __launch_bounds__(NT, 1) sp_patch_kernel(const __grid_constant__
         }
         __syncthreads();  // raw counts of the group complete; X may be overwritten
         // a3/a4: per tile
-        batched_topk<CPT, NW>(p, rawbuf, scratch, s_bc, in0, gs, 0u, 1u, wi, lane);
+        batched_topk<CPT, NW>(p, rawbuf, scratch, scratch, p.region_bytes, s_bc, in0, gs, 0u, 1u, wi, lane);
         __syncthreads();  // rawbuf / scratch reused by the next group
     }
 }

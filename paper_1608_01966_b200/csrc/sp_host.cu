@@ -333,6 +333,9 @@ struct sp_handle {
     uint64_t* d_trace = nullptr;  // SP_TRACE=1: per-CTA phase timestamps of the batched kernel
     bool uniform_bc = true;       // all boosts equal (enables the histogram top-k)
     uint32_t batched_threads = 512;  // threads per CTA of the batched kernel
+    // per-column boosts: wavelet local top-k from this radius on, the bit-sliced comparator below
+    // (crossover measured at r ~ 80-100 for C = 1024: scripts/local_general_timing.py)
+    uint32_t wm_min_radius = 96;
     uint32_t learn_Q = 0, learn_smem = 0;  // cluster learning: CTAs per cluster (0 = not eligible)
     bool learn_dbl = false;                 // cluster learning: double-buffered bit-planes
     bool last_learn_cluster = false;
@@ -671,6 +674,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         p.raw_out = rec ? h->d_raw_rec + static_cast<size_t>(row0) * g.C : nullptr;
         p.boosted_out = rec ? h->d_boosted_rec + static_cast<size_t>(row0) * g.C : nullptr;
         p.radius_dev = h->d_radius;
+        p.wm_min_radius = h->wm_min_radius;
         if (!g.whole) {
             p.patch_w = g.pw;
             p.patch_h = g.ph;
@@ -1046,6 +1050,7 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
     }
     if (std::getenv("SP_TRACE")) cudaMalloc(&h->d_trace, 4096u * 6u * sizeof(uint64_t));
     if (const char* et = std::getenv("SP_THREADS")) h->batched_threads = std::atoi(et) == 1024 ? 1024u : 512u;
+    if (const char* ew = std::getenv("SP_WM_MIN_RADIUS")) h->wm_min_radius = static_cast<uint32_t>(std::atoi(ew));
     h->Wn = (g.nbits + 31u) / 32u;
     h->sub_inputs = std::max<uint32_t>(sp::kPerInputChunk, g.P);
     const size_t cs = static_cast<size_t>(g.C) * g.S;

@@ -73,6 +73,7 @@ struct alignas(64) BatchedParams {
     uint16_t* raw_out;         // nullable [num_inputs][C]
     float* boosted_out;        // nullable [num_inputs][C]
     const uint32_t* radius_dev;  // nullable: radius in force (full learning adapts it), else `radius`
+    uint32_t wm_min_radius;    // per-column boosts: wavelet top-k from this radius on (else comparator)
 };
 
 // Full learning (NEXT-1; S:119(b-e); DESIGN R17-R21): device state and constants.

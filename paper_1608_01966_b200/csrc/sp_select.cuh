@@ -454,6 +454,165 @@ __device__ __forceinline__ uint32_t local_general_beats15(const RowT* row, const
     return beats;
 }
 
+// Local inhibition, per-column boosts, by one warp with a wavelet matrix over the positions (any
+// radius; O(C log 2^15) per input instead of the comparator's O(C * r)).  Values: the coarse key
+// u of coarse_map (0 for ineligible columns), stored as u << 1 | lossy, B = bits(max u) <= 15
+// levels.  The descent of column c with window [lo, hi] gives #{d in window : u_d > u_c} (u is
+// monotone in N, so these beat c) and the range [a, b) of the window's columns with u_d == u_c at
+// the bottom level, stable in position ([a, m) are the ones with d < c).  Equal u between two
+// lossless columns means equal N: the lower index wins, i.e. beats += m - a.  When the bottom-level
+// bit-vector of the lossy flags shows a lossy column in [a, b) (c included), the ties of c are
+// re-decided on the exact keys (rare: see coarse_map); the tied columns are read from the
+// bottom-level positions recorded by the first pass (pos[m] = c).
+// Scratch: buf0, buf1 [C32] uint16; lv [B + 1][ncw + 2] uint2 {bits, ones before} per word
+// (level B: lossy flags; entry ncw + 1 holds the level's zero count Z).
+__device__ __forceinline__ uint32_t wm_rank2(const uint2* lvl, uint32_t p) {
+    const uint2 e = lvl[p >> 5];
+    return e.y + __popc(e.x & ((1u << (p & 31u)) - 1u));
+}
+
+template <typename RowT, typename Emit>
+__device__ __forceinline__ void local_general_wavelet(const RowT* row, const uint32_t* bc, uint32_t C, uint32_t C32,
+                                                      uint32_t ncw, uint32_t radius, uint32_t k, uint32_t theta,
+                                                      uint32_t L, const CoarseMap& cm, uint16_t* buf0,
+                                                      uint16_t* buf1, uint2* lv, uint32_t lane, Emit emit) {
+    const uint32_t stride = ncw + 2u;
+    auto sval = [&](uint32_t c) -> uint32_t {  // u << 1 | lossy (0: ineligible or pad column)
+        if (c >= C) return 0u;
+        bool lossy;
+        const uint32_t u = coarse_u15(eligible_N(row[c], bc[c], theta), cm, lossy);
+        return u ? (u << 1) | (lossy ? 1u : 0u) : 0u;
+    };
+    uint32_t umax = 0;
+    for (uint32_t i = lane; i < C32; i += 32u) {
+        const uint32_t v = sval(i);
+        buf0[i] = static_cast<uint16_t>(v);
+        umax = max(umax, v >> 1);
+    }
+    umax = __reduce_max_sync(0xffffffffu, umax);
+    const uint32_t B = umax ? 32u - __clz(umax) : 1u;
+    __syncwarp();
+    uint16_t* src = buf0;
+    uint16_t* dst = buf1;
+    // level l partitions on bit l of u (bit l + 1 of the stored value); level B: the lossy bit
+    for (int l = static_cast<int>(B) - 1; l >= -1; --l) {
+        uint2* lvl = lv + (l >= 0 ? l : static_cast<int>(B)) * stride;
+        const uint32_t sb = static_cast<uint32_t>(l + 1);
+        uint32_t ones = 0;
+#pragma unroll 8
+        for (uint32_t j = 0; j < ncw; ++j) {
+            const uint32_t w = __ballot_sync(0xffffffffu, (src[j * 32u + lane] >> sb) & 1u);
+            if (lane == 0) lvl[j] = make_uint2(w, ones);
+            ones += __popc(w);
+        }
+        const uint32_t Z = C32 - ones;
+        if (lane == 0) lvl[ncw] = make_uint2(0u, ones), lvl[ncw + 1u] = make_uint2(0u, Z);
+        __syncwarp();
+        if (l < 0) break;
+#pragma unroll 8
+        for (uint32_t j = 0; j < ncw; ++j) {
+            const uint32_t i = j * 32u + lane;
+            const uint32_t v = src[i];
+            const uint2 e = lvl[j];
+            const uint32_t r = e.y + __popc(e.x & ((1u << lane) - 1u));
+            dst[((v >> sb) & 1u) ? Z + r : i - r] = static_cast<uint16_t>(v);
+        }
+        __syncwarp();
+        uint16_t* t = src;
+        src = dst;
+        dst = t;
+    }
+    const int R = static_cast<int>(radius), Cn = static_cast<int>(C);
+    const uint2* lvL = lv + B * stride;
+    auto window_of = [&](uint32_t c, uint32_t& lo, uint32_t& hi) {
+        lo = static_cast<uint32_t>(max(0, static_cast<int>(c) - R));
+        hi = static_cast<uint32_t>(min(Cn - 1, static_cast<int>(c) + R)) + 1u;
+    };
+    // pass 1: beats by the index rule for equal u (buf0[c], bit 15 = a lossy column among c's
+    // ties; 0x7FFF = ineligible) and the bottom-level position of every eligible column
+    // (buf1[m] = c), which lists the tied columns of pass 2.  NQ columns per lane descend
+    // together (independent shared-memory chains).
+    uint16_t* beats_s = buf0;
+    uint16_t* pos_s = buf1;
+    constexpr int NQ = 4;
+    for (uint32_t cw0 = 0; cw0 < ncw; cw0 += NQ) {
+        uint32_t c[NQ], u[NQ], a[NQ], m[NQ], b[NQ], lo[NQ], hi[NQ], less[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            c[q] = (cw0 + q) * 32u + lane;
+            u[q] = cw0 + q < ncw ? sval(c[q]) >> 1 : 0u;
+            window_of(c[q], lo[q], hi[q]);
+            a[q] = lo[q], m[q] = c[q], b[q] = hi[q], less[q] = 0u;
+        }
+        for (int l = static_cast<int>(B) - 1; l >= 0; --l) {
+            const uint2* lvl = lv + l * stride;
+            const uint32_t Z = lvl[ncw + 1u].y;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const uint32_t ra = wm_rank2(lvl, a[q]), rm = wm_rank2(lvl, m[q]), rb = wm_rank2(lvl, b[q]);
+                if ((u[q] >> l) & 1u) {
+                    less[q] += (b[q] - a[q]) - (rb - ra);
+                    a[q] = Z + ra, m[q] = Z + rm, b[q] = Z + rb;
+                } else {
+                    a[q] -= ra, m[q] -= rm, b[q] -= rb;
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            if (cw0 + q >= ncw) break;
+            uint16_t out = 0x7FFFu;
+            if (u[q]) {
+                const uint32_t beats = ((hi[q] - lo[q]) - less[q] - (b[q] - a[q])) + (m[q] - a[q]);
+                const bool fix = b[q] - a[q] > 1u && wm_rank2(lvL, b[q]) != wm_rank2(lvL, a[q]);
+                out = static_cast<uint16_t>(beats | (fix ? 0x8000u : 0u));
+                pos_s[m[q]] = static_cast<uint16_t>(c[q]);
+            }
+            beats_s[c[q]] = out;
+        }
+    }
+    __syncwarp();
+    // pass 2: ties involving a lossy column re-decided on the exact keys (rare): sum over the
+    // tied d of [key_d > key_c] - [d < c] (the index rule counted the latter)
+    for (uint32_t cw = 0; cw < ncw; ++cw) {
+        const uint32_t c = cw * 32u + lane;
+        const uint32_t v = beats_s[c];
+        int beats = static_cast<int>(v & 0x7FFFu);
+        if (v & 0x8000u) {
+            const uint64_t Nc = eligible_N(row[c], bc[c], theta);
+            bool lossy_c;
+            const uint32_t uc = coarse_u15(Nc, cm, lossy_c);
+            const uint64_t keyc = (Nc << L) | (((1ull << L) - 1ull) - c);
+            uint32_t lo, hi;
+            window_of(c, lo, hi);
+            uint32_t a = lo, m = c, b = hi;
+            for (int l = static_cast<int>(B) - 1; l >= 0; --l) {
+                const uint2* lvl = lv + l * stride;
+                const uint32_t ra = wm_rank2(lvl, a), rm = wm_rank2(lvl, m), rb = wm_rank2(lvl, b);
+                if ((uc >> l) & 1u) {
+                    const uint32_t Z = lvl[ncw + 1u].y;
+                    a = Z + ra, m = Z + rm, b = Z + rb;
+                } else {
+                    a -= ra, m -= rm, b -= rb;
+                }
+            }
+            for (uint32_t q = a; q < b; ++q) {
+                const uint32_t d = pos_s[q];
+                if (d == c) continue;
+                const uint64_t Nd = eligible_N(row[d], bc[d], theta);
+                bool lossy_d;
+                coarse_u15(Nd, cm, lossy_d);
+                if (lossy_c || lossy_d) {
+                    const uint64_t keyd = (Nd << L) | (((1ull << L) - 1ull) - d);
+                    beats += (keyd > keyc ? 1 : 0) - (d < c ? 1 : 0);
+                }
+            }
+        }
+        emit(cw, __ballot_sync(0xffffffffu, v != 0x7FFFu && beats < static_cast<int>(k)));
+    }
+    __syncwarp();
+}
+
 // Winners of word cw (local inhibition, per-column boosts), all lanes of the warp call it.
 template <typename RowT>
 __device__ __forceinline__ uint32_t local_general_word15(const RowT* row, const uint32_t* bc,

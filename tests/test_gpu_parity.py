@@ -320,6 +320,40 @@ def test_full_size_inference_parity(radius, boost_mode):
         check_results(results, *run_gpu(make_sp(cfg, state, path, max_inputs=64), frames))
 
 
+def near1_boosts(C, seed=11):
+    """Per-column boosts that make the batched kernel's coarse keys tie with lossy columns:
+    half the columns at 1.0, a quarter at 1 + j*2^-23 (j = 1..8: N = raw*(2^23 + j) lands in
+    the bucket of raw*2^23 but beats it exactly), a quarter seeded in [1, 1.01]."""
+    rng = np.random.default_rng(seed)
+    b = np.ones(C, np.float32)
+    kind = rng.integers(0, 4, C)
+    tiny = np.float32(1.0) + rng.integers(1, 9, C).astype(np.float32) * np.float32(2.0 ** -23)
+    b[kind == 2] = tiny[kind == 2]
+    b[kind == 3] = sp_inputs.boosts(seed, C, 1.0, 1.01)[kind == 3]
+    return b
+
+
+@pytest.mark.parametrize("selector", ["wavelet", "comparator"])
+@pytest.mark.parametrize("radius", [1, 7, 80, 506, 1023, 1100])
+@pytest.mark.parametrize("boost_mode", ["seeded", "near1"])
+def test_local_general_boost_selectors(radius, boost_mode, selector, monkeypatch):
+    """Local inhibition with per-column boosts in the batched kernel: the wavelet matrix over
+    coarse keys (with the exact re-decision of lossy ties) and the bit-sliced comparator
+    (SP_WM_MIN_RADIUS forces it), against the oracle; r >= C - 1 is global inhibition (C9)."""
+    monkeypatch.setenv("SP_WM_MIN_RADIUS", "0" if selector == "wavelet" else "100000")
+    cfg = ocfg(input_width=96, input_height=64, num_columns=1000, synapses_per_column=64,
+               min_overlap=2, winners_set_size=20, inhibition_radius=radius)
+    idx, perm, boost = perturbed_state(cfg)
+    if boost_mode == "near1":
+        boost = near1_boosts(cfg.num_columns)
+    state = (idx, perm, boost)
+    frames = sp_inputs.frames(77, 0, 45, cfg.input_height, cfg.input_width, rho=0.5)
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = [ora.step(x, False) for x in O.encode(frames, cfg)]
+    sp = make_sp(cfg, state, P.SP_PATH_BATCHED)
+    check_results(results, *run_gpu(sp, frames))
+
+
 def test_bench_launch_config_sampled_parity():
     """The exact launch configuration bench.py times: 4096 device-generated frames.
 
