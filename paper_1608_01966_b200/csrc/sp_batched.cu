@@ -296,10 +296,9 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             if (B <= 8u && wbytes * NW <= p.region_bytes) {
                 // wavelet matrix over the positions (sp_select.cuh): O(C log range) per input
                 uint8_t* base = region + wi * wbytes;
-                uint32_t* bv = reinterpret_cast<uint32_t*>(base + 2u * p.C32);
-                uint32_t* pc = bv + B * (p.ncw + 2u);
+                uint2* lv = reinterpret_cast<uint2*>(base + 2u * p.C32);
                 uint32_t total = 0, myword = 0;
-                local_uniform_wavelet(row, p.C, p.C32, p.ncw, radius, p.k, r_lo, xmn, B, base, base + p.C32, bv, pc,
+                local_uniform_wavelet(row, p.C, p.C32, p.ncw, radius, p.k, r_lo, xmn, B, base, base + p.C32, lv,
                                       lane, [&](uint32_t cw, uint32_t word) {
                                           if ((cw & 31u) == lane) myword = word;
                                           total += __popc(word);

@@ -139,16 +139,18 @@ __device__ __forceinline__ uint32_t local_uniform_beats_part(const RowT* row, co
 //     beats(c) = #{d in [lo, hi] : x'_d > x'_c} + #{d in [lo, c) : x'_d == x'_c}
 // from one descent through the levels tracking the positions lo, c and hi+1 (rank queries
 // on per-level bit-vectors with per-word prefix counts).  emit(cw, word) gets the SDR words
-// in order (warp-uniform).  Scratch: buf0, buf1 [C32] bytes; bv, pc [B][ncw + 2] words.
-__device__ __forceinline__ uint32_t wm_rank(const uint32_t* bvl, const uint32_t* pcl, uint32_t p) {
-    return pcl[p >> 5] + __popc(bvl[p >> 5] & ((1u << (p & 31u)) - 1u));
+// in order (warp-uniform).  Scratch: buf0, buf1 [C32] bytes; lv [B][ncw + 2] uint2 {bits, ones
+// before} per word (entry ncw + 1: the level's zero count Z).
+__device__ __forceinline__ uint32_t wm_rank2(const uint2* lvl, uint32_t p) {
+    const uint2 e = lvl[p >> 5];
+    return e.y + __popc(e.x & ((1u << (p & 31u)) - 1u));
 }
 
 template <typename RowT, typename Emit>
 __device__ __forceinline__ void local_uniform_wavelet(const RowT* row, uint32_t C, uint32_t C32, uint32_t ncw,
                                                       uint32_t radius, uint32_t k, uint32_t r_lo, uint32_t xmin,
-                                                      uint32_t B, uint8_t* buf0, uint8_t* buf1, uint32_t* bv,
-                                                      uint32_t* pc, uint32_t lane, Emit emit) {
+                                                      uint32_t B, uint8_t* buf0, uint8_t* buf1, uint2* lv,
+                                                      uint32_t lane, Emit emit) {
     const uint32_t stride = ncw + 2u;
     auto xval = [&](uint32_t c) -> uint32_t {
         const uint32_t x = c < C ? static_cast<uint32_t>(row[c]) : 0u;
@@ -159,23 +161,23 @@ __device__ __forceinline__ void local_uniform_wavelet(const RowT* row, uint32_t 
     uint8_t* src = buf0;
     uint8_t* dst = buf1;
     for (int l = static_cast<int>(B) - 1; l >= 0; --l) {
-        uint32_t* bvl = bv + l * stride;
-        uint32_t* pcl = pc + l * stride;
+        uint2* lvl = lv + l * stride;
         uint32_t ones = 0;
 #pragma unroll 8
         for (uint32_t j = 0; j < ncw; ++j) {
             const uint32_t w = __ballot_sync(0xffffffffu, (src[j * 32u + lane] >> l) & 1u);
-            if (lane == 0) bvl[j] = w, pcl[j] = ones;
+            if (lane == 0) lvl[j] = make_uint2(w, ones);
             ones += __popc(w);
         }
         const uint32_t Z = C32 - ones;
-        if (lane == 0) bvl[ncw] = 0u, pcl[ncw] = ones, pcl[ncw + 1u] = Z;
+        if (lane == 0) lvl[ncw] = make_uint2(0u, ones), lvl[ncw + 1u] = make_uint2(0u, Z);
         __syncwarp();
 #pragma unroll 8
         for (uint32_t j = 0; j < ncw; ++j) {
             const uint32_t i = j * 32u + lane;
             const uint32_t v = src[i];
-            const uint32_t r = pcl[j] + __popc(bvl[j] & ((1u << lane) - 1u));
+            const uint2 e = lvl[j];
+            const uint32_t r = e.y + __popc(e.x & ((1u << lane) - 1u));
             dst[((v >> l) & 1u) ? Z + r : i - r] = static_cast<uint8_t>(v);
         }
         __syncwarp();
@@ -184,38 +186,39 @@ __device__ __forceinline__ void local_uniform_wavelet(const RowT* row, uint32_t 
         dst = t;
     }
     const int R = static_cast<int>(radius), Cn = static_cast<int>(C);
-    // beats of column c (its descent through the levels); independent columns interleave
-    auto beats_of = [&](uint32_t c, uint32_t x) -> uint32_t {
-        const uint32_t lo = static_cast<uint32_t>(max(0, static_cast<int>(c) - R));
-        const uint32_t hi = static_cast<uint32_t>(min(Cn - 1, static_cast<int>(c) + R)) + 1u;
-        uint32_t a = lo, m = c, b = hi, less = 0;
+    // beats of NQ columns per lane (independent descents interleave):
+    //   greater + equal before c = (hi - lo) - less - (b - a) + (m - a)
+    constexpr int NQ = 4;
+    for (uint32_t cw0 = 0; cw0 < ncw; cw0 += NQ) {
+        uint32_t x[NQ], a[NQ], m[NQ], b[NQ], lo[NQ], hi[NQ], less[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const uint32_t c = (cw0 + q) * 32u + lane;
+            x[q] = cw0 + q < ncw ? xval(c) : 0u;
+            lo[q] = static_cast<uint32_t>(max(0, static_cast<int>(c) - R));
+            hi[q] = static_cast<uint32_t>(min(Cn - 1, static_cast<int>(c) + R)) + 1u;
+            a[q] = lo[q], m[q] = c, b[q] = hi[q], less[q] = 0u;
+        }
         for (int l = static_cast<int>(B) - 1; l >= 0; --l) {
-            const uint32_t* bvl = bv + l * stride;
-            const uint32_t* pcl = pc + l * stride;
-            const uint32_t ra = wm_rank(bvl, pcl, a), rm = wm_rank(bvl, pcl, m), rb = wm_rank(bvl, pcl, b);
-            if ((x >> l) & 1u) {
-                const uint32_t Z = pcl[ncw + 1u];
-                less += (b - a) - (rb - ra);
-                a = Z + ra, m = Z + rm, b = Z + rb;
-            } else {
-                a -= ra, m -= rm, b -= rb;
+            const uint2* lvl = lv + l * stride;
+            const uint32_t Z = lvl[ncw + 1u].y;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const uint32_t ra = wm_rank2(lvl, a[q]), rm = wm_rank2(lvl, m[q]), rb = wm_rank2(lvl, b[q]);
+                if ((x[q] >> l) & 1u) {
+                    less[q] += (b[q] - a[q]) - (rb - ra);
+                    a[q] = Z + ra, m[q] = Z + rm, b[q] = Z + rb;
+                } else {
+                    a[q] -= ra, m[q] -= rm, b[q] -= rb;
+                }
             }
         }
-        return ((hi - lo) - less - (b - a)) + (m - a);  // greater + equal before c
-    };
-    uint32_t cw = 0;
-    for (; cw + 1u < ncw; cw += 2u) {
-        const uint32_t c0 = cw * 32u + lane, c1 = c0 + 32u;
-        const uint32_t x0 = xval(c0), x1 = xval(c1);
-        const uint32_t b0 = x0 ? beats_of(c0, x0) : 0u, b1 = x1 ? beats_of(c1, x1) : 0u;
-        emit(cw, __ballot_sync(0xffffffffu, x0 > 0u && b0 < k));
-        emit(cw + 1u, __ballot_sync(0xffffffffu, x1 > 0u && b1 < k));
-    }
-    if (cw < ncw) {
-        const uint32_t c0 = cw * 32u + lane;
-        const uint32_t x0 = xval(c0);
-        const uint32_t b0 = x0 ? beats_of(c0, x0) : 0u;
-        emit(cw, __ballot_sync(0xffffffffu, x0 > 0u && b0 < k));
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            if (cw0 + q >= ncw) break;
+            const uint32_t beats = ((hi[q] - lo[q]) - less[q] - (b[q] - a[q])) + (m[q] - a[q]);
+            emit(cw0 + q, __ballot_sync(0xffffffffu, x[q] > 0u && beats < k));
+        }
     }
     __syncwarp();
 }
@@ -466,11 +469,6 @@ __device__ __forceinline__ uint32_t local_general_beats15(const RowT* row, const
 // bottom-level positions recorded by the first pass (pos[m] = c).
 // Scratch: buf0, buf1 [C32] uint16; lv [B + 1][ncw + 2] uint2 {bits, ones before} per word
 // (level B: lossy flags; entry ncw + 1 holds the level's zero count Z).
-__device__ __forceinline__ uint32_t wm_rank2(const uint2* lvl, uint32_t p) {
-    const uint2 e = lvl[p >> 5];
-    return e.y + __popc(e.x & ((1u << (p & 31u)) - 1u));
-}
-
 template <typename RowT, typename Emit>
 __device__ __forceinline__ void local_general_wavelet(const RowT* row, const uint32_t* bc, uint32_t C, uint32_t C32,
                                                       uint32_t ncw, uint32_t radius, uint32_t k, uint32_t theta,
