@@ -255,6 +255,35 @@ sp_status sp_compute_host(sp_handle* h, const uint8_t* frames_host, uint32_t num
                           int learn, uint32_t* sdr_host, uint32_t* count_host,
                           void* cuda_stream);
 
+/* ---- bit-plane input ------------------------------------------------------------
+ * "Changing from integer to boolean data type will result in approximately 32-fold reduction of
+ * the amount of data to be transferred to the accelerator".  Frames may be given as
+ * bit-planes: uint32[num_frames][Wp], Wp = ceil(W*H / 32) rounded up to a multiple of 4 (16-byte
+ * rows); bit i of word w is pixel 32w + i in row-major order (R12's bit, LSB first), words and
+ * bits past W*H are ignored.  8x fewer bytes than uint8 frames cross PCIe and HBM.  Whole-frame
+ * configurations (no patches) that the batched kernel serves (sp_plan path BATCHED); inference
+ * only (the state is not changed).  The results are the same as sp_compute on the uint8 frames
+ * whose nonzero bytes are the set bits. */
+
+/* Packs uint8 frames (device, uint8[num_frames][H][W]) into bit-planes (device,
+ * uint32[num_frames][Wp], caller-owned), stream-ordered.  Errors: SP_E_ARG (NULL buffers),
+ * SP_E_CONFIG (patch configuration), SP_E_CUDA. */
+sp_status sp_pack_frames(sp_handle* h, const uint8_t* frames_dev, uint32_t num_frames, uint32_t* planes_dev,
+                         void* cuda_stream);
+
+/* Inference on bit-planes (device, 16-byte aligned): the winners go to sdr_dev / count_dev
+ * (uint32[num_frames][sdr_words] / uint32[num_frames], device) or, both NULL, to the handle's
+ * buffers (read with sp_winners).  Async, stream-ordered.  Errors: SP_E_ARG (NULL planes,
+ * misalignment, one of sdr_dev / count_dev NULL, num_frames > max_inputs), SP_E_CONFIG (patch
+ * configuration or not eligible for the batched kernel), SP_E_CUDA. */
+sp_status sp_compute_packed(sp_handle* h, const uint32_t* planes_dev, uint32_t num_frames, uint32_t* sdr_dev,
+                            uint32_t* count_dev, void* cuda_stream);
+
+/* End-to-end variant of sp_compute_packed with HOST bit-planes and HOST results (as
+ * sp_compute_host; synchronous). */
+sp_status sp_compute_packed_host(sp_handle* h, const uint32_t* planes_host, uint32_t num_frames,
+                                 uint32_t* sdr_host, uint32_t* count_host, void* cuda_stream);
+
 /* Host-only planning (no GPU): the launch plan sp_compute would use for
  * num_frames frames with learn=0, assuming a B200 (148 SMs, 232448 B smem)
  * when sm_count <= 0.  Errors: SP_E_ARG, SP_E_CONFIG. */

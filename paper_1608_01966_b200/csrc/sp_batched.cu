@@ -411,18 +411,24 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
 
 // NT threads per CTA (1024: 1 block of 32 pixels per warp per chunk, 64 registers;
 // 512: 2 blocks per warp per chunk, 128 registers); CPT column-warps per warp.
-template <int CPT, int NT>
+// PK: the frames arrive as bit-planes (sp_compute_packed; P:502's boolean representation):
+// uint32[inputs][Wn4], bit i of word w = pixel 32w + i.  A stage is then one 4 KiB TMA box
+// {32 words, 32 inputs} (= one chunk of kChunkBits pixels), 8x as many stages in the same ring,
+// and the byte flags disappear: lane f's word of a block is already its 32 pixels.
+template <int CPT, int NT, bool PK>
 __global__ void __launch_bounds__(NT, 1)
     sp_batched_kernel(const __grid_constant__ BatchedParams p) {
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr uint32_t NW = NT / 32;        // warps
     constexpr uint32_t BPW = 32u / NW;      // 32-pixel blocks per warp per chunk
+    constexpr uint32_t SB = PK ? 32u * (kChunkBits / 8u) : kStageBytes;  // bytes per stage
+    static_assert(!PK || BPW == 2, "the packed staging reads 2 blocks per lane (LDS.64)");
     const uint32_t tid = threadIdx.x, lane = tid & 31u, wi = tid >> 5;
     const uint32_t NST = p.stages;
 
     uint8_t* stage_base = smem;  // 1024-aligned (swizzle-128B boxes)
     uint16_t* rawbuf = reinterpret_cast<uint16_t*>(stage_base);  // after streaming
-    uint8_t* region = smem + NST * kStageBytes;
+    uint8_t* region = smem + NST * SB;
     uint32_t* words = reinterpret_cast<uint32_t*>(region);
     uint32_t* s_bc = reinterpret_cast<uint32_t*>(region + p.region_bytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_bc + p.C32);
@@ -463,11 +469,15 @@ __global__ void __launch_bounds__(NT, 1)
     auto issue = [&](uint32_t j, uint32_t st) {
         const uint32_t x0 = pix_begin + j * kChunkBits;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive_expect_tx(&bars[st], kStageBytes);
-        uint8_t* dst = stage_base + st * kStageBytes;
+        mbar_arrive_expect_tx(&bars[st], SB);
+        uint8_t* dst = stage_base + st * SB;
+        if (PK) {
+            tma_box_g2s(dst, &p.tmap, x0 / 32u, in0, &bars[st]);  // {32 words, 32 inputs}
+        } else {
 #pragma unroll
-        for (uint32_t b = 0; b < kChunkBits / kBoxBytes; ++b)
-            tma_box_g2s(dst + b * 32u * kBoxBytes, &p.tmap, x0 + b * kBoxBytes, in0, &bars[st]);
+            for (uint32_t b = 0; b < kChunkBits / kBoxBytes; ++b)
+                tma_box_g2s(dst + b * 32u * kBoxBytes, &p.tmap, x0 + b * kBoxBytes, in0, &bars[st]);
+        }
     };
     if (tid == 0) {
         const uint32_t pre = min(NST, nchunks);
@@ -487,6 +497,9 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t blk = wi + NW * i;
         rd[i] = (blk >> 2) * (32u * kBoxBytes) + lane * kBoxBytes + (((2u * (blk & 3u)) ^ (lane & 7u)) << 4);
     }
+    // packed: lane f reads words 2wi, 2wi+1 of row f (one LDS.64; 16-byte slot (2wi)/4 of the
+    // 128 B row, swizzled by XOR with f % 8)
+    const uint32_t rdp = lane * 128u + ((((2u * wi) >> 2) ^ (lane & 7u)) << 4) + ((2u * wi) & 3u) * 4u;
 
     Planes P[CPT];
 #pragma unroll
@@ -535,7 +548,14 @@ __global__ void __launch_bounds__(NT, 1)
             mbar_wait(&bars[st], phase);
             // a1: warp wi turns blocks wi, wi+NW, .. (32 pixels x 32 inputs each) into 32
             // bit-sliced words per block
-            {
+            if (PK) {
+                // blocks 2wi, 2wi+1: lane j of the transpose holds pixel 32*blk + j (natural order)
+                const uint2 v = *reinterpret_cast<const uint2*>(stage_base + st * SB + rdp);
+                const uint32_t t0 = warp_transpose32(v.x & lane_ok, tl);
+                const uint32_t t1 = warp_transpose32(v.y & lane_ok, tl);
+                X[q * kChunkBits + (2u * wi) * 32u + lane] = t0;
+                X[q * kChunkBits + (2u * wi + 1u) * 32u + lane] = t1;
+            } else {
                 const uint8_t* stg = stage_base + st * kStageBytes;
                 uint32_t m[BPW];
 #pragma unroll
@@ -614,7 +634,7 @@ __global__ void __launch_bounds__(NT, 1)
 
     // idle shared memory behind the raw counts: the rest of the ring and the X windows
     const uint32_t raw_bytes = (32u * p.C32 * 2u + 127u) & ~127u;
-    const uint32_t big_bytes = NST * kStageBytes > raw_bytes ? NST * kStageBytes - raw_bytes + p.region_bytes : 0u;
+    const uint32_t big_bytes = NST * SB > raw_bytes ? NST * SB - raw_bytes + p.region_bytes : 0u;
     batched_topk<CPT, NW>(p, rawbuf, region, smem + raw_bytes, big_bytes, s_bc, in0, gs, rank, K, wi, lane);
     if (K > 1) cluster.sync();  // peers may still read this CTA's partial counts
     if (trace) {
@@ -747,15 +767,17 @@ static cudaError_t allow_dynamic_smem(F* fn, int max_smem) {
 
 cudaError_t configure_batched(int max_smem) {
     cudaError_t e = allow_dynamic_smem(sp_patch_kernel<2, 512>, max_smem);
-    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<1, 1024>, max_smem);
-    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2, 1024>, max_smem);
-    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2, 512>, max_smem);
-    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<4, 512>, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<1, 1024, false>, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2, 1024, false>, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2, 512, false>, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<4, 512, false>, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<2, 512, true>, max_smem);
+    if (e == cudaSuccess) e = allow_dynamic_smem(sp_batched_kernel<4, 512, true>, max_smem);
     return e;
 }
 
 cudaError_t launch_batched(const BatchedParams& p, uint32_t smem_bytes, cudaStream_t s) {
-    const uint32_t nt = p.threads == 512 ? 512u : 1024u;
+    const uint32_t nt = p.threads == 512 || p.packed ? 512u : 1024u;
     const uint32_t cpt = (p.ncw + nt / 32u - 1u) / (nt / 32u);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.groups * p.K);
@@ -769,11 +791,14 @@ cudaError_t launch_batched(const BatchedParams& p, uint32_t smem_bytes, cudaStre
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (p.packed)
+        return cpt <= 2 ? cudaLaunchKernelEx(&cfg, sp_batched_kernel<2, 512, true>, p)
+                        : cudaLaunchKernelEx(&cfg, sp_batched_kernel<4, 512, true>, p);
     if (nt == 512)
-        return cpt <= 2 ? cudaLaunchKernelEx(&cfg, sp_batched_kernel<2, 512>, p)
-                        : cudaLaunchKernelEx(&cfg, sp_batched_kernel<4, 512>, p);
-    return cpt <= 1 ? cudaLaunchKernelEx(&cfg, sp_batched_kernel<1, 1024>, p)
-                    : cudaLaunchKernelEx(&cfg, sp_batched_kernel<2, 1024>, p);
+        return cpt <= 2 ? cudaLaunchKernelEx(&cfg, sp_batched_kernel<2, 512, false>, p)
+                        : cudaLaunchKernelEx(&cfg, sp_batched_kernel<4, 512, false>, p);
+    return cpt <= 1 ? cudaLaunchKernelEx(&cfg, sp_batched_kernel<1, 1024, false>, p)
+                    : cudaLaunchKernelEx(&cfg, sp_batched_kernel<2, 1024, false>, p);
 }
 
 cudaError_t launch_patch(const BatchedParams& p, uint32_t smem_bytes, uint32_t ctas, cudaStream_t s) {
@@ -798,7 +823,7 @@ cudaError_t batched_max_clusters(uint32_t smem_bytes, int max_clusters[9]) {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         int n = 0;
-        e = cudaOccupancyMaxActiveClusters(&n, sp_batched_kernel<1, 1024>, &cfg);
+        e = cudaOccupancyMaxActiveClusters(&n, sp_batched_kernel<1, 1024, false>, &cfg);
         if (e != cudaSuccess) {
             (void)cudaGetLastError();
             n = 0;

@@ -278,6 +278,26 @@ bool encode_frames_tmap(CUtensorMap* map, const uint8_t* frames, uint32_t nbits,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Bit-planes uint32[rows][words] (words % 4 == 0: 16-byte row stride), box {32 words, 32 rows}.
+bool encode_packed_tmap(CUtensorMap* map, const uint32_t* planes, uint32_t words, uint32_t rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q{};
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {words, rows};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(words) * 4u};
+    const cuuint32_t box[2] = {kChunkBits / 32u, 32u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(planes), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // Groups of <= 32 inputs and cluster size K: estimated time of each K
 // from an HBM term and a per-CTA term (bytes at a per-SM rate, transpose ALU cycles).
 void plan_batched_grid(const Geometry& g, uint32_t nwin, uint32_t n, int sm_count,
@@ -613,6 +633,84 @@ sp::FullLearn full_learn_params(const sp_handle* h) {
     return f;
 }
 
+// Shared memory of the packed-input batched kernel: the same ring bytes cut into 8x as many
+// 4 KiB stages (one mbarrier + release counter each).
+uint32_t packed_smem_bytes(const sp::BatchedLayout& L) {
+    return L.smem_bytes + L.stages * (sp::kPackedStagesPer - 1u) * 12u;
+}
+
+// The batched path (rows a1-a4) for n inputs of uint8 frames or (planes != NULL) bit-planes.
+sp_status launch_batched_path(sp_handle* h, const uint8_t* frames, const uint32_t* planes, uint32_t n_frames,
+                              uint32_t n, const sp_plan_info& pl, cudaStream_t s, uint32_t row0) {
+    const sp::Geometry& g = h->g;
+    const bool rec = (h->cfg.flags & SP_FLAG_RECORD_OVERLAPS) != 0;
+    cudaError_t e = cudaSuccess;
+    if (h->ell_dirty) {
+        e = sp::launch_refresh_ell(h->d_idx, h->d_perm, h->d_ell_pos, h->cfg.connected_threshold,
+                                   g.C, g.S, h->lay.Lw, reinterpret_cast<uint16_t*>(h->d_ell), s);
+        h->launches++;
+        if (e != cudaSuccess) return cuda_fail(e, "ELL refresh launch");
+        h->ell_dirty = false;
+    }
+    sp::BatchedParams p{};
+    if (planes) {
+        if (!sp::encode_packed_tmap(&p.tmap, planes, ((h->Wn + 3u) / 4u * 4u), n))
+            return fail(SP_E_CUDA, "cuTensorMapEncodeTiled failed for the bit-planes (words %u, rows %u)",
+                        ((h->Wn + 3u) / 4u * 4u), n);
+    } else if (!g.whole) {
+        if (!sp::encode_patches_tmap(&p.tmap, frames, g, n_frames))
+            return fail(SP_E_CUDA, "cuTensorMapEncodeTiled failed for the tiles");
+    } else if (!sp::encode_frames_tmap(&p.tmap, frames, g.nbits, n))
+        return fail(SP_E_CUDA, "cuTensorMapEncodeTiled failed for the frames (nbits %u, rows %u)",
+                    g.nbits, n);
+    p.num_inputs = n;
+    p.nbits = g.nbits;
+    p.C = g.C;
+    p.C32 = g.C32;
+    p.ncw = g.ncw;
+    p.min_overlap = h->cfg.min_overlap;
+    p.k = h->cfg.winners_set_size;
+    p.radius = h->cfg.inhibition_radius;
+    p.keyL = g.keyL;
+    p.keyBits = g.keyBits;
+    p.Lw = h->lay.Lw;
+    p.nwin = h->lay.nwin;
+    p.stages = planes ? h->lay.stages * sp::kPackedStagesPer : h->lay.stages;
+    p.packed = planes ? 1u : 0u;
+    p.region_bytes = h->lay.region_bytes;
+    p.xbufs = h->lay.xbufs;
+    p.one = 1u;
+    p.S = g.S;
+    p.uniform_bc = h->uniform_bc ? 1u : 0u;
+    p.threads = h->batched_threads;
+    p.trace = h->d_trace;
+    p.groups = pl.groups;
+    p.K = pl.cluster;
+    p.ell_off = h->d_ell_off;
+    p.ell_nb = h->d_ell_nb;
+    p.ell = h->d_ell;
+    p.bc = h->d_bc;
+    p.boost = h->d_boost;
+    p.sdr = h->res_sdr + static_cast<size_t>(row0) * g.ncw;
+    p.counts = h->res_counts + row0;
+    p.raw_out = rec ? h->d_raw_rec + static_cast<size_t>(row0) * g.C : nullptr;
+    p.boosted_out = rec ? h->d_boosted_rec + static_cast<size_t>(row0) * g.C : nullptr;
+    p.radius_dev = h->d_radius;
+    p.wm_min_radius = h->wm_min_radius;
+    if (!g.whole) {
+        p.patch_w = g.pw;
+        p.patch_h = g.ph;
+        p.tiles_x = g.W / g.pw;
+        p.patch_stage_bytes = (32u * g.nbits + 1023u) / 1024u * 1024u;
+        e = sp::launch_patch(p, h->lay.smem_bytes, pl.ctas, s);
+    } else {
+        e = sp::launch_batched(p, planes ? packed_smem_bytes(h->lay) : h->lay.smem_bytes, s);
+    }
+    h->launches++;
+    if (e != cudaSuccess) return cuda_fail(e, "batched kernel launch");
+    return SP_OK;
+}
+
 // Launches the hot path for n_frames frames; results go to rows [row0, row0 + n) of the
 // handle's result buffers.
 sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, int learn,
@@ -627,67 +725,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
     const bool rec = (h->cfg.flags & SP_FLAG_RECORD_OVERLAPS) != 0;
     const bool full = learn && (h->cfg.flags & SP_FLAG_FULL_LEARNING) != 0;
     cudaError_t e = cudaSuccess;
-    if (pl.path == SP_PATH_BATCHED) {
-        if (h->ell_dirty) {
-            e = sp::launch_refresh_ell(h->d_idx, h->d_perm, h->d_ell_pos, h->cfg.connected_threshold,
-                                       g.C, g.S, h->lay.Lw, reinterpret_cast<uint16_t*>(h->d_ell), s);
-            h->launches++;
-            if (e != cudaSuccess) return cuda_fail(e, "ELL refresh launch");
-            h->ell_dirty = false;
-        }
-        sp::BatchedParams p{};
-        if (!g.whole) {
-            if (!sp::encode_patches_tmap(&p.tmap, frames, g, n_frames))
-                return fail(SP_E_CUDA, "cuTensorMapEncodeTiled failed for the tiles");
-        } else if (!sp::encode_frames_tmap(&p.tmap, frames, g.nbits, n))
-            return fail(SP_E_CUDA, "cuTensorMapEncodeTiled failed for the frames (nbits %u, rows %u)",
-                        g.nbits, n);
-        p.num_inputs = n;
-        p.nbits = g.nbits;
-        p.C = g.C;
-        p.C32 = g.C32;
-        p.ncw = g.ncw;
-        p.min_overlap = h->cfg.min_overlap;
-        p.k = h->cfg.winners_set_size;
-        p.radius = h->cfg.inhibition_radius;
-        p.keyL = g.keyL;
-        p.keyBits = g.keyBits;
-        p.Lw = h->lay.Lw;
-        p.nwin = h->lay.nwin;
-        p.stages = h->lay.stages;
-        p.region_bytes = h->lay.region_bytes;
-        p.xbufs = h->lay.xbufs;
-        p.one = 1u;
-        p.S = g.S;
-        p.uniform_bc = h->uniform_bc ? 1u : 0u;
-        p.threads = h->batched_threads;
-        p.trace = h->d_trace;
-        p.groups = pl.groups;
-        p.K = pl.cluster;
-        p.ell_off = h->d_ell_off;
-        p.ell_nb = h->d_ell_nb;
-        p.ell = h->d_ell;
-        p.bc = h->d_bc;
-        p.boost = h->d_boost;
-        p.sdr = h->res_sdr + static_cast<size_t>(row0) * g.ncw;
-        p.counts = h->res_counts + row0;
-        p.raw_out = rec ? h->d_raw_rec + static_cast<size_t>(row0) * g.C : nullptr;
-        p.boosted_out = rec ? h->d_boosted_rec + static_cast<size_t>(row0) * g.C : nullptr;
-        p.radius_dev = h->d_radius;
-        p.wm_min_radius = h->wm_min_radius;
-        if (!g.whole) {
-            p.patch_w = g.pw;
-            p.patch_h = g.ph;
-            p.tiles_x = g.W / g.pw;
-            p.patch_stage_bytes = (32u * g.nbits + 1023u) / 1024u * 1024u;
-            e = sp::launch_patch(p, h->lay.smem_bytes, pl.ctas, s);
-        } else {
-            e = sp::launch_batched(p, h->lay.smem_bytes, s);
-        }
-        h->launches++;
-        if (e != cudaSuccess) return cuda_fail(e, "batched kernel launch");
-        return SP_OK;
-    }
+    if (pl.path == SP_PATH_BATCHED) return launch_batched_path(h, frames, nullptr, n_frames, n, pl, s, row0);
     const char* lp = std::getenv("SP_LEARN_PATH");  // development override: cluster | grid | input
     if (full && h->span_dirty) {  // connected spans for the radius adaptation (R21)
         e = sp::launch_span(h->d_idx, h->d_perm, h->cfg.connected_threshold, g.C, g.S, h->d_span, s);
@@ -1320,8 +1358,27 @@ sp_status sp_set_learning_state(sp_handle* h, const float* active_duty, const fl
     return SP_OK;
 }
 
-sp_status sp_compute_host(sp_handle* h, const uint8_t* frames_host, uint32_t num_frames, int learn,
-                          uint32_t* sdr_host, uint32_t* count_host, void* cuda_stream) {
+namespace {
+
+// Words per frame of the bit-plane input: ceil(nbits / 32) rounded up to 4 (16-byte rows).
+uint32_t packed_words(const sp_handle* h) { return (h->Wn + 3u) / 4u * 4u; }
+
+sp_status check_packed(sp_handle* h, uint32_t n, const void* planes) {
+    if (!h->g.whole) return fail(SP_E_CONFIG, "bit-plane input needs a whole-frame configuration (no patches)");
+    const sp_plan_info pl = make_plan(h, n, false, nullptr);
+    if (n > 0 && pl.path != SP_PATH_BATCHED)
+        return fail(SP_E_CONFIG, "bit-plane input runs on the batched kernel only (not eligible: reason 0x%x)",
+                    pl.reason);
+    if (planes && (reinterpret_cast<uintptr_t>(planes) & 15u))
+        return fail(SP_E_ARG, "bit-planes must be 16-byte aligned");
+    return SP_OK;
+}
+
+// End-to-end pipeline shared by sp_compute_host and sp_compute_packed_host: chunks of frames
+// (uint8 frames, or bit-planes when packed) copied host->device on the copy stream into two
+// staging buffers, computed on s, winners copied back on s.
+sp_status compute_host_impl(sp_handle* h, const void* in_host, bool packed, uint32_t num_frames, int learn,
+                            uint32_t* sdr_host, uint32_t* count_host, void* cuda_stream) {
     sp_status st = check_handle(h);
     if (st != SP_OK) return st;
     const sp::Geometry& g = h->g;
@@ -1329,11 +1386,17 @@ sp_status sp_compute_host(sp_handle* h, const uint8_t* frames_host, uint32_t num
     if (n > h->cfg.max_inputs)
         return fail(SP_E_ARG, "num_frames * inputs_per_frame = %llu exceeds max_inputs %u",
                     static_cast<unsigned long long>(n), h->cfg.max_inputs);
-    if (num_frames > 0 && (!frames_host || !sdr_host)) return fail(SP_E_ARG, "NULL host buffer");
+    if (num_frames > 0 && (!in_host || !sdr_host)) return fail(SP_E_ARG, "NULL host buffer");
+    if (packed) {
+        if (learn) return fail(SP_E_ARG, "bit-plane input is inference only (learn must be 0)");
+        st = check_packed(h, static_cast<uint32_t>(n), nullptr);
+        if (st != SP_OK) return st;
+    }
     h->res_sdr = h->d_sdr;  // results staged in the handle's buffers
     h->res_counts = h->d_counts;
     cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
     const size_t frame_bytes = static_cast<size_t>(g.W) * g.H;
+    const size_t in_bytes = packed ? static_cast<size_t>(packed_words(h)) * 4u : frame_bytes;
     cudaError_t e = cudaSuccess;
     if (!h->copy_stream) {
         // chunk of frames per pipeline stage: ~64 MiB, at least 1 frame
@@ -1346,21 +1409,32 @@ sp_status sp_compute_host(sp_handle* h, const uint8_t* frames_host, uint32_t num
         }
         if (e != cudaSuccess) return cuda_fail(e, "end-to-end staging setup");
     }
+    // frames per chunk: as many as a staging buffer holds (bit-planes: ~8x more per chunk)
+    const uint32_t chunk_frames = static_cast<uint32_t>(
+        std::max<size_t>(1, std::min<size_t>(h->stage_frames * frame_bytes / in_bytes, 1u << 30)));
     h->last_inputs = static_cast<uint32_t>(n);
     h->has_result = true;
+    const uint8_t* src = static_cast<const uint8_t*>(in_host);
     uint32_t chunk = 0;
-    for (uint32_t f0 = 0; f0 < num_frames; f0 += h->stage_frames, ++chunk) {
-        const uint32_t nf = std::min(h->stage_frames, num_frames - f0);
+    for (uint32_t f0 = 0; f0 < num_frames; f0 += chunk_frames, ++chunk) {
+        const uint32_t nf = std::min(chunk_frames, num_frames - f0);
         const int b = chunk & 1;
         // H2D on the copy stream once the buffer's previous compute has finished
         if (chunk >= 2) e = cudaStreamWaitEvent(h->copy_stream, h->ev_free[b], 0);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(h->d_stage[b], frames_host + f0 * frame_bytes, nf * frame_bytes,
-                                cudaMemcpyHostToDevice, h->copy_stream);
+            e = cudaMemcpyAsync(h->d_stage[b], src + f0 * in_bytes, nf * in_bytes, cudaMemcpyHostToDevice,
+                                h->copy_stream);
         if (e == cudaSuccess) e = cudaEventRecord(h->ev_h2d[b], h->copy_stream);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(s, h->ev_h2d[b], 0);
         if (e != cudaSuccess) return cuda_fail(e, "end-to-end H2D");
-        st = compute_impl(h, h->d_stage[b], nf, learn, s, f0 * g.P);
+        if (packed) {
+            const uint32_t ni = nf * g.P;
+            st = launch_batched_path(h, nullptr, reinterpret_cast<const uint32_t*>(h->d_stage[b]), nf, ni,
+                                     make_plan(h, ni, false, nullptr), s, f0 * g.P);
+            h->last_plan = make_plan(h, ni, false, nullptr);
+        } else {
+            st = compute_impl(h, h->d_stage[b], nf, learn, s, f0 * g.P);
+        }
         if (st != SP_OK) return st;
         e = cudaEventRecord(h->ev_free[b], s);
         if (e == cudaSuccess)
@@ -1374,6 +1448,64 @@ sp_status sp_compute_host(sp_handle* h, const uint8_t* frames_host, uint32_t num
     }
     e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(e, "end-to-end sync");
+    return SP_OK;
+}
+
+}  // namespace
+
+sp_status sp_compute_host(sp_handle* h, const uint8_t* frames_host, uint32_t num_frames, int learn,
+                          uint32_t* sdr_host, uint32_t* count_host, void* cuda_stream) {
+    return compute_host_impl(h, frames_host, false, num_frames, learn, sdr_host, count_host, cuda_stream);
+}
+
+sp_status sp_compute_packed_host(sp_handle* h, const uint32_t* planes_host, uint32_t num_frames,
+                                 uint32_t* sdr_host, uint32_t* count_host, void* cuda_stream) {
+    return compute_host_impl(h, planes_host, true, num_frames, 0, sdr_host, count_host, cuda_stream);
+}
+
+sp_status sp_compute_packed(sp_handle* h, const uint32_t* planes_dev, uint32_t num_frames, uint32_t* sdr_dev,
+                            uint32_t* count_dev, void* cuda_stream) {
+    sp_status st = check_handle(h);
+    if (st != SP_OK) return st;
+    const uint64_t n = static_cast<uint64_t>(num_frames) * h->g.P;
+    if (n > h->cfg.max_inputs)
+        return fail(SP_E_ARG, "num_frames * inputs_per_frame = %llu exceeds max_inputs %u",
+                    static_cast<unsigned long long>(n), h->cfg.max_inputs);
+    if (num_frames > 0 && !planes_dev) return fail(SP_E_ARG, "planes_dev is NULL");
+    if ((sdr_dev == nullptr) != (count_dev == nullptr))
+        return fail(SP_E_ARG, "sdr_dev and count_dev must both be NULL or both be set");
+    st = check_packed(h, static_cast<uint32_t>(n), planes_dev);
+    if (st != SP_OK) return st;
+    h->last_inputs = static_cast<uint32_t>(n);
+    h->has_result = true;
+    h->res_sdr = sdr_dev ? sdr_dev : h->d_sdr;
+    h->res_counts = count_dev ? count_dev : h->d_counts;
+    if (n == 0) return SP_OK;
+    const sp_plan_info pl = make_plan(h, static_cast<uint32_t>(n), false, nullptr);
+    h->last_plan = pl;
+    return launch_batched_path(h, nullptr, planes_dev, num_frames, static_cast<uint32_t>(n), pl,
+                               static_cast<cudaStream_t>(cuda_stream), 0);
+}
+
+sp_status sp_pack_frames(sp_handle* h, const uint8_t* frames_dev, uint32_t num_frames, uint32_t* planes_dev,
+                         void* cuda_stream) {
+    sp_status st = check_handle(h);
+    if (st != SP_OK) return st;
+    if (!h->g.whole) return fail(SP_E_CONFIG, "bit-plane input needs a whole-frame configuration (no patches)");
+    if (num_frames > 0 && (!frames_dev || !planes_dev)) return fail(SP_E_ARG, "NULL device buffer");
+    const uint32_t words = packed_words(h);
+    for (uint32_t f0 = 0; f0 < num_frames; f0 += 65535u) {  // grid.y limit
+        sp::PerInputParams pk{};
+        pk.frames = frames_dev + static_cast<size_t>(f0) * h->g.W * h->g.H;
+        pk.num_inputs = std::min(65535u, num_frames - f0);
+        pk.g = h->g;
+        pk.bits = planes_dev + static_cast<size_t>(f0) * words;
+        pk.Wn = h->Wn;
+        pk.bits_stride = words;
+        h->launches++;
+        const cudaError_t e = sp::launch_pack(pk, static_cast<cudaStream_t>(cuda_stream));
+        if (e != cudaSuccess) return cuda_fail(e, "pack launch");
+    }
     return SP_OK;
 }
 

@@ -12,6 +12,7 @@ namespace sp {
 constexpr uint32_t kChunkBits = 1024;      // Lc: pixels per input per pipeline stage
 constexpr uint32_t kBoxBytes = 128;        // TMA box: 128 B (pixels) x 32 rows (inputs), swizzle 128B
 constexpr uint32_t kStageBytes = 32u * kChunkBits;  // 8 boxes = 32 KiB per stage
+constexpr uint32_t kPackedStagesPer = 8;  // packed input: 4 KiB stages (one box) per 32 KiB stage
 constexpr uint32_t kMaxBatchedColumns = 2048;
 constexpr uint32_t kMaxBatchedSynapses = 1023;  // 10 vertical-counter planes
 constexpr uint32_t kHiPlanes = 7;          // planes of weight 8..512 (ones/twos/fours separate)
@@ -74,6 +75,7 @@ struct alignas(64) BatchedParams {
     float* boosted_out;        // nullable [num_inputs][C]
     const uint32_t* radius_dev;  // nullable: radius in force (full learning adapts it), else `radius`
     uint32_t wm_min_radius;    // per-column boosts: wavelet top-k from this radius on (else comparator)
+    uint32_t packed;           // frames are bit-planes uint32[inputs][Wn4] (sp_compute_packed)
 };
 
 // Full learning (NEXT-1; S:119(b-e); DESIGN R17-R21): device state and constants.
@@ -212,6 +214,7 @@ cudaError_t configure_per_input(int max_smem);
 
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_batched(const BatchedParams& p, uint32_t smem_bytes, cudaStream_t s);
+bool encode_packed_tmap(CUtensorMap* map, const uint32_t* planes, uint32_t words, uint32_t rows);
 cudaError_t launch_patch(const BatchedParams& p, uint32_t smem_bytes, uint32_t ctas, cudaStream_t s);
 cudaError_t batched_max_clusters(uint32_t smem_bytes, int max_clusters[9]);
 cudaError_t launch_pack(const PerInputParams& p, cudaStream_t s);

@@ -41,7 +41,7 @@ ABI_SYMBOLS = ("sp_config_default", "sp_create", "sp_destroy", "sp_compute", "sp
                "sp_get_learning_state", "sp_set_learning_state", "sp_histograms",
                "sp_compute_into", "sp_synth_frames", "sp_synth_bgr_frames", "sp_encoder_config_default",
                "sp_encoder_create", "sp_encoder_destroy", "sp_encode", "sp_encoder_get_info",
-               "sp_encoder_last_error")
+               "sp_encoder_last_error", "sp_pack_frames", "sp_compute_packed", "sp_compute_packed_host")
 
 
 class SpError(RuntimeError):
@@ -122,6 +122,9 @@ def lib() -> ctypes.CDLL:
         "sp_get_state": [vp, vp, vp, vp],
         "sp_set_state": [vp, vp, vp, vp],
         "sp_compute_host": [vp, vp, u32, ctypes.c_int, vp, vp, vp],
+        "sp_pack_frames": [vp, vp, u32, vp, vp],
+        "sp_compute_packed": [vp, vp, u32, vp, vp, vp],
+        "sp_compute_packed_host": [vp, vp, u32, vp, vp, vp],
         "sp_plan": [P(SpConfig), u32, i32, P(SpPlanInfo)],
         "sp_init_pools_host": [P(SpConfig), vp],
         "sp_get_info": [vp, P(SpInfo)],
@@ -298,6 +301,8 @@ class SpatialPooler:
         self.frame_shape = (H, W)
         self.inputs_per_frame = (W // pw) * (H // ph)
         self.sdr_words = (self.C + 31) // 32
+        # bit-plane input: words per frame = ceil(W*H/32) rounded up to 4
+        self.packed_words = ((H * W + 31) // 32 + 3) // 4 * 4
         self.last_num_inputs = 0
 
     # -- lifetime ---------------------------------------------------------------------
@@ -348,6 +353,57 @@ class SpatialPooler:
         self.last_num_inputs = n
         self._res = (sdr, counts)  # keep the result buffers alive until the next call
         return n
+
+    # -- bit-plane input (include/sp.h "bit-plane input") ---------------------------
+    def pack_frames(self, frames, planes=None, stream=None):
+        """uint8 cuda frames [F, H, W] -> int32-view bit-planes [F, packed_words] (sp_pack_frames)."""
+        import torch
+        _require(frames, torch.uint8, self.device, name="frames")
+        if frames.dim() != 3 or tuple(frames.shape[1:]) != self.frame_shape:
+            raise SpError(SP_E_SHAPE, f"frames must be [F, {self.frame_shape[0]}, {self.frame_shape[1]}]")
+        F = frames.shape[0]
+        if planes is None:
+            planes = torch.empty((F, self.packed_words), dtype=torch.int32, device=frames.device)
+        _require(planes, torch.int32, self.device, (F, self.packed_words), "planes")
+        _check(lib().sp_pack_frames(self._h, ctypes.c_void_p(frames.data_ptr()), F,
+                                    ctypes.c_void_p(planes.data_ptr()), _stream_ptr(stream, frames.device)))
+        return planes
+
+    def compute_packed(self, planes, sdr=None, counts=None, stream=None) -> int:
+        """Inference on bit-planes (int32-view uint32 [F, packed_words] cuda tensor); winners into
+        ``sdr`` / ``counts`` when given, else kept for ``winners()``."""
+        import torch
+        _require(planes, torch.int32, self.device, name="planes")
+        if planes.dim() != 2 or planes.shape[1] != self.packed_words:
+            raise SpError(SP_E_SHAPE, f"planes must be [F, {self.packed_words}]")
+        n = planes.shape[0] * self.inputs_per_frame
+        if (sdr is None) != (counts is None):
+            raise SpError(SP_E_ARG, "give both sdr and counts, or neither")
+        if sdr is not None:
+            _require(sdr, torch.int32, self.device, (n, self.sdr_words), "sdr")
+            _require(counts, torch.int32, self.device, (n,), "counts")
+        _check(lib().sp_compute_packed(self._h, ctypes.c_void_p(planes.data_ptr()), planes.shape[0],
+                                       ctypes.c_void_p(sdr.data_ptr()) if sdr is not None else None,
+                                       ctypes.c_void_p(counts.data_ptr()) if counts is not None else None,
+                                       _stream_ptr(stream, planes.device)))
+        self.last_num_inputs = n
+        self._res = (sdr, counts) if sdr is not None else None
+        return n
+
+    def compute_packed_host_into(self, planes, sdr, counts, stream=None):
+        """End-to-end bit-plane inference with host buffers (numpy arrays or pinned torch CPU
+        tensors): planes uint32 [F, packed_words] -> sdr uint32 [n, words], counts uint32 [n]."""
+        import torch
+
+        def ptr(a):
+            return a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data
+        F = planes.shape[0]
+        if tuple(planes.shape[1:]) != (self.packed_words,):
+            raise SpError(SP_E_SHAPE, f"planes must be [F, {self.packed_words}]")
+        _check(lib().sp_compute_packed_host(self._h, ctypes.c_void_p(ptr(planes)), F, ctypes.c_void_p(ptr(sdr)),
+                                            ctypes.c_void_p(ptr(counts)) if counts is not None else None,
+                                            _stream_ptr(stream, torch.device("cuda", self.device))))
+        self.last_num_inputs = F * self.inputs_per_frame
 
     def winners(self, sdr=None, counts=None, stream=None):
         """SDRs of the last call: (uint32 [n, words] as int32 view, int32 [n]) cuda tensors."""
