@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(NT, 1)
     constexpr uint32_t NW = NT / 32;        // warps
     constexpr uint32_t BPW = 32u / NW;      // 32-pixel blocks per warp per chunk
     constexpr uint32_t SB = PK ? 32u * (kChunkBits / 8u) : kStageBytes;  // bytes per stage
-    static_assert(!PK || BPW == 2, "the packed staging reads 2 blocks per lane (LDS.64)");
+    static_assert(!PK || NW == 16, "the packed staging splits 16 warps into two halves of 8 x 4 blocks");
     const uint32_t tid = threadIdx.x, lane = tid & 31u, wi = tid >> 5;
     const uint32_t NST = p.stages;
 
@@ -497,9 +497,9 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t blk = wi + NW * i;
         rd[i] = (blk >> 2) * (32u * kBoxBytes) + lane * kBoxBytes + (((2u * (blk & 3u)) ^ (lane & 7u)) << 4);
     }
-    // packed: lane f reads words 2wi, 2wi+1 of row f (one LDS.64; 16-byte slot (2wi)/4 of the
-    // 128 B row, swizzled by XOR with f % 8)
-    const uint32_t rdp = lane * 128u + ((((2u * wi) >> 2) ^ (lane & 7u)) << 4) + ((2u * wi) & 3u) * 4u;
+    // packed: lane f reads words 4(wi%8) .. +3 of row f (16-byte slot wi%8 of the 128 B row,
+    // swizzled by XOR with f % 8: the 8 lanes of each LDS.128 phase hit 8 distinct slots)
+    const uint32_t rdp = lane * 128u + (((wi & 7u) ^ (lane & 7u)) << 4);
 
     Planes P[CPT];
 #pragma unroll
@@ -545,17 +545,35 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t wlen = min(p.Lw, p.nbits - wbase);
         const uint32_t nch = (wlen + kChunkBits - 1) / kChunkBits;
         for (uint32_t q = 0; q < nch; ++q) {
+            if (PK) {
+                // packed: the warps of half (wi >> 3) take the chunks of that parity, 4 blocks
+                // each (one conflict-free LDS.128); lane j of a transpose holds pixel 32*blk + j
+                if ((j & 1u) == (wi >> 3)) {
+                    mbar_wait(&bars[st], phase);
+                    const uint4 v = *reinterpret_cast<const uint4*>(stage_base + st * SB + rdp);
+                    const uint32_t t0 = warp_transpose32(v.x & lane_ok, tl);
+                    const uint32_t t1 = warp_transpose32(v.y & lane_ok, tl);
+                    const uint32_t t2 = warp_transpose32(v.z & lane_ok, tl);
+                    const uint32_t t3 = warp_transpose32(v.w & lane_ok, tl);
+                    uint32_t* xo = X + q * kChunkBits + (4u * (wi & 7u)) * 32u + lane;
+                    xo[0] = t0;
+                    xo[32] = t1;
+                    xo[64] = t2;
+                    xo[96] = t3;
+                    if (warp_release_is_last<NW / 2>(released_addr + 4u * st) && j + NST < nchunks)
+                        issue(j + NST, st);
+                }
+                ++j;
+                if (++st == NST) {
+                    st = 0;
+                    phase ^= 1u;
+                }
+                continue;
+            }
             mbar_wait(&bars[st], phase);
             // a1: warp wi turns blocks wi, wi+NW, .. (32 pixels x 32 inputs each) into 32
             // bit-sliced words per block
-            if (PK) {
-                // blocks 2wi, 2wi+1: lane j of the transpose holds pixel 32*blk + j (natural order)
-                const uint2 v = *reinterpret_cast<const uint2*>(stage_base + st * SB + rdp);
-                const uint32_t t0 = warp_transpose32(v.x & lane_ok, tl);
-                const uint32_t t1 = warp_transpose32(v.y & lane_ok, tl);
-                X[q * kChunkBits + (2u * wi) * 32u + lane] = t0;
-                X[q * kChunkBits + (2u * wi + 1u) * 32u + lane] = t1;
-            } else {
+            {
                 const uint8_t* stg = stage_base + st * kStageBytes;
                 uint32_t m[BPW];
 #pragma unroll
