@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-packed", action="store_true", help="skip the bit-plane input leg (P:502)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-learn-full", action="store_true")
     ap.add_argument("--no-encoder", action="store_true")
@@ -426,6 +427,57 @@ def main():
                "steps": args.e2e_steps, "api": "sp_compute_host (pinned host frames)"}
         del host_frames
 
+    # ---- bit-plane input (boolean data, ~32x less to transfer than int): the same frames
+    # packed to 1 bit per pixel by sp_pack_frames (outside the timed regions); device-resident
+    # throughput of sp_compute_packed and end to end from pinned host bit-planes --------------
+    packed = None
+    if not args.no_packed:
+        planes = sp.pack_frames(frames)
+        psdr = torch.empty((F, words), dtype=torch.int32, device=dev)
+        pcnt = torch.empty((F,), dtype=torch.int32, device=dev)
+        for _ in range(3):
+            sp.compute_packed(planes, psdr, pcnt)
+        lb = (args.steps - 1) % nbuf  # the last timed step's winners (same frames)
+        same = bool(torch.equal(psdr, sdrs[lb]) and torch.equal(pcnt, cnts[lb]))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            sp.compute_packed(planes, psdr, pcnt)
+        b.record(stream)
+        torch.cuda.synchronize()
+        pms = a.elapsed_time(b) / args.steps
+        host_planes = planes.cpu().pin_memory()
+        hsdr = torch.empty((F, words), dtype=torch.int32, pin_memory=True)
+        hcnt = torch.empty((F,), dtype=torch.int32, pin_memory=True)
+        sp.compute_packed_host_into(host_planes, hsdr, hcnt)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            sp.compute_packed_host_into(host_planes, hsdr, hcnt)
+        b.record(stream)
+        torch.cuda.synchronize()
+        pems = a.elapsed_time(b) / args.e2e_steps
+        if world > 1:
+            t = torch.tensor([pms, pems], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            pms, pems = float(t[0]), float(t[1])
+        pbytes = sp.packed_words * 4
+        packed = {"value": F * world / (pms / 1e3), "unit": UNIT, "ms_per_step": pms,
+                  "bytes_per_frame": pbytes,
+                  "hbm_frac": round(F * (pbytes + words * 4) / (pms / 1e3) / 1e9 / measured_peak_hbm()[0], 4),
+                  "same_winners_as_uint8_step": same,
+                  "e2e": {"value": F * world / (pems / 1e3), "unit": UNIT, "h2d_bytes_per_step": F * pbytes,
+                          "d2h_bytes_per_step": F * (words * 4 + 4), "steps": args.e2e_steps,
+                          "api": "sp_compute_packed_host (pinned host bit-planes)"},
+                  "note": "frames given as bit-planes uint32[F][16200] (include/sp.h, P:502); "
+                          "packed by sp_pack_frames outside the timed regions"}
+        del planes, host_planes
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -462,7 +514,8 @@ def main():
                                                      "num_windows", "stages", "smem_bytes")}},
             "hbm_frac": round(value / world * ALGO_BYTES_PER_FRAME / 1e9 / peak, 4),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(), "learn": learn, "histograms": histograms, "encoder": encoder}
+            "clocks": clk.summary(), "learn": learn, "histograms": histograms, "encoder": encoder,
+            "packed": packed}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
