@@ -544,32 +544,37 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t wbase = w * p.Lw;
         const uint32_t wlen = min(p.Lw, p.nbits - wbase);
         const uint32_t nch = (wlen + kChunkBits - 1) / kChunkBits;
-        for (uint32_t q = 0; q < nch; ++q) {
-            if (PK) {
-                // packed: the warps of half (wi >> 3) take the chunks of that parity, 4 blocks
-                // each (one conflict-free LDS.128); lane j of a transpose holds pixel 32*blk + j
-                if ((j & 1u) == (wi >> 3)) {
-                    mbar_wait(&bars[st], phase);
-                    const uint4 v = *reinterpret_cast<const uint4*>(stage_base + st * SB + rdp);
-                    const uint32_t t0 = warp_transpose32(v.x & lane_ok, tl);
-                    const uint32_t t1 = warp_transpose32(v.y & lane_ok, tl);
-                    const uint32_t t2 = warp_transpose32(v.z & lane_ok, tl);
-                    const uint32_t t3 = warp_transpose32(v.w & lane_ok, tl);
-                    uint32_t* xo = X + q * kChunkBits + (4u * (wi & 7u)) * 32u + lane;
-                    xo[0] = t0;
-                    xo[32] = t1;
-                    xo[64] = t2;
-                    xo[96] = t3;
-                    if (warp_release_is_last<NW / 2>(released_addr + 4u * st) && j + NST < nchunks)
-                        issue(j + NST, st);
-                }
-                ++j;
-                if (++st == NST) {
-                    st = 0;
-                    phase ^= 1u;
-                }
-                continue;
+        if (PK) {
+            // packed: the warps of half (wi >> 3) take the chunks of that parity (global chunk
+            // index), 4 blocks each (one conflict-free LDS.128); lane j of a transpose holds
+            // pixel 32*blk + j.  NST is even, so a half always sees stages of one parity.
+            const uint32_t q0 = ((wi >> 3) - j) & 1u;
+            uint32_t jj = j + q0, sq = st + q0, ph = phase;
+            if (sq >= NST) sq -= NST, ph ^= 1u;
+            for (uint32_t q = q0; q < nch; q += 2u) {
+                mbar_wait(&bars[sq], ph);
+                const uint4 v = *reinterpret_cast<const uint4*>(stage_base + sq * SB + rdp);
+                const uint32_t t0 = warp_transpose32(v.x & lane_ok, tl);
+                const uint32_t t1 = warp_transpose32(v.y & lane_ok, tl);
+                const uint32_t t2 = warp_transpose32(v.z & lane_ok, tl);
+                const uint32_t t3 = warp_transpose32(v.w & lane_ok, tl);
+                uint32_t* xo = X + q * kChunkBits + (4u * (wi & 7u)) * 32u + lane;
+                xo[0] = t0;
+                xo[32] = t1;
+                xo[64] = t2;
+                xo[96] = t3;
+                if (warp_release_is_last<NW / 2>(released_addr + 4u * sq) && jj + NST < nchunks)
+                    issue(jj + NST, sq);
+                jj += 2u;
+                sq += 2u;
+                if (sq >= NST) sq -= NST, ph ^= 1u;
             }
+            j += nch;  // every warp: the window's chunks are consumed
+            st += nch % NST;
+            phase ^= (nch / NST) & 1u;
+            if (st >= NST) st -= NST, phase ^= 1u;
+        }
+        for (uint32_t q = 0; q < (PK ? 0u : nch); ++q) {
             mbar_wait(&bars[st], phase);
             // a1: warp wi turns blocks wi, wi+NW, .. (32 pixels x 32 inputs each) into 32
             // bit-sliced words per block
