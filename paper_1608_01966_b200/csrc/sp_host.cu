@@ -356,6 +356,7 @@ struct sp_handle {
     // per-column boosts: wavelet local top-k from this radius on, the bit-sliced comparator below
     // (crossover measured at r ~ 80-100 for C = 1024: scripts/local_general_timing.py)
     uint32_t wm_min_radius = 96;
+    uint32_t wm_min_radius_pi = 256;  // the same for the per-input k_inhibit (CTA wavelet)
     uint32_t learn_Q = 0, learn_smem = 0;  // cluster learning: CTAs per cluster (0 = not eligible)
     bool learn_dbl = false;                 // cluster learning: double-buffered bit-planes
     bool last_learn_cluster = false;
@@ -924,6 +925,9 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         p.boosted_out = rec ? h->d_boosted_rec : nullptr;
         p.radius_dev = h->d_radius;
         p.fl = full_learn_params(h);
+        // CTA wavelet for local inhibition with per-column boosts (k_inhibit), when its scratch fits
+        p.wm_ok = static_cast<int>(sp::inhibit_wavelet_smem(g)) <= h->max_smem ? 1u : 0u;
+        p.wm_min_radius = h->wm_min_radius_pi;
         if (full) p.uniform_bc = 0u;
         e = sp::launch_pack(p, s);
         h->launches++;
@@ -1088,7 +1092,8 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
     }
     if (std::getenv("SP_TRACE")) cudaMalloc(&h->d_trace, 4096u * 6u * sizeof(uint64_t));
     if (const char* et = std::getenv("SP_THREADS")) h->batched_threads = std::atoi(et) == 1024 ? 1024u : 512u;
-    if (const char* ew = std::getenv("SP_WM_MIN_RADIUS")) h->wm_min_radius = static_cast<uint32_t>(std::atoi(ew));
+    if (const char* ew = std::getenv("SP_WM_MIN_RADIUS"))
+        h->wm_min_radius = h->wm_min_radius_pi = static_cast<uint32_t>(std::atoi(ew));
     h->Wn = (g.nbits + 31u) / 32u;
     h->sub_inputs = std::max<uint32_t>(sp::kPerInputChunk, g.P);
     const size_t cs = static_cast<size_t>(g.C) * g.S;

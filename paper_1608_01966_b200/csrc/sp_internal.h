@@ -118,7 +118,10 @@ struct PerInputParams {
     float* boosted_out;        // nullable [call inputs][C]
     const uint32_t* radius_dev;  // nullable: radius in force, else `radius`
     FullLearn fl;              // full learning (k_learn keeps spans; k_full runs (b)-(e))
+    uint32_t wm_ok;            // k_inhibit may use the CTA wavelet (smem sized for it)
+    uint32_t wm_min_radius;    // ... from this radius on (per-column boosts)
 };
+uint32_t inhibit_wavelet_smem(const Geometry& g);
 
 struct LearnParams {
     const uint8_t* frames;     // frames of the call

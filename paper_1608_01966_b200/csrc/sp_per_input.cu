@@ -104,6 +104,145 @@ __device__ __forceinline__ uint64_t key_of(uint32_t raw, uint32_t bc, uint32_t t
     return (N << L) | (((1ull << L) - 1ull) - c);
 }
 
+// Local inhibition with per-column boosts and a large radius, by the whole CTA: a wavelet
+// matrix over the 15-bit coarse keys of all C32 columns (the per-warp version of sp_select.cuh
+// at CTA scale: ballots by warps, a CTA scan of the per-word counts, a stable scatter of
+// (value << 16 | position) pairs, so the bottom level lists the columns of every tie range).
+// Every CTA of the input builds it (the build is the latency; the queries are split), then
+// answers the words [w0, w1): beats(c) = #{u_d > u_c} + #{u_d = u_c, d < c} over W(c), the
+// ties with a lossy column re-decided on the exact keys (R4, R6).  Scratch: 2 x C32 pairs +
+// (B + 1) x (ncw + 2) uint2 levels (the last: lossy flags in the bottom order).
+__device__ void inhibit_wavelet(const PerInputParams& p, uint32_t* sm, uint32_t t, uint32_t gin, uint32_t radius,
+                                uint32_t w0, uint32_t w1, uint32_t* s_total) {
+    const Geometry& g = p.g;
+    const uint32_t tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31u, wid = tid >> 5, nw = nthr >> 5;
+    const uint32_t theta = p.min_overlap, L = g.keyL, C32 = g.C32, ncw = g.ncw, stride = ncw + 2u;
+    const uint32_t* row = p.raw + static_cast<size_t>(t) * C32;
+    const uint32_t* bc = p.bc;
+    uint32_t* bufA = sm;
+    uint32_t* bufB = sm + C32;
+    uint2* lv = reinterpret_cast<uint2*>(sm + 2u * C32);
+    __shared__ unsigned long long s_mm[2];
+    __shared__ uint32_t s_red[32];
+    const CoarseMap cm = coarse_map_block(row, bc, theta, 0u, ncw, s_mm);
+    uint32_t umax = 0;
+    for (uint32_t c = tid; c < C32; c += nthr) {
+        bool lossy;
+        const uint32_t u = c < g.C ? coarse_u15(eligible_N(row[c], bc[c], theta), cm, lossy) : 0u;
+        const uint32_t v = u ? (u << 1) | (lossy ? 1u : 0u) : 0u;
+        bufA[c] = (v << 16) | c;
+        umax = max(umax, u);
+    }
+    umax = __reduce_max_sync(0xffffffffu, umax);
+    if (lane == 0) s_red[wid] = umax;
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t m = __reduce_max_sync(0xffffffffu, lane < nw ? s_red[lane] : 0u);
+        if (lane == 0) s_red[0] = m;
+    }
+    __syncthreads();
+    umax = s_red[0];
+    const uint32_t B = umax ? 32u - __clz(umax) : 1u;
+    __syncthreads();
+    uint32_t* src = bufA;
+    uint32_t* dst = bufB;
+    for (int l = static_cast<int>(B) - 1; l >= -1; --l) {
+        uint2* lvl = lv + (l >= 0 ? l : static_cast<int>(B)) * stride;
+        const uint32_t sb = static_cast<uint32_t>(l + 17);  // bit l of u (l = -1: the lossy flag)
+        for (uint32_t j = wid; j < ncw; j += nw) {
+            const uint32_t w = __ballot_sync(0xffffffffu, (src[j * 32u + lane] >> sb) & 1u);
+            if (lane == 0) lvl[j] = make_uint2(w, static_cast<uint32_t>(__popc(w)));
+        }
+        __syncthreads();
+        // exclusive scan of the per-word counts (ncw <= 1024 = one per thread)
+        uint32_t v = tid < ncw ? lvl[tid].y : 0u, x = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+            if (static_cast<int>(lane) >= d) x += y;
+        }
+        if (lane == 31u) s_red[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            uint32_t z = lane < nw ? s_red[lane] : 0u;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, z, d);
+                if (static_cast<int>(lane) >= d) z += y;
+            }
+            s_red[lane] = z;  // inclusive warp totals
+        }
+        __syncthreads();
+        const uint32_t before = (wid ? s_red[wid - 1u] : 0u) + x - v;
+        const uint32_t ones = s_red[nw - 1u];
+        if (tid < ncw) lvl[tid].y = before;
+        if (tid == 0) lvl[ncw] = make_uint2(0u, ones), lvl[ncw + 1u] = make_uint2(0u, C32 - ones);
+        __syncthreads();
+        if (l < 0) break;
+        const uint32_t Z = C32 - ones;
+        for (uint32_t i = tid; i < C32; i += nthr) {
+            const uint32_t e = src[i];
+            const uint2 q = lvl[i >> 5];
+            const uint32_t r = q.y + __popc(q.x & ((1u << (i & 31u)) - 1u));
+            dst[((e >> sb) & 1u) ? Z + r : i - r] = e;
+        }
+        __syncthreads();
+        uint32_t* tt = src;
+        src = dst;
+        dst = tt;
+    }
+    // queries: the columns of words [w0, w1), one per thread
+    const int R = static_cast<int>(radius), Cn = static_cast<int>(g.C);
+    const uint2* lvL = lv + B * stride;
+    uint32_t my_total = 0;
+    for (uint32_t cw = w0 + wid; cw < w1; cw += nw) {
+        const uint32_t c = cw * 32u + lane;
+        bool lossy_c = false;
+        const uint64_t Nc = c < g.C ? eligible_N(row[c], bc[c], theta) : 0ull;
+        const uint32_t uc = coarse_u15(Nc, cm, lossy_c);
+        bool act = false;
+        if (uc) {
+            const uint32_t lo = static_cast<uint32_t>(max(0, static_cast<int>(c) - R));
+            const uint32_t hi = static_cast<uint32_t>(min(Cn - 1, static_cast<int>(c) + R)) + 1u;
+            uint32_t a = lo, m = c, b = hi, less = 0;
+            for (int l = static_cast<int>(B) - 1; l >= 0; --l) {
+                const uint2* lvl = lv + l * stride;
+                const uint32_t ra = wm_rank2(lvl, a), rm = wm_rank2(lvl, m), rb = wm_rank2(lvl, b);
+                if ((uc >> l) & 1u) {
+                    const uint32_t Z = lvl[ncw + 1u].y;
+                    less += (b - a) - (rb - ra);
+                    a = Z + ra, m = Z + rm, b = Z + rb;
+                } else {
+                    a -= ra, m -= rm, b -= rb;
+                }
+            }
+            int beats = static_cast<int>(((hi - lo) - less - (b - a)) + (m - a));
+            if (b - a > 1u && wm_rank2(lvL, b) != wm_rank2(lvL, a)) {
+                // a lossy column among c's ties: exact keys (src = the bottom level, positions)
+                const uint64_t keyc = (Nc << L) | (((1ull << L) - 1ull) - c);
+                for (uint32_t q = a; q < b; ++q) {
+                    const uint32_t d = src[q] & 0xFFFFu;
+                    if (d == c) continue;
+                    const uint64_t Nd = eligible_N(row[d], bc[d], theta);
+                    bool lossy_d;
+                    coarse_u15(Nd, cm, lossy_d);
+                    if (lossy_c || lossy_d) {
+                        const uint64_t keyd = (Nd << L) | (((1ull << L) - 1ull) - d);
+                        beats += (keyd > keyc ? 1 : 0) - (d < c ? 1 : 0);
+                    }
+                }
+            }
+            act = beats < static_cast<int>(p.k);
+        }
+        const uint32_t word = __ballot_sync(0xffffffffu, act);
+        if (lane == 0) {
+            p.sdr[static_cast<size_t>(gin) * ncw + cw] = word;
+            my_total += __popc(word);
+        }
+    }
+    if (lane == 0 && my_total) atomicAdd(s_total, my_total);
+}
+
 __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
     extern __shared__ uint32_t sm[];
     const Geometry& g = p.g;
@@ -120,6 +259,25 @@ __global__ void __launch_bounds__(1024) k_inhibit(const PerInputParams p) {
     const uint32_t w0 = blockIdx.y * g.ncw / parts, w1 = (blockIdx.y + 1u) * g.ncw / parts;
     const uint32_t tid = threadIdx.x, nthr = blockDim.x;
     const uint32_t radius = p.radius_dev ? *p.radius_dev : p.radius;  // adapted by full learning
+    if (radius > 0 && radius + 1u < g.C && !p.uniform_bc && p.wm_ok && radius >= p.wm_min_radius) {
+        if (p.raw_out) {
+            for (uint32_t c = w0 * 32u + tid; c < min(g.C, w1 * 32u); c += nthr) {
+                const uint32_t r = p.raw[static_cast<size_t>(t) * g.C32 + c];
+                p.raw_out[static_cast<size_t>(gin) * g.C + c] = static_cast<uint16_t>(r);
+                p.boosted_out[static_cast<size_t>(gin) * g.C + c] =
+                    r >= p.min_overlap ? __fmul_rn(static_cast<float>(r), p.boost[c]) : 0.0f;
+            }
+        }
+        if (tid == 0) s_total = 0;
+        __syncthreads();
+        inhibit_wavelet(p, sm, t, gin, radius, w0, w1, &s_total);
+        __syncthreads();
+        if (tid == 0) {
+            if (parts == 1u) p.counts[gin] = s_total;
+            else if (s_total) atomicAdd(p.counts + gin, s_total);  // zeroed before the launch
+        }
+        return;
+    }
     for (uint32_t c = tid; c < g.C32; c += nthr) {
         s_raw[c] = p.raw[static_cast<size_t>(t) * g.C32 + c];
         s_bc[c] = p.bc[c];
@@ -489,6 +647,10 @@ static cudaError_t allow_dynamic_smem(F* fn, int max_smem) {
                                 max_smem - static_cast<int>(a.sharedSizeBytes));
 }
 
+uint32_t inhibit_wavelet_smem(const Geometry& g) {
+    return g.C32 * 8u + 16u * (g.ncw + 2u) * 8u;  // pairs x 2, <= 15 levels + the lossy level
+}
+
 cudaError_t configure_per_input(int max_smem) {
     cudaError_t e = allow_dynamic_smem(k_overlap, max_smem);
     if (e == cudaSuccess) e = allow_dynamic_smem(k_inhibit, max_smem);
@@ -504,7 +666,8 @@ cudaError_t launch_overlap(const PerInputParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_inhibit(const PerInputParams& p, cudaStream_t s, uint32_t parts) {
-    const uint32_t smem = p.g.C32 * 8u + p.g.ncw * 16u * 4u;  // raw, Bc, bit-planes
+    uint32_t smem = p.g.C32 * 8u + p.g.ncw * 16u * 4u;  // raw, Bc, bit-planes
+    if (p.wm_ok) smem = max(smem, inhibit_wavelet_smem(p.g));
     const uint32_t threads = p.g.C32 < 1024u ? p.g.C32 : 1024u;
     if (parts > 1u) {
         cudaError_t e = cudaMemsetAsync(p.counts + p.first_input, 0, p.num_inputs * 4u, s);

@@ -333,13 +333,15 @@ def near1_boosts(C, seed=11):
     return b
 
 
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("selector", ["wavelet", "comparator"])
 @pytest.mark.parametrize("radius", [1, 7, 80, 506, 1023, 1100])
 @pytest.mark.parametrize("boost_mode", ["seeded", "near1"])
-def test_local_general_boost_selectors(radius, boost_mode, selector, monkeypatch):
-    """Local inhibition with per-column boosts in the batched kernel: the wavelet matrix over
-    coarse keys (with the exact re-decision of lossy ties) and the bit-sliced comparator
-    (SP_WM_MIN_RADIUS forces it), against the oracle; r >= C - 1 is global inhibition (C9)."""
+def test_local_general_boost_selectors(radius, boost_mode, selector, path, monkeypatch):
+    """Local inhibition with per-column boosts: the wavelet matrices over coarse keys (per warp
+    in the batched kernel, per CTA in the per-input k_inhibit; lossy ties re-decided exactly)
+    and the bit-sliced comparators (SP_WM_MIN_RADIUS forces one or the other), against the
+    oracle; r >= C - 1 is global inhibition (C9)."""
     monkeypatch.setenv("SP_WM_MIN_RADIUS", "0" if selector == "wavelet" else "100000")
     cfg = ocfg(input_width=96, input_height=64, num_columns=1000, synapses_per_column=64,
                min_overlap=2, winners_set_size=20, inhibition_radius=radius)
@@ -350,7 +352,26 @@ def test_local_general_boost_selectors(radius, boost_mode, selector, monkeypatch
     frames = sp_inputs.frames(77, 0, 45, cfg.input_height, cfg.input_width, rho=0.5)
     ora = O.SpatialPoolerOracle(cfg, state)
     results = [ora.step(x, False) for x in O.encode(frames, cfg)]
-    sp = make_sp(cfg, state, P.SP_PATH_BATCHED)
+    sp = make_sp(cfg, state, path)
+    check_results(results, *run_gpu(sp, frames))
+
+
+@pytest.mark.parametrize("radius", [300, 2000, 4094])
+@pytest.mark.parametrize("boost_mode", ["seeded", "near1"])
+def test_per_input_wavelet_split_ctas(radius, boost_mode, monkeypatch):
+    """C32 >= 2048 on the per-input path: k_inhibit splits an input's SDR words over CTAs, each
+    building the CTA wavelet and answering its words; against the oracle."""
+    monkeypatch.setenv("SP_WM_MIN_RADIUS", "0")
+    cfg = ocfg(input_width=96, input_height=64, num_columns=4000, synapses_per_column=48,
+               min_overlap=2, winners_set_size=40, inhibition_radius=radius)
+    idx, perm, boost = perturbed_state(cfg)
+    if boost_mode == "near1":
+        boost = near1_boosts(cfg.num_columns)
+    state = (idx, perm, boost)
+    frames = sp_inputs.frames(78, 0, 6, cfg.input_height, cfg.input_width, rho=0.5)
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = [ora.step(x, False) for x in O.encode(frames, cfg)]
+    sp = make_sp(cfg, state, P.SP_PATH_PER_INPUT)
     check_results(results, *run_gpu(sp, frames))
 
 
