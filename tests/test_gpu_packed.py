@@ -133,3 +133,24 @@ def test_packed_errors():
     bad = torch.zeros((2, sp2.packed_words + 1), dtype=torch.int32, device=DEV)[:, 1:]
     with pytest.raises(P.SpError):
         sp2.compute_packed(bad)  # not contiguous / misaligned
+
+
+def test_packed_host_multi_chunk_pipeline():
+    """sp_compute_packed_host over more frames than one staging chunk (~1035 bit-plane frames of
+    960x540): the double-buffered H2D / compute / D2H pipeline equals the device call."""
+    cfg = ocfg(input_width=960, input_height=540, num_columns=1024, synapses_per_column=256,
+               min_overlap=4, winners_set_size=40)
+    sp = make_sp(cfg, perturbed_state(cfg), P.SP_PATH_BATCHED, max_inputs=2600, record=False)
+    frames = torch.empty((2600, 540, 960), dtype=torch.uint8, device=DEV)
+    P.synth_frames(frames, 0, 31, 0.5)
+    planes = sp.pack_frames(frames)
+    del frames
+    sdr_d = torch.empty((2600, 32), dtype=torch.int32, device=DEV)
+    cnt_d = torch.empty((2600,), dtype=torch.int32, device=DEV)
+    sp.compute_packed(planes, sdr_d, cnt_d)
+    host = planes.cpu()
+    sdr_h = np.empty((2600, 32), np.uint32)
+    cnt_h = np.empty((2600,), np.uint32)
+    sp.compute_packed_host_into(host.numpy(), sdr_h, cnt_h)
+    assert np.array_equal(sdr_h.view(np.int32), sdr_d.cpu().numpy())
+    assert np.array_equal(cnt_h.view(np.int32), cnt_d.cpu().numpy())
