@@ -259,6 +259,38 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             // raw counts (<= 1023, exact in fp16) of this lane's columns, two per half2,
             // zeroed below r_lo; counts of raw >= x with HSET2/HADD2 (FMA pipe, no atomics)
             constexpr int NH = (CPT * NW + 1) / 2;
+            const uint32_t f2 = f + K * NW;
+            if (CPT <= 2 && NW <= 16u && f2 < gs && K == 1u && !p.raw_out) {
+                // this warp's next input too: both searches and SDR loops interleaved
+                const uint16_t* row2 = rawbuf + f2 * p.C32;
+                const uint32_t gin2 = in0 + f2;
+                uint32_t rgt[2], rtie[2], need[2];
+                global_uniform_threshold2<NH>(row, row2, p.C32, p.S, p.k, r_lo, lane, rgt, rtie, need);
+                uint32_t total[2] = {0u, 0u}, tbf[2] = {0u, 0u}, myw[2] = {0u, 0u};
+                for (uint32_t cw = 0; cw < p.ncw; ++cw) {
+                    const uint32_t r[2] = {row[cw * 32u + lane], row2[cw * 32u + lane]};
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                        const uint32_t tb = __ballot_sync(0xffffffffu, r[q] == rtie[q]);
+                        const bool act = r[q] >= rgt[q] ||
+                                         (r[q] == rtie[q] && tbf[q] + __popc(tb & ((1u << lane) - 1u)) < need[q]);
+                        tbf[q] += __popc(tb);
+                        const uint32_t word = __ballot_sync(0xffffffffu, act);
+                        if ((cw & 31u) == lane) myw[q] = word;
+                        total[q] += __popc(word);
+                    }
+                    if ((cw & 31u) == 31u || cw + 1u == p.ncw) {  // coalesced stores of <= 32 words
+                        const uint32_t base = cw & ~31u;
+                        if (lane <= (cw & 31u)) {
+                            p.sdr[static_cast<size_t>(gin) * p.ncw + base + lane] = myw[0];
+                            p.sdr[static_cast<size_t>(gin2) * p.ncw + base + lane] = myw[1];
+                        }
+                    }
+                }
+                if (lane == 0) p.counts[gin] = total[0], p.counts[gin2] = total[1];
+                f = f2;  // the loop's increment moves past f2
+                continue;
+            }
             uint32_t rgt, rtie, need;
             global_uniform_threshold<NH>(row, p.C32, p.S, p.k, r_lo, lane, rgt, rtie, need);
             uint32_t total = 0, ties_before = 0, myword = 0;

@@ -938,6 +938,61 @@ __device__ __forceinline__ void global_uniform_threshold(const RowT* row, uint32
     }
 }
 
+// The same for two inputs at once (rows a and b): two independent count chains per step, so
+// the latency of one search hides behind the other's (a warp's two inputs of the batched top-k).
+template <int NH, typename RowT>
+__device__ __forceinline__ void global_uniform_threshold2(const RowT* ra_row, const RowT* rb_row, uint32_t C32,
+                                                          uint32_t S, uint32_t k, uint32_t r_lo, uint32_t lane,
+                                                          uint32_t rgt[2], uint32_t rtie[2], uint32_t need[2]) {
+    __half2 ha[NH], hb[NH];
+#pragma unroll
+    for (int t = 0; t < NH; ++t) {
+        const uint32_t ca = (2u * t) * 32u + lane, cb = ca + 32u;
+        uint32_t a0 = ca < C32 ? static_cast<uint32_t>(ra_row[ca]) : 0u;
+        uint32_t a1 = cb < C32 ? static_cast<uint32_t>(ra_row[cb]) : 0u;
+        uint32_t b0 = ca < C32 ? static_cast<uint32_t>(rb_row[ca]) : 0u;
+        uint32_t b1 = cb < C32 ? static_cast<uint32_t>(rb_row[cb]) : 0u;
+        a0 = a0 >= r_lo ? a0 : 0u;
+        a1 = a1 >= r_lo ? a1 : 0u;
+        b0 = b0 >= r_lo ? b0 : 0u;
+        b1 = b1 >= r_lo ? b1 : 0u;
+        ha[t] = __halves2half2(__uint2half_rn(a0), __uint2half_rn(a1));
+        hb[t] = __halves2half2(__uint2half_rn(b0), __uint2half_rn(b1));
+    }
+    auto count_ge2 = [&](uint32_t xa, uint32_t xb, uint32_t& na, uint32_t& nb) {
+        const __half2 hxa = __half2half2(__uint2half_rn(xa)), hxb = __half2half2(__uint2half_rn(xb));
+        __half2 a0 = __float2half2_rn(0.0f), a1 = a0, b0 = a0, b1 = a0;
+#pragma unroll
+        for (int t = 0; t < NH; t += 2) {
+            a0 = __hadd2(a0, __hge2(ha[t], hxa));
+            b0 = __hadd2(b0, __hge2(hb[t], hxb));
+            if (t + 1 < NH) {
+                a1 = __hadd2(a1, __hge2(ha[t + 1], hxa));
+                b1 = __hadd2(b1, __hge2(hb[t + 1], hxb));
+            }
+        }
+        const __half2 sa = __hadd2(a0, a1), sb = __hadd2(b0, b1);
+        na = __reduce_add_sync(0xffffffffu, static_cast<uint32_t>(__low2float(sa) + __high2float(sa)));
+        nb = __reduce_add_sync(0xffffffffu, static_cast<uint32_t>(__low2float(sb) + __high2float(sb)));
+    };
+    uint32_t na, nb;
+    count_ge2(r_lo, r_lo, na, nb);
+    const bool sa = na >= k, sb = nb >= k;  // else: every eligible column wins
+    uint32_t Ta = 0, Tb = 0;
+    for (int bit = 31 - __clz(S); bit >= 0; --bit) {
+        count_ge2(Ta | (1u << bit), Tb | (1u << bit), na, nb);
+        if (na >= k) Ta |= 1u << bit;
+        if (nb >= k) Tb |= 1u << bit;
+    }
+    count_ge2(Ta + 1u, Tb + 1u, na, nb);
+    rgt[0] = sa ? Ta + 1u : r_lo;
+    rtie[0] = sa ? Ta : 0xFFFFFFFFu;
+    need[0] = sa ? k - na : 0u;
+    rgt[1] = sb ? Tb + 1u : r_lo;
+    rtie[1] = sb ? Tb : 0xFFFFFFFFu;
+    need[1] = sb ? k - nb : 0u;
+}
+
 // Per-column boosts (R4, R6): (1) the k-th largest 16-bit coarse key u = N >> sh (Tu) by a
 // bitwise search over keys packed two per register (columns 64t+lane, 64t+32+lane);
 // (2) the exact key threshold T2 among the columns tied at u == Tu (a 64-entry list in
