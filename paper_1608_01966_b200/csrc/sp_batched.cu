@@ -266,48 +266,23 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
                 const uint32_t gin2 = in0 + f2;
                 uint32_t rgt[2], rtie[2], need[2];
                 global_uniform_threshold2<NH>(row, row2, p.C32, p.S, p.k, r_lo, lane, rgt, rtie, need);
-                uint32_t total[2] = {0u, 0u}, tbf[2] = {0u, 0u}, myw[2] = {0u, 0u};
-                for (uint32_t cw = 0; cw < p.ncw; ++cw) {
-                    const uint32_t r[2] = {row[cw * 32u + lane], row2[cw * 32u + lane]};
-#pragma unroll
-                    for (int q = 0; q < 2; ++q) {
-                        const uint32_t tb = __ballot_sync(0xffffffffu, r[q] == rtie[q]);
-                        const bool act = r[q] >= rgt[q] ||
-                                         (r[q] == rtie[q] && tbf[q] + __popc(tb & ((1u << lane) - 1u)) < need[q]);
-                        tbf[q] += __popc(tb);
-                        const uint32_t word = __ballot_sync(0xffffffffu, act);
-                        if ((cw & 31u) == lane) myw[q] = word;
-                        total[q] += __popc(word);
-                    }
-                    if ((cw & 31u) == 31u || cw + 1u == p.ncw) {  // coalesced stores of <= 32 words
-                        const uint32_t base = cw & ~31u;
-                        if (lane <= (cw & 31u)) {
-                            p.sdr[static_cast<size_t>(gin) * p.ncw + base + lane] = myw[0];
-                            p.sdr[static_cast<size_t>(gin2) * p.ncw + base + lane] = myw[1];
-                        }
-                    }
-                }
-                if (lane == 0) p.counts[gin] = total[0], p.counts[gin2] = total[1];
+                const uint32_t tot0 = uniform_sdr_words(row, p.ncw, rgt[0], rtie[0], need[0], lane,
+                                                        [&](uint32_t w, uint32_t word) {
+                                                            p.sdr[static_cast<size_t>(gin) * p.ncw + w] = word;
+                                                        });
+                const uint32_t tot1 = uniform_sdr_words(row2, p.ncw, rgt[1], rtie[1], need[1], lane,
+                                                        [&](uint32_t w, uint32_t word) {
+                                                            p.sdr[static_cast<size_t>(gin2) * p.ncw + w] = word;
+                                                        });
+                if (lane == 0) p.counts[gin] = tot0, p.counts[gin2] = tot1;
                 f = f2;  // the loop's increment moves past f2
                 continue;
             }
             uint32_t rgt, rtie, need;
             global_uniform_threshold<NH>(row, p.C32, p.S, p.k, r_lo, lane, rgt, rtie, need);
-            uint32_t total = 0, ties_before = 0, myword = 0;
-            for (uint32_t cw = 0; cw < p.ncw; ++cw) {
-                const uint32_t r = row[cw * 32u + lane];
-                const uint32_t tb = __ballot_sync(0xffffffffu, r == rtie);
-                const bool act = r >= rgt ||
-                                 (r == rtie && ties_before + __popc(tb & ((1u << lane) - 1u)) < need);
-                ties_before += __popc(tb);
-                const uint32_t word = __ballot_sync(0xffffffffu, act);
-                if ((cw & 31u) == lane) myword = word;
-                total += __popc(word);
-                if ((cw & 31u) == 31u || cw + 1u == p.ncw) {  // coalesced store of <= 32 words
-                    const uint32_t base = cw & ~31u;
-                    if (lane <= (cw & 31u)) p.sdr[static_cast<size_t>(gin) * p.ncw + base + lane] = myword;
-                }
-            }
+            const uint32_t total = uniform_sdr_words(row, p.ncw, rgt, rtie, need, lane, [&](uint32_t w, uint32_t word) {
+                p.sdr[static_cast<size_t>(gin) * p.ncw + w] = word;
+            });
             if (lane == 0) p.counts[gin] = total;
             continue;
         }
@@ -714,7 +689,7 @@ __global__ void __launch_bounds__(NT, 1) sp_patch_kernel(const __grid_constant__
     const uint32_t stage_bytes = p.patch_stage_bytes;  // 32 * nbits rounded to 1 KiB
     uint8_t* stage_base = smem;
     uint32_t* X = reinterpret_cast<uint32_t*>(smem + NST * stage_bytes);         // [Lw + 1]
-    uint16_t* rawbuf = reinterpret_cast<uint16_t*>(X + p.Lw + 1u + ((p.Lw + 1u) & 1u));  // [32][C32]
+    uint16_t* rawbuf = reinterpret_cast<uint16_t*>(X + ((p.Lw + 4u) & ~3u));  // [32][C32], 16-byte aligned
     uint8_t* scratch = reinterpret_cast<uint8_t*>(rawbuf + 32u * p.C32);         // top-k scratch
     uint32_t* s_bc = reinterpret_cast<uint32_t*>(scratch + p.region_bytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_bc + p.C32);

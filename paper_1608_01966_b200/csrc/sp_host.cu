@@ -222,7 +222,7 @@ BatchedLayout plan_patch_layout(const Geometry& g, int max_smem) {
     const uint32_t Lw = (g.nbits + 31u) / 32u * 32u;
     const uint32_t topk_bytes = 16u * 1024u * 4u;  // 16 warps: coarse bit-planes <= 1024 words
     for (uint32_t stages = 4; stages >= 2; --stages) {
-        const uint32_t smem = stages * stage_bytes + (Lw + 2u) * 4u + 32u * g.C32 * 2u + topk_bytes +
+        const uint32_t smem = stages * stage_bytes + ((Lw + 4u) & ~3u) * 4u + 32u * g.C32 * 2u + topk_bytes +
                               g.C32 * 4u + stages * 12u;
         if (static_cast<int>(smem) > max_smem) continue;
         L.ok = true;

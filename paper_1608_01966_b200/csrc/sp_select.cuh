@@ -938,6 +938,54 @@ __device__ __forceinline__ void global_uniform_threshold(const RowT* row, uint32
     }
 }
 
+// SDR words of one input (global, uniform boost) from its threshold (rgt, rtie, need): lane j
+// builds words j, j+32, .. from its own 32 raw counts (four conflict-free LDS.128: the 16-byte
+// chunks are visited in a lane-rotated order), so there is no chain across words; the `need`
+// lowest-index columns with raw == rtie win through a warp scan of the per-word tie counts.
+// store(w, word) gets every word once (lane-parallel, coalesced); returns the winner count
+// (all lanes).  row: 16-byte aligned uint16 counts [ncw * 32].
+template <typename Store>
+__device__ __forceinline__ uint32_t uniform_sdr_words(const uint16_t* row, uint32_t ncw, uint32_t rgt,
+                                                      uint32_t rtie, uint32_t need, uint32_t lane, Store store) {
+    uint32_t total = 0, carry = 0;
+    for (uint32_t j0 = 0; j0 < ncw; j0 += 32u) {
+        const uint32_t j = j0 + lane;
+        uint32_t win = 0, tie = 0;
+        if (j < ncw) {
+#pragma unroll
+            for (uint32_t q = 0; q < 4u; ++q) {
+                const uint32_t qq = (q + (lane >> 1)) & 3u;
+                const uint4 v = *reinterpret_cast<const uint4*>(row + 32u * j + 8u * qq);
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (uint32_t e = 0; e < 4u; ++e) {
+                    const uint32_t lo = w[e] & 0xFFFFu, hi = w[e] >> 16;
+                    const uint32_t sh = 8u * qq + 2u * e;
+                    win |= (lo >= rgt ? 1u : 0u) << sh | (hi >= rgt ? 2u : 0u) << sh;
+                    tie |= (lo == rtie ? 1u : 0u) << sh | (hi == rtie ? 2u : 0u) << sh;
+                }
+            }
+        }
+        const uint32_t tc = __popc(tie);
+        uint32_t incl = tc;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+            if (static_cast<int>(lane) >= d) incl += y;
+        }
+        const uint32_t before = carry + incl - tc;
+        uint32_t grant = need > before ? min(need - before, tc) : 0u;
+        while (grant--) {
+            win |= tie & (0u - tie);  // lowest remaining tie
+            tie &= tie - 1u;
+        }
+        if (j < ncw) store(j, win);
+        total += __reduce_add_sync(0xffffffffu, __popc(win));
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    return total;
+}
+
 // The same for two inputs at once (rows a and b): two independent count chains per step, so
 // the latency of one search hides behind the other's (a warp's two inputs of the batched top-k).
 template <int NH, typename RowT>
