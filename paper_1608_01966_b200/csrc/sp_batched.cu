@@ -196,11 +196,56 @@ __device__ __forceinline__ void accumulate8(Planes& P, uint32_t x0, uint32_t x1,
     }
 }
 
-__device__ __forceinline__ uint32_t extract_count(const Planes& P, uint32_t f) {
-    uint32_t v = ((P.ones >> f) & 1u) | (((P.twos >> f) & 1u) << 1) | (((P.fours >> f) & 1u) << 2);
+// Raw counts of column c for the gs inputs of a group into rawbuf[f][c].
+__device__ __forceinline__ void store_counts(const Planes& P, uint16_t* rawbuf, uint32_t C32, uint32_t c,
+                                             uint32_t gs) {
+    // all 32 counts of column c at once: the 10 planes as a 16 x 32 bit matrix (rows b,
+    // bit f = input f), transposed in registers as two 16 x 16 blocks side by side;
+    // then y_j holds count_j (low half) and count_{j+16} (high half)
+    uint32_t y0, y1, y2, y3, y4, y5, y6, y7, y8, y9, y10, y11, y12, y13, y14, y15;
+    static_assert(kHiPlanes == 7, "10 count planes (ones, twos, fours, 7 high)");
+    y0 = P.ones, y1 = P.twos, y2 = P.fours;
+    y3 = P.hi[0], y4 = P.hi[1], y5 = P.hi[2], y6 = P.hi[3], y7 = P.hi[4], y8 = P.hi[5], y9 = P.hi[6];
+    y10 = 0u, y11 = 0u, y12 = 0u, y13 = 0u, y14 = 0u, y15 = 0u;
+    { const uint32_t t = ((y0 >> 8) ^ y8) & 0x00FF00FFu; y8 ^= t; y0 ^= t << 8; }
+    { const uint32_t t = ((y1 >> 8) ^ y9) & 0x00FF00FFu; y9 ^= t; y1 ^= t << 8; }
+    { const uint32_t t = ((y2 >> 8) ^ y10) & 0x00FF00FFu; y10 ^= t; y2 ^= t << 8; }
+    { const uint32_t t = ((y3 >> 8) ^ y11) & 0x00FF00FFu; y11 ^= t; y3 ^= t << 8; }
+    { const uint32_t t = ((y4 >> 8) ^ y12) & 0x00FF00FFu; y12 ^= t; y4 ^= t << 8; }
+    { const uint32_t t = ((y5 >> 8) ^ y13) & 0x00FF00FFu; y13 ^= t; y5 ^= t << 8; }
+    { const uint32_t t = ((y6 >> 8) ^ y14) & 0x00FF00FFu; y14 ^= t; y6 ^= t << 8; }
+    { const uint32_t t = ((y7 >> 8) ^ y15) & 0x00FF00FFu; y15 ^= t; y7 ^= t << 8; }
+    { const uint32_t t = ((y0 >> 4) ^ y4) & 0x0F0F0F0Fu; y4 ^= t; y0 ^= t << 4; }
+    { const uint32_t t = ((y1 >> 4) ^ y5) & 0x0F0F0F0Fu; y5 ^= t; y1 ^= t << 4; }
+    { const uint32_t t = ((y2 >> 4) ^ y6) & 0x0F0F0F0Fu; y6 ^= t; y2 ^= t << 4; }
+    { const uint32_t t = ((y3 >> 4) ^ y7) & 0x0F0F0F0Fu; y7 ^= t; y3 ^= t << 4; }
+    { const uint32_t t = ((y8 >> 4) ^ y12) & 0x0F0F0F0Fu; y12 ^= t; y8 ^= t << 4; }
+    { const uint32_t t = ((y9 >> 4) ^ y13) & 0x0F0F0F0Fu; y13 ^= t; y9 ^= t << 4; }
+    { const uint32_t t = ((y10 >> 4) ^ y14) & 0x0F0F0F0Fu; y14 ^= t; y10 ^= t << 4; }
+    { const uint32_t t = ((y11 >> 4) ^ y15) & 0x0F0F0F0Fu; y15 ^= t; y11 ^= t << 4; }
+    { const uint32_t t = ((y0 >> 2) ^ y2) & 0x33333333u; y2 ^= t; y0 ^= t << 2; }
+    { const uint32_t t = ((y1 >> 2) ^ y3) & 0x33333333u; y3 ^= t; y1 ^= t << 2; }
+    { const uint32_t t = ((y4 >> 2) ^ y6) & 0x33333333u; y6 ^= t; y4 ^= t << 2; }
+    { const uint32_t t = ((y5 >> 2) ^ y7) & 0x33333333u; y7 ^= t; y5 ^= t << 2; }
+    { const uint32_t t = ((y8 >> 2) ^ y10) & 0x33333333u; y10 ^= t; y8 ^= t << 2; }
+    { const uint32_t t = ((y9 >> 2) ^ y11) & 0x33333333u; y11 ^= t; y9 ^= t << 2; }
+    { const uint32_t t = ((y12 >> 2) ^ y14) & 0x33333333u; y14 ^= t; y12 ^= t << 2; }
+    { const uint32_t t = ((y13 >> 2) ^ y15) & 0x33333333u; y15 ^= t; y13 ^= t << 2; }
+    { const uint32_t t = ((y0 >> 1) ^ y1) & 0x55555555u; y1 ^= t; y0 ^= t << 1; }
+    { const uint32_t t = ((y2 >> 1) ^ y3) & 0x55555555u; y3 ^= t; y2 ^= t << 1; }
+    { const uint32_t t = ((y4 >> 1) ^ y5) & 0x55555555u; y5 ^= t; y4 ^= t << 1; }
+    { const uint32_t t = ((y6 >> 1) ^ y7) & 0x55555555u; y7 ^= t; y6 ^= t << 1; }
+    { const uint32_t t = ((y8 >> 1) ^ y9) & 0x55555555u; y9 ^= t; y8 ^= t << 1; }
+    { const uint32_t t = ((y10 >> 1) ^ y11) & 0x55555555u; y11 ^= t; y10 ^= t << 1; }
+    { const uint32_t t = ((y12 >> 1) ^ y13) & 0x55555555u; y13 ^= t; y12 ^= t << 1; }
+    { const uint32_t t = ((y14 >> 1) ^ y15) & 0x55555555u; y15 ^= t; y14 ^= t << 1; }
+    const uint32_t ys[16] = {y0, y1, y2, y3, y4, y5, y6, y7, y8, y9, y10, y11, y12, y13, y14, y15};
 #pragma unroll
-    for (int h = 0; h < (int)kHiPlanes; ++h) v |= ((P.hi[h] >> f) & 1u) << (3 + h);
-    return v;
+    for (int j = 0; j < 16; ++j) {
+        if (static_cast<uint32_t>(j) < gs) rawbuf[j * C32 + c] = static_cast<uint16_t>(ys[j]);
+        if (static_cast<uint32_t>(j) + 16u < gs)
+            rawbuf[(j + 16) * C32 + c] = static_cast<uint16_t>(ys[j] >> 16);
+    }
 }
 
 // Rank key of column c (R4/R6): exact boosted overlap N = raw*Bc over 2^23,
@@ -653,53 +698,7 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t cw = wi + NW * i;
         if (cw < p.ncw) {
             const uint32_t c = cw * 32u + lane;
-            // all 32 counts of column c at once: the 10 planes as a 16 x 32 bit matrix (rows b,
-            // bit f = input f), transposed in registers as two 16 x 16 blocks side by side;
-            // then y_j holds count_j (low half) and count_{j+16} (high half)
-            uint32_t y0, y1, y2, y3, y4, y5, y6, y7, y8, y9, y10, y11, y12, y13, y14, y15;
-            static_assert(kHiPlanes == 7, "10 count planes (ones, twos, fours, 7 high)");
-            y0 = P[i].ones, y1 = P[i].twos, y2 = P[i].fours;
-            y3 = P[i].hi[0], y4 = P[i].hi[1], y5 = P[i].hi[2], y6 = P[i].hi[3], y7 = P[i].hi[4], y8 = P[i].hi[5], y9 = P[i].hi[6];
-            y10 = 0u, y11 = 0u, y12 = 0u, y13 = 0u, y14 = 0u, y15 = 0u;
-            { const uint32_t t = ((y0 >> 8) ^ y8) & 0x00FF00FFu; y8 ^= t; y0 ^= t << 8; }
-            { const uint32_t t = ((y1 >> 8) ^ y9) & 0x00FF00FFu; y9 ^= t; y1 ^= t << 8; }
-            { const uint32_t t = ((y2 >> 8) ^ y10) & 0x00FF00FFu; y10 ^= t; y2 ^= t << 8; }
-            { const uint32_t t = ((y3 >> 8) ^ y11) & 0x00FF00FFu; y11 ^= t; y3 ^= t << 8; }
-            { const uint32_t t = ((y4 >> 8) ^ y12) & 0x00FF00FFu; y12 ^= t; y4 ^= t << 8; }
-            { const uint32_t t = ((y5 >> 8) ^ y13) & 0x00FF00FFu; y13 ^= t; y5 ^= t << 8; }
-            { const uint32_t t = ((y6 >> 8) ^ y14) & 0x00FF00FFu; y14 ^= t; y6 ^= t << 8; }
-            { const uint32_t t = ((y7 >> 8) ^ y15) & 0x00FF00FFu; y15 ^= t; y7 ^= t << 8; }
-            { const uint32_t t = ((y0 >> 4) ^ y4) & 0x0F0F0F0Fu; y4 ^= t; y0 ^= t << 4; }
-            { const uint32_t t = ((y1 >> 4) ^ y5) & 0x0F0F0F0Fu; y5 ^= t; y1 ^= t << 4; }
-            { const uint32_t t = ((y2 >> 4) ^ y6) & 0x0F0F0F0Fu; y6 ^= t; y2 ^= t << 4; }
-            { const uint32_t t = ((y3 >> 4) ^ y7) & 0x0F0F0F0Fu; y7 ^= t; y3 ^= t << 4; }
-            { const uint32_t t = ((y8 >> 4) ^ y12) & 0x0F0F0F0Fu; y12 ^= t; y8 ^= t << 4; }
-            { const uint32_t t = ((y9 >> 4) ^ y13) & 0x0F0F0F0Fu; y13 ^= t; y9 ^= t << 4; }
-            { const uint32_t t = ((y10 >> 4) ^ y14) & 0x0F0F0F0Fu; y14 ^= t; y10 ^= t << 4; }
-            { const uint32_t t = ((y11 >> 4) ^ y15) & 0x0F0F0F0Fu; y15 ^= t; y11 ^= t << 4; }
-            { const uint32_t t = ((y0 >> 2) ^ y2) & 0x33333333u; y2 ^= t; y0 ^= t << 2; }
-            { const uint32_t t = ((y1 >> 2) ^ y3) & 0x33333333u; y3 ^= t; y1 ^= t << 2; }
-            { const uint32_t t = ((y4 >> 2) ^ y6) & 0x33333333u; y6 ^= t; y4 ^= t << 2; }
-            { const uint32_t t = ((y5 >> 2) ^ y7) & 0x33333333u; y7 ^= t; y5 ^= t << 2; }
-            { const uint32_t t = ((y8 >> 2) ^ y10) & 0x33333333u; y10 ^= t; y8 ^= t << 2; }
-            { const uint32_t t = ((y9 >> 2) ^ y11) & 0x33333333u; y11 ^= t; y9 ^= t << 2; }
-            { const uint32_t t = ((y12 >> 2) ^ y14) & 0x33333333u; y14 ^= t; y12 ^= t << 2; }
-            { const uint32_t t = ((y13 >> 2) ^ y15) & 0x33333333u; y15 ^= t; y13 ^= t << 2; }
-            { const uint32_t t = ((y0 >> 1) ^ y1) & 0x55555555u; y1 ^= t; y0 ^= t << 1; }
-            { const uint32_t t = ((y2 >> 1) ^ y3) & 0x55555555u; y3 ^= t; y2 ^= t << 1; }
-            { const uint32_t t = ((y4 >> 1) ^ y5) & 0x55555555u; y5 ^= t; y4 ^= t << 1; }
-            { const uint32_t t = ((y6 >> 1) ^ y7) & 0x55555555u; y7 ^= t; y6 ^= t << 1; }
-            { const uint32_t t = ((y8 >> 1) ^ y9) & 0x55555555u; y9 ^= t; y8 ^= t << 1; }
-            { const uint32_t t = ((y10 >> 1) ^ y11) & 0x55555555u; y11 ^= t; y10 ^= t << 1; }
-            { const uint32_t t = ((y12 >> 1) ^ y13) & 0x55555555u; y13 ^= t; y12 ^= t << 1; }
-            { const uint32_t t = ((y14 >> 1) ^ y15) & 0x55555555u; y15 ^= t; y14 ^= t << 1; }
-            const uint32_t ys[16] = {y0, y1, y2, y3, y4, y5, y6, y7, y8, y9, y10, y11, y12, y13, y14, y15};
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                if (static_cast<uint32_t>(j) < gs) rawbuf[j * p.C32 + c] = static_cast<uint16_t>(ys[j]);
-                if (static_cast<uint32_t>(j) + 16u < gs)
-                    rawbuf[(j + 16) * p.C32 + c] = static_cast<uint16_t>(ys[j] >> 16);
-            }
+            store_counts(P[i], rawbuf, p.C32, c, gs);
         }
     }
     cg::cluster_group cluster = cg::this_cluster();
@@ -820,8 +819,7 @@ __global__ void __launch_bounds__(NT, 1) sp_patch_kernel(const __grid_constant__
                                 X[s8.w & 0xFFFFu], X[s8.w >> 16]);
                 }
                 const uint32_t c = cw * 32u + lane;
-                for (uint32_t f = 0; f < gs; ++f)
-                    rawbuf[f * p.C32 + c] = static_cast<uint16_t>(extract_count(P[i], f));
+                store_counts(P[i], rawbuf, p.C32, c, gs);
             }
         }
         __syncthreads();  // raw counts of the group complete; X may be overwritten
