@@ -333,39 +333,83 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
         }
         if (radius > 0 && p.uniform_bc) {
             const uint32_t r_lo = uniform_r_lo(theta, s_bc[0]);
-            // range of the eligible raw counts of this input: the wavelet path needs <= 8 levels
-            uint32_t xmn = 0xFFFFFFFFu, xmx = 0u;
-            for (uint32_t c = lane; c < p.C; c += 32u) {
-                const uint32_t x = row[c];
-                if (x >= r_lo) xmn = min(xmn, x), xmx = max(xmx, x);
-            }
-            xmn = __reduce_min_sync(0xffffffffu, xmn);
-            xmx = __reduce_max_sync(0xffffffffu, xmx);
-            const uint32_t B = xmn <= xmx ? 32u - __clz(xmx - xmn + 1u) : 1u;
-            // per-warp scratch sized for the largest B (8): the warps' regions must not depend on
-            // their inputs' ranges
+            // range of the eligible raw counts of an input: the wavelet path needs <= 8 levels
+            auto range_of = [&](const uint16_t* rw, uint32_t& xmn, uint32_t& Bo) {
+                uint32_t mn = 0xFFFFFFFFu, mx = 0u;
+                for (uint32_t c = lane; c < p.C; c += 32u) {
+                    const uint32_t x = rw[c];
+                    if (x >= r_lo) mn = min(mn, x), mx = max(mx, x);
+                }
+                mn = __reduce_min_sync(0xffffffffu, mn);
+                mx = __reduce_max_sync(0xffffffffu, mx);
+                xmn = mn;
+                Bo = mn <= mx ? 32u - __clz(mx - mn + 1u) : 1u;
+            };
+            uint32_t xmn, B;
+            range_of(row, xmn, B);
+            // per-warp scratch slots sized for the largest B (8), so the warps' regions do not
+            // depend on their inputs' ranges; a warp's comparator fallback uses its own slot too.
+            // With room in the idle ring + windows (`big`), a slot holds two wavelets and the warp
+            // runs its two inputs together.
             const uint32_t wbytes = (2u * p.C32 + 8u * 8u * (p.ncw + 2u) + 127u) & ~127u;
-            if (B <= 8u && wbytes * NW <= p.region_bytes) {
+            const uint32_t slot2 = max(2u * wbytes, 2560u), slot1 = max(wbytes, 2560u);
+            const bool pairs = K == 1u && !p.raw_out && slot2 * NW <= big_bytes;
+            const bool slotted = pairs || slot1 * NW <= p.region_bytes;
+            uint8_t* wslot = pairs ? big + wi * slot2 : region + wi * slot1;
+            const uint32_t f2 = f + K * NW;
+            if (pairs && f2 < gs && B <= 8u) {
+                const uint16_t* row2 = rawbuf + f2 * p.C32;
+                uint32_t xmn2, B2;
+                range_of(row2, xmn2, B2);
+                if (B2 <= 8u) {
+                    const uint32_t gin2 = in0 + f2;
+                    const uint16_t* rows[2] = {row, row2};
+                    const uint32_t xmins[2] = {xmn, xmn2};
+                    uint8_t* b0s[2] = {wslot, wslot + wbytes};
+                    uint8_t* b1s[2] = {wslot + p.C32, wslot + wbytes + p.C32};
+                    uint2* lvs[2] = {reinterpret_cast<uint2*>(wslot + 2u * p.C32),
+                                     reinterpret_cast<uint2*>(wslot + wbytes + 2u * p.C32)};
+                    uint32_t total[2] = {0u, 0u}, myw[2] = {0u, 0u};
+                    const uint32_t gins[2] = {gin, gin2};
+                    local_uniform_wavelet<2>(rows, p.C, p.C32, p.ncw, radius, p.k, r_lo, xmins, max(B, B2), b0s, b1s,
+                                             lvs, lane, [&](int i, uint32_t cw, uint32_t word) {
+                                                 if ((cw & 31u) == lane) myw[i] = word;
+                                                 total[i] += __popc(word);
+                                                 if ((cw & 31u) == 31u || cw + 1u == p.ncw) {
+                                                     const uint32_t w0 = cw & ~31u;
+                                                     if (lane <= (cw & 31u))
+                                                         p.sdr[static_cast<size_t>(gins[i]) * p.ncw + w0 + lane] = myw[i];
+                                                 }
+                                             });
+                    if (lane == 0) p.counts[gin] = total[0], p.counts[gin2] = total[1];
+                    f = f2;  // the loop's increment moves past f2
+                    continue;
+                }
+            }
+            if (B <= 8u && slotted) {
                 // wavelet matrix over the positions (sp_select.cuh): O(C log range) per input
-                uint8_t* base = region + wi * wbytes;
-                uint2* lv = reinterpret_cast<uint2*>(base + 2u * p.C32);
+                const uint16_t* rows[1] = {row};
+                const uint32_t xmins[1] = {xmn};
+                uint8_t* b0s[1] = {wslot};
+                uint8_t* b1s[1] = {wslot + p.C32};
+                uint2* lvs[1] = {reinterpret_cast<uint2*>(wslot + 2u * p.C32)};
                 uint32_t total = 0, myword = 0;
-                local_uniform_wavelet(row, p.C, p.C32, p.ncw, radius, p.k, r_lo, xmn, B, base, base + p.C32, lv,
-                                      lane, [&](uint32_t cw, uint32_t word) {
-                                          if ((cw & 31u) == lane) myword = word;
-                                          total += __popc(word);
-                                          if ((cw & 31u) == 31u || cw + 1u == p.ncw) {
-                                              const uint32_t b0 = cw & ~31u;
-                                              if (lane <= (cw & 31u))
-                                                  p.sdr[static_cast<size_t>(gin) * p.ncw + b0 + lane] = myword;
-                                          }
-                                      });
+                local_uniform_wavelet<1>(rows, p.C, p.C32, p.ncw, radius, p.k, r_lo, xmins, B, b0s, b1s, lvs, lane,
+                                         [&](int, uint32_t cw, uint32_t word) {
+                                             if ((cw & 31u) == lane) myword = word;
+                                             total += __popc(word);
+                                             if ((cw & 31u) == 31u || cw + 1u == p.ncw) {
+                                                 const uint32_t w0 = cw & ~31u;
+                                                 if (lane <= (cw & 31u))
+                                                     p.sdr[static_cast<size_t>(gin) * p.ncw + w0 + lane] = myword;
+                                             }
+                                         });
                 if (lane == 0) p.counts[gin] = total;
                 continue;
             }
             // local inhibition, uniform boost: bit-sliced window comparator (sp_select.cuh)
             const uint32_t nb = raw_bits(p.S);
-            uint32_t* planes = reinterpret_cast<uint32_t*>(region) + wi * 640u;  // [ncw <= 64][nb <= 10]
+            uint32_t* planes = reinterpret_cast<uint32_t*>(slotted ? wslot : region + wi * 2560u);  // [ncw <= 64][nb <= 10]
             build_raw_planes(row, planes, p.ncw, nb, r_lo, 0u, 1u, lane);
             __syncwarp();
             uint32_t total = 0, myword = 0;

@@ -146,78 +146,112 @@ __device__ __forceinline__ uint32_t wm_rank2(const uint2* lvl, uint32_t p) {
     return e.y + __popc(e.x & ((1u << (p & 31u)) - 1u));
 }
 
-template <typename RowT, typename Emit>
-__device__ __forceinline__ void local_uniform_wavelet(const RowT* row, uint32_t C, uint32_t C32, uint32_t ncw,
-                                                      uint32_t radius, uint32_t k, uint32_t r_lo, uint32_t xmin,
-                                                      uint32_t B, uint8_t* buf0, uint8_t* buf1, uint2* lv,
-                                                      uint32_t lane, Emit emit) {
+// NI inputs of one warp at once (NI = 1 or 2; independent builds and descents interleave, so
+// the latency of one input's chains hides behind the other's).  Input i: row[i], xmin[i];
+// scratch buf0[i], buf1[i] [C32] bytes and lv[i] [B][ncw + 2] uint2; B = the largest of
+// the inputs' level counts (extra top levels of the other input are all-zero partitions).
+// emit(i, cw, word) gets input i's SDR words in order (warp-uniform).
+template <int NI, typename RowT, typename Emit>
+__device__ __forceinline__ void local_uniform_wavelet(const RowT* const* row, uint32_t C, uint32_t C32, uint32_t ncw,
+                                                      uint32_t radius, uint32_t k, uint32_t r_lo,
+                                                      const uint32_t* xmin, uint32_t B, uint8_t* const* buf0,
+                                                      uint8_t* const* buf1, uint2* const* lv, uint32_t lane,
+                                                      Emit emit) {
     const uint32_t stride = ncw + 2u;
-    auto xval = [&](uint32_t c) -> uint32_t {
-        const uint32_t x = c < C ? static_cast<uint32_t>(row[c]) : 0u;
-        return x >= r_lo ? x - xmin + 1u : 0u;
+    auto xval = [&](int i, uint32_t c) -> uint32_t {
+        const uint32_t x = c < C ? static_cast<uint32_t>(row[i][c]) : 0u;
+        return x >= r_lo ? x - xmin[i] + 1u : 0u;
     };
-    for (uint32_t i = lane; i < C32; i += 32u) buf0[i] = static_cast<uint8_t>(xval(i));
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+        for (uint32_t c = lane; c < C32; c += 32u) buf0[i][c] = static_cast<uint8_t>(xval(i, c));
     __syncwarp();
-    uint8_t* src = buf0;
-    uint8_t* dst = buf1;
+    uint8_t* src[NI];
+    uint8_t* dst[NI];
+#pragma unroll
+    for (int i = 0; i < NI; ++i) src[i] = buf0[i], dst[i] = buf1[i];
     for (int l = static_cast<int>(B) - 1; l >= 0; --l) {
-        uint2* lvl = lv + l * stride;
-        uint32_t ones = 0;
-#pragma unroll 8
+        uint32_t ones[NI];
+#pragma unroll
+        for (int i = 0; i < NI; ++i) ones[i] = 0u;
+#pragma unroll 4
         for (uint32_t j = 0; j < ncw; ++j) {
-            const uint32_t w = __ballot_sync(0xffffffffu, (src[j * 32u + lane] >> l) & 1u);
-            if (lane == 0) lvl[j] = make_uint2(w, ones);
-            ones += __popc(w);
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const uint32_t w = __ballot_sync(0xffffffffu, (src[i][j * 32u + lane] >> l) & 1u);
+                if (lane == 0) lv[i][l * stride + j] = make_uint2(w, ones[i]);
+                ones[i] += __popc(w);
+            }
         }
-        const uint32_t Z = C32 - ones;
-        if (lane == 0) lvl[ncw] = make_uint2(0u, ones), lvl[ncw + 1u] = make_uint2(0u, Z);
+        uint32_t Z[NI];
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            Z[i] = C32 - ones[i];
+            if (lane == 0) lv[i][l * stride + ncw] = make_uint2(0u, ones[i]), lv[i][l * stride + ncw + 1u] = make_uint2(0u, Z[i]);
+        }
         __syncwarp();
-#pragma unroll 8
+#pragma unroll 4
         for (uint32_t j = 0; j < ncw; ++j) {
-            const uint32_t i = j * 32u + lane;
-            const uint32_t v = src[i];
-            const uint2 e = lvl[j];
-            const uint32_t r = e.y + __popc(e.x & ((1u << lane) - 1u));
-            dst[((v >> l) & 1u) ? Z + r : i - r] = static_cast<uint8_t>(v);
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const uint32_t c = j * 32u + lane;
+                const uint32_t v = src[i][c];
+                const uint2 e = lv[i][l * stride + j];
+                const uint32_t r = e.y + __popc(e.x & ((1u << lane) - 1u));
+                dst[i][((v >> l) & 1u) ? Z[i] + r : c - r] = static_cast<uint8_t>(v);
+            }
         }
         __syncwarp();
-        uint8_t* t = src;
-        src = dst;
-        dst = t;
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            uint8_t* t = src[i];
+            src[i] = dst[i];
+            dst[i] = t;
+        }
     }
     const int R = static_cast<int>(radius), Cn = static_cast<int>(C);
-    // beats of NQ columns per lane (independent descents interleave):
+    // beats of NQ columns per lane and input (independent descents interleave):
     //   greater + equal before c = (hi - lo) - less - (b - a) + (m - a)
-    constexpr int NQ = 4;
+    constexpr int NQ = NI == 1 ? 4 : 2;
     for (uint32_t cw0 = 0; cw0 < ncw; cw0 += NQ) {
-        uint32_t x[NQ], a[NQ], m[NQ], b[NQ], lo[NQ], hi[NQ], less[NQ];
+        uint32_t x[NI][NQ], a[NI][NQ], m[NI][NQ], b[NI][NQ], lo[NQ], hi[NQ], less[NI][NQ];
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
             const uint32_t c = (cw0 + q) * 32u + lane;
-            x[q] = cw0 + q < ncw ? xval(c) : 0u;
             lo[q] = static_cast<uint32_t>(max(0, static_cast<int>(c) - R));
             hi[q] = static_cast<uint32_t>(min(Cn - 1, static_cast<int>(c) + R)) + 1u;
-            a[q] = lo[q], m[q] = c, b[q] = hi[q], less[q] = 0u;
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                x[i][q] = cw0 + q < ncw ? xval(i, c) : 0u;
+                a[i][q] = lo[q], m[i][q] = c, b[i][q] = hi[q], less[i][q] = 0u;
+            }
         }
         for (int l = static_cast<int>(B) - 1; l >= 0; --l) {
-            const uint2* lvl = lv + l * stride;
-            const uint32_t Z = lvl[ncw + 1u].y;
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                const uint32_t ra = wm_rank2(lvl, a[q]), rm = wm_rank2(lvl, m[q]), rb = wm_rank2(lvl, b[q]);
-                if ((x[q] >> l) & 1u) {
-                    less[q] += (b[q] - a[q]) - (rb - ra);
-                    a[q] = Z + ra, m[q] = Z + rm, b[q] = Z + rb;
-                } else {
-                    a[q] -= ra, m[q] -= rm, b[q] -= rb;
+            for (int i = 0; i < NI; ++i) {
+                const uint2* lvl = lv[i] + l * stride;
+                const uint32_t Z = lvl[ncw + 1u].y;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const uint32_t ra = wm_rank2(lvl, a[i][q]), rm = wm_rank2(lvl, m[i][q]),
+                                   rb = wm_rank2(lvl, b[i][q]);
+                    if ((x[i][q] >> l) & 1u) {
+                        less[i][q] += (b[i][q] - a[i][q]) - (rb - ra);
+                        a[i][q] = Z + ra, m[i][q] = Z + rm, b[i][q] = Z + rb;
+                    } else {
+                        a[i][q] -= ra, m[i][q] -= rm, b[i][q] -= rb;
+                    }
                 }
             }
         }
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
             if (cw0 + q >= ncw) break;
-            const uint32_t beats = ((hi[q] - lo[q]) - less[q] - (b[q] - a[q])) + (m[q] - a[q]);
-            emit(cw0 + q, __ballot_sync(0xffffffffu, x[q] > 0u && beats < k));
+#pragma unroll
+            for (int i = 0; i < NI; ++i) {
+                const uint32_t beats = ((hi[q] - lo[q]) - less[i][q] - (b[i][q] - a[i][q])) + (m[i][q] - a[i][q]);
+                emit(i, cw0 + q, __ballot_sync(0xffffffffu, x[i][q] > 0u && beats < k));
+            }
         }
     }
     __syncwarp();
