@@ -518,3 +518,25 @@ def test_extreme_sizes(case):
     assert np.array_equal(sp.get_state()[1].view(np.uint32), ora.perm.view(np.uint32))
     want2 = [ora.step(x, False) for x in O.encode(frames, cfg)]
     check_results(want2, *run_gpu(sp, frames))
+
+
+def test_local_uniform_mixed_level_counts():
+    """Local inhibition, uniform boost, batched kernel: inputs whose eligible raw counts span
+    more than 255 values (> 8 wavelet levels: the comparator fallback) interleaved with narrow
+    ones (the paired wavelet) in the same CTA; every warp keeps to its own scratch slot."""
+    cfg = ocfg(input_width=64, input_height=48, num_columns=1024, synapses_per_column=512,
+               min_overlap=2, winners_set_size=20, inhibition_radius=100)
+    idx, perm, _ = O.init_pools(cfg)
+    perm = perm.copy()
+    perm[512:, 6:] = np.float32(0.0)  # columns 512.. keep 6 connected synapses: raw <= 6
+    state = (idx, perm, np.ones(cfg.num_columns, np.float32))
+    dense = sp_inputs.frames(5, 0, 24, 48, 64, rho=0.7)    # raw up to ~360 on columns < 512
+    sparse = sp_inputs.frames(6, 0, 24, 48, 64, rho=0.1)   # raw <= ~60
+    frames = np.empty((48, 48, 64), np.uint8)
+    frames[0::2], frames[1::2] = dense, sparse
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = [ora.step(x, False) for x in O.encode(frames, cfg)]
+    spread = [int(r.raw[r.raw >= 2].max() - r.raw[r.raw >= 2].min()) for r in results]
+    assert max(spread) >= 256 and min(spread) < 128
+    sp = make_sp(cfg, state, P.SP_PATH_BATCHED)
+    check_results(results, *run_gpu(sp, frames))
