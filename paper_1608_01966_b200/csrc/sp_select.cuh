@@ -1043,17 +1043,14 @@ __device__ __forceinline__ void global_uniform_threshold2(const RowT* ra_row, co
     }
     auto count_ge2 = [&](uint32_t xa, uint32_t xb, uint32_t& na, uint32_t& nb) {
         const __half2 hxa = __half2half2(__uint2half_rn(xa)), hxb = __half2half2(__uint2half_rn(xb));
-        __half2 a0 = __float2half2_rn(0.0f), a1 = a0, b0 = a0, b1 = a0;
+        __half2 va[NH], vb[NH];
 #pragma unroll
-        for (int t = 0; t < NH; t += 2) {
-            a0 = __hadd2(a0, __hge2(ha[t], hxa));
-            b0 = __hadd2(b0, __hge2(hb[t], hxb));
-            if (t + 1 < NH) {
-                a1 = __hadd2(a1, __hge2(ha[t + 1], hxa));
-                b1 = __hadd2(b1, __hge2(hb[t + 1], hxb));
-            }
-        }
-        const __half2 sa = __hadd2(a0, a1), sb = __hadd2(b0, b1);
+        for (int t = 0; t < NH; ++t) va[t] = __hge2(ha[t], hxa), vb[t] = __hge2(hb[t], hxb);
+#pragma unroll
+        for (int d = 1; d < NH; d <<= 1)  // pairwise tree: log2(NH) dependent adds, not NH/2
+#pragma unroll
+            for (int t = 0; t + d < NH; t += 2 * d) va[t] = __hadd2(va[t], va[t + d]), vb[t] = __hadd2(vb[t], vb[t + d]);
+        const __half2 sa = va[0], sb = vb[0];
         na = __reduce_add_sync(0xffffffffu, static_cast<uint32_t>(__low2float(sa) + __high2float(sa)));
         nb = __reduce_add_sync(0xffffffffu, static_cast<uint32_t>(__low2float(sb) + __high2float(sb)));
     };
