@@ -275,7 +275,20 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
     const uint32_t nbN = p.keyBits - L;             // significant bits of N
     const uint32_t sh = nbN > 16u ? nbN - 16u : 0u;  // coarse key u = N >> sh has <= 16 bits
     uint64_t* tie_list = reinterpret_cast<uint64_t*>(region) + wi * 64u;  // X window is idle now
-    for (uint32_t f = rank + K * wi; f < gs; f += K * NW) {
+    // local inhibition with a uniform boost: per-warp wavelet slots (sized for 8 levels; below).
+    // When 16 slots fit neither in the windows nor in `big` (C32 = 2048: the raw counts fill the
+    // ring), only the warps whose slots fit in `big` take inputs ("narrow"), so every input
+    // still gets the O(C log range) wavelet instead of the O(C r) comparator.
+    const uint32_t wbytes = (2u * p.C32 + 8u * 8u * (p.ncw + 2u) + 127u) & ~127u;
+    const uint32_t slot2 = max(2u * wbytes, 2560u), slot1 = max(wbytes, 2560u);
+    uint32_t nwork = NW;
+    bool narrow = false;
+    if (radius > 0 && p.uniform_bc && slot1 * NW > p.region_bytes && slot2 * NW > big_bytes &&
+        slot1 * NW > big_bytes && slot1 * (NW / 2u) <= big_bytes) {
+        nwork = big_bytes / slot1;
+        narrow = true;
+    }
+    for (uint32_t f = rank + K * wi; wi < nwork && f < gs; f += K * nwork) {
         uint16_t* row = rawbuf + f * p.C32;
         if (K > 1) {
             for (uint32_t c = lane; c < p.C32; c += 32u) {
@@ -351,11 +364,9 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             // depend on their inputs' ranges; a warp's comparator fallback uses its own slot too.
             // With room in the idle ring + windows (`big`), a slot holds two wavelets and the warp
             // runs its two inputs together.
-            const uint32_t wbytes = (2u * p.C32 + 8u * 8u * (p.ncw + 2u) + 127u) & ~127u;
-            const uint32_t slot2 = max(2u * wbytes, 2560u), slot1 = max(wbytes, 2560u);
-            const bool pairs = K == 1u && !p.raw_out && slot2 * NW <= big_bytes;
-            const bool slotted = pairs || slot1 * NW <= p.region_bytes;
-            uint8_t* wslot = pairs ? big + wi * slot2 : region + wi * slot1;
+            const bool pairs = !narrow && K == 1u && !p.raw_out && slot2 * NW <= big_bytes;
+            const bool slotted = pairs || narrow || slot1 * NW <= p.region_bytes;
+            uint8_t* wslot = pairs ? big + wi * slot2 : narrow ? big + wi * slot1 : region + wi * slot1;
             const uint32_t f2 = f + K * NW;
             if (pairs && f2 < gs && B <= 8u) {
                 const uint16_t* row2 = rawbuf + f2 * p.C32;
@@ -752,7 +763,7 @@ __global__ void __launch_bounds__(NT, 1)
 
     // idle shared memory behind the raw counts: the rest of the ring and the X windows
     const uint32_t raw_bytes = (32u * p.C32 * 2u + 127u) & ~127u;
-    const uint32_t big_bytes = NST * SB > raw_bytes ? NST * SB - raw_bytes + p.region_bytes : 0u;
+    const uint32_t big_bytes = NST * SB >= raw_bytes ? NST * SB - raw_bytes + p.region_bytes : 0u;
     batched_topk<CPT, NW>(p, rawbuf, region, smem + raw_bytes, big_bytes, s_bc, in0, gs, rank, K, wi, lane);
     if (K > 1) cluster.sync();  // peers may still read this CTA's partial counts
     if (trace) {
