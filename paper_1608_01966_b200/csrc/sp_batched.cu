@@ -445,7 +445,7 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             uint8_t* base = big + wi * gwb;
             uint16_t* b0 = reinterpret_cast<uint16_t*>(base);
             uint2* lv = reinterpret_cast<uint2*>(base + 4u * p.C32);
-            const CoarseMap cm = coarse_map_warp(row, s_bc, theta, 0u, p.ncw, lane);
+            const CoarseMap cm = coarse_map_warp(row, s_bc, theta, 0u, p.ncw, lane, p.wm_umax);
             uint32_t total = 0, myword = 0;
             local_general_wavelet(row, s_bc, p.C, p.C32, p.ncw, radius, p.k, theta, L, cm, b0, b0 + p.C32, lv,
                                   lane, [&](uint32_t cw, uint32_t word) {

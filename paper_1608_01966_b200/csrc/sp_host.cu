@@ -357,6 +357,8 @@ struct sp_handle {
     // (crossover measured at r ~ 80-100 for C = 1024: scripts/local_general_timing.py)
     uint32_t wm_min_radius = 96;
     uint32_t wm_min_radius_pi = 256;  // the same for the per-input k_inhibit (CTA wavelet)
+    uint32_t wm_umax = 4094u;         // per-warp wavelet coarse keys: u - 1 <= wm_umax (12 levels;
+                                      // 15 bits: 0.614 vs 0.603 ms at r 506, more lossy ties fixed)
     uint32_t learn_Q = 0, learn_smem = 0;  // cluster learning: CTAs per cluster (0 = not eligible)
     bool learn_dbl = false;                 // cluster learning: double-buffered bit-planes
     bool last_learn_cluster = false;
@@ -698,6 +700,7 @@ sp_status launch_batched_path(sp_handle* h, const uint8_t* frames, const uint32_
     p.boosted_out = rec ? h->d_boosted_rec + static_cast<size_t>(row0) * g.C : nullptr;
     p.radius_dev = h->d_radius;
     p.wm_min_radius = h->wm_min_radius;
+    p.wm_umax = h->wm_umax;
     if (!g.whole) {
         p.patch_w = g.pw;
         p.patch_h = g.ph;
@@ -1094,6 +1097,7 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
     if (const char* et = std::getenv("SP_THREADS")) h->batched_threads = std::atoi(et) == 1024 ? 1024u : 512u;
     if (const char* ew = std::getenv("SP_WM_MIN_RADIUS"))
         h->wm_min_radius = h->wm_min_radius_pi = static_cast<uint32_t>(std::atoi(ew));
+    if (const char* eu = std::getenv("SP_WM_UMAX")) h->wm_umax = static_cast<uint32_t>(std::atoi(eu));  // experiments
     h->Wn = (g.nbits + 31u) / 32u;
     h->sub_inputs = std::max<uint32_t>(sp::kPerInputChunk, g.P);
     const size_t cs = static_cast<size_t>(g.C) * g.S;

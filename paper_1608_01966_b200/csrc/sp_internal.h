@@ -76,6 +76,7 @@ struct alignas(64) BatchedParams {
     const uint32_t* radius_dev;  // nullable: radius in force (full learning adapts it), else `radius`
     uint32_t wm_min_radius;    // per-column boosts: wavelet top-k from this radius on (else comparator)
     uint32_t packed;           // frames are bit-planes uint32[inputs][Wn4] (sp_compute_packed)
+    uint32_t wm_umax;          // per-column-boost wavelet: largest coarse key - 1 (levels = its bits)
 };
 
 // Full learning (NEXT-1; S:119(b-e); DESIGN R17-R21): device state and constants.

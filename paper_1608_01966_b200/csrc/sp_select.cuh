@@ -345,14 +345,15 @@ struct CoarseMap {
     uint32_t sh;   // right shift of N - nlo, so that u - 1 < 2^15
 };
 
-__device__ __forceinline__ CoarseMap coarse_map(uint64_t nmin, uint64_t nmax) {
+// umax_lim: largest u - 1 (32766: 15-bit keys; the per-warp wavelet may ask for fewer levels)
+__device__ __forceinline__ CoarseMap coarse_map(uint64_t nmin, uint64_t nmax, uint32_t umax_lim = 32766u) {
     CoarseMap m{0ull, 0u};
     if (nmin > nmax) return m;  // no eligible column
     // nlo aligned to 2^sh: then "lossless" is N % 2^sh == 0, which holds for every column with a
     // boost of 1 (N = raw * 2^23) whenever sh <= 23, so equal-N ties stay index ties
     for (;; ++m.sh) {
         m.nlo = nmin & ~((1ull << m.sh) - 1ull);
-        if (((nmax - m.nlo) >> m.sh) <= 32766ull) break;
+        if (((nmax - m.nlo) >> m.sh) <= umax_lim) break;
     }
     return m;
 }
@@ -386,7 +387,7 @@ __device__ __forceinline__ void minmax64_warp(uint64_t& mn, uint64_t& mx) {
 // eligible-N range of words [w0, w1) by one warp (all lanes get the result)
 template <typename RowT>
 __device__ __forceinline__ CoarseMap coarse_map_warp(const RowT* row, const uint32_t* bc, uint32_t theta, uint32_t w0,
-                                                     uint32_t w1, uint32_t lane) {
+                                                     uint32_t w1, uint32_t lane, uint32_t umax_lim = 32766u) {
     uint64_t mn = ~0ull, mx = 0ull;
     for (uint32_t cw = w0; cw < w1; ++cw) {
         const uint32_t c = cw * 32u + lane;
@@ -394,7 +395,7 @@ __device__ __forceinline__ CoarseMap coarse_map_warp(const RowT* row, const uint
         if (N) mn = N < mn ? N : mn, mx = N > mx ? N : mx;
     }
     minmax64_warp(mn, mx);
-    return coarse_map(mn, mx);
+    return coarse_map(mn, mx, umax_lim);
 }
 
 // the same by the threads [0, nthr) of a CTA; s_mm[2] is shared scratch.  Contains barriers.

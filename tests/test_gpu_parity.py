@@ -540,3 +540,23 @@ def test_local_uniform_mixed_level_counts():
     assert max(spread) >= 256 and min(spread) < 128
     sp = make_sp(cfg, state, P.SP_PATH_BATCHED)
     check_results(results, *run_gpu(sp, frames))
+
+
+@pytest.mark.parametrize("umax", [62, 4094])
+@pytest.mark.parametrize("boost_mode", ["seeded", "near1"])
+def test_local_general_wavelet_coarse_key_width(umax, boost_mode, monkeypatch):
+    """The per-warp wavelet over coarse keys of a given width (SP_WM_UMAX: u - 1 <= umax); a
+    6-bit map makes most columns tie in u, so nearly every decision goes through the exact
+    re-decision of lossy ties from the bottom-level positions."""
+    monkeypatch.setenv("SP_WM_MIN_RADIUS", "0")
+    monkeypatch.setenv("SP_WM_UMAX", str(umax))
+    cfg = ocfg(input_width=96, input_height=64, num_columns=1000, synapses_per_column=64,
+               min_overlap=2, winners_set_size=20, inhibition_radius=300)
+    idx, perm, boost = perturbed_state(cfg)
+    if boost_mode == "near1":
+        boost = near1_boosts(cfg.num_columns)
+    state = (idx, perm, boost)
+    frames = sp_inputs.frames(79, 0, 45, cfg.input_height, cfg.input_width, rho=0.5)
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = [ora.step(x, False) for x in O.encode(frames, cfg)]
+    check_results(results, *run_gpu(make_sp(cfg, state, P.SP_PATH_BATCHED), frames))
