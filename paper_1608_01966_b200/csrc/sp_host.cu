@@ -357,8 +357,9 @@ struct sp_handle {
     // (crossover measured at r ~ 80-100 for C = 1024: scripts/local_general_timing.py)
     uint32_t wm_min_radius = 96;
     uint32_t wm_min_radius_pi = 256;  // the same for the per-input k_inhibit (CTA wavelet)
-    uint32_t wm_umax = 4094u;         // per-warp wavelet coarse keys: u - 1 <= wm_umax (12 levels;
-                                      // 15 bits: 0.614 vs 0.603 ms at r 506, more lossy ties fixed)
+    uint32_t wm_umax = 32766u;        // per-warp wavelet coarse keys: u - 1 <= wm_umax (15 levels;
+                                      // 12 bits: 0.603 vs 0.614 ms with seeded boosts in [1, 2] but
+                                      // 0.697 vs 0.665 ms with full-learning boosts near 1)
     uint32_t learn_Q = 0, learn_smem = 0;  // cluster learning: CTAs per cluster (0 = not eligible)
     bool learn_dbl = false;                 // cluster learning: double-buffered bit-planes
     bool last_learn_cluster = false;
