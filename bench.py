@@ -48,9 +48,11 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--frames", type=int, default=4096, help="frames per GPU (weak) or total (--strong)")
     ap.add_argument("--strong", action="store_true", help="fixed total batch split over the GPUs")
-    ap.add_argument("--learn-frames", type=int, default=256)
+    ap.add_argument("--learn-frames", type=int, default=1004,
+                    help="learning stream length (4 warm-up + 1000 timed = config 2's 1000 frames)")
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=16.0,
+                    help="oracle timing budget: half on 1 process, half on a Pool of every core")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-packed", action="store_true", help="skip the bit-plane input leg (P:502)")
     ap.add_argument("--no-cpu", action="store_true")
@@ -59,7 +61,10 @@ def parse():
     ap.add_argument("--encoder-frames", type=int, default=2048)
     ap.add_argument("--overlap-gather", action="store_true",
                     help="N > 1: all-gather of step i on NCCL's stream while step i+1 computes "
-                         "(SURVEY 8(e) streamed mode; double-buffered SDR tensors)")
+                         "(SURVEY 8(e) streamed mode; double-buffered SDR tensors).  At N = 1 a "
+                         "one-rank NCCL group runs the same path (the 'fake shard' mode)")
+    ap.add_argument("--no-strong-shards", action="store_true",
+                    help="skip timing the strong-scaling shards (F/2, F/4, F/8 frames) on this GPU")
     return ap.parse_args()
 
 
@@ -150,11 +155,60 @@ def oracle_cfg():
                           seed=SEED_STATE)
 
 
-def time_oracle(seconds: float, first_frame: int = 0, chunk: int = 4):
-    """Oracle inference on consecutive frames of the inference stream until ~seconds of CPU work."""
+def host_cpu():
+    """CPU model and the cores this process may run on (SURVEY 8(d) "Oracle timing")."""
+    model = "unknown"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, len(os.sched_getaffinity(0))
+
+
+_POOL_STATE = None  # (cfg, state) inherited by forked oracle workers
+
+
+def _oracle_worker(args):
+    """One forked worker: regenerates its frames (untimed), waits at the barrier, then times the
+    oracle on them.  Frames are independent at inference, so workers split the stream."""
+    first, count, barrier = args
     import oracle as O
     import sp_inputs
-    ora = O.SpatialPoolerOracle(oracle_cfg())
+    cfg, state = _POOL_STATE
+    ora = O.SpatialPoolerOracle(cfg, state)
+    frames = sp_inputs.frames(SEED_INFER, first, count, H, W, rho=0.5)
+    barrier.wait()
+    t0 = time.time()
+    ora.compute(frames, learning=False)
+    return count, t0, time.time()
+
+
+def time_oracle_pool(state, frames_per_worker: int, workers: int, first_frame: int = 0):
+    """The oracle (as it stands) on ``workers`` forked processes, each on its own consecutive
+    frames of the inference stream; throughput = all frames / (last end - first start)."""
+    import multiprocessing as mp
+    global _POOL_STATE
+    _POOL_STATE = (oracle_cfg(), state)
+    ctx = mp.get_context("fork")
+    with ctx.Manager() as man:
+        barrier = man.Barrier(workers)
+        with ctx.Pool(workers) as pool:
+            jobs = [(first_frame + w * frames_per_worker, frames_per_worker, barrier) for w in range(workers)]
+            res = pool.map(_oracle_worker, jobs, chunksize=1)
+    done = sum(r[0] for r in res)
+    wall = max(r[2] for r in res) - min(r[1] for r in res)
+    return done, wall
+
+
+def time_oracle(seconds: float, state=None, first_frame: int = 0, chunk: int = 4):
+    """Oracle inference (1 process) on consecutive frames of the inference stream until ~seconds
+    of CPU work; ``state`` = (idx, perm, boost) of the learned SP (None: the oracle's own init)."""
+    import oracle as O
+    import sp_inputs
+    ora = O.SpatialPoolerOracle(oracle_cfg(), state)
     done, busy, f = 0, 0.0, first_frame
     while busy < seconds or done == 0:
         frames = sp_inputs.frames(SEED_INFER, f, chunk, H, W, rho=0.5)
@@ -166,29 +220,59 @@ def time_oracle(seconds: float, first_frame: int = 0, chunk: int = 4):
     return done, busy
 
 
+def cpu_baseline(seconds: float, state, state_note: str):
+    """cpu_baseline object: the oracle at 1 process and on every usable core (a Pool over frame
+    chunks), with the CPU model and len(os.sched_getaffinity(0))."""
+    model, ncores = host_cpu()
+    done1, busy1 = time_oracle(seconds / 2, state)
+    rate1 = done1 / busy1
+    workers = max(1, min(ncores, 128))
+    per = max(2, int(rate1 * seconds / 2))  # ~seconds/2 of work per worker at the 1-core rate
+    try:
+        doneN, wallN = time_oracle_pool(state, per, workers)
+        rateN = doneN / wallN
+    except Exception as e:  # pragma: no cover - depends on the host
+        doneN, wallN, rateN = 0, 0.0, None
+        workers = 1
+        state_note += f"; pool failed: {e!r}"
+    best = rateN if rateN is not None and rateN > rate1 else rate1
+    return {"value": best, "unit": UNIT, "cores": workers if best is rateN else 1, "kind": "oracle",
+            "cpu_model": model, "sched_getaffinity": ncores,
+            "one_process": {"value": rate1, "frames": done1, "seconds": round(busy1, 2)},
+            "pool": {"value": rateN, "processes": workers, "frames": doneN, "seconds": round(wallN, 2)},
+            "sample": f"config-4 inference stream (NumPy oracle as it stands, {state_note}): "
+                      f"{done1} frames on 1 process ({busy1:.1f} s), then {doneN} frames on a fork Pool of "
+                      f"{workers} processes ({wallN:.1f} s wall, frames split in consecutive chunks)"}
+
+
 def reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    per_step = 2  # frames per step: a bounded sample of the workload
     import oracle as O
-    import sp_inputs
-    ora = O.SpatialPoolerOracle(oracle_cfg())
-    frames = sp_inputs.frames(SEED_INFER, 0, per_step * (args.warmup + args.steps), H, W, rho=0.5)
-    for i in range(args.warmup):
-        ora.compute(frames[i * per_step:(i + 1) * per_step], learning=False)
-    t0 = time.perf_counter()
-    for i in range(args.warmup, args.warmup + args.steps):
-        ora.compute(frames[i * per_step:(i + 1) * per_step], learning=False)
-    el = time.perf_counter() - t0
-    value = per_step * args.steps / el
-    sample = f"{per_step} frames of the config-4 inference stream per step (oracle, NumPy, 1 process)"
+    model, ncores = host_cpu()
+    workers = max(1, min(ncores, 128))
+    per_worker = 2  # frames per worker per step: a bounded sample of the workload
+    per_step = per_worker * workers
+    state = O.init_pools(oracle_cfg())
+    steps = []
+    for i in range(args.warmup + args.steps):
+        done, wall = time_oracle_pool(state, per_worker, workers, first_frame=i * per_step)
+        steps.append((done, wall))
+    timed = steps[args.warmup:]
+    frames = sum(d for d, _ in timed)
+    el = sum(w for _, w in timed)
+    value = frames / el
+    sample = (f"{per_step} frames of the config-4 inference stream per step ({per_worker} per process on "
+              f"{workers} forked processes; NumPy oracle as it stands, SP from the oracle's own init -- "
+              f"inference cost does not depend on the learned state); CPU {model}")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "int64/f32 (NumPy)", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "frames_per_step": per_step, "host": "cpu"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "config": {"workload": WORKLOAD, "frames_per_step": per_step, "host": "cpu",
+                       "cpu_model": model, "sched_getaffinity": ncores},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "oracle",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -214,12 +298,22 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # one rank per GPU over NCCL; at N = 1 --overlap-gather runs a one-rank NCCL group, so the
+    # streamed all-gather path is exercised on a single GPU (SURVEY §4 "fake shard")
+    use_dist = world > 1 or args.overlap_gather
+    if use_dist:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=dev)
     from paper_1608_01966_b200 import dist as D
 
+    if args.strong and args.frames % world:
+        raise SystemExit(f"--strong needs --frames divisible by the world size ({args.frames} % {world})")
     F = args.frames // world if args.strong else args.frames
-    F0 = D.shard_range(args.frames, rank, world)[0] if args.strong else rank * F
+    F0 = rank * F  # contiguous shards by global frame index (= shard_range when F divides)
     sp = P.SpatialPooler(input_width=W, input_height=H, num_columns=C, synapses_per_column=S,
                          min_overlap=THETA, winners_set_size=K_WIN, inhibition_radius=0,
                          seed=SEED_STATE, device=local, max_inputs=max(F, args.learn_frames))
@@ -268,18 +362,19 @@ def main():
                                          "1000, max_boost 2, initial radius 80 (Tab. 2), adapted"}
             spf.close()
         del lf
-    if world > 1:
+    if use_dist:
         D.broadcast_state(sp, src=0, device=dev)
+    learned_state = sp.get_state() if rank == 0 else None
 
     # ---- inference frames of this rank (generated before the timed region) --------------
     frames = torch.empty((F, H, W), dtype=torch.uint8, device=dev)
     P.synth_frames(frames, F0, SEED_INFER, 0.5)
     words = sp.sdr_words
-    nbuf = 2 if (args.overlap_gather and world > 1) else 1
+    nbuf = 2 if args.overlap_gather else 1
     sdrs = [torch.empty((F, words), dtype=torch.int32, device=dev) for _ in range(nbuf)]
     cnts = [torch.empty((F,), dtype=torch.int32, device=dev) for _ in range(nbuf)]
     gath = [torch.empty((F * world, words), dtype=torch.int32, device=dev) for _ in range(nbuf)] \
-        if world > 1 else None
+        if use_dist else None
     sdr, counts = sdrs[0], cnts[0]
     works = []  # --overlap-gather: the all-gather of step i runs while step i+1 computes
 
@@ -293,7 +388,7 @@ def main():
         sp.compute_into(frames, sdrs[b], cnts[b], learn=False)
         if ev is not None:
             ev[1].record(stream)
-        if world > 1:
+        if use_dist:
             if nbuf > 1:
                 works.append(dist.all_gather_into_tensor(gath[b], sdrs[b], async_op=True))
             else:
@@ -478,8 +573,39 @@ def main():
                           "packed by sp_pack_frames outside the timed regions"}
         del planes, host_planes
 
+    # ---- strong-scaling readiness (B = 4096 total over G GPUs): the
+    # shard one GPU would own at G = 2, 4, 8, timed here; the implied ceiling on strong-scaling
+    # efficiency is T(F) / (G * T(F/G)) before any gather cost ----------------------------------
+    strong_shards = None
+    if not args.no_strong_shards and world == 1 and not args.strong:
+        strong_shards = {"frames_total": F, "shards": []}
+        for G in (2, 4, 8):
+            n = F // G
+            ssp = torch.empty((n, words), dtype=torch.int32, device=dev)
+            scn = torch.empty((n,), dtype=torch.int32, device=dev)
+            sub = frames[:n]
+            for _ in range(3):
+                sp.compute_into(sub, ssp, scn)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(args.steps, 10)
+            a.record(stream)
+            for _ in range(reps):
+                sp.compute_into(sub, ssp, scn)
+            b.record(stream)
+            torch.cuda.synchronize()
+            sms = a.elapsed_time(b) / reps
+            pl = sp.info()["plan"]
+            strong_shards["shards"].append({
+                "G": G, "frames": n, "ms": sms, "frames_per_s": n / sms * 1e3,
+                "implied_efficiency": (ms / args.steps) / (G * sms),
+                "plan": {k: pl[k] for k in ("groups", "cluster", "ctas")}})
+        strong_shards["note"] = ("per-GPU shard of a fixed 4096-frame batch timed alone on one GPU "
+                                 "(CUDA events, back to back); implied_efficiency = T(4096)/(G*T(4096/G)), "
+                                 "the compute-only ceiling before the SDR all-gather")
+
     if rank != 0:
-        if world > 1:
+        if use_dist:
             dist.destroy_process_group()
         return 0
 
@@ -495,10 +621,9 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu:
-        done, busy = time_oracle(args.cpu_seconds)
-        cpu = {"value": done / busy, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"{done} frames of the config-4 inference stream (NumPy oracle, 1 process, "
-                         f"untrained SP from the oracle's own init), {busy:.1f} s"}
+        note = ("the GPU arm's learned SP exported by sp_get_state" if args.learn_frames > 0
+                else "the SP at creation")
+        cpu = cpu_baseline(args.cpu_seconds, learned_state, note)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -515,9 +640,9 @@ def main():
             "hbm_frac": round(value / world * ALGO_BYTES_PER_FRAME / 1e9 / peak, 4),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "learn": learn, "histograms": histograms, "encoder": encoder,
-            "packed": packed}
+            "packed": packed, "strong_shards": strong_shards}
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
     return 0
 

@@ -36,19 +36,39 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compiles every csrc/*.cu to an object in parallel, then links libsp.so."""
     if not force and not needs_build():
         return LIB
-    cmd = [NVCC, *NVCC_FLAGS, "-o", LIB + ".tmp", *sources()]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared", "-cudart", "static")]
+    jobs = []
+    for src in sources():
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        jobs.append((src, [NVCC, *compile_flags, "-c", "-o", obj, src], obj))
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(lambda j: subprocess.run(j[1], capture_output=True, text=True), jobs))
+    log_lines = []
+    failed = False
+    for (src, cmd, _), res in zip(jobs, results):
+        log_lines.append(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+        failed |= res.returncode != 0
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+            "-Xcompiler", "-fPIC", "-o", LIB + ".tmp", *[j[2] for j in jobs]]
+    if not failed:
+        res = subprocess.run(link, capture_output=True, text=True)
+        log_lines.append(" ".join(link) + "\n" + res.stdout + res.stderr)
+        failed = res.returncode != 0
     log = os.path.join(HERE, "build.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError(f"nvcc failed ({res.returncode}); see {log}")
+        f.write("\n".join(log_lines))
+    if failed:
+        sys.stderr.write("\n".join(log_lines)[-20000:])
+        raise RuntimeError(f"nvcc failed; see {log}")
     os.replace(LIB + ".tmp", LIB)
     if verbose:
-        print(res.stderr)
+        print("\n".join(log_lines))
     return LIB
 
 

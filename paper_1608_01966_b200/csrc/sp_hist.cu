@@ -20,8 +20,8 @@ namespace {
 
 __global__ void __launch_bounds__(256) k_hist_count(const uint32_t* __restrict__ sdr, uint32_t ncw, uint32_t C,
                                                     const uint32_t* __restrict__ off, uint32_t* __restrict__ counts,
-                                                    float* __restrict__ hist) {
-    const uint32_t v = blockIdx.y;
+                                                    float* __restrict__ hist, uint32_t v0) {
+    const uint32_t v = v0 + blockIdx.y;  // videos beyond gridDim.y's 65535 go to further launches
     const uint32_t cw = blockIdx.x * 8u + (threadIdx.x >> 5);
     const uint32_t lane = threadIdx.x & 31u;
     if (cw >= ncw) return;
@@ -78,9 +78,14 @@ cudaError_t launch_histograms(const uint32_t* sdr, uint32_t ncw, uint32_t C, con
     nz = std::min<uint32_t>(nz, 65535u);
     cudaError_t e = cudaSuccess;
     if (nz > 1u && (e = cudaMemsetAsync(counts, 0, static_cast<size_t>(V) * C * 4u, s)) != cudaSuccess) return e;
-    k_hist_count<<<dim3(bx, V, nz), 256, 0, s>>>(sdr, ncw, C, off_dev, counts, hist);
-    *launches = (nz > 1u && hist) ? 2u : 1u;
-    e = cudaGetLastError();
+    *launches = 0;
+    for (uint32_t v0 = 0; v0 < V && e == cudaSuccess; v0 += 65535u) {  // gridDim.y <= 65535
+        k_hist_count<<<dim3(bx, std::min(V - v0, 65535u), nz), 256, 0, s>>>(sdr, ncw, C, off_dev, counts, hist,
+                                                                           v0);
+        ++*launches;
+        e = cudaGetLastError();
+    }
+    if (nz > 1u && hist) ++*launches;
     if (e != cudaSuccess || !hist || nz == 1u) return e;
     const size_t n = static_cast<size_t>(V) * C;
     k_hist_norm<<<static_cast<uint32_t>((n + 255u) / 256u), 256, 0, s>>>(counts, off_dev, C, V, hist);

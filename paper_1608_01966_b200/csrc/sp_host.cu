@@ -1098,7 +1098,10 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
     if (const char* et = std::getenv("SP_THREADS")) h->batched_threads = std::atoi(et) == 1024 ? 1024u : 512u;
     if (const char* ew = std::getenv("SP_WM_MIN_RADIUS"))
         h->wm_min_radius = h->wm_min_radius_pi = static_cast<uint32_t>(std::atoi(ew));
-    if (const char* eu = std::getenv("SP_WM_UMAX")) h->wm_umax = static_cast<uint32_t>(std::atoi(eu));  // experiments
+    if (const char* eu = std::getenv("SP_WM_UMAX")) {  // experiments; the per-warp wavelet scratch holds
+        const long u = std::atol(eu);                   // at most 15 levels + the lossy plane
+        h->wm_umax = static_cast<uint32_t>(std::min<long>(std::max<long>(u, 1), 32766));
+    }
     h->Wn = (g.nbits + 31u) / 32u;
     h->sub_inputs = std::max<uint32_t>(sp::kPerInputChunk, g.P);
     const size_t cs = static_cast<size_t>(g.C) * g.S;

@@ -39,12 +39,20 @@ def broadcast_arrays(arrays, src: int, device=None):
 
 
 def broadcast_state(sp, src: int = 0, device=None):
-    """Replicates the learned state of rank ``src``'s SpatialPooler to every rank."""
+    """Replicates the learned state of rank ``src``'s SpatialPooler to every rank.
+
+    Besides the synapses and boosts this carries the learning state (duty cycles and the
+    inhibition radius in force): with full learning the radius adapts (R21) and the
+    batched inference reads it, so a replica left at the configured radius would pick
+    different winners than one GPU does."""
     idx, perm, boost = sp.get_state()
-    idx, perm, boost = broadcast_arrays([idx, perm, boost], src, device)
+    adc, odc, radius, _ = sp.get_learning_state()
+    r = np.array([radius], dtype=np.int64)
+    idx, perm, boost, adc, odc, r = broadcast_arrays([idx, perm, boost, adc, odc, r], src, device)
     import torch.distributed as dist
     if dist.get_rank() != src:
         sp.set_state(idx, perm, boost)
+        sp.set_learning_state(adc, odc, int(r[0]))
     return idx, perm, boost
 
 

@@ -203,6 +203,37 @@ def _require(t, dtype, device, shape=None, name="tensor"):
         raise SpError(SP_E_SHAPE, f"{name} shape {tuple(t.shape)} != {tuple(shape)}")
 
 
+def _host_buffer(a, dtype, shape, name):
+    """Checks a host buffer (numpy array or CPU torch tensor) for a host-pointer entry point and
+    returns its address: the C ABI copies exactly the bytes the shape implies, so a short,
+    mistyped or strided buffer would be overrun silently (heap corruption) without this check."""
+    import torch
+    if isinstance(a, torch.Tensor):
+        if a.device.type != "cpu":
+            raise SpError(SP_E_SHAPE, f"{name} must be a host (CPU) buffer, got {a.device}")
+        tdt = {np.uint8: torch.uint8, np.uint32: (torch.uint32, torch.int32)}[dtype]
+        ok = a.dtype in tdt if isinstance(tdt, tuple) else a.dtype == tdt
+        if not ok:
+            raise SpError(SP_E_SHAPE, f"{name} dtype {a.dtype} is not {np.dtype(dtype).name}")
+        if not a.is_contiguous():
+            raise SpError(SP_E_SHAPE, f"{name} must be C-contiguous")
+        got, addr = tuple(a.shape), a.data_ptr()
+    elif isinstance(a, np.ndarray):
+        ok = a.dtype == dtype or (dtype is np.uint32 and a.dtype == np.int32)
+        if not ok:
+            raise SpError(SP_E_SHAPE, f"{name} dtype {a.dtype} is not {np.dtype(dtype).name}")
+        if not a.flags["C_CONTIGUOUS"]:
+            raise SpError(SP_E_SHAPE, f"{name} must be C-contiguous")
+        if name != "frames" and name != "planes" and not a.flags["WRITEABLE"]:
+            raise SpError(SP_E_SHAPE, f"{name} must be writeable")
+        got, addr = tuple(a.shape), a.ctypes.data
+    else:
+        raise SpError(SP_E_SHAPE, f"{name} must be a numpy array or a CPU torch.Tensor")
+    if got != tuple(shape):
+        raise SpError(SP_E_SHAPE, f"{name} shape {got} != {tuple(shape)}")
+    return addr
+
+
 def synth_frames(out, first_frame: int, seed: int, rho: float = 0.5, nonzero: str = "255",
                  stream=None):
     """Fills uint8 cuda tensor ``out[F, H, W]`` with frames of the seeded stream (bench/test)."""
@@ -392,18 +423,20 @@ class SpatialPooler:
 
     def compute_packed_host_into(self, planes, sdr, counts, stream=None):
         """End-to-end bit-plane inference with host buffers (numpy arrays or pinned torch CPU
-        tensors): planes uint32 [F, packed_words] -> sdr uint32 [n, words], counts uint32 [n]."""
+        tensors): planes uint32 [F, packed_words] -> sdr uint32 [n, words], counts uint32 [n]
+        (or None).  Shapes, dtypes and contiguity are checked here (SP_E_SHAPE)."""
         import torch
-
-        def ptr(a):
-            return a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data
-        F = planes.shape[0]
-        if tuple(planes.shape[1:]) != (self.packed_words,):
+        if getattr(planes, "ndim", 0) != 2:
             raise SpError(SP_E_SHAPE, f"planes must be [F, {self.packed_words}]")
-        _check(lib().sp_compute_packed_host(self._h, ctypes.c_void_p(ptr(planes)), F, ctypes.c_void_p(ptr(sdr)),
-                                            ctypes.c_void_p(ptr(counts)) if counts is not None else None,
+        F = int(planes.shape[0])
+        n = F * self.inputs_per_frame
+        pp = _host_buffer(planes, np.uint32, (F, self.packed_words), "planes")
+        sp_ = _host_buffer(sdr, np.uint32, (n, self.sdr_words), "sdr")
+        cp = _host_buffer(counts, np.uint32, (n,), "counts") if counts is not None else None
+        _check(lib().sp_compute_packed_host(self._h, ctypes.c_void_p(pp), F, ctypes.c_void_p(sp_),
+                                            ctypes.c_void_p(cp) if cp is not None else None,
                                             _stream_ptr(stream, torch.device("cuda", self.device))))
-        self.last_num_inputs = F * self.inputs_per_frame
+        self.last_num_inputs = n
 
     def winners(self, sdr=None, counts=None, stream=None):
         """SDRs of the last call: (uint32 [n, words] as int32 view, int32 [n]) cuda tensors."""
@@ -461,17 +494,22 @@ class SpatialPooler:
         return sdr, counts
 
     def compute_host_into(self, frames, sdr, counts, learn: bool = False, stream=None):
-        """Same with caller buffers (numpy arrays or pinned torch CPU tensors)."""
+        """Same with caller buffers (numpy arrays or pinned torch CPU tensors): frames uint8
+        [F, H, W] -> sdr uint32 [n, words], counts uint32 [n] (or None).  Shapes, dtypes and
+        contiguity are checked here (SP_E_SHAPE): the C ABI copies by the implied sizes."""
         import torch
-
-        def ptr(a):
-            return a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data
-        F = frames.shape[0]
-        _check(lib().sp_compute_host(self._h, ctypes.c_void_p(ptr(frames)), F, int(bool(learn)),
-                                     ctypes.c_void_p(ptr(sdr)),
-                                     ctypes.c_void_p(ptr(counts)) if counts is not None else None,
+        if getattr(frames, "ndim", 0) != 3:
+            raise SpError(SP_E_SHAPE, "frames must be [F, H, W] uint8")
+        F = int(frames.shape[0])
+        n = F * self.inputs_per_frame
+        fp = _host_buffer(frames, np.uint8, (F, *self.frame_shape), "frames")
+        sp_ = _host_buffer(sdr, np.uint32, (n, self.sdr_words), "sdr")
+        cp = _host_buffer(counts, np.uint32, (n,), "counts") if counts is not None else None
+        _check(lib().sp_compute_host(self._h, ctypes.c_void_p(fp), F, int(bool(learn)),
+                                     ctypes.c_void_p(sp_),
+                                     ctypes.c_void_p(cp) if cp is not None else None,
                                      _stream_ptr(stream, torch.device("cuda", self.device))))
-        self.last_num_inputs = F * self.inputs_per_frame
+        self.last_num_inputs = n
 
     # -- state ------------------------------------------------------------------------
     def get_state(self):
