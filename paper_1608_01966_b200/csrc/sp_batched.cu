@@ -299,14 +299,18 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             __syncwarp();
         }
         const uint32_t gin = in0 + f;
-        if (p.raw_out) {
+        // optional test outputs (SP_FLAG_RECORD_OVERLAPS); the paired branches below record
+        // their second input too, so recording does not change which selection code runs
+        auto record = [&](const uint16_t* rw, uint32_t g) {
+            if (!p.raw_out) return;
             for (uint32_t c = lane; c < p.C; c += 32u) {
-                const uint32_t r = row[c];
-                p.raw_out[static_cast<size_t>(gin) * p.C + c] = static_cast<uint16_t>(r);
-                p.boosted_out[static_cast<size_t>(gin) * p.C + c] =
+                const uint32_t r = rw[c];
+                p.raw_out[static_cast<size_t>(g) * p.C + c] = static_cast<uint16_t>(r);
+                p.boosted_out[static_cast<size_t>(g) * p.C + c] =
                     r >= theta ? __fmul_rn(static_cast<float>(r), p.boost[c]) : 0.0f;
             }
-        }
+        };
+        record(row, gin);
         if (radius == 0 && p.uniform_bc) {
             // Uniform boost: the key order is (raw desc, index asc), so the k-th largest key
             // is found from a histogram of the raw counts: with one boost
@@ -318,10 +322,11 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             // zeroed below r_lo; counts of raw >= x with HSET2/HADD2 (FMA pipe, no atomics)
             constexpr int NH = (CPT * NW + 1) / 2;
             const uint32_t f2 = f + K * NW;
-            if (CPT <= 2 && NW <= 16u && f2 < gs && K == 1u && !p.raw_out) {
+            if (CPT <= 2 && NW <= 16u && f2 < gs && K == 1u) {
                 // this warp's next input too: both searches and SDR loops interleaved
                 const uint16_t* row2 = rawbuf + f2 * p.C32;
                 const uint32_t gin2 = in0 + f2;
+                record(row2, gin2);
                 uint32_t rgt[2], rtie[2], need[2];
                 global_uniform_threshold2<NH>(row, row2, p.C32, p.S, p.k, r_lo, lane, rgt, rtie, need);
                 const uint32_t tot0 = uniform_sdr_words(row, p.ncw, rgt[0], rtie[0], need[0], lane,
@@ -364,7 +369,7 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             // depend on their inputs' ranges; a warp's comparator fallback uses its own slot too.
             // With room in the idle ring + windows (`big`), a slot holds two wavelets and the warp
             // runs its two inputs together.
-            const bool pairs = !narrow && K == 1u && !p.raw_out && slot2 * NW <= big_bytes;
+            const bool pairs = !narrow && K == 1u && slot2 * NW <= big_bytes;
             const bool slotted = pairs || narrow || slot1 * NW <= p.region_bytes;
             uint8_t* wslot = pairs ? big + wi * slot2 : narrow ? big + wi * slot1 : region + wi * slot1;
             const uint32_t f2 = f + K * NW;
@@ -374,6 +379,7 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
                 range_of(row2, xmn2, B2);
                 if (B2 <= 8u) {
                     const uint32_t gin2 = in0 + f2;
+                    record(row2, gin2);
                     const uint16_t* rows[2] = {row, row2};
                     const uint32_t xmins[2] = {xmn, xmn2};
                     uint8_t* b0s[2] = {wslot, wslot + wbytes};

@@ -357,6 +357,7 @@ struct sp_handle {
     // (crossover measured at r ~ 80-100 for C = 1024: scripts/local_general_timing.py)
     uint32_t wm_min_radius = 96;
     uint32_t wm_min_radius_pi = 256;  // the same for the per-input k_inhibit (CTA wavelet)
+    uint32_t force_groups = 0;        // SP_GROUPS (tests): batched groups per call, cluster size 1
     uint32_t wm_umax = 32766u;        // per-warp wavelet coarse keys: u - 1 <= wm_umax (15 levels;
                                       // 12 bits: 0.603 vs 0.614 ms with seeded boosts in [1, 2] but
                                       // 0.697 vs 0.665 ms with full-learning boosts near 1)
@@ -472,6 +473,10 @@ sp_plan_info make_plan(const sp_handle* h, uint32_t n, bool learn, const uint8_t
         uint32_t G = 0, K = 1;
         sp::plan_batched_grid(g, h->lay.nwin, n, h->sm_count, h->max_clusters[1] ? h->max_clusters : nullptr, &G,
                               &K);
+        if (h->force_groups) {  // test override: fewer, fuller groups (the paired top-k branches
+            G = std::max<uint32_t>((n + 31u) / 32u, std::min<uint32_t>(n, h->force_groups));  // need > NW
+            K = 1;                                                                 // inputs per group)
+        }
         pl.groups = G;
         pl.cluster = K;
         pl.ctas = G * K;
@@ -1094,6 +1099,8 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
                 h->grid_stages = st;
             }
     }
+    if (const char* eg = std::getenv("SP_GROUPS"))
+        h->force_groups = static_cast<uint32_t>(std::max(0, std::atoi(eg)));
     if (std::getenv("SP_TRACE")) cudaMalloc(&h->d_trace, 4096u * 6u * sizeof(uint64_t));
     if (const char* et = std::getenv("SP_THREADS")) h->batched_threads = std::atoi(et) == 1024 ? 1024u : 512u;
     if (const char* ew = std::getenv("SP_WM_MIN_RADIUS"))

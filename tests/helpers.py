@@ -42,3 +42,49 @@ def perturbed_state(cfg: O.OracleConfig, seed: int = 5, boost_seed: int = 7, boo
 
 def sdr_of(active):
     return O.sdr_words(active).view(np.int32)
+
+
+# --------------------------------------------------------------------------- #
+# oracle on many frames: a fork Pool over frame chunks (inference inputs are independent)
+# --------------------------------------------------------------------------- #
+_POOL = None
+
+
+def _pool_job(job):
+    first, count, stride = job
+    cfg, state, seed, rho = _POOL
+    ora = O.SpatialPoolerOracle(cfg, state)
+    out = []
+    for j in range(count):
+        f = first + j * stride
+        x = O.encode(sp_inputs.frames(seed, f, 1, cfg.input_height, cfg.input_width, rho=rho), cfg)
+        for xi in x:
+            r = ora.step(xi, False)
+            out.append((f, sdr_of(r.active), int(r.active.sum())))
+    return out
+
+
+def oracle_infer_frames(cfg, state, seed, frame_ids, rho=0.5, processes=None):
+    """Oracle inference on frames ``frame_ids`` of the seeded stream ``seed`` (regenerated on the
+    host from sp_inputs), split over a fork Pool: {frame: [(sdr int32 words, count) per input]}."""
+    import multiprocessing as mp
+    import os
+    global _POOL
+    _POOL = (cfg, state, seed, rho)
+    ids = list(frame_ids)
+    n = processes or max(1, min(len(os.sched_getaffinity(0)), 64))
+    chunks = [ids[i::n] for i in range(n)]
+    jobs = []
+    for ch in chunks:
+        if not ch:
+            continue
+        stride = ch[1] - ch[0] if len(ch) > 1 else 1
+        assert all(ch[i] == ch[0] + i * stride for i in range(len(ch)))
+        jobs.append((ch[0], len(ch), stride))
+    with mp.get_context("fork").Pool(len(jobs)) as pool:
+        parts = pool.map(_pool_job, jobs, chunksize=1)
+    res = {}
+    for part in parts:
+        for f, s, c in part:
+            res.setdefault(f, []).append((s, c))
+    return res

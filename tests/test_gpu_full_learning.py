@@ -220,3 +220,41 @@ def test_full_learning_many_columns_per_input_path():
     check_inputs(results, *run(sp, frames, True))
     check_state(sp, ora)
     assert ora.radius != 100
+
+
+HAND = {
+    # tests/test_oracle_full_learning.py::test_full_learning_radius_after_bump_hand_worked
+    "radius_after_bump": (dict(num_columns=4, synapses_per_column=8, min_overlap=2, winners_set_size=1,
+                               inhibition_radius=1, full_learning=True, duty_cycle_period=2),
+                          [[0, 1, 2, 3, 4, 5, 6, 63], [0, 9, 18, 27, 36, 45, 54, 63], list(range(20, 28)),
+                           [1, 10, 19, 28, 37, 46, 55, 62]], {2: 0.19}, list(range(8)) + [63]),
+    # ...::test_full_learning_hand_worked_bump_and_boost
+    "bump_and_boost": (dict(num_columns=4, synapses_per_column=8, min_overlap=4, winners_set_size=1,
+                            inhibition_radius=0, full_learning=True, duty_cycle_period=2, max_boost=2.0),
+                       [list(range(8 * c, 8 * c + 8)) for c in range(4)], {},
+                       list(range(0, 8)) + list(range(8, 14)) + [16, 17]),
+}
+
+
+@pytest.mark.parametrize("path", LEARN_PATHS)
+@pytest.mark.parametrize("case", sorted(HAND))
+def test_hand_worked_full_learning_cases(case, path):
+    """The oracle's hand-worked wiring pins (overlap duty from Alg. 1's non-zero overlap, bump
+    from the overlap duty, radius after the bump) through the CUDA path: 3 frames (the worked
+    frame, an all-zero frame, the worked frame again), every state array bit-exact."""
+    kw, idx, low, on = HAND[case]
+    cfg = ocfg(**kw)
+    idx = np.array(idx, np.int64)
+    perm = np.full(idx.shape, np.float32(0.21), np.float32)
+    for c, v in low.items():
+        perm[c] = np.float32(v)
+    state = (idx, perm, np.ones(cfg.num_columns, np.float32))
+    frames = np.zeros((3, 8, 8), np.uint8)
+    frames[0].reshape(-1)[on] = 255
+    frames[2] = frames[0]
+    ora = O.SpatialPoolerOracle(cfg, state)
+    want = ora.compute(frames, learning=True)
+    sp = make_sp(cfg, state, path)
+    check_inputs(want, *run(sp, frames, True))
+    check_path(sp, path)
+    check_state(sp, ora)

@@ -560,3 +560,82 @@ def test_local_general_wavelet_coarse_key_width(umax, boost_mode, monkeypatch):
     ora = O.SpatialPoolerOracle(cfg, state)
     results = [ora.step(x, False) for x in O.encode(frames, cfg)]
     check_results(results, *run_gpu(make_sp(cfg, state, P.SP_PATH_BATCHED), frames))
+
+
+# --------------------------------------------------------------------------- #
+# the timed selection branches: full groups, overlap recording on and off
+# --------------------------------------------------------------------------- #
+def run_gpu_sdr(sp, frames):
+    """winners only (recording off): (sdr int32 [n, words], counts int32 [n])"""
+    sp.compute(to_dev(frames))
+    sdr, counts = sp.winners()
+    torch.cuda.synchronize()
+    return sdr.cpu().numpy(), counts.cpu().numpy()
+
+
+def check_sdrs(results, sdr, counts):
+    for r, res in enumerate(results):
+        assert np.array_equal(sdr[r], sdr_of(res.active)), f"winners mismatch at input {r}"
+        assert counts[r] == res.active.sum(), f"count mismatch at input {r}"
+
+
+@pytest.mark.parametrize("record", [True, False])
+@pytest.mark.parametrize("boost_mode", ["seeded", "uniform1", "uniform1.5"])
+@pytest.mark.parametrize("kw", SMALL)
+def test_inference_parity_full_groups(kw, boost_mode, record, monkeypatch):
+    """45 inputs in 2 groups of 23/22 (SP_GROUPS=2): with 16 warps per CTA, warps 0..6 take two
+    inputs each, so the paired branches (global uniform: interleaved threshold searches;
+    local uniform: the two-input wavelet) run next to the single-input ones -- with and without
+    SP_FLAG_RECORD_OVERLAPS (recording must not change which selection code runs)."""
+    monkeypatch.setenv("SP_GROUPS", "2")
+    cfg = ocfg(**kw)
+    state = with_boost(perturbed_state(cfg), boost_mode)
+    frames = sp_inputs.frames(2002, 0, 45, cfg.input_height, cfg.input_width, rho=0.5, nonzero="random")
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = [ora.step(x, False) for x in O.encode(frames, cfg)]
+    sp = make_sp(cfg, state, P.SP_PATH_BATCHED, record=record)
+    if record:
+        check_results(results, *run_gpu(sp, frames))
+    else:
+        check_sdrs(results, *run_gpu_sdr(sp, frames))
+    pl = sp.info()["plan"]
+    assert pl["path"] == P.SP_PATH_BATCHED and pl["groups"] == 2 and pl["cluster"] == 1
+
+
+@pytest.mark.parametrize("record", [True, False])
+@pytest.mark.parametrize("radius", [0, 80, 506])
+@pytest.mark.parametrize("boost_mode", ["uniform1", "seeded"])
+def test_full_size_full_groups(radius, boost_mode, record, monkeypatch):
+    """BASELINE config 2/4 geometry (960x540, C 1024, S 256, theta 4, k 40) in groups of 23/22
+    inputs: global uniform (the headline's paired threshold search), local uniform r 80 / 506
+    (the paired local-uniform wavelet, never compared with the oracle in round 1), and the
+    per-column-boost selectors, each with recording on and off."""
+    monkeypatch.setenv("SP_GROUPS", "2")
+    cfg = headline_cfg(inhibition_radius=radius)
+    state = with_boost(perturbed_state(cfg), boost_mode)
+    frames = sp_inputs.frames(2002, 100, 45, 540, 960, rho=0.5)
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = [ora.step(x, False) for x in O.encode(frames, cfg)]
+    sp = make_sp(cfg, state, P.SP_PATH_BATCHED, max_inputs=64, record=record)
+    if record:
+        check_results(results, *run_gpu(sp, frames))
+    else:
+        check_sdrs(results, *run_gpu_sdr(sp, frames))
+    assert sp.info()["plan"]["groups"] == 2
+
+
+def test_bench_launch_config_recording_off_equals_on():
+    """The bench's exact launch (4096 frames, recording off, 148 groups of 27-28: every warp
+    pairs its inputs) gives the same winners as the recorded launch on all 4096 frames."""
+    cfg = headline_cfg()
+    state = perturbed_state(cfg, boost_hi=1.0)
+    frames = torch.empty((4096, 540, 960), dtype=torch.uint8, device=DEV)
+    P.synth_frames(frames, 0, 2002, rho=0.5)
+    outs = []
+    for record in (False, True):
+        sp = make_sp(cfg, state, max_inputs=4096, record=record)
+        sp.compute(frames)
+        sdr, counts = sp.winners()
+        outs.append((sdr.clone(), counts.clone()))
+        sp.close()
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])

@@ -228,6 +228,120 @@ def test_full_learning_invariants():
     assert np.max(np.abs(d - ora.active_duty)) <= 3 * 60 * ULP1
 
 
+def test_full_learning_both_duties_match_the_trace():
+    """Both duty cycles against float64 EMAs recomputed from the trace (S:119(b)), each
+    flag derived in the test from Alg. 1 itself: active duty <- the winners; overlap duty <-
+    the overlap Alg. 1 leaves non-zero, i.e. raw >= min_overlap (l.6-8 zero the rest)
+    and raw > 0.  Columns with few connected synapses (S = 6, theta 3, sparse frames) make
+    0 < raw < theta common, so feeding the raw count (or the active flag) to the overlap duty
+    fails here by orders of magnitude more than the fp32 error bound."""
+    cfg = ocfg(full_learning=True, duty_cycle_period=10, inhibition_radius=8, synapses_per_column=6,
+               min_overlap=3, winners_set_size=6)
+    frames = sp_inputs.frames(1003, 0, 60, 8, 8, rho=0.35)
+    ora, trace = _run(cfg, frames)
+    below = sum(int(((r.raw > 0) & (r.raw < cfg.min_overlap)).sum()) for r in trace)
+    assert below > 200, "the stream must exercise 0 < raw < min_overlap"
+    a = np.zeros(cfg.num_columns)
+    o = np.zeros(cfg.num_columns)
+    for r in trace:
+        a = a * 0.9 + r.active * 0.1
+        o = o * 0.9 + ((r.raw >= cfg.min_overlap) & (r.raw > 0)) * 0.1
+    assert np.max(np.abs(a - ora.active_duty)) <= 3 * 60 * ULP1
+    assert np.max(np.abs(o - ora.overlap_duty)) <= 3 * 60 * ULP1
+
+
+def _hand_sp(period=2, max_boost=2.0):
+    """4 columns x 8 synapses on an 8x8 input, hand-placed pools: column c sees bits 8c..8c+7."""
+    cfg = ocfg(num_columns=4, synapses_per_column=8, min_overlap=4, winners_set_size=1,
+               inhibition_radius=0, full_learning=True, duty_cycle_period=period, max_boost=max_boost)
+    idx = np.arange(32, dtype=np.int64).reshape(4, 8)
+    perm = np.full((4, 8), np.float32(0.21), np.float32)
+    return cfg, O.SpatialPoolerOracle(cfg, (idx, perm, np.ones(4, np.float32)))
+
+
+def test_full_learning_hand_worked_bump_and_boost():
+    """S:119(b-d) worked by hand on one frame.  Input bits on: 0..7 (all 8 of column 0), 8..13
+    (6 of column 1's), 16..17 (2 of column 2's), none of column 3's.  theta 4, k 1, period 2:
+      overlaps (Alg. 1): 8, 6, 0 (2 < theta is cut), 0; winner: column 0 only (k = 1);
+      (a) column 0: every input bit on -> perm 0.21 + 0.1 on all 8 synapses;
+      (b) active duty = (0*1 + a)/2 = [.5, 0, 0, 0]; overlap duty = [.5, .5, 0, 0]
+          (column 1 overlaps without winning; column 2's raw 2 is cut to 0, so it does not count);
+      (c) minA = 0.01*.5: columns 1-3 have adc 0 < minA -> boost 1 + (minA/minA)(2-1) = 2.0;
+      (d) minO = 0.01*.5: columns 2 and 3 (odc 0) are weak -> every perm + 0.1*0.2 = 0.23;
+          column 1 (odc .5, adc 0) is NOT bumped, column 0 not either.
+    A second, all-zero frame: no overlaps, no winners; duties halve; 2 and 3 are bumped again."""
+    cfg, ora = _hand_sp()
+    frame = np.zeros((1, 8, 8), np.uint8)
+    on = list(range(0, 8)) + list(range(8, 14)) + [16, 17]
+    frame.reshape(-1)[on] = 255
+    r = ora.step(O.encode(frame, cfg)[0], True)
+    assert list(r.raw) == [8, 6, 2, 0] and list(r.active) == [True, False, False, False]
+    assert list(ora.active_duty) == [0.5, 0.0, 0.0, 0.0]
+    assert list(ora.overlap_duty) == [0.5, 0.5, 0.0, 0.0]
+    assert list(ora.boost) == [1.0, 2.0, 2.0, 2.0]
+    p31 = np.float32(np.float32(0.21) + np.float32(0.1))
+    p23 = np.float32(np.float32(0.21) + np.float32(np.float32(0.1) * np.float32(0.2)))
+    assert np.all(ora.perm[0] == p31) and np.all(ora.perm[1] == np.float32(0.21))
+    assert np.all(ora.perm[2] == p23) and np.all(ora.perm[3] == p23)
+    r = ora.step(O.encode(np.zeros((1, 8, 8), np.uint8), cfg)[0], True)
+    assert not r.active.any()
+    assert list(ora.active_duty) == [0.25, 0.0, 0.0, 0.0]
+    assert list(ora.overlap_duty) == [0.25, 0.25, 0.0, 0.0]
+    p25 = np.float32(p23 + np.float32(np.float32(0.1) * np.float32(0.2)))
+    assert np.all(ora.perm[0] == p31) and np.all(ora.perm[1] == np.float32(0.21))
+    assert np.all(ora.perm[2] == p25) and np.all(ora.perm[3] == p25)
+
+
+def test_full_learning_overlap_below_theta_is_weak():
+    """S:119(d) "overlap duty below 1% of the neighbourhood maximum": a column whose raw count
+    stays in (0, theta) never has a non-zero Alg. 1 overlap, so after 5 frames its overlap duty
+    is still 0 and it has been bumped on every frame (5 x 0.02 above the start), while a column
+    that overlaps on every frame without ever winning keeps its permanences."""
+    cfg, ora = _hand_sp(period=3, max_boost=1.0)  # boosts stay 1: column 0 keeps winning
+    frame = np.zeros((1, 8, 8), np.uint8)
+    frame.reshape(-1)[list(range(0, 8)) + list(range(8, 13)) + [16, 17, 18]] = 255
+    for _ in range(5):
+        r = ora.step(O.encode(frame, cfg)[0], True)
+        assert list(r.raw) == [8, 5, 3, 0]
+    assert ora.overlap_duty[2] == 0.0 and ora.overlap_duty[1] > 0.5 and ora.active_duty[1] == 0.0
+    assert np.all(ora.perm[1] == np.float32(0.21))
+    p = np.float32(0.21)
+    for _ in range(5):
+        p = np.float32(p + np.float32(np.float32(0.1) * np.float32(0.2)))
+    assert np.all(ora.perm[2] == p) and np.all(ora.perm[3] == p)
+
+
+def test_full_learning_radius_after_bump_hand_worked():
+    """S:119's order: (d) the bump, THEN (e) the radius from the connected spans, so a synapse
+    the bump lifts across tau widens the span the radius sees.  By hand, 64-bit input, C 4,
+    S 8, theta 2, k 1, radius 1 in force, period 2; input bits 0..7 and 63 on:
+      col 0 pool {0..6, 63}: raw 8, the winner; all its bits on -> stays connected, span 64;
+      col 1 pool {0, 9, ..., 63} (step 9): raw 2, eligible, loses -> overlap duty .5, span 64;
+      col 2 pool {20..27} at perm 0.19 (< tau, so raw 0 and span 0): overlap duty 0 < 1% of the
+            max over its window {1, 2, 3} (.5) -> bumped to 0.19 + 0.02 >= tau: span 8;
+      col 3 pool {1, 10, ..., 55, 62}: raw 1 < theta (cut), overlap duty 0, but its window {2, 3}
+            has max 0, so it is not weak (0 < 0 is false); span 62.
+    radius = floor((sum span + nbits) / (2 nbits)): (64+64+8+62+64)/128 = 2.05 -> 2; computing it
+    before the bump would see span 0 for column 2: (190+64)/128 = 1.98 -> 1."""
+    cfg = ocfg(num_columns=4, synapses_per_column=8, min_overlap=2, winners_set_size=1,
+               inhibition_radius=1, full_learning=True, duty_cycle_period=2)
+    idx = np.array([[0, 1, 2, 3, 4, 5, 6, 63], [0, 9, 18, 27, 36, 45, 54, 63],
+                    list(range(20, 28)), [1, 10, 19, 28, 37, 46, 55, 62]], np.int64)
+    perm = np.full((4, 8), np.float32(0.21), np.float32)
+    perm[2] = np.float32(0.19)
+    ora = O.SpatialPoolerOracle(cfg, (idx, perm, np.ones(4, np.float32)))
+    frame = np.zeros((1, 8, 8), np.uint8)
+    frame.reshape(-1)[list(range(8)) + [63]] = 255
+    r = ora.step(O.encode(frame, cfg)[0], True)
+    assert list(r.raw) == [8, 2, 0, 1] and list(r.active) == [True, False, False, False]
+    assert list(ora.overlap_duty) == [0.5, 0.5, 0.0, 0.0]
+    p = np.float32(np.float32(0.19) + np.float32(np.float32(0.1) * np.float32(0.2)))
+    assert p >= np.float32(0.2) and np.all(ora.perm[2] == p)
+    assert np.all(ora.perm[3] == np.float32(0.21))
+    assert list(O.connected_span(ora.idx, ora.perm, 0.2)) == [64, 64, 8, 62]
+    assert ora.radius == 2
+
+
 def test_full_learning_off_equals_hot_path_step():
     # full_learning=False leaves boost, duty and radius untouched (regression of the a5 path)
     cfg = ocfg(inhibition_radius=4)
