@@ -61,13 +61,16 @@ enum {
     SP_FLAG_RECORD_OVERLAPS = 1u, /* keep raw/boosted overlaps of the last call for sp_overlaps */
     SP_FLAG_LEARN_GRID = 2u,      /* learn=1: prefer the grid-resident kernel (one CTA per SM) over
                                      the cluster-resident one (default: cluster when it fits) */
-    SP_FLAG_FULL_LEARNING = 4u    /* learn=1 also runs S:119(b-e) after each input's permanence
+    SP_FLAG_FULL_LEARNING = 4u,   /* learn=1 also runs S:119(b-e) after each input's permanence
                                      update (DESIGN R17-R21): active/overlap duty cycles (EMA of
                                      period duty_cycle_period), boost = linear rule up to
                                      max_boost, weak-column bump by 0.1*tau, and, when
                                      inhibition_radius > 0, the radius recomputed from the
                                      connected spans.  The radius in force governs inhibition
                                      of every later call (learn or not). */
+    SP_FLAG_PATCH_GATHER = 8u     /* patch mode inference: use the bit-sliced gather kernel even
+                                     where the tensor-core GEMM kernel is eligible (NEXT-2; the
+                                     two give identical results, this exists for A/B tests) */
 };
 
 /*
@@ -126,6 +129,8 @@ typedef struct sp_plan_info {
     uint32_t stages;             /* pipeline depth of the bulk-copy ring */
     uint32_t smem_bytes;         /* dynamic shared memory per CTA */
     uint32_t reason;             /* why not batched: 0 eligible, else bitmask */
+    uint32_t tensor_cores;       /* patch mode: 1 if the overlap runs as a tcgen05 kind::i8 GEMM
+                                    (NEXT-2; groups = blocks of 4 tile-rows, cluster = C32/128) */
 } sp_plan_info;
 
 /* Run-time information about a handle. */

@@ -259,6 +259,38 @@ bool encode_patches_tmap(CUtensorMap* map, const uint8_t* frames, const Geometry
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Tensor-core patch kernel (sp_patch_mma.cu): the connectivity matrix conn u8 [C32][nbits],
+// box {32 bytes of K, 128 columns}, and the tiles {x in tile, tile, y in tile, tile-row}, box
+// {32 px, 32 tiles, 1 row, 4 tile-rows} -- both SWIZZLE_32B, the K-major canonical layout the
+// tcgen05 descriptors name (rows of 32 B, 8-row groups of 256 B).
+bool encode_mma_tmaps(CUtensorMap* a, CUtensorMap* b, const uint8_t* conn, const uint8_t* frames,
+                      const Geometry& g, uint32_t frames_n) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q{};
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fn)
+            return false;
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t adims[2] = {g.nbits, g.C32};
+    const cuuint64_t astr[1] = {g.nbits};
+    const cuuint32_t abox[2] = {32u, 128u};
+    const cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
+    if (encode(a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(conn), adims, astr, abox, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    const uint32_t tx = g.W / g.pw, ty = g.H / g.ph;
+    const cuuint64_t bdims[4] = {g.pw, tx, g.ph, static_cast<cuuint64_t>(ty) * frames_n};
+    const cuuint64_t bstr[3] = {g.pw, g.W, static_cast<cuuint64_t>(g.W) * g.ph};
+    const cuuint32_t bbox[4] = {32u, 32u, 1u, 4u};
+    return encode(b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(frames), bdims, bstr, bbox, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool encode_frames_tmap(CUtensorMap* map, const uint8_t* frames, uint32_t nbits, uint32_t rows) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
@@ -358,6 +390,10 @@ struct sp_handle {
     uint32_t wm_min_radius = 96;
     uint32_t wm_min_radius_pi = 256;  // the same for the per-input k_inhibit (CTA wavelet)
     uint32_t force_groups = 0;        // SP_GROUPS (tests): batched groups per call, cluster size 1
+    // tensor-core patch kernel (NEXT-2, sp_patch_mma.cu): 0 clusters = not eligible
+    uint8_t* d_conn = nullptr;        // conn u8 [C32][nbits]: 1 where a connected synapse sits
+    bool conn_dirty = true;
+    uint32_t mma_Q = 0, mma_smem = 0, mma_region = 0, mma_stages = 0, mma_clusters = 0;
     uint32_t wm_umax = 32766u;        // per-warp wavelet coarse keys: u - 1 <= wm_umax (15 levels;
                                       // 12 bits: 0.603 vs 0.614 ms with seeded boosts in [1, 2] but
                                       // 0.697 vs 0.665 ms with full-learning boosts near 1)
@@ -427,7 +463,7 @@ void release(sp_handle* h) {
                     h->d_raw,  h->d_sdr,     h->d_counts,  h->d_raw_rec, h->d_boosted_rec,
                     h->d_stage[0], h->d_stage[1], h->d_synT,  h->d_gbar, h->d_adc, h->d_odc,
                     h->d_span, h->d_radius, h->d_fscratch, h->d_hist_off, h->d_hist_counts,
-                    h->d_bits_all};
+                    h->d_bits_all, h->d_conn};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
@@ -456,6 +492,24 @@ sp_plan_info make_plan(const sp_handle* h, uint32_t n, bool learn, const uint8_t
     if (h->cfg.force_path == SP_PATH_PER_INPUT) reason |= sp::kNotBatchedForced;
     if (!h->lay.ok) reason |= sp::kNotBatchedSmem;
     pl.reason = reason;
+    const bool mma = !g.whole && !learn && h->mma_clusters && !(h->cfg.flags & SP_FLAG_PATCH_GATHER) &&
+                     h->cfg.force_path != SP_PATH_PER_INPUT && !(frames && (reinterpret_cast<uintptr_t>(frames) & 15u));
+    if (mma && n > 0) {
+        // tensor-core patch kernel: blocks of 4 tile-rows x 32 slots, clusters of C32/128 CTAs
+        const uint32_t tile_rows = n / (g.W / g.pw);
+        pl.path = SP_PATH_BATCHED;
+        pl.reason = 0;
+        pl.tensor_cores = 1;
+        pl.groups = (tile_rows + 3u) / 4u;
+        pl.cluster = h->mma_Q;
+        pl.ctas = std::min(pl.groups, h->mma_clusters) * h->mma_Q;
+        pl.window_bits = g.nbits;
+        pl.num_windows = 1;
+        pl.chunk_bits = 32;
+        pl.stages = h->mma_stages;
+        pl.smem_bytes = h->mma_smem;
+        return pl;
+    }
     if (reason == 0 && n > 0 && !g.whole) {
         // patch kernel: groups of <= 32 tiles of one tile-row, persistent CTAs
         const uint32_t tx = g.W / g.pw;
@@ -576,6 +630,7 @@ sp_status upload_state(sp_handle* h, const uint32_t* idx, const float* perm, con
     h->syn_dirty = false;
     h->synT_dirty = true;
     h->span_dirty = true;
+    h->conn_dirty = true;
     if (h->lay.ok) return build_ell(h, perm);
     return SP_OK;
 }
@@ -707,7 +762,29 @@ sp_status launch_batched_path(sp_handle* h, const uint8_t* frames, const uint32_
     p.radius_dev = h->d_radius;
     p.wm_min_radius = h->wm_min_radius;
     p.wm_umax = h->wm_umax;
-    if (!g.whole) {
+    if (pl.tensor_cores) {
+        if (h->conn_dirty) {
+            e = sp::launch_build_conn(h->d_idx, h->d_perm, h->cfg.connected_threshold, g.C, g.C32, g.S, g.nbits,
+                                      h->d_conn, s);
+            h->launches++;
+            if (e != cudaSuccess) return cuda_fail(e, "connectivity build launch");
+            h->conn_dirty = false;
+        }
+        sp::PatchMmaParams q{};
+        if (!sp::encode_mma_tmaps(&q.tmap_a, &q.tmap_b, h->d_conn, frames, g, n_frames))
+            return fail(SP_E_CUDA, "cuTensorMapEncodeTiled failed for the tensor-core patch kernel");
+        q.bp = p;
+        q.bp.region_bytes = h->mma_region;
+        q.Q = h->mma_Q;
+        q.slabs = g.nbits / 32u;
+        q.xchunks = g.pw / 32u;
+        q.tiles_x = g.W / g.pw;
+        q.tile_rows = n_frames * (g.H / g.ph);
+        q.nblocks = (q.tile_rows + 3u) / 4u;
+        q.stages = h->mma_stages;
+        q.region_bytes = h->mma_region;
+        e = sp::launch_patch_mma(q, h->mma_smem, std::min(q.nblocks, h->mma_clusters), s);
+    } else if (!g.whole) {
         p.patch_w = g.pw;
         p.patch_h = g.ph;
         p.tiles_x = g.W / g.pw;
@@ -820,6 +897,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
             if (e != cudaSuccess) return cuda_fail(e, "grid learning launch");
         }
         h->ell_dirty = true;
+        h->conn_dirty = true;
         h->syn_dirty = true;
         h->last_plan.path = SP_PATH_PER_INPUT;
         h->last_learn_cluster = false;
@@ -892,6 +970,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
             if (e != cudaSuccess) return cuda_fail(e, "cluster learning launch");
         }
         h->ell_dirty = true;
+        h->conn_dirty = true;
         h->last_plan.path = SP_PATH_PER_INPUT;
         h->last_learn_cluster = true;
         h->last_learn_path = SP_LEARN_CLUSTER;
@@ -970,6 +1049,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
             if (e != cudaSuccess) return cuda_fail(e, "learning step launch");
         }
         h->ell_dirty = true;
+        h->conn_dirty = true;
     }
     return SP_OK;
 }
@@ -1053,6 +1133,32 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
         return cuda_fail(e, "kernel attributes");
     }
     if (h->lay.ok && h->g.whole) sp::batched_max_clusters(h->lay.smem_bytes, h->max_clusters);
+    // tensor-core patch kernel (NEXT-2): tiles of whole 32-px row chunks, <= 32 tiles per row,
+    // C32 = 128 Q columns (Q = 1, 2, 4, 8 CTAs per cluster), the resident connectivity slice
+    // plus the ring, two raw-count buffers and >= 20 KB of top-k scratch (8 warps' local
+    // comparator planes; the tie lists of the global selection share it) in shared memory
+    if (!g.whole && g.pw % 32u == 0 && g.W / g.pw <= 32u && g.C32 % 128u == 0 && g.S <= 1023u &&
+        !std::getenv("SP_NO_PATCH_MMA")) {
+        const uint32_t Q = g.C32 / 128u;
+        if (Q == 1 || Q == 2 || Q == 4 || Q == 8) {
+            const uint32_t stages = 4, slabs = g.nbits / 32u;
+            const uint32_t base = sp::patch_mma_smem(slabs, stages, Q, g.C32, 0u);
+            const int avail = h->max_smem - 1024 - static_cast<int>(base);
+            const uint32_t region = avail > 0 ? std::min<uint32_t>(static_cast<uint32_t>(avail) & ~127u, 65536u) : 0u;
+            if (region >= 20480u && sp::configure_patch_mma(h->max_smem) == cudaSuccess) {
+                const uint32_t smem = sp::patch_mma_smem(slabs, stages, Q, g.C32, region);
+                int nc = 0;
+                if (sp::patch_mma_max_clusters(smem, Q, &nc) == cudaSuccess && nc > 0) {
+                    h->mma_Q = Q;
+                    h->mma_smem = smem;
+                    h->mma_region = region;
+                    h->mma_stages = stages;
+                    h->mma_clusters = static_cast<uint32_t>(nc);
+                }
+                (void)cudaGetLastError();
+            }
+        }
+    }
     // cluster-resident learning: the largest cluster (<= 16 CTAs, >= 32 columns each) whose
     // synapse slice + bit-plane fit in shared memory and that can be co-scheduled
     // (the warp-level global selection holds C32 <= 2048 columns in registers)
@@ -1114,6 +1220,7 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
     const size_t cs = static_cast<size_t>(g.C) * g.S;
     const size_t cap = cfg->max_inputs;
     e = dalloc(&h->d_idx, cs);
+    if (e == cudaSuccess && h->mma_clusters) e = dalloc(&h->d_conn, static_cast<size_t>(g.C32) * g.nbits);
     if (e == cudaSuccess) e = dalloc(&h->d_perm, cs);
     if (e == cudaSuccess) e = dalloc(&h->d_boost, g.C32);
     if (e == cudaSuccess) e = dalloc(&h->d_bc, g.C32);

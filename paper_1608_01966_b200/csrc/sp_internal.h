@@ -79,6 +79,28 @@ struct alignas(64) BatchedParams {
     uint32_t wm_umax;          // per-column-boost wavelet: largest coarse key - 1 (levels = its bits)
 };
 
+// Tensor-core patch kernel (NEXT-2, sp_patch_mma.cu): raw counts of 128 tile slots per block
+// as a kind::i8 GEMM conn[C32 x nbits] . tiles[nbits x 128], one cluster of Q = C32/128 CTAs.
+struct alignas(64) PatchMmaParams {
+    CUtensorMap tmap_a;        // conn u8 [C32][nbits], box {32, 128}, SWIZZLE_32B
+    CUtensorMap tmap_b;        // frames {pw, tiles_x, ph, tile_rows}, box {32, 32, 1, 4}, SWIZZLE_32B
+    BatchedParams bp;          // selection parameters and outputs (sp_topk.cuh)
+    uint32_t Q;                // CTAs per cluster (128 columns each)
+    uint32_t slabs;            // nbits / 32 K-slabs
+    uint32_t xchunks;          // pw / 32 slabs per tile row
+    uint32_t tile_rows;        // frames * (H / ph)
+    uint32_t tiles_x;          // W / pw (<= 32)
+    uint32_t nblocks;          // ceil(tile_rows / 4)
+    uint32_t stages;           // ring slabs
+    uint32_t region_bytes;     // top-k scratch
+};
+uint32_t patch_mma_smem(uint32_t slabs, uint32_t stages, uint32_t Q, uint32_t C32, uint32_t region_bytes);
+cudaError_t configure_patch_mma(int max_smem);
+cudaError_t launch_patch_mma(const PatchMmaParams& p, uint32_t smem_bytes, uint32_t clusters, cudaStream_t s);
+cudaError_t patch_mma_max_clusters(uint32_t smem_bytes, uint32_t Q, int* n);
+cudaError_t launch_build_conn(const uint32_t* idx, const float* perm, float tau, uint32_t C, uint32_t C32, uint32_t S,
+                              uint32_t nbits, uint8_t* conn, cudaStream_t s);
+
 // Full learning (NEXT-1; S:119(b-e); DESIGN R17-R21): device state and constants.
 struct FullLearn {
     uint32_t on;               // SP_FLAG_FULL_LEARNING

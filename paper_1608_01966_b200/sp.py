@@ -22,6 +22,7 @@ SP_PATH_AUTO, SP_PATH_PER_INPUT, SP_PATH_BATCHED = 0, 1, 2
 SP_FLAG_RECORD_OVERLAPS = 1
 SP_FLAG_LEARN_GRID = 2
 SP_FLAG_FULL_LEARNING = 4
+SP_FLAG_PATCH_GATHER = 8
 SP_LEARN_PER_INPUT, SP_LEARN_CLUSTER, SP_LEARN_GRID = 0, 1, 2
 
 
@@ -71,7 +72,7 @@ class SpPlanInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint32) for n in (
         "path", "input_bits", "inputs_per_frame", "num_inputs", "columns_padded", "sdr_words",
         "groups", "cluster", "ctas", "window_bits", "num_windows", "chunk_bits", "stages",
-        "smem_bytes", "reason")]
+        "smem_bytes", "reason", "tensor_cores")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
