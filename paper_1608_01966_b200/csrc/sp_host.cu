@@ -259,12 +259,15 @@ bool encode_patches_tmap(CUtensorMap* map, const uint8_t* frames, const Geometry
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Tensor-core patch kernel (sp_patch_mma.cu): the connectivity matrix conn u8 [C32][nbits],
-// box {32 bytes of K, 128 columns}, and the tiles {x in tile, tile, y in tile, tile-row}, box
-// {32 px, 32 tiles, 1 row, 4 tile-rows} -- both SWIZZLE_32B, the K-major canonical layout the
-// tcgen05 descriptors name (rows of 32 B, 8-row groups of 256 B).
-bool encode_mma_tmaps(CUtensorMap* a, CUtensorMap* b, const uint8_t* conn, const uint8_t* frames,
-                      const Geometry& g, uint32_t frames_n) {
+// Tensor-core patch kernel (sp_patch_mma.cu): whole frame rows of 4 tile-rows, as a view
+// {W/k, k, y in tile, tile-row} with W/k <= 256 (TMA box dimension limit); box {W/k, k, sps, 4}.
+uint32_t mma_row_split(uint32_t W) {
+    for (uint32_t k = 1; k <= W; ++k)
+        if (W % k == 0 && W / k <= 256u && (W / k) % 16u == 0) return k;
+    return 0;
+}
+
+bool encode_mma_tmap(CUtensorMap* b, const uint8_t* frames, const Geometry& g, uint32_t frames_n, uint32_t sps) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q{};
@@ -274,20 +277,14 @@ bool encode_mma_tmaps(CUtensorMap* a, CUtensorMap* b, const uint8_t* conn, const
             return false;
         encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     }
-    const cuuint64_t adims[2] = {g.nbits, g.C32};
-    const cuuint64_t astr[1] = {g.nbits};
-    const cuuint32_t abox[2] = {32u, 128u};
+    const uint32_t k = mma_row_split(g.W), ty = g.H / g.ph;
+    if (!k) return false;
+    const cuuint64_t dims[4] = {g.W / k, k, g.ph, static_cast<cuuint64_t>(ty) * frames_n};
+    const cuuint64_t str[3] = {g.W / k, g.W, static_cast<cuuint64_t>(g.W) * g.ph};
+    const cuuint32_t box[4] = {g.W / k, k, sps, 4u};
     const cuuint32_t estr[4] = {1u, 1u, 1u, 1u};
-    if (encode(a, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(conn), adims, astr, abox, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return false;
-    const uint32_t tx = g.W / g.pw, ty = g.H / g.ph;
-    const cuuint64_t bdims[4] = {g.pw, tx, g.ph, static_cast<cuuint64_t>(ty) * frames_n};
-    const cuuint64_t bstr[3] = {g.pw, g.W, static_cast<cuuint64_t>(g.W) * g.ph};
-    const cuuint32_t bbox[4] = {32u, 32u, 1u, 4u};
-    return encode(b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(frames), bdims, bstr, bbox, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+    return encode(b, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(frames), dims, str, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -393,7 +390,8 @@ struct sp_handle {
     // tensor-core patch kernel (NEXT-2, sp_patch_mma.cu): 0 clusters = not eligible
     uint8_t* d_conn = nullptr;        // conn u8 [C32][nbits]: 1 where a connected synapse sits
     bool conn_dirty = true;
-    uint32_t mma_Q = 0, mma_smem = 0, mma_region = 0, mma_stages = 0, mma_clusters = 0;
+    uint32_t mma_Q = 0, mma_smem = 0, mma_region = 0, mma_raw_stages = 0, mma_conv_stages = 0, mma_sps = 1,
+             mma_clusters = 0;
     uint32_t wm_umax = 32766u;        // per-warp wavelet coarse keys: u - 1 <= wm_umax (15 levels;
                                       // 12 bits: 0.603 vs 0.614 ms with seeded boosts in [1, 2] but
                                       // 0.697 vs 0.665 ms with full-learning boosts near 1)
@@ -506,7 +504,7 @@ sp_plan_info make_plan(const sp_handle* h, uint32_t n, bool learn, const uint8_t
         pl.window_bits = g.nbits;
         pl.num_windows = 1;
         pl.chunk_bits = 32;
-        pl.stages = h->mma_stages;
+        pl.stages = h->mma_raw_stages;
         pl.smem_bytes = h->mma_smem;
         return pl;
     }
@@ -771,19 +769,68 @@ sp_status launch_batched_path(sp_handle* h, const uint8_t* frames, const uint32_
             h->conn_dirty = false;
         }
         sp::PatchMmaParams q{};
-        if (!sp::encode_mma_tmaps(&q.tmap_a, &q.tmap_b, h->d_conn, frames, g, n_frames))
+        if (!sp::encode_mma_tmap(&q.tmap_b, frames, g, n_frames, h->mma_sps))
             return fail(SP_E_CUDA, "cuTensorMapEncodeTiled failed for the tensor-core patch kernel");
         q.bp = p;
         q.bp.region_bytes = h->mma_region;
         q.Q = h->mma_Q;
-        q.slabs = g.nbits / 32u;
+        q.W = g.W;
+        q.nbits = g.nbits;
+        q.patch_w = g.pw;
+        q.patch_h = g.ph;
         q.xchunks = g.pw / 32u;
+        q.sps = h->mma_sps;
         q.tiles_x = g.W / g.pw;
         q.tile_rows = n_frames * (g.H / g.ph);
         q.nblocks = (q.tile_rows + 3u) / 4u;
-        q.stages = h->mma_stages;
+        q.raw_stages = h->mma_raw_stages;
+        q.conv_stages = h->mma_conv_stages;
+        q.raw_stage_bytes = g.W * h->mma_sps * 4u;
         q.region_bytes = h->mma_region;
-        e = sp::launch_patch_mma(q, h->mma_smem, std::min(q.nblocks, h->mma_clusters), s);
+        q.conn = h->d_conn;
+        q.multicast = q.Q > 1 ? 1u : 0u;
+        if (const char* em = std::getenv("SP_MMA_MULTICAST")) q.multicast = q.Q > 1 && std::atoi(em) ? 1u : 0u;
+        if (const char* ed = std::getenv("SP_MMA_DBG")) q.dbg = static_cast<uint32_t>(std::atoi(ed));
+        const uint32_t clusters = std::min(q.nblocks, h->mma_clusters);
+        static uint64_t* d_mtrace = nullptr;  // development aid: phase stamps of the tensor-core kernel
+        const bool mtrace = std::getenv("SP_MMA_TRACE") != nullptr;
+        if (mtrace) {
+            q.trace_blocks = 256;
+            if (!d_mtrace) cudaMalloc(&d_mtrace, 148u * 256u * 8u * 8u);
+            cudaMemsetAsync(d_mtrace, 0, 148u * 256u * 8u * 8u, s);
+            q.trace = d_mtrace;
+        }
+        e = sp::launch_patch_mma(q, h->mma_smem, clusters, s);
+        if (mtrace && e == cudaSuccess) {
+            std::vector<uint64_t> t(148u * 256u * 8u);
+            cudaStreamSynchronize(s);
+            cudaMemcpy(t.data(), d_mtrace, t.size() * 8u, cudaMemcpyDeviceToHost);
+            double acc[8] = {0};
+            uint64_t n = 0, t0 = ~0ull, t1 = 0;
+            for (uint32_t c = 0; c < clusters * q.Q; ++c)
+                for (uint32_t j = 0; j + 1u < 256u; ++j) {
+                    const uint64_t* a = &t[(static_cast<size_t>(c) * 256u + j) * 8u];
+                    const uint64_t* b = a + 8;
+                    if (!a[0] || !a[5] || !b[0]) continue;
+                    acc[0] += double(a[1] - a[0]);   // MMA issue span of a block
+                    acc[1] += double(a[3] - a[2]);   // drain
+                    acc[2] += double(a[5] - a[4]);   // top-k
+                    acc[3] += double(a[2] - a[1]);   // last MMA issued -> drain start
+                    acc[4] += double(a[4] - a[3]);   // drain end -> top-k start (this CTA's view)
+                    acc[5] += double(b[0] - a[0]);   // block period
+                    acc[6] += double(a[6]);          // converters waiting for raw data
+                    acc[7] += double(a[7]);          // converters waiting for a free converted slot
+                    t0 = std::min(t0, a[0]);
+                    t1 = std::max(t1, a[5]);
+                    ++n;
+                }
+            if (n)
+                std::fprintf(stderr,
+                             "[SP_MMA_TRACE] blocks %llu: mma span %.0f ns, drain %.0f, topk %.0f, mma->drain %.0f, "
+                             "period %.0f ns, converters wait raw %.0f / slot %.0f ns\n",
+                             (unsigned long long)n, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n,
+                             acc[5] / n, acc[6] / n, acc[7] / n);
+        }
     } else if (!g.whole) {
         p.patch_w = g.pw;
         p.patch_h = g.ph;
@@ -1133,31 +1180,39 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
         return cuda_fail(e, "kernel attributes");
     }
     if (h->lay.ok && h->g.whole) sp::batched_max_clusters(h->lay.smem_bytes, h->max_clusters);
-    // tensor-core patch kernel (NEXT-2): tiles of whole 32-px row chunks, <= 32 tiles per row,
-    // C32 = 128 Q columns (Q = 1, 2, 4, 8 CTAs per cluster), the resident connectivity slice
-    // plus the ring, two raw-count buffers and >= 20 KB of top-k scratch (8 warps' local
-    // comparator planes; the tie lists of the global selection share it) in shared memory
-    if (!g.whole && g.pw % 32u == 0 && g.W / g.pw <= 32u && g.C32 % 128u == 0 && g.S <= 1023u &&
+    // tensor-core patch kernel (NEXT-2): global inhibition (the selection it feeds is the global
+    // top-k; local windows stay on the bit-sliced gather kernel, measured faster there), patch
+    // width a power of two >= 32, <= 32 tiles per row, nbits <= 1024 (A in tensor memory beside
+    // two accumulators), C32 = 128 Q columns (Q = 1, 2, 4, 8 CTAs per cluster); shared memory:
+    // the converted ring (4 stages), two raw-count buffers, the top-k tie lists (8 warps x 512 B)
+    // and as many raw frame-row stages as fit (>= 3)
+    if (!g.whole && cfg->inhibition_radius == 0 && g.pw % 32u == 0 && (g.pw & (g.pw - 1u)) == 0 &&
+        g.W * (g.ph % 2u == 0 ? 2u : 1u) * 4u <= 64u * 8u * 16u &&  // one stage = 64 threads x 8 chunks
+        g.W / g.pw <= 32u && g.nbits <= 1024u && g.C32 % 128u == 0 && g.S <= 1023u && sp::mma_row_split(g.W) &&
         !std::getenv("SP_NO_PATCH_MMA")) {
         const uint32_t Q = g.C32 / 128u;
-        if (Q == 1 || Q == 2 || Q == 4 || Q == 8) {
-            const uint32_t stages = 4, slabs = g.nbits / 32u;
-            const uint32_t base = sp::patch_mma_smem(slabs, stages, Q, g.C32, 0u);
-            const int avail = h->max_smem - 1024 - static_cast<int>(base);
-            const uint32_t region = avail > 0 ? std::min<uint32_t>(static_cast<uint32_t>(avail) & ~127u, 65536u) : 0u;
-            if (region >= 20480u && sp::configure_patch_mma(h->max_smem) == cudaSuccess) {
-                const uint32_t smem = sp::patch_mma_smem(slabs, stages, Q, g.C32, region);
-                int nc = 0;
-                if (sp::patch_mma_max_clusters(smem, Q, &nc) == cudaSuccess && nc > 0) {
+        const uint32_t sps = g.ph % 2u == 0 ? 2u : 1u, region = 4096u, nc = 4u;
+        if ((Q == 1 || Q == 2 || Q == 4 || Q == 8) && sp::configure_patch_mma(h->max_smem) == cudaSuccess) {
+            uint32_t nr = 0;
+            while (sp::patch_mma_smem(g.W, sps, g.pw / 32u, nr + 1u, nc, Q, g.C32, region) + 1024u <=
+                       static_cast<uint32_t>(h->max_smem) && nr < 16u)
+                ++nr;
+            if (const char* es = std::getenv("SP_MMA_STAGES")) nr = std::min<uint32_t>(nr, std::atoi(es));
+            if (nr >= 3u) {
+                const uint32_t smem = sp::patch_mma_smem(g.W, sps, g.pw / 32u, nr, nc, Q, g.C32, region);
+                int ncl = 0;
+                if (sp::patch_mma_max_clusters(smem, Q, &ncl) == cudaSuccess && ncl > 0) {
                     h->mma_Q = Q;
                     h->mma_smem = smem;
                     h->mma_region = region;
-                    h->mma_stages = stages;
-                    h->mma_clusters = static_cast<uint32_t>(nc);
+                    h->mma_raw_stages = nr;
+                    h->mma_conv_stages = nc;
+                    h->mma_sps = sps;
+                    h->mma_clusters = static_cast<uint32_t>(ncl);
                 }
-                (void)cudaGetLastError();
             }
         }
+        (void)cudaGetLastError();
     }
     // cluster-resident learning: the largest cluster (<= 16 CTAs, >= 32 columns each) whose
     // synapse slice + bit-plane fit in shared memory and that can be co-scheduled

@@ -82,19 +82,28 @@ struct alignas(64) BatchedParams {
 // Tensor-core patch kernel (NEXT-2, sp_patch_mma.cu): raw counts of 128 tile slots per block
 // as a kind::i8 GEMM conn[C32 x nbits] . tiles[nbits x 128], one cluster of Q = C32/128 CTAs.
 struct alignas(64) PatchMmaParams {
-    CUtensorMap tmap_a;        // conn u8 [C32][nbits], box {32, 128}, SWIZZLE_32B
-    CUtensorMap tmap_b;        // frames {pw, tiles_x, ph, tile_rows}, box {32, 32, 1, 4}, SWIZZLE_32B
+    CUtensorMap tmap_b;        // frames {W/k, k, ph, tile_rows}, box {W/k, k, sps, 4}: whole rows
     BatchedParams bp;          // selection parameters and outputs (sp_topk.cuh)
     uint32_t Q;                // CTAs per cluster (128 columns each)
-    uint32_t slabs;            // nbits / 32 K-slabs
+    uint32_t W;                // frame width (bytes per frame row)
+    uint32_t nbits;            // pw * ph = K
+    uint32_t patch_w, patch_h; // pw (a power of two, multiple of 32), ph
     uint32_t xchunks;          // pw / 32 slabs per tile row
+    uint32_t sps;              // frame rows y per stage: 2 when ph is even, else 1
     uint32_t tile_rows;        // frames * (H / ph)
     uint32_t tiles_x;          // W / pw (<= 32)
     uint32_t nblocks;          // ceil(tile_rows / 4)
-    uint32_t stages;           // ring slabs
+    uint32_t raw_stages, conv_stages, raw_stage_bytes;
+    uint32_t multicast;        // one CTA fetches each raw stage for the whole cluster (TMA multicast)
     uint32_t region_bytes;     // top-k scratch
+    const uint8_t* conn;       // conn u8 [C32][nbits], loaded into TMEM with tcgen05.st
+    uint32_t dbg;              // development (SP_MMA_DBG): 1 skip the selection, 2 the exchange,
+                               // 4 the MMAs, 8 the conversion, 16 the exchange handshakes
+    uint64_t* trace;           // nullable (SP_MMA_TRACE): [ctas][trace_blocks][6] %globaltimer stamps
+    uint32_t trace_blocks;
 };
-uint32_t patch_mma_smem(uint32_t slabs, uint32_t stages, uint32_t Q, uint32_t C32, uint32_t region_bytes);
+uint32_t patch_mma_smem(uint32_t W, uint32_t sps, uint32_t xchunks, uint32_t raw_stages, uint32_t conv_stages,
+                        uint32_t Q, uint32_t C32, uint32_t region_bytes);
 cudaError_t configure_patch_mma(int max_smem);
 cudaError_t launch_patch_mma(const PatchMmaParams& p, uint32_t smem_bytes, uint32_t clusters, cudaStream_t s);
 cudaError_t patch_mma_max_clusters(uint32_t smem_bytes, uint32_t Q, int* n);
