@@ -488,7 +488,7 @@ def main():
                    "hbm_frac": enc_bytes / (enc_ms / 1e3) / 1e9 / peak_hbm,
                    "encode_plus_sp_frames_per_s": EF / both_ms * 1e3,
                    "sp": "Tab. 2 SP on the encoded frames (2048 columns, 128 synapses, k 40)",
-                   "plan": {k: v for k, v in enc.info().items() if k != "kernel_q8"}}
+                   "plan": {k: v for k, v in enc.info().items() if k != "kernel"}}
         enc.close()
         sp2.close()
         del bgr, binf

@@ -9,8 +9,10 @@
  *   R23 downscale src -> dst by OpenCV INTER_AREA (fp32 area weights, OpenCV's order of
  *       operations, round half to even), channels independent;
  *   R24 gray: Y = (3735 B + 19235 G + 9798 R + 2^14) >> 15 (OpenCV 8-bit BGR2GRAY);
- *   R25 mean = OpenCV's bit-exact 8-bit Gaussian blur of the block_size window (replicated
- *       borders); output byte = 255 if Y - mean > -ceil(bias) else 0.
+ *   R25 mean = cv2.adaptiveThreshold's Gaussian mean: float32 blur of the block_size window
+ *       (replicated borders; OpenCV's float32 kernel; row then symmetric column pass, one fp32
+ *       FMA per tap in OpenCV's order), rounded half to even; output byte = 255 if
+ *       Y - mean > -ceil(bias) else 0.
  * Conventions as in sp.h: sp_status results, device pointers owned by the caller,
  * stream-ordered asynchronous calls, no CPU fallback.
  */
@@ -43,7 +45,7 @@ typedef struct sp_encoder_info {
     uint32_t ctas_per_sm;
     uint32_t xfast;          /* 1 if the x table is an exact 4:1 average (vectorised path) */
     uint64_t kernel_launches;
-    int32_t kernel_q8[16];   /* the 8-bit Gaussian kernel (sum 256) */
+    float kernel[16];        /* the float32 Gaussian kernel (block_size weights) */
 } sp_encoder_info;
 
 /* Defaults: 960x540 -> 240x134, block 11, bias 2, device 0.  SP_E_ARG for NULL. */

@@ -20,20 +20,28 @@ names OpenCV, so the steps follow OpenCV's 8-bit definitions, written out here:
    ``COLOR_BGR2GRAY``; pinned against cv2 over all 2^24 colours).
 3. adaptive threshold (R25): T(p) = Gaussian-weighted mean of the k x k neighbourhood
    (replicated borders) - bias; bit = intensity > T (strict).  The mean is
-   OpenCV's bit-exact 8-bit Gaussian blur: sigma = 0.3*((k-1)/2 - 1) + 0.8, the kernel
-   quantised to 8 fractional bits by error diffusion (sum exactly 256), a separable row
-   then column pass in integers and (acc + 2^15) >> 16; the bias enters as ceil(bias)
-   (OpenCV's THRESH_BINARY rule), so bit = g - mean > -ceil(bias).  Output bytes 255 / 0.
+   the one ``cv2.adaptiveThreshold(..., ADAPTIVE_THRESH_GAUSSIAN_C, ...)`` takes: the gray
+   image converted to float32, OpenCV's float32 Gaussian kernel (``getGaussianKernel``:
+   fixed tables for k <= 9, else exp(-x^2 / (2 sigma^2)) with sigma = fma(k, 0.15, 0.35)
+   normalised in double and rounded to float32), a row pass then a column pass in float32
+   with one fused multiply-add per tap (the order of OpenCV's AVX2/FMA3 filter: row
+   ``s = fma(x_j, k_j, s)`` for j = 0..k-1 from s = 0; column ``s = fma(r_0, k_0, 0)``, then
+   ``s = fma(r_+j + r_-j, k_j, s)`` for j = 1..k/2, the pair sum one float32 add), the
+   float mean rounded half-to-even and saturated to uint8 (``convertTo``).  The bias enters
+   as ceil(bias) (OpenCV's THRESH_BINARY rule), so bit = g - mean > -ceil(bias).  Output
+   bytes 255 / 0.
 """
 from __future__ import annotations
 
 import math
+from fractions import Fraction
 
 import numpy as np
 
 # OpenCV's fixed small Gaussian kernels for ksize <= 7 and sigma <= 0 (getGaussianKernel)
 _SMALL = {1: [1.0], 3: [0.25, 0.5, 0.25], 5: [0.0625, 0.25, 0.375, 0.25, 0.0625],
-          7: [0.03125, 0.109375, 0.21875, 0.28125, 0.21875, 0.109375, 0.03125]}
+          7: [0.03125, 0.109375, 0.21875, 0.28125, 0.21875, 0.109375, 0.03125],
+          9: [4 / 256, 13 / 256, 30 / 256, 51 / 256, 60 / 256, 51 / 256, 30 / 256, 13 / 256, 4 / 256]}
 
 
 # --------------------------------------------------------------------------- #
@@ -102,47 +110,69 @@ def bgr2gray(img: np.ndarray) -> np.ndarray:
 # --------------------------------------------------------------------------- #
 # 3. adaptive threshold, Gaussian (R25)
 # --------------------------------------------------------------------------- #
-def gaussian_kernel_q8(ksize: int):
-    """OpenCV's bit-exact 8-bit Gaussian kernel: double weights, then error-diffused
-    rounding to 8 fractional bits, centre = 256 - the others."""
+def fma32(a, b, c) -> np.ndarray:
+    """float32 fused multiply-add, round(a*b + c) to nearest-even, elementwise.
+
+    a*b of two float32 is exact in float64 (24 + 24 significand bits); s = fl64(a*b + c) with
+    its exact error e (TwoSum, so s + e = a*b + c).  Rounding s to float32 equals rounding
+    s + e except when s lies exactly halfway between two float32 and e != 0: then the true
+    value is on e's side of the midpoint."""
+    a = np.asarray(a, np.float32).astype(np.float64)
+    b = np.asarray(b, np.float32).astype(np.float64)
+    c = np.asarray(c, np.float32).astype(np.float64)
+    p = a * b
+    s = p + c
+    bv = s - p
+    e = (p - (s - bv)) + (c - bv)
+    r = s.astype(np.float32)
+    up = np.nextafter(r, np.float32(np.inf))
+    dn = np.nextafter(r, np.float32(-np.inf))
+    r64 = r.astype(np.float64)
+    to_up = (s == (r64 + up.astype(np.float64)) / 2) & (e > 0)
+    to_dn = (s == (r64 + dn.astype(np.float64)) / 2) & (e < 0)
+    return np.where(to_up, up, np.where(to_dn, dn, r)).astype(np.float32)
+
+
+def gaussian_kernel_f32(ksize: int) -> np.ndarray:
+    """OpenCV's ``getGaussianKernel(ksize, 0, CV_32F)``: weights in double (sigma =
+    fma(ksize, 0.15, 0.35) = 0.3*((ksize-1)/2 - 1) + 0.8, the sum of the outer weights
+    doubled plus the centre's 1, each weight times 1/sum), stored as float32."""
     assert ksize % 2 == 1 and ksize >= 3
-    n2 = ksize // 2
     if ksize in _SMALL:
-        k = _SMALL[ksize]
-    else:
-        sigma = ksize * 0.15 + 0.35            # = 0.3*((ksize-1)/2 - 1) + 0.8
-        s2 = -0.125 / (sigma * sigma)
-        vals = [math.exp(float((2 * i - (ksize - 1)) ** 2) * s2) for i in range(n2)]
-        total = 2.0 * sum(vals) + 1.0
-        k = [v * (1.0 / total) for v in vals]
-    q, err = [0] * ksize, 0.0
-    for i in range(n2):
-        adj = k[i] * 256.0 + err
-        v0 = int(np.rint(adj))
-        err = adj - v0
-        q[i] = q[ksize - 1 - i] = v0
-    q[n2] = 256 - 2 * sum(q[:n2])
-    return q
+        return np.array(_SMALL[ksize], np.float32)
+    n2 = ksize // 2
+    sigma = float(Fraction(ksize) * Fraction(0.15) + Fraction(0.35))   # one rounding (fma)
+    s2 = -0.125 / (sigma * sigma)
+    vals = [math.exp(float((2 * i - (ksize - 1)) ** 2) * s2) for i in range(n2)]
+    total = 0.0
+    for v in vals:
+        total += v
+    total = total * 2.0 + 1.0
+    mul = 1.0 / total
+    k = [v * mul for v in vals]
+    return np.array(k + [1.0 * mul] + k[::-1], np.float32)
 
 
-def gaussian_mean_u8(gray: np.ndarray, ksize: int) -> np.ndarray:
-    """Separable 8-bit Gaussian blur with replicated borders, exact integers."""
-    q = gaussian_kernel_q8(ksize)
+def gaussian_mean_f32(gray: np.ndarray, ksize: int) -> np.ndarray:
+    """float32 Gaussian mean of ``uint8[H, W]`` with replicated borders: row pass, then the
+    symmetric column pass, one float32 FMA per tap (module docstring, step 3)."""
+    k = gaussian_kernel_f32(ksize)
     r = ksize // 2
     H, W = gray.shape
-    p = np.pad(gray.astype(np.int64), r, mode="edge")
-    rows = np.zeros((H + 2 * r, W), dtype=np.int64)
+    p = np.pad(gray.astype(np.float32), r, mode="edge")
+    rows = np.zeros((H + 2 * r, W), np.float32)
     for j in range(ksize):
-        rows += q[j] * p[:, j:j + W]
-    cols = np.zeros((H, W), dtype=np.int64)
-    for j in range(ksize):
-        cols += q[j] * rows[j:j + H, :]
-    return ((cols + (1 << 15)) >> 16).astype(np.uint8)
+        rows = fma32(p[:, j:j + W], k[j], rows)
+    mean = fma32(rows[r:r + H], k[r], np.zeros((H, W), np.float32))
+    for j in range(1, r + 1):
+        pair = (rows[r + j:r + j + H] + rows[r - j:r - j + H]).astype(np.float32)
+        mean = fma32(pair, k[r + j], mean)
+    return mean
 
 
 def adaptive_threshold(gray: np.ndarray, ksize: int = 11, bias: float = 2.0) -> np.ndarray:
-    """bit = g > mean - ceil(bias), as bytes 255 / 0."""
-    m = gaussian_mean_u8(gray, ksize).astype(np.int64)
+    """bit = g > round(mean) - ceil(bias), as bytes 255 / 0."""
+    m = np.clip(np.rint(gaussian_mean_f32(gray, ksize)), 0, 255).astype(np.int64)  # half to even
     return np.where(gray.astype(np.int64) - m > -math.ceil(bias), 255, 0).astype(np.uint8)
 
 

@@ -7,9 +7,10 @@
 // band by band (a band = the source rows of `band_rows` output rows: contiguous bytes, one
 // cp.async.bulk per band into a ring of shared-memory stages, mbarrier completion), the band
 // is area-downscaled (R23: OpenCV INTER_AREA, its fp32 operation order) and converted to gray
-// (R24) into a resident gray image; then the Gaussian mean (R25: 8-bit bit-exact blur, exact
-// integers, so the separable passes may run in any order) and the threshold are computed by a
-// register sliding window down each column, while the ring already streams the next frame.
+// (R24) into a resident gray image; then the Gaussian mean (R25: cv2.adaptiveThreshold's
+// float32 blur -- a row pass then a symmetric column pass, one fp32 FMA per tap in OpenCV's
+// order -- rounded half to even) and the threshold are computed by a register sliding window
+// of row sums down each column pair, while the ring already streams the next frame.
 // The path is HBM-bound: 3*W0*H0 bytes read, W1*H1 written per frame.
 #include <algorithm>
 #include <cmath>
@@ -46,7 +47,7 @@ struct EncParams {
     const uint32_t* xsx;       // [.] source column of the entry
     const float* xalpha;       // [.]
     int32_t K, cbias;          // Gaussian window, ceil(bias)
-    int32_t q[16];             // 8-bit quantised Gaussian kernel (sum 256)
+    float kw[16];              // float32 Gaussian kernel (OpenCV getGaussianKernel, CV_32F)
     uint32_t ny_entries, nx_entries;  // table sizes (staged in shared memory per CTA)
     uint32_t table_bytes;      // shared-memory bytes of the staged tables
 };
@@ -158,8 +159,12 @@ __device__ __forceinline__ void downscale_band(const EncParams& p, const EncTabl
     }
 }
 
-// R25: Gaussian mean (exact integers) and threshold, a register window of K horizontal sums
-// down columns x and x+1 (one thread, shared loads) for rows [y0, y1)
+// R25: Gaussian mean and threshold for columns x and x+1 (one thread, shared loads), rows
+// [y0, y1).  A register window holds the K row sums rs(y - R .. y + R) of both columns; row
+// sums of the replicated rows outside the image are those of the clamped rows (OpenCV pads the
+// source before its row filter).  Row pass: s = fma(g[x + j - R], k_j, s), j = 0..K-1, from
+// s = 0; column pass: m = fma(rs(y), k_R, 0), then m = fma(rs(y + j) + rs(y - j), k_{R+j}, m),
+// j = 1..R (OpenCV's AVX2/FMA3 RowVec_32f and symmetric SymmColumnVec_32f order).
 template <int K>
 __device__ __forceinline__ void blur_columns(const EncParams& p, const uint8_t* gray, uint8_t* out, uint32_t x,
                                              uint32_t y0, uint32_t y1) {
@@ -169,30 +174,35 @@ __device__ __forceinline__ void blur_columns(const EncParams& p, const uint8_t* 
     int cx[K + 1];
 #pragma unroll
     for (int j = 0; j <= K; ++j) cx[j] = min(W - 1, max(0, static_cast<int>(x) + j - R));
-    int q[K];
+    float kw[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) q[j] = p.q[j];
-    auto hsum = [&](int yy, int& a, int& b) {
+    for (int j = 0; j < K; ++j) kw[j] = p.kw[j];
+    auto hsum = [&](int yy, float& a, float& b) {
         const uint8_t* row = gray + min(H - 1, max(0, yy)) * W;
-        int v[K + 1];
+        float v[K + 1];
 #pragma unroll
-        for (int j = 0; j <= K; ++j) v[j] = row[cx[j]];
-        a = 0, b = 0;
+        for (int j = 0; j <= K; ++j) v[j] = static_cast<float>(row[cx[j]]);
+        a = 0.0f, b = 0.0f;
 #pragma unroll
-        for (int j = 0; j < K; ++j) a += q[j] * v[j], b += q[j] * v[j + 1];
+        for (int j = 0; j < K; ++j) a = __fmaf_rn(v[j], kw[j], a), b = __fmaf_rn(v[j + 1], kw[j], b);
     };
-    int ha[K], hb[K];
+    float ha[K], hb[K];
 #pragma unroll
     for (int i = 0; i < K - 1; ++i) hsum(static_cast<int>(y0) - R + i, ha[i], hb[i]);
     for (int y = static_cast<int>(y0); y < static_cast<int>(y1); ++y) {
         hsum(y + R, ha[K - 1], hb[K - 1]);
-        int acca = 0, accb = 0;
+        float ma = __fmaf_rn(ha[R], kw[R], 0.0f), mb = __fmaf_rn(hb[R], kw[R], 0.0f);
 #pragma unroll
-        for (int i = 0; i < K; ++i) acca += q[i] * ha[i], accb += q[i] * hb[i];
+        for (int j = 1; j <= R; ++j) {
+            ma = __fmaf_rn(__fadd_rn(ha[R + j], ha[R - j]), kw[R + j], ma);
+            mb = __fmaf_rn(__fadd_rn(hb[R + j], hb[R - j]), kw[R + j], mb);
+        }
+        // convertTo(CV_8U): round half to even, saturate
+        const int mua = min(255, max(0, __float2int_rn(ma))), mub = min(255, max(0, __float2int_rn(mb)));
         const uint8_t* grow = gray + y * W + x;
         uint8_t* orow = out + static_cast<size_t>(y) * W + x;
-        orow[0] = static_cast<int>(grow[0]) - ((acca + 32768) >> 16) > -p.cbias ? 255u : 0u;
-        if (two) orow[1] = static_cast<int>(grow[1]) - ((accb + 32768) >> 16) > -p.cbias ? 255u : 0u;
+        orow[0] = static_cast<int>(grow[0]) - mua > -p.cbias ? 255u : 0u;
+        if (two) orow[1] = static_cast<int>(grow[1]) - mub > -p.cbias ? 255u : 0u;
 #pragma unroll
         for (int i = 0; i < K - 1; ++i) ha[i] = ha[i + 1], hb[i] = hb[i + 1];
     }
@@ -384,40 +394,34 @@ sp_status efail(sp_status st, const char* msg) {
     return st;
 }
 
-// 8-bit Gaussian kernel (R25): OpenCV's small tables for k <= 7, else exp(-x^2/(2 sigma^2))
-// with sigma = 0.15 k + 0.35, normalised; error-diffused to 8 fractional bits, centre = rest
-void gaussian_q8(int k, int* q) {
+// float32 Gaussian kernel (R25), OpenCV getGaussianKernel(k, 0, CV_32F): fixed tables for
+// k <= 9, else exp(-x^2 / (2 sigma^2)) with sigma = fma(k, 0.15, 0.35), normalised in double
+// (outer weights summed in order, doubled, plus the centre's 1), rounded to float
+void gaussian_f32(int k, float* kw) {
     static const double small3[] = {0.25, 0.5, 0.25};
     static const double small5[] = {0.0625, 0.25, 0.375, 0.25, 0.0625};
     static const double small7[] = {0.03125, 0.109375, 0.21875, 0.28125, 0.21875, 0.109375, 0.03125};
+    static const double small9[] = {4 / 256., 13 / 256., 30 / 256., 51 / 256., 60 / 256.,
+                                    51 / 256., 30 / 256., 13 / 256., 4 / 256.};
+    if (k <= 9) {
+        const double* t = k == 3 ? small3 : (k == 5 ? small5 : (k == 7 ? small7 : small9));
+        for (int i = 0; i < k; ++i) kw[i] = static_cast<float>(t[i]);
+        return;
+    }
     const int n2 = k / 2;
     std::vector<double> w(n2);
-    if (k <= 7) {
-        const double* t = k == 3 ? small3 : (k == 5 ? small5 : small7);
-        for (int i = 0; i < n2; ++i) w[i] = t[i];
-    } else {
-        const double sigma = k * 0.15 + 0.35;
-        const double s2 = -0.125 / (sigma * sigma);
-        double total = 0.0;
-        for (int i = 0; i < n2; ++i) {
-            const double x = 2.0 * i - (k - 1);
-            w[i] = std::exp(x * x * s2);
-            total += w[i];
-        }
-        total = 2.0 * total + 1.0;
-        const double mul = 1.0 / total;
-        for (int i = 0; i < n2; ++i) w[i] *= mul;
-    }
-    double err = 0.0;
-    int sum = 0;
+    const double sigma = std::fma(static_cast<double>(k), 0.15, 0.35);
+    const double s2 = -0.125 / (sigma * sigma);
+    double total = 0.0;
     for (int i = 0; i < n2; ++i) {
-        const double adj = w[i] * 256.0 + err;
-        const double v0 = std::nearbyint(adj);
-        err = adj - v0;
-        q[i] = q[k - 1 - i] = static_cast<int>(v0);
-        sum += 2 * static_cast<int>(v0);
+        const double x = 2.0 * i - (k - 1);
+        w[i] = std::exp(x * x * s2);
+        total += w[i];
     }
-    q[n2] = 256 - sum;
+    total = total * 2.0 + 1.0;
+    const double mul = 1.0 / total;
+    for (int i = 0; i < n2; ++i) kw[i] = kw[k - 1 - i] = static_cast<float>(w[i] * mul);
+    kw[n2] = static_cast<float>(1.0 * mul);
 }
 
 }  // namespace
@@ -465,7 +469,7 @@ sp_status sp_encoder_create(const sp_encoder_config* cfg, sp_encoder** out) {
     p.row_bytes = 3u * p.W0;
     p.K = static_cast<int32_t>(cfg->block_size);
     p.cbias = static_cast<int32_t>(std::ceil(cfg->bias));
-    gaussian_q8(p.K, p.q);
+    gaussian_f32(p.K, p.kw);
     std::vector<uint32_t> yoff, ysy, xoff, xsx;
     std::vector<float> ybeta, xalpha;
     sp::area_table(p.H0, p.H1, yoff, ysy, ybeta);
@@ -602,7 +606,7 @@ sp_status sp_encoder_get_info(sp_encoder* e, sp_encoder_info* out) {
     out->ctas_per_sm = e->ctas_per_sm;
     out->xfast = e->p.xfast;
     out->kernel_launches = e->launches;
-    for (int i = 0; i < 16; ++i) out->kernel_q8[i] = i < e->p.K ? e->p.q[i] : 0;
+    for (int i = 0; i < 16; ++i) out->kernel[i] = i < e->p.K ? e->p.kw[i] : 0.0f;
     return SP_OK;
 }
 

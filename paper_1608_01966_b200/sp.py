@@ -87,7 +87,7 @@ class SpEncoderConfig(ctypes.Structure):
 class SpEncoderInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint32) for n in ("band_rows", "bands", "stages", "stage_bytes", "smem_bytes",
                                                "ctas_per_sm", "xfast")] + \
-               [("kernel_launches", ctypes.c_uint64), ("kernel_q8", ctypes.c_int32 * 16)]
+               [("kernel_launches", ctypes.c_uint64), ("kernel", ctypes.c_float * 16)]
 
 
 class SpInfo(ctypes.Structure):
@@ -311,8 +311,8 @@ class Encoder:
     def info(self) -> dict:
         out = SpEncoderInfo()
         _check(lib().sp_encoder_get_info(self._h, ctypes.byref(out)))
-        d = {n: int(getattr(out, n)) for n, _ in out._fields_ if n != "kernel_q8"}
-        d["kernel_q8"] = list(out.kernel_q8)[:int(self.cfg.block_size)]
+        d = {n: int(getattr(out, n)) for n, _ in out._fields_ if n != "kernel"}
+        d["kernel"] = list(out.kernel)[:int(self.cfg.block_size)]
         return d
 
 

@@ -38,7 +38,7 @@ def test_encoder_parity(src, dst, k, bias):
                     block_size=k, bias=bias)
     got = enc.encode(torch.from_numpy(bgr).to(DEV)).cpu().numpy()
     torch.cuda.synchronize()
-    assert enc.info()["kernel_q8"] == E.gaussian_kernel_q8(k)
+    assert np.array_equal(np.array(enc.info()["kernel"], np.float32), E.gaussian_kernel_f32(k))
     for f in range(F):
         assert np.array_equal(got[f], want[f]), f"frame {f}: {np.count_nonzero(got[f] != want[f])} px differ"
 

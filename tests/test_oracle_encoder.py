@@ -5,6 +5,7 @@ oracle is checked against the library routine it restates (an independent implem
 plus the SPEC's worked examples and properties.  cv2 is never used by the product path.
 """
 import math
+from fractions import Fraction
 
 import numpy as np
 import pytest
@@ -58,34 +59,73 @@ def test_gray_equals_opencv_on_a_colour_cube_sample():
 # --------------------------------------------------------------------------- #
 # R25: Gaussian mean and adaptive threshold
 # --------------------------------------------------------------------------- #
+def test_fma32_against_exact_rationals():
+    # brute force: the exact a*b + c as a Fraction, rounded to the nearest float32 (ties to
+    # even) by comparing the three float32 around it
+    rng = np.random.default_rng(3)
+    a = (rng.random(3000) * 300).astype(np.float32)
+    b = rng.random(3000).astype(np.float32)
+    c = (rng.random(3000) * 100 - 20).astype(np.float32)
+    # ties: a*b + c exactly halfway between two float32 (c absorbs the low half of a*b)
+    a[:200] = np.float32(1 + 2.0 ** -12)
+    b[:200] = np.float32(1 + 2.0 ** -12)
+    c[:200] = np.float32(0)
+    got = E.fma32(a, b, c)
+    for i in range(len(a)):
+        ex = Fraction(float(a[i])) * Fraction(float(b[i])) + Fraction(float(c[i]))
+        f = np.float32(float(ex))
+        cands = [np.nextafter(f, np.float32(-np.inf)), f, np.nextafter(f, np.float32(np.inf))]
+        d = [abs(Fraction(float(x)) - ex) for x in cands]
+        best = [x for x, dd in zip(cands, d) if dd == min(d)]
+        if len(best) > 1:
+            best = [x for x in best if int(x.view(np.uint32)) % 2 == 0]
+        assert got[i] == best[0], i
+
+
 @pytest.mark.parametrize("ksize", [3, 5, 7, 9, 11, 13, 15])
-def test_gaussian_mean_equals_opencv_8bit_blur(ksize):
+def test_gaussian_kernel_equals_opencv(ksize):
+    assert np.array_equal(E.gaussian_kernel_f32(ksize), cv2.getGaussianKernel(ksize, 0, cv2.CV_32F).ravel())
+
+
+def test_kernel_11_closed_form():
+    # sigma = 0.3*((11-1)/2 - 1) + 0.8 = 2.0: w_x = exp(-x^2/8) / sum, |x| <= 5
+    w = np.exp(-np.arange(-5, 6) ** 2 / 8.0)
+    assert np.allclose(E.gaussian_kernel_f32(11), w / w.sum(), rtol=1e-7, atol=0)
+
+
+@pytest.mark.parametrize("ksize", [3, 5, 7, 9, 11, 13, 15])
+def test_gaussian_mean_equals_opencv_float_blur(ksize):
+    # OpenCV's vector path covers rows whose width is a multiple of 16 (240 = the paper's
+    # encoded width); the float mean is then bit-equal
     rng = np.random.default_rng(ksize)
     for g in (rng.integers(0, 256, (134, 240), dtype=np.uint8),
-              cv2.GaussianBlur(rng.integers(0, 256, (67, 91), dtype=np.uint8), (0, 0), 3)):
-        want = cv2.GaussianBlur(g, (ksize, ksize), 0, borderType=cv2.BORDER_REPLICATE)
-        assert np.array_equal(E.gaussian_mean_u8(g, ksize), want)
-    q = E.gaussian_kernel_q8(ksize)
-    assert sum(q) == 256 and q == q[::-1]
+              cv2.GaussianBlur(rng.integers(0, 256, (67, 96), dtype=np.uint8), (0, 0), 3)):
+        want = cv2.GaussianBlur(g.astype(np.float32), (ksize, ksize), 0,
+                                borderType=cv2.BORDER_REPLICATE | cv2.BORDER_ISOLATED)
+        assert np.array_equal(E.gaussian_mean_f32(g, ksize).view(np.uint32), want.view(np.uint32))
 
 
-def test_kernel_11_values():
-    # sigma = 0.3*((11-1)/2 - 1) + 0.8 = 2.0; 256 * exp(-x^2/8) / sum, error-diffused
-    assert E.gaussian_kernel_q8(11) == [2, 7, 17, 31, 45, 52, 45, 31, 17, 7, 2]
+def test_gaussian_mean_close_to_exact_weighted_mean():
+    # independent of OpenCV: the float32 mean is within a few ulp of the exact double sum
+    rng = np.random.default_rng(4)
+    g = rng.integers(0, 256, (40, 48), dtype=np.uint8)
+    k = E.gaussian_kernel_f32(11).astype(np.float64)
+    p = np.pad(g.astype(np.float64), 5, mode="edge")
+    exact = np.zeros(g.shape)
+    for i in range(11):
+        for j in range(11):
+            exact += k[i] * k[j] * p[i:i + 40, j:j + 48]
+    assert np.max(np.abs(E.gaussian_mean_f32(g, 11) - exact)) < 1e-4
 
 
-def test_threshold_vs_opencv_adaptive_threshold():
-    # cv2.adaptiveThreshold takes its Gaussian mean in float32 and rounds it; R25 uses the
-    # 8-bit blur.  The decisions agree except where the two means round differently: there
-    # the float mean lies within half a level of the decision boundary g + ceil(bias).
-    rng = np.random.default_rng(5)
-    g = rng.integers(0, 256, (134, 240), dtype=np.uint8)
-    ours = E.adaptive_threshold(g, 11, 2.0)
-    theirs = cv2.adaptiveThreshold(g, 255, cv2.ADAPTIVE_THRESH_GAUSSIAN_C, cv2.THRESH_BINARY, 11, 2)
-    mf = cv2.GaussianBlur(g.astype(np.float32), (11, 11), 0, borderType=cv2.BORDER_REPLICATE)
-    diff = ours != theirs
-    assert diff.mean() < 0.005
-    assert np.all(np.abs(mf[diff] - (g[diff].astype(np.float32) + 2) + 0.5) <= 1.0)
+@pytest.mark.parametrize("ksize", [3, 5, 7, 9, 11, 13, 15])
+def test_threshold_equals_opencv_adaptive_threshold(ksize):
+    # the routine P:168 names, zero differing pixels
+    rng = np.random.default_rng(5 + ksize)
+    for bias in (2.0, 0.0, -3.5, 7.25):
+        g = rng.integers(0, 256, (134, 240), dtype=np.uint8)
+        want = cv2.adaptiveThreshold(g, 255, cv2.ADAPTIVE_THRESH_GAUSSIAN_C, cv2.THRESH_BINARY, ksize, bias)
+        assert np.array_equal(E.adaptive_threshold(g, ksize, bias), want)
 
 
 def test_spec_examples():
@@ -104,7 +144,8 @@ def test_spec_examples():
     ring[1, 1] = 0
     assert np.all(ring == 0)
     assert out[0, 0] == 255 and out[8, 8] == 255
-    assert E.gaussian_mean_u8(d, 5)[4, 4] == 36 and E.gaussian_mean_u8(d, 5)[4, 5] == 24
+    m = E.gaussian_mean_f32(d, 5)
+    assert m[4, 4] == np.float32(255 * 36 / 256) and m[4, 5] == np.float32(255 * 24 / 256)
 
 
 def test_shift_covariance_and_monotonicity():
@@ -120,13 +161,12 @@ def test_shift_covariance_and_monotonicity():
 
 
 def test_encode_pipeline_matches_opencv_chain():
-    # the whole chain against cv2 (resize -> gray -> GaussianBlur 8-bit -> compare), frames of
-    # the synthetic recipe
-    fr = sp_inputs.bgr_frames(11, 0, 2, 540, 960)
+    # the whole chain against cv2 (resize -> gray -> adaptiveThreshold), frames of the
+    # synthetic recipe, zero differing pixels
+    fr = sp_inputs.bgr_frames(11, 0, 4, 540, 960)
     out = E.encode_bgr(fr, 240, 134)
-    for f in range(2):
+    for f in range(4):
         g = cv2.cvtColor(cv2.resize(fr[f], (240, 134), interpolation=cv2.INTER_AREA), cv2.COLOR_BGR2GRAY)
-        m = cv2.GaussianBlur(g, (11, 11), 0, borderType=cv2.BORDER_REPLICATE)
-        want = np.where(g.astype(int) - m.astype(int) > -2, 255, 0).astype(np.uint8)
+        want = cv2.adaptiveThreshold(g, 255, cv2.ADAPTIVE_THRESH_GAUSSIAN_C, cv2.THRESH_BINARY, 11, 2)
         assert np.array_equal(out[f], want)
     assert 0.2 < (out == 255).mean() < 0.95
