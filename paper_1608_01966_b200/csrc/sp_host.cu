@@ -386,6 +386,12 @@ struct sp_handle {
     // (crossover measured at r ~ 80-100 for C = 1024: scripts/local_general_timing.py)
     uint32_t wm_min_radius = 96;
     uint32_t wm_min_radius_pi = 256;  // the same for the per-input k_inhibit (CTA wavelet)
+    // local inhibition (batched kernels): candidate pruning from this radius on, when the
+    // candidates fit the warp's scratch (else the wavelet / comparator).  Set at create from the
+    // expected candidate count ~ k*C/(2r) (scripts/local_topk_timing.py): it beats
+    // the 15-level per-column-boost wavelet / comparator below ~350 candidates and the <= 8-level
+    // uniform wavelet below ~130.
+    uint32_t cand_min_radius = 0, cand_min_radius_u = 0;
     uint32_t force_groups = 0;        // SP_GROUPS (tests): batched groups per call, cluster size 1
     // tensor-core patch kernel (NEXT-2, sp_patch_mma.cu): 0 clusters = not eligible
     uint8_t* d_conn = nullptr;        // conn u8 [C32][nbits]: 1 where a connected synapse sits
@@ -760,6 +766,8 @@ sp_status launch_batched_path(sp_handle* h, const uint8_t* frames, const uint32_
     p.radius_dev = h->d_radius;
     p.wm_min_radius = h->wm_min_radius;
     p.wm_umax = h->wm_umax;
+    p.cand_min_radius = h->cand_min_radius;
+    p.cand_min_radius_u = h->cand_min_radius_u;
     if (pl.tensor_cores) {
         if (h->conn_dirty) {
             e = sp::launch_build_conn(h->d_idx, h->d_perm, h->cfg.connected_threshold, g.C, g.C32, g.S, g.nbits,
@@ -1266,6 +1274,13 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
     if (const char* et = std::getenv("SP_THREADS")) h->batched_threads = std::atoi(et) == 1024 ? 1024u : 512u;
     if (const char* ew = std::getenv("SP_WM_MIN_RADIUS"))
         h->wm_min_radius = h->wm_min_radius_pi = static_cast<uint32_t>(std::atoi(ew));
+    {
+        const uint64_t kc = static_cast<uint64_t>(cfg->winners_set_size) * g.C;
+        h->cand_min_radius = static_cast<uint32_t>((kc + 699u) / 700u);
+        h->cand_min_radius_u = static_cast<uint32_t>((kc + 259u) / 260u);
+    }
+    if (const char* ec = std::getenv("SP_CAND_MIN_RADIUS"))  // experiments / tests (huge = off)
+        h->cand_min_radius = h->cand_min_radius_u = static_cast<uint32_t>(std::strtoul(ec, nullptr, 10));
     if (const char* eu = std::getenv("SP_WM_UMAX")) {  // experiments; the per-warp wavelet scratch holds
         const long u = std::atol(eu);                   // at most 15 levels + the lossy plane
         h->wm_umax = static_cast<uint32_t>(std::min<long>(std::max<long>(u, 1), 32766));

@@ -77,6 +77,8 @@ struct alignas(64) BatchedParams {
     uint32_t wm_min_radius;    // per-column boosts: wavelet top-k from this radius on (else comparator)
     uint32_t packed;           // frames are bit-planes uint32[inputs][Wn4] (sp_compute_packed)
     uint32_t wm_umax;          // per-column-boost wavelet: largest coarse key - 1 (levels = its bits)
+    uint32_t cand_min_radius;  // local inhibition, per-column boosts: candidate pruning from this radius on
+    uint32_t cand_min_radius_u;  // the same with a uniform boost (sp_select.cuh local_candidates)
 };
 
 // Tensor-core patch kernel (NEXT-2, sp_patch_mma.cu): raw counts of 128 tile slots per block

@@ -1161,6 +1161,175 @@ __device__ __forceinline__ bool global_general_wins(uint64_t N, uint64_t key, ui
     return Tu == 0 ? u > 0 : (u > Tu || (u == Tu && key >= T2));
 }
 
+// ---- local inhibition by candidate pruning (any boosts, one warp) -------------------------
+// Column c wins iff it is eligible and fewer than k columns of W(c)\{c} have a larger exact key
+// (R4-R7, R9).  Let v be monotone in the exact key (uniform boost: raw; per-column boosts: the
+// coarse key u of coarse_map, < 2^15), 0 for ineligible columns, and M_t = {d : v_d >= t},
+// t >= 1.  If every window W(c) with v_c < t holds >= k members of M_t, each such c has >= k
+// larger keys in its window and loses: only the candidates M_t can win, and only candidates
+// can beat a candidate (every other column of the window has a smaller v, hence a smaller
+// key).  The largest t passing a conservative test is searched bitwise: the columns of word j
+// share the window core I_j = [max(0, 32j+31-r), min(C-1, 32j+r)], which must hold >= k
+// members of M_t.  The candidates are compacted in position order with their exact keys; the
+// candidates of W(c) are then a contiguous range of that list, and c counts the larger keys in
+// it (stopping at k).  Lane j owns the column-words j and j + 32 (NW2 = 2 when ncw > 32): v of
+// its 32 columns sits two per register (columns i and i + 16), biased by 0x8000 per half, so
+// the word of M_t is 16 subtractions, shifts and LOP3s with no cross-lane traffic.  Cost per
+// input ~ (C/32) * bits(v) for the search plus ~ P * |range| / 32 compares per lane (P ~
+// C*k/r candidates).  Returns false without emitting anything when more candidates remain
+// than the scratch holds (small radii): the caller falls back to the wavelet / comparator.
+// KeyT: uint32_t (uniform: raw << L | (2^L-1-c), raw <= 1023, L <= 11) or uint64_t
+// (exact_key).  emit(cw, word) gets the SDR words in order (warp-uniform).  Scratch: [64] SDR
+// words, then keys and positions u16.
+template <int NW2, bool UNIFORM, typename KeyT, typename RowT, typename Emit>
+__device__ __forceinline__ bool local_candidates(const RowT* row, const uint32_t* bc, uint32_t C, uint32_t ncw,
+                                                 uint32_t radius, uint32_t k, uint32_t theta, uint32_t r_lo,
+                                                 uint32_t L, const CoarseMap& cm, uint8_t* scratch,
+                                                 uint32_t scratch_bytes, uint32_t lane, Emit emit) {
+    static_assert(NW2 == 1 || NW2 == 2, "at most 64 column-words");
+    const uint32_t full = 0xffffffffu;
+    auto value = [&](uint32_t c) -> uint32_t {
+        if (UNIFORM) {
+            const uint32_t x = row[c];
+            return x >= r_lo ? x : 0u;
+        } else {
+            bool lossy;
+            return coarse_u15(eligible_N(row[c], bc[c], theta), cm, lossy);
+        }
+    };
+    // vb[h][i] = (v(32j + i) | 0x8000) | (v(32j + i + 16) | 0x8000) << 16, j = lane + 32h
+    uint32_t vb[NW2][16];
+    uint32_t vmax = 0;
+#pragma unroll
+    for (int h = 0; h < NW2; ++h) {
+        const uint32_t j = lane + 32u * h;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const uint32_t a = j < ncw ? value(32u * j + i) : 0u;
+            const uint32_t b = j < ncw ? value(32u * j + i + 16u) : 0u;
+            vmax = max(vmax, max(a, b));
+            vb[h][i] = (a | (b << 16)) | 0x80008000u;
+        }
+    }
+    vmax = __reduce_max_sync(full, vmax);
+    uint32_t* sdr = reinterpret_cast<uint32_t*>(scratch);
+    if (vmax == 0u) {  // no eligible column
+        for (uint32_t cw = 0; cw < ncw; ++cw) emit(cw, 0u);
+        return true;
+    }
+    // M_t: lane j's words m[h] (natural bit order) and their exclusive prefix counts e[h]
+    uint32_t m[NW2], e[NW2], total;
+    auto masks = [&](uint32_t t) {
+        const uint32_t tt = t | (t << 16);  // v >= t  <=>  bit 15 of (v | 0x8000) - t is set
+#pragma unroll
+        for (int h = 0; h < NW2; ++h) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc |= ((vb[h][i] - tt) >> (15 - i)) & (0x00010001u << i);
+            m[h] = acc;
+        }
+        uint32_t p[NW2];
+#pragma unroll
+        for (int h = 0; h < NW2; ++h) p[h] = __popc(m[h]);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+            for (int h = 0; h < NW2; ++h) {
+                const uint32_t a = __shfl_up_sync(full, p[h], d);
+                if (lane >= static_cast<uint32_t>(d)) p[h] += a;
+            }
+        }
+        const uint32_t t0 = __shfl_sync(full, p[0], 31);
+        total = t0;
+        e[0] = p[0] - __popc(m[0]);
+        if (NW2 > 1) {
+            total += __shfl_sync(full, p[NW2 - 1], 31);
+            e[NW2 - 1] = t0 + p[NW2 - 1] - __popc(m[NW2 - 1]);
+        }
+    };
+    // #{d < x : d in M_t}, x in [0, C] (warp-uniform call, per-lane x)
+    auto cntlt = [&](uint32_t x) -> uint32_t {
+        const uint32_t w = x >> 5, src = w & 31u;
+        uint32_t ev = __shfl_sync(full, e[0], src), mv = __shfl_sync(full, m[0], src);
+        if (NW2 > 1) {
+            const uint32_t eb = __shfl_sync(full, e[NW2 - 1], src), mb = __shfl_sync(full, m[NW2 - 1], src);
+            if (w >= 32u) ev = eb, mv = mb;
+        }
+        return x >= C ? total : ev + __popc(mv & ((1u << (x & 31u)) - 1u));
+    };
+    auto core_ok = [&](uint32_t j) -> bool {  // the window core of word j holds >= k of M_t
+        const uint32_t lo = 32u * j + 31u >= radius ? 32u * j + 31u - radius : 0u;
+        const uint32_t hi1 = min(C, 32u * j + radius + 1u);
+        const uint32_t n = cntlt(hi1) - cntlt(lo);
+        return j >= ncw || (lo < hi1 && n >= k);
+    };
+    // bitwise search of the largest passing t over the top 10 bits of v (the low bits would only
+    // trim a few candidates more)
+    const int nb = 32 - __clz(vmax);
+    uint32_t t = 0;
+    for (int b = nb - 1; b >= max(0, nb - 10); --b) {
+        const uint32_t tt = t | (1u << b);
+        if (tt > vmax) continue;
+        masks(tt);
+        bool ok = core_ok(lane);
+        if (NW2 > 1) {
+            const bool ok1 = core_ok(lane + 32u);  // not short-circuited: core_ok shuffles
+            ok = ok && ok1;
+        }
+        if (__all_sync(full, ok)) t = tt;
+    }
+    t = max(t, 1u);
+    masks(t);
+    const uint32_t P = total;
+    constexpr uint32_t kHead = 64u * 4u;
+    const uint32_t cap = scratch_bytes > kHead ? (scratch_bytes - kHead) / (sizeof(KeyT) + 2u) : 0u;
+    if (P > cap) return false;
+    KeyT* skey = reinterpret_cast<KeyT*>(scratch + kHead);                              // [cap]
+    uint16_t* spos = reinterpret_cast<uint16_t*>(scratch + kHead + cap * sizeof(KeyT));  // [cap]
+    for (uint32_t w = lane; w < ncw; w += 32u) sdr[w] = 0u;
+    // compaction in position order, with the exact keys: lane j writes the candidates of its words
+#pragma unroll
+    for (int h = 0; h < NW2; ++h) {
+        uint32_t mm = m[h], at = e[h];
+        const uint32_t j = lane + 32u * h;
+        while (mm) {
+            const uint32_t c = 32u * j + (__ffs(mm) - 1u);
+            mm &= mm - 1u;
+            spos[at] = static_cast<uint16_t>(c);
+            if (UNIFORM) {
+                skey[at] = static_cast<KeyT>((static_cast<uint32_t>(row[c]) << L) | ((1u << L) - 1u - c));
+            } else {
+                uint64_t N;
+                skey[at] = static_cast<KeyT>(exact_key(row[c], bc[c], theta, c, L, N));
+            }
+            ++at;
+        }
+    }
+    __syncwarp();
+    // beats of each candidate among the candidates of its window (a contiguous range)
+    for (uint32_t i0 = 0; i0 < P; i0 += 32u) {
+        const uint32_t i = i0 + lane;
+        const bool has = i < P;
+        const uint32_t c = has ? spos[i] : 0u;
+        const uint32_t a = cntlt(c >= radius ? c - radius : 0u);
+        const uint32_t b = cntlt(min(C, c + radius + 1u));
+        if (has) {
+            const KeyT key = skey[i];
+            uint32_t beats = 0;
+            uint32_t j = a;
+            for (; j + 4u <= b && beats < k; j += 4u)
+                beats += (skey[j] > key ? 1u : 0u) + (skey[j + 1u] > key ? 1u : 0u) +
+                         (skey[j + 2u] > key ? 1u : 0u) + (skey[j + 3u] > key ? 1u : 0u);
+            for (; j < b && beats < k; ++j) beats += skey[j] > key ? 1u : 0u;
+            if (beats < k) atomicOr(&sdr[c >> 5], 1u << (c & 31u));
+        }
+    }
+    __syncwarp();
+    for (uint32_t cw = 0; cw < ncw; ++cw) emit(cw, sdr[cw]);
+    __syncwarp();  // the scratch is reused by the caller's next input
+    return true;
+}
+
 // bits needed for raw values 0..S
 __device__ __forceinline__ uint32_t raw_bits(uint32_t S) { return 32u - __clz(S); }
 

@@ -128,8 +128,6 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
                 xmn = mn;
                 Bo = mn <= mx ? 32u - __clz(mx - mn + 1u) : 1u;
             };
-            uint32_t xmn, B;
-            range_of(row, xmn, B);
             // per-warp scratch slots sized for the largest B (8), so the warps' regions do not
             // depend on their inputs' ranges; a warp's comparator fallback uses its own slot too.
             // With room in the idle ring + windows (`big`), a slot holds two wavelets and the warp
@@ -137,6 +135,29 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             const bool pairs = !narrow && K == 1u && slot2 * NW <= big_bytes;
             const bool slotted = pairs || narrow || slot1 * NW <= p.region_bytes;
             uint8_t* wslot = pairs ? big + wi * slot2 : narrow ? big + wi * slot1 : region + wi * slot1;
+            if (radius >= p.cand_min_radius_u && slotted) {
+                // candidate pruning (sp_select.cuh): O(C k / r) per input
+                constexpr int NW2 = CPT * NW > 32 ? 2 : 1;
+                uint32_t total = 0, myword = 0;
+                const CoarseMap cm0{0ull, 0u};
+                if (local_candidates<NW2, true, uint32_t>(row, s_bc, p.C, p.ncw, radius, p.k, theta, r_lo, L, cm0,
+                                                         wslot, pairs ? slot2 : slot1, lane,
+                                                         [&](uint32_t cw, uint32_t word) {
+                                                             if ((cw & 31u) == lane) myword = word;
+                                                             total += __popc(word);
+                                                             if ((cw & 31u) == 31u || cw + 1u == p.ncw) {
+                                                                 const uint32_t w0 = cw & ~31u;
+                                                                 if (lane <= (cw & 31u))
+                                                                     p.sdr[static_cast<size_t>(gin) * p.ncw + w0 +
+                                                                           lane] = myword;
+                                                             }
+                                                         })) {
+                    if (lane == 0) p.counts[gin] = total;
+                    continue;
+                }
+            }
+            uint32_t xmn, B;
+            range_of(row, xmn, B);
             const uint32_t f2 = f + K * NW;
             if (pairs && f2 < gs && B <= 8u) {
                 const uint16_t* row2 = rawbuf + f2 * p.C32;
@@ -210,6 +231,35 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             continue;
         }
         const uint32_t gwb = (4u * p.C32 + 2u * 16u * (p.ncw + 2u) * 4u + 127u) & ~127u;  // <= 15 levels + lossy
+        // this warp's scratch slot for local inhibition with per-column boosts; every selector of
+        // the warp (candidates, wavelet, comparator fallback) uses it, so warps that take
+        // different selectors for different inputs never overlap
+        uint8_t* cs = nullptr;
+        uint32_t cbytes = 0;
+        if (gwb * NW <= big_bytes) cs = big + wi * gwb, cbytes = gwb;
+        else if (NW * 4096u <= p.region_bytes) cs = region + wi * 4096u, cbytes = 4096u;
+        if (radius > 0 && radius >= p.cand_min_radius) {
+            // local inhibition, per-column boosts: candidate pruning (sp_select.cuh), O(C k / r)
+            if (cs) {
+                constexpr int NW2 = CPT * NW > 32 ? 2 : 1;
+                const CoarseMap cm = coarse_map_warp(row, s_bc, theta, 0u, p.ncw, lane, p.wm_umax);
+                uint32_t total = 0, myword = 0;
+                if (local_candidates<NW2, false, uint64_t>(row, s_bc, p.C, p.ncw, radius, p.k, theta, 0u, L, cm, cs,
+                                                          cbytes, lane, [&](uint32_t cw, uint32_t word) {
+                                                              if ((cw & 31u) == lane) myword = word;
+                                                              total += __popc(word);
+                                                              if ((cw & 31u) == 31u || cw + 1u == p.ncw) {
+                                                                  const uint32_t w0 = cw & ~31u;
+                                                                  if (lane <= (cw & 31u))
+                                                                      p.sdr[static_cast<size_t>(gin) * p.ncw + w0 +
+                                                                            lane] = myword;
+                                                              }
+                                                          })) {
+                    if (lane == 0) p.counts[gin] = total;
+                    continue;
+                }
+            }
+        }
         if (radius > 0 && radius >= p.wm_min_radius && gwb * NW <= big_bytes) {
             // local inhibition, per-column boosts: wavelet matrix over the coarse keys + exact
             // lossy ties (sp_select.cuh), O(C log 2^15) per input
@@ -231,9 +281,9 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
             if (lane == 0) p.counts[gin] = total;
             continue;
         }
-        if (radius > 0 && p.ncw * 16u <= 1024u && NW <= 16u && NW * 4096u <= p.region_bytes) {
+        if (radius > 0 && p.ncw * 16u <= 1024u && cs) {
             // local inhibition, per-column boosts: coarse bit-sliced + exact ties
-            uint32_t* planes = reinterpret_cast<uint32_t*>(region) + wi * 1024u;  // [ncw][16]
+            uint32_t* planes = reinterpret_cast<uint32_t*>(cs);  // [ncw][16] (ncw * 64 <= 4096 bytes)
             const CoarseMap cm = coarse_map_warp(row, s_bc, theta, 0u, p.ncw, lane);
             build_coarse_planes15(row, s_bc, planes, p.ncw, theta, cm, 0u, 1u, lane);
             __syncwarp();

@@ -334,14 +334,18 @@ def near1_boosts(C, seed=11):
 
 
 @pytest.mark.parametrize("path", PATHS)
-@pytest.mark.parametrize("selector", ["wavelet", "comparator"])
+@pytest.mark.parametrize("selector", ["candidates", "wavelet", "comparator"])
 @pytest.mark.parametrize("radius", [1, 7, 80, 506, 1023, 1100])
 @pytest.mark.parametrize("boost_mode", ["seeded", "near1"])
 def test_local_general_boost_selectors(radius, boost_mode, selector, path, monkeypatch):
-    """Local inhibition with per-column boosts: the wavelet matrices over coarse keys (per warp
-    in the batched kernel, per CTA in the per-input k_inhibit; lossy ties re-decided exactly)
-    and the bit-sliced comparators (SP_WM_MIN_RADIUS forces one or the other), against the
-    oracle; r >= C - 1 is global inhibition (C9)."""
+    """Local inhibition with per-column boosts: candidate pruning (batched kernel), the wavelet
+    matrices over coarse keys (per warp in the batched kernel, per CTA in the per-input
+    k_inhibit; lossy ties re-decided exactly) and the bit-sliced comparators
+    (SP_CAND_MIN_RADIUS / SP_WM_MIN_RADIUS force one or the other), against the oracle;
+    r >= C - 1 is global inhibition (C9)."""
+    if selector == "candidates" and path != P.SP_PATH_BATCHED:
+        pytest.skip("candidate pruning runs in the batched kernels")
+    monkeypatch.setenv("SP_CAND_MIN_RADIUS", "0" if selector == "candidates" else "100000")
     monkeypatch.setenv("SP_WM_MIN_RADIUS", "0" if selector == "wavelet" else "100000")
     cfg = ocfg(input_width=96, input_height=64, num_columns=1000, synapses_per_column=64,
                min_overlap=2, winners_set_size=20, inhibition_radius=radius)
@@ -603,14 +607,16 @@ def test_inference_parity_full_groups(kw, boost_mode, record, monkeypatch):
 
 
 @pytest.mark.parametrize("record", [True, False])
-@pytest.mark.parametrize("radius", [0, 80, 506])
+@pytest.mark.parametrize("radius,selector", [(0, "-"), (80, "candidates"), (80, "wavelet"), (506, "candidates"),
+                                             (506, "wavelet")])
 @pytest.mark.parametrize("boost_mode", ["uniform1", "seeded"])
-def test_full_size_full_groups(radius, boost_mode, record, monkeypatch):
+def test_full_size_full_groups(radius, selector, boost_mode, record, monkeypatch):
     """BASELINE config 2/4 geometry (960x540, C 1024, S 256, theta 4, k 40) in groups of 23/22
-    inputs: global uniform (the headline's paired threshold search), local uniform r 80 / 506
-    (the paired local-uniform wavelet, never compared with the oracle in round 1), and the
-    per-column-boost selectors, each with recording on and off."""
+    inputs: global uniform (the headline's paired threshold search), local r 80 / 506 by
+    candidate pruning or by the wavelets (the paired local-uniform wavelet, never compared with
+    the oracle in round 1; the per-column-boost wavelet), each with recording on and off."""
     monkeypatch.setenv("SP_GROUPS", "2")
+    monkeypatch.setenv("SP_CAND_MIN_RADIUS", "0" if selector == "candidates" else "100000")
     cfg = headline_cfg(inhibition_radius=radius)
     state = with_boost(perturbed_state(cfg), boost_mode)
     frames = sp_inputs.frames(2002, 100, 45, 540, 960, rho=0.5)
@@ -639,3 +645,52 @@ def test_bench_launch_config_recording_off_equals_on():
         outs.append((sdr.clone(), counts.clone()))
         sp.close()
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("boost_mode", ["uniform1", "seeded", "near1"])
+@pytest.mark.parametrize("radius", [16, 24, 32, 40, 48, 64, 100, 200, 300, 506, 900, 1021])
+@pytest.mark.parametrize("k", [5, 40])
+def test_local_candidates_radius_sweep(radius, k, boost_mode, monkeypatch):
+    """Candidate pruning (sp_select.cuh local_candidates) over radii from the point where the
+    candidates overflow the warp's scratch (fallback to wavelet / comparator) to nearly global,
+    with uniform boosts (raw ties: many candidates share the threshold value), seeded and near-1
+    boosts (coarse-key ties, exact 64-bit keys decide); 45 inputs in 2 groups so warps run
+    several inputs; recording off (the timed configuration) and on, against the oracle."""
+    monkeypatch.setenv("SP_GROUPS", "2")
+    monkeypatch.setenv("SP_CAND_MIN_RADIUS", "0")
+    cfg = ocfg(input_width=96, input_height=64, num_columns=1024, synapses_per_column=64,
+               min_overlap=3, winners_set_size=k, inhibition_radius=radius)
+    idx, perm, boost = perturbed_state(cfg)
+    if boost_mode == "near1":
+        boost = near1_boosts(cfg.num_columns)
+    elif boost_mode == "uniform1":
+        boost = np.ones_like(boost)
+    state = (idx, perm, boost)
+    frames = sp_inputs.frames(79, 0, 45, cfg.input_height, cfg.input_width, rho=0.5)
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = [ora.step(x, False) for x in O.encode(frames, cfg)]
+    check_sdrs(results, *run_gpu_sdr(make_sp(cfg, state, P.SP_PATH_BATCHED, record=False), frames))
+    check_results(results, *run_gpu(make_sp(cfg, state, P.SP_PATH_BATCHED), frames))
+
+
+@pytest.mark.parametrize("radius,boost_mode", [(48, "near1"), (56, "seeded"), (64, "uniform1")])
+def test_local_candidates_fallback_mixing(radius, boost_mode, monkeypatch):
+    """Headline geometry at radii where the candidate count straddles the warp scratch's
+    capacity (per-column boosts: ~820 keys of 8 B), so within one CTA some warps run candidate
+    pruning and others fall back to the comparator for their next input: every selector of a
+    warp must use that warp's own scratch slot (a round-2 bug let a comparator fallback write
+    into a neighbour's candidate list).  Recording off and on, against the oracle."""
+    monkeypatch.setenv("SP_GROUPS", "2")
+    monkeypatch.setenv("SP_CAND_MIN_RADIUS", "0")
+    cfg = headline_cfg(inhibition_radius=radius)
+    idx, perm, boost = perturbed_state(cfg)
+    if boost_mode == "near1":
+        boost = near1_boosts(cfg.num_columns)
+    elif boost_mode == "uniform1":
+        boost = np.ones_like(boost)
+    state = (idx, perm, boost)
+    frames = sp_inputs.frames(2002, 200, 45, 540, 960, rho=0.5)
+    ora = O.SpatialPoolerOracle(cfg, state)
+    results = [ora.step(x, False) for x in O.encode(frames, cfg)]
+    check_sdrs(results, *run_gpu_sdr(make_sp(cfg, state, P.SP_PATH_BATCHED, max_inputs=64, record=False), frames))
+    check_results(results, *run_gpu(make_sp(cfg, state, P.SP_PATH_BATCHED, max_inputs=64), frames))
