@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-learn-full", action="store_true")
     ap.add_argument("--no-encoder", action="store_true")
+    ap.add_argument("--no-patch", action="store_true", help="skip the patch-mode leg (NEXT-2)")
+    ap.add_argument("--patch-frames", type=int, default=256)
+    ap.add_argument("--no-local", action="store_true", help="skip the full-learning inference leg")
     ap.add_argument("--encoder-frames", type=int, default=2048)
     ap.add_argument("--overlap-gather", action="store_true",
                     help="N > 1: all-gather of step i on NCCL's stream while step i+1 computes "
@@ -321,6 +324,7 @@ def main():
 
     # ---- a5: learning stream on rank 0 -> learned SP, broadcast to all ranks --------------
     learn = None
+    fl_state = None  # (state, adapted radius) of the full-learning run, for the local leg
     if rank == 0 and args.learn_frames > 0:
         lf = torch.empty((args.learn_frames, H, W), dtype=torch.uint8, device=dev)
         P.synth_frames(lf, 0, SEED_LEARN, 0.5)
@@ -355,6 +359,7 @@ def main():
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1)
             radius = spf.get_learning_state()[2]
+            fl_state = (spf.get_state(), radius)
             learn["full"] = {"frames": nl, "ms": ms, "us_per_frame": ms * 1e3 / nl,
                              "frames_per_s": nl / ms * 1e3, "kernel_launches": spf.kernel_launches() - l0,
                              "path": P.learn_path_name(spf.info()), "radius_after": radius,
@@ -573,6 +578,81 @@ def main():
                           "packed by sp_pack_frames outside the timed regions"}
         del planes, host_planes
 
+    # ---- inference with the full-learning SP (learned boosts, radius adapted 80 -> ~506):
+    # local inhibition with per-column boosts, the round-1 weakest kernel (candidate pruning) --
+    local_fl = None
+    if fl_state is not None and not args.no_local:
+        (fidx, fperm, fboost), fr = fl_state
+        spl = P.SpatialPooler(input_width=W, input_height=H, num_columns=C, synapses_per_column=S,
+                              min_overlap=THETA, winners_set_size=K_WIN, inhibition_radius=fr,
+                              seed=SEED_STATE, device=local, max_inputs=F)
+        spl.set_state(fidx, fperm, fboost)
+        lsdr = torch.empty((F, words), dtype=torch.int32, device=dev)
+        lcnt = torch.empty((F,), dtype=torch.int32, device=dev)
+        for _ in range(3):
+            spl.compute_into(frames, lsdr, lcnt)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            spl.compute_into(frames, lsdr, lcnt)
+        b.record(stream)
+        torch.cuda.synchronize()
+        lms = a.elapsed_time(b) / args.steps
+        local_fl = {"value": F / (lms / 1e3), "unit": UNIT, "ms_per_step": lms, "radius": fr,
+                    "boosted_columns": int((fboost > 1).sum()),
+                    "hbm_frac": round(F * ALGO_BYTES_PER_FRAME / (lms / 1e3) / 1e9 / measured_peak_hbm()[0], 4),
+                    "mean_winners": float(lcnt.float().mean()),
+                    "workload": "the step's frames through the full-learning SP (learned boosts, local "
+                                "inhibition at the adapted radius; sp_select.cuh candidate pruning)"}
+        spl.close()
+
+    # ---- NEXT-2 patch mode (BASELINE config 2 "tiled into patches"; R13): 32x30 tiles of the
+    # step's frames, 540 SP inputs per frame; the bit-sliced gather kernel (default, faster) and
+    # the tcgen05 kind::i8 GEMM kernel, each against its own roof --------------------------------
+    patch = None
+    if not args.no_patch and world == 1:
+        PF = min(F, args.patch_frames)
+        pf = frames[:PF]
+        patch = {"frames": PF, "tile": "32x30", "inputs_per_frame": 540, "kernels": {}}
+        i8_peak = 2.0 * json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"] \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 4500.0
+        outs = {}
+        for name, flags in (("gather", P.SP_FLAG_PATCH_GATHER), ("tcgen05", 0)):
+            spp = P.SpatialPooler(input_width=W, input_height=H, patch_width=32, patch_height=30,
+                                  num_columns=C, synapses_per_column=S, min_overlap=THETA,
+                                  winners_set_size=K_WIN, seed=SEED_STATE, device=local,
+                                  max_inputs=PF * 540, flags=flags)
+            psd = torch.empty((PF * 540, words), dtype=torch.int32, device=dev)
+            pcn = torch.empty((PF * 540,), dtype=torch.int32, device=dev)
+            for _ in range(3):
+                spp.compute_into(pf, psd, pcn)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for _ in range(args.steps):
+                spp.compute_into(pf, psd, pcn)
+            b.record(stream)
+            torch.cuda.synchronize()
+            pms = a.elapsed_time(b) / args.steps
+            tc = bool(spp.info()["plan"]["tensor_cores"])
+            d = {"frames_per_s": PF / (pms / 1e3), "inputs_per_s": PF * 540 / (pms / 1e3), "ms": pms,
+                 "tensor_cores": tc}
+            if tc:
+                tops = 2.0 * C * 960 * PF * 540 / (pms / 1e3) / 1e12
+                d["tensor"] = {"tops": tops, "peak_tops": i8_peak, "frac": tops / i8_peak,
+                               "note": "dense 0/1 GEMM [C x 960] . [960 x tiles] (kind::i8, s32 accumulators); "
+                                       "peak = measured bf16 dense x 2 (nominal i8:bf16 ratio)"}
+            else:
+                d["synapse_tests_per_s"] = float(C) * S * PF * 540 / (pms / 1e3)
+            patch["kernels"][name] = d
+            outs[name] = (psd.clone(), pcn.clone())
+            spp.close()
+        patch["same_winners"] = bool(torch.equal(outs["gather"][0], outs["tcgen05"][0]) and
+                                     torch.equal(outs["gather"][1], outs["tcgen05"][1]))
+        best = max(patch["kernels"], key=lambda k: patch["kernels"][k]["frames_per_s"])
+        patch["value"], patch["unit"], patch["faster"] = patch["kernels"][best]["frames_per_s"], UNIT, best
+
     # ---- strong-scaling readiness (B = 4096 total over G GPUs): the
     # shard one GPU would own at G = 2, 4, 8, timed here; the implied ceiling on strong-scaling
     # efficiency is T(F) / (G * T(F/G)) before any gather cost ----------------------------------
@@ -640,7 +720,8 @@ def main():
             "hbm_frac": round(value / world * ALGO_BYTES_PER_FRAME / 1e9 / peak, 4),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "learn": learn, "histograms": histograms, "encoder": encoder,
-            "packed": packed, "strong_shards": strong_shards}
+            "packed": packed, "strong_shards": strong_shards, "local_full_learning": local_fl,
+            "patch": patch}
     print(json.dumps(line), flush=True)
     if use_dist:
         dist.destroy_process_group()
