@@ -485,6 +485,20 @@ def main():
         torch.cuda.synchronize()
         enc_ms = ea.elapsed_time(eb) / reps
         both_ms = eb.elapsed_time(ec) / reps
+        # the fused call: raw BGR -> SDRs, the binarised chunk held in a persisting-L2 window
+        fsdr = torch.empty((EF, sp2.sdr_words), dtype=torch.int32, device=dev)
+        fcnt = torch.empty((EF,), dtype=torch.int32, device=dev)
+        enc.encode_compute(sp2, bgr, fsdr, fcnt)
+        fused_same = bool(torch.equal(fsdr, sp2.winners()[0]))
+        sp2.compute(binf)
+        fused_same = fused_same and bool(torch.equal(fsdr, sp2.winners()[0]))
+        torch.cuda.synchronize()
+        ea.record(stream)
+        for _ in range(reps):
+            enc.encode_compute(sp2, bgr, fsdr, fcnt)
+        eb.record(stream)
+        torch.cuda.synchronize()
+        fused_ms = ea.elapsed_time(eb) / reps
         enc_bytes = EF * (H * W * 3 + 134 * 240)
         peak_hbm, _ = measured_peak_hbm()
         encoder = {"frames": EF, "src": f"{W}x{H} BGR", "dst": "240x134", "block_size": 11, "bias": 2.0,
@@ -492,6 +506,10 @@ def main():
                    "achieved_gbs": enc_bytes / (enc_ms / 1e3) / 1e9,
                    "hbm_frac": enc_bytes / (enc_ms / 1e3) / 1e9 / peak_hbm,
                    "encode_plus_sp_frames_per_s": EF / both_ms * 1e3,
+                   "encode_compute_frames_per_s": EF / fused_ms * 1e3,
+                   "encode_compute_same_winners": fused_same,
+                   "encode_compute_note": "sp_encode_compute: one call, binarised chunks in a persisting-L2 "
+                                          "window between the encoder and the SP (no HBM round trip)",
                    "sp": "Tab. 2 SP on the encoded frames (2048 columns, 128 synapses, k 40)",
                    "plan": {k: v for k, v in enc.info().items() if k != "kernel"}}
         enc.close()

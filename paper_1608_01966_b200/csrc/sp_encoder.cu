@@ -383,6 +383,12 @@ struct sp_encoder {
     uint32_t* d_u32 = nullptr;  // band_sy0 | band_n | yoff | ysy | xoff | xsx
     float* d_f32 = nullptr;     // ybeta | xalpha
     uint64_t launches = 0;
+    // sp_encode_compute: chunk of binarised frames kept in a persisting-L2 window between the
+    // encoder and the SP (never written back to HBM while it stays resident)
+    uint32_t chunk = 1024;
+    uint8_t* d_chunk = nullptr;
+    size_t l2_window = 0;       // bytes of the window (0: no persisting L2 on this device)
+    uint64_t fused_calls = 0;
 };
 
 namespace {
@@ -574,7 +580,73 @@ sp_status sp_encoder_destroy(sp_encoder* e) {
     cudaDeviceSynchronize();
     cudaFree(e->d_u32);
     cudaFree(e->d_f32);
+    if (e->d_chunk) cudaFree(e->d_chunk);
     delete e;
+    return SP_OK;
+}
+
+sp_status sp_encode_compute(sp_encoder* e, sp_handle* sp, const uint8_t* bgr_dev, uint32_t num_frames,
+                            uint32_t* sdr_dev, uint32_t* count_dev, void* cuda_stream) {
+    if (!e || !sp) return efail(SP_E_ARG, "encoder or SP handle is NULL");
+    uint32_t W = 0, H = 0, P = 0, words = 0;
+    int dev = 0;
+    if (sp::handle_frame_dims(sp, &W, &H, &P, &words, &dev) != SP_OK) return efail(SP_E_ARG, "SP handle");
+    if (W != e->p.W1 || H != e->p.H1)
+        return efail(SP_E_CONFIG, "the SP's input frame must be the encoder's output frame (dst_width x dst_height)");
+    if (dev != e->device) return efail(SP_E_ARG, "encoder and SP on different devices");
+    if (num_frames == 0) return SP_OK;
+    if (!bgr_dev || !sdr_dev || !count_dev) return efail(SP_E_ARG, "NULL buffer");
+    cudaSetDevice(e->device);
+    cudaStream_t s = static_cast<cudaStream_t>(cuda_stream);
+    const size_t fbytes = static_cast<size_t>(e->p.W1) * e->p.H1;
+    if (!e->d_chunk) {
+        if (const char* ec = std::getenv("SP_ENC_CHUNK")) e->chunk = std::max(1, std::atoi(ec));
+        cudaError_t err = cudaMalloc(&e->d_chunk, e->chunk * fbytes);
+        if (err != cudaSuccess) {
+            e->d_chunk = nullptr;
+            return efail(SP_E_OOM, cudaGetErrorString(err));
+        }
+        // persisting L2 set-aside for the chunk buffer (device-wide limit, raised only)
+        int max_persist = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, e->device);
+        const size_t want = std::min<size_t>(static_cast<size_t>(max_persist), e->chunk * fbytes);
+        size_t cur = 0;
+        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+        if (want > cur) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+        e->l2_window = std::min<size_t>(cur, e->chunk * fbytes);
+        (void)cudaGetLastError();
+    }
+    // the chunk buffer is the stream's access-policy window while the call runs: hits persist
+    cudaStreamAttrValue old_attr{}, attr{};
+    const bool windowed = e->l2_window > 0 &&
+                          cudaStreamGetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &old_attr) == cudaSuccess;
+    if (windowed) {
+        attr.accessPolicyWindow.base_ptr = e->d_chunk;
+        attr.accessPolicyWindow.num_bytes = e->chunk * fbytes;
+        attr.accessPolicyWindow.hitRatio =
+            std::min(1.0f, static_cast<float>(e->l2_window) / static_cast<float>(e->chunk * fbytes));
+        attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &attr);
+    }
+    (void)cudaGetLastError();
+    sp_status st = SP_OK;
+    for (uint32_t f0 = 0; f0 < num_frames && st == SP_OK; f0 += e->chunk) {
+        const uint32_t n = std::min(e->chunk, num_frames - f0);
+        st = sp_encode(e, bgr_dev + static_cast<size_t>(f0) * 3u * e->p.W0 * e->p.H0, n, e->d_chunk, cuda_stream);
+        if (st != SP_OK) break;
+        const size_t row = static_cast<size_t>(f0) * P;
+        st = sp_compute_into(sp, e->d_chunk, n, 0, sdr_dev + row * words, count_dev + row, cuda_stream);
+    }
+    if (windowed) {
+        cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &old_attr);
+        (void)cudaGetLastError();
+    }
+    if (st != SP_OK) return efail(st, sp_last_error());
+    // the winners of the whole call are the SP's "last results" (sp_winners, sp_histograms)
+    sp::handle_set_result(sp, sdr_dev, count_dev, static_cast<uint32_t>(static_cast<uint64_t>(num_frames) * P));
+    e->fused_calls++;
     return SP_OK;
 }
 

@@ -1111,7 +1111,20 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
 
 }  // namespace
 
+namespace sp {
+sp_status handle_frame_dims(const sp_handle* h, uint32_t* W, uint32_t* H, uint32_t* P, uint32_t* words,
+                            int* device) {
+    if (!h) return SP_E_ARG;
+    *W = h->cfg.input_width, *H = h->cfg.input_height, *P = h->g.P, *words = h->g.ncw, *device = h->device;
+    return SP_OK;
+}
+void handle_set_result(sp_handle* h, uint32_t* sdr, uint32_t* counts, uint32_t inputs) {
+    h->res_sdr = sdr, h->res_counts = counts, h->last_inputs = inputs, h->has_result = true;
+}
+}  // namespace sp
+
 extern "C" {
+
 
 const char* sp_last_error(void) { return g_err.c_str(); }
 

@@ -272,6 +272,11 @@ cudaError_t launch_refresh_ell(const uint32_t* idx, const float* perm, const uin
                                float tau, uint32_t C, uint32_t S, uint32_t Lw, uint16_t* ell,
                                cudaStream_t s);
 
+// handle accessors for the encoder's fused call (sp_encode_compute, sp_encoder.cu)
+sp_status handle_frame_dims(const sp_handle* h, uint32_t* W, uint32_t* H, uint32_t* P, uint32_t* words,
+                            int* device);
+void handle_set_result(sp_handle* h, uint32_t* sdr, uint32_t* counts, uint32_t inputs);
+
 inline uint32_t ceil_log2(uint32_t v) {
     uint32_t l = 0;
     while ((1ull << l) < v) ++l;

@@ -42,7 +42,7 @@ ABI_SYMBOLS = ("sp_config_default", "sp_create", "sp_destroy", "sp_compute", "sp
                "sp_get_learning_state", "sp_set_learning_state", "sp_histograms",
                "sp_compute_into", "sp_synth_frames", "sp_synth_bgr_frames", "sp_encoder_config_default",
                "sp_encoder_create", "sp_encoder_destroy", "sp_encode", "sp_encoder_get_info",
-               "sp_encoder_last_error", "sp_pack_frames", "sp_compute_packed", "sp_compute_packed_host")
+               "sp_encoder_last_error", "sp_encode_compute", "sp_pack_frames", "sp_compute_packed", "sp_compute_packed_host")
 
 
 class SpError(RuntimeError):
@@ -138,6 +138,7 @@ def lib() -> ctypes.CDLL:
         "sp_encoder_create": [P(SpEncoderConfig), P(vp)],
         "sp_encoder_destroy": [vp],
         "sp_encode": [vp, vp, u32, vp, vp],
+        "sp_encode_compute": [vp, vp, vp, u32, vp, vp, vp],
         "sp_encoder_get_info": [vp, P(SpEncoderInfo)],
     }
     for name, args in sig.items():
@@ -307,6 +308,30 @@ class Encoder:
         if st != SP_OK:
             raise SpError(st, lib().sp_encoder_last_error().decode())
         return out
+
+    def encode_compute(self, sp, bgr, sdr=None, counts=None, stream=None):
+        """Raw BGR video -> SDRs in one call (``sp_encode_compute``): ``bgr`` uint8 cuda
+        [F, H0, W0, 3] through the encoder and ``sp``'s inference, the binarised frames held in
+        a persisting-L2 chunk buffer between the two.  Returns (sdr int32 [F*P, words],
+        counts int32 [F*P])."""
+        import torch
+        _require(bgr, torch.uint8, self.device, name="bgr")
+        if bgr.dim() != 4 or tuple(bgr.shape[1:]) != self.src_shape:
+            raise SpError(SP_E_SHAPE, f"bgr must be [F, {self.src_shape}]")
+        n = bgr.shape[0] * sp.inputs_per_frame
+        if sdr is None:
+            sdr = torch.empty((n, sp.sdr_words), dtype=torch.int32, device=bgr.device)
+        if counts is None:
+            counts = torch.empty((n,), dtype=torch.int32, device=bgr.device)
+        _require(sdr, torch.int32, self.device, (n, sp.sdr_words), "sdr")
+        _require(counts, torch.int32, self.device, (n,), "counts")
+        st = lib().sp_encode_compute(self._h, sp._h, ctypes.c_void_p(bgr.data_ptr()), bgr.shape[0],
+                                     ctypes.c_void_p(sdr.data_ptr()), ctypes.c_void_p(counts.data_ptr()),
+                                     _stream_ptr(stream, bgr.device))
+        if st != SP_OK:
+            raise SpError(st, lib().sp_encoder_last_error().decode())
+        sp.last_num_inputs = n
+        return sdr, counts
 
     def info(self) -> dict:
         out = SpEncoderInfo()

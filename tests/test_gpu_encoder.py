@@ -82,3 +82,34 @@ def test_encoder_config_errors():
         with pytest.raises(P.SpError) as e:
             P.Encoder(**kw)
         assert e.value.status == P.SP_E_CONFIG
+
+
+@pytest.mark.parametrize("chunk", ["7", "1024"])
+def test_encode_compute_fused_call(chunk, monkeypatch):
+    """sp_encode_compute (raw BGR -> SDRs, binarised chunk in a persisting-L2 window): equal to
+    the oracle chain (encoder oracle -> SP oracle) on the first frames, and to sp_encode +
+    sp_compute on all frames, across chunk boundaries (7 frames per chunk: ragged last chunk)."""
+    monkeypatch.setenv("SP_ENC_CHUNK", chunk)
+    F = 23
+    bgr = sp_inputs.bgr_frames(91, 0, F, 540, 960)
+    cfg = ocfg(input_width=240, input_height=134, num_columns=2048, synapses_per_column=128,
+               min_overlap=8, winners_set_size=40, inhibition_radius=80)
+    enc = P.Encoder()
+    sp = P.SpatialPooler(**gpu_kwargs(cfg, max_inputs=64))
+    dbgr = torch.from_numpy(bgr).to(DEV)
+    sdr, counts = enc.encode_compute(sp, dbgr)
+    s2, c2 = sp.winners()
+    assert torch.equal(s2, sdr) and torch.equal(c2, counts)  # the SP's last results = the whole call
+    binf = enc.encode(dbgr)
+    sp.compute(binf)
+    ref_sdr, ref_counts = sp.winners()
+    assert torch.equal(sdr, ref_sdr) and torch.equal(counts, ref_counts)
+    ora = O.SpatialPoolerOracle(cfg, sp.get_state())
+    want = E.encode_bgr(bgr[:4], 240, 134)
+    got = sdr.cpu().numpy()
+    for f, x in enumerate(O.encode(want, cfg)):
+        r = ora.step(x, False)
+        assert np.array_equal(got[f], O.sdr_words(r.active).view(np.int32)), f"frame {f}"
+    with pytest.raises(P.SpError):  # the SP's input frame must be the encoder's output frame
+        enc.encode_compute(P.SpatialPooler(input_width=96, input_height=64, num_columns=128,
+                                           synapses_per_column=16, min_overlap=2, winners_set_size=8), dbgr)
