@@ -46,6 +46,9 @@ typedef struct sp_encoder_info {
     uint32_t xfast;          /* 1 if the x table is an exact 4:1 average (vectorised path) */
     uint64_t kernel_launches;
     float kernel[16];        /* the float32 Gaussian kernel (block_size weights) */
+    uint32_t chunk_frames;   /* sp_encode_compute: frames per chunk */
+    uint32_t l2_window_set;  /* 1 if the chunk buffer is a persisting-L2 access-policy window */
+    uint64_t l2_window_bytes; /* persisting-L2 set-aside granted for it (0 before the first call) */
 } sp_encoder_info;
 
 /* Defaults: 960x540 -> 240x134, block 11, bias 2, device 0.  SP_E_ARG for NULL. */

@@ -389,6 +389,9 @@ struct sp_encoder {
     uint8_t* d_chunk = nullptr;
     size_t l2_window = 0;       // bytes of the window (0: no persisting L2 on this device)
     uint64_t fused_calls = 0;
+    cudaStream_t fstream = nullptr;  // internal stream carrying the access-policy window
+    cudaEvent_t fev[2] = {nullptr, nullptr};
+    bool window_set = false;    // the stream attribute was accepted
 };
 
 namespace {
@@ -581,6 +584,9 @@ sp_status sp_encoder_destroy(sp_encoder* e) {
     cudaFree(e->d_u32);
     cudaFree(e->d_f32);
     if (e->d_chunk) cudaFree(e->d_chunk);
+    if (e->fstream) cudaStreamDestroy(e->fstream);
+    for (cudaEvent_t ev : e->fev)
+        if (ev) cudaEventDestroy(ev);
     delete e;
     return SP_OK;
 }
@@ -615,35 +621,42 @@ sp_status sp_encode_compute(sp_encoder* e, sp_handle* sp, const uint8_t* bgr_dev
         if (want > cur) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
         cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
         e->l2_window = std::min<size_t>(cur, e->chunk * fbytes);
+        // an internal stream whose access-policy window is the chunk buffer (the caller's stream,
+        // possibly the legacy default stream, is left untouched); ordered by events
+        cudaError_t es = cudaStreamCreateWithFlags(&e->fstream, cudaStreamNonBlocking);
+        if (es == cudaSuccess) es = cudaEventCreateWithFlags(&e->fev[0], cudaEventDisableTiming);
+        if (es == cudaSuccess) es = cudaEventCreateWithFlags(&e->fev[1], cudaEventDisableTiming);
+        if (es != cudaSuccess) return efail(SP_E_CUDA, cudaGetErrorString(es));
+        if (e->l2_window > 0) {
+            cudaStreamAttrValue attr{};
+            attr.accessPolicyWindow.base_ptr = e->d_chunk;
+            attr.accessPolicyWindow.num_bytes = e->chunk * fbytes;
+            attr.accessPolicyWindow.hitRatio =
+                std::min(1.0f, static_cast<float>(e->l2_window) / static_cast<float>(e->chunk * fbytes));
+            attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            e->window_set = cudaStreamSetAttribute(e->fstream, cudaStreamAttributeAccessPolicyWindow, &attr) ==
+                            cudaSuccess;
+        }
         (void)cudaGetLastError();
     }
-    // the chunk buffer is the stream's access-policy window while the call runs: hits persist
-    cudaStreamAttrValue old_attr{}, attr{};
-    const bool windowed = e->l2_window > 0 &&
-                          cudaStreamGetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &old_attr) == cudaSuccess;
-    if (windowed) {
-        attr.accessPolicyWindow.base_ptr = e->d_chunk;
-        attr.accessPolicyWindow.num_bytes = e->chunk * fbytes;
-        attr.accessPolicyWindow.hitRatio =
-            std::min(1.0f, static_cast<float>(e->l2_window) / static_cast<float>(e->chunk * fbytes));
-        attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &attr);
-    }
-    (void)cudaGetLastError();
+    cudaStream_t fs = e->fstream;
+    cudaError_t ee = cudaEventRecord(e->fev[0], s);
+    if (ee == cudaSuccess) ee = cudaStreamWaitEvent(fs, e->fev[0], 0);
+    if (ee != cudaSuccess) return efail(SP_E_CUDA, cudaGetErrorString(ee));
     sp_status st = SP_OK;
     for (uint32_t f0 = 0; f0 < num_frames && st == SP_OK; f0 += e->chunk) {
         const uint32_t n = std::min(e->chunk, num_frames - f0);
-        st = sp_encode(e, bgr_dev + static_cast<size_t>(f0) * 3u * e->p.W0 * e->p.H0, n, e->d_chunk, cuda_stream);
+        st = sp_encode(e, bgr_dev + static_cast<size_t>(f0) * 3u * e->p.W0 * e->p.H0, n, e->d_chunk, fs);
         if (st != SP_OK) break;
         const size_t row = static_cast<size_t>(f0) * P;
-        st = sp_compute_into(sp, e->d_chunk, n, 0, sdr_dev + row * words, count_dev + row, cuda_stream);
+        st = sp_compute_into(sp, e->d_chunk, n, 0, sdr_dev + row * words, count_dev + row, fs);
     }
-    if (windowed) {
-        cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &old_attr);
-        (void)cudaGetLastError();
-    }
+    // the caller's stream continues after the last chunk
+    ee = cudaEventRecord(e->fev[1], fs);
+    if (ee == cudaSuccess) ee = cudaStreamWaitEvent(s, e->fev[1], 0);
     if (st != SP_OK) return efail(st, sp_last_error());
+    if (ee != cudaSuccess) return efail(SP_E_CUDA, cudaGetErrorString(ee));
     // the winners of the whole call are the SP's "last results" (sp_winners, sp_histograms)
     sp::handle_set_result(sp, sdr_dev, count_dev, static_cast<uint32_t>(static_cast<uint64_t>(num_frames) * P));
     e->fused_calls++;
@@ -679,6 +692,9 @@ sp_status sp_encoder_get_info(sp_encoder* e, sp_encoder_info* out) {
     out->xfast = e->p.xfast;
     out->kernel_launches = e->launches;
     for (int i = 0; i < 16; ++i) out->kernel[i] = i < e->p.K ? e->p.kw[i] : 0.0f;
+    out->chunk_frames = e->chunk;
+    out->l2_window_set = e->window_set ? 1u : 0u;
+    out->l2_window_bytes = e->l2_window;
     return SP_OK;
 }
 

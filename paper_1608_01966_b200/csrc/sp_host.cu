@@ -408,6 +408,9 @@ struct sp_handle {
     uint32_t* d_synT = nullptr;  // [C32][S] idx | connected << 31
     uint32_t* d_gbar = nullptr;  // grid barrier counter
     uint32_t grid_G = 0, grid_smem = 0, grid_own = 0, grid_win = 0, grid_ccols = 0, grid_stages = 0;
+    // grid-resident learning with the full learning step (sp_learn_grid_full.cu)
+    uint32_t gridf_G = 0, gridf_smem = 0, gridf_own = 0, gridf_ccols = 0, gridf_stages = 0, gridf_cap = 0;
+    unsigned long long* d_span_part = nullptr;  // [2][gridf_G]
     bool grid_dbl = false;
     bool synT_dirty = true;      // d_synT must be rebuilt from idx/perm before grid learning
     // full learning (NEXT-1; DESIGN R17-R21)
@@ -467,7 +470,7 @@ void release(sp_handle* h) {
                     h->d_raw,  h->d_sdr,     h->d_counts,  h->d_raw_rec, h->d_boosted_rec,
                     h->d_stage[0], h->d_stage[1], h->d_synT,  h->d_gbar, h->d_adc, h->d_odc,
                     h->d_span, h->d_radius, h->d_fscratch, h->d_hist_off, h->d_hist_counts,
-                    h->d_bits_all, h->d_conn};
+                    h->d_bits_all, h->d_conn, h->d_span_part};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
@@ -884,9 +887,13 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
     const bool want_grid = learn && !full && h->grid_G && h->cfg.force_path != SP_PATH_PER_INPUT &&
                            (lp ? std::strcmp(lp, "grid") == 0
                                : ((h->cfg.flags & SP_FLAG_LEARN_GRID) != 0 || h->learn_Q == 0));
+    // full learning on the grid: when the cluster kernel cannot hold the table (config 5), or asked
+    const bool want_grid_full = learn && full && h->gridf_G && h->cfg.force_path != SP_PATH_PER_INPUT &&
+                                (lp ? std::strcmp(lp, "grid") == 0
+                                    : ((h->cfg.flags & SP_FLAG_LEARN_GRID) != 0 || h->learn_Q == 0));
     const bool want_cluster = learn && h->learn_Q && h->cfg.force_path != SP_PATH_PER_INPUT && !want_grid &&
-                              !(lp && std::strcmp(lp, "input") == 0);
-    if (want_grid) {
+                              !want_grid_full && !(lp && std::strcmp(lp, "input") == 0);
+    if (want_grid || want_grid_full) {
         // the whole sequential stream in one cooperative launch over the SMs
         if (h->synT_dirty) {
             e = sp::launch_build_synT(h->d_idx, h->d_perm, h->cfg.connected_threshold, g.C, g.C32, g.S,
@@ -900,13 +907,19 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         q.first_input = row0;
         q.num_inputs = n;
         q.g = g;
-        q.G = h->grid_G;
+        q.G = want_grid_full ? h->gridf_G : h->grid_G;
         q.Wn = h->Wn;
-        q.own_words = h->grid_own;
+        q.own_words = want_grid_full ? h->gridf_own : h->grid_own;
         q.win_words = h->grid_win;
-        q.ccols = h->grid_ccols;
-        q.stages = h->grid_stages;
-        q.dbl_bits = h->grid_dbl ? 1u : 0u;
+        q.ccols = want_grid_full ? h->gridf_ccols : h->grid_ccols;
+        q.stages = want_grid_full ? h->gridf_stages : h->grid_stages;
+        q.dbl_bits = h->grid_dbl && !want_grid_full ? 1u : 0u;
+        if (want_grid_full) {
+            q.fl = full_learn_params(h);
+            q.span_part = h->d_span_part;
+            q.cand_cap = h->gridf_cap;
+            q.vsh = sp::bits_for(g.S) + 27u > 16u ? sp::bits_for(g.S) + 27u - 16u : 0u;  // N < 2^(bits(S)+27)
+        }
         q.min_overlap = h->cfg.min_overlap;
         q.k = h->cfg.winners_set_size;
         q.radius = h->cfg.inhibition_radius;
@@ -929,7 +942,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         q.trace = h->d_trace;
         // bit-planes prepacked per chunk by k_pack (as for the cluster kernel)
         const uint32_t Wn4 = (h->Wn + 3u) / 4u * 4u;
-        const bool prepack = !std::getenv("SP_NO_PREPACK");
+        const bool prepack = want_grid_full || !std::getenv("SP_NO_PREPACK");
         const uint32_t fpc = prepack ? std::max<uint32_t>(1u, kPrepackInputs / g.P) : n_frames;
         if (prepack) {
             sp_status st = ensure_prepack_scratch(h, fpc, n_frames, Wn4);
@@ -947,7 +960,8 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
                 qc.bits_g = h->d_bits_all;
                 qc.prepacked = 1u;
             }
-            e = sp::launch_learn_grid(qc, h->grid_smem, s);
+            e = want_grid_full ? sp::launch_learn_grid_full(qc, h->gridf_smem, s)
+                               : sp::launch_learn_grid(qc, h->grid_smem, s);
             h->launches++;
             if (e != cudaSuccess) return cuda_fail(e, "grid learning launch");
         }
@@ -1002,7 +1016,7 @@ sp_status compute_impl(sp_handle* h, const uint8_t* frames, uint32_t n_frames, i
         // HBM-bound pass), and the cluster kernel only bulk-loads them (no packing on the
         // sequential critical path).  Chunks bound the scratch; the state carries over.
         const uint32_t Wn4 = (h->Wn + 3u) / 4u * 4u;
-        const bool prepack = !std::getenv("SP_NO_PREPACK");
+        const bool prepack = want_grid_full || !std::getenv("SP_NO_PREPACK");
         const uint32_t fpc = prepack ? std::max<uint32_t>(1u, kPrepackInputs / g.P) : n_frames;
         if (prepack) {
             sp_status st = ensure_prepack_scratch(h, fpc, n_frames, Wn4);
@@ -1281,6 +1295,21 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
                 h->grid_stages = st;
             }
     }
+    // the full-learning grid kernel (radius adaptation needs every window size up to C): one
+    // bit-plane buffer, the whole raw row and a candidate list in shared memory
+    if (coop && (cfg->flags & SP_FLAG_FULL_LEARNING) && h->g.S % 4u == 0 &&
+        sp::configure_learn_grid_full(h->max_smem) == cudaSuccess) {
+        const uint32_t G = std::min<uint32_t>(static_cast<uint32_t>(h->sm_count), h->g.ncw);
+        const uint32_t cap = 2048u;
+        for (uint32_t st = 8; st >= 2 && !h->gridf_G; --st) {
+            const uint32_t smem = sp::learn_grid_full_smem(h->g, G, st, cap, &h->gridf_own, &h->gridf_ccols);
+            if (!smem || static_cast<int>(smem) > h->max_smem - 2048) continue;
+            int n = 0;
+            sp::learn_grid_full_max_ctas(smem, &n);
+            if (n < static_cast<int>(G)) continue;
+            h->gridf_G = G, h->gridf_smem = smem, h->gridf_stages = st, h->gridf_cap = cap;
+        }
+    }
     if (const char* eg = std::getenv("SP_GROUPS"))
         h->force_groups = static_cast<uint32_t>(std::max(0, std::atoi(eg)));
     if (std::getenv("SP_TRACE")) cudaMalloc(&h->d_trace, 4096u * 6u * sizeof(uint64_t));
@@ -1314,10 +1343,11 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
     if (e == cudaSuccess) e = dalloc(&h->d_raw, static_cast<size_t>(h->sub_inputs) * g.C32);
     if (e == cudaSuccess) e = dalloc(&h->d_sdr, cap * g.ncw);
     if (e == cudaSuccess) e = dalloc(&h->d_counts, cap);
-    if (e == cudaSuccess && h->grid_G) {
+    if (e == cudaSuccess && (h->grid_G || h->gridf_G)) {
         e = dalloc(&h->d_synT, static_cast<size_t>(g.C32) * g.S);
         if (e == cudaSuccess) e = dalloc(&h->d_gbar, 1);
     }
+    if (e == cudaSuccess && h->gridf_G) e = dalloc(&h->d_span_part, 2u * h->gridf_G);
     if (e == cudaSuccess) e = dalloc(&h->d_adc, g.C32);
     if (e == cudaSuccess) e = dalloc(&h->d_odc, g.C32);
     if (e == cudaSuccess) e = dalloc(&h->d_span, g.C32);
@@ -1731,7 +1761,7 @@ sp_status sp_get_info(sp_handle* h, sp_info* out) {
     out->max_smem_optin = h->max_smem;
     out->learn_cluster = h->learn_Q;
     out->last_learn_cluster = h->last_learn_cluster ? 1u : 0u;
-    out->learn_grid_ctas = h->grid_G;
+    out->learn_grid_ctas = (h->cfg.flags & SP_FLAG_FULL_LEARNING) ? h->gridf_G : h->grid_G;
     out->last_learn_path = h->last_learn_path;
     return SP_OK;
 }

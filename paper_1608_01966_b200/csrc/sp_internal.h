@@ -214,6 +214,11 @@ struct LearnGridParams {
     float* boosted_out;        // nullable
     uint32_t dbg;              // development switches (see LearnParams)
     uint64_t* trace;           // nullable [6] summed phase times of CTA 0 (development aid)
+    // full-learning grid kernel (sp_learn_grid_full.cu)
+    FullLearn fl;              // duty cycles, boosts, spans, radius, window-maximum scratch
+    unsigned long long* span_part;  // [2][G] per-CTA connected-span sums, by input parity
+    uint32_t cand_cap;         // candidate list capacity (shared memory)
+    uint32_t vsh;              // selection value v = N >> vsh (< 2^16)
 };
 
 // grid learning (sp_learn_grid.cu)
@@ -222,6 +227,13 @@ uint32_t learn_grid_smem(const Geometry& g, uint32_t radius, uint32_t G, bool db
 cudaError_t configure_learn_grid(int max_smem);
 cudaError_t learn_grid_max_ctas(uint32_t smem, int* n);
 cudaError_t launch_learn_grid(const LearnGridParams& p, uint32_t smem, cudaStream_t s);
+// grid learning with the full learning step (sp_learn_grid_full.cu)
+uint32_t learn_grid_full_smem(const Geometry& g, uint32_t G, uint32_t stages, uint32_t cap, uint32_t* own_words,
+                              uint32_t* ccols);
+cudaError_t configure_learn_grid_full(int max_smem);
+cudaError_t learn_grid_full_max_ctas(uint32_t smem, int* n);
+cudaError_t launch_learn_grid_full(const LearnGridParams& p, uint32_t smem, cudaStream_t s);
+uint32_t learn_grid_chunk_cols(uint32_t S);
 cudaError_t launch_build_synT(const uint32_t* idx, const float* perm, float tau, uint32_t C, uint32_t C32,
                               uint32_t S, uint32_t* synT, cudaStream_t s);
 

@@ -87,7 +87,9 @@ class SpEncoderConfig(ctypes.Structure):
 class SpEncoderInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint32) for n in ("band_rows", "bands", "stages", "stage_bytes", "smem_bytes",
                                                "ctas_per_sm", "xfast")] + \
-               [("kernel_launches", ctypes.c_uint64), ("kernel", ctypes.c_float * 16)]
+               [("kernel_launches", ctypes.c_uint64), ("kernel", ctypes.c_float * 16),
+                ("chunk_frames", ctypes.c_uint32), ("l2_window_set", ctypes.c_uint32),
+                ("l2_window_bytes", ctypes.c_uint64)]
 
 
 class SpInfo(ctypes.Structure):

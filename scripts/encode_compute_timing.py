@@ -54,7 +54,9 @@ def main():
         b.record()
         torch.cuda.synchronize()
         ms = a.elapsed_time(b) / reps
+        inf = enc.info()
         print(json.dumps({"mode": "encode_compute", "chunk": chunk, "frames": F, "ms": round(ms, 4),
+                          "l2_window_set": inf["l2_window_set"], "l2_window_bytes": inf["l2_window_bytes"],
                           "frames_per_s": round(F / ms * 1e3), "same_winners": bool(torch.equal(sdr, ref))}),
               flush=True)
         enc.close()

@@ -18,11 +18,11 @@ pytestmark = pytest.mark.gpu
 import paper_1608_01966_b200 as P  # noqa: E402
 
 DEV = torch.device("cuda", 0)
-LEARN_PATHS = ["cluster", "input"]
+LEARN_PATHS = ["cluster", "grid", "input"]
 
 
 def make_sp(cfg, state=None, path="cluster", max_inputs=256):
-    flags = P.SP_FLAG_RECORD_OVERLAPS | P.SP_FLAG_FULL_LEARNING
+    flags = P.SP_FLAG_RECORD_OVERLAPS | P.SP_FLAG_FULL_LEARNING | (P.SP_FLAG_LEARN_GRID if path == "grid" else 0)
     force = P.SP_PATH_PER_INPUT if path == "input" else P.SP_PATH_AUTO
     sp = P.SpatialPooler(**gpu_kwargs(cfg, force_path=force, max_inputs=max_inputs, flags=flags,
                                       duty_cycle_period=cfg.duty_cycle_period,
@@ -60,8 +60,12 @@ def check_inputs(results, sdr, counts, raw, boosted):
 
 
 def check_path(sp, path):
+    """the learning call ran on the requested kernel, or on the documented fallback (grid ->
+    cluster -> per-input kernels when a resident kernel is not eligible)"""
     info = sp.info()
-    if path == "input" or not info["learn_cluster"]:
+    if path == "grid" and info["learn_grid_ctas"]:
+        assert info["last_learn_path"] == P.SP_LEARN_GRID, info
+    elif path == "input" or not info["learn_cluster"]:
         assert info["last_learn_path"] == P.SP_LEARN_PER_INPUT, info
     else:
         assert info["last_learn_path"] == P.SP_LEARN_CLUSTER, info
@@ -257,4 +261,27 @@ def test_hand_worked_full_learning_cases(case, path):
     sp = make_sp(cfg, state, path)
     check_inputs(want, *run(sp, frames, True))
     check_path(sp, path)
+    check_state(sp, ora)
+
+
+@pytest.mark.parametrize("radius", [80, 0])
+def test_full_learning_config5_grid(radius):
+    """BASELINE config 5 geometry (16384 columns, 512 synapses, theta 8, k 40, 960x540) with full
+    learning on the grid-resident kernel (sp_learn_grid_full.cu: two grid barriers per input,
+    CTA-level candidate selection, duty tables through global memory): 8 sequential inputs from
+    seeded duty cycles (boosts and bumps trigger, the radius adapts from 80), then the state,
+    against the oracle."""
+    cfg = ocfg(full_learning=True, input_width=960, input_height=540, num_columns=16384,
+               synapses_per_column=512, min_overlap=8, winners_set_size=40, inhibition_radius=radius,
+               duty_cycle_period=1000)
+    state = perturbed_state(cfg)
+    frames = sp_inputs.frames(1001, 0, 8, 540, 960, rho=0.5)
+    ora = O.SpatialPoolerOracle(cfg, state)
+    adc, odc = seeded_duty(31, cfg.num_columns), seeded_duty(32, cfg.num_columns)
+    ora.active_duty, ora.overlap_duty = adc.copy(), odc.copy()
+    results = ora.compute(frames, learning=True)
+    sp = make_sp(cfg, state, "grid", max_inputs=16)
+    sp.set_learning_state(adc, odc, cfg.inhibition_radius)
+    check_inputs(results, *run(sp, frames, True))
+    assert sp.info()["last_learn_path"] == P.SP_LEARN_GRID
     check_state(sp, ora)
