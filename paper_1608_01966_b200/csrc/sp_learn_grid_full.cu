@@ -111,8 +111,8 @@ __global__ void __launch_bounds__(kGfThreads, 1)
     uint32_t* s_ring = s_bits + Wn4;                                              // [stages][chunk]
     uint32_t* s_craw = s_ring + static_cast<size_t>(stages) * chunk_words;        // [own cols]
     uint32_t* s_sdr = s_craw + p.own_words * 32u;                                 // [own words (+1)]
-    uint32_t* s_oc = s_sdr + (p.own_words + 1u) / 2u * 2u;                        // [own cols] owned candidates
-    uint64_t* s_key = reinterpret_cast<uint64_t*>(s_oc + (p.own_words * 32u + 1u) / 2u * 2u);  // [cap]
+    uint32_t* s_oc = s_sdr + (p.own_words + 3u) / 4u * 4u;                        // [own cols] owned candidates
+    uint64_t* s_key = reinterpret_cast<uint64_t*>(s_oc + p.own_words * 32u);      // [cap] (16-byte aligned)
     uint16_t* s_rw = reinterpret_cast<uint16_t*>(s_key + cap);                    // [C32]
     uint16_t* s_pos = s_rw + C32;                                                 // [cap]
     float* preA = fl.scratch;
@@ -237,50 +237,49 @@ __global__ void __launch_bounds__(kGfThreads, 1)
         const uint32_t ulo = c0 >= Re ? c0 - Re : 0u, uhi = min(C - 1u, c1 - 1u + Re);  // union window
         const uint32_t klo = c1 - 1u >= Re ? c1 - 1u - Re : 0u, khi = min(C - 1u, c0 + Re);  // common core
         const bool core = klo <= khi;
-        for (uint32_t c = ulo + tid; c <= uhi; c += nthr) s_rw[c] = __ldcg(raw_src + c);
+        // U aligned down to 32 columns: thread i covers the 32 columns ua + 32 i .. + 31 with
+        // 16-byte loads (raw counts from shared memory, Bc from L2); columns outside U are masked
+        const uint32_t ua = ulo & ~31u;
+        for (uint32_t c8 = ua / 8u + tid; c8 <= uhi / 8u; c8 += nthr)
+            reinterpret_cast<uint4*>(s_rw)[c8] = __ldcg(reinterpret_cast<const uint4*>(raw_src) + c8);
         for (uint32_t i = tid; i < nown; i += nthr) s_sdr[i] = 0u;
         if (tid == 0) s_noc = 0u;
         __syncthreads();
-        // v of this thread's 32 consecutive columns of U (two per register)
-        const uint32_t cb = ulo + tid * kGfPer;
+        const uint32_t cb = ua + tid * kGfPer;
         uint32_t vv[kGfPer / 2];
-        uint32_t vmax = 0;
+        uint32_t tmax = 0;  // largest v of this thread's core columns
 #pragma unroll
-        for (uint32_t j = 0; j < kGfPer; j += 2u) {
-            uint32_t v2[2];
-#pragma unroll
-            for (uint32_t h = 0; h < 2u; ++h) {
-                const uint32_t c = cb + j + h;
-                uint32_t v = 0;
-                if (c <= uhi) {
-                    const uint64_t N = eligible_N(s_rw[c], __ldcg(p.bc + c), theta);
-                    v = N ? max(1u, static_cast<uint32_t>(N >> vsh)) : 0u;
-                }
-                v2[h] = v;
-                vmax = max(vmax, v);
+        for (uint32_t q = 0; q < kGfPer / 8u; ++q) {
+            uint4 r8 = make_uint4(0u, 0u, 0u, 0u), b0 = r8, b1 = r8;
+            if (cb <= uhi) {
+                r8 = reinterpret_cast<const uint4*>(s_rw + cb)[q];
+                b0 = __ldcg(reinterpret_cast<const uint4*>(p.bc + cb) + 2u * q);
+                b1 = __ldcg(reinterpret_cast<const uint4*>(p.bc + cb) + 2u * q + 1u);
             }
-            vv[j / 2u] = v2[0] | (v2[1] << 16);
+            const uint32_t rr[4] = {r8.x, r8.y, r8.z, r8.w};
+            const uint32_t bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (uint32_t h = 0; h < 4u; ++h) {
+                uint32_t v2[2];
+#pragma unroll
+                for (uint32_t e2 = 0; e2 < 2u; ++e2) {
+                    const uint32_t j = 8u * q + 2u * h + e2, c = cb + j;
+                    const uint32_t raw = (rr[h] >> (16u * e2)) & 0xFFFFu;
+                    const uint64_t N = (c >= ulo && c <= uhi) ? eligible_N(raw, bb[2u * h + e2], theta) : 0ull;
+                    const uint32_t v = N ? max(1u, static_cast<uint32_t>(N >> vsh)) : 0u;
+                    v2[e2] = v;
+                    if (c >= klo && c <= khi) tmax = max(tmax, v);
+                }
+                vv[4u * q + h] = v2[0] | (v2[1] << 16);
+            }
         }
+        // t: the largest value with >= k threads whose core maximum reaches it -- then >= k core
+        // columns have v >= t (valid), and t is close to the core's k-th largest value
         uint32_t tthr = 0;
         if (core) {
-            vmax = __reduce_max_sync(0xffffffffu, vmax);
-            if (lane == 0) s_red[0][wi] = vmax;
-            __syncthreads();
-            vmax = 0;
-#pragma unroll
-            for (uint32_t w = 0; w < kGfWarps; ++w) vmax = max(vmax, s_red[0][w]);
-            uint32_t par = 1;
-            for (int bit = vmax ? 31 - __clz(vmax) : -1; bit >= 0; --bit) {
+            for (int bit = 15; bit >= 0; --bit) {
                 const uint32_t tt = tthr | (1u << bit);
-                uint32_t cnt = 0;
-#pragma unroll
-                for (uint32_t j = 0; j < kGfPer; ++j) {
-                    const uint32_t c = cb + j, v = (vv[j / 2u] >> (16u * (j & 1u))) & 0xFFFFu;
-                    cnt += (c >= klo && c <= khi && v >= tt) ? 1u : 0u;
-                }
-                const uint32_t tot = block_sum(cnt, s_red[par]);
-                par = par == 1u ? 2u : 1u;  // alternate buffers: one barrier per step
-                if (tot >= k) tthr = tt;
+                if (__syncthreads_count(tmax >= tt) >= static_cast<int>(k)) tthr = tt;
             }
         }
         tthr = max(tthr, 1u);
@@ -535,8 +534,8 @@ uint32_t learn_grid_full_smem(const Geometry& g, uint32_t G, uint32_t stages, ui
     if (ccols) *ccols = cc;
     if (g.C32 > kGfThreads * kGfPer || g.C32 > 65536u) return 0u;  // union window per thread / u16 positions
     const uint32_t own_cols = own * 32u;
-    return 4u * (Wn4 + stages * cc * g.S + own_cols + (own + 1u) / 2u * 2u + (own_cols + 1u) / 2u * 2u) +
-           8u * cap + 2u * g.C32 + 2u * cap;
+    return 4u * (Wn4 + stages * cc * g.S + own_cols + (own + 3u) / 4u * 4u + own_cols) + 8u * cap + 2u * g.C32 +
+           2u * cap;
 }
 
 cudaError_t configure_learn_grid_full(int max_smem) {
