@@ -636,7 +636,7 @@ def main():
         i8_peak = 2.0 * json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["bf16_tflops"] \
             if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 4500.0
         outs = {}
-        for name, flags in (("gather", P.SP_FLAG_PATCH_GATHER), ("tcgen05", 0)):
+        for name, flags in (("gather", P.SP_FLAG_PATCH_GATHER), ("tcgen05", P.SP_FLAG_PATCH_TENSOR)):
             spp = P.SpatialPooler(input_width=W, input_height=H, patch_width=32, patch_height=30,
                                   num_columns=C, synapses_per_column=S, min_overlap=THETA,
                                   winners_set_size=K_WIN, seed=SEED_STATE, device=local,

@@ -68,9 +68,10 @@ enum {
                                      inhibition_radius > 0, the radius recomputed from the
                                      connected spans.  The radius in force governs inhibition
                                      of every later call (learn or not). */
-    SP_FLAG_PATCH_GATHER = 8u     /* patch mode inference: use the bit-sliced gather kernel even
-                                     where the tensor-core GEMM kernel is eligible (NEXT-2; the
-                                     two give identical results, this exists for A/B tests) */
+    SP_FLAG_PATCH_GATHER = 8u,    /* patch mode inference: the bit-sliced gather kernel (the
+                                     default since round 2: measured faster) */
+    SP_FLAG_PATCH_TENSOR = 16u    /* patch mode inference: the tcgen05 kind::i8 GEMM kernel where
+                                     eligible (NEXT-2; identical results; opt-in, A/B tests) */
 };
 
 /*

@@ -499,7 +499,8 @@ sp_plan_info make_plan(const sp_handle* h, uint32_t n, bool learn, const uint8_t
     if (h->cfg.force_path == SP_PATH_PER_INPUT) reason |= sp::kNotBatchedForced;
     if (!h->lay.ok) reason |= sp::kNotBatchedSmem;
     pl.reason = reason;
-    const bool mma = !g.whole && !learn && h->mma_clusters && !(h->cfg.flags & SP_FLAG_PATCH_GATHER) &&
+    const bool mma = !g.whole && !learn && h->mma_clusters && (h->cfg.flags & SP_FLAG_PATCH_TENSOR) &&
+                     !(h->cfg.flags & SP_FLAG_PATCH_GATHER) &&
                      h->cfg.force_path != SP_PATH_PER_INPUT && !(frames && (reinterpret_cast<uintptr_t>(frames) & 15u));
     if (mma && n > 0) {
         // tensor-core patch kernel: blocks of 4 tile-rows x 32 slots, clusters of C32/128 CTAs
@@ -771,6 +772,7 @@ sp_status launch_batched_path(sp_handle* h, const uint8_t* frames, const uint32_
     p.wm_umax = h->wm_umax;
     p.cand_min_radius = h->cand_min_radius;
     p.cand_min_radius_u = h->cand_min_radius_u;
+    if (const char* ecd = std::getenv("SP_CAND_DBG")) p.cand_dbg = static_cast<uint32_t>(std::atoi(ecd));
     if (pl.tensor_cores) {
         if (h->conn_dirty) {
             e = sp::launch_build_conn(h->d_idx, h->d_perm, h->cfg.connected_threshold, g.C, g.C32, g.S, g.nbits,

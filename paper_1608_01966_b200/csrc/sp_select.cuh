@@ -1185,7 +1185,7 @@ template <int NW2, bool UNIFORM, typename KeyT, typename RowT, typename Emit>
 __device__ __forceinline__ bool local_candidates(const RowT* row, const uint32_t* bc, uint32_t C, uint32_t ncw,
                                                  uint32_t radius, uint32_t k, uint32_t theta, uint32_t r_lo,
                                                  uint32_t L, const CoarseMap& cm, uint8_t* scratch,
-                                                 uint32_t scratch_bytes, uint32_t lane, Emit emit) {
+                                                 uint32_t scratch_bytes, uint32_t lane, Emit emit, uint32_t dbg = 0) {
     static_assert(NW2 == 1 || NW2 == 2, "at most 64 column-words");
     const uint32_t full = 0xffffffffu;
     auto value = [&](uint32_t c) -> uint32_t {
@@ -1307,7 +1307,7 @@ __device__ __forceinline__ bool local_candidates(const RowT* row, const uint32_t
     }
     __syncwarp();
     // beats of each candidate among the candidates of its window (a contiguous range)
-    for (uint32_t i0 = 0; i0 < P; i0 += 32u) {
+    for (uint32_t i0 = 0; i0 < (dbg & 1u ? 0u : P); i0 += 32u) {
         const uint32_t i = i0 + lane;
         const bool has = i < P;
         const uint32_t c = has ? spos[i] : 0u;

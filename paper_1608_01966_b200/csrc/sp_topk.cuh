@@ -151,7 +151,7 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
                                                                      p.sdr[static_cast<size_t>(gin) * p.ncw + w0 +
                                                                            lane] = myword;
                                                              }
-                                                         })) {
+                                                         }, p.cand_dbg)) {
                     if (lane == 0) p.counts[gin] = total;
                     continue;
                 }
@@ -254,7 +254,7 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
                                                                       p.sdr[static_cast<size_t>(gin) * p.ncw + w0 +
                                                                             lane] = myword;
                                                               }
-                                                          })) {
+                                                          }, p.cand_dbg)) {
                     if (lane == 0) p.counts[gin] = total;
                     continue;
                 }

@@ -23,6 +23,7 @@ SP_FLAG_RECORD_OVERLAPS = 1
 SP_FLAG_LEARN_GRID = 2
 SP_FLAG_FULL_LEARNING = 4
 SP_FLAG_PATCH_GATHER = 8
+SP_FLAG_PATCH_TENSOR = 16
 SP_LEARN_PER_INPUT, SP_LEARN_CLUSTER, SP_LEARN_GRID = 0, 1, 2
 
 

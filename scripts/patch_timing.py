@@ -18,7 +18,7 @@ import sp_inputs  # noqa: E402
 def time_point(F, C, S, radius, boost, gather, reps=10):
     sp = P.SpatialPooler(input_width=960, input_height=540, patch_width=32, patch_height=30, num_columns=C,
                          synapses_per_column=S, min_overlap=4, winners_set_size=40, inhibition_radius=radius,
-                         max_inputs=F * 540, flags=P.SP_FLAG_PATCH_GATHER if gather else 0)
+                         max_inputs=F * 540, flags=P.SP_FLAG_PATCH_GATHER if gather else P.SP_FLAG_PATCH_TENSOR)
     if boost == "seeded":
         sp.set_state(boost=sp_inputs.boosts(7, C))
     fr = torch.empty((F, 540, 960), dtype=torch.uint8, device="cuda")

@@ -1,6 +1,6 @@
 """NEXT-2: the tensor-core patch kernel (sp_patch_mma.cu; tcgen05 kind::i8 GEMM of the 0/1
 connectivity matrix with the 0/1 tiles, exact s32 accumulation) against the oracle, and A/B
-against the bit-sliced gather kernel (SP_FLAG_PATCH_GATHER).  Bar: raw counts, boosted
+against the bit-sliced gather kernel (the default; SP_FLAG_PATCH_TENSOR opts in to the GEMM kernel).  Bar: raw counts, boosted
 overlaps, winners bit-exact (the same selection code runs after either overlap kernel)."""
 import numpy as np
 import pytest
@@ -18,7 +18,7 @@ DEV = torch.device("cuda", 0)
 
 
 def make_sp(cfg, state=None, record=True, gather=False, max_inputs=4096):
-    flags = (P.SP_FLAG_RECORD_OVERLAPS if record else 0) | (P.SP_FLAG_PATCH_GATHER if gather else 0)
+    flags = (P.SP_FLAG_RECORD_OVERLAPS if record else 0) | (P.SP_FLAG_PATCH_GATHER if gather else P.SP_FLAG_PATCH_TENSOR)
     sp = P.SpatialPooler(**gpu_kwargs(cfg, max_inputs=max_inputs, flags=flags))
     if state is not None:
         sp.set_state(*state)
