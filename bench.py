@@ -617,12 +617,32 @@ def main():
         b.record(stream)
         torch.cuda.synchronize()
         lms = a.elapsed_time(b) / args.steps
+        # the learned SP of the step (uniform boost) with Tab. 2's radius 80 (config 2's local variant)
+        spu = P.SpatialPooler(input_width=W, input_height=H, num_columns=C, synapses_per_column=S,
+                              min_overlap=THETA, winners_set_size=K_WIN, inhibition_radius=80,
+                              seed=SEED_STATE, device=local, max_inputs=F)
+        spu.set_state(*learned_state)
+        for _ in range(3):
+            spu.compute_into(frames, lsdr, lcnt)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(args.steps):
+            spu.compute_into(frames, lsdr, lcnt)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ums = a.elapsed_time(b) / args.steps
+        spu.close()
         local_fl = {"value": F / (lms / 1e3), "unit": UNIT, "ms_per_step": lms, "radius": fr,
                     "boosted_columns": int((fboost > 1).sum()),
                     "hbm_frac": round(F * ALGO_BYTES_PER_FRAME / (lms / 1e3) / 1e9 / measured_peak_hbm()[0], 4),
                     "mean_winners": float(lcnt.float().mean()),
                     "workload": "the step's frames through the full-learning SP (learned boosts, local "
-                                "inhibition at the adapted radius; sp_select.cuh candidate pruning)"}
+                                "inhibition at the adapted radius; sp_select.cuh candidate pruning)",
+                    "uniform_r80": {"value": F / (ums / 1e3), "unit": UNIT, "ms_per_step": ums,
+                                    "hbm_frac": round(F * ALGO_BYTES_PER_FRAME / (ums / 1e3) / 1e9 /
+                                                      measured_peak_hbm()[0], 4),
+                                    "workload": "the step's learned SP (one boost) with local inhibition "
+                                                "at Tab. 2's radius 80 (config 2 local variant)"}}
         spl.close()
 
     # ---- NEXT-2 patch mode (BASELINE config 2 "tiled into patches"; R13): 32x30 tiles of the

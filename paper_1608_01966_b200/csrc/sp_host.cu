@@ -389,8 +389,8 @@ struct sp_handle {
     // local inhibition (batched kernels): candidate pruning from this radius on, when the
     // candidates fit the warp's scratch (else the wavelet / comparator).  Set at create from the
     // expected candidate count ~ k*C/(2r) (scripts/local_topk_timing.py): it beats
-    // the 15-level per-column-boost wavelet / comparator below ~350 candidates and the <= 8-level
-    // uniform wavelet below ~130.
+    // the 15-level per-column-boost wavelet / comparator and (uniform boost, level sweep) the
+    // <= 8-level uniform wavelet below ~350 candidates.
     uint32_t cand_min_radius = 0, cand_min_radius_u = 0;
     uint32_t force_groups = 0;        // SP_GROUPS (tests): batched groups per call, cluster size 1
     // tensor-core patch kernel (NEXT-2, sp_patch_mma.cu): 0 clusters = not eligible
@@ -801,7 +801,7 @@ sp_status launch_batched_path(sp_handle* h, const uint8_t* frames, const uint32_
         q.raw_stage_bytes = g.W * h->mma_sps * 4u;
         q.region_bytes = h->mma_region;
         q.conn = h->d_conn;
-        q.multicast = q.Q > 1 ? 1u : 0u;
+        q.multicast = 0u;  // per-CTA TMA (L2 hits) measured faster than the cluster multicast: 0.876 vs 0.964 ms
         if (const char* em = std::getenv("SP_MMA_MULTICAST")) q.multicast = q.Q > 1 && std::atoi(em) ? 1u : 0u;
         if (const char* ed = std::getenv("SP_MMA_DBG")) q.dbg = static_cast<uint32_t>(std::atoi(ed));
         const uint32_t clusters = std::min(q.nblocks, h->mma_clusters);
@@ -1321,7 +1321,7 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
     {
         const uint64_t kc = static_cast<uint64_t>(cfg->winners_set_size) * g.C;
         h->cand_min_radius = static_cast<uint32_t>((kc + 699u) / 700u);
-        h->cand_min_radius_u = static_cast<uint32_t>((kc + 259u) / 260u);
+        h->cand_min_radius_u = static_cast<uint32_t>((kc + 699u) / 700u);
     }
     if (const char* ec = std::getenv("SP_CAND_MIN_RADIUS"))  // experiments / tests (huge = off)
         h->cand_min_radius = h->cand_min_radius_u = static_cast<uint32_t>(std::strtoul(ec, nullptr, 10));

@@ -1279,9 +1279,101 @@ __device__ __forceinline__ bool local_candidates(const RowT* row, const uint32_t
         if (__all_sync(full, ok)) t = tt;
     }
     t = max(t, 1u);
+    constexpr uint32_t kHead = 64u * 4u;
+    if (UNIFORM && vmax - t < 64u && scratch_bytes >= kHead + 4u * 4u * 65u) {
+        // Uniform boost, few levels: sweep the raw values from the top.  With G = the columns of
+        // value > l and E = those of value l (bit masks over all columns, one word per lane), a
+        // column c of value l has beats(c) = |G & W(c)| + |E & [lo(c), c)| (equal raw: the lower
+        // index wins): two range popcounts from per-word prefix counts, no candidate list.
+        uint32_t* sG = reinterpret_cast<uint32_t*>(scratch + kHead);  // [65] words of G
+        uint32_t* sPG = sG + 65;                                       // [65] exclusive prefix counts
+        uint32_t* sE = sPG + 65;
+        uint32_t* sPE = sE + 65;
+        auto ge = [&](uint32_t l, uint32_t* w) {
+            const uint32_t ll = l | (l << 16);
+#pragma unroll
+            for (int h = 0; h < NW2; ++h) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) acc |= ((vb[h][i] - ll) >> (15 - i)) & (0x00010001u << i);
+                w[h] = acc;
+            }
+        };
+        // exclusive prefix counts of the words w[h] (word lane + 32h) -> sw / sp (+ total at ncw);
+        // ex[h] / tot_out get this lane's exclusive prefixes and the total
+        auto publish = [&](const uint32_t* w, uint32_t* sw, uint32_t* sp, uint32_t* ex, uint32_t& tot_out) {
+            uint32_t q[NW2];
+#pragma unroll
+            for (int h = 0; h < NW2; ++h) q[h] = __popc(w[h]);
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+#pragma unroll
+                for (int h = 0; h < NW2; ++h) {
+                    const uint32_t a = __shfl_up_sync(full, q[h], d);
+                    if (lane >= static_cast<uint32_t>(d)) q[h] += a;
+                }
+            }
+            const uint32_t t0 = __shfl_sync(full, q[0], 31);
+            const uint32_t tot = t0 + (NW2 > 1 ? __shfl_sync(full, q[NW2 - 1], 31) : 0u);
+#pragma unroll
+            for (int h = 0; h < NW2; ++h) {
+                const uint32_t j = lane + 32u * h;
+                ex[h] = (h ? t0 : 0u) + q[h] - __popc(w[h]);
+                if (j < ncw) sw[j] = w[h], sp[j] = ex[h];
+            }
+            if (lane == 0) sw[ncw] = 0u, sp[ncw] = tot;
+            tot_out = tot;
+        };
+        auto cnt = [&](const uint32_t* sw, const uint32_t* sp, uint32_t x) {  // #{d < x}, x <= C
+            const uint32_t w = x >> 5;
+            return sp[w] + __popc(sw[w] & ((1u << (x & 31u)) - 1u));
+        };
+        // G's words and exclusive prefix counts are carried from level to level (G of the next
+        // level = G | E of this one, so its prefix counts are the sums): one scan per level
+        uint32_t gw[NW2], gp[NW2], win[NW2], gtot = 0;
+#pragma unroll
+        for (int h = 0; h < NW2; ++h) gw[h] = 0u, gp[h] = 0u, win[h] = 0u;
+        for (uint32_t l = vmax; l + 1u > t; --l) {
+            uint32_t mw[NW2], ew[NW2], ep[NW2], etot;
+            ge(l, mw);
+            bool any = false;
+#pragma unroll
+            for (int h = 0; h < NW2; ++h) ew[h] = mw[h] & ~gw[h], any |= ew[h] != 0u;
+            if (!__any_sync(full, any)) continue;
+#pragma unroll
+            for (int h = 0; h < NW2; ++h) {
+                const uint32_t j = lane + 32u * h;
+                if (j < ncw) sG[j] = gw[h], sPG[j] = gp[h];
+            }
+            if (lane == 0) sG[ncw] = 0u, sPG[ncw] = gtot;
+            publish(ew, sE, sPE, ep, etot);
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < NW2; ++h) {
+                uint32_t e = ew[h];
+                while (e) {
+                    const uint32_t bit = __ffs(e) - 1u, c = 32u * (lane + 32u * h) + bit;
+                    e &= e - 1u;
+                    const uint32_t lo = c >= radius ? c - radius : 0u, hi1 = min(C, c + radius + 1u);
+                    const uint32_t beats = (cnt(sG, sPG, hi1) - cnt(sG, sPG, lo)) + (cnt(sE, sPE, c) - cnt(sE, sPE, lo));
+                    if (beats < k) win[h] |= 1u << bit;
+                }
+            }
+            __syncwarp();  // sG / sE are rewritten for the next level
+#pragma unroll
+            for (int h = 0; h < NW2; ++h) gw[h] = mw[h], gp[h] += ep[h];
+            gtot += etot;
+        }
+#pragma unroll
+        for (int h = 0; h < NW2; ++h)
+            if (lane + 32u * h < ncw) sdr[lane + 32u * h] = win[h];
+        __syncwarp();
+        for (uint32_t cw = 0; cw < ncw; ++cw) emit(cw, sdr[cw]);
+        __syncwarp();
+        return true;
+    }
     masks(t);
     const uint32_t P = total;
-    constexpr uint32_t kHead = 64u * 4u;
     const uint32_t cap = scratch_bytes > kHead ? (scratch_bytes - kHead) / (sizeof(KeyT) + 2u) : 0u;
     if (P > cap) return false;
     KeyT* skey = reinterpret_cast<KeyT*>(scratch + kHead);                              // [cap]
