@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kGfThreads, 1)
     __shared__ uint32_t s_red[4][kGfWarps];
     __shared__ float s_fred[4][kGfWarps];
     __shared__ uint32_t s_scan[kGfWarps];
-    __shared__ uint32_t s_R, s_noc;
+    __shared__ uint32_t s_R, s_noc, s_P;
     __shared__ unsigned long long s_span;
     const Geometry& g = p.g;
     const FullLearn& fl = p.fl;
@@ -126,10 +126,12 @@ __global__ void __launch_bounds__(kGfThreads, 1)
     auto gbits_of = [&](uint32_t t) { return p.bits_g + static_cast<size_t>(t) * Wn4; };  // prepacked
     // phase timers of CTA 0 / thread 0 (SP_TRACE): [0] bit-plane wait, [1] overlap, [2] B1 + radius,
     // [3] selection, [4] (a) + (b), [5] B2, [6] (c) (d) (e); [7] running timestamp
-    __shared__ uint64_t s_tr[8];
+    // selection sub-phases (SP_TRACE): [8] raw row load, [9] values, [10] threshold, [11] compaction
+    // + owned candidates, [12] beats + SDR
+    __shared__ uint64_t s_tr[13];
     const bool tr = p.trace != nullptr && b == 0 && tid == 0;
     if (tr)
-        for (int i = 0; i < 8; ++i) s_tr[i] = 0;
+        for (int i = 0; i < 13; ++i) s_tr[i] = 0;
     auto stamp = [&](int i) {
         if (tr) {
             const uint64_t now = globaltimer();
@@ -237,42 +239,41 @@ __global__ void __launch_bounds__(kGfThreads, 1)
         const uint32_t ulo = c0 >= Re ? c0 - Re : 0u, uhi = min(C - 1u, c1 - 1u + Re);  // union window
         const uint32_t klo = c1 - 1u >= Re ? c1 - 1u - Re : 0u, khi = min(C - 1u, c0 + Re);  // common core
         const bool core = klo <= khi;
-        // U aligned down to 32 columns: thread i covers the 32 columns ua + 32 i .. + 31 with
-        // 16-byte loads (raw counts from shared memory, Bc from L2); columns outside U are masked
-        const uint32_t ua = ulo & ~31u;
+        // U aligned down to 32 columns; raw counts -> s_rw, Bc -> the synapse ring (idle until the
+        // next input's overlap) when it holds U, both by 16-byte coalesced loads
+        const uint32_t ua = ulo & ~31u, nu = uhi - ua + 1u;
         for (uint32_t c8 = ua / 8u + tid; c8 <= uhi / 8u; c8 += nthr)
             reinterpret_cast<uint4*>(s_rw)[c8] = __ldcg(reinterpret_cast<const uint4*>(raw_src) + c8);
+        const bool bc_smem = stages * chunk_words >= ((nu + 3u) & ~3u);
+        uint32_t* s_bcu = s_ring - ua;  // s_bcu[c], c in U (when bc_smem)
+        if (bc_smem)
+            for (uint32_t c4 = ua / 4u + tid; c4 <= uhi / 4u; c4 += nthr)
+                reinterpret_cast<uint4*>(s_ring)[c4 - ua / 4u] = __ldcg(reinterpret_cast<const uint4*>(p.bc) + c4);
         for (uint32_t i = tid; i < nown; i += nthr) s_sdr[i] = 0u;
-        if (tid == 0) s_noc = 0u;
+        if (tid == 0) s_noc = 0u, s_P = 0u;
         __syncthreads();
-        const uint32_t cb = ua + tid * kGfPer;
+        auto bc_of = [&](uint32_t c) { return bc_smem ? s_bcu[c] : __ldcg(p.bc + c); };
+        stamp(8);
+        // thread i: columns ua + i + 512 j (conflict-free shared loads), v two per register
         uint32_t vv[kGfPer / 2];
         uint32_t tmax = 0;  // largest v of this thread's core columns
 #pragma unroll
-        for (uint32_t q = 0; q < kGfPer / 8u; ++q) {
-            uint4 r8 = make_uint4(0u, 0u, 0u, 0u), b0 = r8, b1 = r8;
-            if (cb <= uhi) {
-                r8 = reinterpret_cast<const uint4*>(s_rw + cb)[q];
-                b0 = __ldcg(reinterpret_cast<const uint4*>(p.bc + cb) + 2u * q);
-                b1 = __ldcg(reinterpret_cast<const uint4*>(p.bc + cb) + 2u * q + 1u);
-            }
-            const uint32_t rr[4] = {r8.x, r8.y, r8.z, r8.w};
-            const uint32_t bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        for (uint32_t j = 0; j < kGfPer; j += 2u) {
+            uint32_t v2[2];
 #pragma unroll
-            for (uint32_t h = 0; h < 4u; ++h) {
-                uint32_t v2[2];
-#pragma unroll
-                for (uint32_t e2 = 0; e2 < 2u; ++e2) {
-                    const uint32_t j = 8u * q + 2u * h + e2, c = cb + j;
-                    const uint32_t raw = (rr[h] >> (16u * e2)) & 0xFFFFu;
-                    const uint64_t N = (c >= ulo && c <= uhi) ? eligible_N(raw, bb[2u * h + e2], theta) : 0ull;
-                    const uint32_t v = N ? max(1u, static_cast<uint32_t>(N >> vsh)) : 0u;
-                    v2[e2] = v;
+            for (uint32_t e2 = 0; e2 < 2u; ++e2) {
+                const uint32_t c = ua + tid + kGfThreads * (j + e2);
+                uint32_t v = 0;
+                if (c >= ulo && c <= uhi) {
+                    const uint64_t N = eligible_N(s_rw[c], bc_of(c), theta);
+                    v = N ? max(1u, static_cast<uint32_t>(N >> vsh)) : 0u;
                     if (c >= klo && c <= khi) tmax = max(tmax, v);
                 }
-                vv[4u * q + h] = v2[0] | (v2[1] << 16);
+                v2[e2] = v;
             }
+            vv[j / 2u] = v2[0] | (v2[1] << 16);
         }
+        stamp(9);
         // t: the largest value with >= k threads whose core maximum reaches it -- then >= k core
         // columns have v >= t (valid), and t is close to the core's k-th largest value
         uint32_t tthr = 0;
@@ -283,58 +284,47 @@ __global__ void __launch_bounds__(kGfThreads, 1)
             }
         }
         tthr = max(tthr, 1u);
-        // compaction of the candidates of U (v >= t) in position order, with exact keys
-        uint32_t mine = 0;
+        stamp(10);
+        // the candidates of U (v >= t), unordered (warp-aggregated appends), with exact keys; the
+        // owned ones also into s_oc
 #pragma unroll
-        for (uint32_t j = 0; j < kGfPer; ++j) mine += ((vv[j / 2u] >> (16u * (j & 1u))) & 0xFFFFu) >= tthr ? 1u : 0u;
-        uint32_t incl = mine;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t x = __shfl_up_sync(0xffffffffu, incl, d);
-            if (lane >= static_cast<uint32_t>(d)) incl += x;
-        }
-        if (lane == 31u) s_scan[wi] = incl;
-        __syncthreads();
-        uint32_t before = 0, P = 0;
-        for (uint32_t w = 0; w < kGfWarps; ++w) {
-            const uint32_t x = s_scan[w];
-            before += w < wi ? x : 0u;
-            P += x;
-        }
-        const bool listed = P <= cap;
-        if (listed) {
-            uint32_t at = before + incl - mine;
-#pragma unroll
-            for (uint32_t j = 0; j < kGfPer; ++j) {
-                const uint32_t c = cb + j;
-                if (((vv[j / 2u] >> (16u * (j & 1u))) & 0xFFFFu) >= tthr) {
-                    uint64_t N;
-                    s_pos[at] = static_cast<uint16_t>(c);
-                    s_key[at] = exact_key(s_rw[c], __ldcg(p.bc + c), theta, c, L, N);
-                    ++at;
-                }
+        for (uint32_t j = 0; j < kGfPer; ++j) {
+            const uint32_t c = ua + tid + kGfThreads * j;
+            const bool is = ((vv[j / 2u] >> (16u * (j & 1u))) & 0xFFFFu) >= tthr;
+            const uint32_t bal = __ballot_sync(0xffffffffu, is);
+            if (bal == 0u) continue;
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(&s_P, static_cast<uint32_t>(__popc(bal)));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (is) {
+                const uint32_t at = base + __popc(bal & ((1u << lane) - 1u));
+                uint64_t N;
+                const uint64_t key = exact_key(s_rw[c], bc_of(c), theta, c, L, N);
+                if (at < cap) s_pos[at] = static_cast<uint16_t>(c), s_key[at] = key;
+                if (c >= c0 && c < c1) s_oc[atomicAdd(&s_noc, 1u)] = c;
             }
         }
-        // the owned candidates (owned eligible columns when the list overflowed)
-        for (uint32_t c = c0 + tid; c < c1; c += nthr) {
-            const uint64_t N = eligible_N(s_rw[c], __ldcg(p.bc + c), theta);
-            const uint32_t v = N ? max(1u, static_cast<uint32_t>(N >> vsh)) : 0u;
-            if (v >= tthr) s_oc[atomicAdd(&s_noc, 1u)] = c;
-        }
         __syncthreads();
+        stamp(11);
+        const uint32_t P = s_P;
+        const bool listed = P <= cap;
         // beats of each owned candidate among the candidates of its window: a warp per candidate
         const uint32_t noc = s_noc;
         for (uint32_t q = wi; q < noc; q += nw) {
             const uint32_t c = s_oc[q];
             const uint32_t lo = c >= Re ? c - Re : 0u, hi = min(C - 1u, c + Re);
             uint64_t N;
-            const uint64_t key = exact_key(s_rw[c], __ldcg(p.bc + c), theta, c, L, N);
+            const uint64_t key = exact_key(s_rw[c], bc_of(c), theta, c, L, N);
             uint32_t beats = 0;
             if (listed) {
-                const uint32_t a = lower_bound_u16(s_pos, P, lo), e = lower_bound_u16(s_pos, P, hi + 1u);
-                for (uint32_t j0 = a; j0 < e && beats < k; j0 += 32u) {
+                for (uint32_t j0 = 0; j0 < P && beats < k; j0 += 32u) {
                     const uint32_t j = j0 + lane;
-                    beats += __popc(__ballot_sync(0xffffffffu, j < e && s_key[j] > key));
+                    bool gt = false;
+                    if (j < P) {
+                        const uint32_t d = s_pos[j];
+                        gt = d >= lo && d <= hi && s_key[j] > key;
+                    }
+                    beats += __popc(__ballot_sync(0xffffffffu, gt));
                 }
             } else {  // direct scan of the window (every column of it)
                 for (uint32_t d0 = lo; d0 <= hi && beats < k; d0 += 32u) {
@@ -355,7 +345,7 @@ __global__ void __launch_bounds__(kGfThreads, 1)
             p.sdr[static_cast<size_t>(gin) * ncw + wb0 + i] = word;
             if (word) atomicAdd(p.counts + gin, static_cast<uint32_t>(__popc(word)));
         }
-        stamp(3);
+        stamp(12);
         // ---- (a) permanence update of the owned winners (warp per column) + their spans ----
         for (uint32_t cl = wi; cl < ncols; cl += nw) {
             const uint32_t c = c0 + cl;
@@ -520,6 +510,7 @@ __global__ void __launch_bounds__(kGfThreads, 1)
     if (tr) {
         for (int i = 0; i < 7; ++i) p.trace[i] = s_tr[i];
         p.trace[7] = n;
+        for (int i = 8; i < 13; ++i) p.trace[i] = s_tr[i];
     }
 }
 

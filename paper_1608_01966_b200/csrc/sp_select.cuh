@@ -1197,18 +1197,41 @@ __device__ __forceinline__ bool local_candidates(const RowT* row, const uint32_t
             return coarse_u15(eligible_N(row[c], bc[c], theta), cm, lossy);
         }
     };
-    // vb[h][i] = (v(32j + i) | 0x8000) | (v(32j + i + 16) | 0x8000) << 16, j = lane + 32h
+    // vb[h][i] = (v(32j + i) | 0x8000) | (v(32j + i + 16) | 0x8000) << 16, j = lane + 32h.  The
+    // values are computed column-coalesced (lane = column of each word) and staged in the scratch
+    // as rows of 34 u16 per word with columns i, i+16 adjacent, then read lane-owned as u32 pairs at
+    // word offset 17 j + i (conflict-free; reading them lane-owned straight from the raw counts
+    // and boosts would be 16- and 32-way bank conflicts)
+    constexpr uint32_t kHead = 64u * 4u;
     uint32_t vb[NW2][16];
     uint32_t vmax = 0;
+    if (scratch_bytes >= kHead + ncw * 68u) {
+        uint16_t* stg = reinterpret_cast<uint16_t*>(scratch + kHead);
+        for (uint32_t cw = 0; cw < ncw; ++cw) {
+            const uint32_t v = value(cw * 32u + lane);
+            vmax = max(vmax, v);
+            stg[cw * 34u + ((lane & 15u) << 1) + (lane >> 4)] = static_cast<uint16_t>(v);
+        }
+        __syncwarp();
 #pragma unroll
-    for (int h = 0; h < NW2; ++h) {
-        const uint32_t j = lane + 32u * h;
+        for (int h = 0; h < NW2; ++h) {
+            const uint32_t j = lane + 32u * h;
+            const uint32_t* rowp = reinterpret_cast<const uint32_t*>(stg) + 17u * j;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const uint32_t a = j < ncw ? value(32u * j + i) : 0u;
-            const uint32_t b = j < ncw ? value(32u * j + i + 16u) : 0u;
-            vmax = max(vmax, max(a, b));
-            vb[h][i] = (a | (b << 16)) | 0x80008000u;
+            for (int i = 0; i < 16; ++i) vb[h][i] = (j < ncw ? rowp[i] : 0u) | 0x80008000u;
+        }
+        __syncwarp();  // the staging area is reused below
+    } else {
+#pragma unroll
+        for (int h = 0; h < NW2; ++h) {
+            const uint32_t j = lane + 32u * h;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const uint32_t a = j < ncw ? value(32u * j + i) : 0u;
+                const uint32_t b = j < ncw ? value(32u * j + i + 16u) : 0u;
+                vmax = max(vmax, max(a, b));
+                vb[h][i] = (a | (b << 16)) | 0x80008000u;
+            }
         }
     }
     vmax = __reduce_max_sync(full, vmax);
@@ -1279,16 +1302,13 @@ __device__ __forceinline__ bool local_candidates(const RowT* row, const uint32_t
         if (__all_sync(full, ok)) t = tt;
     }
     t = max(t, 1u);
-    constexpr uint32_t kHead = 64u * 4u;
-    if (UNIFORM && vmax - t < 64u && scratch_bytes >= kHead + 4u * 4u * 65u) {
+    if (UNIFORM && vmax - t < 64u && scratch_bytes >= kHead + 2u * 8u * 65u) {
         // Uniform boost, few levels: sweep the raw values from the top.  With G = the columns of
         // value > l and E = those of value l (bit masks over all columns, one word per lane), a
         // column c of value l has beats(c) = |G & W(c)| + |E & [lo(c), c)| (equal raw: the lower
         // index wins): two range popcounts from per-word prefix counts, no candidate list.
-        uint32_t* sG = reinterpret_cast<uint32_t*>(scratch + kHead);  // [65] words of G
-        uint32_t* sPG = sG + 65;                                       // [65] exclusive prefix counts
-        uint32_t* sE = sPG + 65;
-        uint32_t* sPE = sE + 65;
+        uint2* sG = reinterpret_cast<uint2*>(scratch + kHead);  // [65] {word of G, exclusive prefix count}
+        uint2* sE = sG + 65;                                     // [65] the same for E
         auto ge = [&](uint32_t l, uint32_t* w) {
             const uint32_t ll = l | (l << 16);
 #pragma unroll
@@ -1301,7 +1321,7 @@ __device__ __forceinline__ bool local_candidates(const RowT* row, const uint32_t
         };
         // exclusive prefix counts of the words w[h] (word lane + 32h) -> sw / sp (+ total at ncw);
         // ex[h] / tot_out get this lane's exclusive prefixes and the total
-        auto publish = [&](const uint32_t* w, uint32_t* sw, uint32_t* sp, uint32_t* ex, uint32_t& tot_out) {
+        auto publish = [&](const uint32_t* w, uint2* sw, uint32_t* ex, uint32_t& tot_out) {
             uint32_t q[NW2];
 #pragma unroll
             for (int h = 0; h < NW2; ++h) q[h] = __popc(w[h]);
@@ -1319,14 +1339,14 @@ __device__ __forceinline__ bool local_candidates(const RowT* row, const uint32_t
             for (int h = 0; h < NW2; ++h) {
                 const uint32_t j = lane + 32u * h;
                 ex[h] = (h ? t0 : 0u) + q[h] - __popc(w[h]);
-                if (j < ncw) sw[j] = w[h], sp[j] = ex[h];
+                if (j < ncw) sw[j] = make_uint2(w[h], ex[h]);
             }
-            if (lane == 0) sw[ncw] = 0u, sp[ncw] = tot;
+            if (lane == 0) sw[ncw] = make_uint2(0u, tot);
             tot_out = tot;
         };
-        auto cnt = [&](const uint32_t* sw, const uint32_t* sp, uint32_t x) {  // #{d < x}, x <= C
-            const uint32_t w = x >> 5;
-            return sp[w] + __popc(sw[w] & ((1u << (x & 31u)) - 1u));
+        auto cnt = [&](const uint2* sw, uint32_t x) {  // #{d < x}, x <= C (one 8-byte load)
+            const uint2 v = sw[x >> 5];
+            return v.y + __popc(v.x & ((1u << (x & 31u)) - 1u));
         };
         // G's words and exclusive prefix counts are carried from level to level (G of the next
         // level = G | E of this one, so its prefix counts are the sums): one scan per level
@@ -1343,10 +1363,10 @@ __device__ __forceinline__ bool local_candidates(const RowT* row, const uint32_t
 #pragma unroll
             for (int h = 0; h < NW2; ++h) {
                 const uint32_t j = lane + 32u * h;
-                if (j < ncw) sG[j] = gw[h], sPG[j] = gp[h];
+                if (j < ncw) sG[j] = make_uint2(gw[h], gp[h]);
             }
-            if (lane == 0) sG[ncw] = 0u, sPG[ncw] = gtot;
-            publish(ew, sE, sPE, ep, etot);
+            if (lane == 0) sG[ncw] = make_uint2(0u, gtot);
+            publish(ew, sE, ep, etot);
             __syncwarp();
 #pragma unroll
             for (int h = 0; h < NW2; ++h) {
@@ -1355,7 +1375,7 @@ __device__ __forceinline__ bool local_candidates(const RowT* row, const uint32_t
                     const uint32_t bit = __ffs(e) - 1u, c = 32u * (lane + 32u * h) + bit;
                     e &= e - 1u;
                     const uint32_t lo = c >= radius ? c - radius : 0u, hi1 = min(C, c + radius + 1u);
-                    const uint32_t beats = (cnt(sG, sPG, hi1) - cnt(sG, sPG, lo)) + (cnt(sE, sPE, c) - cnt(sE, sPE, lo));
+                    const uint32_t beats = (cnt(sG, hi1) - cnt(sG, lo)) + (cnt(sE, c) - cnt(sE, lo));
                     if (beats < k) win[h] |= 1u << bit;
                 }
             }

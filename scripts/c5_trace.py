@@ -30,12 +30,15 @@ sp.compute(fr[n // 2:], learn=True)
 b.record()
 torch.cuda.synchronize()
 m = n - n // 2
-buf = np.zeros(12, np.uint64)
+buf = np.zeros(24, np.uint64)
 P.lib().sp_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32]
-assert P.lib().sp_debug_trace(sp._h, buf.ctypes.data, 2) == 0
+assert P.lib().sp_debug_trace(sp._h, buf.ctypes.data, 4) == 0
 names = ["bits_wait", "overlap", "barrier1_radius", "selection", "perm_update_duties", "barrier2",
          "boost_bump_spans"]
 print(json.dumps({"frames": m, "us_per_frame": round(a.elapsed_time(b) * 1e3 / m, 2),
                   "radius": sp.get_learning_state()[2], "path": P.learn_path_name(sp.info()),
                   "phases_us_per_frame": {k: round(float(buf[i]) / 1e3 / max(1, int(buf[7])), 2)
-                                          for i, k in enumerate(names)}}))
+                                          for i, k in enumerate(names)},
+                  "selection_us_per_frame": {k: round(float(buf[8 + i]) / 1e3 / max(1, int(buf[7])), 2)
+                                             for i, k in enumerate(["raw_row", "values", "threshold",
+                                                                    "compaction_owned", "beats_sdr"])}}))
