@@ -7,12 +7,13 @@
 namespace sp {
 
 // Grid-wide barrier number m (0, 1, ..) over G co-resident CTAs: a monotonic arrival counter
-// in global memory (zeroed before the launch); release/acquire at gpu scope.
+// in global memory (zeroed before the launch); the CTA barrier makes the CTA's writes part of
+// thread 0's causality order, its red.release publishes them at gpu scope, the ld.acquire spin
+// observes every CTA's arrival.
 __device__ __forceinline__ void grid_barrier(uint32_t* gbar, uint32_t target) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(gbar, 1u);
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gbar) : "memory");
         uint32_t v;
         do {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gbar) : "memory");

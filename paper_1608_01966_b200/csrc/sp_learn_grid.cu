@@ -109,8 +109,11 @@ __global__ void __launch_bounds__(kGridThreads, 1) sp_learn_grid_kernel(const __
         const uint32_t gin = p.first_input + t;
         const uint16_t* raw_src = p.raw_g + (t & 1u) * C32;
         if (tr) s_tr[5] = globaltimer();
-        // ---- a2 pipeline start: the first chunks of this CTA's synapse slice -------------
-        if (tid == 0) {
+        // ---- a2 pipeline start: the first chunks of this CTA's synapse slice (TMA ring;
+        // development switch SP_LEARN_DBG & 64 -- the default reads the rows directly below) ----
+        const bool ring = (p.dbg & 64u) != 0u;
+        if (tid == 0 && !ring) prefetch(t + 2u);
+        if (tid == 0 && ring) {
             asm volatile("fence.proxy.async.global;" ::: "memory");  // learning's flag stores
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             for (uint32_t j = 0; j < min(stages, nchunks); ++j)
@@ -130,8 +133,40 @@ __global__ void __launch_bounds__(kGridThreads, 1) sp_learn_grid_kernel(const __
             s_tr[5] = now;
         }
         const uint32_t* bits = bits_of(t);
-        // ---- a2: overlap of the owned columns, chunk by chunk ------------------------------
-        for (uint32_t j = 0; j < nchunks; ++j, ++cc) {
+        // ---- a2: overlap of the owned columns ---------------------------------------------
+        // warp per column pair: the synapse rows (idx | connected << 31, contiguous, L2-resident)
+        // by 16-byte L2 loads, 8 in flight per lane (2x faster than the TMA chunk ring with its
+        // CTA barrier per chunk: config 5 overlap 9.6 -> 4.8 us per input)
+        auto hitd = [&](uint32_t e) { return (bits[(e & 0x7FFFFFFFu) >> 5] >> (e & 31u)) & (e >> 31); };
+        const uint32_t S4 = S / 4u;  // S % 4 == 0 (grid eligibility)
+        for (uint32_t cl0 = wi; !ring && cl0 < ncols; cl0 += 2u * nw) {
+            const uint32_t clb = cl0 + nw;
+            const uint4* ra = reinterpret_cast<const uint4*>(p.synT + static_cast<size_t>(c0 + cl0) * S);
+            const uint4* rb = reinterpret_cast<const uint4*>(p.synT + static_cast<size_t>(c0 + min(clb, ncols - 1u)) * S);
+            uint32_t xa = 0, xb = 0;
+            for (uint32_t q0 = 0; q0 < S4; q0 += 128u) {
+                uint4 ea[4], eb[4];
+#pragma unroll
+                for (uint32_t u = 0; u < 4u; ++u) {
+                    const uint32_t q = q0 + lane + 32u * u;
+                    ea[u] = q < S4 ? __ldcg(ra + q) : make_uint4(0u, 0u, 0u, 0u);
+                    eb[u] = (q < S4 && clb < ncols) ? __ldcg(rb + q) : make_uint4(0u, 0u, 0u, 0u);
+                }
+#pragma unroll
+                for (uint32_t u = 0; u < 4u; ++u) {
+                    xa += (hitd(ea[u].x) + hitd(ea[u].y)) + (hitd(ea[u].z) + hitd(ea[u].w));
+                    xb += (hitd(eb[u].x) + hitd(eb[u].y)) + (hitd(eb[u].z) + hitd(eb[u].w));
+                }
+            }
+            xa = __reduce_add_sync(0xffffffffu, xa);
+            xb = __reduce_add_sync(0xffffffffu, xb);
+            if (lane == 0) {
+                s_craw[cl0] = xa;
+                if (clb < ncols) s_craw[clb] = xb;
+            }
+        }
+        if (!ring) __syncthreads();
+        for (uint32_t j = 0; ring && j < nchunks; ++j, ++cc) {
             const uint32_t slot = ring_slot, parity = ring_par;
             if (++ring_slot == stages) {
                 ring_slot = 0;

@@ -160,21 +160,53 @@ __global__ void __launch_bounds__(kGfThreads, 1)
         const uint32_t gin = p.first_input + t;
         const uint16_t* raw_src = p.raw_g + (t & 1u) * C32;
         if (tr) s_tr[7] = globaltimer();
-        if (tid == 0) {
+        const bool ring = p.dbg & 64u;  // development: the TMA chunk ring of sp_learn_grid.cu
+        if (tid == 0 && ring) {
             asm volatile("fence.proxy.async.global;" ::: "memory");  // flag stores -> TMA reads
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             for (uint32_t j = 0; j < min(stages, nchunks); ++j)
                 bulk_copy(s_ring + ((cc + j) % stages) * chunk_words, my_syn + static_cast<size_t>(j) * chunk_words,
                           chunk_words * 4u, &s_bar_ring[(cc + j) % stages]);
-            if (b == 0 && t + 2u < n) prefetch_l2(gbits_of(t + 2u), Wn4 * 4u);
         }
+        if (tid == 0 && b == 0 && t + 2u < n) prefetch_l2(gbits_of(t + 2u), Wn4 * 4u);
         for (uint32_t i = tid; i < ncols; i += nthr) s_craw[i] = 0u;
         mbar_wait(&s_bar_bits, bits_phase);
         bits_phase ^= 1u;
         __syncthreads();
         stamp(0);
-        // ---- a2: overlap of the owned columns, chunk by chunk -------------------------------
-        for (uint32_t j = 0; j < nchunks; ++j, ++cc) {
+        // ---- a2: overlap of the owned columns ------------------------------------------------
+        // warp per column pair: the synapse rows (idx | connected << 31, contiguous, L2-resident)
+        // by 16-byte L2 loads, 8 in flight per lane; the input bits from shared memory
+        auto hit = [&](uint32_t e) { return (s_bits[(e & 0x7FFFFFFFu) >> 5] >> (e & 31u)) & (e >> 31); };
+        const uint32_t S4 = S / 4u;  // S % 4 == 0 (grid eligibility)
+        for (uint32_t cl0 = wi; !ring && cl0 < ncols; cl0 += 2u * nw) {
+            const uint32_t clb = cl0 + nw;
+            const uint4* ra = reinterpret_cast<const uint4*>(p.synT + static_cast<size_t>(c0 + cl0) * S);
+            const uint4* rb = reinterpret_cast<const uint4*>(p.synT + static_cast<size_t>(c0 + min(clb, ncols - 1u)) * S);
+            uint32_t xa = 0, xb = 0;
+            for (uint32_t q0 = 0; q0 < S4; q0 += 128u) {
+                uint4 ea[4], eb[4];
+#pragma unroll
+                for (uint32_t u = 0; u < 4u; ++u) {
+                    const uint32_t q = q0 + lane + 32u * u;
+                    ea[u] = q < S4 ? __ldcg(ra + q) : make_uint4(0u, 0u, 0u, 0u);
+                    eb[u] = (q < S4 && clb < ncols) ? __ldcg(rb + q) : make_uint4(0u, 0u, 0u, 0u);
+                }
+#pragma unroll
+                for (uint32_t u = 0; u < 4u; ++u) {
+                    xa += (hit(ea[u].x) + hit(ea[u].y)) + (hit(ea[u].z) + hit(ea[u].w));
+                    xb += (hit(eb[u].x) + hit(eb[u].y)) + (hit(eb[u].z) + hit(eb[u].w));
+                }
+            }
+            xa = __reduce_add_sync(0xffffffffu, xa);
+            xb = __reduce_add_sync(0xffffffffu, xb);
+            if (lane == 0) {
+                s_craw[cl0] = xa;
+                if (clb < ncols) s_craw[clb] = xb;
+            }
+        }
+        if (!ring) __syncthreads();
+        for (uint32_t j = 0; ring && j < nchunks; ++j, ++cc) {
             const uint32_t slot = ring_slot, parity = ring_par;
             if (++ring_slot == stages) ring_slot = 0, ring_par ^= 1u;
             mbar_wait(&s_bar_ring[slot], parity);
@@ -182,7 +214,6 @@ __global__ void __launch_bounds__(kGfThreads, 1)
             const uint32_t jc = wi / wpc, part = wi % wpc;
             const uint32_t* col = ch + jc * S;
             uint32_t r0 = 0, r1 = 0;
-            auto hit = [&](uint32_t e) { return (s_bits[(e & 0x7FFFFFFFu) >> 5] >> (e & 31u)) & (e >> 31); };
             if (vec_ok) {
                 const uint32_t lo = part * span, hi = lo + span;
                 for (uint32_t s = lo + 4u * lane; s < hi; s += 256u) {
