@@ -617,6 +617,7 @@ def main():
         b.record(stream)
         torch.cuda.synchronize()
         lms = a.elapsed_time(b) / args.steps
+        fl_winners = float(lcnt.float().mean())
         # the learned SP of the step (uniform boost) with Tab. 2's radius 80 (config 2's local variant)
         spu = P.SpatialPooler(input_width=W, input_height=H, num_columns=C, synapses_per_column=S,
                               min_overlap=THETA, winners_set_size=K_WIN, inhibition_radius=80,
@@ -635,7 +636,7 @@ def main():
         local_fl = {"value": F / (lms / 1e3), "unit": UNIT, "ms_per_step": lms, "radius": fr,
                     "boosted_columns": int((fboost > 1).sum()),
                     "hbm_frac": round(F * ALGO_BYTES_PER_FRAME / (lms / 1e3) / 1e9 / measured_peak_hbm()[0], 4),
-                    "mean_winners": float(lcnt.float().mean()),
+                    "mean_winners": fl_winners,
                     "workload": "the step's frames through the full-learning SP (learned boosts, local "
                                 "inhibition at the adapted radius; sp_select.cuh candidate pruning)",
                     "uniform_r80": {"value": F / (ums / 1e3), "unit": UNIT, "ms_per_step": ums,

@@ -599,7 +599,7 @@ __global__ void __launch_bounds__(NT, 1) sp_patch_kernel(const __grid_constant__
             for (int h = 0; h < (int)kHiPlanes; ++h) P[i].hi[h] = 0u;
             const uint32_t cw = wi + NW * i;
             if (cw < p.ncw) {
-                const uint32_t nb = p.ell_nb[cw];
+                const uint32_t nb = (p.cand_dbg & 4u) ? 0u : p.ell_nb[cw];  // development: skip the gathers
                 const uint4* e = p.ell + p.ell_off[cw] + lane;
 #pragma unroll 4
                 for (uint32_t bk = 0; bk < nb; ++bk) {
@@ -614,7 +614,8 @@ __global__ void __launch_bounds__(NT, 1) sp_patch_kernel(const __grid_constant__
         }
         __syncthreads();  // raw counts of the group complete; X may be overwritten
         // a3/a4: per tile
-        batched_topk<CPT, NW>(p, rawbuf, scratch, scratch, p.region_bytes, s_bc, in0, gs, 0u, 1u, wi, lane);
+        if (!(p.cand_dbg & 2u))  // development: skip the selection
+            batched_topk<CPT, NW>(p, rawbuf, scratch, scratch, p.region_bytes, s_bc, in0, gs, 0u, 1u, wi, lane);
         __syncthreads();  // rawbuf / scratch reused by the next group
     }
 }

@@ -79,7 +79,8 @@ struct alignas(64) BatchedParams {
     uint32_t wm_umax;          // per-column-boost wavelet: largest coarse key - 1 (levels = its bits)
     uint32_t cand_min_radius;  // local inhibition, per-column boosts: candidate pruning from this radius on
     uint32_t cand_min_radius_u;  // the same with a uniform boost (sp_select.cuh local_candidates)
-    uint32_t cand_dbg;           // development (SP_CAND_DBG, timing experiments only): 1 skip the beats step
+    uint32_t cand_dbg;           // development (SP_CAND_DBG, timing experiments only): 1 skip the beats step,
+                                 // 2 skip the patch kernel's selection, 4 its gathers
 };
 
 // Tensor-core patch kernel (NEXT-2, sp_patch_mma.cu): raw counts of 128 tile slots per block

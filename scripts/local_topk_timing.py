@@ -40,6 +40,16 @@ def full_learning_state():
     return st, r
 
 
+def learned_state():
+    learn = torch.empty((1000, 540, 960), dtype=torch.uint8, device="cuda")
+    P.synth_frames(learn, 0, 1001, 0.5)
+    sp = P.SpatialPooler(**KW, max_inputs=1000)
+    sp.compute(learn, learn=True)
+    st = sp.get_state()
+    sp.close()
+    return st
+
+
 def time_point(frames, state, radius, cand, reps=10):
     os.environ["SP_CAND_MIN_RADIUS"] = "0" if cand else "100000"
     n = frames.shape[0]
@@ -71,10 +81,14 @@ def main():
     base = P.SpatialPooler(**KW, max_inputs=1)
     idx, perm, _ = base.get_state()
     base.close()
+    which = os.environ.get("STATES", "uniform1,learned,seeded,full_learning").split(",")
     states = {"uniform1": (idx, perm, np.ones(1024, np.float32)),
+              "learned": learned_state(),
               "seeded": (idx, perm, sp_inputs.boosts(7, 1024, 1.0, 2.0)),
               "full_learning": fl_state}
     for name, st in states.items():
+        if name not in which:
+            continue
         for radius in radii:
             ms0, out0, _ = time_point(frames, st, radius, cand=False)
             ms1, out1, w = time_point(frames, st, radius, cand=True)
