@@ -1302,7 +1302,7 @@ __device__ __forceinline__ bool local_candidates(const RowT* row, const uint32_t
         if (__all_sync(full, ok)) t = tt;
     }
     t = max(t, 1u);
-    if (UNIFORM && vmax - t < 64u && scratch_bytes >= kHead + 4u * 8u * 65u) {
+    if (UNIFORM && vmax - t < 160u && scratch_bytes >= kHead + 4u * 8u * 65u) {
         // Uniform boost, few levels: sweep the raw values from the top.  With G = the columns of
         // value > l and E = those of value l (bit masks over all columns, one word per lane), a
         // column c of value l has beats(c) = |G & W(c)| + |E & [lo(c), c)| (equal raw: the lower
@@ -1353,75 +1353,101 @@ __device__ __forceinline__ bool local_candidates(const RowT* row, const uint32_t
         uint32_t gw[NW2], gp[NW2], win[NW2], gtot = 0;
 #pragma unroll
         for (int h = 0; h < NW2; ++h) gw[h] = 0u, gp[h] = 0u, win[h] = 0u;
-        // two levels per step (l and l-1): their E scans interleave, halving the dependent
-        // shuffle chains; G of level l-1 = G | E of level l
-        uint2* sG2 = sE + 65;
-        uint2* sE2 = sG2 + 65;
+        // LV levels per step (l, l-1, .., l-LV+1): their E scans interleave, dividing the
+        // dependent shuffle chains by LV; G of level l-u = G | E of the levels above it
+        constexpr int LV = 4;
+        const uint32_t nlvmax = scratch_bytes >= kHead + 2u * LV * 8u * 65u ? LV : 2u;
+        uint2* tabs = sG;  // [2 LV][65]: G of level u at tabs[2u], E at tabs[2u + 1]
         for (uint32_t l = vmax; l + 1u > t;) {
-            const bool two = l > t;  // l - 1 >= t
-            uint32_t m1[NW2], m2[NW2], e1[NW2], e2[NW2];
-            ge(l, m1);
-            if (two) ge(l - 1u, m2);
+            const uint32_t nlv = min(nlvmax, l - t + 1u);
+            uint32_t m[LV][NW2], e[LV][NW2];
             bool any = false;
 #pragma unroll
-            for (int h = 0; h < NW2; ++h) {
-                e1[h] = m1[h] & ~gw[h];
-                e2[h] = two ? m2[h] & ~m1[h] : 0u;
-                any |= (e1[h] | e2[h]) != 0u;
-            }
-            l = two ? l - 2u : l - 1u;
-            if (!__any_sync(full, any)) {
-                if (two) {
+            for (int u = 0; u < LV; ++u) {
+                if (static_cast<uint32_t>(u) < nlv) {
+                    ge(l - u, m[u]);
+                } else {
 #pragma unroll
-                    for (int h = 0; h < NW2; ++h) gw[h] = m2[h];
+                    for (int h = 0; h < NW2; ++h) m[u][h] = u ? m[u - 1][h] : gw[h];
                 }
+#pragma unroll
+                for (int h = 0; h < NW2; ++h) {
+                    e[u][h] = m[u][h] & ~(u ? m[u - 1][h] : gw[h]);
+                    any |= e[u][h] != 0u;
+                }
+            }
+            l = l >= nlv ? l - nlv : 0u;
+            if (l + 1u <= t && nlv < 1u) break;
+            if (!__any_sync(full, any)) {
+#pragma unroll
+                for (int h = 0; h < NW2; ++h) gw[h] = m[LV - 1][h];
+                if (l + 1u <= t) break;
                 continue;
             }
-            // exclusive prefix counts of E1 and E2 (interleaved scans)
-            uint32_t q1[NW2], q2[NW2];
+            // exclusive prefix counts of the LV E masks (interleaved scans)
+            uint32_t q[LV][NW2];
 #pragma unroll
-            for (int h = 0; h < NW2; ++h) q1[h] = __popc(e1[h]), q2[h] = __popc(e2[h]);
+            for (int u = 0; u < LV; ++u)
+#pragma unroll
+                for (int h = 0; h < NW2; ++h) q[u][h] = __popc(e[u][h]);
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
 #pragma unroll
-                for (int h = 0; h < NW2; ++h) {
-                    const uint32_t a1 = __shfl_up_sync(full, q1[h], d), a2 = __shfl_up_sync(full, q2[h], d);
-                    if (lane >= static_cast<uint32_t>(d)) q1[h] += a1, q2[h] += a2;
-                }
-            }
-            const uint32_t t1 = __shfl_sync(full, q1[0], 31), t2 = __shfl_sync(full, q2[0], 31);
-            const uint32_t u1 = NW2 > 1 ? __shfl_sync(full, q1[NW2 - 1], 31) : 0u;
-            const uint32_t u2 = NW2 > 1 ? __shfl_sync(full, q2[NW2 - 1], 31) : 0u;
-            uint32_t ep1[NW2], ep2[NW2];
+                for (int u = 0; u < LV; ++u)
 #pragma unroll
-            for (int h = 0; h < NW2; ++h) {
-                ep1[h] = (h ? t1 : 0u) + q1[h] - __popc(e1[h]);
-                ep2[h] = (h ? t2 : 0u) + q2[h] - __popc(e2[h]);
-                const uint32_t j = lane + 32u * h;
-                if (j < ncw) {
-                    sG[j] = make_uint2(gw[h], gp[h]);
-                    sE[j] = make_uint2(e1[h], ep1[h]);
-                    sG2[j] = make_uint2(gw[h] | e1[h], gp[h] + ep1[h]);
-                    sE2[j] = make_uint2(e2[h], ep2[h]);
-                }
+                    for (int h = 0; h < NW2; ++h) {
+                        const uint32_t a = __shfl_up_sync(full, q[u][h], d);
+                        if (lane >= static_cast<uint32_t>(d)) q[u][h] += a;
+                    }
             }
-            const uint32_t etot1 = t1 + u1, etot2 = t2 + u2;
-            if (lane == 0) {
-                sG[ncw] = make_uint2(0u, gtot);
-                sE[ncw] = make_uint2(0u, etot1);
-                sG2[ncw] = make_uint2(0u, gtot + etot1);
-                sE2[ncw] = make_uint2(0u, etot2);
+            uint32_t etot[LV], ep[LV][NW2];
+#pragma unroll
+            for (int u = 0; u < LV; ++u) {
+                const uint32_t t0 = __shfl_sync(full, q[u][0], 31);
+                etot[u] = t0 + (NW2 > 1 ? __shfl_sync(full, q[u][NW2 - 1], 31) : 0u);
+#pragma unroll
+                for (int h = 0; h < NW2; ++h) ep[u][h] = (h ? t0 : 0u) + q[u][h] - __popc(e[u][h]);
+            }
+            // tables: G and E of each level (G of level u = G | E of the levels before it)
+            {
+                uint32_t gwu[NW2], gpu[NW2], gtu = gtot;
+#pragma unroll
+                for (int h = 0; h < NW2; ++h) gwu[h] = gw[h], gpu[h] = gp[h];
+#pragma unroll
+                for (int u = 0; u < LV; ++u) {
+                    if (static_cast<uint32_t>(u) < nlv) {
+#pragma unroll
+                        for (int h = 0; h < NW2; ++h) {
+                            const uint32_t j = lane + 32u * h;
+                            if (j < ncw) {
+                                tabs[(2 * u) * 65 + j] = make_uint2(gwu[h], gpu[h]);
+                                tabs[(2 * u + 1) * 65 + j] = make_uint2(e[u][h], ep[u][h]);
+                            }
+                        }
+                        if (lane == 0) {
+                            tabs[(2 * u) * 65 + ncw] = make_uint2(0u, gtu);
+                            tabs[(2 * u + 1) * 65 + ncw] = make_uint2(0u, etot[u]);
+                        }
+                    }
+#pragma unroll
+                    for (int h = 0; h < NW2; ++h) gwu[h] |= e[u][h], gpu[h] += ep[u][h];
+                    gtu += etot[u];
+                }
             }
             __syncwarp();
 #pragma unroll
             for (int h = 0; h < NW2; ++h) {
-                uint32_t e = e1[h] | e2[h];
-                while (e) {
-                    const uint32_t bit = __ffs(e) - 1u, c = 32u * (lane + 32u * h) + bit;
-                    e &= e - 1u;
-                    const bool lv1 = (e1[h] >> bit) & 1u;
-                    const uint2* G = lv1 ? sG : sG2;
-                    const uint2* E = lv1 ? sE : sE2;
+                uint32_t eall = 0;
+#pragma unroll
+                for (int u = 0; u < LV; ++u) eall |= e[u][h];
+                while (eall) {
+                    const uint32_t bit = __ffs(eall) - 1u, c = 32u * (lane + 32u * h) + bit;
+                    eall &= eall - 1u;
+                    uint32_t u = 0;
+#pragma unroll
+                    for (int v = LV - 1; v > 0; --v) u = ((e[v][h] >> bit) & 1u) ? static_cast<uint32_t>(v) : u;
+                    const uint2* G = tabs + (2u * u) * 65u;
+                    const uint2* E = G + 65;
                     const uint32_t lo = c >= radius ? c - radius : 0u, hi1 = min(C, c + radius + 1u);
                     const uint32_t beats = (cnt(G, hi1) - cnt(G, lo)) + (cnt(E, c) - cnt(E, lo));
                     if (beats < k) win[h] |= 1u << bit;
@@ -1429,8 +1455,12 @@ __device__ __forceinline__ bool local_candidates(const RowT* row, const uint32_t
             }
             __syncwarp();  // the tables are rewritten by the next step
 #pragma unroll
-            for (int h = 0; h < NW2; ++h) gw[h] |= e1[h] | e2[h], gp[h] += ep1[h] + ep2[h];
-            gtot += etot1 + etot2;
+            for (int u = 0; u < LV; ++u) {
+#pragma unroll
+                for (int h = 0; h < NW2; ++h) gw[h] |= e[u][h], gp[h] += ep[u][h];
+                gtot += etot[u];
+            }
+            if (l + 1u <= t) break;
         }
 #pragma unroll
         for (int h = 0; h < NW2; ++h)

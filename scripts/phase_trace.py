@@ -15,6 +15,15 @@ sp = P.SpatialPooler(input_width=960, input_height=540, num_columns=C, synapses_
 if seeded:
     import sp_inputs
     sp.set_state(boost=sp_inputs.boosts(7, C))
+if len(sys.argv) > 5 and sys.argv[5] == "learned":  # the state after a 1000-frame learning stream
+    lf = torch.empty((1000, 540, 960), dtype=torch.uint8, device="cuda")
+    P.synth_frames(lf, 0, 1001, 0.5)
+    sl = P.SpatialPooler(input_width=960, input_height=540, num_columns=C, synapses_per_column=S,
+                         min_overlap=4, winners_set_size=40, max_inputs=1000)
+    sl.compute(lf, learn=True)
+    sp.set_state(*sl.get_state())
+    sl.close()
+    del lf
 fr = torch.empty((n, 540, 960), dtype=torch.uint8, device="cuda")
 P.synth_frames(fr, 0, 2002, 0.5)
 for _ in range(3):
