@@ -189,22 +189,27 @@ __device__ __forceinline__ void blur_columns(const EncParams& p, const uint8_t* 
     float ha[K], hb[K];
 #pragma unroll
     for (int i = 0; i < K - 1; ++i) hsum(static_cast<int>(y0) - R + i, ha[i], hb[i]);
-    for (int y = static_cast<int>(y0); y < static_cast<int>(y1); ++y) {
-        hsum(y + R, ha[K - 1], hb[K - 1]);
-        float ma = __fmaf_rn(ha[R], kw[R], 0.0f), mb = __fmaf_rn(hb[R], kw[R], 0.0f);
+    // the window is a register ring: row y0 - R + s lives in slot s mod K, so the loop is unrolled
+    // K times with compile-time slots instead of shifting K - 1 registers per row
+    for (int y = static_cast<int>(y0); y < static_cast<int>(y1); y += K) {
 #pragma unroll
-        for (int j = 1; j <= R; ++j) {
-            ma = __fmaf_rn(__fadd_rn(ha[R + j], ha[R - j]), kw[R + j], ma);
-            mb = __fmaf_rn(__fadd_rn(hb[R + j], hb[R - j]), kw[R + j], mb);
+        for (int u = 0; u < K; ++u) {
+            const int yy = y + u;
+            if (yy >= static_cast<int>(y1)) break;
+            hsum(yy + R, ha[(u + K - 1) % K], hb[(u + K - 1) % K]);
+            float ma = __fmaf_rn(ha[(u + R) % K], kw[R], 0.0f), mb = __fmaf_rn(hb[(u + R) % K], kw[R], 0.0f);
+#pragma unroll
+            for (int j = 1; j <= R; ++j) {
+                ma = __fmaf_rn(__fadd_rn(ha[(u + R + j) % K], ha[(u + R - j) % K]), kw[R + j], ma);
+                mb = __fmaf_rn(__fadd_rn(hb[(u + R + j) % K], hb[(u + R - j) % K]), kw[R + j], mb);
+            }
+            // convertTo(CV_8U): round half to even, saturate
+            const int mua = min(255, max(0, __float2int_rn(ma))), mub = min(255, max(0, __float2int_rn(mb)));
+            const uint8_t* grow = gray + yy * W + x;
+            uint8_t* orow = out + static_cast<size_t>(yy) * W + x;
+            orow[0] = static_cast<int>(grow[0]) - mua > -p.cbias ? 255u : 0u;
+            if (two) orow[1] = static_cast<int>(grow[1]) - mub > -p.cbias ? 255u : 0u;
         }
-        // convertTo(CV_8U): round half to even, saturate
-        const int mua = min(255, max(0, __float2int_rn(ma))), mub = min(255, max(0, __float2int_rn(mb)));
-        const uint8_t* grow = gray + y * W + x;
-        uint8_t* orow = out + static_cast<size_t>(y) * W + x;
-        orow[0] = static_cast<int>(grow[0]) - mua > -p.cbias ? 255u : 0u;
-        if (two) orow[1] = static_cast<int>(grow[1]) - mub > -p.cbias ? 255u : 0u;
-#pragma unroll
-        for (int i = 0; i < K - 1; ++i) ha[i] = ha[i + 1], hb[i] = hb[i + 1];
     }
 }
 
@@ -239,14 +244,23 @@ __device__ __forceinline__ uint32_t chan_sums(uint32_t w0, uint32_t w1, uint32_t
     return __dp4a(w0, m0, __dp4a(w1, m1, __dp4a(w2, m2, 0u)));
 }
 
+// (row, pair) of a thread's first item and the per-step increment: the same for every band,
+// computed once per kernel (a division per band per thread was 4% of the encoder's samples)
+struct PairMap {
+    uint32_t r0, q0, rstep, qstep;
+};
+
 __device__ __forceinline__ void downscale_band_pairs(const EncParams& p, const EncTables& t, uint32_t b,
-                                                     const uint8_t* buf, uint8_t* gray) {
+                                                     const uint8_t* buf, uint8_t* gray, const PairMap& pm) {
     const uint32_t dy0 = b * p.band_rows, dy1 = min(p.H1, dy0 + p.band_rows);
     const uint32_t pairs = p.W1 / 2u;
     const int32_t rb = static_cast<int32_t>(p.row_bytes);
     const uint8_t* buf0 = buf - static_cast<int32_t>(p.band_sy0[b]) * rb;
+    uint32_t r0 = pm.r0, q0 = pm.q0;
     for (uint32_t i = threadIdx.x; i < (dy1 - dy0) * pairs; i += blockDim.x) {
-        const uint32_t dy = dy0 + i / pairs, dx = 2u * (i % pairs);
+        const uint32_t dy = dy0 + r0, dx = 2u * q0;
+        r0 += pm.rstep, q0 += pm.qstep;  // the next item without a division
+        if (q0 >= pairs) q0 -= pairs, ++r0;
         const uint8_t* col = buf0 + 12u * dx;
         const uint32_t j0 = t.yoff[dy], j1 = t.yoff[dy + 1];
         float s[6];
@@ -274,7 +288,7 @@ __device__ __forceinline__ void downscale_band_pairs(const EncParams& p, const E
     }
 }
 
-__global__ void __launch_bounds__(kEncThreads) k_encode(const __grid_constant__ EncParams p) {
+__global__ void __launch_bounds__(kEncThreads, 2) k_encode(const __grid_constant__ EncParams p) {
     extern __shared__ __align__(128) uint8_t sm[];
     __shared__ __align__(8) uint64_t bars[kMaxStages];
     uint8_t* gray = sm;
@@ -302,6 +316,12 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const __grid_constant__ 
     const uint32_t ty = p.W1 <= blockDim.x ? threadIdx.x / p.W1 : 0u;
     const uint32_t tx = p.W1 <= blockDim.x ? threadIdx.x % p.W1 : threadIdx.x;
     const uint32_t sxs = p.W1 <= blockDim.x ? p.W1 : blockDim.x;
+    PairMap pm{};
+    if (p.W1 >= 2u) {
+        const uint32_t pairs = p.W1 / 2u;
+        pm.r0 = threadIdx.x / pairs, pm.q0 = threadIdx.x - pm.r0 * pairs;
+        pm.rstep = blockDim.x / pairs, pm.qstep = blockDim.x - pm.rstep * pairs;
+    }
     const uint32_t nf = p.F > blockIdx.x ? (p.F - blockIdx.x + gridDim.x - 1u) / gridDim.x : 0u;
     const uint32_t total = nf * p.bands;  // (frame, band) sequence of this CTA
     if (threadIdx.x == 0) {
@@ -326,7 +346,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode(const __grid_constant__ 
                 for (uint32_t k = threadIdx.x; k < bytes; k += blockDim.x) buf[k] = g[k];
                 __syncthreads();
             }
-            if (p.xfast && (p.W1 & 1u) == 0u) downscale_band_pairs(p, t, b, buf, gray);
+            if (p.xfast && (p.W1 & 1u) == 0u) downscale_band_pairs(p, t, b, buf, gray, pm);
             else if (ty < ny) downscale_band(p, t, b, buf, gray, ty, tx, ny, sxs);
             __syncthreads();  // the stage is free; the band's gray rows are complete
             if (p.bulk && threadIdx.x == 0 && seq + p.stages < total) {
