@@ -38,6 +38,8 @@ struct EncParams {
     uint32_t stage_bytes, stages;
     uint32_t bulk;             // rows are 16-byte aligned: bulk copies, else cooperative loads
     uint32_t xfast;            // x table = {4dx + j, 0.25}, j < 4 (an exact 4:1 x scale)
+    uint32_t l2hint;           // sp_encode_compute: BGR reads evict-first, binarised writes evict-last
+                               // in L2 (the binarised chunk stays resident for the SP's loads)
     const uint32_t* band_sy0;  // [bands] first source row of the band
     const uint32_t* band_n;    // [bands] source rows of the band
     const uint32_t* yoff;      // [H1 + 1] y-table range of each output row
@@ -88,13 +90,22 @@ __device__ __forceinline__ void issue_band(const EncParams& p, uint32_t f, uint3
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of buf before async writes
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(ba), "r"(bytes) : "memory");
     constexpr uint32_t kChunk = 32768u;
+    uint64_t pol = 0;
+    if (p.l2hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     for (uint32_t off = 0; off < bytes; off += kChunk) {
         const uint32_t n = min(kChunk, bytes - off);
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                static_cast<uint32_t>(__cvta_generic_to_shared(buf + off))),
-            "l"(g + off), "r"(n), "r"(ba)
-            : "memory");
+        if (p.l2hint)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+                "[%3], %4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(buf + off))),
+                "l"(g + off), "r"(n), "r"(ba), "l"(pol)
+                : "memory");
+        else
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    static_cast<uint32_t>(__cvta_generic_to_shared(buf + off))),
+                "l"(g + off), "r"(n), "r"(ba)
+                : "memory");
     }
 }
 
@@ -207,8 +218,19 @@ __device__ __forceinline__ void blur_columns(const EncParams& p, const uint8_t* 
             const int mua = min(255, max(0, __float2int_rn(ma))), mub = min(255, max(0, __float2int_rn(mb)));
             const uint8_t* grow = gray + yy * W + x;
             uint8_t* orow = out + static_cast<size_t>(yy) * W + x;
-            orow[0] = static_cast<int>(grow[0]) - mua > -p.cbias ? 255u : 0u;
-            if (two) orow[1] = static_cast<int>(grow[1]) - mub > -p.cbias ? 255u : 0u;
+            const uint32_t o0 = static_cast<int>(grow[0]) - mua > -p.cbias ? 255u : 0u;
+            const uint32_t o1 = two && static_cast<int>(grow[1]) - mub > -p.cbias ? 255u : 0u;
+            if (p.l2hint) {  // keep the binarised rows in L2 for the SP (sp_encode_compute)
+                uint64_t pol;
+                asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+                asm volatile("st.global.L2::cache_hint.u8 [%0], %1, %2;" ::"l"(orow), "r"(o0), "l"(pol) : "memory");
+                if (two)
+                    asm volatile("st.global.L2::cache_hint.u8 [%0], %1, %2;" ::"l"(orow + 1), "r"(o1), "l"(pol)
+                                 : "memory");
+            } else {
+                orow[0] = static_cast<uint8_t>(o0);
+                if (two) orow[1] = static_cast<uint8_t>(o1);
+            }
         }
     }
 }
@@ -453,6 +475,26 @@ void gaussian_f32(int k, float* kw) {
     kw[n2] = static_cast<float>(1.0 * mul);
 }
 
+sp_status encode_impl(sp_encoder* e, const uint8_t* bgr_dev, uint32_t num_frames, uint8_t* out_dev, void* cuda_stream,
+                      uint32_t l2hint) {
+    if (!e) return efail(SP_E_ARG, "encoder is NULL");
+    if (num_frames == 0) return SP_OK;
+    if (!bgr_dev || !out_dev) return efail(SP_E_ARG, "NULL frame buffer");
+    cudaSetDevice(e->device);
+    sp::EncParams p = e->p;
+    p.src = bgr_dev;
+    p.dst = out_dev;
+    p.F = num_frames;
+    p.bulk = ((reinterpret_cast<uintptr_t>(bgr_dev) & 15u) == 0 && (p.row_bytes & 15u) == 0) ? 1u : 0u;
+    p.l2hint = l2hint;
+    const uint32_t grid = std::min<uint32_t>(num_frames, e->ctas_per_sm * static_cast<uint32_t>(e->sm_count));
+    sp::k_encode<<<grid, sp::kEncThreads, e->smem, static_cast<cudaStream_t>(cuda_stream)>>>(p);
+    e->launches++;
+    const cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) return efail(SP_E_CUDA, cudaGetErrorString(err));
+    return SP_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -667,7 +709,7 @@ sp_status sp_encode_compute(sp_encoder* e, sp_handle* sp, const uint8_t* bgr_dev
     sp_status st = SP_OK;
     for (uint32_t f0 = 0; f0 < num_frames && st == SP_OK; f0 += e->chunk) {
         const uint32_t n = std::min(e->chunk, num_frames - f0);
-        st = sp_encode(e, bgr_dev + static_cast<size_t>(f0) * 3u * e->p.W0 * e->p.H0, n, e->d_chunk, fs);
+        st = encode_impl(e, bgr_dev + static_cast<size_t>(f0) * 3u * e->p.W0 * e->p.H0, n, e->d_chunk, fs, 1u);
         if (st != SP_OK) break;
         const size_t row = static_cast<size_t>(f0) * P;
         st = sp_compute_into(sp, e->d_chunk, n, 0, sdr_dev + row * words, count_dev + row, fs);
@@ -684,21 +726,7 @@ sp_status sp_encode_compute(sp_encoder* e, sp_handle* sp, const uint8_t* bgr_dev
 }
 
 sp_status sp_encode(sp_encoder* e, const uint8_t* bgr_dev, uint32_t num_frames, uint8_t* out_dev, void* cuda_stream) {
-    if (!e) return efail(SP_E_ARG, "encoder is NULL");
-    if (num_frames == 0) return SP_OK;
-    if (!bgr_dev || !out_dev) return efail(SP_E_ARG, "NULL frame buffer");
-    cudaSetDevice(e->device);
-    sp::EncParams p = e->p;
-    p.src = bgr_dev;
-    p.dst = out_dev;
-    p.F = num_frames;
-    p.bulk = ((reinterpret_cast<uintptr_t>(bgr_dev) & 15u) == 0 && (p.row_bytes & 15u) == 0) ? 1u : 0u;
-    const uint32_t grid = std::min<uint32_t>(num_frames, e->ctas_per_sm * static_cast<uint32_t>(e->sm_count));
-    sp::k_encode<<<grid, sp::kEncThreads, e->smem, static_cast<cudaStream_t>(cuda_stream)>>>(p);
-    e->launches++;
-    const cudaError_t err = cudaGetLastError();
-    if (err != cudaSuccess) return efail(SP_E_CUDA, cudaGetErrorString(err));
-    return SP_OK;
+    return encode_impl(e, bgr_dev, num_frames, out_dev, cuda_stream, 0u);
 }
 
 sp_status sp_encoder_get_info(sp_encoder* e, sp_encoder_info* out) {
