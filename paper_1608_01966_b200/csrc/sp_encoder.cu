@@ -178,7 +178,7 @@ __device__ __forceinline__ void downscale_band(const EncParams& p, const EncTabl
 // j = 1..R (OpenCV's AVX2/FMA3 RowVec_32f and symmetric SymmColumnVec_32f order).
 template <int K>
 __device__ __forceinline__ void blur_columns(const EncParams& p, const uint8_t* gray, uint8_t* out, uint32_t x,
-                                             uint32_t y0, uint32_t y1) {
+                                             uint32_t y0, uint32_t y1, uint64_t pol) {
     constexpr int R = K / 2;
     const int W = static_cast<int>(p.W1), H = static_cast<int>(p.H1);
     const bool two = static_cast<int>(x) + 1 < W;
@@ -221,8 +221,6 @@ __device__ __forceinline__ void blur_columns(const EncParams& p, const uint8_t* 
             const uint32_t o0 = static_cast<int>(grow[0]) - mua > -p.cbias ? 255u : 0u;
             const uint32_t o1 = two && static_cast<int>(grow[1]) - mub > -p.cbias ? 255u : 0u;
             if (p.l2hint) {  // keep the binarised rows in L2 for the SP (sp_encode_compute)
-                uint64_t pol;
-                asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
                 asm volatile("st.global.L2::cache_hint.u8 [%0], %1, %2;" ::"l"(orow), "r"(o0), "l"(pol) : "memory");
                 if (two)
                     asm volatile("st.global.L2::cache_hint.u8 [%0], %1, %2;" ::"l"(orow + 1), "r"(o1), "l"(pol)
@@ -236,6 +234,8 @@ __device__ __forceinline__ void blur_columns(const EncParams& p, const uint8_t* 
 }
 
 __device__ __forceinline__ void blur_frame(const EncParams& p, const uint8_t* gray, uint8_t* out) {
+    uint64_t pol = 0;  // L2 evict-last policy of the binarised stores (sp_encode_compute)
+    if (p.l2hint) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     // column pairs x0 = 2c; the rows are split into segments so that all threads have work
     // (the K-1 halo rows of a segment are recomputed)
     const uint32_t pairs = (p.W1 + 1u) / 2u;
@@ -244,13 +244,13 @@ __device__ __forceinline__ void blur_frame(const EncParams& p, const uint8_t* gr
         const uint32_t x = 2u * (t % pairs), sgi = t / pairs;
         const uint32_t y0 = p.H1 * sgi / segs, y1 = p.H1 * (sgi + 1u) / segs;
         switch (p.K) {
-            case 3: blur_columns<3>(p, gray, out, x, y0, y1); break;
-            case 5: blur_columns<5>(p, gray, out, x, y0, y1); break;
-            case 7: blur_columns<7>(p, gray, out, x, y0, y1); break;
-            case 9: blur_columns<9>(p, gray, out, x, y0, y1); break;
-            case 11: blur_columns<11>(p, gray, out, x, y0, y1); break;
-            case 13: blur_columns<13>(p, gray, out, x, y0, y1); break;
-            default: blur_columns<15>(p, gray, out, x, y0, y1); break;
+            case 3: blur_columns<3>(p, gray, out, x, y0, y1, pol); break;
+            case 5: blur_columns<5>(p, gray, out, x, y0, y1, pol); break;
+            case 7: blur_columns<7>(p, gray, out, x, y0, y1, pol); break;
+            case 9: blur_columns<9>(p, gray, out, x, y0, y1, pol); break;
+            case 11: blur_columns<11>(p, gray, out, x, y0, y1, pol); break;
+            case 13: blur_columns<13>(p, gray, out, x, y0, y1, pol); break;
+            default: blur_columns<15>(p, gray, out, x, y0, y1, pol); break;
         }
     }
 }
