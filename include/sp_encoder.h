@@ -76,14 +76,16 @@ sp_status sp_encode(sp_encoder* enc, const uint8_t* bgr_dev, uint32_t num_frames
  * buffer that is the stream's persisting-L2 access-policy window for the call (the binarised
  * frames go from the encoder's stores to the SP's TMA loads through L2, not HBM: the
  * "encoder fused into staging" of SURVEY §8(f) NEXT-3 at the memory level; the device-wide
- * persisting-L2 limit is raised to the buffer size at first use).  Chunk: 1024 frames
- * (env SP_ENC_CHUNK).
+ * persisting-L2 limit is raised to the buffer size for the call and restored at its end, which
+ * makes the call wait for its last chunk; the encoder's BGR reads are marked L2 evict-first and
+ * its binarised writes evict-last).  Chunk: 1024 frames (env SP_ENC_CHUNK).
  *   sp:        an SP handle whose input frame is dst_width x dst_height, on the same device;
  *   bgr_dev:   uint8[num_frames][src_height][src_width][3], device memory;
  *   sdr_dev:   uint32[num_frames * P][sdr_words], count_dev: uint32[num_frames * P], device
  *              memory (P = the SP's inputs per frame); they become the SP's last results.
  * Errors: SP_E_ARG (NULL, device mismatch), SP_E_CONFIG (frame size mismatch), SP_E_OOM,
- * the SP's errors (e.g. chunk * P > max_inputs: SP_E_ARG).  Asynchronous on cuda_stream. */
+ * the SP's errors (e.g. chunk * P > max_inputs: SP_E_ARG).  Ordered on cuda_stream; returns after
+ * the last chunk completed when the persisting set-aside was raised. */
 sp_status sp_encode_compute(sp_encoder* enc, sp_handle* sp, const uint8_t* bgr_dev, uint32_t num_frames,
                             uint32_t* sdr_dev, uint32_t* count_dev, void* cuda_stream);
 

@@ -674,15 +674,11 @@ sp_status sp_encode_compute(sp_encoder* e, sp_handle* sp, const uint8_t* bgr_dev
             e->d_chunk = nullptr;
             return efail(SP_E_OOM, cudaGetErrorString(err));
         }
-        // persisting L2 set-aside for the chunk buffer (device-wide limit, raised only)
+        // persisting L2 set-aside for the chunk buffer: raised for the duration of each call
+        // and restored afterwards (a standing set-aside shrinks L2 for every other kernel)
         int max_persist = 0;
         cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, e->device);
-        const size_t want = std::min<size_t>(static_cast<size_t>(max_persist), e->chunk * fbytes);
-        size_t cur = 0;
-        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-        if (want > cur) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-        e->l2_window = std::min<size_t>(cur, e->chunk * fbytes);
+        e->l2_window = std::min<size_t>(static_cast<size_t>(max_persist), e->chunk * fbytes);
         // an internal stream whose access-policy window is the chunk buffer (the caller's stream,
         // possibly the legacy default stream, is left untouched); ordered by events
         cudaError_t es = cudaStreamCreateWithFlags(&e->fstream, cudaStreamNonBlocking);
@@ -702,6 +698,10 @@ sp_status sp_encode_compute(sp_encoder* e, sp_handle* sp, const uint8_t* bgr_dev
         }
         (void)cudaGetLastError();
     }
+    size_t old_limit = 0;
+    cudaDeviceGetLimit(&old_limit, cudaLimitPersistingL2CacheSize);
+    if (e->l2_window > old_limit) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, e->l2_window);
+    (void)cudaGetLastError();
     cudaStream_t fs = e->fstream;
     cudaError_t ee = cudaEventRecord(e->fev[0], s);
     if (ee == cudaSuccess) ee = cudaStreamWaitEvent(fs, e->fev[0], 0);
@@ -717,6 +717,13 @@ sp_status sp_encode_compute(sp_encoder* e, sp_handle* sp, const uint8_t* bgr_dev
     // the caller's stream continues after the last chunk
     ee = cudaEventRecord(e->fev[1], fs);
     if (ee == cudaSuccess) ee = cudaStreamWaitEvent(s, e->fev[1], 0);
+    if (e->l2_window > old_limit) {
+        // the persisting lines go back to normal once the SP has read the last chunk
+        cudaStreamSynchronize(fs);
+        cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, old_limit);
+        (void)cudaGetLastError();
+    }
     if (st != SP_OK) return efail(st, sp_last_error());
     if (ee != cudaSuccess) return efail(SP_E_CUDA, cudaGetErrorString(ee));
     // the winners of the whole call are the SP's "last results" (sp_winners, sp_histograms)

@@ -331,24 +331,32 @@ bool encode_packed_tmap(CUtensorMap* map, const uint32_t* planes, uint32_t words
 // from an HBM term and a per-CTA term (bytes at a per-SM rate, transpose ALU cycles).
 void plan_batched_grid(const Geometry& g, uint32_t nwin, uint32_t n, int sm_count,
                        const int* max_clusters, uint32_t* groups, uint32_t* Kout) {
+    // Time model, fitted to measurements (960x540, C 1024, S 256): a CTA streams
+    // every window of its share as 32-input boxes whatever its group size (rows of the next
+    // group are L2 hits), at ~47 GB/s per SM (7.6 us per 11264-pixel window), so its time is
+    // ceil(nwin / K) windows; the chip's HBM bounds the whole batch; the cluster tail (DSMEM sum
+    // of the partial counts, one warp per input's selection) grows with K: ~5 + 4.5 K us.
+    // K <= 6: 8-CTA clusters measured slower (512 frames: 0.130 ms vs 0.089 at K = 6).
     const double hbm_bpc = 3400.0;   // chip HBM bytes per SM-cycle (~6.5 TB/s @ 1.9 GHz)
-    const double sm_bpc = 48.0;      // one SM's sustainable stream rate, bytes per cycle
-    const double alu_per_px = 0.65;  // transpose cycles per pixel per CTA (32 inputs at once)
+    const double sm_bpc = 24.7;      // one SM's sustained box-stream rate, bytes per cycle
+    const double cyc_us = 1900.0;
     const uint32_t gmin = (n + 31u) / 32u;
     double best = 1e300;
     uint32_t bestG = gmin, bestK = 1;
-    for (uint32_t K = 1; K <= 8; ++K) {
+    const char* fk = std::getenv("SP_FORCE_K");  // development: cluster size K (timing experiments)
+    const uint32_t force_k = fk ? static_cast<uint32_t>(std::atoi(fk)) : 0u;
+    const char* fg = std::getenv("SP_FORCE_FULL_GROUPS");  // development: groups of 32 inputs
+    for (uint32_t K = 1; K <= (force_k ? 8u : 6u); ++K) {
         if (K > nwin) break;
+        if (force_k && K != force_k) continue;
         int cap = max_clusters ? max_clusters[K] : sm_count / static_cast<int>(K);
         if (cap <= 0) continue;
-        const uint32_t G = std::max<uint32_t>(gmin, std::min<uint32_t>(n, static_cast<uint32_t>(cap)));
+        const uint32_t G = fg ? gmin : std::max<uint32_t>(gmin, std::min<uint32_t>(n, static_cast<uint32_t>(cap)));
         const uint32_t waves = (G + cap - 1) / cap;
-        const uint32_t gs = (n + G - 1) / G;
-        const double bytes_cta = static_cast<double>(gs) * g.nbits / K;
-        const double alu_cta = alu_per_px * g.nbits / K +
-                               ((gs + K - 1) / K > 0 ? 6.0 * g.keyBits * g.ncw : 0.0);
-        const double t = std::max(static_cast<double>(n) * g.nbits / hbm_bpc,
-                                  waves * std::max(bytes_cta / sm_bpc, alu_cta));
+        const double win_px = static_cast<double>(g.nbits) / nwin;
+        const double stream_cta = ((nwin + K - 1) / K) * 32.0 * win_px / sm_bpc;
+        const double t = std::max(static_cast<double>(n) * g.nbits / hbm_bpc, waves * stream_cta) +
+                         (5.0 + 4.5 * K) * cyc_us;
         if (t < best * 0.98) {
             best = t;
             bestG = G;
