@@ -694,3 +694,30 @@ def test_local_candidates_fallback_mixing(radius, boost_mode, monkeypatch):
     results = [ora.step(x, False) for x in O.encode(frames, cfg)]
     check_sdrs(results, *run_gpu_sdr(make_sp(cfg, state, P.SP_PATH_BATCHED, max_inputs=64, record=False), frames))
     check_results(results, *run_gpu(make_sp(cfg, state, P.SP_PATH_BATCHED, max_inputs=64), frames))
+
+
+@pytest.mark.parametrize("n,radius,boost_mode", [(512, 0, "uniform1"), (1024, 0, "seeded"), (2048, 0, "uniform1"),
+                                                 (512, 506, "seeded"), (1024, 80, "uniform1")])
+def test_strong_shard_launch_configs(n, radius, boost_mode):
+    """The shards one GPU owns at G = 8, 4, 2 of a 4096-frame batch (bench strong_shards):
+    the planner splits each group's windows over clusters of K = 6, 4, 2 CTAs whose partial
+    counts are summed over DSMEM before the selection; recording off (the timed path) against
+    the oracle on sampled frames, the winner-count invariant on all (global inhibition)."""
+    cfg = headline_cfg(inhibition_radius=radius)
+    state = with_boost(perturbed_state(cfg), boost_mode)
+    sp = make_sp(cfg, state, max_inputs=n, record=False)
+    frames = torch.empty((n, 540, 960), dtype=torch.uint8, device=DEV)
+    P.synth_frames(frames, 0, 2002, rho=0.5)
+    sp.compute(frames)
+    sdr, counts = sp.winners()
+    torch.cuda.synchronize()
+    pl = sp.info()["plan"]
+    assert pl["path"] == P.SP_PATH_BATCHED and pl["cluster"] > 1, pl
+    sdr, counts = sdr.cpu().numpy(), counts.cpu().numpy()
+    rng = np.random.default_rng(n + radius)
+    sample = sorted(set(rng.choice(n, 6, replace=False).tolist()) | {0, n - 1})
+    ora = O.SpatialPoolerOracle(cfg, state)
+    for f in sample:
+        res = ora.step(O.encode(sp_inputs.frames(2002, f, 1, 540, 960, rho=0.5), cfg)[0], False)
+        assert np.array_equal(sdr[f], sdr_of(res.active)), f"winners mismatch at frame {f}"
+        assert counts[f] == res.active.sum()
