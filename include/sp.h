@@ -132,6 +132,8 @@ typedef struct sp_plan_info {
     uint32_t reason;             /* why not batched: 0 eligible, else bitmask */
     uint32_t tensor_cores;       /* patch mode: 1 if the overlap runs as a tcgen05 kind::i8 GEMM
                                     (NEXT-2; groups = blocks of 4 tile-rows, cluster = C32/128) */
+    uint32_t group_inputs;       /* whole frames: inputs per group (the TMA box rows, <= 32);
+                                    group g = inputs [g*group_inputs, min(n, (g+1)*group_inputs)) */
 } sp_plan_info;
 
 /* Run-time information about a handle. */

@@ -30,6 +30,10 @@
 
 namespace cg = cooperative_groups;
 
+#ifndef SP_RELEASE_ACQREL  // development A/B: 1 = the round-2 acq_rel stage release
+#define SP_RELEASE_ACQREL 0
+#endif
+
 namespace sp {
 
 namespace {
@@ -108,9 +112,29 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, const Transpose
 // One elected lane of the (converged) warp adds 1 to a shared counter with acq_rel
 // semantics; returns true on that lane iff the counter was at NW-1 mod NW (i.e. this warp
 // is the last of the CTA's NW warps to release the stage; NW is a power of two).
-template <uint32_t NW>
+// RELAXED: a relaxed add, for callers whose reads of the stage have all returned (their values
+// consumed into registers before the call, the warp converged): nothing is left to order, and
+// the acq_rel fence waited on every outstanding load of the thread (the ELL prefetch).
+template <uint32_t NW, bool RELAXED = false>
 __device__ __forceinline__ bool warp_release_is_last(uint32_t addr) {
     uint32_t last;
+    if (RELAXED) {
+        asm volatile(
+            "{\n"
+            ".reg .pred P1, P2;\n"
+            ".reg .b32 old;\n"
+            "elect.sync _|P1, 0xffffffff;\n"
+            "mov.u32 old, 0;\n"
+            "@P1 atom.relaxed.cta.shared::cta.add.u32 old, [%1], 1;\n"
+            "and.b32 old, old, %2;\n"
+            "setp.eq.and.u32 P2, old, %2, P1;\n"
+            "selp.u32 %0, 1, 0, P2;\n"
+            "}\n"
+            : "=r"(last)
+            : "r"(addr), "n"(NW - 1)
+            : "memory");
+        return last != 0;
+    }
     asm volatile(
         "{\n"
         ".reg .pred P1, P2;\n"
@@ -141,6 +165,34 @@ __device__ __forceinline__ uint32_t nz_flags(uint32_t v, uint32_t one) {
     return (t | v) & 0x80808080u;
 }
 
+#ifndef SP_MASK_SHIFT  // development A/B: 0 = the round-1 IMAD.HI merge
+#define SP_MASK_SHIFT 1
+#endif
+#if SP_MASK_SHIFT
+// Round 2: word k's flags (bits 8b+7) shifted right by k and added (disjoint bits): pixel 4k+b
+// lands at bit 8b+7-k, all 32 distinct; 7 IMAD.HI instead of 7 (IMAD.HI + LOP3) + IMAD + LOP3.
+__device__ __forceinline__ uint32_t nonzero_mask32(const uint4 a, const uint4 b, uint32_t one) {
+    const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    // the shifted flags are disjoint, so OR = ADD: one mad.hi (FMA pipe) per word shifts by
+    // multiplying with 2^(32-k) and accumulates; no ALU op for the merge
+    uint32_t m = nz_flags(v[0], one);
+    // (the multiplier goes through the run-time `one`, or ptxas turns the mad.hi into LEA.HI on
+    // the ALU pipe, the loop's bottleneck)
+#define SP_MADHI_ACC(k) asm("mad.hi.u32 %0, %1, %2, %0;" : "+r"(m) : "r"(nz_flags(v[k], one)), "r"(one << (32 - (k))))
+    SP_MADHI_ACC(1);
+    SP_MADHI_ACC(2);
+    SP_MADHI_ACC(3);
+    SP_MADHI_ACC(4);
+    SP_MADHI_ACC(5);
+    SP_MADHI_ACC(6);
+    SP_MADHI_ACC(7);
+#undef SP_MADHI_ACC
+    return m;
+}
+
+// Pixel (0..31 within a block) whose flag ends at bit j of nonzero_mask32's result.
+__device__ __forceinline__ uint32_t pixel_of_bit(uint32_t j) { return 4u * (7u - (j & 7u)) + (j >> 3); }
+#else
 __device__ __forceinline__ uint32_t nonzero_mask32(const uint4 a, const uint4 b, uint32_t one) {
     const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
     uint32_t m = 0;
@@ -164,6 +216,7 @@ __device__ __forceinline__ uint32_t pixel_of_bit(uint32_t j) {
     const uint32_t base = b == 0 ? 0u : (b == 1 ? 7u : (b == 2 ? 15u : 23u));
     return 4u * (j - base) + b;
 }
+#endif
 
 struct Planes {
     uint32_t ones, twos, fours;
@@ -263,14 +316,18 @@ __global__ void __launch_bounds__(NT, 1)
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr uint32_t NW = NT / 32;        // warps
     constexpr uint32_t BPW = 32u / NW;      // 32-pixel blocks per warp per chunk
-    constexpr uint32_t SB = PK ? 32u * (kChunkBits / 8u) : kStageBytes;  // bytes per stage
+    constexpr uint32_t SB = PK ? 32u * (kChunkBits / 8u) : kStageBytes;  // bytes per 32-row stage
     static_assert(!PK || NW == 16, "the packed staging splits 16 warps into two halves of 8 x 4 blocks");
     const uint32_t tid = threadIdx.x, lane = tid & 31u, wi = tid >> 5;
     const uint32_t NST = p.stages;
+    // uint8 frames: a stage is 8 boxes of `rows` x 128 B packed back to back (rows * 1 KiB), so
+    // groups of fewer than 32 inputs fit more stages in the ring; packed: 4 KiB boxes of 32 rows
+    const uint32_t SBs = PK ? SB : p.rows * 1024u;
+    const uint32_t box_pitch = p.rows * kBoxBytes;  // bytes between the boxes of a stage
 
     uint8_t* stage_base = smem;  // 1024-aligned (swizzle-128B boxes)
     uint16_t* rawbuf = reinterpret_cast<uint16_t*>(stage_base);  // after streaming
-    uint8_t* region = smem + NST * SB;
+    uint8_t* region = smem + p.ring_bytes;
     uint32_t* words = reinterpret_cast<uint32_t*>(region);
     uint32_t* s_bc = reinterpret_cast<uint32_t*>(region + p.region_bytes);
     uint64_t* bars = reinterpret_cast<uint64_t*>(s_bc + p.C32);
@@ -278,10 +335,11 @@ __global__ void __launch_bounds__(NT, 1)
 
     const uint32_t K = p.K;
     const uint32_t group = blockIdx.x / K, rank = blockIdx.x % K;
-    const uint32_t in0 = static_cast<uint32_t>(static_cast<uint64_t>(group) * p.num_inputs / p.groups);
-    const uint32_t in1 =
-        static_cast<uint32_t>(static_cast<uint64_t>(group + 1) * p.num_inputs / p.groups);
-    const uint32_t gs = in1 - in0;  // 1..32 inputs in this group
+    const uint32_t in0 = group * p.rows;
+    const uint32_t in1 = min(p.num_inputs, in0 + p.rows);
+    const uint32_t gs = in1 - in0;  // 1..rows inputs in this group
+    // bytes a stage's boxes deliver: rows past the batch are zero-filled by TMA and counted
+    const uint32_t tx_bytes = PK ? SB / 32u * p.rows : SBs;
     const uint32_t w0 = rank * p.nwin / K, w1 = (rank + 1) * p.nwin / K;
     const uint32_t pix_begin = w0 * p.Lw;
     const uint32_t pix_end = min(w1 * p.Lw, p.nbits);
@@ -305,20 +363,22 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();
 
     // Producer step for chunk j (one thread): expect the stage's bytes, then 8 TMA boxes of
-    // 128 pixels x 32 inputs (rows beyond the batch and pixels beyond nbits are zero-filled).
+    // 128 pixels x `rows` inputs back to back (rows beyond the batch and pixels beyond nbits are
+    // zero-filled; lanes >= gs read the next box's rows and are masked by lane_ok).
     // Called by thread 0 for the prologue and afterwards by the lane that releases a stage
     // last, so the ring refills without any CTA-wide barrier.
     auto issue = [&](uint32_t j, uint32_t st) {
+        if (p.bdbg & 8u) return;  // development: consumer-only timing (no loads)
         const uint32_t x0 = pix_begin + j * kChunkBits;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive_expect_tx(&bars[st], SB);
-        uint8_t* dst = stage_base + st * SB;
+        mbar_arrive_expect_tx(&bars[st], tx_bytes);
+        uint8_t* dst = stage_base + st * SBs;
         if (PK) {
-            tma_box_g2s(dst, &p.tmap, x0 / 32u, in0, &bars[st]);  // {32 words, 32 inputs}
+            tma_box_g2s(dst, &p.tmap, x0 / 32u, in0, &bars[st]);  // {32 words, rows inputs}
         } else {
 #pragma unroll
             for (uint32_t b = 0; b < kChunkBits / kBoxBytes; ++b)
-                tma_box_g2s(dst + b * 32u * kBoxBytes, &p.tmap, x0 + b * kBoxBytes, in0, &bars[st]);
+                tma_box_g2s(dst + b * box_pitch, &p.tmap, x0 + b * kBoxBytes, in0, &bars[st]);
         }
     };
     if (tid == 0) {
@@ -331,13 +391,16 @@ __global__ void __launch_bounds__(NT, 1)
     const uint32_t lane_ok = lane < gs ? 0xFFFFFFFFu : 0u;
     const uint32_t pob = pixel_of_bit(lane);  // pixel of the word this lane writes per block
     // lane f reads its 32 bytes of block blk from box blk/4, row f, 16-byte slots
-    // 2*(blk%4) and +1, swizzled by XOR with (f % 8) (CU_TENSOR_MAP_SWIZZLE_128B); the
-    // second slot is the first XOR 16 bytes
+    // 2*(blk%4) and +1, swizzled by XOR with bits 7..9 of the row's shared-memory address
+    // (CU_TENSOR_MAP_SWIZZLE_128B; a stage starts 1 KiB-aligned, a box at a multiple of
+    // rows x 128 B, so row f of box b is 128-byte row b*rows + f of the stage); the second
+    // slot is the first XOR 16 bytes
     uint32_t rd[BPW];
 #pragma unroll
     for (uint32_t i = 0; i < BPW; ++i) {
         const uint32_t blk = wi + NW * i;
-        rd[i] = (blk >> 2) * (32u * kBoxBytes) + lane * kBoxBytes + (((2u * (blk & 3u)) ^ (lane & 7u)) << 4);
+        const uint32_t r128 = (blk >> 2) * p.rows + lane;
+        rd[i] = r128 * kBoxBytes + (((2u * (blk & 3u)) ^ (r128 & 7u)) << 4);
     }
     // packed: lane f reads words 4(wi%8) .. +3 of row f (16-byte slot wi%8 of the 128 B row,
     // swizzled by XOR with f % 8: the 8 lanes of each LDS.128 phase hit 8 distinct slots)
@@ -417,11 +480,11 @@ __global__ void __launch_bounds__(NT, 1)
             if (st >= NST) st -= NST, phase ^= 1u;
         }
         for (uint32_t q = 0; q < (PK ? 0u : nch); ++q) {
-            mbar_wait(&bars[st], phase);
+            if (!(p.bdbg & 8u)) mbar_wait(&bars[st], phase);
             // a1: warp wi turns blocks wi, wi+NW, .. (32 pixels x 32 inputs each) into 32
             // bit-sliced words per block
             {
-                const uint8_t* stg = stage_base + st * kStageBytes;
+                const uint8_t* stg = stage_base + st * SBs;
                 uint32_t m[BPW];
 #pragma unroll
                 for (uint32_t i = 0; i < BPW; ++i) {
@@ -429,12 +492,25 @@ __global__ void __launch_bounds__(NT, 1)
                     const uint4 b = *reinterpret_cast<const uint4*>(stg + (rd[i] ^ 16u));
                     m[i] = nonzero_mask32(a, b, p.one) & lane_ok;
                 }
+                // release the stage as soon as the warp's bytes are in registers (the flags
+                // consume every loaded value; the warp converges before the elected lane's
+                // release), so the refill's TMA latency overlaps the transposes; the warp that
+                // releases it last refills it (chunk j + NST)
+                if (!(p.bdbg & 36u)) {  // (development: 32 = no release at all, with 8 only)
 #pragma unroll
-                for (uint32_t i = 0; i < BPW; ++i)
-                    X[q * kChunkBits + (wi + NW * i) * 32u + pob] = warp_transpose32(m[i], tl);
+                    for (uint32_t i = 0; i < BPW; ++i) asm volatile("" ::"r"(m[i]));
+                    __syncwarp();
+                    if (warp_release_is_last<NW, !SP_RELEASE_ACQREL>(released_addr + 4u * st) && j + NST < nchunks)
+                        issue(j + NST, st);
+                }
+                if (!(p.bdbg & 2u)) {
+#pragma unroll
+                    for (uint32_t i = 0; i < BPW; ++i)
+                        X[q * kChunkBits + (wi + NW * i) * 32u + pob] = warp_transpose32(m[i], tl);
+                }
             }
-            // release the stage; the warp that releases it last refills it (chunk j + NST)
-            if (warp_release_is_last<NW>(released_addr + 4u * st) && j + NST < nchunks)
+            // (development switch 4: release after the transposes, as before)
+            if ((p.bdbg & 4u) && warp_release_is_last<NW>(released_addr + 4u * st) && j + NST < nchunks)
                 issue(j + NST, st);
             ++j;
             if (++st == NST) {
@@ -448,7 +524,7 @@ __global__ void __launch_bounds__(NT, 1)
         // a2: bit-sliced gather-count of this window's synapses (ELL, 8 slots per block)
 #pragma unroll
         for (int i = 0; i < CPT; ++i) {
-            const uint32_t nb = pnb[i];
+            const uint32_t nb = (p.bdbg & 1u) ? 0u : pnb[i];
             const uint4* e = p.ell + poff[i] + lane;
 #pragma unroll
             for (uint32_t bk = 0; bk < PE; ++bk) {
@@ -498,7 +574,7 @@ __global__ void __launch_bounds__(NT, 1)
 
     // idle shared memory behind the raw counts: the rest of the ring and the X windows
     const uint32_t raw_bytes = (32u * p.C32 * 2u + 127u) & ~127u;
-    const uint32_t big_bytes = NST * SB >= raw_bytes ? NST * SB - raw_bytes + p.region_bytes : 0u;
+    const uint32_t big_bytes = p.ring_bytes >= raw_bytes ? p.ring_bytes - raw_bytes + p.region_bytes : 0u;
     batched_topk<CPT, NW>(p, rawbuf, region, smem + raw_bytes, big_bytes, s_bc, in0, gs, rank, K, wi, lane);
     if (K > 1) cluster.sync();  // peers may still read this CTA's partial counts
     if (trace) {

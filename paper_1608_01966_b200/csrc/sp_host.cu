@@ -165,21 +165,29 @@ BatchedLayout plan_batched_layout(const Geometry& g, int max_smem) {
     const uint32_t nbits_r = (g.nbits + kChunkBits - 1) / kChunkBits * kChunkBits;
     const char* es = std::getenv("SP_STAGES");  // development overrides (experiments only)
     const char* eb = std::getenv("SP_XBUFS");
+    const char* er = std::getenv("SP_RING_KB");
     const uint32_t want_stages = es ? static_cast<uint32_t>(std::atoi(es)) : 0u;
     const uint32_t want_xbufs = eb ? static_cast<uint32_t>(std::atoi(eb)) : 0u;
+    const uint32_t want_ring = er ? static_cast<uint32_t>(std::atoi(er)) * 1024u : 0u;
     // preference (measured on B200, 4096 x 960x540, C=1024, 512 threads, ELL prefetch):
     // 4 stages + double-buffered X 0.376 ms; 4 stages, one X 0.380; 3 stages + 2 X 0.383;
     // 3 stages, one X 0.384.  (The 1024-thread kernel without prefetch preferred one X.)
     // C32 > 1024 (4 column-warps per warp, no ELL prefetch registers): one X window wins
-    // (C=2048, S=256: 0.458 vs 0.494 ms).
-    const uint32_t pref2[6][2] = {{4, 2}, {4, 1}, {3, 2}, {3, 1}, {2, 1}, {2, 2}};
-    const uint32_t pref1[6][2] = {{4, 1}, {3, 1}, {2, 1}, {4, 2}, {3, 2}, {2, 2}};
+    // (C=2048, S=256: 0.458 vs 0.494 ms).  Round 2: a stage is `rows` KiB, so a 140 KiB ring
+    // holds 5 stages of 28-input groups (the headline's) where 4 x 32 KiB held 4.
+    const uint32_t K32 = kStageBytes;
+    const uint32_t pref2[9][2] = {{5 * 28672u, 2}, {4 * K32, 2}, {4 * K32, 1}, {3 * K32, 2}, {3 * K32, 1},
+                                  {2 * K32, 1},    {2 * K32, 2}, {5 * K32, 1}, {5 * K32, 2}};
+    const uint32_t pref1[9][2] = {{4 * K32, 1}, {3 * K32, 1}, {2 * K32, 1}, {4 * K32, 2}, {3 * K32, 2},
+                                  {2 * K32, 2}, {5 * K32, 1}, {5 * K32, 2}, {5 * 28672u, 1}};
     const auto& options = g.C32 > 1024u ? pref1 : pref2;
     for (const auto& o : options) {
-        const uint32_t stages = o[0], xbufs = o[1];
-        if ((want_stages && stages != want_stages) || (want_xbufs && xbufs != want_xbufs)) continue;
-        if (stages * kStageBytes < counts_bytes) continue;
-        const int64_t avail = static_cast<int64_t>(max_smem) - stages * kStageBytes - fixed;
+        const uint32_t ring = o[0], xbufs = o[1], stages = ring / K32;
+        if ((want_stages && (stages != want_stages || ring % K32)) || (want_xbufs && xbufs != want_xbufs) ||
+            (want_ring && ring != want_ring))
+            continue;
+        if (ring < counts_bytes) continue;
+        const int64_t avail = static_cast<int64_t>(max_smem) - ring - fixed;
         if (avail < 8 * static_cast<int64_t>(kChunkBits + 1)) continue;
         // largest Lw (multiple of the chunk, local idx < 65536) with xbufs*(Lw+1)*4 <= avail
         uint32_t Lw = static_cast<uint32_t>((avail / 4 / xbufs - 1) / kChunkBits * kChunkBits);
@@ -196,6 +204,7 @@ BatchedLayout plan_batched_layout(const Geometry& g, int max_smem) {
         Lw = (per + kChunkBits - 1) / kChunkBits * kChunkBits;
         L.ok = true;
         L.stages = stages;
+        L.ring_bytes = ring;
         L.xbufs = xbufs;
         L.Lw = Lw;
         L.nwin = (g.nbits + Lw - 1) / Lw;
@@ -204,7 +213,7 @@ BatchedLayout plan_batched_layout(const Geometry& g, int max_smem) {
         // coarse-key bit-planes (ncw x 16 <= 1024 words), 16 warps
         const uint32_t topk_bytes = std::max(32u * 64u * 8u, std::max(32u * 640u * 4u, 16u * 1024u * 4u));
         L.region_bytes = (std::max(xbufs * (Lw + 1u) * 4u, topk_bytes) + 127u) & ~127u;
-        L.smem_bytes = stages * kStageBytes + L.region_bytes + g.C32 * 4u + stages * 12u;
+        L.smem_bytes = ring + L.region_bytes + g.C32 * 4u + BatchedLayout::kMaxStages * 12u;
         if (static_cast<int64_t>(L.smem_bytes) > max_smem) {
             L.ok = false;
             continue;
@@ -288,7 +297,7 @@ bool encode_mma_tmap(CUtensorMap* b, const uint8_t* frames, const Geometry& g, u
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-bool encode_frames_tmap(CUtensorMap* map, const uint8_t* frames, uint32_t nbits, uint32_t rows) {
+bool encode_frames_tmap(CUtensorMap* map, const uint8_t* frames, uint32_t nbits, uint32_t rows, uint32_t box_rows) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q{};
@@ -300,7 +309,7 @@ bool encode_frames_tmap(CUtensorMap* map, const uint8_t* frames, uint32_t nbits,
     }
     const cuuint64_t dims[2] = {nbits, rows};
     const cuuint64_t strides[1] = {nbits};
-    const cuuint32_t box[2] = {kBoxBytes, 32u};
+    const cuuint32_t box[2] = {kBoxBytes, box_rows};
     const cuuint32_t estr[2] = {1u, 1u};
     return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(frames), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -308,7 +317,7 @@ bool encode_frames_tmap(CUtensorMap* map, const uint8_t* frames, uint32_t nbits,
 }
 
 // Bit-planes uint32[rows][words] (words % 4 == 0: 16-byte row stride), box {32 words, 32 rows}.
-bool encode_packed_tmap(CUtensorMap* map, const uint32_t* planes, uint32_t words, uint32_t rows) {
+bool encode_packed_tmap(CUtensorMap* map, const uint32_t* planes, uint32_t words, uint32_t rows, uint32_t box_rows) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q{};
@@ -320,51 +329,63 @@ bool encode_packed_tmap(CUtensorMap* map, const uint32_t* planes, uint32_t words
     }
     const cuuint64_t dims[2] = {words, rows};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(words) * 4u};
-    const cuuint32_t box[2] = {kChunkBits / 32u, 32u};
+    const cuuint32_t box[2] = {kChunkBits / 32u, box_rows};
     const cuuint32_t estr[2] = {1u, 1u};
     return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(planes), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Groups of <= 32 inputs and cluster size K: estimated time of each K
-// from an HBM term and a per-CTA term (bytes at a per-SM rate, transpose ALU cycles).
+// Groups of R <= 32 inputs and cluster size K: estimated time of each (K, R)
+// from an HBM term, a per-CTA streaming term and the cluster tail.
 void plan_batched_grid(const Geometry& g, uint32_t nwin, uint32_t n, int sm_count,
-                       const int* max_clusters, uint32_t* groups, uint32_t* Kout) {
-    // Time model, fitted to measurements (960x540, C 1024, S 256): a CTA streams
-    // every window of its share as 32-input boxes whatever its group size (rows of the next
-    // group are L2 hits), at ~47 GB/s per SM (7.6 us per 11264-pixel window), so its time is
-    // ceil(nwin / K) windows; the chip's HBM bounds the whole batch; the cluster tail (DSMEM sum
-    // of the partial counts, one warp per input's selection) grows with K: ~5 + 4.5 K us.
-    // K <= 6: 8-CTA clusters measured slower (512 frames: 0.130 ms vs 0.089 at K = 6).
-    const double hbm_bpc = 3400.0;   // chip HBM bytes per SM-cycle (~6.5 TB/s @ 1.9 GHz)
-    const double sm_bpc = 24.7;      // one SM's sustained box-stream rate, bytes per cycle
-    const double cyc_us = 1900.0;
+                       const int* max_clusters, uint32_t* groups, uint32_t* Kout, uint32_t* Rout) {
+    // Time model, fitted to measurements (960x540, C 1024, S 256): a CTA's time is
+    // its ceil(nwin / K) windows at ~0.7 us per 1024-pixel chunk whatever its rows R (16..32:
+    // the per-SM transpose/flag/release work, not HBM, sets the pace: 4096 frames on one CTA per
+    // SM and 512 frames on 6-CTA clusters both spend ~7 us per 10-chunk window); R only decides
+    // how many groups (clusters) there are, so one wave needs G = ceil(n / R) <= cap; the chip's
+    // HBM (~7 TB/s) bounds the whole batch; the cluster tail (DSMEM sum of the partial counts,
+    // one warp per input's selection) is ~17 us for K > 1, ~9 us for K = 1.
+    const double hbm_bpc = 3600.0;   // chip HBM read bytes per SM-cycle (~7 TB/s @ 1.95 GHz)
+    const double chunk_cyc = 0.70 * 1950.0;
+    const double cyc_us = 1950.0;
     const uint32_t gmin = (n + 31u) / 32u;
     double best = 1e300;
-    uint32_t bestG = gmin, bestK = 1;
+    uint32_t bestG = gmin, bestK = 1, bestR = (n + gmin - 1u) / gmin;
     const char* fk = std::getenv("SP_FORCE_K");  // development: cluster size K (timing experiments)
     const uint32_t force_k = fk ? static_cast<uint32_t>(std::atoi(fk)) : 0u;
-    const char* fg = std::getenv("SP_FORCE_FULL_GROUPS");  // development: groups of 32 inputs
-    for (uint32_t K = 1; K <= (force_k ? 8u : 6u); ++K) {
+    const char* fr = std::getenv("SP_FORCE_R");  // development: inputs per group
+    const uint32_t force_r = fr ? static_cast<uint32_t>(std::atoi(fr)) : 0u;
+    const double win_chunks = std::ceil(static_cast<double>(g.nbits) / nwin / kChunkBits);
+    for (uint32_t K = 1; K <= 8u; ++K) {
         if (K > nwin) break;
         if (force_k && K != force_k) continue;
         int cap = max_clusters ? max_clusters[K] : sm_count / static_cast<int>(K);
         if (cap <= 0) continue;
-        const uint32_t G = fg ? gmin : std::max<uint32_t>(gmin, std::min<uint32_t>(n, static_cast<uint32_t>(cap)));
-        const uint32_t waves = (G + cap - 1) / cap;
-        const double win_px = static_cast<double>(g.nbits) / nwin;
-        const double stream_cta = ((nwin + K - 1) / K) * 32.0 * win_px / sm_bpc;
-        const double t = std::max(static_cast<double>(n) * g.nbits / hbm_bpc, waves * stream_cta) +
-                         (5.0 + 4.5 * K) * cyc_us;
-        if (t < best * 0.98) {
-            best = t;
-            bestG = G;
-            bestK = K;
+        const uint32_t rlo = std::max<uint32_t>(1u, (n + cap - 1u) / static_cast<uint32_t>(cap));
+        for (uint32_t R = force_r ? std::min(force_r, 32u) : std::min<uint32_t>(rlo, 32u); R <= 32u; ++R) {
+            if (force_r && R != std::min(force_r, 32u)) continue;
+            const uint32_t G = (n + R - 1u) / R;
+            const uint32_t waves = (G + cap - 1) / cap;
+            const double stream_cta = ((nwin + K - 1) / K) * win_chunks * chunk_cyc;
+            const double t = std::max(static_cast<double>(n) * g.nbits / hbm_bpc, waves * stream_cta) +
+                             (K > 1 ? 17.0 : 9.0) * cyc_us;
+            if (std::getenv("SP_PLAN_DEBUG"))
+                std::fprintf(stderr, "plan n %u K %u cap %d R %u G %u waves %u t_us %.1f\n", n, K, cap, R, G, waves,
+                             t / cyc_us);
+            if (t < best * 0.98) {
+                best = t;
+                bestG = G;
+                bestK = K;
+                bestR = R;
+            }
+            if (R >= n) break;
         }
     }
     *groups = bestG;
     *Kout = bestK;
+    *Rout = bestR;
 }
 
 }  // namespace sp
@@ -540,20 +561,27 @@ sp_plan_info make_plan(const sp_handle* h, uint32_t n, bool learn, const uint8_t
         pl.smem_bytes = h->lay.smem_bytes;
     } else if (reason == 0 && n > 0) {
         pl.path = SP_PATH_BATCHED;
-        uint32_t G = 0, K = 1;
+        uint32_t G = 0, K = 1, R = 32;
         sp::plan_batched_grid(g, h->lay.nwin, n, h->sm_count, h->max_clusters[1] ? h->max_clusters : nullptr, &G,
-                              &K);
+                              &K, &R);
         if (h->force_groups) {  // test override: fewer, fuller groups (the paired top-k branches
             G = std::max<uint32_t>((n + 31u) / 32u, std::min<uint32_t>(n, h->force_groups));  // need > NW
             K = 1;                                                                 // inputs per group)
+            R = (n + G - 1u) / G;
+            G = (n + R - 1u) / R;
         }
+        // groups of exactly R inputs (the last one shorter): a box of R rows reads only its own
+        // group's frames (with balanced groups of 27/28 in 32-row boxes, 13% of the bytes a CTA
+        // ingested were its neighbour's rows, L2 hits that still cost the SM's TMA ingest)
+        pl.group_inputs = R;
         pl.groups = G;
         pl.cluster = K;
         pl.ctas = G * K;
         pl.window_bits = h->lay.Lw;
         pl.num_windows = h->lay.nwin;
         pl.chunk_bits = sp::kChunkBits;
-        pl.stages = h->lay.stages;
+        // stages of R KiB (8 boxes of R rows x 128 B) in the ring
+        pl.stages = std::min<uint32_t>(sp::BatchedLayout::kMaxStages, h->lay.ring_bytes / (R * 1024u));
         pl.smem_bytes = h->lay.smem_bytes;
     } else {
         pl.path = SP_PATH_PER_INPUT;
@@ -805,16 +833,17 @@ sp_status launch_batched_path(sp_handle* h, const uint8_t* frames, const uint32_
     }
     sp::BatchedParams p{};
     if (planes) {
-        if (!sp::encode_packed_tmap(&p.tmap, planes, ((h->Wn + 3u) / 4u * 4u), n))
+        if (!sp::encode_packed_tmap(&p.tmap, planes, ((h->Wn + 3u) / 4u * 4u), n, pl.group_inputs))
             return fail(SP_E_CUDA, "cuTensorMapEncodeTiled failed for the bit-planes (words %u, rows %u)",
                         ((h->Wn + 3u) / 4u * 4u), n);
     } else if (!g.whole) {
         if (!sp::encode_patches_tmap(&p.tmap, frames, g, n_frames))
             return fail(SP_E_CUDA, "cuTensorMapEncodeTiled failed for the tiles");
-    } else if (!sp::encode_frames_tmap(&p.tmap, frames, g.nbits, n))
+    } else if (!sp::encode_frames_tmap(&p.tmap, frames, g.nbits, n, pl.group_inputs))
         return fail(SP_E_CUDA, "cuTensorMapEncodeTiled failed for the frames (nbits %u, rows %u)",
                     g.nbits, n);
     p.num_inputs = n;
+    p.rows = pl.group_inputs;
     p.nbits = g.nbits;
     p.C = g.C;
     p.C32 = g.C32;
@@ -826,7 +855,8 @@ sp_status launch_batched_path(sp_handle* h, const uint8_t* frames, const uint32_
     p.keyBits = g.keyBits;
     p.Lw = h->lay.Lw;
     p.nwin = h->lay.nwin;
-    p.stages = planes ? h->lay.stages * sp::kPackedStagesPer : h->lay.stages;
+    p.stages = planes ? h->lay.stages * sp::kPackedStagesPer : pl.stages;
+    p.ring_bytes = h->lay.ring_bytes;
     p.packed = planes ? 1u : 0u;
     p.region_bytes = h->lay.region_bytes;
     p.xbufs = h->lay.xbufs;
@@ -852,6 +882,7 @@ sp_status launch_batched_path(sp_handle* h, const uint8_t* frames, const uint32_
     p.cand_min_radius = h->cand_min_radius;
     p.cand_min_radius_u = h->cand_min_radius_u;
     if (const char* ecd = std::getenv("SP_CAND_DBG")) p.cand_dbg = static_cast<uint32_t>(std::atoi(ecd));
+    if (const char* ebd = std::getenv("SP_BATCHED_DBG")) p.bdbg = static_cast<uint32_t>(std::atoi(ebd));
     if (pl.tensor_cores) {
         if (h->conn_dirty) {
             e = sp::launch_build_conn(h->d_idx, h->d_perm, h->cfg.connected_threshold, g.C, g.C32, g.S, g.nbits,

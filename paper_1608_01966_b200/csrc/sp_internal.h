@@ -46,12 +46,21 @@ struct Geometry {
 struct BatchedLayout {
     bool ok = false;
     uint32_t stages = 0, xbufs = 0, Lw = 0, nwin = 0;
+    uint32_t ring_bytes = 0;   // TMA ring; `stages` = the 32-row (32 KiB) stages it holds
+    static constexpr uint32_t kMaxStages = 8;  // barriers reserved for uint8 stages of fewer rows
     uint32_t region_bytes = 0, smem_bytes = 0;
 };
 
 struct alignas(64) BatchedParams {
-    CUtensorMap tmap;          // 2-D uint8 view of the frames: {nbits, num_inputs}, box {128, 32}
+    CUtensorMap tmap;          // 2-D uint8 view of the frames: {nbits, num_inputs}, box {128, rows}
     uint32_t num_inputs, nbits;
+    uint32_t bdbg;             // development (SP_BATCHED_DBG, timing experiments only): 1 skip the
+                               // gathers, 2 skip the transposes (results are wrong), 4 release a
+                               // stage after its transposes (the round-2 order), 8 no loads
+                               // (consumer-only timing)
+    uint32_t ring_bytes;       // TMA ring (stages * rows KiB <= ring_bytes; the window region follows)
+    uint32_t rows;             // whole frames: inputs per group = TMA box rows (<= 32); group g holds
+                               // inputs [g*rows, min(n, (g+1)*rows)), so no box reads another group's rows
     uint32_t C, C32, ncw;
     uint32_t min_overlap, k, radius;
     uint32_t keyL, keyBits;
@@ -253,10 +262,10 @@ BatchedLayout plan_batched_layout(const Geometry& g, int max_smem);
 BatchedLayout plan_patch_layout(const Geometry& g, int max_smem);
 void plan_batched_grid(const Geometry& g, uint32_t nwin, uint32_t num_inputs, int sm_count,
                        const int* max_clusters /* [9] by K, or nullptr */,
-                       uint32_t* groups, uint32_t* K);
+                       uint32_t* groups, uint32_t* K, uint32_t* R);
 
 // TMA descriptor of the frames for the batched kernel (sp_host.cu); false on failure
-bool encode_frames_tmap(CUtensorMap* map, const uint8_t* frames, uint32_t nbits, uint32_t rows);
+bool encode_frames_tmap(CUtensorMap* map, const uint8_t* frames, uint32_t nbits, uint32_t rows, uint32_t box_rows);
 bool encode_patches_tmap(CUtensorMap* map, const uint8_t* frames, const Geometry& g, uint32_t frames_n);
 
 // one-time kernel attributes (max dynamic smem)
@@ -265,7 +274,7 @@ cudaError_t configure_per_input(int max_smem);
 
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_batched(const BatchedParams& p, uint32_t smem_bytes, cudaStream_t s);
-bool encode_packed_tmap(CUtensorMap* map, const uint32_t* planes, uint32_t words, uint32_t rows);
+bool encode_packed_tmap(CUtensorMap* map, const uint32_t* planes, uint32_t words, uint32_t rows, uint32_t box_rows);
 cudaError_t launch_patch(const BatchedParams& p, uint32_t smem_bytes, uint32_t ctas, cudaStream_t s);
 cudaError_t batched_max_clusters(uint32_t smem_bytes, int max_clusters[9]);
 cudaError_t launch_pack(const PerInputParams& p, cudaStream_t s);

@@ -56,10 +56,30 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
     for (uint32_t f = rank + K * wi; wi < nwork && f < gs; f += K * nwork) {
         uint16_t* row = rawbuf + f * p.C32;
         if (K > 1) {
-            for (uint32_t c = lane; c < p.C32; c += 32u) {
-                uint32_t sum = 0;
-                for (uint32_t q = 0; q < K; ++q) sum += cluster.map_shared_rank(row, q)[c];
-                row[c] = static_cast<uint16_t>(sum);
+            // sum the K partial rows (DSMEM): 16-byte loads of 8 counts, packed u16 adds (a sum
+            // is a raw count <= S < 2^16, so no carry crosses a half); every load of a pass is
+            // issued before its stores, so the remote latencies overlap
+            uint4* row4 = reinterpret_cast<uint4*>(row);
+            const uint32_t nv = p.C32 / 8u;
+            for (uint32_t v0 = lane; v0 < nv; v0 += 128u) {
+                uint4 acc[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    acc[i] = v0 + 32u * i < nv ? row4[v0 + 32u * i] : make_uint4(0u, 0u, 0u, 0u);
+                for (uint32_t q = 0; q < K; ++q) {
+                    if (q == rank) continue;
+                    const uint4* rr = cluster.map_shared_rank(row4, q);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        if (v0 + 32u * i < nv) {
+                            const uint4 t = rr[v0 + 32u * i];
+                            acc[i].x += t.x, acc[i].y += t.y, acc[i].z += t.z, acc[i].w += t.w;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (v0 + 32u * i < nv) row4[v0 + 32u * i] = acc[i];
             }
             __syncwarp();
         }

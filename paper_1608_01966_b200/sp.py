@@ -15,7 +15,8 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsp.so")
+# SP_LIB_PATH: development A/B runs of alternative in-tree builds (scripts/_*); default libsp.so
+LIB_PATH = os.environ.get("SP_LIB_PATH") or os.path.join(HERE, "libsp.so")
 
 SP_OK, SP_E_CONFIG, SP_E_ARG, SP_E_SHAPE, SP_E_CUDA, SP_E_OOM, SP_E_STATE = range(7)
 SP_PATH_AUTO, SP_PATH_PER_INPUT, SP_PATH_BATCHED = 0, 1, 2
@@ -73,7 +74,7 @@ class SpPlanInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint32) for n in (
         "path", "input_bits", "inputs_per_frame", "num_inputs", "columns_padded", "sdr_words",
         "groups", "cluster", "ctas", "window_bits", "num_windows", "chunk_bits", "stages",
-        "smem_bytes", "reason", "tensor_cores")]
+        "smem_bytes", "reason", "tensor_cores", "group_inputs")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

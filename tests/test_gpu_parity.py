@@ -721,3 +721,32 @@ def test_strong_shard_launch_configs(n, radius, boost_mode):
         res = ora.step(O.encode(sp_inputs.frames(2002, f, 1, 540, 960, rho=0.5), cfg)[0], False)
         assert np.array_equal(sdr[f], sdr_of(res.active)), f"winners mismatch at frame {f}"
         assert counts[f] == res.active.sum()
+
+
+@pytest.mark.parametrize("n,K,R", [(200, 8, 25), (200, 7, 9), (130, 3, 3), (96, 5, 32), (77, 1, 13), (64, 2, 1)])
+def test_cluster_sizes_and_group_rows(monkeypatch, n, K, R):
+    """Every cluster size K <= 8 (the DSMEM sum of the K partial count rows, 16-byte packed-u16
+    loads) and groups of exactly R inputs (TMA boxes of R rows, the last group shorter, rows
+    < 8 inside one swizzle atom), recording off (the timed path), against the oracle on sampled
+    frames and the winner-count invariant on all."""
+    monkeypatch.setenv("SP_FORCE_K", str(K))
+    monkeypatch.setenv("SP_FORCE_R", str(R))
+    cfg = headline_cfg()
+    state = with_boost(perturbed_state(cfg), "uniform1")
+    sp = make_sp(cfg, state, max_inputs=n, record=False)
+    frames = torch.empty((n, 540, 960), dtype=torch.uint8, device=DEV)
+    P.synth_frames(frames, 0, 3003, rho=0.5)
+    sp.compute(frames)
+    sdr, counts = sp.winners()
+    torch.cuda.synchronize()
+    pl = sp.info()["plan"]
+    assert pl["cluster"] == K and pl["group_inputs"] == min(R, n), pl
+    assert pl["groups"] == -(-n // pl["group_inputs"]), pl
+    sdr, counts = sdr.cpu().numpy(), counts.cpu().numpy()
+    assert (counts == cfg.winners_set_size).all()
+    rng = np.random.default_rng(n * 10 + K)
+    sample = sorted(set(rng.choice(n, 5, replace=False).tolist()) | {0, R - 1, min(R, n - 1), n - 1})
+    ora = O.SpatialPoolerOracle(cfg, state)
+    for f in sample:
+        res = ora.step(O.encode(sp_inputs.frames(3003, f, 1, 540, 960, rho=0.5), cfg)[0], False)
+        assert np.array_equal(sdr[f], sdr_of(res.active)), f"winners mismatch at frame {f}"
