@@ -82,11 +82,16 @@ __device__ __forceinline__ void tma_box_g2s(void* dst, const CUtensorMap* map, u
 }
 
 // 32x32 bit-matrix transpose across a warp (row = lane, column = bit):
-// afterwards lane j bit f = lane f bit j.  Recursive block swap, 5 stages of
-// SHFL + rotate (SHF.L.W) + select (LOP3) with per-lane rotate amounts and keep
-// masks precomputed once.
+// afterwards lane j bit f = lane f bit j.  Recursive block swap, 5 stages of SHFL + merge with
+// per-lane constants precomputed once: the 16- and 8-bit stages move whole
+// bytes, so one PRMT (byte permute of x and the partner's y, per-lane selector) does the
+// rotate + select; the 4-, 2- and 1-bit stages rotate (SHF.L.W) and select (LOP3).
+#ifndef SP_PRMT_TRANSPOSE  // development A/B: 0 = rotate + select in all five stages
+#define SP_PRMT_TRANSPOSE 1
+#endif
 struct TransposeLane {
     uint32_t rot[5], keep[5];
+    uint32_t sel16, sel8;
     __device__ __forceinline__ explicit TransposeLane(uint32_t lane) {
         const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
 #pragma unroll
@@ -96,6 +101,10 @@ struct TransposeLane {
             rot[i] = lo ? s : 32u - s;
             keep[i] = lo ? masks[i] : ~masks[i];
         }
+        // bytes of x (0-3) and y (4-7): lo lanes keep their low half / even bytes and take the
+        // partner's low half / even bytes above them; hi lanes the mirror image
+        sel16 = (lane & 16u) == 0 ? 0x5410u : 0x3276u;
+        sel8 = (lane & 8u) == 0 ? 0x6240u : 0x3715u;
     }
 };
 
@@ -103,8 +112,12 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, const Transpose
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
         const uint32_t y = __shfl_xor_sync(0xffffffffu, x, 16u >> i);
-        const uint32_t r = __funnelshift_l(y, y, t.rot[i]);
-        x = (x & t.keep[i]) | (r & ~t.keep[i]);
+        if (SP_PRMT_TRANSPOSE && i < 2) {
+            x = __byte_perm(x, y, i == 0 ? t.sel16 : t.sel8);
+        } else {
+            const uint32_t r = __funnelshift_l(y, y, t.rot[i]);
+            x = (x & t.keep[i]) | (r & ~t.keep[i]);
+        }
     }
     return x;
 }
@@ -159,26 +172,36 @@ __device__ __forceinline__ bool warp_release_is_last(uint32_t addr) {
 // Resulting position of pixel 4k+b: k, 7+k, 15+k, 23+k (k < 7); 14, 22, 30, 31 (k = 7).
 // `one` is 1 at run time (a kernel parameter): the add becomes an IMAD on the FMA pipe
 // instead of an IADD on the ALU pipe, which is this loop's bottleneck.
-__device__ __forceinline__ uint32_t nz_flags(uint32_t v, uint32_t one) {
+__device__ __forceinline__ uint32_t nz_flags(uint32_t v, uint32_t one, uint32_t okm = 0x80808080u) {
     uint32_t t;
     asm("mad.lo.u32 %0, %1, %2, 0x7F7F7F7F;" : "=r"(t) : "r"(v & 0x7F7F7F7Fu), "r"(one));
-    return (t | v) & 0x80808080u;
+    return (t | v) & okm;
 }
 
 #ifndef SP_MASK_SHIFT  // development A/B: 0 = the round-1 IMAD.HI merge
 #define SP_MASK_SHIFT 1
 #endif
+#ifndef SP_MADHI_RT  // development A/B: 1 = multiplier through `one` (IMAD.HI), 0 = LEA.HI
+#define SP_MADHI_RT 0
+#endif
 #if SP_MASK_SHIFT
 // Round 2: word k's flags (bits 8b+7) shifted right by k and added (disjoint bits): pixel 4k+b
 // lands at bit 8b+7-k, all 32 distinct; 7 IMAD.HI instead of 7 (IMAD.HI + LOP3) + IMAD + LOP3.
-__device__ __forceinline__ uint32_t nonzero_mask32(const uint4 a, const uint4 b, uint32_t one) {
+// okm = 0x80808080 for an input lane, 0 for a lane past the group (its row is another
+// group's or stale): the flag mask doubles as the lane mask, no extra AND per block.
+__device__ __forceinline__ uint32_t nonzero_mask32(const uint4 a, const uint4 b, uint32_t one,
+                                                   uint32_t okm = 0x80808080u) {
     const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
     // the shifted flags are disjoint, so OR = ADD: one mad.hi (FMA pipe) per word shifts by
     // multiplying with 2^(32-k) and accumulates; no ALU op for the merge
-    uint32_t m = nz_flags(v[0], one);
-    // (the multiplier goes through the run-time `one`, or ptxas turns the mad.hi into LEA.HI on
-    // the ALU pipe, the loop's bottleneck)
-#define SP_MADHI_ACC(k) asm("mad.hi.u32 %0, %1, %2, %0;" : "+r"(m) : "r"(nz_flags(v[k], one)), "r"(one << (32 - (k))))
+    uint32_t m = nz_flags(v[0], one, okm);
+    // (SP_MADHI_RT: the multiplier goes through the run-time `one`, else ptxas turns the mad.hi
+    // into LEA.HI on the ALU pipe)
+#if SP_MADHI_RT
+#define SP_MADHI_ACC(k) asm("mad.hi.u32 %0, %1, %2, %0;" : "+r"(m) : "r"(nz_flags(v[k], one, okm)), "r"(one << (32 - (k))))
+#else
+#define SP_MADHI_ACC(k) asm("mad.hi.u32 %0, %1, %2, %0;" : "+r"(m) : "r"(nz_flags(v[k], one, okm)), "n"(1u << (32 - (k))))
+#endif
     SP_MADHI_ACC(1);
     SP_MADHI_ACC(2);
     SP_MADHI_ACC(3);
@@ -389,6 +412,7 @@ __global__ void __launch_bounds__(NT, 1)
     const uint32_t released_addr = smem_addr(released);
     const TransposeLane tl(lane);
     const uint32_t lane_ok = lane < gs ? 0xFFFFFFFFu : 0u;
+    const uint32_t okm = lane_ok & 0x80808080u;  // flag mask of this lane (0 past the group)
     const uint32_t pob = pixel_of_bit(lane);  // pixel of the word this lane writes per block
     // lane f reads its 32 bytes of block blk from box blk/4, row f, 16-byte slots
     // 2*(blk%4) and +1, swizzled by XOR with bits 7..9 of the row's shared-memory address
@@ -490,7 +514,7 @@ __global__ void __launch_bounds__(NT, 1)
                 for (uint32_t i = 0; i < BPW; ++i) {
                     const uint4 a = *reinterpret_cast<const uint4*>(stg + rd[i]);
                     const uint4 b = *reinterpret_cast<const uint4*>(stg + (rd[i] ^ 16u));
-                    m[i] = nonzero_mask32(a, b, p.one) & lane_ok;
+                    m[i] = SP_MASK_SHIFT ? nonzero_mask32(a, b, p.one, okm) : nonzero_mask32(a, b, p.one) & lane_ok;
                 }
                 // release the stage as soon as the warp's bytes are in registers (the flags
                 // consume every loaded value; the warp converges before the elected lane's

@@ -105,7 +105,8 @@ def test_bench_launch_1024_frames_vs_oracle_pool():
     sdr = torch.empty((4096, 32), dtype=torch.int32, device=DEV)
     cnt = torch.empty((4096,), dtype=torch.int32, device=DEV)
     sp.compute_into(frames, sdr, cnt)
-    assert sp.info()["plan"]["groups"] == 148
+    pl = sp.info()["plan"]
+    assert pl["groups"] == 147 and pl["group_inputs"] == 28 and pl["cluster"] == 1, pl  # 146 x 28 + 8
     sdr, cnt = sdr.cpu().numpy(), cnt.cpu().numpy()
     del frames
     want = oracle_infer_frames(cfg, state, 2002, range(0, 4096, 4))
