@@ -30,9 +30,10 @@
 
 namespace cg = cooperative_groups;
 
-#ifndef SP_RELEASE_ACQREL  // development A/B: 1 = the round-2 acq_rel stage release
-#define SP_RELEASE_ACQREL 0
+#ifndef SP_BATCHED_DBG_ON  // development builds only: honour SP_BATCHED_DBG (timing switches)
+#define SP_BATCHED_DBG_ON 0
 #endif
+constexpr bool kDbg = SP_BATCHED_DBG_ON != 0;
 
 namespace sp {
 
@@ -69,6 +70,26 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "}\n" ::"r"(smem_addr(bar)),
         "r"(parity)
         : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+// 16-byte shared load at a shared-window address (hoisted once per kernel: a generic pointer
+// made ptxas re-derive the window base, S2UR SR_CgaCtaId, every chunk)
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
 }
 
 // One 2-D TMA box {128 pixels, 32 inputs} at (x, row) of the frames' tensor map.
@@ -391,7 +412,7 @@ __global__ void __launch_bounds__(NT, 1)
     // Called by thread 0 for the prologue and afterwards by the lane that releases a stage
     // last, so the ring refills without any CTA-wide barrier.
     auto issue = [&](uint32_t j, uint32_t st) {
-        if (p.bdbg & 8u) return;  // development: consumer-only timing (no loads)
+        if (kDbg && (p.bdbg & 8u)) return;  // development: consumer-only timing (no loads)
         const uint32_t x0 = pix_begin + j * kChunkBits;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive_expect_tx(&bars[st], tx_bytes);
@@ -410,6 +431,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
 
     const uint32_t released_addr = smem_addr(released);
+    const uint32_t bars_s = smem_addr(bars), stage_s = smem_addr(stage_base);  // shared addresses
     const TransposeLane tl(lane);
     const uint32_t lane_ok = lane < gs ? 0xFFFFFFFFu : 0u;
     const uint32_t okm = lane_ok & 0x80808080u;  // flag mask of this lane (0 past the group)
@@ -504,38 +526,33 @@ __global__ void __launch_bounds__(NT, 1)
             if (st >= NST) st -= NST, phase ^= 1u;
         }
         for (uint32_t q = 0; q < (PK ? 0u : nch); ++q) {
-            if (!(p.bdbg & 8u)) mbar_wait(&bars[st], phase);
+            if (!(kDbg && (p.bdbg & 8u))) mbar_wait_s(bars_s + 8u * st, phase);
             // a1: warp wi turns blocks wi, wi+NW, .. (32 pixels x 32 inputs each) into 32
             // bit-sliced words per block
-            {
-                const uint8_t* stg = stage_base + st * SBs;
-                uint32_t m[BPW];
+            const uint32_t stg = stage_s + st * SBs;
+            uint32_t m[BPW];
 #pragma unroll
-                for (uint32_t i = 0; i < BPW; ++i) {
-                    const uint4 a = *reinterpret_cast<const uint4*>(stg + rd[i]);
-                    const uint4 b = *reinterpret_cast<const uint4*>(stg + (rd[i] ^ 16u));
-                    m[i] = SP_MASK_SHIFT ? nonzero_mask32(a, b, p.one, okm) : nonzero_mask32(a, b, p.one) & lane_ok;
-                }
-                // release the stage as soon as the warp's bytes are in registers (the flags
-                // consume every loaded value; the warp converges before the elected lane's
-                // release), so the refill's TMA latency overlaps the transposes; the warp that
-                // releases it last refills it (chunk j + NST)
-                if (!(p.bdbg & 36u)) {  // (development: 32 = no release at all, with 8 only)
-#pragma unroll
-                    for (uint32_t i = 0; i < BPW; ++i) asm volatile("" ::"r"(m[i]));
-                    __syncwarp();
-                    if (warp_release_is_last<NW, !SP_RELEASE_ACQREL>(released_addr + 4u * st) && j + NST < nchunks)
-                        issue(j + NST, st);
-                }
-                if (!(p.bdbg & 2u)) {
-#pragma unroll
-                    for (uint32_t i = 0; i < BPW; ++i)
-                        X[q * kChunkBits + (wi + NW * i) * 32u + pob] = warp_transpose32(m[i], tl);
-                }
+            for (uint32_t i = 0; i < BPW; ++i) {
+                const uint4 a = lds128(stg + rd[i]);
+                const uint4 b = lds128(stg + (rd[i] ^ 16u));
+                m[i] = SP_MASK_SHIFT ? nonzero_mask32(a, b, p.one, okm) : nonzero_mask32(a, b, p.one) & lane_ok;
             }
-            // (development switch 4: release after the transposes, as before)
-            if ((p.bdbg & 4u) && warp_release_is_last<NW>(released_addr + 4u * st) && j + NST < nchunks)
-                issue(j + NST, st);
+            // release the stage as soon as the warp's bytes are in registers (the flags consume
+            // every loaded value; the warp converges before the elected lane's relaxed add); the
+            // warp that releases it last refills it (chunk j + NST) at once (reading the add's
+            // result only after the transposes measured 10% slower: once this loop is trimmed
+            // the stream bounds the kernel)
+            if (!(kDbg && (p.bdbg & 36u))) {  // (development: 32 = no release at all, with 8 only)
+#pragma unroll
+                for (uint32_t i = 0; i < BPW; ++i) asm volatile("" ::"r"(m[i]));
+                __syncwarp();
+                if (warp_release_is_last<NW, true>(released_addr + 4u * st) && j + NST < nchunks) issue(j + NST, st);
+            }
+            if (!(kDbg && (p.bdbg & 2u))) {
+#pragma unroll
+                for (uint32_t i = 0; i < BPW; ++i)
+                    X[q * kChunkBits + (wi + NW * i) * 32u + pob] = warp_transpose32(m[i], tl);
+            }
             ++j;
             if (++st == NST) {
                 st = 0;
@@ -548,7 +565,7 @@ __global__ void __launch_bounds__(NT, 1)
         // a2: bit-sliced gather-count of this window's synapses (ELL, 8 slots per block)
 #pragma unroll
         for (int i = 0; i < CPT; ++i) {
-            const uint32_t nb = (p.bdbg & 1u) ? 0u : pnb[i];
+            const uint32_t nb = (kDbg && (p.bdbg & 1u)) ? 0u : pnb[i];
             const uint4* e = p.ell + poff[i] + lane;
 #pragma unroll
             for (uint32_t bk = 0; bk < PE; ++bk) {

@@ -54,10 +54,9 @@ struct BatchedLayout {
 struct alignas(64) BatchedParams {
     CUtensorMap tmap;          // 2-D uint8 view of the frames: {nbits, num_inputs}, box {128, rows}
     uint32_t num_inputs, nbits;
-    uint32_t bdbg;             // development (SP_BATCHED_DBG, timing experiments only): 1 skip the
-                               // gathers, 2 skip the transposes (results are wrong), 4 release a
-                               // stage after its transposes (the round-2 order), 8 no loads
-                               // (consumer-only timing)
+    uint32_t bdbg;             // development (SP_BATCHED_DBG; honoured only by -DSP_BATCHED_DBG_ON=1
+                               // builds, timing experiments): 1 skip the gathers, 2 skip the
+                               // transposes, 8 no loads (consumer-only), 32 no release (results wrong)
     uint32_t ring_bytes;       // TMA ring (stages * rows KiB <= ring_bytes; the window region follows)
     uint32_t rows;             // whole frames: inputs per group = TMA box rows (<= 32); group g holds
                                // inputs [g*rows, min(n, (g+1)*rows)), so no box reads another group's rows
