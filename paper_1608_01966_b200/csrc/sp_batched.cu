@@ -60,18 +60,6 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  : "memory");
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred P1;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_addr(bar)),
-        "r"(parity)
-        : "memory");
-}
-
 __device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n"
@@ -391,7 +379,7 @@ __global__ void __launch_bounds__(NT, 1)
 
     // ---- setup ---------------------------------------------------------------------------
     uint64_t* trace = p.trace ? p.trace + blockIdx.x * 6u : nullptr;
-    uint64_t t_win = 0, t_gather = 0;  // phase timestamps (dev aid)
+    uint64_t t_win = 0;  // phase timestamps (dev aid)
     if (trace && tid == 0) trace[0] = global_ns();
     if (tid == 0 && (smem_addr(smem) & 1023u)) __trap();  // swizzled boxes need 1 KiB alignment
     if (tid < NST) {
@@ -503,8 +491,8 @@ __global__ void __launch_bounds__(NT, 1)
             uint32_t jj = j + q0, sq = st + q0, ph = phase;
             if (sq >= NST) sq -= NST, ph ^= 1u;
             for (uint32_t q = q0; q < nch; q += 2u) {
-                mbar_wait(&bars[sq], ph);
-                const uint4 v = *reinterpret_cast<const uint4*>(stage_base + sq * SB + rdp);
+                mbar_wait_s(bars_s + 8u * sq, ph);
+                const uint4 v = lds128(stage_s + sq * SB + rdp);
                 const uint32_t t0 = warp_transpose32(v.x & lane_ok, tl);
                 const uint32_t t1 = warp_transpose32(v.y & lane_ok, tl);
                 const uint32_t t2 = warp_transpose32(v.z & lane_ok, tl);
@@ -680,6 +668,7 @@ __global__ void __launch_bounds__(NT, 1) sp_patch_kernel(const __grid_constant__
     const TransposeLane tl(lane);
     const uint32_t pob = pixel_of_bit(lane);
     const uint32_t released_addr = smem_addr(released);
+    const uint32_t bars_s = smem_addr(bars), stage_s = smem_addr(stage_base);  // shared addresses
     const uint32_t bpr = pw / 32u;            // 32-pixel blocks per tile row
     const uint32_t nblk = bpr * ph;           // blocks per tile
     uint32_t st = 0, phase = 0;
@@ -688,17 +677,17 @@ __global__ void __launch_bounds__(NT, 1) sp_patch_kernel(const __grid_constant__
         const uint32_t row = g / gpr, px0 = (g % gpr) * 32u;
         const uint32_t gs = min(32u, tpr - px0);
         const uint32_t in0 = row * tpr + px0;
-        const uint32_t lane_ok = lane < gs ? 0xFFFFFFFFu : 0u;
-        mbar_wait(&bars[st], phase);
+        const uint32_t okm = lane < gs ? 0x80808080u : 0u;  // flag mask (0 past the group)
+        mbar_wait_s(bars_s + 8u * st, phase);
         // a1: lane f = tile f of the group; block b = row y, pixels 32*xb .. 32*xb+31
         {
-            const uint8_t* stg = stage_base + st * stage_bytes;
+            const uint32_t stg = stage_s + st * stage_bytes;
             for (uint32_t b = wi; b < nblk; b += NW) {
                 const uint32_t y = b / bpr, xb = b % bpr;
-                const uint8_t* src = stg + (y * 32u + lane) * pw + xb * 32u;
-                const uint4 a = *reinterpret_cast<const uint4*>(src);
-                const uint4 bb = *reinterpret_cast<const uint4*>(src + 16);
-                X[y * pw + xb * 32u + pob] = warp_transpose32(nonzero_mask32(a, bb, p.one) & lane_ok, tl);
+                const uint32_t src = stg + (y * 32u + lane) * pw + xb * 32u;
+                const uint4 a = lds128(src);
+                const uint4 bb = lds128(src + 16u);
+                X[y * pw + xb * 32u + pob] = warp_transpose32(nonzero_mask32(a, bb, p.one, okm), tl);
             }
         }
         if (warp_release_is_last<NW>(released_addr + 4u * st) && j + NST < ngroups) issue(j + NST, st);
