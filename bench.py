@@ -684,6 +684,19 @@ def main():
                                        "peak = measured bf16 dense x 2 (nominal i8:bf16 ratio)"}
             else:
                 d["synapse_tests_per_s"] = float(C) * S * PF * 540 / (pms / 1e3)
+                # ALU-pipe roofline (the gather kernel is ALU-bound, not HBM-bound: ncu ALU pipe 71%,
+                # L2 11%, DRAM 2%): its ALU warp-instructions per frame (one ncu capture, static
+                # like roofline.traffic) at this run's rate vs 2 per SM-cycle x SMs x max clock
+                pa = os.path.join(ROOT, "profiles", "ncu_patch_alu.json")
+                if os.path.exists(pa):
+                    na = json.load(open(pa))
+                    clk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"] * 1e6 \
+                        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1.965e9
+                    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+                    ach = na["alu_warp_instructions_per_frame"] * PF / (pms / 1e3) / 1e9
+                    pk = na["peak_alu_warp_instructions_per_sm_cycle"] * nsm * clk / 1e9
+                    d["roofline"] = {"bound": "alu", "achieved": ach, "peak": pk, "unit": "G warp-instr/s",
+                                     "frac": ach / pk, "source": "profiles/ncu_patch_alu.json"}
             patch["kernels"][name] = d
             outs[name] = (psd.clone(), pcn.clone())
             spp.close()
