@@ -134,6 +134,9 @@ typedef struct sp_plan_info {
                                     (NEXT-2; groups = blocks of 4 tile-rows, cluster = C32/128) */
     uint32_t group_inputs;       /* whole frames: inputs per group (the TMA box rows, <= 32);
                                     group g = inputs [g*group_inputs, min(n, (g+1)*group_inputs)) */
+    uint32_t global_split;       /* 1: the `cluster` CTAs of a group are no thread-block cluster but
+                                    members of one cooperative launch, partial counts summed through
+                                    global memory (small batches) */
 } sp_plan_info;
 
 /* Run-time information about a handle. */

@@ -336,6 +336,51 @@ __device__ __forceinline__ void store_counts(const Planes& P, uint16_t* rawbuf, 
 
 }  // namespace
 
+// Global split (p.gsplit): the K CTAs of a group are not a cluster but members of
+// a cooperative launch (all resident).  Each writes its partial counts rawbuf[f < gs] to
+// part[group][rank], arrives on the group's counter and waits for the K arrivals; then CTA rank
+// sums the K partial rows of its inputs f = rank, rank + K, .. into its own rawbuf (the rows
+// batched_topk then reads), and departs; the last departure zeroes both counters for the next
+// launch (stream order: it starts after this one has finished).
+__device__ __noinline__ void global_split_sum(const BatchedParams& p, uint16_t* rawbuf, uint32_t group,
+                                              uint32_t rank, uint32_t K, uint32_t gs, uint32_t tid,
+                                              uint32_t nt) {
+    const uint32_t nv = p.C32 / 8u;  // uint4 per row
+    uint4* mine = p.part + (static_cast<size_t>(group) * K + rank) * 32u * nv;
+    const uint4* raw4 = reinterpret_cast<const uint4*>(rawbuf);
+    for (uint32_t i = tid; i < gs * nv; i += nt) __stcg(mine + i, raw4[i]);
+    __threadfence();
+    __syncthreads();
+    uint32_t* arr = p.gbar + group;
+    uint32_t* dep = p.gbar + p.groups + group;
+    if (tid == 0) {
+        atomicAdd(arr, 1u);
+        uint32_t seen = 0, spins = 0;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(arr) : "memory");
+            if (++spins > (1u << 28)) __trap();  // a missing peer: fail loudly, never hang
+        } while (seen < K);
+    }
+    __syncthreads();
+    const uint32_t mine_n = gs > rank ? (gs - rank + K - 1u) / K : 0u;  // inputs rank, rank+K, ..
+    uint4* sum4 = reinterpret_cast<uint4*>(rawbuf);
+    const uint4* base = p.part + static_cast<size_t>(group) * K * 32u * nv;
+    for (uint32_t i = tid; i < mine_n * nv; i += nt) {
+        const uint32_t f = rank + K * (i / nv), v = i % nv;
+        uint4 acc = make_uint4(0u, 0u, 0u, 0u);
+        for (uint32_t q = 0; q < K; ++q) {  // packed u16 adds: every sum is a raw count <= S
+            const uint4 t = __ldcg(base + (static_cast<size_t>(q) * 32u + f) * nv + v);
+            acc.x += t.x, acc.y += t.y, acc.z += t.z, acc.w += t.w;
+        }
+        sum4[f * nv + v] = acc;
+    }
+    __syncthreads();
+    if (tid == 0 && atomicAdd(dep, 1u) == K - 1u) {
+        atomicExch(arr, 0u);
+        atomicExch(dep, 0u);
+    }
+}
+
 // NT threads per CTA (1024: 1 block of 32 pixels per warp per chunk, 64 registers;
 // 512: 2 blocks per warp per chunk, 128 registers); CPT column-warps per warp.
 // PK: the frames arrive as bit-planes (sp_compute_packed; P:502's boolean representation):
@@ -597,15 +642,16 @@ __global__ void __launch_bounds__(NT, 1)
         }
     }
     cg::cluster_group cluster = cg::this_cluster();
-    if (K > 1) cluster.sync();
+    if (K > 1 && !p.gsplit) cluster.sync();
     else __syncthreads();
+    if (K > 1 && p.gsplit) global_split_sum(p, rawbuf, group, rank, K, gs, tid, NT);
     if (trace && tid == 0) trace[2] = global_ns();
 
     // idle shared memory behind the raw counts: the rest of the ring and the X windows
     const uint32_t raw_bytes = (32u * p.C32 * 2u + 127u) & ~127u;
     const uint32_t big_bytes = p.ring_bytes >= raw_bytes ? p.ring_bytes - raw_bytes + p.region_bytes : 0u;
     batched_topk<CPT, NW>(p, rawbuf, region, smem + raw_bytes, big_bytes, s_bc, in0, gs, rank, K, wi, lane);
-    if (K > 1) cluster.sync();  // peers may still read this CTA's partial counts
+    if (K > 1 && !p.gsplit) cluster.sync();  // peers may still read this CTA's partial counts
     if (trace) {
         __syncthreads();
         if (tid == 0) trace[3] = global_ns();
@@ -755,10 +801,15 @@ cudaError_t launch_batched(const BatchedParams& p, uint32_t smem_bytes, cudaStre
     cfg.dynamicSmemBytes = smem_bytes;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = p.K;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
+    if (p.gsplit) {  // every CTA resident (one per SM): the group barrier cannot deadlock
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+    } else {
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = p.K;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+    }
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (p.packed)

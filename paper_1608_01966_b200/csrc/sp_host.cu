@@ -339,7 +339,8 @@ bool encode_packed_tmap(CUtensorMap* map, const uint32_t* planes, uint32_t words
 // Groups of R <= 32 inputs and cluster size K: estimated time of each (K, R)
 // from an HBM term, a per-CTA streaming term and the cluster tail.
 void plan_batched_grid(const Geometry& g, uint32_t nwin, uint32_t n, int sm_count,
-                       const int* max_clusters, uint32_t* groups, uint32_t* Kout, uint32_t* Rout) {
+                       const int* max_clusters, uint32_t* groups, uint32_t* Kout, uint32_t* Rout,
+                       uint32_t* gsplit_out) {
     // Time model, fitted to measurements (960x540, C 1024, S 256): a CTA's time is
     // its ceil(nwin / K) windows at ~0.7 us per 1024-pixel chunk whatever its rows R (16..32:
     // the per-SM transpose/flag/release work, not HBM, sets the pace: 4096 frames on one CTA per
@@ -383,9 +384,40 @@ void plan_batched_grid(const Geometry& g, uint32_t nwin, uint32_t n, int sm_coun
             if (R >= n) break;
         }
     }
+    // global split (K CTAs per group in one cooperative launch, partial counts through L2): any
+    // K, all SMs usable (clusters of 6+ pack into GPCs badly: 22 of 6, 15 of 8 or 9), one wave
+    // only; its tail (partial counts to L2, the group barrier, the K-row sums) measured ~22 us
+    // (512 frames: K 9 on 144 SMs 0.064 ms vs clusters of 6 on 132 SMs 0.069; 1024 and 2048
+    // frames stay on clusters: 0.103 vs 0.106, 0.182 vs 0.187)
+    uint32_t bestS = 0;
+    const char* fs = std::getenv("SP_FORCE_GSPLIT");  // development / tests: 1 force, 0 forbid
+    const int force_s = fs ? std::atoi(fs) : -1;
+    if (force_s == 1) best = 1e300;
+    for (uint32_t K = 2; force_s != 0 && K <= 16u && K <= nwin; ++K) {
+        if (force_k && K != force_k) continue;
+        const uint32_t cap = static_cast<uint32_t>(sm_count) / K;
+        if (cap == 0) continue;
+        uint32_t R = std::max<uint32_t>(1u, (n + cap - 1u) / cap);
+        if (force_r) R = std::min(force_r, 32u);
+        if (R > 32u) continue;
+        const uint32_t G = (n + R - 1u) / R;
+        if (G > cap) continue;
+        const double stream_cta = ((nwin + K - 1) / K) * win_chunks * chunk_cyc;
+        const double t = std::max(static_cast<double>(n) * g.nbits / hbm_bpc, stream_cta) + 22.0 * cyc_us;
+        if (std::getenv("SP_PLAN_DEBUG"))
+            std::fprintf(stderr, "plan gsplit n %u K %u cap %u R %u G %u t_us %.1f\n", n, K, cap, R, G, t / cyc_us);
+        if (t < best * 0.98) {
+            best = t;
+            bestG = G;
+            bestK = K;
+            bestR = R;
+            bestS = 1;
+        }
+    }
     *groups = bestG;
     *Kout = bestK;
     *Rout = bestR;
+    *gsplit_out = bestS;
 }
 
 }  // namespace sp
@@ -409,6 +441,8 @@ struct sp_handle {
     uint32_t ell_slots = 0;
     bool ell_dirty = false;
     uint64_t* d_trace = nullptr;  // SP_TRACE=1: per-CTA phase timestamps of the batched kernel
+    uint4* d_part = nullptr;      // global split: partial counts [SMs][32][C32] u16
+    uint32_t* d_gsbar = nullptr;  // global split: [2][SMs] group barrier counters (zero at rest)
     bool uniform_bc = true;       // all boosts equal (enables the histogram top-k)
     uint32_t batched_threads = 512;  // threads per CTA of the batched kernel
     // per-column boosts: wavelet local top-k from this radius on, the bit-sliced comparator below
@@ -494,7 +528,7 @@ cudaError_t dalloc(T** p, size_t count) {
 void release(sp_handle* h) {
     if (!h) return;
     cudaSetDevice(h->device);
-    void* ptrs[] = {h->d_trace, h->d_idx,  h->d_perm,    h->d_boost,   h->d_bc,      h->d_syn,
+    void* ptrs[] = {h->d_part, h->d_gsbar, h->d_trace, h->d_idx,  h->d_perm,    h->d_boost,   h->d_bc,      h->d_syn,
                     h->d_ell,  h->d_ell_off, h->d_ell_nb,  h->d_ell_pos, h->d_bits,
                     h->d_raw,  h->d_sdr,     h->d_counts,  h->d_raw_rec, h->d_boosted_rec,
                     h->d_stage[0], h->d_stage[1], h->d_synT,  h->d_gbar, h->d_adc, h->d_odc,
@@ -561,15 +595,17 @@ sp_plan_info make_plan(const sp_handle* h, uint32_t n, bool learn, const uint8_t
         pl.smem_bytes = h->lay.smem_bytes;
     } else if (reason == 0 && n > 0) {
         pl.path = SP_PATH_BATCHED;
-        uint32_t G = 0, K = 1, R = 32;
+        uint32_t G = 0, K = 1, R = 32, S = 0;
         sp::plan_batched_grid(g, h->lay.nwin, n, h->sm_count, h->max_clusters[1] ? h->max_clusters : nullptr, &G,
-                              &K, &R);
+                              &K, &R, &S);
         if (h->force_groups) {  // test override: fewer, fuller groups (the paired top-k branches
             G = std::max<uint32_t>((n + 31u) / 32u, std::min<uint32_t>(n, h->force_groups));  // need > NW
             K = 1;                                                                 // inputs per group)
             R = (n + G - 1u) / G;
             G = (n + R - 1u) / R;
+            S = 0;
         }
+        pl.global_split = S;
         // groups of exactly R inputs (the last one shorter): a box of R rows reads only its own
         // group's frames (with balanced groups of 27/28 in 32-row boxes, 13% of the bytes a CTA
         // ingested were its neighbour's rows, L2 hits that still cost the SM's TMA ingest)
@@ -857,6 +893,11 @@ sp_status launch_batched_path(sp_handle* h, const uint8_t* frames, const uint32_
     p.nwin = h->lay.nwin;
     p.stages = planes ? h->lay.stages * sp::kPackedStagesPer : pl.stages;
     p.ring_bytes = h->lay.ring_bytes;
+    p.gsplit = pl.global_split;
+    p.part = h->d_part;
+    p.gbar = h->d_gsbar;
+    if (p.gsplit && (!p.part || !p.gbar || pl.ctas > static_cast<uint32_t>(h->sm_count)))
+        return fail(SP_E_STATE, "global split without its scratch or with more CTAs than SMs");
     p.packed = planes ? 1u : 0u;
     p.region_bytes = h->lay.region_bytes;
     p.xbufs = h->lay.xbufs;
@@ -1326,7 +1367,17 @@ sp_status sp_create(const sp_config* cfg, sp_handle** out) {
         release(h);
         return cuda_fail(e, "kernel attributes");
     }
-    if (h->lay.ok && h->g.whole) sp::batched_max_clusters(h->lay.smem_bytes, h->max_clusters);
+    if (h->lay.ok && h->g.whole) {
+        sp::batched_max_clusters(h->lay.smem_bytes, h->max_clusters);
+        // global-split scratch: one CTA per SM, 32 partial count rows each
+        const size_t pb = static_cast<size_t>(h->sm_count) * 32u * h->g.C32 * 2u;
+        if (cudaMalloc(&h->d_part, pb) != cudaSuccess ||
+            cudaMalloc(&h->d_gsbar, 2u * h->sm_count * sizeof(uint32_t)) != cudaSuccess ||
+            cudaMemset(h->d_gsbar, 0, 2u * h->sm_count * sizeof(uint32_t)) != cudaSuccess) {
+            release(h);
+            return fail(SP_E_OOM, "global-split scratch (%zu bytes)", pb);
+        }
+    }
     // tensor-core patch kernel (NEXT-2): global inhibition (the selection it feeds is the global
     // top-k; local windows stay on the bit-sliced gather kernel, measured faster there), patch
     // width a power of two >= 32, <= 32 tiles per row, nbits <= 1024 (A in tensor memory beside

@@ -58,6 +58,10 @@ struct alignas(64) BatchedParams {
                                // builds, timing experiments): 1 skip the gathers, 2 skip the
                                // transposes, 8 no loads (consumer-only), 32 no release (results wrong)
     uint32_t ring_bytes;       // TMA ring (stages * rows KiB <= ring_bytes; the window region follows)
+    uint32_t gsplit;           // K CTAs per group WITHOUT a cluster (cooperative launch, all resident):
+                               // partial counts through global memory (part), group barrier (gbar)
+    uint4* part;               // gsplit: [groups][K][32][C32] u16 partial counts (L2)
+    uint32_t* gbar;            // gsplit: [2][groups] arrivals, departures (zero between launches)
     uint32_t rows;             // whole frames: inputs per group = TMA box rows (<= 32); group g holds
                                // inputs [g*rows, min(n, (g+1)*rows)), so no box reads another group's rows
     uint32_t C, C32, ncw;
@@ -261,7 +265,7 @@ BatchedLayout plan_batched_layout(const Geometry& g, int max_smem);
 BatchedLayout plan_patch_layout(const Geometry& g, int max_smem);
 void plan_batched_grid(const Geometry& g, uint32_t nwin, uint32_t num_inputs, int sm_count,
                        const int* max_clusters /* [9] by K, or nullptr */,
-                       uint32_t* groups, uint32_t* K, uint32_t* R);
+                       uint32_t* groups, uint32_t* K, uint32_t* R, uint32_t* gsplit);
 
 // TMA descriptor of the frames for the batched kernel (sp_host.cu); false on failure
 bool encode_frames_tmap(CUtensorMap* map, const uint8_t* frames, uint32_t nbits, uint32_t rows, uint32_t box_rows);

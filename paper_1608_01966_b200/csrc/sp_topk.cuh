@@ -55,7 +55,7 @@ __device__ __noinline__ void batched_topk(const BatchedParams& p, uint16_t* rawb
     }
     for (uint32_t f = rank + K * wi; wi < nwork && f < gs; f += K * nwork) {
         uint16_t* row = rawbuf + f * p.C32;
-        if (K > 1) {
+        if (K > 1 && !p.gsplit) {
             // sum the K partial rows (DSMEM): 16-byte loads of 8 counts, packed u16 adds (a sum
             // is a raw count <= S < 2^16, so no carry crosses a half); every load of a pass is
             // issued before its stores, so the remote latencies overlap

@@ -74,7 +74,7 @@ class SpPlanInfo(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint32) for n in (
         "path", "input_bits", "inputs_per_frame", "num_inputs", "columns_padded", "sdr_words",
         "groups", "cluster", "ctas", "window_bits", "num_windows", "chunk_bits", "stages",
-        "smem_bytes", "reason", "tensor_cores", "group_inputs")]
+        "smem_bytes", "reason", "tensor_cores", "group_inputs", "global_split")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

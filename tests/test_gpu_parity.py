@@ -750,3 +750,33 @@ def test_cluster_sizes_and_group_rows(monkeypatch, n, K, R):
     for f in sample:
         res = ora.step(O.encode(sp_inputs.frames(3003, f, 1, 540, 960, rho=0.5), cfg)[0], False)
         assert np.array_equal(sdr[f], sdr_of(res.active)), f"winners mismatch at frame {f}"
+
+
+@pytest.mark.parametrize("n,K,R", [(512, 9, 32), (144, 12, 16), (130, 2, 3), (96, 5, 32), (64, 16, 32), (33, 4, 1)])
+def test_global_split_groups(monkeypatch, n, K, R):
+    """The global split: K CTAs per group in one cooperative launch, partial counts
+    written to L2, a per-group arrival barrier, each CTA summing its inputs' K partial rows
+    (recording off, the timed path) -- against the oracle on sampled frames, the winner-count
+    invariant on all; run twice, so the barrier counters' reset between launches is exercised."""
+    monkeypatch.setenv("SP_FORCE_K", str(K))
+    monkeypatch.setenv("SP_FORCE_R", str(R))
+    monkeypatch.setenv("SP_FORCE_GSPLIT", "1")
+    cfg = headline_cfg()
+    state = with_boost(perturbed_state(cfg), "uniform1")
+    sp = make_sp(cfg, state, max_inputs=n, record=False)
+    frames = torch.empty((n, 540, 960), dtype=torch.uint8, device=DEV)
+    P.synth_frames(frames, 0, 4004, rho=0.5)
+    for _ in range(2):
+        sp.compute(frames)
+    sdr, counts = sp.winners()
+    torch.cuda.synchronize()
+    pl = sp.info()["plan"]
+    assert pl["global_split"] == 1 and pl["cluster"] == K and pl["group_inputs"] == min(R, n), pl
+    sdr, counts = sdr.cpu().numpy(), counts.cpu().numpy()
+    assert (counts == cfg.winners_set_size).all()
+    rng = np.random.default_rng(n * 7 + K)
+    sample = sorted(set(rng.choice(n, 5, replace=False).tolist()) | {0, min(R, n - 1), n - 1})
+    ora = O.SpatialPoolerOracle(cfg, state)
+    for f in sample:
+        res = ora.step(O.encode(sp_inputs.frames(4004, f, 1, 540, 960, rho=0.5), cfg)[0], False)
+        assert np.array_equal(sdr[f], sdr_of(res.active)), f"winners mismatch at frame {f}"
