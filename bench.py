@@ -690,11 +690,11 @@ def main():
                 pa = os.path.join(ROOT, "profiles", "ncu_patch_alu.json")
                 if os.path.exists(pa):
                     na = json.load(open(pa))
-                    clk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"] * 1e6 \
+                    sm_hz = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"] * 1e6 \
                         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1.965e9
                     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
                     ach = na["alu_warp_instructions_per_frame"] * PF / (pms / 1e3) / 1e9
-                    pk = na["peak_alu_warp_instructions_per_sm_cycle"] * nsm * clk / 1e9
+                    pk = na["peak_alu_warp_instructions_per_sm_cycle"] * nsm * sm_hz / 1e9
                     d["roofline"] = {"bound": "alu", "achieved": ach, "peak": pk, "unit": "G warp-instr/s",
                                      "frac": ach / pk, "source": "profiles/ncu_patch_alu.json"}
             patch["kernels"][name] = d
