@@ -585,7 +585,21 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             pms, pems = float(t[0]), float(t[1])
         pbytes = sp.packed_words * 4
-        packed = {"value": F * world / (pms / 1e3), "unit": UNIT, "ms_per_step": pms,
+        # issue-slot roofline (the bit-plane path is issue/latency-bound, not HBM-bound: ncu issue
+        # 53%, ALU 53%, LSU 40%, DRAM 17%): the capture's warp-instructions per frame at this
+        # run's rate vs 4 per SM-cycle x SMs x max clock (static per-frame count, like traffic)
+        proof = None
+        pi = os.path.join(ROOT, "profiles", "ncu_packed_issue.json")
+        if os.path.exists(pi):
+            ni = json.load(open(pi))
+            sm_hz = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["sm_max_mhz"] * 1e6 \
+                if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1.965e9
+            nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+            ach = ni["warp_instructions_per_frame"] * F / (pms / 1e3) / 1e9
+            pk = ni["peak_warp_instructions_per_sm_cycle"] * nsm * sm_hz / 1e9
+            proof = {"bound": "issue", "achieved": ach, "peak": pk, "unit": "G warp-instr/s", "frac": ach / pk,
+                     "source": "profiles/ncu_packed_issue.json"}
+        packed = {"value": F * world / (pms / 1e3), "unit": UNIT, "ms_per_step": pms, "roofline": proof,
                   "bytes_per_frame": pbytes,
                   "hbm_frac": round(F * (pbytes + words * 4) / (pms / 1e3) / 1e9 / measured_peak_hbm()[0], 4),
                   "same_winners_as_uint8_step": same,
