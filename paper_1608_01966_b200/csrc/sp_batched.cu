@@ -417,10 +417,16 @@ __global__ void __launch_bounds__(NT, 1)
     const uint32_t gs = in1 - in0;  // 1..rows inputs in this group
     // bytes a stage's boxes deliver: rows past the batch are zero-filled by TMA and counted
     const uint32_t tx_bytes = PK ? SB / 32u * p.rows : SBs;
-    const uint32_t w0 = rank * p.nwin / K, w1 = (rank + 1) * p.nwin / K;
-    const uint32_t pix_begin = w0 * p.Lw;
-    const uint32_t pix_end = min(w1 * p.Lw, p.nbits);
-    const uint32_t nchunks = pix_end > pix_begin ? (pix_end - pix_begin + kChunkBits - 1) / kChunkBits : 0;
+    // a group's K CTAs split its chunks (not its windows: 51 windows over 9 CTAs is 5 or 6 each,
+    // 507 chunks 56 or 57): CTA rank streams chunks [c0, c1), windows w0 .. w1-1, the first and
+    // last of which may be partial (X is zeroed outside the CTA's chunks, so the window's full
+    // ELL cell counts only them)
+    const uint32_t cpw = p.Lw / kChunkBits;  // chunks per window (Lw is a multiple of the chunk)
+    const uint32_t nct = (p.nbits + kChunkBits - 1) / kChunkBits;
+    const uint32_t c0 = rank * nct / K, c1 = (rank + 1) * nct / K;
+    const uint32_t w0 = c0 / cpw, w1 = c1 > c0 ? (c1 + cpw - 1u) / cpw : w0;
+    const uint32_t pix_begin = c0 * kChunkBits;
+    const uint32_t nchunks = c1 - c0;
 
     // ---- setup ---------------------------------------------------------------------------
     uint64_t* trace = p.trace ? p.trace + blockIdx.x * 6u : nullptr;
@@ -528,6 +534,15 @@ __global__ void __launch_bounds__(NT, 1)
         const uint32_t wbase = w * p.Lw;
         const uint32_t wlen = min(p.Lw, p.nbits - wbase);
         const uint32_t nch = (wlen + kChunkBits - 1) / kChunkBits;
+        // this CTA's chunks of the window: [qa, qb); zero X outside them (partial windows of a
+        // split group only; the buffer is free: every warp passed the previous window's barrier)
+        const uint32_t qa = c0 > w * cpw ? c0 - w * cpw : 0u;
+        const uint32_t qb = min(nch, c1 - w * cpw);
+        if (qa > 0u || qb < nch) {
+            for (uint32_t i = tid; i < qa * kChunkBits; i += NT) X[i] = 0u;
+            for (uint32_t i = qb * kChunkBits + tid; i < nch * kChunkBits; i += NT) X[i] = 0u;
+        }
+        const uint32_t nmine = qb - qa;
         if (PK) {
             // packed: the warps of half (wi >> 3) take the chunks of that parity (global chunk
             // index), 4 blocks each (one conflict-free LDS.128); lane j of a transpose holds
@@ -535,7 +550,7 @@ __global__ void __launch_bounds__(NT, 1)
             const uint32_t q0 = ((wi >> 3) - j) & 1u;
             uint32_t jj = j + q0, sq = st + q0, ph = phase;
             if (sq >= NST) sq -= NST, ph ^= 1u;
-            for (uint32_t q = q0; q < nch; q += 2u) {
+            for (uint32_t q = qa + q0; q < qb; q += 2u) {
                 mbar_wait_s(bars_s + 8u * sq, ph);
                 const uint4 v = lds128(stage_s + sq * SB + rdp);
                 const uint32_t t0 = warp_transpose32(v.x & lane_ok, tl);
@@ -553,12 +568,12 @@ __global__ void __launch_bounds__(NT, 1)
                 sq += 2u;
                 if (sq >= NST) sq -= NST, ph ^= 1u;
             }
-            j += nch;  // every warp: the window's chunks are consumed
-            st += nch % NST;
-            phase ^= (nch / NST) & 1u;
+            j += nmine;  // every warp: the window's chunks are consumed
+            st += nmine % NST;
+            phase ^= (nmine / NST) & 1u;
             if (st >= NST) st -= NST, phase ^= 1u;
         }
-        for (uint32_t q = 0; q < (PK ? 0u : nch); ++q) {
+        for (uint32_t q = qa; q < (PK ? 0u : qb); ++q) {
             if (!(kDbg && (p.bdbg & 8u))) mbar_wait_s(bars_s + 8u * st, phase);
             // a1: warp wi turns blocks wi, wi+NW, .. (32 pixels x 32 inputs each) into 32
             // bit-sliced words per block

@@ -358,7 +358,11 @@ void plan_batched_grid(const Geometry& g, uint32_t nwin, uint32_t n, int sm_coun
     const uint32_t force_k = fk ? static_cast<uint32_t>(std::atoi(fk)) : 0u;
     const char* fr = std::getenv("SP_FORCE_R");  // development: inputs per group
     const uint32_t force_r = fr ? static_cast<uint32_t>(std::atoi(fr)) : 0u;
-    const double win_chunks = std::ceil(static_cast<double>(g.nbits) / nwin / kChunkBits);
+    // a group's K CTAs split its chunks evenly (sp_batched.cu); a split CTA may gather up to two
+    // partial windows in full (their ELL cells), ~1.5 chunks' time
+    const uint32_t nct = (g.nbits + kChunkBits - 1u) / kChunkBits;
+    auto cta_chunks = [&](uint32_t K) { return (nct + K - 1u) / K + (K > 1u ? 1.5 : 0.0); };
+    (void)nwin;
     for (uint32_t K = 1; K <= 8u; ++K) {
         if (K > nwin) break;
         if (force_k && K != force_k) continue;
@@ -369,7 +373,7 @@ void plan_batched_grid(const Geometry& g, uint32_t nwin, uint32_t n, int sm_coun
             if (force_r && R != std::min(force_r, 32u)) continue;
             const uint32_t G = (n + R - 1u) / R;
             const uint32_t waves = (G + cap - 1) / cap;
-            const double stream_cta = ((nwin + K - 1) / K) * win_chunks * chunk_cyc;
+            const double stream_cta = cta_chunks(K) * chunk_cyc;
             const double t = std::max(static_cast<double>(n) * g.nbits / hbm_bpc, waves * stream_cta) +
                              (K > 1 ? 17.0 : 9.0) * cyc_us;
             if (std::getenv("SP_PLAN_DEBUG"))
@@ -402,7 +406,7 @@ void plan_batched_grid(const Geometry& g, uint32_t nwin, uint32_t n, int sm_coun
         if (R > 32u) continue;
         const uint32_t G = (n + R - 1u) / R;
         if (G > cap) continue;
-        const double stream_cta = ((nwin + K - 1) / K) * win_chunks * chunk_cyc;
+        const double stream_cta = cta_chunks(K) * chunk_cyc;
         const double t = std::max(static_cast<double>(n) * g.nbits / hbm_bpc, stream_cta) + 22.0 * cyc_us;
         if (std::getenv("SP_PLAN_DEBUG"))
             std::fprintf(stderr, "plan gsplit n %u K %u cap %u R %u G %u t_us %.1f\n", n, K, cap, R, G, t / cyc_us);
