@@ -367,9 +367,20 @@ __device__ __noinline__ void global_split_sum(const BatchedParams& p, uint16_t* 
     const uint4* base = p.part + static_cast<size_t>(group) * K * 32u * nv;
     for (uint32_t i = tid; i < mine_n * nv; i += nt) {
         const uint32_t f = rank + K * (i / nv), v = i % nv;
+        // packed u16 adds (every sum is a raw count <= S); four L2 loads in flight per thread
+        // (a serial loop over K waited one L2 round trip per partial row)
+        const uint4* src = base + static_cast<size_t>(f) * nv + v;
+        const size_t rs = 32u * static_cast<size_t>(nv);  // between the K partial rows of f
         uint4 acc = make_uint4(0u, 0u, 0u, 0u);
-        for (uint32_t q = 0; q < K; ++q) {  // packed u16 adds: every sum is a raw count <= S
-            const uint4 t = __ldcg(base + (static_cast<size_t>(q) * 32u + f) * nv + v);
+        uint32_t q = 0;
+        for (; q + 4u <= K; q += 4u) {
+            const uint4 t0 = __ldcg(src + q * rs), t1 = __ldcg(src + (q + 1u) * rs);
+            const uint4 t2 = __ldcg(src + (q + 2u) * rs), t3 = __ldcg(src + (q + 3u) * rs);
+            acc.x += (t0.x + t1.x) + (t2.x + t3.x), acc.y += (t0.y + t1.y) + (t2.y + t3.y);
+            acc.z += (t0.z + t1.z) + (t2.z + t3.z), acc.w += (t0.w + t1.w) + (t2.w + t3.w);
+        }
+        for (; q < K; ++q) {
+            const uint4 t = __ldcg(src + q * rs);
             acc.x += t.x, acc.y += t.y, acc.z += t.z, acc.w += t.w;
         }
         sum4[f * nv + v] = acc;
