@@ -358,7 +358,7 @@ __device__ __noinline__ void global_split_sum(const BatchedParams& p, uint16_t* 
         uint32_t seen = 0, spins = 0;
         do {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(arr) : "memory");
-            if (++spins > (1u << 28)) __trap();  // a missing peer: fail loudly, never hang
+            if (++spins > (1u << 22)) __trap();  // a missing peer (seconds of spinning): fail loudly, never hang
         } while (seen < K);
     }
     __syncthreads();
