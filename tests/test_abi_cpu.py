@@ -130,3 +130,27 @@ def test_encoder_create_without_gpu_fails_loudly():
     with pytest.raises(P.SpError) as e:
         P.Encoder()
     assert e.value.status == P.SP_E_CUDA
+
+
+@pytest.mark.parametrize("n", [1, 7, 33, 100, 256, 512, 777, 1024, 2048, 4095, 4096, 10000])
+@pytest.mark.parametrize("sm_count", [148, 132])
+def test_plan_groups_of_exact_rows(n, sm_count):
+    """Whole-frame plans: groups of exactly R <= 32 inputs (the TMA box rows), the
+    last one shorter; stages of R KiB in the 140 KiB ring (4..8); a global split never needs
+    more CTAs than SMs (cooperative launch), a cluster never more than 16 CTAs."""
+    pl = P.plan(n, sm_count=sm_count, input_width=960, input_height=540, num_columns=1024,
+                synapses_per_column=256)
+    R, G, K = pl["group_inputs"], pl["groups"], pl["cluster"]
+    assert pl["path"] == P.SP_PATH_BATCHED and 1 <= R <= 32
+    assert G == -(-n // R) and pl["ctas"] == G * K
+    assert 4 <= pl["stages"] <= 8 and pl["stages"] * R * 1024 <= 140 * 1024
+    if pl["global_split"]:
+        assert 2 <= K <= 16 and pl["ctas"] <= sm_count
+    else:
+        assert 1 <= K <= 8
+
+
+def test_plan_headline_groups_of_28():
+    pl = P.plan(4096, sm_count=148, input_width=960, input_height=540, num_columns=1024,
+                synapses_per_column=256, min_overlap=4, winners_set_size=40)
+    assert (pl["groups"], pl["group_inputs"], pl["cluster"], pl["stages"], pl["global_split"]) == (147, 28, 1, 5, 0)
